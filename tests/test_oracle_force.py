@@ -1,0 +1,161 @@
+"""Pins for oracle.sph.force_at / particle_state.
+
+Pinned against: zero force on a perfect lattice at rest (symmetry); a
+two-particle case derived by hand from Eqs. 4-5 and the viscosity display
+(P:191-195); exact momentum and energy conservation of the
+pairwise-antisymmetric equations (any dropped term, wrong sign, wrong index or
+wrong 1/4 vs 1/8 prefactor breaks one of them); viscous heating >= 0;
+Galilean invariance (only v_ij enters).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+
+
+def _eval(p, h=None, v=None):
+    v = p.v if v is None else v
+    return oracle.evaluate_all(p.x, v, p.m, p.u, p.box, h=h)
+
+
+def test_perfect_lattice_at_rest_has_zero_force():
+    p = workloads.c2_exact(k=16)
+    out = _eval(p)
+    scale = out["S_a"].max()
+    assert np.abs(out["a"]).max() <= 1e-12 * scale
+    assert np.abs(out["dudt"]).max() == 0.0       # v = 0 exactly
+
+
+@pytest.mark.parametrize("t", [0, 1, 2, 3])
+def test_conservation(t):
+    """sum m a = 0 and sum m (v.a + du/dt) = 0 to rounding."""
+    p = workloads.tiny(t, n=500)
+    out = _eval(p, h=p.h0.astype(np.float64) * 1.5)
+    m = p.m.astype(np.float64)
+    v = p.v.astype(np.float64)
+    mom = (m[:, None] * out["a"]).sum(0)
+    mom_scale = (m[:, None] * np.abs(out["a"])).sum()
+    assert np.abs(mom).max() <= 1e-12 * mom_scale
+    e = (m * ((v * out["a"]).sum(1) + out["dudt"])).sum()
+    e_scale = (m * (np.abs((v * out["a"]).sum(1)) + np.abs(out["dudt"]))).sum()
+    assert abs(e) <= 1e-12 * e_scale
+    # viscosity is active and heats: per particle du_visc >= 0, total > 0
+    assert np.all(out["dudt_visc"] >= -1e-300)
+    assert out["dudt_visc"].sum() > 0
+    # magnitude scales bound the results
+    assert np.all(np.linalg.norm(out["a"], axis=1) <= out["S_a"] * (1 + 1e-12))
+    assert np.all(np.abs(out["dudt"]) <= out["S_u"] * (1 + 1e-12))
+
+
+def test_galilean_invariance():
+    p = workloads.tiny(6, n=400)
+    h = p.h0.astype(np.float64) * 1.5
+    a0 = _eval(p, h=h)
+    a1 = _eval(p, h=h, v=p.v.astype(np.float64) + np.array([5.0, -1.0, 2.0]))
+    assert np.allclose(a0["a"], a1["a"], rtol=1e-8, atol=1e-8 * np.abs(a0["a"]).max())
+    assert np.allclose(a0["dudt"], a1["dudt"], rtol=1e-8, atol=1e-8 * np.abs(a0["dudt"]).max())
+
+
+def test_uniform_velocity_has_no_viscosity():
+    p = workloads.tiny(7, n=300)
+    h = p.h0.astype(np.float64) * 1.5
+    v = np.tile(np.array([[0.3, -0.2, 0.1]]), (p.n, 1))
+    out = _eval(p, h=h, v=v)
+    assert np.all(out["dudt_visc"] == 0.0)
+    assert np.allclose(out["dudt"], 0.0, atol=1e-12 * out["S_u"].max() + 1e-300)
+
+
+def _W(r, h):
+    q = r / h
+    if q <= 0.5:
+        fq = 1 - 6 * q * q + 6 * q ** 3
+    elif q <= 1:
+        fq = 2 * (1 - q) ** 3
+    else:
+        fq = 0.0
+    return 8 / (math.pi * h ** 3) * fq
+
+
+def _dWdr(r, h):
+    q = r / h
+    if q <= 0.5:
+        fp = -12 * q + 18 * q * q
+    elif q <= 1:
+        fp = -6 * (1 - q) ** 2
+    else:
+        fp = 0.0
+    return 8 / (math.pi * h ** 4) * fp
+
+
+def test_two_particles_by_hand():
+    """Two particles, unequal m, h, u; velocities with shear (so the Balsara
+    limiter is non-zero) and approach (so the viscosity is on). Each quantity
+    is written out from the paper for N = 2 with scalar arithmetic."""
+    L = 1.0
+    xi = np.array([0.30, 0.50, 0.50])
+    xj = np.array([0.34, 0.53, 0.50])
+    vi = np.array([0.40, 0.10, 0.0])
+    vj = np.array([-0.20, -0.30, 0.05])
+    mi, mj = 2.0e-3, 3.0e-3
+    hi, hj = 0.06, 0.045
+    ui, uj = 1.3, 0.7
+    gam, alpha = 5.0 / 3.0, 0.8
+    dx = xi - xj
+    r = float(np.linalg.norm(dx))
+    assert hj < r < hi                    # asymmetric: j is in range of i only
+    # Eq. 2 (self included, R2): rho_i sees j; rho_j sees only itself
+    rho_i = mi * _W(0, hi) + mj * _W(r, hi)
+    rho_j = mj * _W(0, hj)
+    # Omega = 1 + h/(3 rho) d rho/dh with dW/dh = -(3W + r dW/dr)/h
+    dWdh = lambda rr, h: -(3 * _W(rr, h) + rr * _dWdr(rr, h)) / h
+    om_i = 1 + hi / (3 * rho_i) * (mi * dWdh(0, hi) + mj * dWdh(r, hi))
+    om_j = 1 + hj / (3 * rho_j) * (mj * dWdh(0, hj))          # = 0 exactly (isolated)
+    assert abs(om_j) < 1e-15
+    # div/curl of i (j has none): gradW_i = dW/dr(r,h_i) * dx / r
+    gw = _dWdr(r, hi) * dx / r
+    div_i = mj * np.dot(vj - vi, gw) / rho_i
+    curl_i = -mj * np.cross(vj - vi, gw) / rho_i
+    P_i, P_j = (gam - 1) * rho_i * ui, (gam - 1) * rho_j * uj
+    c_i, c_j = math.sqrt(gam * P_i / rho_i), math.sqrt(gam * P_j / rho_j)
+    f_i = np.linalg.norm(curl_i) / (abs(div_i) + np.linalg.norm(curl_i) + 1e-4 * c_i / hi)
+    f_j = 0.0                            # curl_j = 0 (no neighbours), div_j = 0 -> 0/(0+0+eps)
+    # density-level checks
+    x = np.stack([xi, xj])
+    v = np.stack([vi, vj])
+    m = np.array([mi, mj])
+    h = np.array([hi, hj])
+    u = np.array([ui, uj])
+    d = oracle.density_at(x, v, m, h, (L, L, L))
+    assert d["rho"] == pytest.approx([rho_i, rho_j], rel=1e-14)
+    assert d["omega"][0] == pytest.approx(om_i, rel=1e-12)
+    assert d["div"][0] == pytest.approx(div_i, rel=1e-12)
+    assert np.allclose(d["curl"][0], curl_i, rtol=1e-12)
+    st = oracle.particle_state(d["rho"], d["omega"], u, h, d["div"], d["curl"])
+    assert st["f"][0] == pytest.approx(f_i, rel=1e-12) and st["f"][1] == 0.0
+    # Eq. 4 + viscosity for the pair r < max(h_i,h_j) = h_i. Omega_j = 0 makes A_j
+    # infinite, but G_j = 0 (r > h_j) so the A_j term must be excluded, not 0*inf:
+    # use a finite stand-in A_j to check that the oracle ignores it.
+    A_i = P_i / (om_i * rho_i ** 2)
+    A_j = 123.0
+    G_i = _dWdr(r, hi) / r
+    vij = vi - vj
+    w = min(0.0, np.dot(vij, dx) / r)
+    assert w < 0                          # approaching
+    Pi = -alpha * (c_i + c_j - 3 * w) * w / (rho_i + rho_j)
+    a_i = -mj * (A_i * G_i + 0.25 * Pi * (f_i + f_j) * G_i) * dx
+    a_j = +mi * (A_i * G_i + 0.25 * Pi * (f_i + f_j) * G_i) * dx
+    du_i = mj * np.dot(vij, dx) * (A_i * G_i + 0.125 * Pi * (f_i + f_j) * G_i)
+    du_j = mi * np.dot(vij, dx) * (0.125 * Pi * (f_i + f_j) * G_i)
+    fo = oracle.force_at(x, v, m, h, d["rho"], np.array([A_i, A_j]),
+                         np.array([c_i, c_j]), np.array([f_i, f_j]), (L, L, L), alpha=alpha)
+    assert np.allclose(fo["a"][0], a_i, rtol=1e-12)
+    assert np.allclose(fo["a"][1], a_j, rtol=1e-12)
+    assert fo["dudt"][0] == pytest.approx(du_i, rel=1e-12)
+    assert fo["dudt"][1] == pytest.approx(du_j, rel=1e-12)
+    assert fo["vsig"][0] == pytest.approx(c_i + c_j - 3 * w, rel=1e-14)
+    assert list(fo["n_nbr_force"]) == [1, 1]
+    # pressure pushes i away from j (repulsive): a_i . (x_i - x_j) > 0
+    assert np.dot(fo["a"][0], dx) > 0
