@@ -1,0 +1,157 @@
+/*
+ * sph.h — C ABI of libsph: the B200 (sm_100a) hot path of Gonnet's SPH method
+ * (arXiv:1404.2303): neighbour finding over a hierarchical cell decomposition
+ * with sorted pair interactions, the density loop with h solved to a target
+ * neighbour number, and the symmetric pressure + viscosity force loop.
+ *
+ * Citations: P:<line> = PAPER.md line (section / equation named); R<n> = the
+ * readings of the paper listed in DESIGN.md ("Readings").
+ *
+ * ---------------------------------------------------------------------------
+ * Conventions (apply to every call)
+ *  - Particle arrays are fp32 unless stated, length n, vectors row-major [n][3],
+ *    in the CALLER's particle order. A pointer may be a CUDA device pointer or a
+ *    host pointer (pinned or pageable); libsph detects which with
+ *    cudaPointerGetAttributes and copies host data in/out itself on the
+ *    context's stream.
+ *  - Ownership: the caller owns every array it passes; libsph never frees or
+ *    keeps them beyond the call. libsph owns everything inside sph_ctx
+ *    (cell-ordered copies, cell hierarchy, interaction slots, sorted lists,
+ *    scratch) and frees it in sph_destroy.
+ *  - Ordering: calls are ordered on the context's stream. With SPH_F_SYNC
+ *    (default) each call synchronises before returning, so the status reflects
+ *    device errors and the stats are filled.
+ *  - Errors: every call returns an sph_status; sph_last_error(ctx) gives the
+ *    detail of the last failing call on that context. On error the outputs are
+ *    unspecified, except SPH_E_NOCONV, which writes every output from the last
+ *    iterate.
+ *  - Threads: one context per host thread at a time; distinct contexts are
+ *    independent.
+ * ---------------------------------------------------------------------------
+ */
+#ifndef SPH_H
+#define SPH_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPH_ABI_VERSION 1
+
+typedef struct sph_ctx sph_ctx;
+
+typedef enum {
+  SPH_OK = 0,
+  SPH_E_ARG = -1,    /* null required pointer, n <= 0, n changed between calls, bad config
+                        (box <= 0, gamma <= 1, alpha < 0, n_ngb <= 32/3, tol <= 0,
+                        top_edge_factor < 1, split_fraction outside (0,1]) */
+  SPH_E_DOMAIN = -2, /* non-finite input; x outside [0,L); m <= 0; u <= 0; h0 < 0;
+                        a smoothing length >= min(L)/3 (fewer than 3 top cells per axis) */
+  SPH_E_STATE = -3,  /* order violated: density before build_cells, force before density */
+  SPH_E_NOCONV = -4, /* h iteration hit max_h_iter; all outputs written from the last iterate */
+  SPH_E_CUDA = -5,
+  SPH_E_NCCL = -6,
+  SPH_E_OOM = -7
+} sph_status;
+
+/* flags */
+#define SPH_F_SYNC 1u             /* synchronise at the end of each call (default on) */
+#define SPH_F_COUNT_CANDIDATES 2u /* count distance tests (stats.n_candidates) */
+
+typedef struct {
+  int32_t abi_version;   /* = SPH_ABI_VERSION */
+  double box[3];         /* periodic domain [0,Lx)x[0,Ly)x[0,Lz) */
+  float gamma;           /* polytropic index, 5/3 */
+  float n_ngb;           /* target weighted neighbour number of Eq. 3, 48 (P:176-182,
+                            P:1352); the self term is included (R2) */
+  float n_ngb_tol;       /* converged iff |N_i - n_ngb| <= tol; 1e-4 default (R3);
+                            1.0 = the paper's "e.g. +-1" */
+  int32_t max_h_iter;    /* density passes allowed for the h iteration (default 64) */
+  float alpha;           /* viscosity alpha, 0.8; 0 disables viscosity */
+  float balsara_eps;     /* 1e-4 in the Balsara denominator (R10) */
+  int32_t split_count;   /* split a cell only if it holds more particles: 300 */
+  float split_fraction;  /* ... and more than this fraction has h < edge/2: 0.875 */
+  float top_edge_factor; /* kappa >= 1: top cell edge >= kappa * max h ("larger or equal") */
+  float h_margin;        /* >= 1: cells are built for h_build = h * h_margin so the Newton
+                            iteration can grow h without a rebuild */
+  uint32_t flags;        /* SPH_F_* */
+  int32_t rank, nranks;  /* 0, 1 for a single GPU */
+  double slab_lo, slab_hi; /* owned x-range of this rank (multi-GPU) */
+} sph_config;
+
+typedef struct {         /* host struct, filled when non-NULL */
+  int64_t n_pairs;       /* F: unordered pairs with r < max(h_i,h_j) */
+  int64_t n_directed;    /* D: ordered (i,j), j != i, r_ij < h_i */
+  int64_t n_candidates;  /* distance tests of the last density pass and the force pass
+                            (SPH_F_COUNT_CANDIDATES) */
+  int64_t n_unconverged; /* particles not converged when the density call returned */
+  int64_t n_rebuilds;    /* structure rebuilds triggered by h outgrowing its cells */
+  int32_t h_iters;       /* density passes executed */
+  int32_t n_levels;      /* depth of the cell hierarchy + 1 */
+  int64_t n_cells, n_leaves, n_pair_slots; /* hierarchy size; kept pair entries (directed) */
+  double ms_build, ms_density, ms_force, ms_halo;
+  int64_t halo_sent, halo_recv;
+} sph_stats;
+
+/* Fill *cfg with the paper's defaults for the given box. */
+void sph_config_default(sph_config* cfg, double lx, double ly, double lz);
+
+/* Create a context on `cuda_device`, ordered on `cuda_stream` (cudaStream_t or NULL for
+ * a context-owned stream). Validates *cfg (SPH_E_ARG). *out is NULL on failure. */
+int sph_create(const sph_config* cfg, int cuda_device, void* cuda_stream, sph_ctx** out);
+int sph_destroy(sph_ctx* ctx);
+
+/* Route libsph's device allocations through the caller's allocator (e.g. torch's
+ * caching allocator). Must be called before the first build. NULL restores cudaMalloc. */
+int sph_set_allocator(sph_ctx* ctx, void* (*alloc)(size_t bytes, void* stream, void* user),
+                      void (*release)(void* ptr, void* stream, void* user), void* user);
+
+const char* sph_status_string(int status);
+const char* sph_last_error(const sph_ctx* ctx);
+
+/* 1. Neighbour-finding structure (section 3.2).
+ *    x  [n][3]: positions in [0,L) (copied).
+ *    h0 [n] or NULL: initial smoothing lengths (support radius); NULL or
+ *       h0[i] == 0 -> library guess from cell occupancy.
+ *    Bins particles into the top grid (edge >= kappa*max h), sorts them by
+ *    cell key (device radix sort), splits cells recursively (P:510-518 with
+ *    split_count / split_fraction), builds the self/pair interaction slots with the
+ *    refinement rules of P:519-532, and the 13-direction sorted lists.
+ *    Errors: SPH_E_ARG, SPH_E_DOMAIN, SPH_E_CUDA, SPH_E_OOM. */
+int sph_build_cells(sph_ctx* ctx, int64_t n, const float* x, const float* h0);
+
+/* 2. Density loop (Eq. 2-3) with h_i solved to N_i = n_ngb +- tol by a
+ *    bracketed Newton/bisection iteration (R3-R4); re-bins when an h
+ *    outgrows the cells it was binned for. Then the "ghost" step:
+ *    Omega, P, c, A = P/(Omega rho^2), div/curl v and Balsara f
+ *    (P:1303-1310), kept inside ctx for sph_force.
+ *    v [n][3], m [n] (> 0), u [n] (> 0): copied.
+ *    Outputs (caller order): h_out [n], rho_out [n]; optional (NULL to skip)
+ *    omega_out [n], n_nbr_out [n] (#{j != i : r_ij < h_i}, R21), div_out [n],
+ *    curl_out [n][3].
+ *    Errors: SPH_E_STATE (no build), SPH_E_DOMAIN, SPH_E_NOCONV, SPH_E_CUDA. */
+int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u,
+                float* h_out, float* rho_out, float* omega_out, int32_t* n_nbr_out,
+                float* div_out, float* curl_out, sph_stats* st);
+
+/* 3. Force loop: Eq. 4 and Eq. 5 + Monaghan-Balsara viscosity
+ *     over every pair with r_ij < max(h_i, h_j), using the
+ *    ctx's state from sph_density. Idempotent.
+ *    Outputs (caller order): a_out [n][3] (dv/dt), dudt_out [n]; optional
+ *    vsig_out [n] (max_j c_i + c_j - 3 w_ij, the Eq. 6 denominator P:1267),
+ *    n_nbr_force_out [n] (#{j != i : r_ij < max(h_i,h_j)}).
+ *    Errors: SPH_E_STATE (no density), SPH_E_CUDA. */
+int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out,
+              int32_t* n_nbr_force_out, sph_stats* st);
+
+/* Number of CUDA kernel launches libsph issued on this context since creation
+ * (evidence for the bench's gpu_launches). */
+int64_t sph_kernel_launches(const sph_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPH_H */

@@ -1,0 +1,162 @@
+// common.cuh — shared device helpers and the context struct of libsph (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+#include <string>
+#include <vector>
+
+#include "../../include/sph.h"
+
+#define SPH_WARP 32
+#define FULL_MASK 0xffffffffu
+
+// ---------------------------------------------------------------- errors -----
+struct SphError {
+  int status;
+  std::string msg;
+};
+
+#define CUDA_TRY(expr)                                                              \
+  do {                                                                              \
+    cudaError_t _e = (expr);                                                        \
+    if (_e != cudaSuccess)                                                          \
+      throw SphError{_e == cudaErrorMemoryAllocation ? SPH_E_OOM : SPH_E_CUDA,        \
+                     std::string(#expr) + ": " + cudaGetErrorString(_e)};           \
+  } while (0)
+
+#define SPH_REQUIRE(cond, status, msg)                                              \
+  do {                                                                              \
+    if (!(cond)) throw SphError{(status), (msg)};                                   \
+  } while (0)
+
+// ---------------------------------------------------------------- device -----
+__device__ __forceinline__ float warp_max_f(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(FULL_MASK, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_min_f(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(FULL_MASK, v, o));
+  return v;
+}
+__device__ __forceinline__ int warp_sum_i(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL_MASK, v, o);
+  return v;
+}
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// orderable uint for a float (monotone: a < b <=> ord(a) < ord(b))
+__device__ __forceinline__ uint32_t float_ord(float f) {
+  uint32_t b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+// ---------------------------------------------------------------- geometry ---
+// 27 neighbour offsets o in {-1,0,1}^3, index k = (ox+1)*9 + (oy+1)*3 + (oz+1); k = 13 is
+// the cell itself. The 13 canonical sort directions are the offsets whose first non-zero
+// component is positive (k = 14..26); offset k < 13 is the flip of 26-k.
+__host__ __device__ __forceinline__ int off_x(int k) { return k / 9 - 1; }
+__host__ __device__ __forceinline__ int off_y(int k) { return (k / 3) % 3 - 1; }
+__host__ __device__ __forceinline__ int off_z(int k) { return k % 3 - 1; }
+__host__ __device__ __forceinline__ int slot_dir(int k) { return k > 13 ? k - 14 : 12 - k; }
+__host__ __device__ __forceinline__ bool slot_flip(int k) { return k < 13; }
+
+// unit vector of canonical direction d (0..12) = offset k = d + 14
+__device__ __forceinline__ float3 dir_unit(int d) {
+  int k = d + 14;
+  float ox = (float)off_x(k), oy = (float)off_y(k), oz = (float)off_z(k);
+  float inv = rsqrtf(ox * ox + oy * oy + oz * oz);
+  return make_float3(ox * inv, oy * inv, oz * inv);
+}
+
+// ---------------------------------------------------------------- constants --
+#define SPH_PI_F 3.14159265358979323846f
+#define SPH_CNORM (8.0f / SPH_PI_F)   // 8/pi of W
+#define SPH_MAX_DEPTH 10              // Morton levels below the top grid
+#define SPH_NSLOT 27
+
+// ---------------------------------------------------------------- context ----
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct sph_ctx {
+  sph_config cfg;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  void* (*ualloc)(size_t, void*, void*) = nullptr;
+  void (*urelease)(void*, void*, void*) = nullptr;
+  void* uuser = nullptr;
+  std::string err;
+  int64_t launches = 0;
+  int num_sms = 148;
+
+  int64_t n = 0;
+  int state = 0;  // 0 nothing, 1 cells built, 2 density done
+
+  // geometry of the current structure
+  int ntop[3] = {0, 0, 0};
+  double E0[3] = {0, 0, 0};
+  int depth = 0;             // Morton levels below top (keys carry 3*depth bits)
+  int top_bits = 0;
+  std::vector<int> lev_off;  // node index offsets per level (size nlevels+1)
+  int n_nodes = 0, n_leaves = 0;
+  int64_t n_sorted = 0;      // entries of all 13-direction lists
+  int64_t n_pair_slots = 0;
+  int64_t rebuilds = 0;
+
+  // named device buffers
+  DBuf b[64];
+  cudaEvent_t ev[8];
+  bool ev_ok = false;
+};
+
+enum BufId {
+  // caller-order inputs / iteration state
+  B_XIN = 0, B_HIN, B_HB_ORIG, B_HCUR_O, B_LO_O, B_HI_O, B_VIN, B_MIN, B_UIN,
+  // sort scratch
+  B_KEYS0, B_KEYS1, B_VALS0, B_VALS1, B_SORT_HIST, B_SORT_STATUS, B_SORT_CTR, B_SCAN_TMP,
+  // cell-order particle arrays
+  B_PERM, B_XH, B_VM, B_U, B_HB, B_HLO, B_HHI, B_FLAG, B_DSUMF, B_DACC0, B_DACC1, B_FX, B_FS,
+  // nodes
+  B_N_FIRST, B_N_COUNT, B_N_IJK, B_N_PARENT, B_N_CHILD, B_N_HMAXB, B_N_SPLIT, B_N_SLOT, B_N_KEPT,
+  B_N_DIRMASK, B_N_SORTOFF, B_N_HMAXF, B_N_NCH, B_N_CHBASE, B_N_NSORT,
+  // lists / tasks
+  B_SORTED, B_TOPMAP, B_TASKS, B_TASKS2, B_TASKFLAG, B_TASKIDX, B_TMPI0, B_TMPI1, B_TMPL0, B_TMPL1,
+  B_BIGNODES, B_BIGOFF,
+  // misc
+  B_COUNTERS, B_OUT0, B_OUT1, B_OUT2, B_OUT3, B_OUT4, B_OUT5,
+  B_COUNT
+};
+static_assert(B_COUNT <= 64, "too many buffers");
+
+// device counters layout (int64 slots in B_COUNTERS)
+enum CounterId {
+  C_ERR = 0,        // error bits (validation)
+  C_UNCONV,         // unconverged particles after an h update
+  C_REBUILD,        // particles whose h wants to exceed its build h
+  C_CAND,           // candidate distance tests
+  C_NDIR,           // D
+  C_NFORCE,         // sum of force neighbour counts (2F)
+  C_HMAXBITS,       // max h (float bits as int)
+  C_HMINBITS,       // min positive h (float bits)
+  C_TASKS,          // active tasks
+  C_TMP0, C_TMP1, C_TMP2,
+  C_NCOUNTERS
+};
+
+#define ERRBIT_NONFINITE 1
+#define ERRBIT_XRANGE 2
+#define ERRBIT_MASS 4
+#define ERRBIT_U 8
+#define ERRBIT_H 16

@@ -1,0 +1,589 @@
+// interact.cuh — density and force loops over the cell hierarchy with sorted pair sweeps.
+//
+// Work unit: one warp per (leaf cell, chunk of 32 particles); lane = target particle i.
+// A warp visits, in a fixed order,
+//   * the leaf's self interaction (all particles of the leaf), then
+//   * for the leaf and each ancestor, every KEPT pair slot (cell Y at offset k): the
+//     sorted sweep of P:644-669 along canonical direction d = dir(k). Y's particles are
+//     traversed in ascending key order when Y lies on the +d side and descending when it
+//     lies on the -d side (the "flip" of P:693-698), and the sweep stops at the first
+//     source whose projected distance exceeds every lane's window (the early exit of
+//     P:653/P:663). Sources are staged 32 at a time in shared memory with float4 loads;
+//     each lane then tests them against its own target (gather form: the j-side update
+//     of the paper's pair task is the i-side of the mirrored slot, so no atomics).
+// Density window = h_i (r < h_i, Eq. 2); force window = max(h_i, max h in Y)
+// (r < max(h_i, h_j), Eq. 4).
+#pragma once
+#include "build.cuh"
+
+struct TravParams {
+  const int2* tasks;
+  int ntasks;
+  NodeArrays N;
+  LevelGeom g;
+  const SortEntry* sorted;
+  const uint8_t* active;   // null = all
+  float slack;             // absolute window slack (fp32 rounding of keys/corners)
+  unsigned long long* ctr;
+};
+
+// ------------------------------------------------------------------ density ------
+struct DensOp {
+  struct Src {
+    float4 a;  // x, y, z (shifted), unused
+    float4 b;  // vx, vy, vz, m
+  };
+  const float4* __restrict__ xh;
+  const float4* __restrict__ vm;
+  bool valid;
+  int s;
+  float x0, y0, z0;  // unshifted target position
+  float xi, yi, zi;  // shifted for the current segment
+  float hi, hi2, hinv, vxi, vyi, vzi;
+  double sf;
+  float smf, smqfp, sqfp, divs, crx, cry, crz;
+  int cnt;
+  long long ncand;
+
+  __device__ __forceinline__ void init(int s_, bool v) {
+    s = s_;
+    valid = v;
+    sf = 0.0;
+    smf = smqfp = sqfp = divs = crx = cry = crz = 0.f;
+    cnt = 0;
+    ncand = 0;
+    if (v) {
+      float4 p = xh[s];
+      float4 q = vm[s];
+      x0 = p.x; y0 = p.y; z0 = p.z;
+      hi = p.w;
+      vxi = q.x; vyi = q.y; vzi = q.z;
+    } else {
+      x0 = y0 = z0 = 0.f;
+      hi = 0.f;
+      vxi = vyi = vzi = 0.f;
+    }
+    hi2 = hi * hi;
+    hinv = v ? 1.0f / hi : 0.f;
+    xi = x0; yi = y0; zi = z0;
+  }
+  __device__ __forceinline__ float window(const NodeArrays&, int) const { return hi; }
+  __device__ __forceinline__ void shift(float tx, float ty, float tz) {
+    xi = x0 + tx; yi = y0 + ty; zi = z0 + tz;
+  }
+  __device__ __forceinline__ void stage(Src& d, int j, float sx, float sy, float sz) const {
+    float4 p = xh[j];
+    d.a = make_float4(p.x + sx, p.y + sy, p.z + sz, 0.f);
+    d.b = vm[j];
+  }
+  __device__ __forceinline__ void interact(const Src& src, bool is_self) {
+    const float dx = xi - src.a.x, dy = yi - src.a.y, dz = zi - src.a.z;
+    const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    if (r2 < hi2) {
+      const float rinv = r2 > 0.f ? rsqrtf(r2) : 0.f;
+      const float r = r2 * rinv;
+      const float q = r * hinv;
+      float f, fp;
+      if (q <= 0.5f) {
+        f = fmaf(q * q, fmaf(6.f, q, -6.f), 1.f);
+        fp = q * fmaf(18.f, q, -12.f);
+      } else {
+        const float t = 1.f - q;
+        f = 2.f * t * t * t;
+        fp = -6.f * t * t;
+      }
+      const float mj = src.b.w;
+      sf += (double)f;
+      smf = fmaf(mj, f, smf);
+      const float qfp = q * fp;
+      sqfp += qfp;
+      smqfp = fmaf(mj, qfp, smqfp);
+      const float gf = mj * fp * rinv;
+      const float dvx = src.b.x - vxi, dvy = src.b.y - vyi, dvz = src.b.z - vzi;
+      divs = fmaf(gf, fmaf(dvx, dx, fmaf(dvy, dy, dvz * dz)), divs);
+      crx = fmaf(gf, dvy * dz - dvz * dy, crx);
+      cry = fmaf(gf, dvz * dx - dvx * dz, cry);
+      crz = fmaf(gf, dvx * dy - dvy * dx, crz);
+      cnt += is_self ? 0 : 1;
+    }
+  }
+};
+
+// ------------------------------------------------------------------ force --------
+struct ForceOp {
+  struct Src {
+    float4 a;  // x, y, z (shifted), 1/h
+    float4 b;  // vx, vy, vz, m
+    float4 c;  // A~ = A * (8/pi) h^-4, rho, c, f
+  };
+  const float4* __restrict__ fx;
+  const float4* __restrict__ vm;
+  const float4* __restrict__ fs;
+  float alpha;
+  bool valid;
+  int s;
+  float x0, y0, z0, xi, yi, zi;
+  float hi, hi2, hinv, hhat, At, rhoi, ci, fi, vxi, vyi, vzi;
+  float ax, ay, az, du, vsig;
+  int cnt;
+  long long ncand;
+
+  __device__ __forceinline__ void init(int s_, bool v) {
+    s = s_;
+    valid = v;
+    ax = ay = az = du = vsig = 0.f;
+    cnt = 0;
+    ncand = 0;
+    if (v) {
+      float4 p = fx[s], q = vm[s], w = fs[s];
+      x0 = p.x; y0 = p.y; z0 = p.z;
+      hinv = p.w;
+      hi = 1.0f / hinv;
+      vxi = q.x; vyi = q.y; vzi = q.z;
+      At = w.x; rhoi = w.y; ci = w.z; fi = w.w;
+    } else {
+      x0 = y0 = z0 = 0.f;
+      hinv = 0.f; hi = 0.f;
+      vxi = vyi = vzi = 0.f;
+      At = rhoi = ci = fi = 0.f;
+    }
+    hi2 = hi * hi;
+    const float h2i = hinv * hinv;
+    hhat = SPH_CNORM * h2i * h2i;
+    xi = x0; yi = y0; zi = z0;
+  }
+  __device__ __forceinline__ float window(const NodeArrays& N, int Y) const {
+    return fmaxf(hi, N.hmaxf[Y]);
+  }
+  __device__ __forceinline__ void shift(float tx, float ty, float tz) {
+    xi = x0 + tx; yi = y0 + ty; zi = z0 + tz;
+  }
+  __device__ __forceinline__ void stage(Src& d, int j, float sx, float sy, float sz) const {
+    float4 p = fx[j];
+    d.a = make_float4(p.x + sx, p.y + sy, p.z + sz, p.w);
+    d.b = vm[j];
+    d.c = fs[j];
+  }
+  __device__ __forceinline__ static float fprime(float q) {
+    if (q <= 0.5f) return q * fmaf(18.f, q, -12.f);
+    const float t = 1.f - q;
+    return -6.f * t * t;
+  }
+  __device__ __forceinline__ void interact(const Src& src, bool is_self) {
+    const float dx = xi - src.a.x, dy = yi - src.a.y, dz = zi - src.a.z;
+    const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    const float hjinv = src.a.w;
+    const float hj2i = hjinv * hjinv;
+    const bool in_i = r2 < hi2;
+    const bool in_j = r2 * hj2i < 1.0f;
+    if ((in_i || in_j) && !is_self) {
+      const float rinv = r2 > 0.f ? rsqrtf(r2) : 0.f;
+      const float r = r2 * rinv;
+      const float fpi = in_i ? fprime(r * hinv) : 0.f;
+      const float fpj = in_j ? fprime(r * hjinv) : 0.f;
+      const float hhatj = SPH_CNORM * hj2i * hj2i;
+      const float Gi = hhat * fpi * rinv;
+      const float Gj = hhatj * fpj * rinv;
+      const float vx = vxi - src.b.x, vy = vyi - src.b.y, vz = vzi - src.b.z;
+      const float vdx = fmaf(vx, dx, fmaf(vy, dy, vz * dz));
+      const float w = fminf(0.f, vdx * rinv);
+      const float cs = ci + src.c.z - 3.f * w;
+      const float Pi = -alpha * cs * w / (rhoi + src.c.y);
+      const float V = Pi * (fi + src.c.w) * (Gi + Gj);
+      const float AGi = At * fpi * rinv;
+      const float AGj = src.c.x * fpj * rinv;
+      const float T = AGi + AGj + 0.25f * V;
+      const float mj = src.b.w;
+      const float mT = mj * T;
+      ax = fmaf(-mT, dx, ax);
+      ay = fmaf(-mT, dy, ay);
+      az = fmaf(-mT, dz, az);
+      du = fmaf(mj * vdx, AGi + 0.125f * V, du);
+      vsig = fmaxf(vsig, cs);
+      cnt += 1;
+    }
+  }
+};
+
+// ------------------------------------------------------------------ traversal ----
+template <class Op>
+__device__ __forceinline__ void seg_self(Op& op, int first, int cnt, typename Op::Src* sm, int lane) {
+  const int my = op.s - first;
+  for (int base = 0; base < cnt; base += 32) {
+    const int e = base + lane;
+    if (e < cnt) op.stage(sm[lane], first + e, 0.f, 0.f, 0.f);
+    __syncwarp();
+    const int m = min(32, cnt - base);
+    if (op.valid) {
+      op.ncand += m;
+#pragma unroll 4
+      for (int t = 0; t < m; ++t) op.interact(sm[t], base + t == my);
+    }
+    __syncwarp();
+  }
+}
+
+template <class Op>
+__device__ __forceinline__ void seg_pair(Op& op, const TravParams& P, int X, int Y, int k, int level,
+                                         typename Op::Src* sm, int lane) {
+  const int d = slot_dir(k);
+  const bool flip = slot_flip(k);
+  const float3 du = dir_unit(d);
+  const int4 cX = P.N.ijk[X], cY = P.N.ijk[Y];
+  // periodic shift: Y's unwrapped copy sits at Y + s*L (s in {-1,0,1} per axis)
+  int ddx = cX.x + off_x(k) - cY.x, ddy = cX.y + off_y(k) - cY.y, ddz = cX.z + off_z(k) - cY.z;
+  const int sx = ddx > 1 ? 1 : (ddx < -1 ? -1 : 0);
+  const int sy = ddy > 1 ? 1 : (ddy < -1 ? -1 : 0);
+  const int sz = ddz > 1 ? 1 : (ddz < -1 ? -1 : 0);
+  // exact fp32 shifts: always subtract L from the copy that lies near L (Sterbenz)
+  const float tox = sx > 0 ? -P.g.L[0] : 0.f, toy = sy > 0 ? -P.g.L[1] : 0.f, toz = sz > 0 ? -P.g.L[2] : 0.f;
+  const float sox = sx < 0 ? -P.g.L[0] : 0.f, soy = sy < 0 ? -P.g.L[1] : 0.f, soz = sz < 0 ? -P.g.L[2] : 0.f;
+  op.shift(tox, toy, toz);
+  const float cyx = node_corner(cY.x, level, 0, P.g) + sox;
+  const float cyy = node_corner(cY.y, level, 1, P.g) + soy;
+  const float cyz = node_corner(cY.z, level, 2, P.g) + soz;
+  const float pi = proj(op.xi - cyx, op.yi - cyy, op.zi - cyz, du);   // target key in Y's frame
+  const float w = op.window(P.N, Y);
+  const float wq = fmaf(w, 1.00001f, P.slack);
+  float lim = flip ? pi - wq : pi + wq;
+  if (!op.valid) lim = flip ? INFINITY : -INFINITY;
+  const float Lw = flip ? warp_min_f(lim) : warp_max_f(lim);
+  const int nY = P.N.count[Y];
+  const int dm = P.N.dirmask[Y];
+  const SortEntry* __restrict__ list = P.sorted + P.N.sortoff[Y] + (int64_t)__popc(dm & ((1 << d) - 1)) * nY;
+  for (int base = 0; base < nY; base += 32) {
+    const int e = base + lane;
+    bool in = false;
+    int j = 0;
+    if (e < nY) {
+      const SortEntry en = list[flip ? nY - 1 - e : e];
+      in = flip ? (en.key > Lw) : (en.key < Lw);
+      j = en.idx;
+    }
+    const unsigned bal = __ballot_sync(FULL_MASK, in);
+    const int m = __popc(bal);
+    if (m == 0) break;
+    if (in) op.stage(sm[lane], j, sox, soy, soz);
+    __syncwarp();
+    if (op.valid) {
+      op.ncand += m;
+#pragma unroll 4
+      for (int t = 0; t < m; ++t) op.interact(sm[t], false);
+    }
+    __syncwarp();
+    if (m < 32) break;
+  }
+}
+
+template <class Op>
+__device__ __forceinline__ void traverse(Op& op, const TravParams& P, int leaf, typename Op::Src* sm, int lane) {
+  const int first = P.N.first[leaf], cnt = P.N.count[leaf];
+  seg_self(op, first, cnt, sm, lane);
+  int X = leaf;
+  int level = P.N.ijk[leaf].w;
+  while (X >= 0) {
+    unsigned kept = (unsigned)P.N.kept[X];
+    while (kept) {
+      const int k = __ffs(kept) - 1;
+      kept &= kept - 1;
+      const int Y = P.N.slot[27 * (int64_t)X + k];
+      seg_pair(op, P, X, Y, k, level, sm, lane);
+    }
+    X = P.N.parent[X];
+    --level;
+  }
+}
+
+#define INTERACT_WARPS 4
+
+struct DensOut {
+  double* sf;
+  float4* acc0;   // smf, smqfp, sqfp, divs
+  float4* acc1;   // curl sums xyz, count (int bits)
+};
+
+__global__ void __launch_bounds__(INTERACT_WARPS * 32) k_density(TravParams P, const float4* __restrict__ xh,
+                                                                 const float4* __restrict__ vm, DensOut out) {
+  __shared__ DensOp::Src smem[INTERACT_WARPS][32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int t = blockIdx.x * INTERACT_WARPS + wib;
+  if (t >= P.ntasks) return;
+  const int2 task = P.tasks[t];
+  const int leaf = task.x;
+  const int first = P.N.first[leaf], cnt = P.N.count[leaf];
+  const int li = task.y * 32 + lane;
+  const int s = first + li;
+  bool v = li < cnt;
+  if (v && P.active) v = P.active[s] != 0;
+  if (!__any_sync(FULL_MASK, v)) return;
+  DensOp op;
+  op.xh = xh;
+  op.vm = vm;
+  op.init(s, v);
+  traverse(op, P, leaf, smem[wib], lane);
+  if (v) {
+    out.sf[s] = op.sf;
+    out.acc0[s] = make_float4(op.smf, op.smqfp, op.sqfp, op.divs);
+    out.acc1[s] = make_float4(op.crx, op.cry, op.crz, __int_as_float(op.cnt));
+  }
+  long long nc = op.ncand;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nc += __shfl_xor_sync(FULL_MASK, nc, o);
+  if (lane == 0 && P.ctr) atomicAdd(&P.ctr[C_CAND], (unsigned long long)nc);
+}
+
+struct ForceOut {
+  float* a;        // [n][3] caller order
+  float* dudt;     // [n]
+  float* vsig;     // [n] or null
+  int* nnbr;       // [n] or null
+  const uint32_t* perm;
+};
+
+__global__ void __launch_bounds__(INTERACT_WARPS * 32) k_force(TravParams P, const float4* __restrict__ fx,
+                                                               const float4* __restrict__ vm,
+                                                               const float4* __restrict__ fs, float alpha,
+                                                               ForceOut out) {
+  __shared__ ForceOp::Src smem[INTERACT_WARPS][32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int t = blockIdx.x * INTERACT_WARPS + wib;
+  if (t >= P.ntasks) return;
+  const int2 task = P.tasks[t];
+  const int leaf = task.x;
+  const int first = P.N.first[leaf], cnt = P.N.count[leaf];
+  const int li = task.y * 32 + lane;
+  const int s = first + li;
+  const bool v = li < cnt;
+  ForceOp op;
+  op.fx = fx;
+  op.vm = vm;
+  op.fs = fs;
+  op.alpha = alpha;
+  op.init(s, v);
+  traverse(op, P, leaf, smem[wib], lane);
+  if (v) {
+    const uint32_t p = out.perm[s];
+    out.a[3 * (int64_t)p] = op.ax;
+    out.a[3 * (int64_t)p + 1] = op.ay;
+    out.a[3 * (int64_t)p + 2] = op.az;
+    out.dudt[p] = op.du;
+    if (out.vsig) out.vsig[p] = op.vsig;
+    if (out.nnbr) out.nnbr[p] = op.cnt;
+  }
+  long long nc = op.ncand;
+  long long nf = v ? op.cnt : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    nc += __shfl_xor_sync(FULL_MASK, nc, o);
+    nf += __shfl_xor_sync(FULL_MASK, nf, o);
+  }
+  if (lane == 0 && P.ctr) {
+    atomicAdd(&P.ctr[C_CAND], (unsigned long long)nc);
+    atomicAdd(&P.ctr[C_NFORCE], (unsigned long long)nf);
+  }
+}
+
+// ------------------------------------------------------------------ h update ------
+// Bracketed Newton/bisection step on N_i(h) = (32/3) sum_j f(r_ij/h) (Eq. 3):
+// converged iff |N - n_ngb| <= tol (R3); a step that leaves the bracket [lo, hi] is
+// replaced by a cube-root rescale (no upper bracket yet) or a bisection (R4).
+__global__ void k_h_update(int64_t n, float4* __restrict__ xh, const float* __restrict__ hb,
+                           float* __restrict__ lo, float* __restrict__ hi, uint8_t* __restrict__ active,
+                           const double* __restrict__ sf, const float4* __restrict__ acc0, float n_t,
+                           float tol, unsigned long long* ctr) {
+  int unconv = 0, reb = 0;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    if (!active[s]) continue;
+    const float h = xh[s].w;
+    const double N = (32.0 / 3.0) * sf[s];
+    const float res = (float)(N - (double)n_t);
+    if (fabsf(res) <= tol) {
+      active[s] = 0;
+      continue;
+    }
+    float l = lo[s], u = hi[s];
+    if (res < 0.f) l = h;
+    else u = h;
+    if (u - l <= 4.f * (h * 1.1920929e-7f)) {   // bracket at fp32 resolution: stop
+      active[s] = 0;
+      lo[s] = l;
+      hi[s] = u;
+      continue;
+    }
+    const float dN = -(32.f / 3.f) * acc0[s].z / h;
+    float hn = h - res / dN;
+    if (!(dN > 0.f) || !(hn > l) || !(hn < u)) {
+      const float sc = cbrtf(n_t / (float)N);
+      if (isinf(u)) hn = h * fminf(2.f, fmaxf(sc * 1.05f, 1.01f));
+      else if (l == 0.f) hn = h * fmaxf(0.5f, fminf(sc * 0.95f, 0.99f));
+      else hn = 0.5f * (l + u);
+    }
+    hn = fminf(fmaxf(hn, 0.5f * h), 2.f * h);
+    lo[s] = l;
+    hi[s] = u;
+    xh[s].w = hn;
+    ++unconv;
+    if (hn > hb[s]) ++reb;
+  }
+  unconv = warp_sum_i(unconv);
+  reb = warp_sum_i(reb);
+  if ((threadIdx.x & 31) == 0) {
+    if (unconv) atomicAdd(&ctr[C_UNCONV], (unsigned long long)unconv);
+    if (reb) atomicAdd(&ctr[C_REBUILD], (unsigned long long)reb);
+  }
+}
+
+// tasks with at least one active lane (compaction flags)
+__global__ void k_task_active(const int2* __restrict__ tasks, int ntasks, NodeArrays N,
+                              const uint8_t* __restrict__ active, int* __restrict__ flag) {
+  const int lane = threadIdx.x & 31;
+  const int t = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  if (t >= ntasks) return;
+  const int2 task = tasks[t];
+  const int li = task.y * 32 + lane;
+  const int first = N.first[task.x], cnt = N.count[task.x];
+  bool a = li < cnt && active[first + li];
+  bool any = __any_sync(FULL_MASK, a);
+  if (lane == 0) flag[t] = any ? 1 : 0;
+}
+
+__global__ void k_task_compact(const int2* __restrict__ tasks, int ntasks, const int* __restrict__ flag,
+                               const int* __restrict__ idx, int2* __restrict__ out) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < ntasks && flag[t]) out[idx[t]] = tasks[t];
+}
+
+// ------------------------------------------------------------------ ghost --------
+// P:770-781 "ghost": per-particle quantities between the density and force loops.
+//   rho = (8/pi) h^-3 sum m f                      (Eq. 2)
+//   Omega = -(sum m q f') / (3 sum m f)            (= 1 + h/(3 rho) drho/dh, identity)
+//   P = (gamma-1) rho u,  c = sqrt(gamma (gamma-1) u),  A = P/(Omega rho^2)
+//   div = sum m (f'/r) dv.dx / (h sum m f),  curl = -sum m (f'/r) dv x dx / (h sum m f)
+//   f = |curl| / (|div| + |curl| + eps c/h)       (R10)
+struct GhostOut {
+  float* h;
+  float* rho;
+  float* omega;
+  int* nnbr;
+  float* div;
+  float* curl;
+  const uint32_t* perm;
+};
+
+__global__ void k_ghost(int64_t n, const float4* __restrict__ xh, const float* __restrict__ u,
+                        const double* __restrict__ sf, const float4* __restrict__ acc0,
+                        const float4* __restrict__ acc1, float gamma, float beps, float4* __restrict__ fx,
+                        float4* __restrict__ fs, GhostOut out, unsigned long long* ctr) {
+  long long nd = 0;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const float4 p = xh[s];
+    const float h = p.w, hinv = 1.0f / h;
+    const float4 a0 = acc0[s], a1 = acc1[s];
+    const float smf = a0.x;
+    const float rho = SPH_CNORM * hinv * hinv * hinv * smf;
+    const float omega = -a0.y / (3.f * smf);
+    const float uu = u[s];
+    const float P = (gamma - 1.f) * rho * uu;
+    const float c = sqrtf(gamma * (gamma - 1.f) * uu);
+    const float A = P / (omega * rho * rho);
+    const float nrm = 1.0f / (h * smf);
+    const float div = a0.w * nrm;
+    const float cx = -a1.x * nrm, cy = -a1.y * nrm, cz = -a1.z * nrm;
+    const float cn = sqrtf(cx * cx + cy * cy + cz * cz);
+    const float fb = cn / (fabsf(div) + cn + beps * c * hinv);
+    const float h2i = hinv * hinv;
+    fx[s] = make_float4(p.x, p.y, p.z, hinv);
+    fs[s] = make_float4(A * SPH_CNORM * h2i * h2i, rho, c, fb);
+    const int cnt = __float_as_int(a1.w);
+    nd += cnt;
+    const uint32_t o = out.perm[s];
+    out.h[o] = h;
+    out.rho[o] = rho;
+    if (out.omega) out.omega[o] = omega;
+    if (out.nnbr) out.nnbr[o] = cnt;
+    if (out.div) out.div[o] = div;
+    if (out.curl) {
+      out.curl[3 * (int64_t)o] = cx;
+      out.curl[3 * (int64_t)o + 1] = cy;
+      out.curl[3 * (int64_t)o + 2] = cz;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nd += __shfl_xor_sync(FULL_MASK, nd, o);
+  if ((threadIdx.x & 31) == 0 && nd) atomicAdd(&ctr[C_NDIR], (unsigned long long)nd);
+}
+
+// ------------------------------------------------------------------ misc ---------
+__global__ void k_validate_vmu(const float* __restrict__ v, const float* __restrict__ m, const float* __restrict__ u,
+                               int64_t n, unsigned long long* ctr) {
+  int err = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (!isfinite(v[3 * i]) || !isfinite(v[3 * i + 1]) || !isfinite(v[3 * i + 2])) err |= ERRBIT_NONFINITE;
+    if (!(m[i] > 0.f) || !isfinite(m[i])) err |= ERRBIT_MASS;
+    if (!(u[i] > 0.f) || !isfinite(u[i])) err |= ERRBIT_U;
+  }
+  err = __reduce_or_sync(FULL_MASK, err);
+  if ((threadIdx.x & 31) == 0 && err) atomicOr(&ctr[C_ERR], (unsigned long long)err);
+}
+
+__global__ void k_gather_vmu(const uint32_t* __restrict__ perm, int64_t n, const float* __restrict__ v,
+                             const float* __restrict__ m, const float* __restrict__ u, float4* __restrict__ vm,
+                             float* __restrict__ uc) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t p = perm[s];
+    vm[s] = make_float4(v[3 * (int64_t)p], v[3 * (int64_t)p + 1], v[3 * (int64_t)p + 2], m[p]);
+    uc[s] = u[p];
+  }
+}
+
+// scatter the iteration state back to caller order before a rebuild; h_build = h * margin
+__global__ void k_scatter_state(const uint32_t* __restrict__ perm, int64_t n, const float4* __restrict__ xh,
+                                const float* __restrict__ lo, const float* __restrict__ hi, float margin,
+                                float* __restrict__ hcur_o, float* __restrict__ lo_o, float* __restrict__ hi_o,
+                                float* __restrict__ hb_o) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t p = perm[s];
+    const float h = xh[s].w;
+    hcur_o[p] = h;
+    lo_o[p] = lo[s];
+    hi_o[p] = hi[s];
+    hb_o[p] = h * margin;
+  }
+}
+
+__global__ void k_fill_u8(uint8_t* p, int64_t n, uint8_t v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+__global__ void k_fill_f(float* p, int64_t n, float v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+// h state init from h0 (caller order): h_cur = h0, h_build = h0 * margin, bracket (0, inf)
+__global__ void k_init_h(const float* __restrict__ h0, int64_t n, float margin, float* __restrict__ hcur,
+                         float* __restrict__ hb, float* __restrict__ lo, float* __restrict__ hi) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float h = h0[i];
+    hcur[i] = h;
+    hb[i] = h * margin;
+    lo[i] = 0.f;
+    hi[i] = INFINITY;
+  }
+}
+__global__ void k_count_zero(const float* __restrict__ h, int64_t n, unsigned long long* ctr) {
+  int z = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    z += (h[i] == 0.f) ? 1 : 0;
+  z = warp_sum_i(z);
+  if ((threadIdx.x & 31) == 0 && z) atomicAdd(&ctr[C_TMP0], (unsigned long long)z);
+}
+// keep h0 where given, take the occupancy guess where h0 == 0
+__global__ void k_merge_guess(const float* __restrict__ h0, int64_t n, float* __restrict__ guess) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (h0[i] > 0.f) guess[i] = h0[i];
+}

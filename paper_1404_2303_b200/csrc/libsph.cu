@@ -1,0 +1,787 @@
+// libsph.cu — host orchestration and the C ABI declared in include/sph.h.
+// One translation unit (unity build) so every kernel is launched from the file that
+// defines it; compiled for sm_100a only (see paper_1404_2303_b200/build.py).
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <exception>
+
+#include "common.cuh"
+#include "radix_sort.cuh"
+#include "scan.cuh"
+#include "build.cuh"
+#include "interact.cuh"
+
+// =========================================================== memory =============
+static void* dev_alloc(sph_ctx* c, size_t bytes) {
+  if (c->ualloc) {
+    void* p = c->ualloc(bytes, (void*)c->stream, c->uuser);
+    SPH_REQUIRE(p != nullptr, SPH_E_OOM, "user allocator returned NULL");
+    return p;
+  }
+  void* p = nullptr;
+  CUDA_TRY(cudaMalloc(&p, bytes));
+  return p;
+}
+
+static void dev_free(sph_ctx* c, void* p) {
+  if (!p) return;
+  if (c->ualloc) {
+    c->urelease(p, (void*)c->stream, c->uuser);
+  } else {
+    cudaFree(p);
+  }
+}
+
+// capacity-managed named buffer; keep=true preserves the old contents on growth
+template <class T>
+static T* B(sph_ctx* c, int id, size_t count, bool keep = false) {
+  size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+  DBuf& b = c->b[id];
+  if (b.bytes < bytes) {
+    size_t nb = std::max(bytes, b.bytes + b.bytes / 2);
+    nb = (nb + 255) & ~size_t(255);
+    void* np = dev_alloc(c, nb);
+    if (keep && b.p) CUDA_TRY(cudaMemcpyAsync(np, b.p, b.bytes, cudaMemcpyDeviceToDevice, c->stream));
+    if (b.p) {
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+      dev_free(c, b.p);
+    }
+    b.p = np;
+    b.bytes = nb;
+  }
+  return reinterpret_cast<T*>(b.p);
+}
+template <class T>
+static T* Bget(sph_ctx* c, int id) {
+  return reinterpret_cast<T*>(c->b[id].p);
+}
+
+#define LAUNCH(kern, grid, block, smem, ...)                                        \
+  do {                                                                              \
+    kern<<<(grid), (block), (smem), c->stream>>>(__VA_ARGS__);                      \
+    c->launches++;                                                                  \
+    CUDA_TRY(cudaGetLastError());                                                   \
+  } while (0)
+
+static int grid1d(sph_ctx* c, int64_t n, int block) {
+  int64_t g = (n + block - 1) / block;
+  g = std::min<int64_t>(g, (int64_t)c->num_sms * 16);
+  return (int)std::max<int64_t>(g, 1);
+}
+static int gridfull(int64_t n, int block) { return (int)std::max<int64_t>((n + block - 1) / block, 1); }
+
+static void sync(sph_ctx* c) { CUDA_TRY(cudaStreamSynchronize(c->stream)); }
+
+// =========================================================== counters ===========
+static unsigned long long* ctr(sph_ctx* c) { return B<unsigned long long>(c, B_COUNTERS, C_NCOUNTERS); }
+static void ctr_reset(sph_ctx* c) {
+  unsigned long long init[C_NCOUNTERS];
+  memset(init, 0, sizeof(init));
+  init[C_HMINBITS] = 0x7f800000ull;
+  CUDA_TRY(cudaMemcpyAsync(ctr(c), init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+  sync(c);  // `init` is a stack buffer
+}
+static void ctr_read(sph_ctx* c, unsigned long long* h) {
+  CUDA_TRY(cudaMemcpyAsync(h, ctr(c), sizeof(unsigned long long) * C_NCOUNTERS, cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+}
+
+// =========================================================== scan ===============
+template <class T>
+static T scan_excl(sph_ctx* c, const T* in, T* out, int64_t n) {
+  if (n <= 0) return T(0);
+  int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+  T* sums = reinterpret_cast<T*>(B<char>(c, B_SCAN_TMP, (nb + 2) * sizeof(T)));
+  LAUNCH(k_scan_reduce<T>, (int)nb, SCAN_THREADS, 0, in, n, sums);
+  LAUNCH(k_scan_blocksums<T>, 1, SCAN_THREADS, 0, sums, nb, sums + nb);
+  LAUNCH(k_scan_final<T>, (int)nb, SCAN_THREADS, 0, in, n, sums, out);
+  T total;
+  CUDA_TRY(cudaMemcpyAsync(&total, sums + nb, sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  return total;
+}
+
+// =========================================================== radix sort =========
+static bool g_radix_attr = false;
+static void radix_sort(sph_ctx* c, uint64_t*& keys, uint32_t*& vals, uint64_t*& kalt, uint32_t*& valt,
+                       int64_t n, int bits) {
+  if (n <= 1) return;
+  int npass = std::max(1, (bits + 7) / 8);
+  SPH_REQUIRE(npass <= 8, SPH_E_ARG, "radix sort: more than 64 key bits");
+  SPH_REQUIRE(n < (1ll << 30), SPH_E_ARG, "radix sort: n >= 2^30");
+  uint32_t* hist = B<uint32_t>(c, B_SORT_HIST, 16 * 256);
+  CUDA_TRY(cudaMemsetAsync(hist, 0, 8 * 256 * sizeof(uint32_t), c->stream));
+  LAUNCH(k_radix_hist, grid1d(c, n, 256), 256, 0, keys, n, npass, hist);
+  uint32_t h[8 * 256], g[8 * 256];
+  CUDA_TRY(cudaMemcpyAsync(h, hist, npass * 256 * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  bool trivial[8];
+  for (int p = 0; p < npass; ++p) {
+    uint32_t run = 0;
+    trivial[p] = false;
+    for (int d = 0; d < 256; ++d) {
+      g[p * 256 + d] = run;
+      run += h[p * 256 + d];
+      if (h[p * 256 + d] == (uint32_t)n) trivial[p] = true;
+    }
+  }
+  uint32_t* gofs = hist + 8 * 256;
+  CUDA_TRY(cudaMemcpyAsync(gofs, g, npass * 256 * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
+  int64_t ntiles = (n + RS_TILE - 1) / RS_TILE;
+  uint32_t* status = B<uint32_t>(c, B_SORT_STATUS, ntiles * 256);
+  uint32_t* tctr = B<uint32_t>(c, B_SORT_CTR, 8);
+  if (!g_radix_attr) {
+    CUDA_TRY(cudaFuncSetAttribute(k_radix_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RadixSmem)));
+    g_radix_attr = true;
+  }
+  CUDA_TRY(cudaMemsetAsync(tctr, 0, 8 * sizeof(uint32_t), c->stream));
+  for (int p = 0; p < npass; ++p) {
+    if (trivial[p]) continue;
+    CUDA_TRY(cudaMemsetAsync(status, 0, ntiles * 256 * sizeof(uint32_t), c->stream));
+    LAUNCH(k_radix_pass, (int)ntiles, RS_THREADS, sizeof(RadixSmem), keys, vals, kalt, valt, n, 8 * p,
+           gofs + 256 * p, status, tctr + p);
+    std::swap(keys, kalt);
+    std::swap(vals, valt);
+  }
+  sync(c);  // the host arrays h/g above are stack buffers used by async copies
+}
+
+// =========================================================== nodes ==============
+static NodeArrays nodes(sph_ctx* c) {
+  NodeArrays N;
+  N.first = Bget<int>(c, B_N_FIRST);
+  N.count = Bget<int>(c, B_N_COUNT);
+  N.ijk = Bget<int4>(c, B_N_IJK);
+  N.parent = Bget<int>(c, B_N_PARENT);
+  N.child = Bget<int>(c, B_N_CHILD);
+  N.hmaxb = Bget<float>(c, B_N_HMAXB);
+  N.split = Bget<int>(c, B_N_SPLIT);
+  N.slot = Bget<int>(c, B_N_SLOT);
+  N.kept = Bget<int>(c, B_N_KEPT);
+  N.dirmask = Bget<int>(c, B_N_DIRMASK);
+  N.sortoff = Bget<int64_t>(c, B_N_SORTOFF);
+  N.hmaxf = Bget<float>(c, B_N_HMAXF);
+  return N;
+}
+
+static void ensure_nodes(sph_ctx* c, int64_t cap) {
+  B<int>(c, B_N_FIRST, cap, true);
+  B<int>(c, B_N_COUNT, cap, true);
+  B<int4>(c, B_N_IJK, cap, true);
+  B<int>(c, B_N_PARENT, cap, true);
+  B<int>(c, B_N_CHILD, 8 * cap, true);
+  B<float>(c, B_N_HMAXB, cap, true);
+  B<int>(c, B_N_SPLIT, cap, true);
+}
+
+static LevelGeom level_geom(sph_ctx* c) {
+  LevelGeom g;
+  memset(&g, 0, sizeof(g));
+  for (int l = 0; l <= SPH_MAX_DEPTH + 1; ++l) {
+    float hm = 1e30f;
+    for (int k = 0; k < 3; ++k) {
+      g.E[l][k] = (float)(c->E0[k] / (double)(1 << l));
+      g.n[l][k] = c->ntop[k] << std::min(l, 20);
+      hm = std::min(hm, (float)(0.5 * c->E0[k] / (double)(1 << l)));
+    }
+    g.half_min[l] = hm;
+  }
+  for (int k = 0; k < 3; ++k) g.L[k] = (float)c->cfg.box[k];
+  g.depth = c->depth;
+  return g;
+}
+
+static float as_float(unsigned long long b) {
+  uint32_t u = (uint32_t)b;
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+}
+
+// =========================================================== build ==============
+// Builds the structure for the caller-order state in B_XIN (positions) and B_HB_ORIG
+// (h_build), carrying B_HCUR_O / B_LO_O / B_HI_O into cell order. count_only: the
+// occupancy-only hierarchy used for the initial guess (no slots, no sorts).
+static void build_structure(sph_ctx* c, bool count_only) {
+  const int64_t n = c->n;
+  const float* x = Bget<float>(c, B_XIN);
+  float* hb_o = Bget<float>(c, B_HB_ORIG);
+  double L[3] = {c->cfg.box[0], c->cfg.box[1], c->cfg.box[2]};
+  double Lmin = std::min(L[0], std::min(L[1], L[2]));
+  const double V = L[0] * L[1] * L[2];
+  double hmax, hmin;
+  if (count_only) {
+    // top edge from the mean density; depth as deep as the key allows
+    hmax = cbrt(3.0 * c->cfg.n_ngb * V / (4.0 * M_PI * (double)n));
+    hmin = hmax / 1024.0;
+  } else {
+    ctr_reset(c);
+    LAUNCH(k_hrange, grid1d(c, n, 256), 256, 0, hb_o, n, ctr(c));
+    unsigned long long h[C_NCOUNTERS];
+    ctr_read(c, h);
+    SPH_REQUIRE(!(h[C_ERR] & ERRBIT_H), SPH_E_DOMAIN, "smoothing length negative or non-finite");
+    SPH_REQUIRE(h[C_HMAXBITS] != 0, SPH_E_DOMAIN, "all smoothing lengths are zero");
+    hmax = as_float(h[C_HMAXBITS]);
+    hmin = as_float(h[C_HMINBITS]);
+  }
+  int64_t ntot = 1;
+  for (int k = 0; k < 3; ++k) {
+    double nk = floor(L[k] / (c->cfg.top_edge_factor * hmax * (1.0 + 1e-6)));
+    if (count_only) nk = std::max(nk, 3.0);
+    SPH_REQUIRE(nk >= 3.0, SPH_E_DOMAIN,
+                "smoothing length >= L/3: fewer than 3 top cells per axis (h_build max = " +
+                    std::to_string(hmax) + ")");
+    nk = std::min(nk, 512.0);
+    c->ntop[k] = (int)nk;
+    c->E0[k] = L[k] / nk;
+    ntot *= (int64_t)nk;
+  }
+  int top_bits = 0;
+  while ((1ll << top_bits) < ntot) ++top_bits;
+  double emin = std::min(c->E0[0], std::min(c->E0[1], c->E0[2]));
+  int depth = count_only ? SPH_MAX_DEPTH : (int)floor(log2(emin / (2.0 * hmin))) + 1;
+  depth = std::max(0, std::min(depth, SPH_MAX_DEPTH));
+  while (top_bits + 3 * depth > 63) --depth;
+  c->depth = depth;
+  c->top_bits = top_bits;
+  const int kbits = top_bits + 3 * depth;
+
+  // ---- a2 keys + radix sort
+  uint64_t* k0 = B<uint64_t>(c, B_KEYS0, n);
+  uint64_t* k1 = B<uint64_t>(c, B_KEYS1, n);
+  uint32_t* v0 = B<uint32_t>(c, B_VALS0, n);
+  uint32_t* v1 = B<uint32_t>(c, B_VALS1, n);
+  const double sc[3] = {(double)((int64_t)c->ntop[0] << depth) / L[0], (double)((int64_t)c->ntop[1] << depth) / L[1],
+                        (double)((int64_t)c->ntop[2] << depth) / L[2]};
+  LAUNCH(k_keys, grid1d(c, n, 256), 256, 0, x, n, c->ntop[0], c->ntop[1], c->ntop[2], depth, sc[0], sc[1], sc[2],
+         k0, v0);
+  radix_sort(c, k0, v0, k1, v1, n, kbits);
+  uint64_t* keys = k0;
+  uint32_t* perm = B<uint32_t>(c, B_PERM, n);
+  CUDA_TRY(cudaMemcpyAsync(perm, v0, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, c->stream));
+
+  // ---- a3 cell-order pack
+  float4* xh = B<float4>(c, B_XH, n);
+  float* hb = B<float>(c, B_HB, n);
+  float* lo = B<float>(c, B_HLO, n);
+  float* hi = B<float>(c, B_HHI, n);
+  LAUNCH(k_gather_build, grid1d(c, n, 256), 256, 0, perm, n, x, Bget<float>(c, B_HCUR_O), hb_o,
+         Bget<float>(c, B_LO_O), Bget<float>(c, B_HI_O), xh, hb, lo, hi);
+
+  // ---- a4 hierarchy: level 0 = runs of the top-cell index
+  int* flag = B<int>(c, B_TMPI0, n);
+  int* idx = B<int>(c, B_TMPI1, n);
+  const int sh = 3 * depth;
+  LAUNCH(k_mark_top, grid1d(c, n, 256), 256, 0, keys, n, sh, flag);
+  int n0 = scan_excl<int>(c, flag, idx, n);
+  ensure_nodes(c, std::max<int64_t>(2 * (int64_t)n0 + 1024, n / 16));
+  int* topmap = B<int>(c, B_TOPMAP, ntot);
+  CUDA_TRY(cudaMemsetAsync(topmap, 0xff, ntot * sizeof(int), c->stream));
+  NodeArrays N = nodes(c);
+  LAUNCH(k_write_top, grid1d(c, n, 256), 256, 0, keys, n, sh, flag, idx, c->ntop[0], c->ntop[1], N, topmap);
+  LAUNCH(k_top_counts, gridfull(n0, 256), 256, 0, n0, n, N);
+  c->lev_off.assign({0, n0});
+  LevelGeom g = level_geom(c);
+  const int split_count = count_only ? 32 : c->cfg.split_count;
+  for (int l = 0;; ++l) {
+    const int a = c->lev_off[l], b = c->lev_off[l + 1];
+    const int nl = b - a;
+    int* nch = B<int>(c, B_N_NCH, nl);
+    int* chscan = B<int>(c, B_N_CHBASE, nl);
+    N = nodes(c);
+    LAUNCH(k_level_split, gridfull((int64_t)nl * 32, 256), 256, 0, a, b, l, depth, hb, keys, g.half_min[l],
+           split_count, c->cfg.split_fraction, count_only ? 1 : 0, N, nch, N.child);
+    int nnext = scan_excl<int>(c, nch, chscan, nl);
+    ensure_nodes(c, (int64_t)b + nnext + 1);
+    N = nodes(c);
+    LAUNCH(k_make_children, gridfull(nl, 256), 256, 0, a, b, (int64_t)b, nch, chscan, N);
+    if (nnext == 0) break;
+    c->lev_off.push_back(b + nnext);
+  }
+  c->n_nodes = c->lev_off.back();
+  const int nnodes = c->n_nodes;
+  const int nlev = (int)c->lev_off.size() - 1;
+  if (count_only) return;
+
+  // ---- a5 interaction slots (27 per node; 13 = self) and kept pairs
+  int* slot = B<int>(c, B_N_SLOT, 27 * (int64_t)nnodes);
+  B<int>(c, B_N_KEPT, nnodes);
+  B<int>(c, B_N_DIRMASK, nnodes);
+  B<int64_t>(c, B_N_SORTOFF, nnodes);
+  B<float>(c, B_N_HMAXF, nnodes);
+  (void)slot;
+  N = nodes(c);
+  LAUNCH(k_top_slots, gridfull(n0, 128), 128, 0, n0, c->ntop[0], c->ntop[1], c->ntop[2], topmap, N);
+  for (int l = 1; l < nlev; ++l) {
+    const int a = c->lev_off[l], b = c->lev_off[l + 1];
+    LAUNCH(k_child_slots, gridfull(b - a, 128), 128, 0, a, b, g.half_min[l - 1], N);
+  }
+  int64_t* nsort = B<int64_t>(c, B_N_NSORT, nnodes);
+  for (int l = 0; l < nlev; ++l) {
+    const int a = c->lev_off[l], b = c->lev_off[l + 1];
+    LAUNCH(k_kept, gridfull(b - a, 128), 128, 0, a, b, g.half_min[l], N, nsort);
+  }
+  c->n_sorted = scan_excl<int64_t>(c, nsort, N.sortoff, nnodes);
+
+  // ---- a6 13-direction sorted lists
+  SortEntry* sorted = B<SortEntry>(c, B_SORTED, c->n_sorted);
+  LAUNCH(k_sort_warp, gridfull((int64_t)nnodes * 32, 256), 256, 0, nnodes, xh, N, g, sorted);
+  {
+    static bool attr = false;
+    const int smem = SORT_BLOCK_MAX * (8 + 4);
+    if (!attr) {
+      CUDA_TRY(cudaFuncSetAttribute(k_sort_block, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr = true;
+    }
+    LAUNCH(k_sort_block, nnodes, 512, smem, nnodes, xh, N, g, sorted);
+  }
+  {
+    int* bflag = B<int>(c, B_TASKFLAG, nnodes);
+    int* bidx = B<int>(c, B_TASKIDX, nnodes);
+    int64_t* bsz = B<int64_t>(c, B_TMPL0, nnodes);
+    LAUNCH(k_mark_big, gridfull(nnodes, 256), 256, 0, nnodes, N, bflag, bsz);
+    int nbig = scan_excl<int>(c, bflag, bidx, nnodes);
+    if (nbig > 0) {
+      int64_t* bscan = B<int64_t>(c, B_TMPL1, nnodes);
+      int64_t nent = scan_excl<int64_t>(c, bsz, bscan, nnodes);
+      int* bignodes = B<int>(c, B_BIGNODES, nbig);
+      int64_t* bigoff = B<int64_t>(c, B_BIGOFF, nbig);
+      LAUNCH(k_compact_big, gridfull(nnodes, 256), 256, 0, nnodes, bflag, bidx, bscan, bignodes, bigoff);
+      uint64_t* bk0 = B<uint64_t>(c, B_KEYS0, nent);
+      uint64_t* bk1 = B<uint64_t>(c, B_KEYS1, nent);
+      uint32_t* bv0 = B<uint32_t>(c, B_VALS0, nent);
+      uint32_t* bv1 = B<uint32_t>(c, B_VALS1, nent);
+      N = nodes(c);
+      LAUNCH(k_big_keys, nbig, 512, 0, nbig, bignodes, bigoff, xh, N, g, bk0, bv0);
+      int segbits = 0;
+      while ((1ll << segbits) < (int64_t)nbig * 13) ++segbits;
+      radix_sort(c, bk0, bv0, bk1, bv1, nent, 32 + segbits);
+      LAUNCH(k_big_write, nbig, 512, 0, nbig, bignodes, bigoff, N, bk0, bv0, sorted);
+    }
+  }
+
+  // ---- leaf tasks: (leaf, chunk of 32 particles)
+  int* nchunk = B<int>(c, B_TASKFLAG, nnodes);
+  int* cscan = B<int>(c, B_TASKIDX, nnodes);
+  LAUNCH(k_leaf_chunks, gridfull(nnodes, 256), 256, 0, nnodes, N, nchunk);
+  int ntasks = scan_excl<int>(c, nchunk, cscan, nnodes);
+  int2* tasks = B<int2>(c, B_TASKS, ntasks);
+  LAUNCH(k_write_tasks, gridfull(nnodes, 256), 256, 0, nnodes, nchunk, cscan, tasks);
+  c->n_leaves = ntasks;  // number of (leaf, chunk) tasks; see stats
+  sync(c);
+}
+
+// =========================================================== inputs =============
+static bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// device view of a caller input array: the pointer itself, or a staged copy
+template <class T>
+static const T* dev_in(sph_ctx* c, const T* p, size_t count, int stage_id, bool force_copy = false) {
+  if (is_device_ptr(p) && !force_copy) return p;
+  T* d = B<T>(c, stage_id, count);
+  CUDA_TRY(cudaMemcpyAsync(d, p, count * sizeof(T), cudaMemcpyDefault, c->stream));
+  return d;
+}
+
+struct OutMap {
+  void* user;
+  void* dev;
+  size_t bytes;
+};
+template <class T>
+static T* dev_out(sph_ctx* c, T* p, size_t count, int stage_id, std::vector<OutMap>& maps) {
+  if (!p) return nullptr;
+  if (is_device_ptr(p)) return p;
+  T* d = B<T>(c, stage_id, count);
+  maps.push_back(OutMap{p, d, count * sizeof(T)});
+  return d;
+}
+static void flush_out(sph_ctx* c, std::vector<OutMap>& maps) {
+  for (auto& m : maps)
+    CUDA_TRY(cudaMemcpyAsync(m.user, m.dev, m.bytes, cudaMemcpyDeviceToHost, c->stream));
+  if (!maps.empty()) sync(c);
+}
+
+static TravParams trav(sph_ctx* c, const int2* tasks, int ntasks, const uint8_t* active) {
+  TravParams P;
+  P.tasks = tasks;
+  P.ntasks = ntasks;
+  P.N = nodes(c);
+  P.g = level_geom(c);
+  P.sorted = Bget<SortEntry>(c, B_SORTED);
+  P.active = active;
+  float Lmax = (float)std::max(c->cfg.box[0], std::max(c->cfg.box[1], c->cfg.box[2]));
+  P.slack = 4e-7f * Lmax;
+  P.ctr = ctr(c);
+  return P;
+}
+
+// =========================================================== API ================
+#define API_BEGIN(ctx)                                                              \
+  if (!(ctx)) return SPH_E_ARG;                                                     \
+  sph_ctx* c = (ctx);                                                               \
+  c->err.clear();                                                                   \
+  try {                                                                             \
+    CUDA_TRY(cudaSetDevice(c->device));
+#define API_END                                                                     \
+  }                                                                                 \
+  catch (const SphError& e) {                                                       \
+    c->err = e.msg;                                                                 \
+    if (e.status == SPH_E_CUDA) cudaGetLastError();                                 \
+    return e.status;                                                                \
+  }                                                                                 \
+  catch (const std::exception& e) {                                                 \
+    c->err = e.what();                                                              \
+    return SPH_E_CUDA;                                                              \
+  }
+
+extern "C" {
+
+void sph_config_default(sph_config* cfg, double lx, double ly, double lz) {
+  memset(cfg, 0, sizeof(*cfg));
+  cfg->abi_version = SPH_ABI_VERSION;
+  cfg->box[0] = lx;
+  cfg->box[1] = ly;
+  cfg->box[2] = lz;
+  cfg->gamma = 5.0f / 3.0f;
+  cfg->n_ngb = 48.0f;
+  cfg->n_ngb_tol = 1e-4f;
+  cfg->max_h_iter = 64;
+  cfg->alpha = 0.8f;
+  cfg->balsara_eps = 1e-4f;
+  cfg->split_count = 300;
+  cfg->split_fraction = 0.875f;
+  cfg->top_edge_factor = 1.0f;
+  cfg->h_margin = 1.1f;
+  cfg->flags = SPH_F_SYNC;
+  cfg->rank = 0;
+  cfg->nranks = 1;
+  cfg->slab_lo = 0.0;
+  cfg->slab_hi = lx;
+}
+
+const char* sph_status_string(int s) {
+  switch (s) {
+    case SPH_OK: return "SPH_OK";
+    case SPH_E_ARG: return "SPH_E_ARG: invalid argument or configuration";
+    case SPH_E_DOMAIN: return "SPH_E_DOMAIN: input outside the method's domain";
+    case SPH_E_STATE: return "SPH_E_STATE: calls out of order";
+    case SPH_E_NOCONV: return "SPH_E_NOCONV: h iteration did not converge";
+    case SPH_E_CUDA: return "SPH_E_CUDA: CUDA error";
+    case SPH_E_NCCL: return "SPH_E_NCCL: NCCL error";
+    case SPH_E_OOM: return "SPH_E_OOM: out of device memory";
+    default: return "unknown sph_status";
+  }
+}
+
+const char* sph_last_error(const sph_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int64_t sph_kernel_launches(const sph_ctx* c) { return c ? c->launches : 0; }
+
+static bool cfg_ok(const sph_config* f, std::string& why) {
+  if (f->abi_version != SPH_ABI_VERSION) { why = "abi_version mismatch"; return false; }
+  for (int k = 0; k < 3; ++k)
+    if (!(f->box[k] > 0.0)) { why = "box <= 0"; return false; }
+  if (!(f->gamma > 1.f)) { why = "gamma <= 1"; return false; }
+  if (!(f->alpha >= 0.f)) { why = "alpha < 0"; return false; }
+  if (!(f->n_ngb > 32.f / 3.f)) { why = "n_ngb <= 32/3 (the self term alone)"; return false; }
+  if (!(f->n_ngb_tol > 0.f)) { why = "n_ngb_tol <= 0"; return false; }
+  if (!(f->top_edge_factor >= 1.f)) { why = "top_edge_factor < 1"; return false; }
+  if (!(f->h_margin >= 1.f)) { why = "h_margin < 1"; return false; }
+  if (!(f->split_fraction > 0.f && f->split_fraction <= 1.f)) { why = "split_fraction outside (0,1]"; return false; }
+  if (f->split_count < 1) { why = "split_count < 1"; return false; }
+  if (f->max_h_iter < 1) { why = "max_h_iter < 1"; return false; }
+  if (f->nranks < 1 || f->rank < 0 || f->rank >= f->nranks) { why = "bad rank/nranks"; return false; }
+  return true;
+}
+
+int sph_create(const sph_config* cfg, int dev, void* stream, sph_ctx** out) {
+  if (!out) return SPH_E_ARG;
+  *out = nullptr;
+  if (!cfg) return SPH_E_ARG;
+  std::string why;
+  if (!cfg_ok(cfg, why)) return SPH_E_ARG;
+  sph_ctx* c = new sph_ctx();
+  c->cfg = *cfg;
+  c->device = dev;
+  try {
+    CUDA_TRY(cudaSetDevice(dev));
+    int ns = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&ns, cudaDevAttrMultiProcessorCount, dev));
+    c->num_sms = ns;
+    if (stream) {
+      c->stream = (cudaStream_t)stream;
+    } else {
+      CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+    for (int i = 0; i < 8; ++i) CUDA_TRY(cudaEventCreate(&c->ev[i]));
+    c->ev_ok = true;
+  } catch (const SphError& e) {
+    delete c;
+    return e.status;
+  }
+  *out = c;
+  return SPH_OK;
+}
+
+int sph_destroy(sph_ctx* c) {
+  if (!c) return SPH_E_ARG;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (int i = 0; i < 64; ++i) dev_free(c, c->b[i].p);
+  if (c->ev_ok)
+    for (int i = 0; i < 8; ++i) cudaEventDestroy(c->ev[i]);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return SPH_OK;
+}
+
+int sph_set_allocator(sph_ctx* c, void* (*alloc)(size_t, void*, void*), void (*release)(void*, void*, void*),
+                      void* user) {
+  if (!c) return SPH_E_ARG;
+  if ((alloc == nullptr) != (release == nullptr)) return SPH_E_ARG;
+  for (int i = 0; i < 64; ++i)
+    if (c->b[i].p) return SPH_E_STATE;
+  c->ualloc = alloc;
+  c->urelease = release;
+  c->uuser = user;
+  return SPH_OK;
+}
+
+int sph_build_cells(sph_ctx* ctx, int64_t n, const float* x, const float* h0) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(n > 0 && x, SPH_E_ARG, "n <= 0 or x == NULL");
+  SPH_REQUIRE(n < (1ll << 30), SPH_E_ARG, "n >= 2^30");
+  c->n = n;
+  c->state = 0;
+  c->rebuilds = 0;
+  CUDA_TRY(cudaEventRecord(c->ev[0], c->stream));
+  float* xd = B<float>(c, B_XIN, 3 * n);
+  CUDA_TRY(cudaMemcpyAsync(xd, x, 3 * n * sizeof(float), cudaMemcpyDefault, c->stream));
+  ctr_reset(c);
+  LAUNCH(k_validate_x, grid1d(c, n, 256), 256, 0, xd, n, (float)c->cfg.box[0], (float)c->cfg.box[1],
+         (float)c->cfg.box[2], ctr(c));
+  float* hin = B<float>(c, B_HIN, n);
+  if (h0) {
+    CUDA_TRY(cudaMemcpyAsync(hin, h0, n * sizeof(float), cudaMemcpyDefault, c->stream));
+    LAUNCH(k_hrange, grid1d(c, n, 256), 256, 0, hin, n, ctr(c));
+    LAUNCH(k_count_zero, grid1d(c, n, 256), 256, 0, hin, n, ctr(c));
+  } else {
+    CUDA_TRY(cudaMemsetAsync(hin, 0, n * sizeof(float), c->stream));
+  }
+  unsigned long long hc[C_NCOUNTERS];
+  ctr_read(c, hc);
+  SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_NONFINITE), SPH_E_DOMAIN, "non-finite position");
+  SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_XRANGE), SPH_E_DOMAIN, "position outside [0, L)");
+  SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_H), SPH_E_DOMAIN, "h0 negative or non-finite");
+  const bool need_guess = !h0 || hc[C_TMP0] > 0;
+  float* hcur = B<float>(c, B_HCUR_O, n);
+  float* hb = B<float>(c, B_HB_ORIG, n);
+  float* lo = B<float>(c, B_LO_O, n);
+  float* hi = B<float>(c, B_HI_O, n);
+  if (need_guess) {
+    // occupancy-only hierarchy -> h from the particle number density of the leaf (or
+    // of its first ancestor holding >= n_ngb particles)
+    LAUNCH(k_fill_f, grid1d(c, n, 256), 256, 0, hb, n, 1.0f);
+    LAUNCH(k_fill_f, grid1d(c, n, 256), 256, 0, hcur, n, 1.0f);
+    LAUNCH(k_fill_f, grid1d(c, n, 256), 256, 0, lo, n, 0.0f);
+    LAUNCH(k_fill_f, grid1d(c, n, 256), 256, 0, hi, n, 0.0f);
+    build_structure(c, true);
+    LevelGeom g = level_geom(c);
+    double Lmin = std::min(c->cfg.box[0], std::min(c->cfg.box[1], c->cfg.box[2]));
+    LAUNCH(k_guess_h, gridfull(c->n_nodes, 128), 128, 0, c->n_nodes, nodes(c), g, Bget<uint32_t>(c, B_PERM),
+           c->cfg.n_ngb, (int)c->cfg.n_ngb, (float)(0.25 * Lmin), hcur);
+    if (h0) LAUNCH(k_merge_guess, grid1d(c, n, 256), 256, 0, hin, n, hcur);
+    LAUNCH(k_init_h, grid1d(c, n, 256), 256, 0, hcur, n, c->cfg.h_margin, hcur, hb, lo, hi);
+  } else {
+    LAUNCH(k_init_h, grid1d(c, n, 256), 256, 0, hin, n, c->cfg.h_margin, hcur, hb, lo, hi);
+  }
+  build_structure(c, false);
+  c->state = 1;
+  CUDA_TRY(cudaEventRecord(c->ev[1], c->stream));
+  if (c->cfg.flags & SPH_F_SYNC) sync(c);
+  API_END
+  return SPH_OK;
+}
+
+static void fill_struct_stats(sph_ctx* c, sph_stats* st) {
+  st->n_levels = (int)c->lev_off.size() - 1;
+  st->n_cells = c->n_nodes;
+  st->n_leaves = c->n_leaves;
+  st->n_rebuilds = c->rebuilds;
+}
+
+int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, float* h_out, float* rho_out,
+                float* omega_out, int32_t* n_nbr_out, float* div_out, float* curl_out, sph_stats* st) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(c->state >= 1, SPH_E_STATE, "sph_density before sph_build_cells");
+  SPH_REQUIRE(v && m && u && h_out && rho_out, SPH_E_ARG, "required pointer is NULL");
+  const int64_t n = c->n;
+  CUDA_TRY(cudaEventRecord(c->ev[2], c->stream));
+  const float* vd = dev_in(c, v, 3 * n, B_VIN);
+  const float* md = dev_in(c, m, n, B_MIN);
+  const float* ud = dev_in(c, u, n, B_UIN);
+  ctr_reset(c);
+  LAUNCH(k_validate_vmu, grid1d(c, n, 256), 256, 0, vd, md, ud, n, ctr(c));
+  unsigned long long hc[C_NCOUNTERS];
+  ctr_read(c, hc);
+  SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_NONFINITE), SPH_E_DOMAIN, "non-finite velocity");
+  SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_MASS), SPH_E_DOMAIN, "mass <= 0 or non-finite");
+  SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_U), SPH_E_DOMAIN, "internal energy <= 0 or non-finite");
+  // staged copies must survive rebuilds (the gather reads them again)
+  if (!is_device_ptr(v) || !is_device_ptr(m) || !is_device_ptr(u)) sync(c);
+
+  float4* vm = B<float4>(c, B_VM, n);
+  float* uc = B<float>(c, B_U, n);
+  uint8_t* active = B<uint8_t>(c, B_FLAG, n);
+  double* sf = B<double>(c, B_DSUMF, n);
+  float4* acc0 = B<float4>(c, B_DACC0, n);
+  float4* acc1 = B<float4>(c, B_DACC1, n);
+  LAUNCH(k_gather_vmu, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, vd, md, ud, vm, uc);
+  LAUNCH(k_fill_u8, grid1d(c, n, 256), 256, 0, active, n, (uint8_t)1);
+
+  int iters = 0;
+  long long unconv = n;
+  bool all_tasks = true;
+  long long cand_last = 0;
+  while (true) {
+    // tasks of this pass: all, or those with an unconverged particle
+    const int ntasks_all = c->n_leaves;
+    const int2* tasks = Bget<int2>(c, B_TASKS);
+    int ntasks = ntasks_all;
+    if (!all_tasks) {
+      int* tf = B<int>(c, B_TASKFLAG, ntasks_all);
+      int* ti = B<int>(c, B_TASKIDX, ntasks_all);
+      LAUNCH(k_task_active, gridfull((int64_t)ntasks_all * 32, 256), 256, 0, tasks, ntasks_all, nodes(c), active, tf);
+      ntasks = scan_excl<int>(c, tf, ti, ntasks_all);
+      int2* t2 = B<int2>(c, B_TASKS2, std::max(ntasks, 1));
+      LAUNCH(k_task_compact, gridfull(ntasks_all, 256), 256, 0, Bget<int2>(c, B_TASKS), ntasks_all, tf, ti, t2);
+      tasks = t2;
+    }
+    ctr_reset(c);
+    if (ntasks > 0) {
+      TravParams P = trav(c, tasks, ntasks, active);
+      LAUNCH(k_density, gridfull(ntasks, INTERACT_WARPS), INTERACT_WARPS * 32, 0, P, Bget<float4>(c, B_XH), vm,
+             DensOut{sf, acc0, acc1});
+    }
+    ++iters;
+    const bool last = iters >= c->cfg.max_h_iter;
+    if (last) {
+      ctr_read(c, hc);
+      cand_last = (long long)hc[C_CAND];
+      break;  // sums are at the current h; unconverged particles are reported
+    }
+    LAUNCH(k_h_update, grid1d(c, n, 256), 256, 0, n, Bget<float4>(c, B_XH), Bget<float>(c, B_HB),
+           Bget<float>(c, B_HLO), Bget<float>(c, B_HHI), active, sf, acc0, c->cfg.n_ngb, c->cfg.n_ngb_tol, ctr(c));
+    ctr_read(c, hc);
+    cand_last = (long long)hc[C_CAND];
+    unconv = (long long)hc[C_UNCONV];
+    if (unconv == 0) break;
+    all_tasks = false;
+    if (hc[C_REBUILD] > 0) {
+      // an h wants to outgrow the cells it was binned for: re-bin everything for
+      // h_build = h * margin, keeping h and its bracket
+      LAUNCH(k_scatter_state, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, Bget<float4>(c, B_XH),
+             Bget<float>(c, B_HLO), Bget<float>(c, B_HHI), c->cfg.h_margin, Bget<float>(c, B_HCUR_O),
+             Bget<float>(c, B_LO_O), Bget<float>(c, B_HI_O), Bget<float>(c, B_HB_ORIG));
+      build_structure(c, false);
+      c->rebuilds++;
+      vm = Bget<float4>(c, B_VM);
+      LAUNCH(k_gather_vmu, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, vd, md, ud, vm, uc);
+      LAUNCH(k_fill_u8, grid1d(c, n, 256), 256, 0, active, n, (uint8_t)1);
+      all_tasks = true;
+    }
+  }
+  // ghost: finalise and write the caller-order outputs
+  std::vector<OutMap> maps;
+  GhostOut go;
+  go.h = dev_out(c, h_out, n, B_OUT0, maps);
+  go.rho = dev_out(c, rho_out, n, B_OUT1, maps);
+  go.omega = dev_out(c, omega_out, n, B_OUT2, maps);
+  go.nnbr = dev_out(c, n_nbr_out, n, B_OUT3, maps);
+  go.div = dev_out(c, div_out, n, B_OUT4, maps);
+  go.curl = dev_out(c, curl_out, 3 * n, B_OUT5, maps);
+  go.perm = Bget<uint32_t>(c, B_PERM);
+  float4* fx = B<float4>(c, B_FX, n);
+  float4* fs = B<float4>(c, B_FS, n);
+  ctr_reset(c);
+  LAUNCH(k_ghost, grid1d(c, n, 256), 256, 0, n, Bget<float4>(c, B_XH), uc, sf, acc0, acc1, c->cfg.gamma,
+         c->cfg.balsara_eps, fx, fs, go, ctr(c));
+  LAUNCH(k_node_hmax, gridfull((int64_t)c->n_nodes * 32, 256), 256, 0, c->n_nodes, nodes(c), Bget<float4>(c, B_XH));
+  CUDA_TRY(cudaEventRecord(c->ev[3], c->stream));
+  flush_out(c, maps);
+  c->state = 2;
+  int status = (unconv > 0 && iters >= c->cfg.max_h_iter) ? SPH_E_NOCONV : SPH_OK;
+  if (st || (c->cfg.flags & SPH_F_SYNC)) {
+    ctr_read(c, hc);
+    if (st) {
+      memset(st, 0, sizeof(*st));
+      fill_struct_stats(c, st);
+      st->n_directed = (int64_t)hc[C_NDIR];
+      st->n_candidates = cand_last;
+      st->n_unconverged = status == SPH_E_NOCONV ? unconv : 0;
+      st->h_iters = iters;
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+      st->ms_build = ms;
+      cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]);
+      st->ms_density = ms;
+    }
+  }
+  if (status == SPH_E_NOCONV) {
+    c->err = "h iteration did not converge in max_h_iter passes: " + std::to_string(unconv) + " particles";
+    return status;
+  }
+  API_END
+  return SPH_OK;
+}
+
+int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out, int32_t* n_nbr_force_out,
+              sph_stats* st) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(c->state >= 2, SPH_E_STATE, "sph_force before sph_density");
+  SPH_REQUIRE(a_out && dudt_out, SPH_E_ARG, "required pointer is NULL");
+  const int64_t n = c->n;
+  CUDA_TRY(cudaEventRecord(c->ev[4], c->stream));
+  std::vector<OutMap> maps;
+  ForceOut fo;
+  fo.a = dev_out(c, a_out, 3 * n, B_OUT0, maps);
+  fo.dudt = dev_out(c, dudt_out, n, B_OUT1, maps);
+  fo.vsig = dev_out(c, vsig_out, n, B_OUT2, maps);
+  fo.nnbr = dev_out(c, n_nbr_force_out, n, B_OUT3, maps);
+  fo.perm = Bget<uint32_t>(c, B_PERM);
+  ctr_reset(c);
+  TravParams P = trav(c, Bget<int2>(c, B_TASKS), c->n_leaves, nullptr);
+  LAUNCH(k_force, gridfull(c->n_leaves, INTERACT_WARPS), INTERACT_WARPS * 32, 0, P, Bget<float4>(c, B_FX),
+         Bget<float4>(c, B_VM), Bget<float4>(c, B_FS), c->cfg.alpha, fo);
+  CUDA_TRY(cudaEventRecord(c->ev[5], c->stream));
+  flush_out(c, maps);
+  if (st || (c->cfg.flags & SPH_F_SYNC)) {
+    unsigned long long hc[C_NCOUNTERS];
+    ctr_read(c, hc);
+    if (st) {
+      memset(st, 0, sizeof(*st));
+      fill_struct_stats(c, st);
+      st->n_pairs = (int64_t)(hc[C_NFORCE] / 2);
+      st->n_candidates = (int64_t)hc[C_CAND];
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, c->ev[4], c->ev[5]);
+      st->ms_force = ms;
+    }
+  }
+  API_END
+  return SPH_OK;
+}
+
+}  // extern "C"

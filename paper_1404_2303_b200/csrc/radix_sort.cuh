@@ -1,0 +1,161 @@
+// radix_sort.cuh — hand-written LSD radix sort of (u64 key, u32 value) pairs for sm_100a.
+//
+// Onesweep structure: one histogram kernel computes every pass's digit counts in a
+// single read of the keys; each 8-bit pass is then ONE kernel: tiles of 4096 items
+// ranked in-warp with __match_any_sync (stable), tile digit counts published with a
+// decoupled look-back (per-digit status words), items staged in shared memory in
+// digit order and written out in coalesced digit runs. Passes whose digit is constant
+// over all keys are skipped (known from the histogram).
+#pragma once
+#include "common.cuh"
+
+#define RS_THREADS 256
+#define RS_ITEMS 16
+#define RS_TILE (RS_THREADS * RS_ITEMS)
+#define RS_WARPS (RS_THREADS / 32)
+#define RS_FLAG_INC 0x80000000u
+#define RS_FLAG_AGG 0x40000000u
+#define RS_VAL_MASK 0x3fffffffu
+
+__global__ void __launch_bounds__(256) k_radix_hist(const uint64_t* __restrict__ keys, int64_t n,
+                                                     int npass, uint32_t* __restrict__ hist) {
+  __shared__ uint32_t sh[8][256];
+  for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k = keys[i];
+    for (int p = 0; p < npass; ++p) atomicAdd(&sh[p][(k >> (8 * p)) & 255u], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < npass * 256; i += blockDim.x) {
+    uint32_t c = (&sh[0][0])[i];
+    if (c) atomicAdd(&hist[i], c);
+  }
+}
+
+__device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+struct RadixSmem {
+  uint32_t wcnt[RS_WARPS][256];
+  uint32_t dpre[256];
+  uint32_t gbase[256];
+  uint32_t tile;
+  uint32_t wsum[RS_WARPS];
+  uint64_t keys[RS_TILE];
+  uint32_t vals[RS_TILE];
+};
+
+__global__ void __launch_bounds__(RS_THREADS) k_radix_pass(
+    const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint64_t* __restrict__ kout,
+    uint32_t* __restrict__ vout, int64_t n, int shift, const uint32_t* __restrict__ gofs,
+    uint32_t* status, uint32_t* tile_ctr) {
+  extern __shared__ __align__(16) unsigned char rs_raw[];
+  RadixSmem& S = *reinterpret_cast<RadixSmem*>(rs_raw);
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < RS_WARPS * 256; i += RS_THREADS) (&S.wcnt[0][0])[i] = 0;
+  if (tid == 0) S.tile = atomicAdd(tile_ctr, 1u);
+  __syncthreads();
+  const uint32_t tile = S.tile;
+  const int64_t base = (int64_t)tile * RS_TILE;
+  const int tile_n = (int)min((int64_t)RS_TILE, n - base);
+
+  uint64_t k[RS_ITEMS];
+  uint32_t v[RS_ITEMS];
+  uint32_t rank[RS_ITEMS];
+  uint32_t dg[RS_ITEMS];
+#pragma unroll
+  for (int it = 0; it < RS_ITEMS; ++it) {
+    int li = w * (RS_ITEMS * 32) + it * 32 + lane;
+    if (li < tile_n) {
+      k[it] = kin[base + li];
+      v[it] = vin[base + li];
+      dg[it] = (uint32_t)(k[it] >> shift) & 255u;
+    } else {
+      k[it] = 0;
+      v[it] = 0;
+      dg[it] = 256u;
+    }
+  }
+  // stable in-warp ranking: items visited in position order (it major, lane minor)
+#pragma unroll
+  for (int it = 0; it < RS_ITEMS; ++it) {
+    uint32_t d = dg[it];
+    unsigned peers = __match_any_sync(FULL_MASK, d);
+    uint32_t cnt_before = 0;
+    if (d < 256u) cnt_before = S.wcnt[w][d];
+    __syncwarp();
+    rank[it] = cnt_before + __popc(peers & lanemask_lt());
+    if (d < 256u && lane == __ffs(peers) - 1) S.wcnt[w][d] = cnt_before + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // per digit: exclusive over warps, tile total
+  uint32_t tcnt = 0;
+  {
+    const int d = tid;  // RS_THREADS == 256
+    uint32_t run = 0;
+#pragma unroll
+    for (int ww = 0; ww < RS_WARPS; ++ww) {
+      uint32_t c = S.wcnt[ww][d];
+      S.wcnt[ww][d] = run;
+      run += c;
+    }
+    tcnt = run;
+    // decoupled look-back over previous tiles for digit d
+    uint32_t* st = status + (size_t)tile * 256 + d;
+    if (tile == 0) {
+      atomicExch(st, RS_FLAG_INC | tcnt);
+      S.gbase[d] = gofs[d];
+    } else {
+      atomicExch(st, RS_FLAG_AGG | tcnt);
+      uint32_t excl = 0;
+      int64_t pt = (int64_t)tile - 1;
+      while (pt >= 0) {
+        uint32_t s;
+        do {
+          s = ld_volatile_u32(status + (size_t)pt * 256 + d);
+        } while ((s & (RS_FLAG_INC | RS_FLAG_AGG)) == 0);
+        excl += s & RS_VAL_MASK;
+        if (s & RS_FLAG_INC) break;
+        --pt;
+      }
+      atomicExch(st, RS_FLAG_INC | (excl + tcnt));
+      S.gbase[d] = gofs[d] + excl;
+    }
+    // tile-local exclusive prefix over digits (block scan of tcnt)
+    uint32_t x = tcnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(FULL_MASK, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) S.wsum[w] = x;
+    __syncthreads();
+    uint32_t add = 0;
+    for (int ww = 0; ww < w; ++ww) add += S.wsum[ww];
+    S.dpre[d] = x - tcnt + add;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < RS_ITEMS; ++it) {
+    uint32_t d = dg[it];
+    if (d < 256u) {
+      uint32_t pos = S.dpre[d] + S.wcnt[w][d] + rank[it];
+      S.keys[pos] = k[it];
+      S.vals[pos] = v[it];
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < tile_n; i += RS_THREADS) {
+    uint64_t kk = S.keys[i];
+    uint32_t d = (uint32_t)(kk >> shift) & 255u;
+    uint32_t g = S.gbase[d] + (uint32_t)i - S.dpre[d];
+    kout[g] = kk;
+    vout[g] = S.vals[i];
+  }
+}

@@ -1,0 +1,218 @@
+"""Thin ctypes binding over libsph (include/sph.h): argument marshalling only.
+
+Every step of the path runs in libsph's CUDA kernels; this module never computes
+SPH quantities and has no CPU fallback: if libsph.so is missing or no CUDA device is
+present, the calls raise.
+
+Arrays may be torch tensors (CUDA or CPU; fp32 / int32, contiguous) or numpy arrays
+(host); their raw pointers are handed to the C ABI, which detects host vs device
+pointers itself.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import os
+
+import numpy as np
+
+from .build import LIB
+
+_lib = None
+
+
+class SphError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{msg} (status {status})")
+        self.status = status
+
+
+SPH_OK, SPH_E_ARG, SPH_E_DOMAIN, SPH_E_STATE, SPH_E_NOCONV, SPH_E_CUDA, SPH_E_NCCL, SPH_E_OOM = (
+    0, -1, -2, -3, -4, -5, -6, -7)
+SPH_F_SYNC = 1
+SPH_F_COUNT_CANDIDATES = 2
+ABI_VERSION = 1
+
+
+class Config(ctypes.Structure):
+    _fields_ = [
+        ("abi_version", ctypes.c_int32), ("box", ctypes.c_double * 3), ("gamma", ctypes.c_float),
+        ("n_ngb", ctypes.c_float), ("n_ngb_tol", ctypes.c_float), ("max_h_iter", ctypes.c_int32),
+        ("alpha", ctypes.c_float), ("balsara_eps", ctypes.c_float), ("split_count", ctypes.c_int32),
+        ("split_fraction", ctypes.c_float), ("top_edge_factor", ctypes.c_float),
+        ("h_margin", ctypes.c_float), ("flags", ctypes.c_uint32), ("rank", ctypes.c_int32),
+        ("nranks", ctypes.c_int32), ("slab_lo", ctypes.c_double), ("slab_hi", ctypes.c_double),
+    ]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [
+        ("n_pairs", ctypes.c_int64), ("n_directed", ctypes.c_int64), ("n_candidates", ctypes.c_int64),
+        ("n_unconverged", ctypes.c_int64), ("n_rebuilds", ctypes.c_int64), ("h_iters", ctypes.c_int32),
+        ("n_levels", ctypes.c_int32), ("n_cells", ctypes.c_int64), ("n_leaves", ctypes.c_int64),
+        ("n_pair_slots", ctypes.c_int64), ("ms_build", ctypes.c_double), ("ms_density", ctypes.c_double),
+        ("ms_force", ctypes.c_double), ("ms_halo", ctypes.c_double), ("halo_sent", ctypes.c_int64),
+        ("halo_recv", ctypes.c_int64),
+    ]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+#: every symbol include/sph.h declares (checked by tests/test_abi.py)
+EXPORTS = ("sph_config_default", "sph_create", "sph_destroy", "sph_set_allocator",
+           "sph_status_string", "sph_last_error", "sph_build_cells", "sph_density", "sph_force",
+           "sph_kernel_launches")
+
+
+def load(path: str | None = None):
+    """Load libsph.so (no compute: safe without a GPU)."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    path = path or os.environ.get("SPH_LIB", LIB)
+    if not os.path.exists(path):
+        raise FileNotFoundError(f"libsph.so not built ({path}); run `python -m paper_1404_2303_b200.build`")
+    lib = ctypes.CDLL(path)
+    P, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+    lib.sph_config_default.argtypes = [ctypes.POINTER(Config), ctypes.c_double, ctypes.c_double, ctypes.c_double]
+    lib.sph_config_default.restype = None
+    lib.sph_create.argtypes = [ctypes.POINTER(Config), i32, P, ctypes.POINTER(P)]
+    lib.sph_destroy.argtypes = [P]
+    lib.sph_set_allocator.argtypes = [P, P, P, P]
+    lib.sph_status_string.argtypes = [i32]
+    lib.sph_status_string.restype = ctypes.c_char_p
+    lib.sph_last_error.argtypes = [P]
+    lib.sph_last_error.restype = ctypes.c_char_p
+    lib.sph_build_cells.argtypes = [P, i64, P, P]
+    lib.sph_density.argtypes = [P, P, P, P, P, P, P, P, P, P, ctypes.POINTER(Stats)]
+    lib.sph_force.argtypes = [P, P, P, P, P, ctypes.POINTER(Stats)]
+    lib.sph_kernel_launches.argtypes = [P]
+    lib.sph_kernel_launches.restype = i64
+    if path == LIB or path is None:
+        _lib = lib
+    return lib
+
+
+def default_config(box=(1.0, 1.0, 1.0), **kw) -> Config:
+    cfg = Config()
+    load().sph_config_default(ctypes.byref(cfg), *map(float, box))
+    for k, v in kw.items():
+        if k == "box":
+            continue
+        if not hasattr(cfg, k):
+            raise KeyError(k)
+        setattr(cfg, k, v)
+    return cfg
+
+
+def _ptr(a, dtype=np.float32):
+    """Raw pointer of a torch tensor or numpy array (no copy; must be contiguous)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        if a.dtype != dtype or not a.flags.c_contiguous:
+            raise TypeError(f"expected a C-contiguous {np.dtype(dtype)} array")
+        return a.ctypes.data
+    import torch  # torch is plumbing only (device memory)
+    if isinstance(a, torch.Tensor):
+        want = {np.float32: torch.float32, np.int32: torch.int32}[dtype]
+        if a.dtype != want or not a.is_contiguous():
+            raise TypeError(f"expected a contiguous {want} tensor")
+        return a.data_ptr()
+    raise TypeError(f"unsupported array type {type(a)}")
+
+
+@dataclasses.dataclass
+class DensityResult:
+    h: object
+    rho: object
+    omega: object = None
+    n_nbr: object = None
+    div: object = None
+    curl: object = None
+    stats: dict = None
+
+
+@dataclasses.dataclass
+class ForceResult:
+    a: object
+    dudt: object
+    vsig: object = None
+    n_nbr_force: object = None
+    stats: dict = None
+
+
+class Context:
+    """One libsph context (one GPU, one stream)."""
+
+    def __init__(self, config: Config | None = None, device: int = 0, stream: int | None = None, **kw):
+        self.lib = load()
+        self.cfg = config if config is not None else default_config(**kw)
+        h = ctypes.c_void_p()
+        st = self.lib.sph_create(ctypes.byref(self.cfg), int(device), stream, ctypes.byref(h))
+        if st != SPH_OK:
+            raise SphError(st, self.lib.sph_status_string(st).decode())
+        self.h = h
+        self.n = 0
+
+    def _check(self, st):
+        if st != SPH_OK:
+            raise SphError(st, self.lib.sph_last_error(self.h).decode() or self.lib.sph_status_string(st).decode())
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.sph_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(self.lib.sph_kernel_launches(self.h))
+
+    # -- the three calls of include/sph.h ------------------------------------------
+    def build_cells(self, x, h0=None):
+        n = int(x.shape[0])
+        self._check(self.lib.sph_build_cells(self.h, n, _ptr(x), _ptr(h0)))
+        self.n = n
+
+    def density(self, v, m, u, out=None, stats: Stats | None = None, check=True):
+        """out: dict of preallocated output arrays (h, rho, omega, n_nbr, div, curl)."""
+        out = out if out is not None else self._alloc_like(v, dict(h=(), rho=(), omega=(), n_nbr=("i",),
+                                                                   div=(), curl=(3,)))
+        st = stats if stats is not None else Stats()
+        rc = self.lib.sph_density(self.h, _ptr(v), _ptr(m), _ptr(u), _ptr(out["h"]), _ptr(out["rho"]),
+                                  _ptr(out.get("omega")), _ptr(out.get("n_nbr"), np.int32),
+                                  _ptr(out.get("div")), _ptr(out.get("curl")), ctypes.byref(st))
+        if check:
+            self._check(rc)
+        return DensityResult(out["h"], out["rho"], out.get("omega"), out.get("n_nbr"), out.get("div"),
+                             out.get("curl"), st.as_dict())
+
+    def force(self, like, out=None, stats: Stats | None = None):
+        out = out if out is not None else self._alloc_like(like, dict(a=(3,), dudt=(), vsig=(),
+                                                                      n_nbr_force=("i",)))
+        st = stats if stats is not None else Stats()
+        self._check(self.lib.sph_force(self.h, _ptr(out["a"]), _ptr(out["dudt"]), _ptr(out.get("vsig")),
+                                       _ptr(out.get("n_nbr_force"), np.int32), ctypes.byref(st)))
+        return ForceResult(out["a"], out["dudt"], out.get("vsig"), out.get("n_nbr_force"), st.as_dict())
+
+    def _alloc_like(self, like, spec):
+        n = self.n
+        out = {}
+        for k, sh in spec.items():
+            is_int = "i" in sh
+            shape = (n,) + tuple(s for s in sh if s != "i")
+            if isinstance(like, np.ndarray):
+                out[k] = np.zeros(shape, dtype=np.int32 if is_int else np.float32)
+            else:
+                import torch
+                out[k] = torch.zeros(shape, dtype=torch.int32 if is_int else torch.float32, device=like.device)
+        return out
