@@ -1,0 +1,341 @@
+#!/usr/bin/env python
+"""bench.py — one JSON line for the driver.
+
+Step = one pass of the whole hot path on one batch of synthetic input:
+sph_build_cells (binning, radix sort, hierarchy, interaction slots, 13-direction
+lists) + sph_density (h iteration to N_ngb = 48, ghost) + sph_force, cold h0 as the
+config specifies. Metric = SPH pair interactions per second: 2F per step (F unordered
+pairs with r < max(h_i,h_j), once for density and once for force) over
+the whole step's device time.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl sph|reference] [--config C4]
+
+N > 1 runs under torch.distributed.run: one process per GPU, each an independent
+replica of the workload (the path does not exchange data between replicas: "replicas
+only"); the time is the max over ranks, value = all ranks' pairs / that time.
+--impl reference times the fp64 oracle (oracle/) on a bounded sample of the same
+workload on this host's CPU cores (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SPH pair interactions/s (density+force), whole step"
+UNIT = "pair-interactions/s"
+# FLOP per unit: density 27 per unordered pair + 25 per directed
+# contribution (first full pass); force 74 per unordered pair.
+FLOP_DENS_PAIR, FLOP_DENS_DIR, FLOP_FORCE_PAIR = 27, 25, 74
+# FP32 ALU peak derived from the unit counts and clock (B200_PROFILING.md: 148 SMs,
+# clocks.max.sm 1965 MHz; 128 FP32 lanes/SM, FMA = 2 FLOP). Measured: 72.6 TFLOP/s
+# (tools/fp32_peak.cu, profiles/round1/fp32_peak.json).
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+
+CONFIG_TUNING = dict(split_count=64, split_fraction=0.0)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="sph", choices=["sph", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------- clocks ---
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi missing"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            r = [x.strip() for x in r]
+            try:
+                sm.append(float(r[0]))
+                smax.append(float(r[1]))
+            except (ValueError, IndexError):
+                continue
+            for k, nm in enumerate(names):
+                if len(r) > 4 + k and r[4 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------- oracle ---
+def oracle_sample(budget_s: float):
+    """Time the oracle (as it stands) on a bounded sample of the C4 workload: the same
+    clustered generator (64 clumps, seed 140423034) at a reduced N, full evaluation
+    (h root + density + force). N is chosen from a calibration run to fit budget_s."""
+    import numpy as np
+
+    import oracle
+    import workloads
+
+    def one(n):
+        p = workloads.c4(n=n)
+        t0 = time.perf_counter()
+        out = oracle.evaluate_all(p.x, p.v, p.m, p.u, p.box)
+        return time.perf_counter() - t0, int(out["n_pairs"])
+
+    t_cal, _ = one(8192)
+    n = int(8192 * max(1.0, budget_s / max(t_cal, 1e-3)))
+    n = int(2 ** math.floor(math.log2(max(8192, min(n, 1 << 20)))))
+    return n, one, np
+
+
+def cores_used():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count()
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    n, one, _ = oracle_sample(min(args.cpu_budget_s, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        one(n)
+    ts, fs = [], []
+    for _ in range(args.steps):
+        t, F = one(n)
+        ts.append(t)
+        fs.append(F)
+    T = sum(ts)
+    value = 2.0 * sum(fs) / T
+    sample = (f"C4 generator (64 Plummer clumps + 30% background, seed 140423034) at N={n}; "
+              f"full oracle evaluation per step: h root (Eq. 3) + density + force, fp64 numpy/scipy")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": f"C4-recipe sample N={n} (oracle)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores_used(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------- ours -----
+def traffic_from_profiles(kernel: str):
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        d = json.load(open(path))
+        return d.get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
+def run_sph(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    import paper_1404_2303_b200 as sph
+    import workloads
+
+    assert torch.cuda.is_available(), "bench.py needs a CUDA device"
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = world > 1
+    if dist:
+        import torch.distributed as td
+    p = workloads.make(args.config)
+    N = p.n
+    stream = torch.cuda.current_stream(dev)
+    cfg = sph.default_config(p.box, **CONFIG_TUNING)
+    ctx = sph.Context(cfg, device=local_rank, stream=stream.cuda_stream)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    x, v, m, u = t(p.x), t(p.v), t(p.m), t(p.u)
+    h0 = t(p.h0) if np.any(p.h0 > 0) else None
+    out_d = dict(h=torch.empty(N, device=dev), rho=torch.empty(N, device=dev))
+    out_f = dict(a=torch.empty(N, 3, device=dev), dudt=torch.empty(N, device=dev))
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step(xx, hh, vv, mm, uu, od, of):
+        ctx.build_cells(xx, hh)
+        d = ctx.density(vv, mm, uu, out=od)
+        f = ctx.force(vv, out=of)
+        return d.stats, f.stats
+
+    for _ in range(args.warmup):
+        step(x, h0, v, m, u, out_d, out_f)
+    torch.cuda.synchronize()
+
+    def timed(inputs, outs_d, outs_f):
+        stats = []
+        total_ms = 0.0
+        if dist:
+            td.barrier()
+        torch.cuda.synchronize()
+        l0 = ctx.kernel_launches
+        clk = Clocks(local_rank)
+        for _ in range(args.steps):
+            flush.zero_()                       # evict the inputs from L2 between steps
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            sd, sf = step(*inputs, outs_d, outs_f)
+            e1.record(stream)
+            e1.synchronize()
+            total_ms += e0.elapsed_time(e1)
+            stats.append((sd, sf))
+        clocks = clk.stop()
+        torch.cuda.synchronize()
+        if dist:
+            td.barrier()
+        return total_ms, stats, ctx.kernel_launches - l0, clocks
+
+    total_ms, stats, launches, clocks = timed((x, h0, v, m, u), out_d, out_f)
+    F = stats[-1][1]["n_pairs"]
+    D = stats[-1][0]["n_directed"]
+    # e2e: same steps through the C ABI with pinned HOST buffers (copies inside the region)
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        hx, hv, hm, hu = pin(p.x), pin(p.v), pin(p.m), pin(p.u)
+        hh0 = pin(p.h0) if h0 is not None else None
+        hod = dict(h=torch.empty(N).pin_memory(), rho=torch.empty(N).pin_memory())
+        hof = dict(a=torch.empty(N, 3).pin_memory(), dudt=torch.empty(N).pin_memory())
+        e2e_ms, e2e_stats, _, _ = timed((hx, hh0, hv, hm, hu), hod, hof)
+        h2d = sum(a.numel() * 4 for a in (hx, hv, hm, hu)) + (hh0.numel() * 4 if hh0 is not None else 0)
+        d2h = sum(a.numel() * 4 for a in (*hod.values(), *hof.values()))
+        e2e = {"t_ms": e2e_ms, "pairs": 2.0 * sum(s[1]["n_pairs"] for s in e2e_stats),
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+        # the host path must reproduce the device path bit for bit
+        assert torch.equal(hod["rho"], out_d["rho"].cpu()) and torch.equal(hof["a"], out_f["a"].cpu())
+
+    pairs_local = 2.0 * sum(s[1]["n_pairs"] for s in stats)
+    t_max = total_ms
+    pairs_all = pairs_local
+    e2e_tmax = e2e["t_ms"] if e2e else None
+    e2e_pairs = e2e["pairs"] if e2e else None
+    if dist:
+        tt = torch.tensor([total_ms, e2e_tmax or 0.0], dtype=torch.float64, device=dev)
+        td.all_reduce(tt, op=td.ReduceOp.MAX)
+        pp = torch.tensor([pairs_local, e2e_pairs or 0.0], dtype=torch.float64, device=dev)
+        td.all_reduce(pp)
+        t_max, e2e_tmax = float(tt[0]), float(tt[1])
+        pairs_all, e2e_pairs = float(pp[0]), float(pp[1])
+    if rank != 0:
+        ctx.close()
+        return
+
+    sd = [s[0] for s in stats]
+    sfo = [s[1] for s in stats]
+    med = lambda key, arr: statistics.median(a[key] for a in arr)
+    k_force_ms = med("ms_kernel_force", sfo)
+    k_dens_ms = med("ms_kernel_density_full", sd)
+    flop_force = FLOP_FORCE_PAIR * F
+    flop_dens = FLOP_DENS_PAIR * F + FLOP_DENS_DIR * D
+    ms_density = med("ms_density", sd)
+    ms_force = med("ms_force", sfo)
+    ms_build = med("ms_build", sd)
+
+    def roof(name, flop, ms):
+        ach = flop / (ms * 1e-3) / 1e12
+        return {"kernel": name, "bound": "alu", "achieved": ach, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": ach / FP32_PEAK_TFLOPS, "traffic": traffic_from_profiles(name),
+                "flop_per_launch": flop, "ms_per_launch": ms,
+                "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (measured FFMA 72.6)"}
+
+    r_force = roof("k_force", flop_force, k_force_ms)
+    r_dens = roof("k_density", flop_dens, k_dens_ms)
+    # dominant kernel per step: all density passes vs the force launch
+    dens_kernels_ms = ms_density  # upper bound of the density kernels' share
+    dominant, secondary = (r_force, r_dens) if k_force_ms >= k_dens_ms else (r_dens, r_force)
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        n_s, one, _ = oracle_sample(args.cpu_budget_s)
+        t_s, F_s = one(n_s)
+        cpu = {"value": 2.0 * F_s / t_s, "unit": UNIT, "cores": cores_used(), "kind": "oracle",
+               "sample": (f"C4 generator (64 clumps, seed 140423034) at N={n_s}: one full oracle evaluation "
+                          f"(h root + density + force) in {t_s:.1f} s, fp64 numpy/scipy (cKDTree queries "
+                          f"threaded, sums single-threaded)")}
+    value = pairs_all / (t_max * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {N} particles ({p.name} generator, seeds in workloads/), "
+                               f"cold h0" + (" (library guess)" if h0 is None else ""),
+                   "N": N, "box": list(p.box), "l2": "flushed (256 MiB write) before every timed step",
+                   "parallelism": "replicas" if world > 1 else "single GPU",
+                   "split_count": CONFIG_TUNING["split_count"], "split_fraction": CONFIG_TUNING["split_fraction"],
+                   "n_ngb": 48, "n_ngb_tol": cfg.n_ngb_tol},
+        "roofline": dominant,
+        "roofline_secondary": secondary,
+        "cpu_baseline": cpu,
+        "e2e": ({"value": e2e_pairs / (e2e_tmax * 1e-3), "unit": UNIT,
+                 "h2d_bytes_per_step": e2e["h2d_bytes_per_step"], "d2h_bytes_per_step": e2e["d2h_bytes_per_step"]}
+                if e2e else None),
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "breakdown": {"F_pairs": F, "D_directed": D, "ms_build": ms_build, "ms_density": ms_density,
+                      "ms_force": ms_force, "ms_kernel_density_full": k_dens_ms, "ms_kernel_force": k_force_ms,
+                      "rate_loops_2F_over_tdens_plus_tforce": 2.0 * F / ((ms_density + ms_force) * 1e-3),
+                      "h_iters": sd[-1]["h_iters"], "rebuilds": sd[-1]["n_rebuilds"],
+                      "cand_density_full": sd[-1]["n_candidates_density_full"],
+                      "cand_force": sfo[-1]["n_candidates"], "levels": sd[-1]["n_levels"],
+                      "cells": sd[-1]["n_cells"]},
+    }
+    print(json.dumps(line), flush=True)
+    ctx.close()
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as td
+        torch.cuda.set_device(local_rank)
+        td.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_sph(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as td
+            td.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

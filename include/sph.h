@@ -92,8 +92,12 @@ typedef struct {         /* host struct, filled when non-NULL */
   int32_t h_iters;       /* density passes executed */
   int32_t n_levels;      /* depth of the cell hierarchy + 1 */
   int64_t n_cells, n_leaves, n_pair_slots; /* hierarchy size; kept pair entries (directed) */
-  double ms_build, ms_density, ms_force, ms_halo;
+  double ms_build, ms_density, ms_force, ms_halo; /* whole calls (CUDA events on the ctx stream) */
   int64_t halo_sent, halo_recv;
+  /* kernel-only times (CUDA events bracketing the single launch on the ctx stream) */
+  double ms_kernel_density_full; /* first density pass: every particle active */
+  double ms_kernel_force;        /* the force kernel */
+  int64_t n_candidates_density_full; /* distance tests of that first full density pass */
 } sph_stats;
 
 /* Fill *cfg with the paper's defaults for the given box. */

@@ -117,7 +117,7 @@ struct sph_ctx {
 
   // named device buffers
   DBuf b[64];
-  cudaEvent_t ev[8];
+  cudaEvent_t ev[12];
   bool ev_ok = false;
 };
 

@@ -43,11 +43,12 @@ struct DensOp {
   double sf;
   float smf, smqfp, sqfp, divs, crx, cry, crz;
   int cnt;
-  long long ncand;
+  long long ncand, nself;
 
   __device__ __forceinline__ void init(int s_, bool v) {
     s = s_;
     valid = v;
+    nself = 0;
     sf = 0.0;
     smf = smqfp = sqfp = divs = crx = cry = crz = 0.f;
     cnt = 0;
@@ -126,11 +127,12 @@ struct ForceOp {
   float hi, hi2, hinv, hhat, At, rhoi, ci, fi, vxi, vyi, vzi;
   float ax, ay, az, du, vsig;
   int cnt;
-  long long ncand;
+  long long ncand, nself;
 
   __device__ __forceinline__ void init(int s_, bool v) {
     s = s_;
     valid = v;
+    nself = 0;
     ax = ay = az = du = vsig = 0.f;
     cnt = 0;
     ncand = 0;
@@ -216,6 +218,7 @@ __device__ __forceinline__ void seg_self(Op& op, int first, int cnt, typename Op
     const int m = min(32, cnt - base);
     if (op.valid) {
       op.ncand += m;
+      op.nself += m;
 #pragma unroll 4
       for (int t = 0; t < m; ++t) op.interact(sm[t], base + t == my);
     }
@@ -326,10 +329,16 @@ __global__ void __launch_bounds__(INTERACT_WARPS * 32) k_density(TravParams P, c
     out.acc0[s] = make_float4(op.smf, op.smqfp, op.sqfp, op.divs);
     out.acc1[s] = make_float4(op.crx, op.cry, op.crz, __int_as_float(op.cnt));
   }
-  long long nc = op.ncand;
+  long long nc = op.ncand, ns = op.nself;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) nc += __shfl_xor_sync(FULL_MASK, nc, o);
-  if (lane == 0 && P.ctr) atomicAdd(&P.ctr[C_CAND], (unsigned long long)nc);
+  for (int o = 16; o > 0; o >>= 1) {
+    nc += __shfl_xor_sync(FULL_MASK, nc, o);
+    ns += __shfl_xor_sync(FULL_MASK, ns, o);
+  }
+  if (lane == 0 && P.ctr) {
+    atomicAdd(&P.ctr[C_CAND], (unsigned long long)nc);
+    atomicAdd(&P.ctr[C_TMP1], (unsigned long long)ns);
+  }
 }
 
 struct ForceOut {
@@ -370,15 +379,17 @@ __global__ void __launch_bounds__(INTERACT_WARPS * 32) k_force(TravParams P, con
     if (out.vsig) out.vsig[p] = op.vsig;
     if (out.nnbr) out.nnbr[p] = op.cnt;
   }
-  long long nc = op.ncand;
+  long long nc = op.ncand, ns = op.nself;
   long long nf = v ? op.cnt : 0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     nc += __shfl_xor_sync(FULL_MASK, nc, o);
+    ns += __shfl_xor_sync(FULL_MASK, ns, o);
     nf += __shfl_xor_sync(FULL_MASK, nf, o);
   }
   if (lane == 0 && P.ctr) {
     atomicAdd(&P.ctr[C_CAND], (unsigned long long)nc);
+    atomicAdd(&P.ctr[C_TMP1], (unsigned long long)ns);
     atomicAdd(&P.ctr[C_NFORCE], (unsigned long long)nf);
   }
 }

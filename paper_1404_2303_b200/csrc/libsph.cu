@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstring>
 #include <exception>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "radix_sort.cuh"
@@ -72,6 +73,16 @@ static int grid1d(sph_ctx* c, int64_t n, int block) {
 static int gridfull(int64_t n, int block) { return (int)std::max<int64_t>((n + block - 1) / block, 1); }
 
 static void sync(sph_ctx* c) { CUDA_TRY(cudaStreamSynchronize(c->stream)); }
+
+static bool dbg_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SPH_DEBUG");
+    v = (e && e[0] && e[0] != '0') ? 1 : 0;
+  }
+  return v == 1;
+}
+#define DBG(...) do { if (dbg_on()) { fprintf(stderr, "[sph] " __VA_ARGS__); fflush(stderr); } } while (0)
 
 // =========================================================== counters ===========
 static unsigned long long* ctr(sph_ctx* c) { return B<unsigned long long>(c, B_COUNTERS, C_NCOUNTERS); }
@@ -370,6 +381,8 @@ static void build_structure(sph_ctx* c, bool count_only) {
   LAUNCH(k_write_tasks, gridfull(nnodes, 256), 256, 0, nnodes, nchunk, cscan, tasks);
   c->n_leaves = ntasks;  // number of (leaf, chunk) tasks; see stats
   sync(c);
+  DBG("build: n %lld top %dx%dx%d depth %d levels %d nodes %d tasks %d sorted %lld big %s\n", (long long)n,
+      c->ntop[0], c->ntop[1], c->ntop[2], depth, nlev, nnodes, ntasks, (long long)c->n_sorted, "");
 }
 
 // =========================================================== inputs =============
@@ -406,9 +419,10 @@ static T* dev_out(sph_ctx* c, T* p, size_t count, int stage_id, std::vector<OutM
   maps.push_back(OutMap{p, d, count * sizeof(T)});
   return d;
 }
-static void flush_out(sph_ctx* c, std::vector<OutMap>& maps) {
+static void flush_out(sph_ctx* c, std::vector<OutMap>& maps, cudaEvent_t done) {
   for (auto& m : maps)
     CUDA_TRY(cudaMemcpyAsync(m.user, m.dev, m.bytes, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaEventRecord(done, c->stream));
   if (!maps.empty()) sync(c);
 }
 
@@ -525,7 +539,7 @@ int sph_create(const sph_config* cfg, int dev, void* stream, sph_ctx** out) {
       CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
       c->own_stream = true;
     }
-    for (int i = 0; i < 8; ++i) CUDA_TRY(cudaEventCreate(&c->ev[i]));
+    for (int i = 0; i < 12; ++i) CUDA_TRY(cudaEventCreate(&c->ev[i]));
     c->ev_ok = true;
   } catch (const SphError& e) {
     delete c;
@@ -541,7 +555,7 @@ int sph_destroy(sph_ctx* c) {
   cudaStreamSynchronize(c->stream);
   for (int i = 0; i < 64; ++i) dev_free(c, c->b[i].p);
   if (c->ev_ok)
-    for (int i = 0; i < 8; ++i) cudaEventDestroy(c->ev[i]);
+    for (int i = 0; i < 12; ++i) cudaEventDestroy(c->ev[i]);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
   return SPH_OK;
@@ -672,21 +686,25 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
     ctr_reset(c);
     if (ntasks > 0) {
       TravParams P = trav(c, tasks, ntasks, active);
+      if (iters == 0) CUDA_TRY(cudaEventRecord(c->ev[6], c->stream));
       LAUNCH(k_density, gridfull(ntasks, INTERACT_WARPS), INTERACT_WARPS * 32, 0, P, Bget<float4>(c, B_XH), vm,
              DensOut{sf, acc0, acc1});
+      if (iters == 0) CUDA_TRY(cudaEventRecord(c->ev[7], c->stream));
     }
     ++iters;
     const bool last = iters >= c->cfg.max_h_iter;
     if (last) {
       ctr_read(c, hc);
-      cand_last = (long long)hc[C_CAND];
+      if (iters == 1) cand_last = (long long)hc[C_CAND];
       break;  // sums are at the current h; unconverged particles are reported
     }
     LAUNCH(k_h_update, grid1d(c, n, 256), 256, 0, n, Bget<float4>(c, B_XH), Bget<float>(c, B_HB),
            Bget<float>(c, B_HLO), Bget<float>(c, B_HHI), active, sf, acc0, c->cfg.n_ngb, c->cfg.n_ngb_tol, ctr(c));
     ctr_read(c, hc);
-    cand_last = (long long)hc[C_CAND];
+    if (iters == 1) cand_last = (long long)hc[C_CAND];
     unconv = (long long)hc[C_UNCONV];
+    DBG("density pass %d: tasks %d cand %llu (self %llu) -> unconverged %lld rebuild %llu\n", iters, ntasks,
+        hc[C_CAND], hc[C_TMP1], unconv, hc[C_REBUILD]);
     if (unconv == 0) break;
     all_tasks = false;
     if (hc[C_REBUILD] > 0) {
@@ -719,8 +737,7 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   LAUNCH(k_ghost, grid1d(c, n, 256), 256, 0, n, Bget<float4>(c, B_XH), uc, sf, acc0, acc1, c->cfg.gamma,
          c->cfg.balsara_eps, fx, fs, go, ctr(c));
   LAUNCH(k_node_hmax, gridfull((int64_t)c->n_nodes * 32, 256), 256, 0, c->n_nodes, nodes(c), Bget<float4>(c, B_XH));
-  CUDA_TRY(cudaEventRecord(c->ev[3], c->stream));
-  flush_out(c, maps);
+  flush_out(c, maps, c->ev[3]);
   c->state = 2;
   int status = (unconv > 0 && iters >= c->cfg.max_h_iter) ? SPH_E_NOCONV : SPH_OK;
   if (st || (c->cfg.flags & SPH_F_SYNC)) {
@@ -730,6 +747,7 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
       fill_struct_stats(c, st);
       st->n_directed = (int64_t)hc[C_NDIR];
       st->n_candidates = cand_last;
+      st->n_candidates_density_full = cand_last;
       st->n_unconverged = status == SPH_E_NOCONV ? unconv : 0;
       st->h_iters = iters;
       float ms = 0.f;
@@ -737,6 +755,8 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
       st->ms_build = ms;
       cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]);
       st->ms_density = ms;
+      cudaEventElapsedTime(&ms, c->ev[6], c->ev[7]);
+      st->ms_kernel_density_full = ms;
     }
   }
   if (status == SPH_E_NOCONV) {
@@ -763,21 +783,25 @@ int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out, int3
   fo.perm = Bget<uint32_t>(c, B_PERM);
   ctr_reset(c);
   TravParams P = trav(c, Bget<int2>(c, B_TASKS), c->n_leaves, nullptr);
+  CUDA_TRY(cudaEventRecord(c->ev[8], c->stream));
   LAUNCH(k_force, gridfull(c->n_leaves, INTERACT_WARPS), INTERACT_WARPS * 32, 0, P, Bget<float4>(c, B_FX),
          Bget<float4>(c, B_VM), Bget<float4>(c, B_FS), c->cfg.alpha, fo);
-  CUDA_TRY(cudaEventRecord(c->ev[5], c->stream));
-  flush_out(c, maps);
+  CUDA_TRY(cudaEventRecord(c->ev[9], c->stream));
+  flush_out(c, maps, c->ev[5]);
   if (st || (c->cfg.flags & SPH_F_SYNC)) {
     unsigned long long hc[C_NCOUNTERS];
     ctr_read(c, hc);
     if (st) {
       memset(st, 0, sizeof(*st));
       fill_struct_stats(c, st);
+      DBG("force: tasks %d cand %llu (self %llu) pairs %llu\n", c->n_leaves, hc[C_CAND], hc[C_TMP1], hc[C_NFORCE] / 2);
       st->n_pairs = (int64_t)(hc[C_NFORCE] / 2);
       st->n_candidates = (int64_t)hc[C_CAND];
       float ms = 0.f;
       cudaEventElapsedTime(&ms, c->ev[4], c->ev[5]);
       st->ms_force = ms;
+      cudaEventElapsedTime(&ms, c->ev[8], c->ev[9]);
+      st->ms_kernel_force = ms;
     }
   }
   API_END

@@ -52,7 +52,8 @@ class Stats(ctypes.Structure):
         ("n_levels", ctypes.c_int32), ("n_cells", ctypes.c_int64), ("n_leaves", ctypes.c_int64),
         ("n_pair_slots", ctypes.c_int64), ("ms_build", ctypes.c_double), ("ms_density", ctypes.c_double),
         ("ms_force", ctypes.c_double), ("ms_halo", ctypes.c_double), ("halo_sent", ctypes.c_int64),
-        ("halo_recv", ctypes.c_int64),
+        ("halo_recv", ctypes.c_int64), ("ms_kernel_density_full", ctypes.c_double),
+        ("ms_kernel_force", ctypes.c_double), ("n_candidates_density_full", ctypes.c_int64),
     ]
 
     def as_dict(self):
