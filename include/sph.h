@@ -47,7 +47,7 @@ typedef enum {
   SPH_OK = 0,
   SPH_E_ARG = -1,    /* null required pointer, n <= 0, n changed between calls, bad config
                         (box <= 0, gamma <= 1, alpha < 0, n_ngb <= 32/3, tol <= 0,
-                        top_edge_factor < 1, split_fraction outside (0,1]) */
+                        top_edge_factor < 1, split_fraction outside [0,1)) */
   SPH_E_DOMAIN = -2, /* non-finite input; x outside [0,L); m <= 0; u <= 0; h0 < 0;
                         a smoothing length >= min(L)/3 (fewer than 3 top cells per axis) */
   SPH_E_STATE = -3,  /* order violated: density before build_cells, force before density */

@@ -512,7 +512,7 @@ static bool cfg_ok(const sph_config* f, std::string& why) {
   if (!(f->n_ngb_tol > 0.f)) { why = "n_ngb_tol <= 0"; return false; }
   if (!(f->top_edge_factor >= 1.f)) { why = "top_edge_factor < 1"; return false; }
   if (!(f->h_margin >= 1.f)) { why = "h_margin < 1"; return false; }
-  if (!(f->split_fraction > 0.f && f->split_fraction <= 1.f)) { why = "split_fraction outside (0,1]"; return false; }
+  if (!(f->split_fraction >= 0.f && f->split_fraction < 1.f)) { why = "split_fraction outside [0,1)"; return false; }
   if (f->split_count < 1) { why = "split_count < 1"; return false; }
   if (f->max_h_iter < 1) { why = "max_h_iter < 1"; return false; }
   if (f->nranks < 1 || f->rank < 0 || f->rank >= f->nranks) { why = "bad rank/nranks"; return false; }
