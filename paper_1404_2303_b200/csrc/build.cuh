@@ -7,13 +7,25 @@
 //  a4  k_level_split / k_make_children : recursive split, "more than some minimal number"
 //                                 and "a reasonable fraction" with h < edge/2 (P:510-518,
 //                                 constants P:1354-1356), one level per launch
-//  a5  k_top_slots / k_child_slots / k_kept : interaction slots. Top cells pair with their
-//                                 26 periodic neighbours; a split cell's self
-//                                 becomes 8 child selfs + 28 sibling pairs;
-//                                 a pair is refined iff both cells are split and all h in
-//                                 both are < edge/2, else kept whole.
-//  a6  k_sort_warp / k_sort_block / big-node radix path : per (cell, direction) lists
-//                                 sorted along the 13 canonical axes
+//  a5  k_top_slots / k_child_slots : every cell's 26 same-level neighbours (periodic at the
+//                                 top; children inherit them through their
+//                                 parent, which is the self refinement into 8 child selfs +
+//                                 28 sibling pairs of P:519-522 and the pair refinement of
+//                                 P:523-532).
+//      k_tau / k_level_counts / k_list_masks : the interaction level of each particle.
+//                                 tau_i = min(leaf level, deepest level with edge >= h_i).
+//                                 The pair {i,j} is enumerated exactly once, at level
+//                                 min(tau_i, tau_j), between the cells of i and j at that level
+//                                 (equal or adjacent since r < max(h) <= edge). This is the
+//                                 paper's refinement rule ("refine iff all h < edge/2")
+//                                 applied per particle instead of per cell pair: the large-h
+//                                 particles stay at the coarse level as a residue while the
+//                                 rest of the pair is refined. Per cell and level
+//                                 two source lists: A = {tau >= l} (targets with tau == l
+//                                 sweep them) and R = {tau == l} (deeper targets sweep them).
+//  a6  k_sort_warp / k_sort_block / big radix path : the A and R lists of each cell sorted
+//                                 along the 13 canonical axes where a neighbour needs them
+//                                 (P:687-698), plus an unsorted copy for the cell's own sweep
 #pragma once
 #include "common.cuh"
 
@@ -26,11 +38,16 @@ struct NodeArrays {
   float* hmaxb;     // max h_build in the cell
   int* split;       // 1 if split into children
   int* slot;        // [27*node + k] neighbour cell at offset k (same level), -1 if none
-  int* kept;        // 27-bit mask of kept pair slots
-  int* dirmask;     // 13-bit mask of sorted directions needed (as a source)
-  int64_t* sortoff; // offset of the node's sorted block in the list array
-  float* hmaxf;     // max final h in the cell (force window)
+  int* nA;          // #{i in cell : tau_i >= level}   (list A)
+  int* nR;          // #{i in cell : tau_i == level}   (list R)
+  int* amask;       // 14-bit: directions 0..12 (+ bit 13 unsorted) of list A that are needed
+  int* rmask;       // 14-bit, list R
+  int64_t* offA;    // offsets of the node's A / R blocks in the list array
+  int64_t* offR;
+  float* hmaxA;     // max final h over list A / R (force window)
+  float* hmaxR;
 };
+#define LIST_SELF 13  // "direction" of the unsorted copy used for the cell's own sweep
 
 struct LevelGeom {           // per-level edges (fp32), up to SPH_MAX_DEPTH+1 levels
   float E[SPH_MAX_DEPTH + 2][3];
@@ -248,12 +265,10 @@ __global__ void k_top_slots(int n0, int nx, int ny, int nz, const int* __restric
   }
 }
 
-__device__ __forceinline__ bool refine_pair(const NodeArrays& N, int x, int y, float half_edge) {
-  return N.split[x] && N.split[y] && N.hmaxb[x] < half_edge && N.hmaxb[y] < half_edge;
-}
-
-// slots of the nodes of level l >= 1 from their parent's slots (gather form: no atomics)
-__global__ void k_child_slots(int a, int b, float parent_half_edge, NodeArrays N) {
+// slots of the nodes of level l >= 1 from their parent's slots (gather form: no atomics).
+// Every existing same-level neighbour is recorded; which pairs a level enumerates is
+// decided per particle by tau (k_tau), not per cell pair.
+__global__ void k_child_slots(int a, int b, NodeArrays N) {
   int c = a + blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= b) return;
   int X = N.parent[c];
@@ -270,28 +285,85 @@ __global__ void k_child_slots(int a, int b, float parent_half_edge, NodeArrays N
       } else {
         int kp = (Px + 1) * 9 + (Py + 1) * 3 + (Pz + 1);
         int Y = N.slot[27 * (int64_t)X + kp];
-        if (Y >= 0 && refine_pair(N, X, Y, parent_half_edge)) y = N.child[8 * (int64_t)Y + bo];
+        if (Y >= 0) y = N.child[8 * (int64_t)Y + bo];              // pair refinement
       }
     }
     N.slot[27 * (int64_t)c + k] = y;
   }
 }
 
-// kept pair slots and the sorted directions each cell needs as a source
-__global__ void k_kept(int a, int b, float half_edge, NodeArrays N, int64_t* __restrict__ nsort) {
-  int x = a + blockIdx.x * blockDim.x + threadIdx.x;
-  if (x >= b) return;
-  int kept = 0, dm = 0;
-  for (int k = 0; k < 27; ++k) {
-    int y = N.slot[27 * (int64_t)x + k];
-    if (y >= 0 && !refine_pair(N, x, y, half_edge)) {
-      kept |= 1 << k;
-      dm |= 1 << slot_dir(k);
-    }
+// tau_i = min(leaf level, deepest level l with min edge E_l >= h_build,i): at that level
+// every partner j with r < max(h_i, h_j) and tau_j >= tau_i lies in the 27 cells around i.
+__global__ void k_tau(int nnodes, NodeArrays N, LevelGeom g, const float* __restrict__ hb,
+                      uint8_t* __restrict__ tau) {
+  const int lane = threadIdx.x & 31;
+  const int node = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  if (node >= nnodes || N.split[node]) return;
+  const int first = N.first[node], cnt = N.count[node], L = N.ijk[node].w;
+  for (int s = first + lane; s < first + cnt; s += 32) {
+    const float h = hb[s] * 1.000001f;
+    int t = L;
+    while (t > 0 && 2.f * g.half_min[t] < h) --t;
+    tau[s] = (uint8_t)t;
   }
-  N.kept[x] = kept;
-  N.dirmask[x] = dm;
-  nsort[x] = (int64_t)__popc(dm) * N.count[x];
+}
+
+__global__ void k_level_counts(int nnodes, NodeArrays N, const uint8_t* __restrict__ tau) {
+  const int lane = threadIdx.x & 31;
+  const int node = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  if (node >= nnodes) return;
+  const int first = N.first[node], cnt = N.count[node], l = N.ijk[node].w;
+  int na = 0, nr = 0;
+  for (int s = first + lane; s < first + cnt; s += 32) {
+    const int t = tau[s];
+    na += t >= l;
+    nr += t == l;
+  }
+  na = warp_sum_i(na);
+  nr = warp_sum_i(nr);
+  if (lane == 0) {
+    N.nA[node] = na;
+    N.nR[node] = nr;
+  }
+}
+
+// which lists a cell must provide as a source: its neighbour X (or itself, bit 13) sweeps
+// list A of this cell if X has targets with tau == l, list R if X has targets with tau > l.
+// A direction is sorted only if enough targets sweep it (or the list is tiny): otherwise
+// the sweeping warps read the unsorted copy (bit 13) with the box filter alone, which is
+// cheaper than sorting a list that one or two warps visit.
+#define SORT_DEMAND_MIN 64
+__global__ void k_list_masks(int nnodes, NodeArrays N, int64_t* __restrict__ nsort /*[2*nnodes]*/) {
+  const int y = blockIdx.x * blockDim.x + threadIdx.x;
+  if (y >= nnodes) return;
+  const int na = N.nA[y], nr = N.nR[y];
+  int demA[14], demR[14];
+#pragma unroll
+  for (int d = 0; d < 14; ++d) demA[d] = demR[d] = 0;
+  for (int k = 0; k < 27; ++k) {
+    const int x = (k == 13) ? y : N.slot[27 * (int64_t)y + k];
+    if (x < 0) continue;
+    const int d = (k == 13) ? LIST_SELF : slot_dir(k);
+    demA[d] += N.nR[x];
+    demR[d] += N.nA[x] - N.nR[x];
+  }
+  int am = 0, rm = 0;
+#pragma unroll
+  for (int d = 0; d < 14; ++d) {
+    if (na > 0 && demA[d] > 0) am |= (d == LIST_SELF || demA[d] >= SORT_DEMAND_MIN || na <= 32) ? (1 << d) : (1 << LIST_SELF);
+    if (nr > 0 && demR[d] > 0) rm |= (d == LIST_SELF || demR[d] >= SORT_DEMAND_MIN || nr <= 32) ? (1 << d) : (1 << LIST_SELF);
+  }
+  N.amask[y] = am;
+  N.rmask[y] = rm;
+  nsort[2 * (int64_t)y] = (int64_t)__popc(am) * na;
+  nsort[2 * (int64_t)y + 1] = (int64_t)__popc(rm) * nr;
+}
+
+__global__ void k_split_offsets(int nnodes, const int64_t* __restrict__ scan2, NodeArrays N) {
+  const int y = blockIdx.x * blockDim.x + threadIdx.x;
+  if (y >= nnodes) return;
+  N.offA[y] = scan2[2 * (int64_t)y];
+  N.offR[y] = scan2[2 * (int64_t)y + 1];
 }
 
 // ---------------------------------------------------------------- a6 ---------
@@ -304,31 +376,45 @@ struct SortEntry {  // 8 bytes: projection key and cell-order particle index
   int idx;
 };
 
-// warp per node with count <= 32: one particle per lane, warp bitonic sort per direction
-__global__ void k_sort_warp(int nnodes, const float4* __restrict__ xh, NodeArrays N, LevelGeom g,
-                            SortEntry* __restrict__ out) {
+struct ListSeg {     // one (cell, kind) list family: members, directions, destination
+  int cnt, mask;
+  int64_t off;
+};
+__device__ __forceinline__ ListSeg list_seg(const NodeArrays& N, int node, int kind) {
+  ListSeg L;
+  L.cnt = kind ? N.nR[node] : N.nA[node];
+  L.mask = kind ? N.rmask[node] : N.amask[node];
+  L.off = kind ? N.offR[node] : N.offA[node];
+  return L;
+}
+__device__ __forceinline__ bool list_member(int t, int l, int kind) { return kind ? (t == l) : (t >= l); }
+
+// warp per (node, kind) with node count <= 32: one particle per lane, warp bitonic sort
+__global__ void k_sort_warp(int nnodes, const float4* __restrict__ xh, const uint8_t* __restrict__ tau,
+                            NodeArrays N, LevelGeom g, SortEntry* __restrict__ out) {
   const int lane = threadIdx.x & 31;
-  const int node = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int node = (int)(wid >> 1), kind = (int)(wid & 1);
   if (node >= nnodes) return;
-  const int cnt = N.count[node];
-  const int dm = N.dirmask[node];
-  if (dm == 0 || cnt > 32) return;
+  const ListSeg L = list_seg(N, node, kind);
+  const int cnt_node = N.count[node];
+  if (L.mask == 0 || L.cnt == 0 || cnt_node > 32) return;
   const int first = N.first[node];
   const int4 c = N.ijk[node];
   float rx = 0.f, ry = 0.f, rz = 0.f;
-  if (lane < cnt) {
+  bool mem = false;
+  if (lane < cnt_node) {
     float4 p = xh[first + lane];
     rx = p.x - node_corner(c.x, c.w, 0, g);
     ry = p.y - node_corner(c.y, c.w, 1, g);
     rz = p.z - node_corner(c.z, c.w, 2, g);
+    mem = list_member(tau[first + lane], c.w, kind);
   }
-  int64_t base = N.sortoff[node];
   int r = 0;
-  for (int d = 0; d < 13; ++d) {
-    if (!((dm >> d) & 1)) continue;
-    float key = proj(rx, ry, rz, dir_unit(d));
-    uint64_t v = (lane < cnt) ? (((uint64_t)float_ord(key) << 32) | (uint32_t)lane) : ~0ull;
-    // bitonic sort of 32 values across the warp (ascending)
+  for (int d = 0; d < 14; ++d) {
+    if (!((L.mask >> d) & 1)) continue;
+    float key = (d == LIST_SELF) ? 0.f : proj(rx, ry, rz, dir_unit(d));
+    uint64_t v = mem ? (((uint64_t)float_ord(key) << 32) | (uint32_t)lane) : ~0ull;
 #pragma unroll
     for (int size = 2; size <= 32; size <<= 1) {
 #pragma unroll
@@ -340,39 +426,74 @@ __global__ void k_sort_warp(int nnodes, const float4* __restrict__ xh, NodeArray
         v = (lower == up) ? mn : mx;
       }
     }
-    int li = (lane < cnt) ? (int)(uint32_t)v : 0;
+    int li = (lane < L.cnt) ? (int)(uint32_t)v : 0;
     float kk = __shfl_sync(FULL_MASK, key, li);
-    if (lane < cnt) out[base + (int64_t)r * cnt + lane] = SortEntry{kk, first + li};
+    if (lane < L.cnt) out[L.off + (int64_t)r * L.cnt + lane] = SortEntry{kk, first + li};
     ++r;
   }
 }
 
+// deterministic block compaction of the members of (node, kind) into smem (cell order)
+__device__ __forceinline__ int block_compact_members(int first, int cnt_node, int l, int kind,
+                                                     const uint8_t* __restrict__ tau, int* mem, int cap,
+                                                     int* wsum) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int total = 0;
+  for (int base = 0; base < cnt_node; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const bool m = i < cnt_node && list_member(tau[first + i], l, kind);
+    const unsigned bal = __ballot_sync(FULL_MASK, m);
+    if (lane == 0) wsum[w] = __popc(bal);
+    __syncthreads();
+    int before = 0;
+    for (int ww = 0; ww < w; ++ww) before += wsum[ww];
+    int tot = 0;
+    for (int ww = 0; ww < nw; ++ww) tot += wsum[ww];
+    const int pos = total + before + __popc(bal & lanemask_lt());
+    if (m && pos < cap) mem[pos] = i;
+    total += tot;
+    __syncthreads();
+  }
+  return total;
+}
+
 #define SORT_BLOCK_MAX 4096
-// CTA per node with 32 < count <= SORT_BLOCK_MAX: shared-memory bitonic sort per direction
-__global__ void __launch_bounds__(512) k_sort_block(int nnodes, const float4* __restrict__ xh, NodeArrays N,
-                                                     LevelGeom g, SortEntry* __restrict__ out) {
+// CTA per (node, kind) with 32 < node count and members <= SORT_BLOCK_MAX: shared-memory
+// bitonic sort per direction of (key, member index) composites
+__global__ void __launch_bounds__(512) k_sort_block(int nnodes, const float4* __restrict__ xh,
+                                                     const uint8_t* __restrict__ tau, NodeArrays N, LevelGeom g,
+                                                     SortEntry* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char sb_raw[];
   uint64_t* sk = reinterpret_cast<uint64_t*>(sb_raw);
   float* skey = reinterpret_cast<float*>(sk + SORT_BLOCK_MAX);
-  const int node = blockIdx.x;
+  int* mem = reinterpret_cast<int*>(skey + SORT_BLOCK_MAX);
+  __shared__ int wsum[32];
+  const int node = blockIdx.x >> 1, kind = blockIdx.x & 1;
   if (node >= nnodes) return;
-  const int cnt = N.count[node];
-  const int dm = N.dirmask[node];
-  if (dm == 0 || cnt <= 32 || cnt > SORT_BLOCK_MAX) return;
+  const ListSeg L = list_seg(N, node, kind);
+  const int cnt_node = N.count[node];
+  if (L.mask == 0 || L.cnt == 0 || cnt_node <= 32 || L.cnt > SORT_BLOCK_MAX) return;
   const int first = N.first[node];
   const int4 c = N.ijk[node];
+  block_compact_members(first, cnt_node, c.w, kind, tau, mem, SORT_BLOCK_MAX, wsum);
+  const int cnt = L.cnt;
   const float cx = node_corner(c.x, c.w, 0, g), cy = node_corner(c.y, c.w, 1, g),
               cz = node_corner(c.z, c.w, 2, g);
   int P = 64;
   while (P < cnt) P <<= 1;
-  int64_t base = N.sortoff[node];
   int r = 0;
-  for (int d = 0; d < 13; ++d) {
-    if (!((dm >> d) & 1)) continue;
+  for (int d = 0; d < 14; ++d) {
+    if (!((L.mask >> d) & 1)) continue;
+    if (d == LIST_SELF) {
+      for (int i = threadIdx.x; i < cnt; i += blockDim.x)
+        out[L.off + (int64_t)r * cnt + i] = SortEntry{0.f, first + mem[i]};
+      ++r;
+      continue;
+    }
     float3 dv = dir_unit(d);
     for (int i = threadIdx.x; i < P; i += blockDim.x) {
       if (i < cnt) {
-        float4 p = xh[first + i];
+        float4 p = xh[first + mem[i]];
         float key = proj(p.x - cx, p.y - cy, p.z - cz, dv);
         skey[i] = key;
         sk[i] = ((uint64_t)float_ord(key) << 32) | (uint32_t)i;
@@ -398,37 +519,57 @@ __global__ void __launch_bounds__(512) k_sort_block(int nnodes, const float4* __
     }
     for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
       int li = (int)(uint32_t)sk[i];
-      out[base + (int64_t)r * cnt + i] = SortEntry{skey[li], first + li};
+      out[L.off + (int64_t)r * cnt + i] = SortEntry{skey[li], first + mem[li]};
     }
     __syncthreads();
     ++r;
   }
 }
 
-// big nodes (count > SORT_BLOCK_MAX): composite keys (segment, key) sorted by the radix sort
-__global__ void k_big_keys(int nbig, const int* __restrict__ bignodes, const int64_t* __restrict__ bigoff,
-                           const float4* __restrict__ xh, NodeArrays N, LevelGeom g,
-                           uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
-  int bi = blockIdx.x;
+// big lists (members > SORT_BLOCK_MAX): composite keys (segment, key) for the radix sort.
+// Segment ids grow with the destination offset, so the sorted order is the layout order.
+__global__ void __launch_bounds__(512) k_big_keys(int nbig, const int* __restrict__ bigseg,
+                                                  const int64_t* __restrict__ bigoff, const float4* __restrict__ xh,
+                                                  const uint8_t* __restrict__ tau, NodeArrays N, LevelGeom g,
+                                                  uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  __shared__ int wsum[32];
+  const int bi = blockIdx.x;
   if (bi >= nbig) return;
-  int node = bignodes[bi];
-  int cnt = N.count[node], dm = N.dirmask[node], first = N.first[node];
-  int4 c = N.ijk[node];
+  const int node = bigseg[bi] >> 1, kind = bigseg[bi] & 1;
+  const ListSeg L = list_seg(N, node, kind);
+  const int first = N.first[node], cnt_node = N.count[node];
+  const int4 c = N.ijk[node];
   const float cx = node_corner(c.x, c.w, 0, g), cy = node_corner(c.y, c.w, 1, g),
               cz = node_corner(c.z, c.w, 2, g);
-  int64_t base = bigoff[bi];
-  int r = 0;
-  for (int d = 0; d < 13; ++d) {
-    if (!((dm >> d) & 1)) continue;
-    float3 dv = dir_unit(d);
-    uint64_t seg = (uint64_t)bi * 13 + r;
-    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-      float4 p = xh[first + i];
-      float key = proj(p.x - cx, p.y - cy, p.z - cz, dv);
-      keys[base + (int64_t)r * cnt + i] = (seg << 32) | float_ord(key);
-      vals[base + (int64_t)r * cnt + i] = (uint32_t)(first + i);
+  const int64_t base = bigoff[bi];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int total = 0;
+  for (int b0 = 0; b0 < cnt_node; b0 += blockDim.x) {
+    const int i = b0 + threadIdx.x;
+    const bool m = i < cnt_node && list_member(tau[first + i], c.w, kind);
+    const unsigned bal = __ballot_sync(FULL_MASK, m);
+    if (lane == 0) wsum[w] = __popc(bal);
+    __syncthreads();
+    int before = 0, tot = 0;
+    for (int ww = 0; ww < nw; ++ww) {
+      if (ww < w) before += wsum[ww];
+      tot += wsum[ww];
     }
-    ++r;
+    if (m) {
+      const int pos = total + before + __popc(bal & lanemask_lt());
+      const float4 p = xh[first + i];
+      int r = 0;
+      for (int d = 0; d < 14; ++d) {
+        if (!((L.mask >> d) & 1)) continue;
+        const float key = (d == LIST_SELF) ? 0.f : proj(p.x - cx, p.y - cy, p.z - cz, dir_unit(d));
+        const uint64_t seg = (uint64_t)bi * 14 + r;
+        keys[base + (int64_t)r * L.cnt + pos] = (seg << 32) | float_ord(key);
+        vals[base + (int64_t)r * L.cnt + pos] = (uint32_t)(first + i);
+        ++r;
+      }
+    }
+    total += tot;
+    __syncthreads();
   }
 }
 
@@ -437,33 +578,118 @@ __device__ __forceinline__ float ord_float(uint32_t u) {
   return __uint_as_float(b);
 }
 
-__global__ void k_big_write(int nbig, const int* __restrict__ bignodes, const int64_t* __restrict__ bigoff,
+__global__ void k_big_write(int nbig, const int* __restrict__ bigseg, const int64_t* __restrict__ bigoff,
                             NodeArrays N, const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals,
                             SortEntry* __restrict__ out) {
   int bi = blockIdx.x;
   if (bi >= nbig) return;
-  int node = bignodes[bi];
-  int64_t n_ent = (int64_t)__popc(N.dirmask[node]) * N.count[node];
-  int64_t src = bigoff[bi], dst = N.sortoff[node];
+  const ListSeg L = list_seg(N, bigseg[bi] >> 1, bigseg[bi] & 1);
+  int64_t n_ent = (int64_t)__popc(L.mask) * L.cnt;
+  int64_t src = bigoff[bi];
   for (int64_t i = threadIdx.x; i < n_ent; i += blockDim.x)
-    out[dst + i] = SortEntry{ord_float((uint32_t)keys[src + i]), (int)vals[src + i]};
+    out[L.off + i] = SortEntry{ord_float((uint32_t)keys[src + i]), (int)vals[src + i]};
 }
 
 __global__ void k_mark_big(int nnodes, NodeArrays N, int* __restrict__ flag, int64_t* __restrict__ sz) {
   int x = blockIdx.x * blockDim.x + threadIdx.x;
-  if (x >= nnodes) return;
-  bool big = N.dirmask[x] != 0 && N.count[x] > SORT_BLOCK_MAX;
+  if (x >= 2 * nnodes) return;
+  const ListSeg L = list_seg(N, x >> 1, x & 1);
+  bool big = L.mask != 0 && L.cnt > SORT_BLOCK_MAX;
   flag[x] = big ? 1 : 0;
-  sz[x] = big ? (int64_t)__popc(N.dirmask[x]) * N.count[x] : 0;
+  sz[x] = big ? (int64_t)__popc(L.mask) * L.cnt : 0;
 }
 
-__global__ void k_compact_big(int nnodes, const int* __restrict__ flag, const int* __restrict__ idx,
-                              const int64_t* __restrict__ szscan, int* __restrict__ bignodes,
+__global__ void k_compact_big(int nseg, const int* __restrict__ flag, const int* __restrict__ idx,
+                              const int64_t* __restrict__ szscan, int* __restrict__ bigseg,
                               int64_t* __restrict__ bigoff) {
   int x = blockIdx.x * blockDim.x + threadIdx.x;
-  if (x >= nnodes || !flag[x]) return;
-  bignodes[idx[x]] = x;
+  if (x >= nseg || !flag[x]) return;
+  bigseg[idx[x]] = x;
   bigoff[idx[x]] = szscan[x];
+}
+
+// positions of the list entries, stored beside them so a sweep reads them with the
+// (coalesced) list instead of gathering through the index
+__global__ void k_list_pos(int64_t n_sorted, const SortEntry* __restrict__ sorted, const float4* __restrict__ xh,
+                           float4* __restrict__ lpos) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_sorted; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 p = xh[sorted[i].idx];
+    lpos[i] = make_float4(p.x, p.y, p.z, 0.f);
+  }
+}
+
+// Per target cell X and kind (0: A-lists for targets with tau == level, 1: R-lists for
+// deeper targets): the non-empty source lists of the 27 cells around X, as descriptors
+// with the list offset for the sweep direction, the periodic shift and Y's corner.
+struct SegDesc {   // 32 bytes
+  long long off;   // first entry of the list in the sweep direction
+  int cnt;         // entries
+  int meta;        // bits 0-4 k (slot), 5 flip, 6 self (k == 13), 7 unsorted copy (no window),
+                   // 8-13 shift codes (2 bits/axis: 1 = +1, 2 = -1), 16-19 dir
+  float cx, cy, cz;  // Y's corner + source shift (frame of the keys)
+  int Y;
+};
+
+__device__ __forceinline__ bool seg_needed(const NodeArrays& N, int X, int kind) {
+  return kind ? (N.nA[X] - N.nR[X]) > 0 : N.nR[X] > 0;
+}
+
+__global__ void k_seg_count(int nnodes, NodeArrays N, int* __restrict__ cnt2) {
+  const int X = blockIdx.x * blockDim.x + threadIdx.x;
+  if (X >= nnodes) return;
+  for (int kind = 0; kind < 2; ++kind) {
+    int c = 0;
+    if (seg_needed(N, X, kind)) {
+      for (int k = 0; k < 27; ++k) {
+        const int Y = (k == 13) ? X : N.slot[27 * (int64_t)X + k];
+        if (Y >= 0 && (kind ? N.nR[Y] : N.nA[Y]) > 0) ++c;
+      }
+    }
+    cnt2[2 * X + kind] = c;
+  }
+}
+
+__global__ void k_seg_fill(int nnodes, NodeArrays N, LevelGeom g, const int* __restrict__ off2,
+                           SegDesc* __restrict__ out) {
+  const int X = blockIdx.x * blockDim.x + threadIdx.x;
+  if (X >= nnodes) return;
+  const int4 cX = N.ijk[X];
+  const int l = cX.w;
+  for (int kind = 0; kind < 2; ++kind) {
+    if (!seg_needed(N, X, kind)) continue;
+    int o = off2[2 * X + kind];
+    for (int k = 0; k < 27; ++k) {
+      const int Y = (k == 13) ? X : N.slot[27 * (int64_t)X + k];
+      if (Y < 0) continue;
+      const ListSeg L = list_seg(N, Y, kind);
+      if (L.cnt == 0) continue;
+      int d = (k == 13) ? LIST_SELF : slot_dir(k);
+      const bool unsorted = !((L.mask >> d) & 1);    // demand too low: unsorted copy, no window
+      if (unsorted) d = LIST_SELF;
+      SegDesc sd;
+      sd.off = L.off + (long long)__popc(L.mask & ((1 << d) - 1)) * L.cnt;
+      sd.cnt = L.cnt;
+      sd.Y = Y;
+      int meta = k | (slot_flip(k) ? 32 : 0) | (k == 13 ? 64 : 0) | (unsorted ? 128 : 0) | (d << 16);
+      float so[3] = {0.f, 0.f, 0.f};
+      if (k != 13) {
+        const int4 cY = N.ijk[Y];
+        const int dd[3] = {cX.x + off_x(k) - cY.x, cX.y + off_y(k) - cY.y, cX.z + off_z(k) - cY.z};
+        for (int a = 0; a < 3; ++a) {
+          const int sa = dd[a] > 1 ? 1 : (dd[a] < -1 ? -1 : 0);
+          meta |= (sa > 0 ? 1 : (sa < 0 ? 2 : 0)) << (8 + 2 * a);
+          so[a] = sa < 0 ? -g.L[a] : 0.f;
+        }
+        sd.cx = node_corner(cY.x, l, 0, g) + so[0];
+        sd.cy = node_corner(cY.y, l, 1, g) + so[1];
+        sd.cz = node_corner(cY.z, l, 2, g) + so[2];
+      } else {
+        sd.cx = sd.cy = sd.cz = 0.f;
+      }
+      sd.meta = meta;
+      out[o++] = sd;
+    }
+  }
 }
 
 // ---------------------------------------------------------------- leaves -----
@@ -481,16 +707,25 @@ __global__ void k_write_tasks(int nnodes, const int* __restrict__ nchunk, const 
   for (int i = 0; i < c; ++i) tasks[b + i] = make_int2(x, i);
 }
 
-// per node max of the final h (force window)
-__global__ void k_node_hmax(int nnodes, NodeArrays N, const float4* __restrict__ xh) {
+// per node max of the final h over lists A and R (force window)
+__global__ void k_node_hmax(int nnodes, NodeArrays N, const float4* __restrict__ xh, const uint8_t* __restrict__ tau) {
   const int lane = threadIdx.x & 31;
   const int node = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   if (node >= nnodes) return;
-  int first = N.first[node], cnt = N.count[node];
-  float hm = 0.f;
-  for (int s = first + lane; s < first + cnt; s += 32) hm = fmaxf(hm, xh[s].w);
-  hm = warp_max_f(hm);
-  if (lane == 0) N.hmaxf[node] = hm;
+  const int first = N.first[node], cnt = N.count[node], l = N.ijk[node].w;
+  float ha = 0.f, hr = 0.f;
+  for (int s = first + lane; s < first + cnt; s += 32) {
+    const int t = tau[s];
+    const float h = xh[s].w;
+    if (t >= l) ha = fmaxf(ha, h);
+    if (t == l) hr = fmaxf(hr, h);
+  }
+  ha = warp_max_f(ha);
+  hr = warp_max_f(hr);
+  if (lane == 0) {
+    N.hmaxA[node] = ha;
+    N.hmaxR[node] = hr;
+  }
 }
 
 // initial guess from cell occupancy: N = (4 pi/3) n h^3 for uniform density n (Eq. 3)

@@ -69,19 +69,17 @@ __host__ __device__ __forceinline__ int off_z(int k) { return k % 3 - 1; }
 __host__ __device__ __forceinline__ int slot_dir(int k) { return k > 13 ? k - 14 : 12 - k; }
 __host__ __device__ __forceinline__ bool slot_flip(int k) { return k < 13; }
 
-// unit vector of canonical direction d (0..12) = offset k = d + 14
-__device__ __forceinline__ float3 dir_unit(int d) {
-  int k = d + 14;
-  float ox = (float)off_x(k), oy = (float)off_y(k), oz = (float)off_z(k);
-  float inv = rsqrtf(ox * ox + oy * oy + oz * oz);
-  return make_float3(ox * inv, oy * inv, oz * inv);
-}
+// unit vectors of the 13 canonical directions d (offset k = d + 14), computed on the host
+// once (sph_dirs_init) so every kernel uses bit-identical values
+__constant__ float c_dirs[14][3];
+__device__ __forceinline__ float3 dir_unit(int d) { return make_float3(c_dirs[d][0], c_dirs[d][1], c_dirs[d][2]); }
 
 // ---------------------------------------------------------------- constants --
 #define SPH_PI_F 3.14159265358979323846f
 #define SPH_CNORM (8.0f / SPH_PI_F)   // 8/pi of W
 #define SPH_MAX_DEPTH 10              // Morton levels below the top grid
 #define SPH_NSLOT 27
+#define SPH_COLD_MARGIN 1.3f          // extra h_build margin when h0 is the occupancy guess
 
 // ---------------------------------------------------------------- context ----
 struct DBuf {
@@ -116,7 +114,7 @@ struct sph_ctx {
   int64_t rebuilds = 0;
 
   // named device buffers
-  DBuf b[64];
+  DBuf b[96];
   cudaEvent_t ev[12];
   bool ev_ok = false;
 };
@@ -129,8 +127,9 @@ enum BufId {
   // cell-order particle arrays
   B_PERM, B_XH, B_VM, B_U, B_HB, B_HLO, B_HHI, B_FLAG, B_DSUMF, B_DACC0, B_DACC1, B_FX, B_FS,
   // nodes
-  B_N_FIRST, B_N_COUNT, B_N_IJK, B_N_PARENT, B_N_CHILD, B_N_HMAXB, B_N_SPLIT, B_N_SLOT, B_N_KEPT,
-  B_N_DIRMASK, B_N_SORTOFF, B_N_HMAXF, B_N_NCH, B_N_CHBASE, B_N_NSORT,
+  B_N_FIRST, B_N_COUNT, B_N_IJK, B_N_PARENT, B_N_CHILD, B_N_HMAXB, B_N_SPLIT, B_N_SLOT, B_N_NA,
+  B_N_NR, B_N_AMASK, B_N_RMASK, B_N_OFFA, B_N_OFFR, B_N_HMAXA, B_N_HMAXR, B_N_NCH, B_N_CHBASE, B_N_NSORT,
+  B_TAU, B_STATE_O, B_SF_O, B_ACC0_O, B_ACC1_O, B_LPOS, B_SEGCNT2, B_SEGOFF2, B_SEGDESC,
   // lists / tasks
   B_SORTED, B_TOPMAP, B_TASKS, B_TASKS2, B_TASKFLAG, B_TASKIDX, B_TMPI0, B_TMPI1, B_TMPL0, B_TMPL1,
   B_BIGNODES, B_BIGOFF,
@@ -138,7 +137,7 @@ enum BufId {
   B_COUNTERS, B_OUT0, B_OUT1, B_OUT2, B_OUT3, B_OUT4, B_OUT5,
   B_COUNT
 };
-static_assert(B_COUNT <= 64, "too many buffers");
+static_assert(B_COUNT <= 96, "too many buffers");
 
 // device counters layout (int64 slots in B_COUNTERS)
 enum CounterId {

@@ -16,12 +16,21 @@
 #pragma once
 #include "build.cuh"
 
+// per-particle h-iteration state
+#define HS_DONE 0
+#define HS_ACTIVE 1
+#define HS_PARKED 2
+
 struct TravParams {
   const int2* tasks;
   int ntasks;
   NodeArrays N;
   LevelGeom g;
   const SortEntry* sorted;
+  const float4* lpos;       // positions of the list entries
+  const SegDesc* seg;       // per (cell, kind) source-list descriptors
+  const int* segoff2;
+  const int* segcnt2;
   const uint8_t* active;   // null = all
   float slack;             // absolute window slack (fp32 rounding of keys/corners)
   unsigned long long* ctr;
@@ -35,7 +44,7 @@ struct DensOp {
   };
   const float4* __restrict__ xh;
   const float4* __restrict__ vm;
-  bool valid;
+  bool valid, act;
   int s;
   float x0, y0, z0;  // unshifted target position
   float xi, yi, zi;  // shifted for the current segment
@@ -68,13 +77,21 @@ struct DensOp {
     hinv = v ? 1.0f / hi : 0.f;
     xi = x0; yi = y0; zi = z0;
   }
-  __device__ __forceinline__ float window(const NodeArrays&, int) const { return hi; }
+  __device__ __forceinline__ float window(float) const { return hi; }
   __device__ __forceinline__ void shift(float tx, float ty, float tz) {
     xi = x0 + tx; yi = y0 + ty; zi = z0 + tz;
   }
   __device__ __forceinline__ void stage(Src& d, int j, float sx, float sy, float sz) const {
     float4 p = xh[j];
     d.a = make_float4(p.x + sx, p.y + sy, p.z + sz, 0.f);
+    d.b = vm[j];
+  }
+  // box filter support: reach of a source list, and the fields staged for survivors
+  static constexpr bool kListHmax = false;
+  __device__ __forceinline__ float reach(float hmt, float) const { return hmt; }
+  __device__ __forceinline__ float target_reach() const { return hi; }
+  __device__ __forceinline__ void stage_rest(Src& d, int j, float4 ps) const {
+    d.a = make_float4(ps.x, ps.y, ps.z, 0.f);
     d.b = vm[j];
   }
   __device__ __forceinline__ void interact(const Src& src, bool is_self) {
@@ -121,7 +138,7 @@ struct ForceOp {
   const float4* __restrict__ vm;
   const float4* __restrict__ fs;
   float alpha;
-  bool valid;
+  bool valid, act;
   int s;
   float x0, y0, z0, xi, yi, zi;
   float hi, hi2, hinv, hhat, At, rhoi, ci, fi, vxi, vyi, vzi;
@@ -154,15 +171,21 @@ struct ForceOp {
     hhat = SPH_CNORM * h2i * h2i;
     xi = x0; yi = y0; zi = z0;
   }
-  __device__ __forceinline__ float window(const NodeArrays& N, int Y) const {
-    return fmaxf(hi, N.hmaxf[Y]);
-  }
+  __device__ __forceinline__ float window(float hmax_list) const { return fmaxf(hi, hmax_list); }
   __device__ __forceinline__ void shift(float tx, float ty, float tz) {
     xi = x0 + tx; yi = y0 + ty; zi = z0 + tz;
   }
   __device__ __forceinline__ void stage(Src& d, int j, float sx, float sy, float sz) const {
     float4 p = fx[j];
     d.a = make_float4(p.x + sx, p.y + sy, p.z + sz, p.w);
+    d.b = vm[j];
+    d.c = fs[j];
+  }
+  static constexpr bool kListHmax = true;
+  __device__ __forceinline__ float reach(float hmt, float hmax_list) const { return fmaxf(hmt, hmax_list); }
+  __device__ __forceinline__ float target_reach() const { return hi; }
+  __device__ __forceinline__ void stage_rest(Src& d, int j, float4 ps) const {
+    d.a = make_float4(ps.x, ps.y, ps.z, fx[j].w);
     d.b = vm[j];
     d.c = fs[j];
   }
@@ -208,89 +231,143 @@ struct ForceOp {
 };
 
 // ------------------------------------------------------------------ traversal ----
+struct WarpBox {
+  float3 lo, hi;  // bounding box of the warp's participating targets (unshifted)
+  float hmax;     // max target window base (h_i)
+};
+
 template <class Op>
-__device__ __forceinline__ void seg_self(Op& op, int first, int cnt, typename Op::Src* sm, int lane) {
-  const int my = op.s - first;
+__device__ __forceinline__ WarpBox warp_box(const Op& op) {
+  WarpBox b;
+  b.lo = make_float3(warp_min_f(op.act ? op.x0 : INFINITY), warp_min_f(op.act ? op.y0 : INFINITY),
+                     warp_min_f(op.act ? op.z0 : INFINITY));
+  b.hi = make_float3(warp_max_f(op.act ? op.x0 : -INFINITY), warp_max_f(op.act ? op.y0 : -INFINITY),
+                     warp_max_f(op.act ? op.z0 : -INFINITY));
+  b.hmax = warp_max_f(op.act ? op.target_reach() : 0.f);
+  return b;
+}
+
+// One source list swept by the warp. windowed: sorted sweep with early exit at the first
+// entry beyond every lane's window (Lw = warp-wide limit on the key); otherwise the whole
+// list. Each chunk of 32 entries (keys, indices and positions read coalesced) is filtered
+// by a sphere/box test against the participating targets' bounding box (reach = max target
+// window, or the list's max h for the force); survivors are staged in shared memory and
+// every participating lane tests them.
+template <class Op>
+__device__ __forceinline__ void seg_list(Op& op, const TravParams& P, const WarpBox& B, int64_t off, int cnt,
+                                         bool windowed, bool flip, float Lw, float sox, float soy, float soz,
+                                         float tox, float toy, float toz, float reach, bool selfcheck,
+                                         typename Op::Src* sm, int* smj, int lane) {
+  const SortEntry* __restrict__ list = P.sorted + off;
+  const float4* __restrict__ lp = P.lpos + off;
+  const float blx = B.lo.x + tox, bly = B.lo.y + toy, blz = B.lo.z + toz;
+  const float bhx = B.hi.x + tox, bhy = B.hi.y + toy, bhz = B.hi.z + toz;
+  const float rr = fmaf(reach, 1.00001f, P.slack);
+  const float rr2 = rr * rr;
   for (int base = 0; base < cnt; base += 32) {
     const int e = base + lane;
-    if (e < cnt) op.stage(sm[lane], first + e, 0.f, 0.f, 0.f);
-    __syncwarp();
-    const int m = min(32, cnt - base);
-    if (op.valid) {
-      op.ncand += m;
-      op.nself += m;
-#pragma unroll 4
-      for (int t = 0; t < m; ++t) op.interact(sm[t], base + t == my);
-    }
-    __syncwarp();
-  }
-}
-
-template <class Op>
-__device__ __forceinline__ void seg_pair(Op& op, const TravParams& P, int X, int Y, int k, int level,
-                                         typename Op::Src* sm, int lane) {
-  const int d = slot_dir(k);
-  const bool flip = slot_flip(k);
-  const float3 du = dir_unit(d);
-  const int4 cX = P.N.ijk[X], cY = P.N.ijk[Y];
-  // periodic shift: Y's unwrapped copy sits at Y + s*L (s in {-1,0,1} per axis)
-  int ddx = cX.x + off_x(k) - cY.x, ddy = cX.y + off_y(k) - cY.y, ddz = cX.z + off_z(k) - cY.z;
-  const int sx = ddx > 1 ? 1 : (ddx < -1 ? -1 : 0);
-  const int sy = ddy > 1 ? 1 : (ddy < -1 ? -1 : 0);
-  const int sz = ddz > 1 ? 1 : (ddz < -1 ? -1 : 0);
-  // exact fp32 shifts: always subtract L from the copy that lies near L (Sterbenz)
-  const float tox = sx > 0 ? -P.g.L[0] : 0.f, toy = sy > 0 ? -P.g.L[1] : 0.f, toz = sz > 0 ? -P.g.L[2] : 0.f;
-  const float sox = sx < 0 ? -P.g.L[0] : 0.f, soy = sy < 0 ? -P.g.L[1] : 0.f, soz = sz < 0 ? -P.g.L[2] : 0.f;
-  op.shift(tox, toy, toz);
-  const float cyx = node_corner(cY.x, level, 0, P.g) + sox;
-  const float cyy = node_corner(cY.y, level, 1, P.g) + soy;
-  const float cyz = node_corner(cY.z, level, 2, P.g) + soz;
-  const float pi = proj(op.xi - cyx, op.yi - cyy, op.zi - cyz, du);   // target key in Y's frame
-  const float w = op.window(P.N, Y);
-  const float wq = fmaf(w, 1.00001f, P.slack);
-  float lim = flip ? pi - wq : pi + wq;
-  if (!op.valid) lim = flip ? INFINITY : -INFINITY;
-  const float Lw = flip ? warp_min_f(lim) : warp_max_f(lim);
-  const int nY = P.N.count[Y];
-  const int dm = P.N.dirmask[Y];
-  const SortEntry* __restrict__ list = P.sorted + P.N.sortoff[Y] + (int64_t)__popc(dm & ((1 << d) - 1)) * nY;
-  for (int base = 0; base < nY; base += 32) {
-    const int e = base + lane;
-    bool in = false;
+    bool in = false, keep = false;
     int j = 0;
-    if (e < nY) {
-      const SortEntry en = list[flip ? nY - 1 - e : e];
-      in = flip ? (en.key > Lw) : (en.key < Lw);
+    float4 ps;
+    if (e < cnt) {
+      const int ei = flip ? cnt - 1 - e : e;
+      const SortEntry en = list[ei];
+      const float4 pr = lp[ei];
+      in = !windowed || (flip ? (en.key > Lw) : (en.key < Lw));
       j = en.idx;
+      ps = make_float4(pr.x + sox, pr.y + soy, pr.z + soz, 0.f);
+      const float ex = fmaxf(fmaxf(blx - ps.x, ps.x - bhx), 0.f);
+      const float ey = fmaxf(fmaxf(bly - ps.y, ps.y - bhy), 0.f);
+      const float ez = fmaxf(fmaxf(blz - ps.z, ps.z - bhz), 0.f);
+      keep = in && fmaf(ex, ex, fmaf(ey, ey, ez * ez)) < rr2;
     }
-    const unsigned bal = __ballot_sync(FULL_MASK, in);
+    const unsigned bal_in = __ballot_sync(FULL_MASK, in);
+    const unsigned bal = __ballot_sync(FULL_MASK, keep);
     const int m = __popc(bal);
-    if (m == 0) break;
-    if (in) op.stage(sm[lane], j, sox, soy, soz);
-    __syncwarp();
-    if (op.valid) {
-      op.ncand += m;
-#pragma unroll 4
-      for (int t = 0; t < m; ++t) op.interact(sm[t], false);
+    if (keep) {
+      const int pos = __popc(bal & lanemask_lt());
+      op.stage_rest(sm[pos], j, ps);
+      smj[pos] = j;
     }
     __syncwarp();
-    if (m < 32) break;
+    if (op.act) {
+      op.ncand += m;
+      if (selfcheck) {
+        for (int t = 0; t < m; ++t) op.interact(sm[t], smj[t] == op.s);
+      } else {
+#pragma unroll 4
+        for (int t = 0; t < m; ++t) op.interact(sm[t], false);
+      }
+    }
+    __syncwarp();
+    if (__popc(bal_in) < 32) break;
   }
 }
 
+// Visit every pair of the warp's targets exactly once:
+// at each level l of the leaf's ancestor chain, targets with tau == l sweep list A of the
+// 27 cells around their level-l cell, targets with tau > l sweep list R. The cells' source
+// lists come as precomputed descriptors (k_seg_fill).
 template <class Op>
-__device__ __forceinline__ void traverse(Op& op, const TravParams& P, int leaf, typename Op::Src* sm, int lane) {
-  const int first = P.N.first[leaf], cnt = P.N.count[leaf];
-  seg_self(op, first, cnt, sm, lane);
+__device__ __forceinline__ void traverse(Op& op, const TravParams& P, const uint8_t* __restrict__ tau, int leaf,
+                                         typename Op::Src* sm, int* smj, int lane) {
+  const int ti = op.valid ? (int)tau[op.s] : -1;
+  const int tmax = (int)__reduce_max_sync(FULL_MASK, (unsigned)(ti + 1)) - 1;
   int X = leaf;
   int level = P.N.ijk[leaf].w;
   while (X >= 0) {
-    unsigned kept = (unsigned)P.N.kept[X];
-    while (kept) {
-      const int k = __ffs(kept) - 1;
-      kept &= kept - 1;
-      const int Y = P.N.slot[27 * (int64_t)X + k];
-      seg_pair(op, P, X, Y, k, level, sm, lane);
+    if (level <= tmax) {
+#pragma unroll 1
+      for (int kind = 1; kind >= 0; --kind) {   // R (deeper targets), then A (tau == l)
+        op.act = op.valid && (kind ? ti > level : ti == level);
+        if (!__any_sync(FULL_MASK, op.act)) continue;
+        const WarpBox B = warp_box(op);
+        const int s0 = P.segoff2[2 * X + kind], ns = P.segcnt2[2 * X + kind];
+#pragma unroll 1
+        for (int b0 = 0; b0 < ns; b0 += 32) {
+          SegDesc mine;
+          if (b0 + lane < ns) mine = P.seg[s0 + b0 + lane];
+          const int mseg = min(32, ns - b0);
+#pragma unroll 1
+          for (int t = 0; t < mseg; ++t) {
+            const long long off = __shfl_sync(FULL_MASK, mine.off, t);
+            const int cnt = __shfl_sync(FULL_MASK, mine.cnt, t);
+            const int meta = __shfl_sync(FULL_MASK, mine.meta, t);
+            const float cyx = __shfl_sync(FULL_MASK, mine.cx, t);
+            const float cyy = __shfl_sync(FULL_MASK, mine.cy, t);
+            const float cyz = __shfl_sync(FULL_MASK, mine.cz, t);
+            const int Y = __shfl_sync(FULL_MASK, mine.Y, t);
+            const float hl = Op::kListHmax ? (kind ? P.N.hmaxR[Y] : P.N.hmaxA[Y]) : 0.f;
+            const float reach = op.reach(B.hmax, hl);
+            if (meta & 64) {   // the cell itself: whole list, no window
+              op.shift(0.f, 0.f, 0.f);
+              seg_list(op, P, B, off, cnt, false, false, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, reach, kind == 0, sm,
+                       smj, lane);
+              continue;
+            }
+            const bool flip = (meta & 32) != 0;
+            const float3 du = dir_unit(meta >> 16);
+            const int cx = (meta >> 8) & 3, cy = (meta >> 10) & 3, cz = (meta >> 12) & 3;
+            // exact fp32 shifts: always subtract L from the copy that lies near L (Sterbenz)
+            const float tox = cx == 1 ? -P.g.L[0] : 0.f, toy = cy == 1 ? -P.g.L[1] : 0.f,
+                        toz = cz == 1 ? -P.g.L[2] : 0.f;
+            const float sox = cx == 2 ? -P.g.L[0] : 0.f, soy = cy == 2 ? -P.g.L[1] : 0.f,
+                        soz = cz == 2 ? -P.g.L[2] : 0.f;
+            op.shift(tox, toy, toz);
+            if (meta & 128) {   // unsorted copy: box filter only
+              seg_list(op, P, B, off, cnt, false, false, 0.f, sox, soy, soz, tox, toy, toz, reach, false, sm, smj,
+                       lane);
+              continue;
+            }
+            const float pi = proj(op.xi - cyx, op.yi - cyy, op.zi - cyz, du);   // target key in Y's frame
+            const float wq = fmaf(op.window(hl), 1.00001f, P.slack);
+            float lim = flip ? pi - wq : pi + wq;
+            if (!op.act) lim = flip ? INFINITY : -INFINITY;
+            const float Lw = flip ? warp_min_f(lim) : warp_max_f(lim);
+            seg_list(op, P, B, off, cnt, true, flip, Lw, sox, soy, soz, tox, toy, toz, reach, false, sm, smj, lane);
+          }
+        }
+      }
     }
     X = P.N.parent[X];
     --level;
@@ -305,9 +382,11 @@ struct DensOut {
   float4* acc1;   // curl sums xyz, count (int bits)
 };
 
-__global__ void __launch_bounds__(INTERACT_WARPS * 32) k_density(TravParams P, const float4* __restrict__ xh,
-                                                                 const float4* __restrict__ vm, DensOut out) {
+__global__ void __launch_bounds__(INTERACT_WARPS * 32, 6) k_density(TravParams P, const float4* __restrict__ xh,
+                                                                 const float4* __restrict__ vm,
+                                                                 const uint8_t* __restrict__ tau, DensOut out) {
   __shared__ DensOp::Src smem[INTERACT_WARPS][32];
+  __shared__ int smj[INTERACT_WARPS][32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int t = blockIdx.x * INTERACT_WARPS + wib;
   if (t >= P.ntasks) return;
@@ -317,13 +396,13 @@ __global__ void __launch_bounds__(INTERACT_WARPS * 32) k_density(TravParams P, c
   const int li = task.y * 32 + lane;
   const int s = first + li;
   bool v = li < cnt;
-  if (v && P.active) v = P.active[s] != 0;
+  if (v && P.active) v = P.active[s] == HS_ACTIVE;
   if (!__any_sync(FULL_MASK, v)) return;
   DensOp op;
   op.xh = xh;
   op.vm = vm;
   op.init(s, v);
-  traverse(op, P, leaf, smem[wib], lane);
+  traverse(op, P, tau, leaf, smem[wib], smj[wib], lane);
   if (v) {
     out.sf[s] = op.sf;
     out.acc0[s] = make_float4(op.smf, op.smqfp, op.sqfp, op.divs);
@@ -349,11 +428,12 @@ struct ForceOut {
   const uint32_t* perm;
 };
 
-__global__ void __launch_bounds__(INTERACT_WARPS * 32) k_force(TravParams P, const float4* __restrict__ fx,
+__global__ void __launch_bounds__(INTERACT_WARPS * 32, 5) k_force(TravParams P, const float4* __restrict__ fx,
                                                                const float4* __restrict__ vm,
                                                                const float4* __restrict__ fs, float alpha,
-                                                               ForceOut out) {
+                                                               const uint8_t* __restrict__ tau, ForceOut out) {
   __shared__ ForceOp::Src smem[INTERACT_WARPS][32];
+  __shared__ int smj[INTERACT_WARPS][32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int t = blockIdx.x * INTERACT_WARPS + wib;
   if (t >= P.ntasks) return;
@@ -369,7 +449,7 @@ __global__ void __launch_bounds__(INTERACT_WARPS * 32) k_force(TravParams P, con
   op.fs = fs;
   op.alpha = alpha;
   op.init(s, v);
-  traverse(op, P, leaf, smem[wib], lane);
+  traverse(op, P, tau, leaf, smem[wib], smj[wib], lane);
   if (v) {
     const uint32_t p = out.perm[s];
     out.a[3 * (int64_t)p] = op.ax;
@@ -395,53 +475,57 @@ __global__ void __launch_bounds__(INTERACT_WARPS * 32) k_force(TravParams P, con
 }
 
 // ------------------------------------------------------------------ h update ------
-// Bracketed Newton/bisection step on N_i(h) = (32/3) sum_j f(r_ij/h) (Eq. 3):
-// converged iff |N - n_ngb| <= tol (R3); a step that leaves the bracket [lo, hi] is
-// replaced by a cube-root rescale (no upper bracket yet) or a bisection (R4).
+// Safeguarded Newton iteration for N_i(h) = (32/3) sum_j f(r_ij/h) = n_ngb (Eq. 3,
+// P:183-185; R3, R4), the step taken in log space: h' = h (n_ngb/N)^(1/nu) with
+// nu = d ln N / d ln h = h N'/N from the same pass's sums (exact for N ~ h^nu, quadratic
+// near the root like plain Newton). Steps are clamped to [h/2, 2h] and replaced by a
+// bisection when they leave the bracket [lo, hi] of evaluated points. Converged iff
+// |N - n_ngb| <= tol. A particle whose next h exceeds the h it was binned for (h_build)
+// parks (state 2) until every other particle has converged; the cells are then rebuilt
+// once for all parked particles.
 __global__ void k_h_update(int64_t n, float4* __restrict__ xh, const float* __restrict__ hb,
-                           float* __restrict__ lo, float* __restrict__ hi, uint8_t* __restrict__ active,
+                           float* __restrict__ lo, float* __restrict__ hi, uint8_t* __restrict__ state,
                            const double* __restrict__ sf, const float4* __restrict__ acc0, float n_t,
                            float tol, unsigned long long* ctr) {
-  int unconv = 0, reb = 0;
+  int unconv = 0, parked = 0;
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n;
        s += (int64_t)gridDim.x * blockDim.x) {
-    if (!active[s]) continue;
+    if (state[s] != HS_ACTIVE) continue;
     const float h = xh[s].w;
-    const double N = (32.0 / 3.0) * sf[s];
-    const float res = (float)(N - (double)n_t);
+    const double Nd = (32.0 / 3.0) * sf[s];
+    const float N = (float)Nd;
+    const float res = (float)(Nd - (double)n_t);
     if (fabsf(res) <= tol) {
-      active[s] = 0;
+      state[s] = HS_DONE;
       continue;
     }
     float l = lo[s], u = hi[s];
     if (res < 0.f) l = h;
     else u = h;
-    if (u - l <= 4.f * (h * 1.1920929e-7f)) {   // bracket at fp32 resolution: stop
-      active[s] = 0;
-      lo[s] = l;
-      hi[s] = u;
-      continue;
-    }
-    const float dN = -(32.f / 3.f) * acc0[s].z / h;
-    float hn = h - res / dN;
-    if (!(dN > 0.f) || !(hn > l) || !(hn < u)) {
-      const float sc = cbrtf(n_t / (float)N);
-      if (isinf(u)) hn = h * fminf(2.f, fmaxf(sc * 1.05f, 1.01f));
-      else if (l == 0.f) hn = h * fmaxf(0.5f, fminf(sc * 0.95f, 0.99f));
-      else hn = 0.5f * (l + u);
-    }
-    hn = fminf(fmaxf(hn, 0.5f * h), 2.f * h);
     lo[s] = l;
     hi[s] = u;
+    if (u - l <= 4.f * (h * 1.1920929e-7f)) {   // bracket at fp32 resolution: stop
+      state[s] = HS_DONE;
+      continue;
+    }
+    const float dN = -(32.f / 3.f) * acc0[s].z / h;   // >= 0
+    const float nu = h * dN / N;
+    float hn = (nu > 0.25f) ? h * __expf(__logf(n_t / N) / nu) : (res < 0.f ? 2.f * h : 0.5f * h);
+    hn = fminf(fmaxf(hn, 0.5f * h), 2.f * h);
+    if (!(hn > l && hn < u)) hn = 0.5f * (l + u);
     xh[s].w = hn;
-    ++unconv;
-    if (hn > hb[s]) ++reb;
+    if (hn > hb[s]) {
+      state[s] = HS_PARKED;
+      ++parked;
+    } else {
+      ++unconv;
+    }
   }
   unconv = warp_sum_i(unconv);
-  reb = warp_sum_i(reb);
+  parked = warp_sum_i(parked);
   if ((threadIdx.x & 31) == 0) {
     if (unconv) atomicAdd(&ctr[C_UNCONV], (unsigned long long)unconv);
-    if (reb) atomicAdd(&ctr[C_REBUILD], (unsigned long long)reb);
+    if (parked) atomicAdd(&ctr[C_REBUILD], (unsigned long long)parked);
   }
 }
 
@@ -454,7 +538,7 @@ __global__ void k_task_active(const int2* __restrict__ tasks, int ntasks, NodeAr
   const int2 task = tasks[t];
   const int li = task.y * 32 + lane;
   const int first = N.first[task.x], cnt = N.count[task.x];
-  bool a = li < cnt && active[first + li];
+  bool a = li < cnt && active[first + li] == HS_ACTIVE;
   bool any = __any_sync(FULL_MASK, a);
   if (lane == 0) flag[t] = any ? 1 : 0;
 }
@@ -553,7 +637,8 @@ __global__ void k_gather_vmu(const uint32_t* __restrict__ perm, int64_t n, const
 
 // scatter the iteration state back to caller order before a rebuild; h_build = h * margin
 __global__ void k_scatter_state(const uint32_t* __restrict__ perm, int64_t n, const float4* __restrict__ xh,
-                                const float* __restrict__ lo, const float* __restrict__ hi, float margin,
+                                const float* __restrict__ lo, const float* __restrict__ hi,
+                                const uint8_t* __restrict__ state, float margin, float margin_parked, float hb_cap,
                                 float* __restrict__ hcur_o, float* __restrict__ lo_o, float* __restrict__ hi_o,
                                 float* __restrict__ hb_o) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n;
@@ -563,7 +648,40 @@ __global__ void k_scatter_state(const uint32_t* __restrict__ perm, int64_t n, co
     hcur_o[p] = h;
     lo_o[p] = lo[s];
     hi_o[p] = hi[s];
-    hb_o[p] = h * margin;
+    hb_o[p] = fminf(h * (state[s] == HS_PARKED ? margin_parked : margin), fmaxf(h, hb_cap));
+  }
+}
+
+// carry the density sums and states of converged particles across a rebuild (the sums at a
+// converged h do not depend on the cell structure); parked particles become active again
+__global__ void k_scatter_sums(const uint32_t* __restrict__ perm, int64_t n, const uint8_t* __restrict__ state,
+                               const double* __restrict__ sf, const float4* __restrict__ a0,
+                               const float4* __restrict__ a1, uint8_t* __restrict__ state_o,
+                               double* __restrict__ sf_o, float4* __restrict__ a0_o, float4* __restrict__ a1_o) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t p = perm[s];
+    const uint8_t st = state[s];
+    state_o[p] = st == HS_DONE ? HS_DONE : HS_ACTIVE;
+    if (st == HS_DONE) {
+      sf_o[p] = sf[s];
+      a0_o[p] = a0[s];
+      a1_o[p] = a1[s];
+    }
+  }
+}
+__global__ void k_gather_sums(const uint32_t* __restrict__ perm, int64_t n, const uint8_t* __restrict__ state_o,
+                              const double* __restrict__ sf_o, const float4* __restrict__ a0_o,
+                              const float4* __restrict__ a1_o, uint8_t* __restrict__ state, double* __restrict__ sf,
+                              float4* __restrict__ a0, float4* __restrict__ a1) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t p = perm[s];
+    const uint8_t st = state_o[p];
+    state[s] = st;
+    if (st == HS_DONE) {
+      sf[s] = sf_o[p];
+      a0[s] = a0_o[p];
+      a1[s] = a1_o[p];
+    }
   }
 }
 
@@ -576,12 +694,12 @@ __global__ void k_fill_f(float* p, int64_t n, float v) {
     p[i] = v;
 }
 // h state init from h0 (caller order): h_cur = h0, h_build = h0 * margin, bracket (0, inf)
-__global__ void k_init_h(const float* __restrict__ h0, int64_t n, float margin, float* __restrict__ hcur,
+__global__ void k_init_h(const float* __restrict__ h0, int64_t n, float margin, float hb_cap, float* __restrict__ hcur,
                          float* __restrict__ hb, float* __restrict__ lo, float* __restrict__ hi) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const float h = h0[i];
     hcur[i] = h;
-    hb[i] = h * margin;
+    hb[i] = fminf(h * margin, fmaxf(h, hb_cap));
     lo[i] = 0.f;
     hi[i] = INFINITY;
   }

@@ -169,10 +169,14 @@ static NodeArrays nodes(sph_ctx* c) {
   N.hmaxb = Bget<float>(c, B_N_HMAXB);
   N.split = Bget<int>(c, B_N_SPLIT);
   N.slot = Bget<int>(c, B_N_SLOT);
-  N.kept = Bget<int>(c, B_N_KEPT);
-  N.dirmask = Bget<int>(c, B_N_DIRMASK);
-  N.sortoff = Bget<int64_t>(c, B_N_SORTOFF);
-  N.hmaxf = Bget<float>(c, B_N_HMAXF);
+  N.nA = Bget<int>(c, B_N_NA);
+  N.nR = Bget<int>(c, B_N_NR);
+  N.amask = Bget<int>(c, B_N_AMASK);
+  N.rmask = Bget<int>(c, B_N_RMASK);
+  N.offA = Bget<int64_t>(c, B_N_OFFA);
+  N.offR = Bget<int64_t>(c, B_N_OFFR);
+  N.hmaxA = Bget<float>(c, B_N_HMAXA);
+  N.hmaxR = Bget<float>(c, B_N_HMAXR);
   return N;
 }
 
@@ -201,6 +205,12 @@ static LevelGeom level_geom(sph_ctx* c) {
   for (int k = 0; k < 3; ++k) g.L[k] = (float)c->cfg.box[k];
   g.depth = c->depth;
   return g;
+}
+
+// largest h the cells may be built for: 3 top cells per axis (with rounding slack)
+static float hb_cap(sph_ctx* c) {
+  double Lmin = std::min(c->cfg.box[0], std::min(c->cfg.box[1], c->cfg.box[2]));
+  return (float)(Lmin / (3.0 * c->cfg.top_edge_factor) * (1.0 - 1e-5));
 }
 
 static float as_float(unsigned long long b) {
@@ -315,61 +325,78 @@ static void build_structure(sph_ctx* c, bool count_only) {
   const int nlev = (int)c->lev_off.size() - 1;
   if (count_only) return;
 
-  // ---- a5 interaction slots (27 per node; 13 = self) and kept pairs
-  int* slot = B<int>(c, B_N_SLOT, 27 * (int64_t)nnodes);
-  B<int>(c, B_N_KEPT, nnodes);
-  B<int>(c, B_N_DIRMASK, nnodes);
-  B<int64_t>(c, B_N_SORTOFF, nnodes);
-  B<float>(c, B_N_HMAXF, nnodes);
-  (void)slot;
+  // ---- a5 neighbour slots (27 per node; 13 = self), interaction levels, list sizes
+  B<int>(c, B_N_SLOT, 27 * (int64_t)nnodes);
+  B<int>(c, B_N_NA, nnodes);
+  B<int>(c, B_N_NR, nnodes);
+  B<int>(c, B_N_AMASK, nnodes);
+  B<int>(c, B_N_RMASK, nnodes);
+  B<int64_t>(c, B_N_OFFA, nnodes);
+  B<int64_t>(c, B_N_OFFR, nnodes);
+  B<float>(c, B_N_HMAXA, nnodes);
+  B<float>(c, B_N_HMAXR, nnodes);
+  uint8_t* tau = B<uint8_t>(c, B_TAU, n);
   N = nodes(c);
   LAUNCH(k_top_slots, gridfull(n0, 128), 128, 0, n0, c->ntop[0], c->ntop[1], c->ntop[2], topmap, N);
   for (int l = 1; l < nlev; ++l) {
     const int a = c->lev_off[l], b = c->lev_off[l + 1];
-    LAUNCH(k_child_slots, gridfull(b - a, 128), 128, 0, a, b, g.half_min[l - 1], N);
+    LAUNCH(k_child_slots, gridfull(b - a, 128), 128, 0, a, b, N);
   }
-  int64_t* nsort = B<int64_t>(c, B_N_NSORT, nnodes);
-  for (int l = 0; l < nlev; ++l) {
-    const int a = c->lev_off[l], b = c->lev_off[l + 1];
-    LAUNCH(k_kept, gridfull(b - a, 128), 128, 0, a, b, g.half_min[l], N, nsort);
-  }
-  c->n_sorted = scan_excl<int64_t>(c, nsort, N.sortoff, nnodes);
+  LAUNCH(k_tau, gridfull((int64_t)nnodes * 32, 256), 256, 0, nnodes, N, g, hb, tau);
+  LAUNCH(k_level_counts, gridfull((int64_t)nnodes * 32, 256), 256, 0, nnodes, N, tau);
+  int64_t* nsort = B<int64_t>(c, B_N_NSORT, 2 * (int64_t)nnodes);
+  int64_t* sscan = B<int64_t>(c, B_TMPL1, 2 * (int64_t)nnodes);
+  LAUNCH(k_list_masks, gridfull(nnodes, 128), 128, 0, nnodes, N, nsort);
+  c->n_sorted = scan_excl<int64_t>(c, nsort, sscan, 2 * (int64_t)nnodes);
+  LAUNCH(k_split_offsets, gridfull(nnodes, 256), 256, 0, nnodes, sscan, N);
 
-  // ---- a6 13-direction sorted lists
+  // ---- a6 13-direction sorted lists (+ the unsorted self copy)
   SortEntry* sorted = B<SortEntry>(c, B_SORTED, c->n_sorted);
-  LAUNCH(k_sort_warp, gridfull((int64_t)nnodes * 32, 256), 256, 0, nnodes, xh, N, g, sorted);
+  LAUNCH(k_sort_warp, gridfull((int64_t)nnodes * 64, 256), 256, 0, nnodes, xh, tau, N, g, sorted);
   {
     static bool attr = false;
-    const int smem = SORT_BLOCK_MAX * (8 + 4);
+    const int smem = SORT_BLOCK_MAX * (8 + 4 + 4);
     if (!attr) {
       CUDA_TRY(cudaFuncSetAttribute(k_sort_block, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       attr = true;
     }
-    LAUNCH(k_sort_block, nnodes, 512, smem, nnodes, xh, N, g, sorted);
+    LAUNCH(k_sort_block, 2 * nnodes, 512, smem, nnodes, xh, tau, N, g, sorted);
   }
   {
-    int* bflag = B<int>(c, B_TASKFLAG, nnodes);
-    int* bidx = B<int>(c, B_TASKIDX, nnodes);
-    int64_t* bsz = B<int64_t>(c, B_TMPL0, nnodes);
-    LAUNCH(k_mark_big, gridfull(nnodes, 256), 256, 0, nnodes, N, bflag, bsz);
-    int nbig = scan_excl<int>(c, bflag, bidx, nnodes);
+    const int nseg = 2 * nnodes;
+    int* bflag = B<int>(c, B_TASKFLAG, nseg);
+    int* bidx = B<int>(c, B_TASKIDX, nseg);
+    int64_t* bsz = B<int64_t>(c, B_TMPL0, nseg);
+    LAUNCH(k_mark_big, gridfull(nseg, 256), 256, 0, nnodes, N, bflag, bsz);
+    int nbig = scan_excl<int>(c, bflag, bidx, nseg);
     if (nbig > 0) {
-      int64_t* bscan = B<int64_t>(c, B_TMPL1, nnodes);
-      int64_t nent = scan_excl<int64_t>(c, bsz, bscan, nnodes);
-      int* bignodes = B<int>(c, B_BIGNODES, nbig);
+      int64_t* bscan = B<int64_t>(c, B_TMPL1, nseg);
+      int64_t nent = scan_excl<int64_t>(c, bsz, bscan, nseg);
+      int* bigseg = B<int>(c, B_BIGNODES, nbig);
       int64_t* bigoff = B<int64_t>(c, B_BIGOFF, nbig);
-      LAUNCH(k_compact_big, gridfull(nnodes, 256), 256, 0, nnodes, bflag, bidx, bscan, bignodes, bigoff);
+      LAUNCH(k_compact_big, gridfull(nseg, 256), 256, 0, nseg, bflag, bidx, bscan, bigseg, bigoff);
       uint64_t* bk0 = B<uint64_t>(c, B_KEYS0, nent);
       uint64_t* bk1 = B<uint64_t>(c, B_KEYS1, nent);
       uint32_t* bv0 = B<uint32_t>(c, B_VALS0, nent);
       uint32_t* bv1 = B<uint32_t>(c, B_VALS1, nent);
       N = nodes(c);
-      LAUNCH(k_big_keys, nbig, 512, 0, nbig, bignodes, bigoff, xh, N, g, bk0, bv0);
+      LAUNCH(k_big_keys, nbig, 512, 0, nbig, bigseg, bigoff, xh, tau, N, g, bk0, bv0);
       int segbits = 0;
-      while ((1ll << segbits) < (int64_t)nbig * 13) ++segbits;
+      while ((1ll << segbits) < (int64_t)nbig * 14) ++segbits;
       radix_sort(c, bk0, bv0, bk1, bv1, nent, 32 + segbits);
-      LAUNCH(k_big_write, nbig, 512, 0, nbig, bignodes, bigoff, N, bk0, bv0, sorted);
+      LAUNCH(k_big_write, nbig, 512, 0, nbig, bigseg, bigoff, N, bk0, bv0, sorted);
     }
+  }
+  float4* lpos = B<float4>(c, B_LPOS, c->n_sorted);
+  LAUNCH(k_list_pos, grid1d(c, c->n_sorted, 256), 256, 0, c->n_sorted, sorted, xh, lpos);
+  {
+    int* cnt2 = B<int>(c, B_SEGCNT2, 2 * (int64_t)nnodes);
+    int* off2 = B<int>(c, B_SEGOFF2, 2 * (int64_t)nnodes);
+    LAUNCH(k_seg_count, gridfull(nnodes, 128), 128, 0, nnodes, N, cnt2);
+    const int nseg = scan_excl<int>(c, cnt2, off2, 2 * (int64_t)nnodes);
+    SegDesc* seg = B<SegDesc>(c, B_SEGDESC, nseg);
+    LAUNCH(k_seg_fill, gridfull(nnodes, 128), 128, 0, nnodes, N, g, off2, seg);
+    c->n_pair_slots = nseg;
   }
 
   // ---- leaf tasks: (leaf, chunk of 32 particles)
@@ -433,6 +460,10 @@ static TravParams trav(sph_ctx* c, const int2* tasks, int ntasks, const uint8_t*
   P.N = nodes(c);
   P.g = level_geom(c);
   P.sorted = Bget<SortEntry>(c, B_SORTED);
+  P.lpos = Bget<float4>(c, B_LPOS);
+  P.seg = Bget<SegDesc>(c, B_SEGDESC);
+  P.segoff2 = Bget<int>(c, B_SEGOFF2);
+  P.segcnt2 = Bget<int>(c, B_SEGCNT2);
   P.active = active;
   float Lmax = (float)std::max(c->cfg.box[0], std::max(c->cfg.box[1], c->cfg.box[2]));
   P.slack = 4e-7f * Lmax;
@@ -540,6 +571,17 @@ int sph_create(const sph_config* cfg, int dev, void* stream, sph_ctx** out) {
       c->own_stream = true;
     }
     for (int i = 0; i < 12; ++i) CUDA_TRY(cudaEventCreate(&c->ev[i]));
+    float dirs[14][3];
+    for (int d = 0; d < 13; ++d) {
+      const int k = d + 14;
+      const double ox = off_x(k), oy = off_y(k), oz = off_z(k);
+      const double inv = 1.0 / sqrt(ox * ox + oy * oy + oz * oz);
+      dirs[d][0] = (float)(ox * inv);
+      dirs[d][1] = (float)(oy * inv);
+      dirs[d][2] = (float)(oz * inv);
+    }
+    dirs[13][0] = dirs[13][1] = dirs[13][2] = 0.f;
+    CUDA_TRY(cudaMemcpyToSymbol(c_dirs, dirs, sizeof(dirs)));
     c->ev_ok = true;
   } catch (const SphError& e) {
     delete c;
@@ -553,7 +595,7 @@ int sph_destroy(sph_ctx* c) {
   if (!c) return SPH_E_ARG;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
-  for (int i = 0; i < 64; ++i) dev_free(c, c->b[i].p);
+  for (int i = 0; i < 96; ++i) dev_free(c, c->b[i].p);
   if (c->ev_ok)
     for (int i = 0; i < 12; ++i) cudaEventDestroy(c->ev[i]);
   if (c->own_stream) cudaStreamDestroy(c->stream);
@@ -565,7 +607,7 @@ int sph_set_allocator(sph_ctx* c, void* (*alloc)(size_t, void*, void*), void (*r
                       void* user) {
   if (!c) return SPH_E_ARG;
   if ((alloc == nullptr) != (release == nullptr)) return SPH_E_ARG;
-  for (int i = 0; i < 64; ++i)
+  for (int i = 0; i < 96; ++i)
     if (c->b[i].p) return SPH_E_STATE;
   c->ualloc = alloc;
   c->urelease = release;
@@ -617,9 +659,12 @@ int sph_build_cells(sph_ctx* ctx, int64_t n, const float* x, const float* h0) {
     LAUNCH(k_guess_h, gridfull(c->n_nodes, 128), 128, 0, c->n_nodes, nodes(c), g, Bget<uint32_t>(c, B_PERM),
            c->cfg.n_ngb, (int)c->cfg.n_ngb, (float)(0.25 * Lmin), hcur);
     if (h0) LAUNCH(k_merge_guess, grid1d(c, n, 256), 256, 0, hin, n, hcur);
-    LAUNCH(k_init_h, grid1d(c, n, 256), 256, 0, hcur, n, c->cfg.h_margin, hcur, hb, lo, hi);
+    // the occupancy guess is uncertain: bin for a wider margin so the first passes can
+    // bracket the root without a rebuild
+    LAUNCH(k_init_h, grid1d(c, n, 256), 256, 0, hcur, n, SPH_COLD_MARGIN * c->cfg.h_margin, hb_cap(c), hcur, hb,
+           lo, hi);
   } else {
-    LAUNCH(k_init_h, grid1d(c, n, 256), 256, 0, hin, n, c->cfg.h_margin, hcur, hb, lo, hi);
+    LAUNCH(k_init_h, grid1d(c, n, 256), 256, 0, hin, n, c->cfg.h_margin, hb_cap(c), hcur, hb, lo, hi);
   }
   build_structure(c, false);
   c->state = 1;
@@ -633,6 +678,7 @@ static void fill_struct_stats(sph_ctx* c, sph_stats* st) {
   st->n_levels = (int)c->lev_off.size() - 1;
   st->n_cells = c->n_nodes;
   st->n_leaves = c->n_leaves;
+  st->n_pair_slots = c->n_pair_slots;
   st->n_rebuilds = c->rebuilds;
 }
 
@@ -669,6 +715,7 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   long long unconv = n;
   bool all_tasks = true;
   long long cand_last = 0;
+  long long parked = 0;
   while (true) {
     // tasks of this pass: all, or those with an unconverged particle
     const int ntasks_all = c->n_leaves;
@@ -688,7 +735,7 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
       TravParams P = trav(c, tasks, ntasks, active);
       if (iters == 0) CUDA_TRY(cudaEventRecord(c->ev[6], c->stream));
       LAUNCH(k_density, gridfull(ntasks, INTERACT_WARPS), INTERACT_WARPS * 32, 0, P, Bget<float4>(c, B_XH), vm,
-             DensOut{sf, acc0, acc1});
+             Bget<uint8_t>(c, B_TAU), DensOut{sf, acc0, acc1});
       if (iters == 0) CUDA_TRY(cudaEventRecord(c->ev[7], c->stream));
     }
     ++iters;
@@ -702,23 +749,33 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
            Bget<float>(c, B_HLO), Bget<float>(c, B_HHI), active, sf, acc0, c->cfg.n_ngb, c->cfg.n_ngb_tol, ctr(c));
     ctr_read(c, hc);
     if (iters == 1) cand_last = (long long)hc[C_CAND];
-    unconv = (long long)hc[C_UNCONV];
-    DBG("density pass %d: tasks %d cand %llu (self %llu) -> unconverged %lld rebuild %llu\n", iters, ntasks,
-        hc[C_CAND], hc[C_TMP1], unconv, hc[C_REBUILD]);
+    parked += (long long)hc[C_REBUILD];
+    unconv = (long long)hc[C_UNCONV] + parked;
+    DBG("density pass %d: tasks %d cand %llu -> active %llu parked %lld\n", iters, ntasks, hc[C_CAND],
+        hc[C_UNCONV], parked);
     if (unconv == 0) break;
     all_tasks = false;
-    if (hc[C_REBUILD] > 0) {
-      // an h wants to outgrow the cells it was binned for: re-bin everything for
-      // h_build = h * margin, keeping h and its bracket
+    if (hc[C_UNCONV] == 0 && parked > 0) {
+      // every other particle has converged; the parked ones want an h beyond the cells they
+      // were binned for: re-bin everything (h_build = h * margin, parked ones with a wider
+      // margin), keep h, its bracket and the converged particles' sums, and continue with the
+      // parked ones only
       LAUNCH(k_scatter_state, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, Bget<float4>(c, B_XH),
-             Bget<float>(c, B_HLO), Bget<float>(c, B_HHI), c->cfg.h_margin, Bget<float>(c, B_HCUR_O),
-             Bget<float>(c, B_LO_O), Bget<float>(c, B_HI_O), Bget<float>(c, B_HB_ORIG));
+             Bget<float>(c, B_HLO), Bget<float>(c, B_HHI), active, c->cfg.h_margin, 2.0f * c->cfg.h_margin, hb_cap(c),
+             Bget<float>(c, B_HCUR_O), Bget<float>(c, B_LO_O), Bget<float>(c, B_HI_O), Bget<float>(c, B_HB_ORIG));
+      uint8_t* st_o = B<uint8_t>(c, B_STATE_O, n);
+      double* sf_o = B<double>(c, B_SF_O, n);
+      float4* a0_o = B<float4>(c, B_ACC0_O, n);
+      float4* a1_o = B<float4>(c, B_ACC1_O, n);
+      LAUNCH(k_scatter_sums, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, active, sf, acc0, acc1, st_o,
+             sf_o, a0_o, a1_o);
       build_structure(c, false);
       c->rebuilds++;
+      parked = 0;
       vm = Bget<float4>(c, B_VM);
       LAUNCH(k_gather_vmu, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, vd, md, ud, vm, uc);
-      LAUNCH(k_fill_u8, grid1d(c, n, 256), 256, 0, active, n, (uint8_t)1);
-      all_tasks = true;
+      LAUNCH(k_gather_sums, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, st_o, sf_o, a0_o, a1_o, active,
+             sf, acc0, acc1);
     }
   }
   // ghost: finalise and write the caller-order outputs
@@ -736,7 +793,8 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   ctr_reset(c);
   LAUNCH(k_ghost, grid1d(c, n, 256), 256, 0, n, Bget<float4>(c, B_XH), uc, sf, acc0, acc1, c->cfg.gamma,
          c->cfg.balsara_eps, fx, fs, go, ctr(c));
-  LAUNCH(k_node_hmax, gridfull((int64_t)c->n_nodes * 32, 256), 256, 0, c->n_nodes, nodes(c), Bget<float4>(c, B_XH));
+  LAUNCH(k_node_hmax, gridfull((int64_t)c->n_nodes * 32, 256), 256, 0, c->n_nodes, nodes(c), Bget<float4>(c, B_XH),
+         Bget<uint8_t>(c, B_TAU));
   flush_out(c, maps, c->ev[3]);
   c->state = 2;
   int status = (unconv > 0 && iters >= c->cfg.max_h_iter) ? SPH_E_NOCONV : SPH_OK;
@@ -785,7 +843,7 @@ int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out, int3
   TravParams P = trav(c, Bget<int2>(c, B_TASKS), c->n_leaves, nullptr);
   CUDA_TRY(cudaEventRecord(c->ev[8], c->stream));
   LAUNCH(k_force, gridfull(c->n_leaves, INTERACT_WARPS), INTERACT_WARPS * 32, 0, P, Bget<float4>(c, B_FX),
-         Bget<float4>(c, B_VM), Bget<float4>(c, B_FS), c->cfg.alpha, fo);
+         Bget<float4>(c, B_VM), Bget<float4>(c, B_FS), c->cfg.alpha, Bget<uint8_t>(c, B_TAU), fo);
   CUDA_TRY(cudaEventRecord(c->ev[9], c->stream));
   flush_out(c, maps, c->ev[5]);
   if (st || (c->cfg.flags & SPH_F_SYNC)) {

@@ -10,7 +10,9 @@ ns = int(sys.argv[2]) if len(sys.argv) > 2 else 2000
 p = workloads.make(name) if not name.startswith("tiny") else workloads.tiny(int(name[4:]), n=4000, clump_frac=0.3, n_dup=5)
 if name.startswith("tiny"): p.h0[:] = 0
 t0 = time.time()
-g = P.run_gpu(p)
+import json
+cfgkw = json.loads(os.environ.get("SPH_DBG_CFG", "{}"))
+g = P.run_gpu(p, **cfgkw)
 print(name, "gpu wall", time.time() - t0, flush=True)
 print("density stats", g["stats_density"])
 print("force stats", g["stats_force"])
