@@ -77,6 +77,10 @@ typedef struct {
   float top_edge_factor; /* kappa >= 1: top cell edge >= kappa * max h ("larger or equal") */
   float h_margin;        /* >= 1: cells are built for h_build = h * h_margin so the Newton
                             iteration can grow h without a rebuild */
+  int32_t sort_min_len;  /* a cell's source list is kept presorted along a pair direction only
+                            if it is longer than this and enough targets sweep it; shorter lists
+                            are swept whole (box filter only). 0 = presort every swept
+                            direction (P:687-698 verbatim) */
   uint32_t flags;        /* SPH_F_* */
   int32_t rank, nranks;  /* 0, 1 for a single GPU */
   double slab_lo, slab_hi; /* owned x-range of this rank (multi-GPU) */

@@ -42,7 +42,7 @@ struct NodeArrays {
   int* nR;          // #{i in cell : tau_i == level}   (list R)
   int* amask;       // 14-bit: directions 0..12 (+ bit 13 unsorted) of list A that are needed
   int* rmask;       // 14-bit, list R
-  int64_t* offA;    // offsets of the node's A / R blocks in the list array
+  int64_t* offA;    // offsets of the node's A / R blocks in the list array (see k_list_masks)
   int64_t* offR;
   float* hmaxA;     // max final h over list A / R (force window)
   float* hmaxR;
@@ -329,14 +329,19 @@ __global__ void k_level_counts(int nnodes, NodeArrays N, const uint8_t* __restri
 
 // which lists a cell must provide as a source: its neighbour X (or itself, bit 13) sweeps
 // list A of this cell if X has targets with tau == l, list R if X has targets with tau > l.
-// A direction is sorted only if enough targets sweep it (or the list is tiny): otherwise
-// the sweeping warps read the unsorted copy (bit 13) with the box filter alone, which is
-// cheaper than sorting a list that one or two warps visit.
+// A direction is stored presorted only if the list is longer than sort_min_len
+// and at least SORT_DEMAND_MIN targets sweep it; otherwise the sweeping warps read the whole
+// list with the box filter alone: a warp stages 32 sources at a time, so a sorted window
+// cannot save anything on a list of a few chunks, and sorting a list that one or two warps
+// visit costs more than it saves. An unsorted sweep reads a compacted copy (bit 13), or,
+// when every particle of the cell is a member (bit 14), the cell's own contiguous range.
 #define SORT_DEMAND_MIN 64
-__global__ void k_list_masks(int nnodes, NodeArrays N, int64_t* __restrict__ nsort /*[2*nnodes]*/) {
+#define LIST_RANGE 14
+__global__ void k_list_masks(int nnodes, NodeArrays N, int sort_min_len, int64_t* __restrict__ nsort /*[2*nnodes]*/) {
   const int y = blockIdx.x * blockDim.x + threadIdx.x;
   if (y >= nnodes) return;
-  const int na = N.nA[y], nr = N.nR[y];
+  const int na = N.nA[y], nr = N.nR[y], cnt = N.count[y];
+  (void)cnt;
   int demA[14], demR[14];
 #pragma unroll
   for (int d = 0; d < 14; ++d) demA[d] = demR[d] = 0;
@@ -347,16 +352,27 @@ __global__ void k_list_masks(int nnodes, NodeArrays N, int64_t* __restrict__ nso
     demA[d] += N.nR[x];
     demR[d] += N.nA[x] - N.nR[x];
   }
+  const int uR = (nr == cnt) ? (1 << LIST_RANGE) : (1 << LIST_SELF);
   int am = 0, rm = 0;
 #pragma unroll
   for (int d = 0; d < 14; ++d) {
-    if (na > 0 && demA[d] > 0) am |= (d == LIST_SELF || demA[d] >= SORT_DEMAND_MIN || na <= 32) ? (1 << d) : (1 << LIST_SELF);
-    if (nr > 0 && demR[d] > 0) rm |= (d == LIST_SELF || demR[d] >= SORT_DEMAND_MIN || nr <= 32) ? (1 << d) : (1 << LIST_SELF);
+    // list A (tau >= l) is never stored: it is swept as the cell's own range, culled down its
+    // sub-cells to the targets' reach and filtered by tau (cull_range) -- a 3D filter that
+    // beats a 1D projection window, so sorting it would not pay.
+    // With sort_min_len == 0 it is presorted along every swept direction (paper-literal).
+    if (na > 0 && demA[d] > 0) {
+      const bool srt = d != LIST_SELF && sort_min_len == 0;
+      am |= srt ? (1 << d) : (1 << LIST_RANGE);
+    }
+    if (nr > 0 && demR[d] > 0) {
+      const bool srt = d != LIST_SELF && (sort_min_len == 0 || (demR[d] >= SORT_DEMAND_MIN && nr > sort_min_len));
+      rm |= srt ? (1 << d) : uR;
+    }
   }
   N.amask[y] = am;
   N.rmask[y] = rm;
-  nsort[2 * (int64_t)y] = (int64_t)__popc(am) * na;
-  nsort[2 * (int64_t)y + 1] = (int64_t)__popc(rm) * nr;
+  nsort[2 * (int64_t)y] = (int64_t)__popc(am & 0x3fff) * na;
+  nsort[2 * (int64_t)y + 1] = (int64_t)__popc(rm & 0x3fff) * nr;
 }
 
 __global__ void k_split_offsets(int nnodes, const int64_t* __restrict__ scan2, NodeArrays N) {
@@ -398,7 +414,7 @@ __global__ void k_sort_warp(int nnodes, const float4* __restrict__ xh, const uin
   if (node >= nnodes) return;
   const ListSeg L = list_seg(N, node, kind);
   const int cnt_node = N.count[node];
-  if (L.mask == 0 || L.cnt == 0 || cnt_node > 32) return;
+  if ((L.mask & 0x3fff) == 0 || L.cnt == 0 || cnt_node > 32) return;
   const int first = N.first[node];
   const int4 c = N.ijk[node];
   float rx = 0.f, ry = 0.f, rz = 0.f;
@@ -472,7 +488,7 @@ __global__ void __launch_bounds__(512) k_sort_block(int nnodes, const float4* __
   if (node >= nnodes) return;
   const ListSeg L = list_seg(N, node, kind);
   const int cnt_node = N.count[node];
-  if (L.mask == 0 || L.cnt == 0 || cnt_node <= 32 || L.cnt > SORT_BLOCK_MAX) return;
+  if ((L.mask & 0x3fff) == 0 || L.cnt == 0 || cnt_node <= 32 || L.cnt > SORT_BLOCK_MAX) return;
   const int first = N.first[node];
   const int4 c = N.ijk[node];
   block_compact_members(first, cnt_node, c.w, kind, tau, mem, SORT_BLOCK_MAX, wsum);
@@ -584,7 +600,7 @@ __global__ void k_big_write(int nbig, const int* __restrict__ bigseg, const int6
   int bi = blockIdx.x;
   if (bi >= nbig) return;
   const ListSeg L = list_seg(N, bigseg[bi] >> 1, bigseg[bi] & 1);
-  int64_t n_ent = (int64_t)__popc(L.mask) * L.cnt;
+  int64_t n_ent = (int64_t)__popc(L.mask & 0x3fff) * L.cnt;
   int64_t src = bigoff[bi];
   for (int64_t i = threadIdx.x; i < n_ent; i += blockDim.x)
     out[L.off + i] = SortEntry{ord_float((uint32_t)keys[src + i]), (int)vals[src + i]};
@@ -594,9 +610,9 @@ __global__ void k_mark_big(int nnodes, NodeArrays N, int* __restrict__ flag, int
   int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= 2 * nnodes) return;
   const ListSeg L = list_seg(N, x >> 1, x & 1);
-  bool big = L.mask != 0 && L.cnt > SORT_BLOCK_MAX;
+  bool big = (L.mask & 0x3fff) != 0 && L.cnt > SORT_BLOCK_MAX;
   flag[x] = big ? 1 : 0;
-  sz[x] = big ? (int64_t)__popc(L.mask) * L.cnt : 0;
+  sz[x] = big ? (int64_t)__popc(L.mask & 0x3fff) * L.cnt : 0;
 }
 
 __global__ void k_compact_big(int nseg, const int* __restrict__ flag, const int* __restrict__ idx,
@@ -608,24 +624,15 @@ __global__ void k_compact_big(int nseg, const int* __restrict__ flag, const int*
   bigoff[idx[x]] = szscan[x];
 }
 
-// positions of the list entries, stored beside them so a sweep reads them with the
-// (coalesced) list instead of gathering through the index
-__global__ void k_list_pos(int64_t n_sorted, const SortEntry* __restrict__ sorted, const float4* __restrict__ xh,
-                           float4* __restrict__ lpos) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_sorted; i += (int64_t)gridDim.x * blockDim.x) {
-    const float4 p = xh[sorted[i].idx];
-    lpos[i] = make_float4(p.x, p.y, p.z, 0.f);
-  }
-}
-
 // Per target cell X and kind (0: A-lists for targets with tau == level, 1: R-lists for
 // deeper targets): the non-empty source lists of the 27 cells around X, as descriptors
 // with the list offset for the sweep direction, the periodic shift and Y's corner.
 struct SegDesc {   // 32 bytes
   long long off;   // first entry of the list in the sweep direction
   int cnt;         // entries
-  int meta;        // bits 0-4 k (slot), 5 flip, 6 self (k == 13), 7 unsorted copy (no window),
-                   // 8-13 shift codes (2 bits/axis: 1 = +1, 2 = -1), 16-19 dir
+  int meta;        // bits 0-4 k (slot), 5 flip, 6 self (k == 13), 7 swept whole (no window),
+                   // 8-13 shift codes (2 bits/axis: 1 = +1, 2 = -1), 14 list = cell range,
+                   // 15 range holds non-members (keep tau >= level only), 16-19 dir
   float cx, cy, cz;  // Y's corner + source shift (frame of the keys)
   int Y;
 };
@@ -664,13 +671,16 @@ __global__ void k_seg_fill(int nnodes, NodeArrays N, LevelGeom g, const int* __r
       const ListSeg L = list_seg(N, Y, kind);
       if (L.cnt == 0) continue;
       int d = (k == 13) ? LIST_SELF : slot_dir(k);
-      const bool unsorted = !((L.mask >> d) & 1);    // demand too low: unsorted copy, no window
+      const bool unsorted = (d == LIST_SELF) || !((L.mask >> d) & 1);   // swept whole, no window
+      const bool range = unsorted && ((L.mask >> LIST_RANGE) & 1);       // = the cell's own range
+      const bool tfilter = range && kind == 0 && N.nA[Y] != N.count[Y];  // range holds non-members
       if (unsorted) d = LIST_SELF;
       SegDesc sd;
-      sd.off = L.off + (long long)__popc(L.mask & ((1 << d) - 1)) * L.cnt;
-      sd.cnt = L.cnt;
+      sd.off = range ? (long long)N.first[Y] : L.off + (long long)__popc(L.mask & ((1 << d) - 1)) * L.cnt;
+      sd.cnt = range ? N.count[Y] : L.cnt;
       sd.Y = Y;
-      int meta = k | (slot_flip(k) ? 32 : 0) | (k == 13 ? 64 : 0) | (unsorted ? 128 : 0) | (d << 16);
+      int meta = k | (slot_flip(k) ? 32 : 0) | (k == 13 ? 64 : 0) | (unsorted ? 128 : 0) | (range ? (1 << 14) : 0) |
+                 (tfilter ? (1 << 15) : 0) | (d << 16);
       float so[3] = {0.f, 0.f, 0.f};
       if (k != 13) {
         const int4 cY = N.ijk[Y];
@@ -692,19 +702,20 @@ __global__ void k_seg_fill(int nnodes, NodeArrays N, LevelGeom g, const int* __r
   }
 }
 
-// ---------------------------------------------------------------- leaves -----
+// ---------------------------------------------------------------- tasks ------
+// Work unit of the interaction kernels: a leaf cell's particles in chunks of 32 (cell order).
 __global__ void k_leaf_chunks(int nnodes, NodeArrays N, int* __restrict__ nchunk) {
   int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= nnodes) return;
   nchunk[x] = N.split[x] ? 0 : (N.count[x] + 31) >> 5;
 }
 
-__global__ void k_write_tasks(int nnodes, const int* __restrict__ nchunk, const int* __restrict__ scan,
-                              int2* __restrict__ tasks) {
+__global__ void k_write_tasks(int nnodes, NodeArrays N, const int* __restrict__ nchunk, const int* __restrict__ scan,
+                              int4* __restrict__ tasks) {
   int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= nnodes) return;
-  int c = nchunk[x], b = scan[x];
-  for (int i = 0; i < c; ++i) tasks[b + i] = make_int2(x, i);
+  const int c = nchunk[x], b = scan[x], first = N.first[x], cnt = N.count[x];
+  for (int i = 0; i < c; ++i) tasks[b + i] = make_int4(x, first + 32 * i, min(32, cnt - 32 * i), 0);
 }
 
 // per node max of the final h over lists A and R (force window)

@@ -112,6 +112,7 @@ struct sph_ctx {
   int64_t n_sorted = 0;      // entries of all 13-direction lists
   int64_t n_pair_slots = 0;
   int64_t rebuilds = 0;
+  float margin_used = 1.1f;  // h_build / h of the current structure
 
   // named device buffers
   DBuf b[96];
@@ -129,7 +130,7 @@ enum BufId {
   // nodes
   B_N_FIRST, B_N_COUNT, B_N_IJK, B_N_PARENT, B_N_CHILD, B_N_HMAXB, B_N_SPLIT, B_N_SLOT, B_N_NA,
   B_N_NR, B_N_AMASK, B_N_RMASK, B_N_OFFA, B_N_OFFR, B_N_HMAXA, B_N_HMAXR, B_N_NCH, B_N_CHBASE, B_N_NSORT,
-  B_TAU, B_STATE_O, B_SF_O, B_ACC0_O, B_ACC1_O, B_LPOS, B_SEGCNT2, B_SEGOFF2, B_SEGDESC,
+  B_TAU, B_DSUM2, B_STATE_O, B_SF_O, B_ACC0_O, B_ACC1_O, B_SEGCNT2, B_SEGOFF2, B_SEGDESC,
   // lists / tasks
   B_SORTED, B_TOPMAP, B_TASKS, B_TASKS2, B_TASKFLAG, B_TASKIDX, B_TMPI0, B_TMPI1, B_TMPL0, B_TMPL1,
   B_BIGNODES, B_BIGOFF,

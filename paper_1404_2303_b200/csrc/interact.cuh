@@ -19,20 +19,22 @@
 // per-particle h-iteration state
 #define HS_DONE 0
 #define HS_ACTIVE 1
-#define HS_PARKED 2
+#define HS_PARKED 2   // wants h beyond the top cells: waits for a rebuild
+#define HS_COARSE 3   // h beyond its cells' h_build: evaluated over the 27 top cells (coarse_gather)
 
 struct TravParams {
-  const int2* tasks;
+  const uint8_t* tau;       // interaction level per particle (cell order)
+  const int4* tasks;        // {leaf cell, first particle (cell order), count <= 32, -}
   int ntasks;
   NodeArrays N;
   LevelGeom g;
   const SortEntry* sorted;
-  const float4* lpos;       // positions of the list entries
   const SegDesc* seg;       // per (cell, kind) source-list descriptors
   const int* segoff2;
   const int* segcnt2;
   const uint8_t* active;   // null = all
   float slack;             // absolute window slack (fp32 rounding of keys/corners)
+  int dbg_skip;             // debug only: bit k skips kind k (wrong results; timing experiments)
   unsigned long long* ctr;
 };
 
@@ -51,15 +53,17 @@ struct DensOp {
   float hi, hi2, hinv, vxi, vyi, vzi;
   double sf;
   float smf, smqfp, sqfp, divs, crx, cry, crz;
+  float sq2fpp;        // sum q^2 f''(q): second derivative of N(h) for the Halley step
   int cnt;
-  long long ncand, nself;
+  long long ncand, nself, nseg, nchunk;
 
   __device__ __forceinline__ void init(int s_, bool v) {
     s = s_;
     valid = v;
-    nself = 0;
+    nself = nseg = nchunk = 0;
     sf = 0.0;
     smf = smqfp = sqfp = divs = crx = cry = crz = 0.f;
+    sq2fpp = 0.f;
     cnt = 0;
     ncand = 0;
     if (v) {
@@ -90,9 +94,14 @@ struct DensOp {
   static constexpr bool kListHmax = false;
   __device__ __forceinline__ float reach(float hmt, float) const { return hmt; }
   __device__ __forceinline__ float target_reach() const { return hi; }
+  __device__ __forceinline__ float4 src_pos(int j) const { return xh[j]; }
   __device__ __forceinline__ void stage_rest(Src& d, int j, float4 ps) const {
     d.a = make_float4(ps.x, ps.y, ps.z, 0.f);
     d.b = vm[j];
+  }
+  __device__ __forceinline__ bool test(const Src& src) const {
+    const float dx = xi - src.a.x, dy = yi - src.a.y, dz = zi - src.a.z;
+    return fmaf(dx, dx, fmaf(dy, dy, dz * dz)) < hi2;
   }
   __device__ __forceinline__ void interact(const Src& src, bool is_self) {
     const float dx = xi - src.a.x, dy = yi - src.a.y, dz = zi - src.a.z;
@@ -101,17 +110,20 @@ struct DensOp {
       const float rinv = r2 > 0.f ? rsqrtf(r2) : 0.f;
       const float r = r2 * rinv;
       const float q = r * hinv;
-      float f, fp;
+      float f, fp, fpp;
       if (q <= 0.5f) {
         f = fmaf(q * q, fmaf(6.f, q, -6.f), 1.f);
         fp = q * fmaf(18.f, q, -12.f);
+        fpp = fmaf(36.f, q, -12.f);
       } else {
         const float t = 1.f - q;
         f = 2.f * t * t * t;
         fp = -6.f * t * t;
+        fpp = 12.f * t;
       }
       const float mj = src.b.w;
       sf += (double)f;
+      sq2fpp = fmaf(q * q, fpp, sq2fpp);
       smf = fmaf(mj, f, smf);
       const float qfp = q * fp;
       sqfp += qfp;
@@ -144,12 +156,12 @@ struct ForceOp {
   float hi, hi2, hinv, hhat, At, rhoi, ci, fi, vxi, vyi, vzi;
   float ax, ay, az, du, vsig;
   int cnt;
-  long long ncand, nself;
+  long long ncand, nself, nseg, nchunk;
 
   __device__ __forceinline__ void init(int s_, bool v) {
     s = s_;
     valid = v;
-    nself = 0;
+    nself = nseg = nchunk = 0;
     ax = ay = az = du = vsig = 0.f;
     cnt = 0;
     ncand = 0;
@@ -184,8 +196,9 @@ struct ForceOp {
   static constexpr bool kListHmax = true;
   __device__ __forceinline__ float reach(float hmt, float hmax_list) const { return fmaxf(hmt, hmax_list); }
   __device__ __forceinline__ float target_reach() const { return hi; }
+  __device__ __forceinline__ float4 src_pos(int j) const { return fx[j]; }
   __device__ __forceinline__ void stage_rest(Src& d, int j, float4 ps) const {
-    d.a = make_float4(ps.x, ps.y, ps.z, fx[j].w);
+    d.a = ps;
     d.b = vm[j];
     d.c = fs[j];
   }
@@ -193,6 +206,11 @@ struct ForceOp {
     if (q <= 0.5f) return q * fmaf(18.f, q, -12.f);
     const float t = 1.f - q;
     return -6.f * t * t;
+  }
+  __device__ __forceinline__ bool test(const Src& src) const {
+    const float dx = xi - src.a.x, dy = yi - src.a.y, dz = zi - src.a.z;
+    const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    return r2 < hi2 || r2 * (src.a.w * src.a.w) < 1.0f;
   }
   __device__ __forceinline__ void interact(const Src& src, bool is_self) {
     const float dx = xi - src.a.x, dy = yi - src.a.y, dz = zi - src.a.z;
@@ -255,27 +273,33 @@ __device__ __forceinline__ WarpBox warp_box(const Op& op) {
 // every participating lane tests them.
 template <class Op>
 __device__ __forceinline__ void seg_list(Op& op, const TravParams& P, const WarpBox& B, int64_t off, int cnt,
-                                         bool windowed, bool flip, float Lw, float sox, float soy, float soz,
-                                         float tox, float toy, float toz, float reach, bool selfcheck,
+                                         bool windowed, bool range, bool flip, float Lw, float sox, float soy,
+                                         float soz, float tox, float toy, float toz, float reach, bool selfcheck,
                                          typename Op::Src* sm, int* smj, int lane) {
   const SortEntry* __restrict__ list = P.sorted + off;
-  const float4* __restrict__ lp = P.lpos + off;
   const float blx = B.lo.x + tox, bly = B.lo.y + toy, blz = B.lo.z + toz;
   const float bhx = B.hi.x + tox, bhy = B.hi.y + toy, bhz = B.hi.z + toz;
   const float rr = fmaf(reach, 1.00001f, P.slack);
   const float rr2 = rr * rr;
+  op.nseg += 1;
   for (int base = 0; base < cnt; base += 32) {
+    op.nchunk += 1;
     const int e = base + lane;
     bool in = false, keep = false;
     int j = 0;
     float4 ps;
     if (e < cnt) {
-      const int ei = flip ? cnt - 1 - e : e;
-      const SortEntry en = list[ei];
-      const float4 pr = lp[ei];
-      in = !windowed || (flip ? (en.key > Lw) : (en.key < Lw));
-      j = en.idx;
-      ps = make_float4(pr.x + sox, pr.y + soy, pr.z + soz, 0.f);
+      if (range) {                       // the cell's own contiguous range (cell order)
+        j = (int)off + e;
+        in = true;
+      } else {
+        const int ei = flip ? cnt - 1 - e : e;
+        const SortEntry en = list[ei];
+        in = !windowed || (flip ? (en.key > Lw) : (en.key < Lw));
+        j = en.idx;
+      }
+      const float4 pr = op.src_pos(j);
+      ps = make_float4(pr.x + sox, pr.y + soy, pr.z + soz, pr.w);
       const float ex = fmaxf(fmaxf(blx - ps.x, ps.x - bhx), 0.f);
       const float ey = fmaxf(fmaxf(bly - ps.y, ps.y - bhy), 0.f);
       const float ez = fmaxf(fmaxf(blz - ps.z, ps.z - bhz), 0.f);
@@ -291,12 +315,16 @@ __device__ __forceinline__ void seg_list(Op& op, const TravParams& P, const Warp
     }
     __syncwarp();
     if (op.act) {
+      // two phases: distance tests of all staged sources into a hit mask, then the
+      // interaction body only for the hits (a lane's misses cost no body instructions)
       op.ncand += m;
-      if (selfcheck) {
-        for (int t = 0; t < m; ++t) op.interact(sm[t], smj[t] == op.s);
-      } else {
+      unsigned hm = 0u;
 #pragma unroll 4
-        for (int t = 0; t < m; ++t) op.interact(sm[t], false);
+      for (int t = 0; t < m; ++t) hm |= (unsigned)op.test(sm[t]) << t;
+      while (hm) {
+        const int t = __ffs(hm) - 1;
+        hm &= hm - 1;
+        op.interact(sm[t], selfcheck && smj[t] == op.s);
       }
     }
     __syncwarp();
@@ -304,15 +332,285 @@ __device__ __forceinline__ void seg_list(Op& op, const TravParams& P, const Warp
   }
 }
 
+// Whole-cell ranges swept as one flattened stream: the sub-cell ranges collected by the
+// culling descent (cull_range) are streamed in chunks of 32 without per-range set-up.
+#define RBUF 64
+struct WarpSmemT {
+  SegDesc sd[27];
+  int rs[RBUF];        // range starts (cell order)
+  int rc[RBUF + 1];    // exclusive prefix of range counts
+  int rcode[RBUF];     // target shift code (bits 0-2) | self check (bit 3) | source shift (bits 4-6) |
+                       // tau filter (bit 7, keep tau >= bits 8-11)
+  float rreach[RBUF];  // reach of the range's list (force: includes the list's max h)
+  int stk[96];
+  int nr;
+};
+
+template <class Op>
+__device__ __forceinline__ void flush_ranges(Op& op, const TravParams& P, const WarpBox& B, WarpSmemT& W, float reach,
+                                             typename Op::Src* sm, int* smj, int* smc, int lane) {
+  const int nr = W.nr;
+  if (nr == 0) return;
+  // exclusive prefix of the (<= 64) range counts
+  int c0 = lane < nr ? W.rc[lane] : 0, c1 = lane + 32 < nr ? W.rc[lane + 32] : 0;
+  int i0 = c0, i1 = c1;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y0 = __shfl_up_sync(FULL_MASK, i0, o), y1 = __shfl_up_sync(FULL_MASK, i1, o);
+    if (lane >= o) { i0 += y0; i1 += y1; }
+  }
+  const int t0 = __shfl_sync(FULL_MASK, i0, 31);
+  __syncwarp();
+  if (lane < nr) W.rc[lane] = i0 - c0;
+  if (lane + 32 < nr) W.rc[lane + 32] = t0 + i1 - c1;
+  const int total = t0 + __shfl_sync(FULL_MASK, i1, 31);
+  if (lane == 0) W.rc[nr] = total;
+  __syncwarp();
+  (void)reach;
+  op.nseg += 1;
+  for (int base = 0; base < total; base += 32) {
+    op.nchunk += 1;
+    const int g = base + lane;
+    bool keep = false;
+    int j = 0, code = 0;
+    float4 ps;
+    if (g < total) {
+      int t = 0;                               // range of entry g: rc[t] <= g < rc[t+1]
+#pragma unroll
+      for (int step = 32; step > 0; step >>= 1)
+        if (t + step < nr && W.rc[t + step] <= g) t += step;
+      j = W.rs[t] + (g - W.rc[t]);
+      code = W.rcode[t];
+      const float rrt = fmaf(W.rreach[t], 1.00001f, P.slack);
+      const float sox = (code & 16) ? -P.g.L[0] : 0.f, soy = (code & 32) ? -P.g.L[1] : 0.f,
+                  soz = (code & 64) ? -P.g.L[2] : 0.f;
+      const float tox = (code & 1) ? -P.g.L[0] : 0.f, toy = (code & 2) ? -P.g.L[1] : 0.f,
+                  toz = (code & 4) ? -P.g.L[2] : 0.f;
+      const float4 pr = op.src_pos(j);
+      ps = make_float4(pr.x + sox, pr.y + soy, pr.z + soz, pr.w);
+      const float ex = fmaxf(fmaxf(B.lo.x + tox - ps.x, ps.x - (B.hi.x + tox)), 0.f);
+      const float ey = fmaxf(fmaxf(B.lo.y + toy - ps.y, ps.y - (B.hi.y + toy)), 0.f);
+      const float ez = fmaxf(fmaxf(B.lo.z + toz - ps.z, ps.z - (B.hi.z + toz)), 0.f);
+      keep = fmaf(ex, ex, fmaf(ey, ey, ez * ez)) < rrt * rrt;
+      if (keep && (code & 128)) keep = (int)P.tau[j] >= ((code >> 8) & 15);   // list A membership
+    }
+    const unsigned bal = __ballot_sync(FULL_MASK, keep);
+    const int m = __popc(bal);
+    if (keep) {
+      const int pos = __popc(bal & lanemask_lt());
+      op.stage_rest(sm[pos], j, ps);
+      smj[pos] = j;
+      smc[pos] = code;
+    }
+    __syncwarp();
+    if (op.act) {
+      op.ncand += m;
+      unsigned hm = 0u;
+      for (int t = 0; t < m; ++t) {
+        const int cd = smc[t];
+        bool hit;
+        if (cd & 7) {                          // periodic image: shift the target (exact side)
+          op.shift((cd & 1) ? -P.g.L[0] : 0.f, (cd & 2) ? -P.g.L[1] : 0.f, (cd & 4) ? -P.g.L[2] : 0.f);
+          hit = op.test(sm[t]);
+          op.shift(0.f, 0.f, 0.f);
+        } else {
+          hit = op.test(sm[t]);
+        }
+        hm |= (unsigned)hit << t;
+      }
+      while (hm) {
+        const int t = __ffs(hm) - 1;
+        hm &= hm - 1;
+        const int cd = smc[t];
+        if (cd & 7) {
+          op.shift((cd & 1) ? -P.g.L[0] : 0.f, (cd & 2) ? -P.g.L[1] : 0.f, (cd & 4) ? -P.g.L[2] : 0.f);
+          op.interact(sm[t], false);
+          op.shift(0.f, 0.f, 0.f);
+        } else {
+          op.interact(sm[t], (cd & 8) && smj[t] == op.s);
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) W.nr = 0;
+  __syncwarp();
+}
+
+// distance from the target box (shifted by the target shift) to a cell box
+__device__ __forceinline__ float box_gap2(const WarpBox& B, float tox, float toy, float toz, float cx, float cy,
+                                          float cz, float ex, float ey, float ez) {
+  const float gx = fmaxf(fmaxf(cx - (B.hi.x + tox), (B.lo.x + tox) - (cx + ex)), 0.f);
+  const float gy = fmaxf(fmaxf(cy - (B.hi.y + toy), (B.lo.y + toy) - (cy + ey)), 0.f);
+  const float gz = fmaxf(fmaxf(cz - (B.hi.z + toz), (B.lo.z + toz) - (cz + ez)), 0.f);
+  return fmaf(gx, gx, fmaf(gy, gy, gz * gz));
+}
+
+// A neighbour cell whose list is its whole particle range: descend into its sub-cells and
+// collect (into the range buffer) only those within reach of the targets' box. The cell's
+// range in cell (Morton) order is the concatenation of its children's ranges.
+template <class Op>
+__device__ __forceinline__ void cull_range(Op& op, const TravParams& P, const WarpBox& B, WarpSmemT& W,
+                                           const SegDesc& d, int level, float reach, bool kindA,
+                                           typename Op::Src* sm, int* smj, int* smc, int lane) {
+  const int tf = (d.meta & (1 << 15)) ? (128 | (level << 8)) : 0;
+  const int cx = (d.meta >> 8) & 3, cy = (d.meta >> 10) & 3, cz = (d.meta >> 12) & 3;
+  const float tox = cx == 1 ? -P.g.L[0] : 0.f, toy = cy == 1 ? -P.g.L[1] : 0.f, toz = cz == 1 ? -P.g.L[2] : 0.f;
+  const float sox = cx == 2 ? -P.g.L[0] : 0.f, soy = cy == 2 ? -P.g.L[1] : 0.f, soz = cz == 2 ? -P.g.L[2] : 0.f;
+  const int code = (cx == 1 ? 1 : 0) | (cy == 1 ? 2 : 0) | (cz == 1 ? 4 : 0) | ((kindA && (d.meta & 64)) ? 8 : 0) |
+                   (cx == 2 ? 16 : 0) | (cy == 2 ? 32 : 0) | (cz == 2 ? 64 : 0) | tf;
+  const float rr = fmaf(reach, 1.00001f, P.slack);
+  const float rr2 = rr * rr;
+  int top = 0;
+  if (lane == 0) W.stk[0] = d.Y;
+  top = 1;
+  __syncwarp();
+  while (top > 0) {
+    const int node = W.stk[--top];
+    __syncwarp();
+    const int cnt = P.N.count[node];
+    const int4 ijk = P.N.ijk[node];
+    int ch = -1;
+    bool ok = false;
+    if (cnt > 32 && ijk.w < P.g.depth && lane < 8) {
+      ch = P.N.child[8 * (int64_t)node + lane];
+      if (ch >= 0) {
+        const int4 cc = P.N.ijk[ch];
+        const int l = cc.w;
+        ok = box_gap2(B, tox, toy, toz, node_corner(cc.x, l, 0, P.g) + sox, node_corner(cc.y, l, 1, P.g) + soy,
+                      node_corner(cc.z, l, 2, P.g) + soz, P.g.E[l][0], P.g.E[l][1], P.g.E[l][2]) < rr2;
+      }
+    }
+    const unsigned anych = __ballot_sync(FULL_MASK, ch >= 0);
+    if (anych == 0u) {                         // leaf (or small cell): take its whole range
+      if (lane == 0) {
+        W.rs[W.nr] = P.N.first[node];
+        W.rc[W.nr] = cnt;
+        W.rcode[W.nr] = code;
+        W.rreach[W.nr] = reach;
+        W.nr = W.nr + 1;
+      }
+      __syncwarp();
+      if (W.nr == RBUF) flush_ranges(op, P, B, W, 0.f, sm, smj, smc, lane);
+      continue;
+    }
+    const unsigned okb = __ballot_sync(FULL_MASK, ok);
+    if (ok) W.stk[top + __popc(okb & lanemask_lt())] = ch;
+    top += __popc(okb);
+    __syncwarp();
+  }
+}
+
+// The sources of one (cell X, kind) for the warp's targets: lists that are a cell's whole
+// range are culled down its sub-cells and streamed together; presorted lists are swept with
+// the windowed early exit; compacted lists are swept whole.
+template <class Op>
+__device__ __forceinline__ void sweep_cell(Op& op, const TravParams& P, const WarpBox& B, int X, int level, int kind,
+                                           typename Op::Src* sm, int* smj, int* smc, WarpSmemT& W, int lane) {
+  const int s0 = P.segoff2[2 * X + kind], ns = P.segcnt2[2 * X + kind];
+  SegDesc mine;
+  if (lane < ns) {
+    mine = P.seg[s0 + lane];
+    W.sd[lane] = mine;
+  }
+  __syncwarp();
+  bool isrange = false;
+  if (lane < ns) isrange = (mine.meta & (1 << 14)) != 0;
+  const unsigned rb = __ballot_sync(FULL_MASK, isrange);
+  const unsigned ob = __ballot_sync(FULL_MASK, lane < ns && !isrange);
+  if (rb) {
+    unsigned rem = rb;
+#pragma unroll 1
+    while (rem) {
+      const int t = __ffs(rem) - 1;
+      rem &= rem - 1;
+      const float hl = Op::kListHmax ? (kind ? P.N.hmaxR[W.sd[t].Y] : P.N.hmaxA[W.sd[t].Y]) : 0.f;
+      cull_range(op, P, B, W, W.sd[t], level, op.reach(B.hmax, hl), kind == 0, sm, smj, smc, lane);
+    }
+    flush_ranges(op, P, B, W, 0.f, sm, smj, smc, lane);
+  }
+  unsigned rem = ob;
+#pragma unroll 1
+  while (rem) {
+    const int t = __ffs(rem) - 1;
+    rem &= rem - 1;
+    const SegDesc d = W.sd[t];
+    const float hl = Op::kListHmax ? (kind ? P.N.hmaxR[d.Y] : P.N.hmaxA[d.Y]) : 0.f;
+    const float reach = op.reach(B.hmax, hl);
+    const int cx = (d.meta >> 8) & 3, cy = (d.meta >> 10) & 3, cz = (d.meta >> 12) & 3;
+    // exact fp32 shifts: always subtract L from the copy that lies near L (Sterbenz)
+    const float tox = cx == 1 ? -P.g.L[0] : 0.f, toy = cy == 1 ? -P.g.L[1] : 0.f, toz = cz == 1 ? -P.g.L[2] : 0.f;
+    const float sox = cx == 2 ? -P.g.L[0] : 0.f, soy = cy == 2 ? -P.g.L[1] : 0.f, soz = cz == 2 ? -P.g.L[2] : 0.f;
+    op.shift(tox, toy, toz);
+    if (d.meta & 128) {                        // compacted list, swept whole
+      seg_list(op, P, B, d.off, d.cnt, false, false, false, 0.f, sox, soy, soz, tox, toy, toz, reach,
+               kind == 0 && (d.meta & 64), sm, smj, lane);
+      continue;
+    }
+    const bool flip = (d.meta & 32) != 0;
+    const float3 du = dir_unit(d.meta >> 16);
+    const float pi = proj(op.xi - d.cx, op.yi - d.cy, op.zi - d.cz, du);   // target key in Y's frame
+    const float wq = fmaf(op.window(hl), 1.00001f, P.slack);
+    float lim = flip ? pi - wq : pi + wq;
+    if (!op.act) lim = flip ? INFINITY : -INFINITY;
+    const float Lw = flip ? warp_min_f(lim) : warp_max_f(lim);
+    seg_list(op, P, B, d.off, d.cnt, true, false, flip, Lw, sox, soy, soz, tox, toy, toz, reach, false, sm, smj, lane);
+  }
+  op.shift(0.f, 0.f, 0.f);
+  __syncwarp();
+}
+
+// Coarse gather for density targets whose h exceeds the h their cells were built for (state
+// HS_COARSE): every partner within the top cell edge lies in the 27 top cells around the
+// target, so their whole ranges, culled down to the targets' reach, give the one-sided sum
+// of Eq. 2 exactly (no tau filter: each particle appears in exactly one top cell).
+template <class Op>
+__device__ __forceinline__ void coarse_gather(Op& op, const TravParams& P, int leaf, typename Op::Src* sm, int* smj,
+                                              int* smc, WarpSmemT& W, int lane) {
+  int X = leaf;
+  while (P.N.parent[X] >= 0) X = P.N.parent[X];
+  const WarpBox B = warp_box(op);
+  const int4 cX = P.N.ijk[X];
+  if (lane < 27) {
+    const int k = lane;
+    const int Y = (k == 13) ? X : P.N.slot[27 * (int64_t)X + k];
+    SegDesc d;
+    d.Y = Y;
+    d.off = 0;
+    d.cnt = 0;
+    d.cx = d.cy = d.cz = 0.f;
+    int meta = k | (1 << 14) | (k == 13 ? 64 : 0);
+    if (Y >= 0 && k != 13) {
+      const int4 cY = P.N.ijk[Y];
+      const int dd[3] = {cX.x + off_x(k) - cY.x, cX.y + off_y(k) - cY.y, cX.z + off_z(k) - cY.z};
+      for (int a = 0; a < 3; ++a) {
+        const int sa = dd[a] > 1 ? 1 : (dd[a] < -1 ? -1 : 0);
+        meta |= (sa > 0 ? 1 : (sa < 0 ? 2 : 0)) << (8 + 2 * a);
+      }
+    }
+    d.meta = meta;
+    W.sd[lane] = d;
+  }
+  __syncwarp();
+#pragma unroll 1
+  for (int k = 0; k < 27; ++k) {
+    if (W.sd[k].Y < 0) continue;
+    cull_range(op, P, B, W, W.sd[k], 0, op.reach(B.hmax, 0.f), true, sm, smj, smc, lane);
+  }
+  flush_ranges(op, P, B, W, 0.f, sm, smj, smc, lane);
+}
+
 // Visit every pair of the warp's targets exactly once:
 // at each level l of the leaf's ancestor chain, targets with tau == l sweep list A of the
-// 27 cells around their level-l cell, targets with tau > l sweep list R. The cells' source
-// lists come as precomputed descriptors (k_seg_fill).
+// 27 cells around their level-l cell, targets with tau > l sweep list R (the partners with
+// tau_j == l < tau_i, enumerated at min(tau_i, tau_j)).
 template <class Op>
-__device__ __forceinline__ void traverse(Op& op, const TravParams& P, const uint8_t* __restrict__ tau, int leaf,
-                                         typename Op::Src* sm, int* smj, int lane) {
-  const int ti = op.valid ? (int)tau[op.s] : -1;
+__device__ __forceinline__ void traverse(Op& op, const TravParams& P, int leaf, typename Op::Src* sm, int* smj,
+                                         int* smc, WarpSmemT& W, int lane) {
+  const int ti = op.valid ? (int)P.tau[op.s] : -1;
   const int tmax = (int)__reduce_max_sync(FULL_MASK, (unsigned)(ti + 1)) - 1;
+  if (lane == 0) W.nr = 0;
+  __syncwarp();
   int X = leaf;
   int level = P.N.ijk[leaf].w;
   while (X >= 0) {
@@ -321,52 +619,9 @@ __device__ __forceinline__ void traverse(Op& op, const TravParams& P, const uint
       for (int kind = 1; kind >= 0; --kind) {   // R (deeper targets), then A (tau == l)
         op.act = op.valid && (kind ? ti > level : ti == level);
         if (!__any_sync(FULL_MASK, op.act)) continue;
+        if (P.dbg_skip & (1 << kind)) continue;   // timing experiments only (SPH_DEBUG_SKIP)
         const WarpBox B = warp_box(op);
-        const int s0 = P.segoff2[2 * X + kind], ns = P.segcnt2[2 * X + kind];
-#pragma unroll 1
-        for (int b0 = 0; b0 < ns; b0 += 32) {
-          SegDesc mine;
-          if (b0 + lane < ns) mine = P.seg[s0 + b0 + lane];
-          const int mseg = min(32, ns - b0);
-#pragma unroll 1
-          for (int t = 0; t < mseg; ++t) {
-            const long long off = __shfl_sync(FULL_MASK, mine.off, t);
-            const int cnt = __shfl_sync(FULL_MASK, mine.cnt, t);
-            const int meta = __shfl_sync(FULL_MASK, mine.meta, t);
-            const float cyx = __shfl_sync(FULL_MASK, mine.cx, t);
-            const float cyy = __shfl_sync(FULL_MASK, mine.cy, t);
-            const float cyz = __shfl_sync(FULL_MASK, mine.cz, t);
-            const int Y = __shfl_sync(FULL_MASK, mine.Y, t);
-            const float hl = Op::kListHmax ? (kind ? P.N.hmaxR[Y] : P.N.hmaxA[Y]) : 0.f;
-            const float reach = op.reach(B.hmax, hl);
-            if (meta & 64) {   // the cell itself: whole list, no window
-              op.shift(0.f, 0.f, 0.f);
-              seg_list(op, P, B, off, cnt, false, false, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, reach, kind == 0, sm,
-                       smj, lane);
-              continue;
-            }
-            const bool flip = (meta & 32) != 0;
-            const float3 du = dir_unit(meta >> 16);
-            const int cx = (meta >> 8) & 3, cy = (meta >> 10) & 3, cz = (meta >> 12) & 3;
-            // exact fp32 shifts: always subtract L from the copy that lies near L (Sterbenz)
-            const float tox = cx == 1 ? -P.g.L[0] : 0.f, toy = cy == 1 ? -P.g.L[1] : 0.f,
-                        toz = cz == 1 ? -P.g.L[2] : 0.f;
-            const float sox = cx == 2 ? -P.g.L[0] : 0.f, soy = cy == 2 ? -P.g.L[1] : 0.f,
-                        soz = cz == 2 ? -P.g.L[2] : 0.f;
-            op.shift(tox, toy, toz);
-            if (meta & 128) {   // unsorted copy: box filter only
-              seg_list(op, P, B, off, cnt, false, false, 0.f, sox, soy, soz, tox, toy, toz, reach, false, sm, smj,
-                       lane);
-              continue;
-            }
-            const float pi = proj(op.xi - cyx, op.yi - cyy, op.zi - cyz, du);   // target key in Y's frame
-            const float wq = fmaf(op.window(hl), 1.00001f, P.slack);
-            float lim = flip ? pi - wq : pi + wq;
-            if (!op.act) lim = flip ? INFINITY : -INFINITY;
-            const float Lw = flip ? warp_min_f(lim) : warp_max_f(lim);
-            seg_list(op, P, B, off, cnt, true, flip, Lw, sox, soy, soz, tox, toy, toz, reach, false, sm, smj, lane);
-          }
-        }
+        sweep_cell(op, P, B, X, level, kind, sm, smj, smc, W, lane);
       }
     }
     X = P.N.parent[X];
@@ -380,6 +635,7 @@ struct DensOut {
   double* sf;
   float4* acc0;   // smf, smqfp, sqfp, divs
   float4* acc1;   // curl sums xyz, count (int bits)
+  float* s2;      // sum q^2 f''(q)
 };
 
 __global__ void __launch_bounds__(INTERACT_WARPS * 32, 6) k_density(TravParams P, const float4* __restrict__ xh,
@@ -387,36 +643,42 @@ __global__ void __launch_bounds__(INTERACT_WARPS * 32, 6) k_density(TravParams P
                                                                  const uint8_t* __restrict__ tau, DensOut out) {
   __shared__ DensOp::Src smem[INTERACT_WARPS][32];
   __shared__ int smj[INTERACT_WARPS][32];
+  __shared__ int smc[INTERACT_WARPS][32];
+  __shared__ WarpSmemT wsm[INTERACT_WARPS];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int t = blockIdx.x * INTERACT_WARPS + wib;
   if (t >= P.ntasks) return;
-  const int2 task = P.tasks[t];
-  const int leaf = task.x;
-  const int first = P.N.first[leaf], cnt = P.N.count[leaf];
-  const int li = task.y * 32 + lane;
-  const int s = first + li;
-  bool v = li < cnt;
-  if (v && P.active) v = P.active[s] == HS_ACTIVE;
+  const int4 task = P.tasks[t];   // {leaf, first particle, count <= 32, -}
+  bool v = lane < task.z;
+  const int s = task.y + lane;
+  const uint8_t st = (v && P.active) ? P.active[s] : (uint8_t)HS_ACTIVE;
+  bool vc = v && st == HS_COARSE;
+  if (v && P.active) v = st == HS_ACTIVE || st == HS_COARSE;
   if (!__any_sync(FULL_MASK, v)) return;
   DensOp op;
   op.xh = xh;
   op.vm = vm;
   op.init(s, v);
-  traverse(op, P, tau, leaf, smem[wib], smj[wib], lane);
+  op.valid = v && !vc;
+  traverse(op, P, task.x, smem[wib], smj[wib], smc[wib], wsm[wib], lane);
+  if (__any_sync(FULL_MASK, vc)) {
+    op.valid = op.act = vc;
+    coarse_gather(op, P, task.x, smem[wib], smj[wib], smc[wib], wsm[wib], lane);
+  }
+  op.valid = v;
   if (v) {
     out.sf[s] = op.sf;
     out.acc0[s] = make_float4(op.smf, op.smqfp, op.sqfp, op.divs);
+    out.s2[s] = op.sq2fpp;
     out.acc1[s] = make_float4(op.crx, op.cry, op.crz, __int_as_float(op.cnt));
   }
-  long long nc = op.ncand, ns = op.nself;
+  long long nc = op.ncand;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    nc += __shfl_xor_sync(FULL_MASK, nc, o);
-    ns += __shfl_xor_sync(FULL_MASK, ns, o);
-  }
+  for (int o = 16; o > 0; o >>= 1) nc += __shfl_xor_sync(FULL_MASK, nc, o);
   if (lane == 0 && P.ctr) {
     atomicAdd(&P.ctr[C_CAND], (unsigned long long)nc);
-    atomicAdd(&P.ctr[C_TMP1], (unsigned long long)ns);
+    atomicAdd(&P.ctr[C_TMP1], (unsigned long long)op.nseg);
+    atomicAdd(&P.ctr[C_TMP2], (unsigned long long)op.nchunk);
   }
 }
 
@@ -434,22 +696,21 @@ __global__ void __launch_bounds__(INTERACT_WARPS * 32, 5) k_force(TravParams P, 
                                                                const uint8_t* __restrict__ tau, ForceOut out) {
   __shared__ ForceOp::Src smem[INTERACT_WARPS][32];
   __shared__ int smj[INTERACT_WARPS][32];
+  __shared__ int smc[INTERACT_WARPS][32];
+  __shared__ WarpSmemT wsm[INTERACT_WARPS];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int t = blockIdx.x * INTERACT_WARPS + wib;
   if (t >= P.ntasks) return;
-  const int2 task = P.tasks[t];
-  const int leaf = task.x;
-  const int first = P.N.first[leaf], cnt = P.N.count[leaf];
-  const int li = task.y * 32 + lane;
-  const int s = first + li;
-  const bool v = li < cnt;
+  const int4 task = P.tasks[t];
+  const bool v = lane < task.z;
+  const int s = task.y + lane;
   ForceOp op;
   op.fx = fx;
   op.vm = vm;
   op.fs = fs;
   op.alpha = alpha;
   op.init(s, v);
-  traverse(op, P, tau, leaf, smem[wib], smj[wib], lane);
+  traverse(op, P, task.x, smem[wib], smj[wib], smc[wib], wsm[wib], lane);
   if (v) {
     const uint32_t p = out.perm[s];
     out.a[3 * (int64_t)p] = op.ax;
@@ -459,17 +720,17 @@ __global__ void __launch_bounds__(INTERACT_WARPS * 32, 5) k_force(TravParams P, 
     if (out.vsig) out.vsig[p] = op.vsig;
     if (out.nnbr) out.nnbr[p] = op.cnt;
   }
-  long long nc = op.ncand, ns = op.nself;
+  long long nc = op.ncand;
   long long nf = v ? op.cnt : 0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     nc += __shfl_xor_sync(FULL_MASK, nc, o);
-    ns += __shfl_xor_sync(FULL_MASK, ns, o);
     nf += __shfl_xor_sync(FULL_MASK, nf, o);
   }
   if (lane == 0 && P.ctr) {
     atomicAdd(&P.ctr[C_CAND], (unsigned long long)nc);
-    atomicAdd(&P.ctr[C_TMP1], (unsigned long long)ns);
+    atomicAdd(&P.ctr[C_TMP1], (unsigned long long)op.nseg);
+    atomicAdd(&P.ctr[C_TMP2], (unsigned long long)op.nchunk);
     atomicAdd(&P.ctr[C_NFORCE], (unsigned long long)nf);
   }
 }
@@ -485,12 +746,13 @@ __global__ void __launch_bounds__(INTERACT_WARPS * 32, 5) k_force(TravParams P, 
 // once for all parked particles.
 __global__ void k_h_update(int64_t n, float4* __restrict__ xh, const float* __restrict__ hb,
                            float* __restrict__ lo, float* __restrict__ hi, uint8_t* __restrict__ state,
-                           const double* __restrict__ sf, const float4* __restrict__ acc0, float n_t,
-                           float tol, unsigned long long* ctr) {
-  int unconv = 0, parked = 0;
+                           const double* __restrict__ sf, const float4* __restrict__ acc0,
+                           const float* __restrict__ s2, float n_t, float tol, float coarse_cap,
+                           unsigned long long* ctr) {
+  int unconv = 0, parked = 0, coarse = 0;
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n;
        s += (int64_t)gridDim.x * blockDim.x) {
-    if (state[s] != HS_ACTIVE) continue;
+    if (state[s] != HS_ACTIVE && state[s] != HS_COARSE) continue;
     const float h = xh[s].w;
     const double Nd = (32.0 / 3.0) * sf[s];
     const float N = (float)Nd;
@@ -508,43 +770,73 @@ __global__ void k_h_update(int64_t n, float4* __restrict__ xh, const float* __re
       state[s] = HS_DONE;
       continue;
     }
-    const float dN = -(32.f / 3.f) * acc0[s].z / h;   // >= 0
-    const float nu = h * dN / N;
-    float hn = (nu > 0.25f) ? h * __expf(__logf(n_t / N) / nu) : (res < 0.f ? 2.f * h : 0.5f * h);
+    // g(x) = ln N(e^x) - ln n_ngb with x = ln h:  g' = h N'/N,  g'' = g' + h^2 N''/N - g'^2,
+    // h N' = -(32/3) S1, h^2 N'' = (32/3)(2 S1 + S2), S1 = sum q f'(q), S2 = sum q^2 f''(q)
+    const float S1 = acc0[s].z, S2 = s2[s];
+    const float g = __logf(N / n_t);
+    const float g1 = -(32.f / 3.f) * S1 / N;
+    const float g2 = g1 + (32.f / 3.f) * (2.f * S1 + S2) / N - g1 * g1;
+    float dx;
+    if (g1 > 0.25f) {
+      dx = -g / g1;                                      // log-space Newton
+      const float den = 2.f * g1 * g1 - g * g2;           // Halley (cubic convergence)
+      if (den > 0.5f * g1 * g1) {
+        const float dh = -2.f * g * g1 / den;
+        if (fabsf(dh) <= 2.f * fabsf(dx)) dx = dh;
+      }
+    } else {
+      dx = (res < 0.f) ? 0.6931472f : -0.6931472f;       // no neighbour yet: double / halve
+    }
+    float hn = h * __expf(dx);
     hn = fminf(fmaxf(hn, 0.5f * h), 2.f * h);
     if (!(hn > l && hn < u)) hn = 0.5f * (l + u);
     xh[s].w = hn;
-    if (hn > hb[s]) {
+    if (hn <= hb[s]) {
+      state[s] = HS_ACTIVE;
+      ++unconv;
+    } else if (hn <= coarse_cap) {
+      state[s] = HS_COARSE;
+      ++unconv;
+      ++coarse;
+    } else {
       state[s] = HS_PARKED;
       ++parked;
-    } else {
-      ++unconv;
     }
   }
   unconv = warp_sum_i(unconv);
   parked = warp_sum_i(parked);
+  coarse = warp_sum_i(coarse);
   if ((threadIdx.x & 31) == 0) {
     if (unconv) atomicAdd(&ctr[C_UNCONV], (unsigned long long)unconv);
     if (parked) atomicAdd(&ctr[C_REBUILD], (unsigned long long)parked);
+    if (coarse) atomicAdd(&ctr[C_TMP0], (unsigned long long)coarse);
   }
 }
 
+// particles whose final h exceeds the h their cells were built for
+__global__ void k_count_loose(int64_t n, const float4* __restrict__ xh, const float* __restrict__ hb,
+                              unsigned long long* ctr) {
+  int cnt = 0;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x)
+    cnt += xh[s].w > hb[s] ? 1 : 0;
+  cnt = warp_sum_i(cnt);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&ctr[C_TMP0], (unsigned long long)cnt);
+}
+
 // tasks with at least one active lane (compaction flags)
-__global__ void k_task_active(const int2* __restrict__ tasks, int ntasks, NodeArrays N,
+__global__ void k_task_active(const int4* __restrict__ tasks, int ntasks,
                               const uint8_t* __restrict__ active, int* __restrict__ flag) {
   const int lane = threadIdx.x & 31;
   const int t = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   if (t >= ntasks) return;
-  const int2 task = tasks[t];
-  const int li = task.y * 32 + lane;
-  const int first = N.first[task.x], cnt = N.count[task.x];
-  bool a = li < cnt && active[first + li] == HS_ACTIVE;
+  const int4 task = tasks[t];
+  bool a = lane < task.z && active[task.y + lane] == HS_ACTIVE;
   bool any = __any_sync(FULL_MASK, a);
   if (lane == 0) flag[t] = any ? 1 : 0;
 }
 
-__global__ void k_task_compact(const int2* __restrict__ tasks, int ntasks, const int* __restrict__ flag,
-                               const int* __restrict__ idx, int2* __restrict__ out) {
+__global__ void k_task_compact(const int4* __restrict__ tasks, int ntasks, const int* __restrict__ flag,
+                               const int* __restrict__ idx, int4* __restrict__ out) {
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < ntasks && flag[t]) out[idx[t]] = tasks[t];
 }
@@ -661,7 +953,7 @@ __global__ void k_scatter_sums(const uint32_t* __restrict__ perm, int64_t n, con
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t p = perm[s];
     const uint8_t st = state[s];
-    state_o[p] = st == HS_DONE ? HS_DONE : HS_ACTIVE;
+    state_o[p] = st == HS_DONE ? HS_DONE : HS_ACTIVE;   // coarse / parked particles resume normally
     if (st == HS_DONE) {
       sf_o[p] = sf[s];
       a0_o[p] = a0[s];

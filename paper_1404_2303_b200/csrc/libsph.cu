@@ -6,6 +6,7 @@
 #include <cstring>
 #include <exception>
 #include <cstdlib>
+#include <ctime>
 
 #include "common.cuh"
 #include "radix_sort.cuh"
@@ -83,15 +84,36 @@ static bool dbg_on() {
   return v == 1;
 }
 #define DBG(...) do { if (dbg_on()) { fprintf(stderr, "[sph] " __VA_ARGS__); fflush(stderr); } } while (0)
+// debug wall-clock of a region (device-synchronised), only when SPH_DEBUG is set
+struct DbgTimer {
+  sph_ctx* c;
+  const char* what;
+  double t0;
+  static double now() {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+  }
+  DbgTimer(sph_ctx* c_, const char* w) : c(c_), what(w), t0(0) {
+    if (dbg_on()) {
+      cudaStreamSynchronize(c->stream);
+      t0 = now();
+    }
+  }
+  ~DbgTimer() {
+    if (dbg_on()) {
+      cudaStreamSynchronize(c->stream);
+      fprintf(stderr, "[sph]   %s: %.3f ms\n", what, now() - t0);
+    }
+  }
+};
 
 // =========================================================== counters ===========
 static unsigned long long* ctr(sph_ctx* c) { return B<unsigned long long>(c, B_COUNTERS, C_NCOUNTERS); }
 static void ctr_reset(sph_ctx* c) {
-  unsigned long long init[C_NCOUNTERS];
-  memset(init, 0, sizeof(init));
-  init[C_HMINBITS] = 0x7f800000ull;
+  static const unsigned long long init[C_NCOUNTERS] = {0, 0, 0, 0, 0, 0, 0, 0x7f800000ull};   // C_HMINBITS = +inf
+  static_assert(C_HMINBITS == 7, "counter layout");
   CUDA_TRY(cudaMemcpyAsync(ctr(c), init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
-  sync(c);  // `init` is a stack buffer
 }
 static void ctr_read(sph_ctx* c, unsigned long long* h) {
   CUDA_TRY(cudaMemcpyAsync(h, ctr(c), sizeof(unsigned long long) * C_NCOUNTERS, cudaMemcpyDeviceToHost, c->stream));
@@ -225,6 +247,7 @@ static float as_float(unsigned long long b) {
 // (h_build), carrying B_HCUR_O / B_LO_O / B_HI_O into cell order. count_only: the
 // occupancy-only hierarchy used for the initial guess (no slots, no sorts).
 static void build_structure(sph_ctx* c, bool count_only) {
+  DbgTimer _t(c, count_only ? "build (count only)" : "build");
   const int64_t n = c->n;
   const float* x = Bget<float>(c, B_XIN);
   float* hb_o = Bget<float>(c, B_HB_ORIG);
@@ -346,7 +369,7 @@ static void build_structure(sph_ctx* c, bool count_only) {
   LAUNCH(k_level_counts, gridfull((int64_t)nnodes * 32, 256), 256, 0, nnodes, N, tau);
   int64_t* nsort = B<int64_t>(c, B_N_NSORT, 2 * (int64_t)nnodes);
   int64_t* sscan = B<int64_t>(c, B_TMPL1, 2 * (int64_t)nnodes);
-  LAUNCH(k_list_masks, gridfull(nnodes, 128), 128, 0, nnodes, N, nsort);
+  LAUNCH(k_list_masks, gridfull(nnodes, 128), 128, 0, nnodes, N, c->cfg.sort_min_len, nsort);
   c->n_sorted = scan_excl<int64_t>(c, nsort, sscan, 2 * (int64_t)nnodes);
   LAUNCH(k_split_offsets, gridfull(nnodes, 256), 256, 0, nnodes, sscan, N);
 
@@ -387,8 +410,6 @@ static void build_structure(sph_ctx* c, bool count_only) {
       LAUNCH(k_big_write, nbig, 512, 0, nbig, bigseg, bigoff, N, bk0, bv0, sorted);
     }
   }
-  float4* lpos = B<float4>(c, B_LPOS, c->n_sorted);
-  LAUNCH(k_list_pos, grid1d(c, c->n_sorted, 256), 256, 0, c->n_sorted, sorted, xh, lpos);
   {
     int* cnt2 = B<int>(c, B_SEGCNT2, 2 * (int64_t)nnodes);
     int* off2 = B<int>(c, B_SEGOFF2, 2 * (int64_t)nnodes);
@@ -399,14 +420,18 @@ static void build_structure(sph_ctx* c, bool count_only) {
     c->n_pair_slots = nseg;
   }
 
-  // ---- leaf tasks: (leaf, chunk of 32 particles)
-  int* nchunk = B<int>(c, B_TASKFLAG, nnodes);
-  int* cscan = B<int>(c, B_TASKIDX, nnodes);
-  LAUNCH(k_leaf_chunks, gridfull(nnodes, 256), 256, 0, nnodes, N, nchunk);
-  int ntasks = scan_excl<int>(c, nchunk, cscan, nnodes);
-  int2* tasks = B<int2>(c, B_TASKS, ntasks);
-  LAUNCH(k_write_tasks, gridfull(nnodes, 256), 256, 0, nnodes, nchunk, cscan, tasks);
-  c->n_leaves = ntasks;  // number of (leaf, chunk) tasks; see stats
+  // ---- tasks: leaf cells in chunks of <= 32 particles
+  int ntasks;
+  {
+    int* nchunk = B<int>(c, B_TASKFLAG, nnodes);
+    int* cscan = B<int>(c, B_TASKIDX, nnodes);
+    N = nodes(c);
+    LAUNCH(k_leaf_chunks, gridfull(nnodes, 256), 256, 0, nnodes, N, nchunk);
+    ntasks = scan_excl<int>(c, nchunk, cscan, nnodes);
+    int4* tasks = B<int4>(c, B_TASKS, ntasks);
+    LAUNCH(k_write_tasks, gridfull(nnodes, 256), 256, 0, nnodes, N, nchunk, cscan, tasks);
+    c->n_leaves = ntasks;   // number of tasks (stats.n_leaves)
+  }
   sync(c);
   DBG("build: n %lld top %dx%dx%d depth %d levels %d nodes %d tasks %d sorted %lld big %s\n", (long long)n,
       c->ntop[0], c->ntop[1], c->ntop[2], depth, nlev, nnodes, ntasks, (long long)c->n_sorted, "");
@@ -453,20 +478,24 @@ static void flush_out(sph_ctx* c, std::vector<OutMap>& maps, cudaEvent_t done) {
   if (!maps.empty()) sync(c);
 }
 
-static TravParams trav(sph_ctx* c, const int2* tasks, int ntasks, const uint8_t* active) {
+static TravParams trav(sph_ctx* c, const int4* tasks, int ntasks, const uint8_t* active) {
   TravParams P;
   P.tasks = tasks;
   P.ntasks = ntasks;
   P.N = nodes(c);
   P.g = level_geom(c);
   P.sorted = Bget<SortEntry>(c, B_SORTED);
-  P.lpos = Bget<float4>(c, B_LPOS);
+  P.tau = Bget<uint8_t>(c, B_TAU);
   P.seg = Bget<SegDesc>(c, B_SEGDESC);
   P.segoff2 = Bget<int>(c, B_SEGOFF2);
   P.segcnt2 = Bget<int>(c, B_SEGCNT2);
   P.active = active;
   float Lmax = (float)std::max(c->cfg.box[0], std::max(c->cfg.box[1], c->cfg.box[2]));
   P.slack = 4e-7f * Lmax;
+  {
+    const char* e = getenv("SPH_DEBUG_SKIP");
+    P.dbg_skip = e ? atoi(e) : 0;
+  }
   P.ctr = ctr(c);
   return P;
 }
@@ -508,6 +537,7 @@ void sph_config_default(sph_config* cfg, double lx, double ly, double lz) {
   cfg->split_fraction = 0.875f;
   cfg->top_edge_factor = 1.0f;
   cfg->h_margin = 1.1f;
+  cfg->sort_min_len = 96;
   cfg->flags = SPH_F_SYNC;
   cfg->rank = 0;
   cfg->nranks = 1;
@@ -543,6 +573,7 @@ static bool cfg_ok(const sph_config* f, std::string& why) {
   if (!(f->n_ngb_tol > 0.f)) { why = "n_ngb_tol <= 0"; return false; }
   if (!(f->top_edge_factor >= 1.f)) { why = "top_edge_factor < 1"; return false; }
   if (!(f->h_margin >= 1.f)) { why = "h_margin < 1"; return false; }
+  if (f->sort_min_len < 0) { why = "sort_min_len < 0"; return false; }
   if (!(f->split_fraction >= 0.f && f->split_fraction < 1.f)) { why = "split_fraction outside [0,1)"; return false; }
   if (f->split_count < 1) { why = "split_count < 1"; return false; }
   if (f->max_h_iter < 1) { why = "max_h_iter < 1"; return false; }
@@ -663,8 +694,10 @@ int sph_build_cells(sph_ctx* ctx, int64_t n, const float* x, const float* h0) {
     // bracket the root without a rebuild
     LAUNCH(k_init_h, grid1d(c, n, 256), 256, 0, hcur, n, SPH_COLD_MARGIN * c->cfg.h_margin, hb_cap(c), hcur, hb,
            lo, hi);
+    c->margin_used = SPH_COLD_MARGIN * c->cfg.h_margin;
   } else {
     LAUNCH(k_init_h, grid1d(c, n, 256), 256, 0, hin, n, c->cfg.h_margin, hb_cap(c), hcur, hb, lo, hi);
+    c->margin_used = c->cfg.h_margin;
   }
   build_structure(c, false);
   c->state = 1;
@@ -680,6 +713,36 @@ static void fill_struct_stats(sph_ctx* c, sph_stats* st) {
   st->n_leaves = c->n_leaves;
   st->n_pair_slots = c->n_pair_slots;
   st->n_rebuilds = c->rebuilds;
+}
+
+// re-bin for h_build = h * margin (parked particles: margin_parked), keeping h, its bracket,
+// the states and the converged particles' sums (permuted to the new cell order)
+static void rebuild_keep_sums(sph_ctx* c, const float* vd, const float* md, const float* ud, float margin_parked,
+                              float margin = -1.f) {
+  const int64_t n = c->n;
+  if (margin < 0.f) margin = c->cfg.h_margin;
+  uint8_t* active = Bget<uint8_t>(c, B_FLAG);
+  LAUNCH(k_scatter_state, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, Bget<float4>(c, B_XH),
+         Bget<float>(c, B_HLO), Bget<float>(c, B_HHI), active, margin, margin_parked, hb_cap(c),
+         Bget<float>(c, B_HCUR_O), Bget<float>(c, B_LO_O), Bget<float>(c, B_HI_O), Bget<float>(c, B_HB_ORIG));
+  uint8_t* st_o = B<uint8_t>(c, B_STATE_O, n);
+  double* sf_o = B<double>(c, B_SF_O, n);
+  float4* a0_o = B<float4>(c, B_ACC0_O, n);
+  float4* a1_o = B<float4>(c, B_ACC1_O, n);
+  LAUNCH(k_scatter_sums, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, active, Bget<double>(c, B_DSUMF),
+         Bget<float4>(c, B_DACC0), Bget<float4>(c, B_DACC1), st_o, sf_o, a0_o, a1_o);
+  build_structure(c, false);
+  c->rebuilds++;
+  c->margin_used = margin;
+  LAUNCH(k_gather_vmu, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, vd, md, ud, Bget<float4>(c, B_VM),
+         Bget<float>(c, B_U));
+  LAUNCH(k_gather_sums, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, st_o, sf_o, a0_o, a1_o, active,
+         Bget<double>(c, B_DSUMF), Bget<float4>(c, B_DACC0), Bget<float4>(c, B_DACC1));
+}
+
+// coarse mode covers any h below the top cell edge (the 27 top cells hold every partner)
+static float coarse_cap(sph_ctx* c) {
+  return (float)(std::min(c->E0[0], std::min(c->E0[1], c->E0[2])) * (1.0 - 1e-5));
 }
 
 int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, float* h_out, float* rho_out,
@@ -708,34 +771,25 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   double* sf = B<double>(c, B_DSUMF, n);
   float4* acc0 = B<float4>(c, B_DACC0, n);
   float4* acc1 = B<float4>(c, B_DACC1, n);
+  float* s2 = B<float>(c, B_DSUM2, n);
   LAUNCH(k_gather_vmu, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, vd, md, ud, vm, uc);
   LAUNCH(k_fill_u8, grid1d(c, n, 256), 256, 0, active, n, (uint8_t)1);
 
   int iters = 0;
   long long unconv = n;
-  bool all_tasks = true;
   long long cand_last = 0;
   long long parked = 0;
   while (true) {
-    // tasks of this pass: all, or those with an unconverged particle
-    const int ntasks_all = c->n_leaves;
-    const int2* tasks = Bget<int2>(c, B_TASKS);
-    int ntasks = ntasks_all;
-    if (!all_tasks) {
-      int* tf = B<int>(c, B_TASKFLAG, ntasks_all);
-      int* ti = B<int>(c, B_TASKIDX, ntasks_all);
-      LAUNCH(k_task_active, gridfull((int64_t)ntasks_all * 32, 256), 256, 0, tasks, ntasks_all, nodes(c), active, tf);
-      ntasks = scan_excl<int>(c, tf, ti, ntasks_all);
-      int2* t2 = B<int2>(c, B_TASKS2, std::max(ntasks, 1));
-      LAUNCH(k_task_compact, gridfull(ntasks_all, 256), 256, 0, Bget<int2>(c, B_TASKS), ntasks_all, tf, ti, t2);
-      tasks = t2;
-    }
+    // every task is launched; warps without an unconverged particle exit at once
+    const int ntasks = c->n_leaves;
+    const int4* tasks = Bget<int4>(c, B_TASKS);
     ctr_reset(c);
     if (ntasks > 0) {
+      DbgTimer _t(c, "density kernel");
       TravParams P = trav(c, tasks, ntasks, active);
       if (iters == 0) CUDA_TRY(cudaEventRecord(c->ev[6], c->stream));
       LAUNCH(k_density, gridfull(ntasks, INTERACT_WARPS), INTERACT_WARPS * 32, 0, P, Bget<float4>(c, B_XH), vm,
-             Bget<uint8_t>(c, B_TAU), DensOut{sf, acc0, acc1});
+             Bget<uint8_t>(c, B_TAU), DensOut{sf, acc0, acc1, s2});
       if (iters == 0) CUDA_TRY(cudaEventRecord(c->ev[7], c->stream));
     }
     ++iters;
@@ -746,36 +800,42 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
       break;  // sums are at the current h; unconverged particles are reported
     }
     LAUNCH(k_h_update, grid1d(c, n, 256), 256, 0, n, Bget<float4>(c, B_XH), Bget<float>(c, B_HB),
-           Bget<float>(c, B_HLO), Bget<float>(c, B_HHI), active, sf, acc0, c->cfg.n_ngb, c->cfg.n_ngb_tol, ctr(c));
+           Bget<float>(c, B_HLO), Bget<float>(c, B_HHI), active, sf, acc0, s2, c->cfg.n_ngb, c->cfg.n_ngb_tol,
+           coarse_cap(c), ctr(c));
     ctr_read(c, hc);
     if (iters == 1) cand_last = (long long)hc[C_CAND];
     parked += (long long)hc[C_REBUILD];
     unconv = (long long)hc[C_UNCONV] + parked;
-    DBG("density pass %d: tasks %d cand %llu -> active %llu parked %lld\n", iters, ntasks, hc[C_CAND],
-        hc[C_UNCONV], parked);
+    DBG("density pass %d: cand %llu seg %llu chunks %llu -> active %llu (coarse %llu) parked %lld\n", iters,
+        hc[C_CAND], hc[C_TMP1], hc[C_TMP2], hc[C_UNCONV], hc[C_TMP0], parked);
     if (unconv == 0) break;
-    all_tasks = false;
-    if (hc[C_UNCONV] == 0 && parked > 0) {
-      // every other particle has converged; the parked ones want an h beyond the cells they
-      // were binned for: re-bin everything (h_build = h * margin, parked ones with a wider
-      // margin), keep h, its bracket and the converged particles' sums, and continue with the
-      // parked ones only
-      LAUNCH(k_scatter_state, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, Bget<float4>(c, B_XH),
-             Bget<float>(c, B_HLO), Bget<float>(c, B_HHI), active, c->cfg.h_margin, 2.0f * c->cfg.h_margin, hb_cap(c),
-             Bget<float>(c, B_HCUR_O), Bget<float>(c, B_LO_O), Bget<float>(c, B_HI_O), Bget<float>(c, B_HB_ORIG));
-      uint8_t* st_o = B<uint8_t>(c, B_STATE_O, n);
-      double* sf_o = B<double>(c, B_SF_O, n);
-      float4* a0_o = B<float4>(c, B_ACC0_O, n);
-      float4* a1_o = B<float4>(c, B_ACC1_O, n);
-      LAUNCH(k_scatter_sums, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, active, sf, acc0, acc1, st_o,
-             sf_o, a0_o, a1_o);
-      build_structure(c, false);
-      c->rebuilds++;
+    if (iters == 1 && c->margin_used > 1.2f * c->cfg.h_margin) {
+      // cold start: the cells were binned for the occupancy guess with a wide margin; one
+      // Newton step later h is known to a few per cent, so re-bin for it with the normal margin
+      rebuild_keep_sums(c, vd, md, ud, 2.0f * c->cfg.h_margin);
       parked = 0;
       vm = Bget<float4>(c, B_VM);
-      LAUNCH(k_gather_vmu, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, vd, md, ud, vm, uc);
-      LAUNCH(k_gather_sums, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, st_o, sf_o, a0_o, a1_o, active,
-             sf, acc0, acc1);
+      continue;
+    }
+    if (hc[C_UNCONV] == 0 && parked > 0) {
+      // every other particle has converged; the parked ones want an h beyond the top cells
+      // (coarse_cap): re-bin everything for h_build = h * margin, keep h, its bracket and the
+      // converged particles' sums, and continue with the parked ones only
+      rebuild_keep_sums(c, vd, md, ud, 2.0f * c->cfg.h_margin);
+      parked = 0;
+      vm = Bget<float4>(c, B_VM);
+    }
+  }
+  // cells built for an h the particles no longer have (cold-start margin, or particles that
+  // finished in coarse mode): rebuild once, tight, for the force loop (sums carried over)
+  if (iters < c->cfg.max_h_iter) {
+    ctr_reset(c);
+    LAUNCH(k_count_loose, grid1d(c, n, 256), 256, 0, n, Bget<float4>(c, B_XH), Bget<float>(c, B_HB), ctr(c));
+    ctr_read(c, hc);
+    if (hc[C_TMP0] > 0 || c->margin_used > 1.2f * c->cfg.h_margin) {
+      DBG("final tight rebuild: %llu particles with h > h_build (margin used %.3f)\n", hc[C_TMP0], c->margin_used);
+      rebuild_keep_sums(c, vd, md, ud, 1.0f + 1e-5f, 1.0f + 1e-5f);
+      vm = Bget<float4>(c, B_VM);
     }
   }
   // ghost: finalise and write the caller-order outputs
@@ -840,7 +900,8 @@ int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out, int3
   fo.nnbr = dev_out(c, n_nbr_force_out, n, B_OUT3, maps);
   fo.perm = Bget<uint32_t>(c, B_PERM);
   ctr_reset(c);
-  TravParams P = trav(c, Bget<int2>(c, B_TASKS), c->n_leaves, nullptr);
+  DbgTimer _tf(c, "force call");
+  TravParams P = trav(c, Bget<int4>(c, B_TASKS), c->n_leaves, nullptr);
   CUDA_TRY(cudaEventRecord(c->ev[8], c->stream));
   LAUNCH(k_force, gridfull(c->n_leaves, INTERACT_WARPS), INTERACT_WARPS * 32, 0, P, Bget<float4>(c, B_FX),
          Bget<float4>(c, B_VM), Bget<float4>(c, B_FS), c->cfg.alpha, Bget<uint8_t>(c, B_TAU), fo);
@@ -852,7 +913,8 @@ int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out, int3
     if (st) {
       memset(st, 0, sizeof(*st));
       fill_struct_stats(c, st);
-      DBG("force: tasks %d cand %llu (self %llu) pairs %llu\n", c->n_leaves, hc[C_CAND], hc[C_TMP1], hc[C_NFORCE] / 2);
+      DBG("force: tasks %d cand %llu seg %llu chunks %llu pairs %llu\n", c->n_leaves, hc[C_CAND], hc[C_TMP1],
+          hc[C_TMP2], hc[C_NFORCE] / 2);
       st->n_pairs = (int64_t)(hc[C_NFORCE] / 2);
       st->n_candidates = (int64_t)hc[C_CAND];
       float ms = 0.f;

@@ -40,7 +40,7 @@ class Config(ctypes.Structure):
         ("n_ngb", ctypes.c_float), ("n_ngb_tol", ctypes.c_float), ("max_h_iter", ctypes.c_int32),
         ("alpha", ctypes.c_float), ("balsara_eps", ctypes.c_float), ("split_count", ctypes.c_int32),
         ("split_fraction", ctypes.c_float), ("top_edge_factor", ctypes.c_float),
-        ("h_margin", ctypes.c_float), ("flags", ctypes.c_uint32), ("rank", ctypes.c_int32),
+        ("h_margin", ctypes.c_float), ("sort_min_len", ctypes.c_int32), ("flags", ctypes.c_uint32), ("rank", ctypes.c_int32),
         ("nranks", ctypes.c_int32), ("slab_lo", ctypes.c_double), ("slab_hi", ctypes.c_double),
     ]
 
