@@ -84,6 +84,8 @@ typedef struct {
   uint32_t flags;        /* SPH_F_* */
   int32_t rank, nranks;  /* 0, 1 for a single GPU */
   double slab_lo, slab_hi; /* owned x-range of this rank (multi-GPU) */
+  double halo_width;     /* multi-GPU: width of the halo received at each slab face; an h beyond
+                            it cannot be evaluated (SPH_E_NOCONV "halo too narrow"). 0 = none */
 } sph_config;
 
 typedef struct {         /* host struct, filled when non-NULL */
@@ -154,6 +156,38 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u,
  *    Errors: SPH_E_STATE (no density), SPH_E_CUDA. */
 int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out,
               int32_t* n_nbr_force_out, sph_stats* st);
+
+/* ---- multi-GPU slab decomposition (the paper's proxy cells).
+ * One process and one context per GPU; each rank owns the particles with x in its slab
+ * [lo, hi). The transport (NCCL point-to-point over NVLink) is done by the caller, e.g.
+ * through torch.distributed (paper_1404_2303_b200/slab.py); these calls do the device work.
+ * Sequence per evaluation: sph_halo_select -> exchange x, v, m, u (+h0) of the selected
+ * particles -> sph_build_cells_halo -> sph_density -> sph_export_state of the selected
+ * particles -> exchange -> sph_import_halo_state -> sph_force. */
+
+/* Owned particles (caller indices 0..n_own-1, the targets) followed by n_halo halo
+ * particles (sources only: no outputs, never iterated). x [n_own+n_halo][3], h0 likewise or
+ * NULL. Subsequent sph_density inputs v, m, u cover all n_own+n_halo particles; all outputs
+ * of sph_density / sph_force cover the owned particles only. */
+int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const float* x, const float* h0);
+
+/* Indices (ascending, caller order) of the particles within `width` of the lower face
+ * (x - lo < width) and of the upper face (hi - x < width) of the slab [lo, hi).
+ * idx_lo_out / idx_hi_out have room for n entries; counts_out[0..1] = their lengths. */
+int sph_halo_select(sph_ctx* ctx, int64_t n, const float* x, double lo, double hi, double width,
+                    int32_t* idx_lo_out, int32_t* idx_hi_out, int64_t* counts_out);
+
+/* After sph_density: per listed owned particle, the state its halo copies need for the force
+ * loop ("densities and friends"): state_out [k][5] = {h, A = P/(Omega rho^2),
+ * rho, c, Balsara f}. */
+int sph_export_state(sph_ctx* ctx, int64_t k, const int32_t* idx, float* state_out);
+
+/* Before sph_force: the halo particles' state [n_halo][5] (same layout, halo order). */
+int sph_import_halo_state(sph_ctx* ctx, const float* state);
+
+/* Histogram of x over [lo, hi) into nbins bins (for count-quantile slab cuts). */
+int sph_x_histogram(sph_ctx* ctx, int64_t n, const float* x, double lo, double hi, int32_t nbins,
+                    int64_t* hist_out);
 
 /* Number of CUDA kernel launches libsph issued on this context since creation
  * (evidence for the bench's gpu_launches). */

@@ -99,7 +99,10 @@ struct sph_ctx {
   int64_t launches = 0;
   int num_sms = 148;
 
-  int64_t n = 0;
+  int64_t n = 0;        // particles in the structure: owned + halo
+  int64_t n_own = 0;    // owned (targets); caller indices >= n_own are halo (sources only)
+  int64_t loose = 0;    // particles whose final h exceeds their cells' h_build
+  bool force_ready = false;
   int state = 0;  // 0 nothing, 1 cells built, 2 density done
 
   // geometry of the current structure
@@ -130,7 +133,7 @@ enum BufId {
   // nodes
   B_N_FIRST, B_N_COUNT, B_N_IJK, B_N_PARENT, B_N_CHILD, B_N_HMAXB, B_N_SPLIT, B_N_SLOT, B_N_NA,
   B_N_NR, B_N_AMASK, B_N_RMASK, B_N_OFFA, B_N_OFFR, B_N_HMAXA, B_N_HMAXR, B_N_NCH, B_N_CHBASE, B_N_NSORT,
-  B_TAU, B_DSUM2, B_STATE_O, B_SF_O, B_ACC0_O, B_ACC1_O, B_SEGCNT2, B_SEGOFF2, B_SEGDESC,
+  B_TAU, B_DSUM2, B_HFIN_O, B_GST_O, B_STATE_O, B_SF_O, B_ACC0_O, B_ACC1_O, B_SEGCNT2, B_SEGOFF2, B_SEGDESC,
   // lists / tasks
   B_SORTED, B_TOPMAP, B_TASKS, B_TASKS2, B_TASKFLAG, B_TASKIDX, B_TMPI0, B_TMPI1, B_TMPL0, B_TMPL1,
   B_BIGNODES, B_BIGOFF,
@@ -152,6 +155,8 @@ enum CounterId {
   C_HMINBITS,       // min positive h (float bits)
   C_TASKS,          // active tasks
   C_TMP0, C_TMP1, C_TMP2,
+  C_MAXCH,          // max chunks of one warp (load balance diagnostics)
+  C_HEAVY,          // chunks of warps with > 2000 chunks
   C_NCOUNTERS
 };
 

@@ -35,6 +35,7 @@ struct TravParams {
   const uint8_t* active;   // null = all
   float slack;             // absolute window slack (fp32 rounding of keys/corners)
   int dbg_skip;             // debug only: bit k skips kind k (wrong results; timing experiments)
+  int desc_min;             // culling descends into cells holding more particles than this
   unsigned long long* ctr;
 };
 
@@ -47,6 +48,7 @@ struct DensOp {
   const float4* __restrict__ xh;
   const float4* __restrict__ vm;
   bool valid, act;
+  bool nonly;        // N(h) and its derivatives only (a pass that cannot converge anyone)
   int s;
   float x0, y0, z0;  // unshifted target position
   float xi, yi, zi;  // shifted for the current segment
@@ -97,7 +99,7 @@ struct DensOp {
   __device__ __forceinline__ float4 src_pos(int j) const { return xh[j]; }
   __device__ __forceinline__ void stage_rest(Src& d, int j, float4 ps) const {
     d.a = make_float4(ps.x, ps.y, ps.z, 0.f);
-    d.b = vm[j];
+    if (!nonly) d.b = vm[j];
   }
   __device__ __forceinline__ bool test(const Src& src) const {
     const float dx = xi - src.a.x, dy = yi - src.a.y, dz = zi - src.a.z;
@@ -121,12 +123,13 @@ struct DensOp {
         fp = -6.f * t * t;
         fpp = 12.f * t;
       }
-      const float mj = src.b.w;
       sf += (double)f;
       sq2fpp = fmaf(q * q, fpp, sq2fpp);
-      smf = fmaf(mj, f, smf);
       const float qfp = q * fp;
       sqfp += qfp;
+      if (nonly) return;
+      const float mj = src.b.w;
+      smf = fmaf(mj, f, smf);
       smqfp = fmaf(mj, qfp, smqfp);
       const float gf = mj * fp * rinv;
       const float dvx = src.b.x - vxi, dvy = src.b.y - vyi, dvz = src.b.z - vzi;
@@ -314,7 +317,7 @@ __device__ __forceinline__ void seg_list(Op& op, const TravParams& P, const Warp
       smj[pos] = j;
     }
     __syncwarp();
-    if (op.act) {
+    if (op.act && !(P.dbg_skip & 4)) {
       // two phases: distance tests of all staged sources into a hit mask, then the
       // interaction body only for the hits (a lane's misses cost no body instructions)
       op.ncand += m;
@@ -403,7 +406,7 @@ __device__ __forceinline__ void flush_ranges(Op& op, const TravParams& P, const 
       smc[pos] = code;
     }
     __syncwarp();
-    if (op.act) {
+    if (op.act && !(P.dbg_skip & 4)) {
       op.ncand += m;
       unsigned hm = 0u;
       for (int t = 0; t < m; ++t) {
@@ -472,7 +475,7 @@ __device__ __forceinline__ void cull_range(Op& op, const TravParams& P, const Wa
     const int4 ijk = P.N.ijk[node];
     int ch = -1;
     bool ok = false;
-    if (cnt > 32 && ijk.w < P.g.depth && lane < 8) {
+    if (cnt > P.desc_min && ijk.w < P.g.depth && lane < 8) {
       ch = P.N.child[8 * (int64_t)node + lane];
       if (ch >= 0) {
         const int4 cc = P.N.ijk[ch];
@@ -630,15 +633,22 @@ __device__ __forceinline__ void traverse(Op& op, const TravParams& P, int leaf, 
 }
 
 #define INTERACT_WARPS 4
+#ifndef SPH_DENS_MINB
+#define SPH_DENS_MINB 6
+#endif
+#ifndef SPH_FORCE_MINB
+#define SPH_FORCE_MINB 5
+#endif
 
 struct DensOut {
+  int nonly;      // 1: N-only pass (k_h_update keeps every particle active)
   double* sf;
   float4* acc0;   // smf, smqfp, sqfp, divs
   float4* acc1;   // curl sums xyz, count (int bits)
   float* s2;      // sum q^2 f''(q)
 };
 
-__global__ void __launch_bounds__(INTERACT_WARPS * 32, 6) k_density(TravParams P, const float4* __restrict__ xh,
+__global__ void __launch_bounds__(INTERACT_WARPS * 32, SPH_DENS_MINB) k_density(TravParams P, const float4* __restrict__ xh,
                                                                  const float4* __restrict__ vm,
                                                                  const uint8_t* __restrict__ tau, DensOut out) {
   __shared__ DensOp::Src smem[INTERACT_WARPS][32];
@@ -658,6 +668,7 @@ __global__ void __launch_bounds__(INTERACT_WARPS * 32, 6) k_density(TravParams P
   DensOp op;
   op.xh = xh;
   op.vm = vm;
+  op.nonly = out.nonly != 0;
   op.init(s, v);
   op.valid = v && !vc;
   traverse(op, P, task.x, smem[wib], smj[wib], smc[wib], wsm[wib], lane);
@@ -679,6 +690,10 @@ __global__ void __launch_bounds__(INTERACT_WARPS * 32, 6) k_density(TravParams P
     atomicAdd(&P.ctr[C_CAND], (unsigned long long)nc);
     atomicAdd(&P.ctr[C_TMP1], (unsigned long long)op.nseg);
     atomicAdd(&P.ctr[C_TMP2], (unsigned long long)op.nchunk);
+    atomicMax(&P.ctr[C_MAXCH], (unsigned long long)op.nchunk);
+    if (op.nchunk > 2000) atomicAdd(&P.ctr[C_HEAVY], (unsigned long long)op.nchunk);
+    atomicMax(&P.ctr[C_MAXCH], (unsigned long long)op.nchunk);
+    if (op.nchunk > 2000) atomicAdd(&P.ctr[C_HEAVY], (unsigned long long)op.nchunk);
   }
 }
 
@@ -688,9 +703,10 @@ struct ForceOut {
   float* vsig;     // [n] or null
   int* nnbr;       // [n] or null
   const uint32_t* perm;
+  int64_t n_own;
 };
 
-__global__ void __launch_bounds__(INTERACT_WARPS * 32, 5) k_force(TravParams P, const float4* __restrict__ fx,
+__global__ void __launch_bounds__(INTERACT_WARPS * 32, SPH_FORCE_MINB) k_force(TravParams P, const float4* __restrict__ fx,
                                                                const float4* __restrict__ vm,
                                                                const float4* __restrict__ fs, float alpha,
                                                                const uint8_t* __restrict__ tau, ForceOut out) {
@@ -702,8 +718,9 @@ __global__ void __launch_bounds__(INTERACT_WARPS * 32, 5) k_force(TravParams P, 
   const int t = blockIdx.x * INTERACT_WARPS + wib;
   if (t >= P.ntasks) return;
   const int4 task = P.tasks[t];
-  const bool v = lane < task.z;
   const int s = task.y + lane;
+  const bool v = lane < task.z && out.perm[s] < out.n_own;   // halo particles are sources only
+  if (!__any_sync(FULL_MASK, v)) return;
   ForceOp op;
   op.fx = fx;
   op.vm = vm;
@@ -747,7 +764,7 @@ __global__ void __launch_bounds__(INTERACT_WARPS * 32, 5) k_force(TravParams P, 
 __global__ void k_h_update(int64_t n, float4* __restrict__ xh, const float* __restrict__ hb,
                            float* __restrict__ lo, float* __restrict__ hi, uint8_t* __restrict__ state,
                            const double* __restrict__ sf, const float4* __restrict__ acc0,
-                           const float* __restrict__ s2, float n_t, float tol, float coarse_cap,
+                           const float* __restrict__ s2, float n_t, float tol, float coarse_cap, int nonly,
                            unsigned long long* ctr) {
   int unconv = 0, parked = 0, coarse = 0;
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n;
@@ -758,7 +775,8 @@ __global__ void k_h_update(int64_t n, float4* __restrict__ xh, const float* __re
     const float N = (float)Nd;
     const float res = (float)(Nd - (double)n_t);
     if (fabsf(res) <= tol) {
-      state[s] = HS_DONE;
+      if (!nonly) state[s] = HS_DONE;            // N-only pass: keep h, evaluate the sums next pass
+      else ++unconv;
       continue;
     }
     float l = lo[s], u = hi[s];
@@ -767,7 +785,8 @@ __global__ void k_h_update(int64_t n, float4* __restrict__ xh, const float* __re
     lo[s] = l;
     hi[s] = u;
     if (u - l <= 4.f * (h * 1.1920929e-7f)) {   // bracket at fp32 resolution: stop
-      state[s] = HS_DONE;
+      if (!nonly) state[s] = HS_DONE;
+      else ++unconv;
       continue;
     }
     // g(x) = ln N(e^x) - ln n_ngb with x = ln h:  g' = h N'/N,  g'' = g' + h^2 N''/N - g'^2,
@@ -856,15 +875,20 @@ struct GhostOut {
   float* div;
   float* curl;
   const uint32_t* perm;
+  int64_t n_own;       // caller indices >= n_own are halo (source-only) particles
+  float* h_o;          // caller-order state kept for the force loop: h
+  float4* g_o;         //   {A, rho, c, f}
 };
 
 __global__ void k_ghost(int64_t n, const float4* __restrict__ xh, const float* __restrict__ u,
                         const double* __restrict__ sf, const float4* __restrict__ acc0,
-                        const float4* __restrict__ acc1, float gamma, float beps, float4* __restrict__ fx,
-                        float4* __restrict__ fs, GhostOut out, unsigned long long* ctr) {
+                        const float4* __restrict__ acc1, float gamma, float beps, GhostOut out,
+                        unsigned long long* ctr) {
   long long nd = 0;
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n;
        s += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t o = out.perm[s];
+    if (o >= out.n_own) continue;            // halo particle: its owner computes it
     const float4 p = xh[s];
     const float h = p.w, hinv = 1.0f / h;
     const float4 a0 = acc0[s], a1 = acc1[s];
@@ -880,12 +904,10 @@ __global__ void k_ghost(int64_t n, const float4* __restrict__ xh, const float* _
     const float cx = -a1.x * nrm, cy = -a1.y * nrm, cz = -a1.z * nrm;
     const float cn = sqrtf(cx * cx + cy * cy + cz * cz);
     const float fb = cn / (fabsf(div) + cn + beps * c * hinv);
-    const float h2i = hinv * hinv;
-    fx[s] = make_float4(p.x, p.y, p.z, hinv);
-    fs[s] = make_float4(A * SPH_CNORM * h2i * h2i, rho, c, fb);
+    out.h_o[o] = h;
+    out.g_o[o] = make_float4(A, rho, c, fb);
     const int cnt = __float_as_int(a1.w);
     nd += cnt;
-    const uint32_t o = out.perm[s];
     out.h[o] = h;
     out.rho[o] = rho;
     if (out.omega) out.omega[o] = omega;
@@ -900,6 +922,87 @@ __global__ void k_ghost(int64_t n, const float4* __restrict__ xh, const float* _
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) nd += __shfl_xor_sync(FULL_MASK, nd, o);
   if ((threadIdx.x & 31) == 0 && nd) atomicAdd(&ctr[C_NDIR], (unsigned long long)nd);
+}
+
+// force inputs in the (possibly rebuilt) cell order from the caller-order state:
+//   fx = {x, y, z, 1/h},  fs = {A (8/pi) h^-4, rho, c, f},  vm = {v, m}
+__global__ void k_gather_force(const uint32_t* __restrict__ perm, int64_t n, const float4* __restrict__ xh,
+                               const float* __restrict__ h_o, const float4* __restrict__ g_o,
+                               const float* __restrict__ v, const float* __restrict__ m, float4* __restrict__ fx,
+                               float4* __restrict__ fs, float4* __restrict__ vm) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t o = perm[s];
+    const float4 p = xh[s];
+    const float hinv = 1.0f / h_o[o];
+    const float h2i = hinv * hinv;
+    const float4 g = g_o[o];
+    fx[s] = make_float4(p.x, p.y, p.z, hinv);
+    fs[s] = make_float4(g.x * SPH_CNORM * h2i * h2i, g.y, g.z, g.w);
+    vm[s] = make_float4(v[3 * (int64_t)o], v[3 * (int64_t)o + 1], v[3 * (int64_t)o + 2], m[o]);
+  }
+}
+
+// initial h-iteration state: owned particles active, halo (source-only) particles done
+__global__ void k_init_state(const uint32_t* __restrict__ perm, int64_t n, int64_t n_own, uint8_t* __restrict__ st) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x)
+    st[s] = perm[s] < n_own ? HS_ACTIVE : HS_DONE;
+}
+
+// ------------------------------------------------------------------ slabs --------
+// owned particles within `width` of the lower / upper face of the slab
+// [lo, hi) (in x) are sent to the lower / upper neighbour rank as its halo (proxy cells of
+// P:1065-1105). Flags here; compaction by scan keeps caller order.
+__global__ void k_halo_flags(const float* __restrict__ x, int64_t n, float lo, float hi, float width,
+                             int* __restrict__ flo, int* __restrict__ fhi) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float xi = x[3 * i];
+    flo[i] = (xi - lo < width) ? 1 : 0;
+    fhi[i] = (hi - xi < width) ? 1 : 0;
+  }
+}
+
+__global__ void k_compact_idx(const int* __restrict__ flag, const int* __restrict__ scan, int64_t n,
+                              int32_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (flag[i]) out[scan[i]] = (int32_t)i;
+}
+
+__global__ void k_export_state(const int32_t* __restrict__ idx, int64_t k, const float* __restrict__ h_o,
+                               const float4* __restrict__ g_o, float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t o = idx[i];
+    const float4 g = g_o[o];
+    out[5 * i] = h_o[o];
+    out[5 * i + 1] = g.x;
+    out[5 * i + 2] = g.y;
+    out[5 * i + 3] = g.z;
+    out[5 * i + 4] = g.w;
+  }
+}
+
+__global__ void k_import_state(const float* __restrict__ in, int64_t k, int64_t n_own, float* __restrict__ h_o,
+                               float4* __restrict__ g_o) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+    h_o[n_own + i] = in[5 * i];
+    g_o[n_own + i] = make_float4(in[5 * i + 1], in[5 * i + 2], in[5 * i + 3], in[5 * i + 4]);
+  }
+}
+
+__global__ void k_x_hist(const float* __restrict__ x, int64_t n, float lo, float hi, int nb,
+                         unsigned long long* __restrict__ hist) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int b = (int)floorf((x[3 * i] - lo) / (hi - lo) * nb);
+    b = min(max(b, 0), nb - 1);
+    atomicAdd(&hist[b], 1ull);
+  }
+}
+
+// h_build for the force structure: the final h (plus rounding slack)
+__global__ void k_force_hb(const float* __restrict__ h_o, int64_t n, float* __restrict__ hcur, float* __restrict__ hb) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    hcur[i] = h_o[i];
+    hb[i] = h_o[i] * (1.0f + 1e-5f);
+  }
 }
 
 // ------------------------------------------------------------------ misc ---------

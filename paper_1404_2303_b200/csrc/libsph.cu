@@ -495,6 +495,8 @@ static TravParams trav(sph_ctx* c, const int4* tasks, int ntasks, const uint8_t*
   {
     const char* e = getenv("SPH_DEBUG_SKIP");
     P.dbg_skip = e ? atoi(e) : 0;
+    const char* d = getenv("SPH_DESC_MIN");
+    P.desc_min = d ? atoi(d) : 32;
   }
   P.ctr = ctr(c);
   return P;
@@ -543,6 +545,7 @@ void sph_config_default(sph_config* cfg, double lx, double ly, double lz) {
   cfg->nranks = 1;
   cfg->slab_lo = 0.0;
   cfg->slab_hi = lx;
+  cfg->halo_width = 0.0;
 }
 
 const char* sph_status_string(int s) {
@@ -647,10 +650,17 @@ int sph_set_allocator(sph_ctx* c, void* (*alloc)(size_t, void*, void*), void (*r
 }
 
 int sph_build_cells(sph_ctx* ctx, int64_t n, const float* x, const float* h0) {
+  return sph_build_cells_halo(ctx, n, 0, x, h0);
+}
+
+int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const float* x, const float* h0) {
   API_BEGIN(ctx)
-  SPH_REQUIRE(n > 0 && x, SPH_E_ARG, "n <= 0 or x == NULL");
+  SPH_REQUIRE(n_own > 0 && n_halo >= 0 && x, SPH_E_ARG, "n_own <= 0, n_halo < 0 or x == NULL");
+  const int64_t n = n_own + n_halo;
   SPH_REQUIRE(n < (1ll << 30), SPH_E_ARG, "n >= 2^30");
   c->n = n;
+  c->n_own = n_own;
+  c->force_ready = false;
   c->state = 0;
   c->rebuilds = 0;
   CUDA_TRY(cudaEventRecord(c->ev[0], c->stream));
@@ -742,7 +752,9 @@ static void rebuild_keep_sums(sph_ctx* c, const float* vd, const float* md, cons
 
 // coarse mode covers any h below the top cell edge (the 27 top cells hold every partner)
 static float coarse_cap(sph_ctx* c) {
-  return (float)(std::min(c->E0[0], std::min(c->E0[1], c->E0[2])) * (1.0 - 1e-5));
+  double cap = std::min(c->E0[0], std::min(c->E0[1], c->E0[2])) * (1.0 - 1e-5);
+  if (c->n > c->n_own && c->cfg.halo_width > 0.0) cap = std::min(cap, c->cfg.halo_width);
+  return (float)cap;
 }
 
 int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, float* h_out, float* rho_out,
@@ -752,9 +764,10 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   SPH_REQUIRE(v && m && u && h_out && rho_out, SPH_E_ARG, "required pointer is NULL");
   const int64_t n = c->n;
   CUDA_TRY(cudaEventRecord(c->ev[2], c->stream));
-  const float* vd = dev_in(c, v, 3 * n, B_VIN);
-  const float* md = dev_in(c, m, n, B_MIN);
-  const float* ud = dev_in(c, u, n, B_UIN);
+  // copied: the force loop gathers v and m again after its rebuild
+  const float* vd = dev_in(c, v, 3 * n, B_VIN, true);
+  const float* md = dev_in(c, m, n, B_MIN, true);
+  const float* ud = dev_in(c, u, n, B_UIN, true);
   ctr_reset(c);
   LAUNCH(k_validate_vmu, grid1d(c, n, 256), 256, 0, vd, md, ud, n, ctr(c));
   unsigned long long hc[C_NCOUNTERS];
@@ -762,7 +775,6 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_NONFINITE), SPH_E_DOMAIN, "non-finite velocity");
   SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_MASS), SPH_E_DOMAIN, "mass <= 0 or non-finite");
   SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_U), SPH_E_DOMAIN, "internal energy <= 0 or non-finite");
-  // staged copies must survive rebuilds (the gather reads them again)
   if (!is_device_ptr(v) || !is_device_ptr(m) || !is_device_ptr(u)) sync(c);
 
   float4* vm = B<float4>(c, B_VM, n);
@@ -773,7 +785,7 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   float4* acc1 = B<float4>(c, B_DACC1, n);
   float* s2 = B<float>(c, B_DSUM2, n);
   LAUNCH(k_gather_vmu, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, vd, md, ud, vm, uc);
-  LAUNCH(k_fill_u8, grid1d(c, n, 256), 256, 0, active, n, (uint8_t)1);
+  LAUNCH(k_init_state, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, c->n_own, active);
 
   int iters = 0;
   long long unconv = n;
@@ -783,13 +795,15 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
     // every task is launched; warps without an unconverged particle exit at once
     const int ntasks = c->n_leaves;
     const int4* tasks = Bget<int4>(c, B_TASKS);
+    // cold start: the first pass evaluates N, N', N'' only (nobody converges at the guess)
+    const int nonly = (iters == 0 && c->margin_used > 1.2f * c->cfg.h_margin && c->cfg.max_h_iter > 1) ? 1 : 0;
     ctr_reset(c);
     if (ntasks > 0) {
       DbgTimer _t(c, "density kernel");
       TravParams P = trav(c, tasks, ntasks, active);
       if (iters == 0) CUDA_TRY(cudaEventRecord(c->ev[6], c->stream));
       LAUNCH(k_density, gridfull(ntasks, INTERACT_WARPS), INTERACT_WARPS * 32, 0, P, Bget<float4>(c, B_XH), vm,
-             Bget<uint8_t>(c, B_TAU), DensOut{sf, acc0, acc1, s2});
+             Bget<uint8_t>(c, B_TAU), DensOut{nonly, sf, acc0, acc1, s2});
       if (iters == 0) CUDA_TRY(cudaEventRecord(c->ev[7], c->stream));
     }
     ++iters;
@@ -801,13 +815,14 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
     }
     LAUNCH(k_h_update, grid1d(c, n, 256), 256, 0, n, Bget<float4>(c, B_XH), Bget<float>(c, B_HB),
            Bget<float>(c, B_HLO), Bget<float>(c, B_HHI), active, sf, acc0, s2, c->cfg.n_ngb, c->cfg.n_ngb_tol,
-           coarse_cap(c), ctr(c));
+           coarse_cap(c), nonly, ctr(c));
     ctr_read(c, hc);
     if (iters == 1) cand_last = (long long)hc[C_CAND];
     parked += (long long)hc[C_REBUILD];
     unconv = (long long)hc[C_UNCONV] + parked;
-    DBG("density pass %d: cand %llu seg %llu chunks %llu -> active %llu (coarse %llu) parked %lld\n", iters,
-        hc[C_CAND], hc[C_TMP1], hc[C_TMP2], hc[C_UNCONV], hc[C_TMP0], parked);
+    DBG("density pass %d: cand %llu seg %llu chunks %llu (max/warp %llu, in heavy warps %llu) -> active %llu "
+        "(coarse %llu) parked %lld\n", iters, hc[C_CAND], hc[C_TMP1], hc[C_TMP2], hc[C_MAXCH], hc[C_HEAVY],
+        hc[C_UNCONV], hc[C_TMP0], parked);
     if (unconv == 0) break;
     if (iters == 1 && c->margin_used > 1.2f * c->cfg.h_margin) {
       // cold start: the cells were binned for the occupancy guess with a wide margin; one
@@ -818,6 +833,7 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
       continue;
     }
     if (hc[C_UNCONV] == 0 && parked > 0) {
+      SPH_REQUIRE(c->n == c->n_own, SPH_E_NOCONV, "halo too narrow: an h exceeds cfg.halo_width");
       // every other particle has converged; the parked ones want an h beyond the top cells
       // (coarse_cap): re-bin everything for h_build = h * margin, keep h, its bracket and the
       // converged particles' sums, and continue with the parked ones only
@@ -826,40 +842,32 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
       vm = Bget<float4>(c, B_VM);
     }
   }
-  // cells built for an h the particles no longer have (cold-start margin, or particles that
-  // finished in coarse mode): rebuild once, tight, for the force loop (sums carried over)
-  if (iters < c->cfg.max_h_iter) {
-    ctr_reset(c);
-    LAUNCH(k_count_loose, grid1d(c, n, 256), 256, 0, n, Bget<float4>(c, B_XH), Bget<float>(c, B_HB), ctr(c));
-    ctr_read(c, hc);
-    if (hc[C_TMP0] > 0 || c->margin_used > 1.2f * c->cfg.h_margin) {
-      DBG("final tight rebuild: %llu particles with h > h_build (margin used %.3f)\n", hc[C_TMP0], c->margin_used);
-      rebuild_keep_sums(c, vd, md, ud, 1.0f + 1e-5f, 1.0f + 1e-5f);
-      vm = Bget<float4>(c, B_VM);
-    }
-  }
   // ghost: finalise and write the caller-order outputs
   std::vector<OutMap> maps;
   GhostOut go;
-  go.h = dev_out(c, h_out, n, B_OUT0, maps);
-  go.rho = dev_out(c, rho_out, n, B_OUT1, maps);
-  go.omega = dev_out(c, omega_out, n, B_OUT2, maps);
-  go.nnbr = dev_out(c, n_nbr_out, n, B_OUT3, maps);
-  go.div = dev_out(c, div_out, n, B_OUT4, maps);
-  go.curl = dev_out(c, curl_out, 3 * n, B_OUT5, maps);
+  const int64_t no = c->n_own;
+  go.h = dev_out(c, h_out, no, B_OUT0, maps);
+  go.rho = dev_out(c, rho_out, no, B_OUT1, maps);
+  go.omega = dev_out(c, omega_out, no, B_OUT2, maps);
+  go.nnbr = dev_out(c, n_nbr_out, no, B_OUT3, maps);
+  go.div = dev_out(c, div_out, no, B_OUT4, maps);
+  go.curl = dev_out(c, curl_out, 3 * no, B_OUT5, maps);
   go.perm = Bget<uint32_t>(c, B_PERM);
-  float4* fx = B<float4>(c, B_FX, n);
-  float4* fs = B<float4>(c, B_FS, n);
+  go.n_own = no;
+  go.h_o = B<float>(c, B_HFIN_O, n);
+  go.g_o = B<float4>(c, B_GST_O, n);
+  // particles whose final h exceeds the h their cells were built for (coarse mode)
   ctr_reset(c);
+  LAUNCH(k_count_loose, grid1d(c, n, 256), 256, 0, n, Bget<float4>(c, B_XH), Bget<float>(c, B_HB), ctr(c));
   LAUNCH(k_ghost, grid1d(c, n, 256), 256, 0, n, Bget<float4>(c, B_XH), uc, sf, acc0, acc1, c->cfg.gamma,
-         c->cfg.balsara_eps, fx, fs, go, ctr(c));
-  LAUNCH(k_node_hmax, gridfull((int64_t)c->n_nodes * 32, 256), 256, 0, c->n_nodes, nodes(c), Bget<float4>(c, B_XH),
-         Bget<uint8_t>(c, B_TAU));
+         c->cfg.balsara_eps, go, ctr(c));
   flush_out(c, maps, c->ev[3]);
   c->state = 2;
+  c->force_ready = false;
   int status = (unconv > 0 && iters >= c->cfg.max_h_iter) ? SPH_E_NOCONV : SPH_OK;
-  if (st || (c->cfg.flags & SPH_F_SYNC)) {
-    ctr_read(c, hc);
+  ctr_read(c, hc);
+  c->loose = (int64_t)hc[C_TMP0];
+  {
     if (st) {
       memset(st, 0, sizeof(*st));
       fill_struct_stats(c, st);
@@ -885,22 +893,50 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   return SPH_OK;
 }
 
+// Force-loop structure: the density cells were built for h_build (cold-start margin, or
+// below the h of particles that finished in coarse mode) and without the halo particles'
+// final h; rebuild once, tight (h_build = h), from the caller-order state, then gather the
+// force inputs in the new cell order.
+static void prepare_force(sph_ctx* c) {
+  const int64_t n = c->n;
+  const bool rebuild = c->margin_used > 1.2f * c->cfg.h_margin || c->loose > 0 || c->n > c->n_own;
+  if (rebuild) {
+    DBG("force: tight rebuild (margin used %.3f, %lld loose, %lld halo)\n", c->margin_used, (long long)c->loose,
+        (long long)(c->n - c->n_own));
+    LAUNCH(k_force_hb, grid1d(c, n, 256), 256, 0, Bget<float>(c, B_HFIN_O), n, Bget<float>(c, B_HCUR_O),
+           Bget<float>(c, B_HB_ORIG));
+    build_structure(c, false);
+    c->rebuilds++;
+    c->margin_used = 1.0f;
+  }
+  float4* fx = B<float4>(c, B_FX, n);
+  float4* fs = B<float4>(c, B_FS, n);
+  float4* vm = B<float4>(c, B_VM, n);
+  LAUNCH(k_gather_force, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, Bget<float4>(c, B_XH),
+         Bget<float>(c, B_HFIN_O), Bget<float4>(c, B_GST_O), Bget<float>(c, B_VIN), Bget<float>(c, B_MIN), fx, fs, vm);
+  LAUNCH(k_node_hmax, gridfull((int64_t)c->n_nodes * 32, 256), 256, 0, c->n_nodes, nodes(c), Bget<float4>(c, B_XH),
+         Bget<uint8_t>(c, B_TAU));
+  c->force_ready = true;
+}
+
 int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out, int32_t* n_nbr_force_out,
               sph_stats* st) {
   API_BEGIN(ctx)
   SPH_REQUIRE(c->state >= 2, SPH_E_STATE, "sph_force before sph_density");
   SPH_REQUIRE(a_out && dudt_out, SPH_E_ARG, "required pointer is NULL");
-  const int64_t n = c->n;
+  const int64_t n = c->n, no = c->n_own;
   CUDA_TRY(cudaEventRecord(c->ev[4], c->stream));
+  DbgTimer _tf(c, "force call");
+  if (!c->force_ready) prepare_force(c);
   std::vector<OutMap> maps;
   ForceOut fo;
-  fo.a = dev_out(c, a_out, 3 * n, B_OUT0, maps);
-  fo.dudt = dev_out(c, dudt_out, n, B_OUT1, maps);
-  fo.vsig = dev_out(c, vsig_out, n, B_OUT2, maps);
-  fo.nnbr = dev_out(c, n_nbr_force_out, n, B_OUT3, maps);
+  fo.a = dev_out(c, a_out, 3 * no, B_OUT0, maps);
+  fo.dudt = dev_out(c, dudt_out, no, B_OUT1, maps);
+  fo.vsig = dev_out(c, vsig_out, no, B_OUT2, maps);
+  fo.nnbr = dev_out(c, n_nbr_force_out, no, B_OUT3, maps);
   fo.perm = Bget<uint32_t>(c, B_PERM);
+  fo.n_own = no;
   ctr_reset(c);
-  DbgTimer _tf(c, "force call");
   TravParams P = trav(c, Bget<int4>(c, B_TASKS), c->n_leaves, nullptr);
   CUDA_TRY(cudaEventRecord(c->ev[8], c->stream));
   LAUNCH(k_force, gridfull(c->n_leaves, INTERACT_WARPS), INTERACT_WARPS * 32, 0, P, Bget<float4>(c, B_FX),
@@ -913,8 +949,8 @@ int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out, int3
     if (st) {
       memset(st, 0, sizeof(*st));
       fill_struct_stats(c, st);
-      DBG("force: tasks %d cand %llu seg %llu chunks %llu pairs %llu\n", c->n_leaves, hc[C_CAND], hc[C_TMP1],
-          hc[C_TMP2], hc[C_NFORCE] / 2);
+      DBG("force: tasks %d cand %llu seg %llu chunks %llu (max/warp %llu heavy %llu) pairs %llu\n", c->n_leaves,
+          hc[C_CAND], hc[C_TMP1], hc[C_TMP2], hc[C_MAXCH], hc[C_HEAVY], hc[C_NFORCE] / 2);
       st->n_pairs = (int64_t)(hc[C_NFORCE] / 2);
       st->n_candidates = (int64_t)hc[C_CAND];
       float ms = 0.f;
@@ -924,6 +960,82 @@ int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out, int3
       st->ms_kernel_force = ms;
     }
   }
+  API_END
+  return SPH_OK;
+}
+
+int sph_halo_select(sph_ctx* ctx, int64_t n, const float* x, double lo, double hi, double width,
+                    int32_t* idx_lo_out, int32_t* idx_hi_out, int64_t* counts_out) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(n > 0 && x && idx_lo_out && idx_hi_out && counts_out, SPH_E_ARG, "bad argument");
+  SPH_REQUIRE(hi > lo && width > 0.0, SPH_E_ARG, "need hi > lo and width > 0");
+  const float* xd = dev_in(c, x, 3 * n, B_XIN);
+  int* flo = B<int>(c, B_TMPI0, n);
+  int* fhi = B<int>(c, B_TMPI1, n);
+  int* slo = B<int>(c, B_TASKFLAG, n);
+  int* shi = B<int>(c, B_TASKIDX, n);
+  LAUNCH(k_halo_flags, grid1d(c, n, 256), 256, 0, xd, n, (float)lo, (float)hi, (float)width, flo, fhi);
+  const int nlo = scan_excl<int>(c, flo, slo, n);
+  const int nhi = scan_excl<int>(c, fhi, shi, n);
+  std::vector<OutMap> maps;
+  int32_t* olo = dev_out(c, idx_lo_out, std::max(nlo, 1), B_OUT0, maps);
+  int32_t* ohi = dev_out(c, idx_hi_out, std::max(nhi, 1), B_OUT1, maps);
+  for (auto& mp : maps) mp.bytes = (mp.user == (void*)idx_lo_out ? (size_t)nlo : (size_t)nhi) * sizeof(int32_t);
+  LAUNCH(k_compact_idx, grid1d(c, n, 256), 256, 0, flo, slo, n, olo);
+  LAUNCH(k_compact_idx, grid1d(c, n, 256), 256, 0, fhi, shi, n, ohi);
+  flush_out(c, maps, c->ev[10]);
+  sync(c);
+  counts_out[0] = nlo;
+  counts_out[1] = nhi;
+  API_END
+  return SPH_OK;
+}
+
+int sph_export_state(sph_ctx* ctx, int64_t k, const int32_t* idx, float* state_out) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(c->state >= 2, SPH_E_STATE, "sph_export_state before sph_density");
+  SPH_REQUIRE(k >= 0 && (k == 0 || (idx && state_out)), SPH_E_ARG, "bad argument");
+  if (k == 0) return SPH_OK;
+  const int32_t* id = dev_in(c, idx, k, B_TMPI0);
+  std::vector<OutMap> maps;
+  float* o = dev_out(c, state_out, 5 * k, B_OUT2, maps);
+  LAUNCH(k_export_state, grid1d(c, k, 256), 256, 0, id, k, Bget<float>(c, B_HFIN_O), Bget<float4>(c, B_GST_O), o);
+  flush_out(c, maps, c->ev[10]);
+  sync(c);
+  API_END
+  return SPH_OK;
+}
+
+int sph_import_halo_state(sph_ctx* ctx, const float* state) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(c->state >= 2, SPH_E_STATE, "sph_import_halo_state before sph_density");
+  const int64_t k = c->n - c->n_own;
+  if (k == 0) return SPH_OK;
+  SPH_REQUIRE(state != nullptr, SPH_E_ARG, "state == NULL");
+  const float* sd = dev_in(c, state, 5 * k, B_TMPL0);
+  LAUNCH(k_import_state, grid1d(c, k, 256), 256, 0, sd, k, c->n_own, Bget<float>(c, B_HFIN_O),
+         Bget<float4>(c, B_GST_O));
+  c->force_ready = false;
+  sync(c);
+  API_END
+  return SPH_OK;
+}
+
+int sph_x_histogram(sph_ctx* ctx, int64_t n, const float* x, double lo, double hi, int32_t nbins,
+                    int64_t* hist_out) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(n >= 0 && nbins > 0 && hist_out && (n == 0 || x) && hi > lo, SPH_E_ARG, "bad argument");
+  unsigned long long* hd = B<unsigned long long>(c, B_TMPL1, nbins);
+  CUDA_TRY(cudaMemsetAsync(hd, 0, nbins * sizeof(unsigned long long), c->stream));
+  if (n > 0) {
+    const float* xd = dev_in(c, x, 3 * n, B_XIN);
+    LAUNCH(k_x_hist, grid1d(c, n, 256), 256, 0, xd, n, (float)lo, (float)hi, nbins, hd);
+  }
+  std::vector<OutMap> maps;
+  int64_t* o = dev_out(c, hist_out, nbins, B_OUT3, maps);
+  CUDA_TRY(cudaMemcpyAsync(o, hd, nbins * sizeof(int64_t), cudaMemcpyDeviceToDevice, c->stream));
+  flush_out(c, maps, c->ev[10]);
+  sync(c);
   API_END
   return SPH_OK;
 }

@@ -1,0 +1,212 @@
+"""Multi-GPU slab decomposition (the paper's local / proxy cells and its two
+communication tasks per proxy cell): one process per GPU, each owning the
+particles whose x lies in its slab [lo, hi).
+
+Per evaluation, two halo exchanges with the two slab neighbours (periodic ring):
+  1. before the density loop: x, v, m, u, h0 of the owned particles within `width` of each
+     face (libsph `sph_halo_select`);
+  2. before the force loop: their h, A, rho, c, f (`sph_export_state` /
+     `sph_import_halo_state`).
+Halo particles are sources only; owned-halo pairs are computed on both ranks, each updating
+its own particle (no reverse exchange).
+
+All device work is in libsph; this module moves buffers between ranks through
+torch.distributed (NCCL point-to-point over NVLink on GPUs, gloo in CPU tests) and picks
+the slab cuts (count quantiles of a global x histogram). It holds no SPH arithmetic.
+"""
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+
+
+def slab_cuts(hist, lo: float, hi: float, world: int) -> list[float]:
+    """world+1 slab edges over [lo, hi): interior cuts at the count quantiles of `hist`
+    (equal particle counts, so roughly equal work at ~constant neighbours per particle)."""
+    hist = np.asarray(hist, dtype=np.float64)
+    nb = hist.size
+    cum = np.concatenate([[0.0], np.cumsum(hist)])
+    total = cum[-1]
+    edges = [float(lo)]
+    for k in range(1, world):
+        target = total * k / world
+        b = int(np.searchsorted(cum, target, side="left"))
+        b = min(max(b, 1), nb)
+        # linear interpolation inside bin b-1
+        c0, c1 = cum[b - 1], cum[b]
+        frac = 0.0 if c1 <= c0 else (target - c0) / (c1 - c0)
+        edges.append(float(lo + (hi - lo) * (b - 1 + frac) / nb))
+    edges.append(float(hi))
+    for a, b in zip(edges, edges[1:]):
+        if not b > a:
+            raise ValueError("degenerate slab cut")
+    return edges
+
+
+def neighbours(rank: int, world: int) -> tuple[int, int]:
+    return (rank - 1) % world, (rank + 1) % world
+
+
+class DistTransport:
+    """Exchange with the lower and upper neighbours over torch.distributed P2P.
+
+    Order is fixed so that messages match even when both neighbours are the same rank
+    (world == 2): every rank sends to its upper neighbour first, then to its lower one, and
+    receives from its lower neighbour first, then from its upper one.
+    """
+
+    def __init__(self, rank: int, world: int, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.rank, self.world, self.group = rank, world, group
+        self.lower, self.upper = neighbours(rank, world)
+
+    def _pair(self, send_hi, send_lo, recv_lo, recv_hi):
+        d = self.dist
+        ops = [d.P2POp(d.isend, send_hi, self.upper, self.group), d.P2POp(d.isend, send_lo, self.lower, self.group),
+               d.P2POp(d.irecv, recv_lo, self.lower, self.group), d.P2POp(d.irecv, recv_hi, self.upper, self.group)]
+        for r in d.batch_isend_irecv(ops):
+            r.wait()
+
+    def exchange(self, send_lo, send_hi):
+        """send_lo goes to the lower neighbour, send_hi to the upper one; returns
+        (received from lower, received from upper). Rows of equal width."""
+        import torch
+        dev = send_lo.device
+        c_send = [torch.tensor([send_lo.shape[0]], dtype=torch.int64, device=dev),
+                  torch.tensor([send_hi.shape[0]], dtype=torch.int64, device=dev)]
+        c_recv = [torch.zeros(1, dtype=torch.int64, device=dev), torch.zeros(1, dtype=torch.int64, device=dev)]
+        self._pair(c_send[1], c_send[0], c_recv[0], c_recv[1])
+        w = send_lo.shape[1]
+        r_lo = torch.empty(int(c_recv[0].item()), w, dtype=send_lo.dtype, device=dev)
+        r_hi = torch.empty(int(c_recv[1].item()), w, dtype=send_lo.dtype, device=dev)
+        # zero-length messages are skipped symmetrically on both sides (counts are known)
+        d = self.dist
+        ops = []
+        if send_hi.shape[0]:
+            ops.append(d.P2POp(d.isend, send_hi.contiguous(), self.upper, self.group))
+        if send_lo.shape[0]:
+            ops.append(d.P2POp(d.isend, send_lo.contiguous(), self.lower, self.group))
+        if r_lo.shape[0]:
+            ops.append(d.P2POp(d.irecv, r_lo, self.lower, self.group))
+        if r_hi.shape[0]:
+            ops.append(d.P2POp(d.irecv, r_hi, self.upper, self.group))
+        if ops:
+            for r in d.batch_isend_irecv(ops):
+                r.wait()
+        return r_lo, r_hi
+
+    def allreduce_max(self, value: float) -> float:
+        import torch
+        t = torch.tensor([value], dtype=torch.float64)
+        if self.dist.get_backend(self.group) == "nccl":
+            t = t.cuda()
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())
+
+    def allreduce_sum(self, t):
+        self.dist.all_reduce(t, group=self.group)
+        return t
+
+
+PACK_COLS = 9   # x(3) v(3) m u h0
+
+
+def pack(x, v, m, u, h0):
+    import torch
+    return torch.cat([x, v, m[:, None], u[:, None], h0[:, None]], dim=1)
+
+
+def unpack(p):
+    return p[:, 0:3].contiguous(), p[:, 3:6].contiguous(), p[:, 6].contiguous(), p[:, 7].contiguous(), \
+        p[:, 8].contiguous()
+
+
+@dataclasses.dataclass
+class SlabResult:
+    h: object
+    rho: object
+    a: object
+    dudt: object
+    n_nbr: object
+    n_nbr_force: object
+    n_own: int
+    n_halo: int
+    stats_density: dict
+    stats_force: dict
+
+
+class SlabRank:
+    """One rank's evaluation in the four phases separated by the two exchanges."""
+
+    def __init__(self, ctx, x, v, m, u, h0, lo, hi, width, world):
+        if not (width <= hi - lo):
+            raise ValueError("halo width exceeds the slab width (next-nearest slabs would be needed)")
+        self.ctx, self.x, self.v, self.m, self.u, self.h0 = ctx, x, v, m, u, h0
+        self.lo, self.hi, self.width, self.world = lo, hi, width, world
+        self.n_own = int(x.shape[0])
+
+    def select(self):
+        """Phase 1: (to lower neighbour, to upper neighbour) packed x, v, m, u, h0."""
+        import torch
+        self.idx_lo, self.idx_hi = self.ctx.halo_select(self.x, self.lo, self.hi, self.width)
+        if self.world == 2 and self.idx_lo.numel() and self.idx_hi.numel():
+            # both faces border the same rank: send a particle near both faces only once
+            keep = ~torch.isin(self.idx_hi, self.idx_lo)
+            self.idx_hi = self.idx_hi[keep].contiguous()
+        pk = pack(self.x, self.v, self.m, self.u, self.h0)
+        return pk[self.idx_lo.long()].contiguous(), pk[self.idx_hi.long()].contiguous()
+
+    def density(self, recv_lo, recv_hi):
+        """Phase 2: build over owned + halo particles, h iteration and density loop."""
+        import torch
+        halo = torch.cat([recv_lo, recv_hi])
+        self.n_halo = int(halo.shape[0])
+        hx, hv, hm, hu, hh0 = unpack(halo)
+        X = torch.cat([self.x, hx]).contiguous()
+        V = torch.cat([self.v, hv]).contiguous()
+        M = torch.cat([self.m, hm]).contiguous()
+        U = torch.cat([self.u, hu]).contiguous()
+        H0 = torch.cat([self.h0, hh0]).contiguous()
+        self.ctx.build_cells_halo(X, self.n_own, H0 if bool((H0 > 0).all()) else None)
+        self.d = self.ctx.density(V, M, U)
+        return self.d
+
+    def export(self):
+        """Phase 3: state of the particles sent in phase 1 (same order)."""
+        return self.ctx.export_state(self.idx_lo), self.ctx.export_state(self.idx_hi)
+
+    def force(self, state_lo, state_hi):
+        """Phase 4: halo state in, force loop over the owned particles."""
+        import torch
+        self.ctx.import_halo_state(torch.cat([state_lo, state_hi]).contiguous())
+        self.f = self.ctx.force(self.x)
+        d, f = self.d, self.f
+        return SlabResult(d.h, d.rho, f.a, f.dudt, d.n_nbr, f.n_nbr_force, self.n_own, self.n_halo, d.stats,
+                          f.stats)
+
+
+def evaluate_rank(ctx, x, v, m, u, h0, lo, hi, width, transport):
+    """One rank's evaluation with a live transport (DistTransport)."""
+    r = SlabRank(ctx, x, v, m, u, h0, lo, hi, width, transport.world)
+    s_lo, s_hi = r.select()
+    r.density(*transport.exchange(s_lo, s_hi))
+    e_lo, e_hi = r.export()
+    return r.force(*transport.exchange(e_lo, e_hi))
+
+
+def evaluate_ring_sequential(ranks):
+    """Evaluate a list of SlabRank (ranks 0..P-1 of one ring) one after another in ONE
+    process, passing the halo buffers directly (single-GPU tests of the decomposition)."""
+    P = len(ranks)
+    sent = [r.select() for r in ranks]                       # (to lower, to upper)
+    for k, r in enumerate(ranks):
+        lower, upper = neighbours(k, P)
+        r.density(sent[lower][1], sent[upper][0])            # from lower: its upper face
+    ex = [r.export() for r in ranks]
+    out = []
+    for k, r in enumerate(ranks):
+        lower, upper = neighbours(k, P)
+        out.append(r.force(ex[lower][1], ex[upper][0]))
+    return out

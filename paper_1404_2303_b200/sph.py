@@ -42,6 +42,7 @@ class Config(ctypes.Structure):
         ("split_fraction", ctypes.c_float), ("top_edge_factor", ctypes.c_float),
         ("h_margin", ctypes.c_float), ("sort_min_len", ctypes.c_int32), ("flags", ctypes.c_uint32), ("rank", ctypes.c_int32),
         ("nranks", ctypes.c_int32), ("slab_lo", ctypes.c_double), ("slab_hi", ctypes.c_double),
+        ("halo_width", ctypes.c_double),
     ]
 
 
@@ -63,7 +64,8 @@ class Stats(ctypes.Structure):
 #: every symbol include/sph.h declares (checked by tests/test_abi.py)
 EXPORTS = ("sph_config_default", "sph_create", "sph_destroy", "sph_set_allocator",
            "sph_status_string", "sph_last_error", "sph_build_cells", "sph_density", "sph_force",
-           "sph_kernel_launches")
+           "sph_kernel_launches", "sph_build_cells_halo", "sph_halo_select", "sph_export_state",
+           "sph_import_halo_state", "sph_x_histogram")
 
 
 def load(path: str | None = None):
@@ -90,6 +92,11 @@ def load(path: str | None = None):
     lib.sph_force.argtypes = [P, P, P, P, P, ctypes.POINTER(Stats)]
     lib.sph_kernel_launches.argtypes = [P]
     lib.sph_kernel_launches.restype = i64
+    lib.sph_build_cells_halo.argtypes = [P, i64, i64, P, P]
+    lib.sph_halo_select.argtypes = [P, i64, P, ctypes.c_double, ctypes.c_double, ctypes.c_double, P, P, P]
+    lib.sph_export_state.argtypes = [P, i64, P, P]
+    lib.sph_import_halo_state.argtypes = [P, P]
+    lib.sph_x_histogram.argtypes = [P, i64, P, ctypes.c_double, ctypes.c_double, ctypes.c_int32, P]
     if path == LIB or path is None:
         _lib = lib
     return lib
@@ -117,7 +124,7 @@ def _ptr(a, dtype=np.float32):
         return a.ctypes.data
     import torch  # torch is plumbing only (device memory)
     if isinstance(a, torch.Tensor):
-        want = {np.float32: torch.float32, np.int32: torch.int32}[dtype]
+        want = {np.float32: torch.float32, np.int32: torch.int32, np.int64: torch.int64}[dtype]
         if a.dtype != want or not a.is_contiguous():
             raise TypeError(f"expected a contiguous {want} tensor")
         return a.data_ptr()
@@ -183,6 +190,44 @@ class Context:
         n = int(x.shape[0])
         self._check(self.lib.sph_build_cells(self.h, n, _ptr(x), _ptr(h0)))
         self.n = n
+
+    def build_cells_halo(self, x, n_own, h0=None):
+        """x holds n_own owned particles followed by halo (source-only) particles."""
+        n = int(x.shape[0])
+        self._check(self.lib.sph_build_cells_halo(self.h, int(n_own), n - int(n_own), _ptr(x), _ptr(h0)))
+        self.n = int(n_own)
+
+    def halo_select(self, x, lo, hi, width):
+        """Indices of the particles within `width` of the slab faces: (idx_lo, idx_hi)."""
+        import torch
+        n = int(x.shape[0])
+        dev = x.device if isinstance(x, torch.Tensor) else torch.device("cpu")
+        ilo = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        ihi = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        cnt = np.zeros(2, dtype=np.int64)
+        self._check(self.lib.sph_halo_select(self.h, n, _ptr(x), float(lo), float(hi), float(width),
+                                             _ptr(ilo, np.int32), _ptr(ihi, np.int32), cnt.ctypes.data))
+        return ilo[: int(cnt[0])], ihi[: int(cnt[1])]
+
+    def export_state(self, idx):
+        import torch
+        k = int(idx.shape[0])
+        out = torch.empty(k, 5, dtype=torch.float32, device=idx.device)
+        if k:
+            self._check(self.lib.sph_export_state(self.h, k, _ptr(idx, np.int32), _ptr(out)))
+        return out
+
+    def import_halo_state(self, state):
+        self._check(self.lib.sph_import_halo_state(self.h, _ptr(state) if state.shape[0] else None))
+
+    def x_histogram(self, x, lo, hi, nbins):
+        import torch
+        dev = x.device if isinstance(x, torch.Tensor) else torch.device("cpu")
+        out = torch.zeros(nbins, dtype=torch.int64, device=dev)
+        n = int(x.shape[0])
+        self._check(self.lib.sph_x_histogram(self.h, n, _ptr(x) if n else None, float(lo), float(hi), int(nbins),
+                                             _ptr(out, np.int64)))
+        return out
 
     def density(self, v, m, u, out=None, stats: Stats | None = None, check=True):
         """out: dict of preallocated output arrays (h, rho, omega, n_nbr, div, curl)."""
