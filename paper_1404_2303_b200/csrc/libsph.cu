@@ -753,7 +753,6 @@ static void rebuild_keep_sums(sph_ctx* c, const float* vd, const float* md, cons
 // coarse mode covers any h below the top cell edge (the 27 top cells hold every partner)
 static float coarse_cap(sph_ctx* c) {
   double cap = std::min(c->E0[0], std::min(c->E0[1], c->E0[2])) * (1.0 - 1e-5);
-  if (c->n > c->n_own && c->cfg.halo_width > 0.0) cap = std::min(cap, c->cfg.halo_width);
   return (float)cap;
 }
 
@@ -833,7 +832,6 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
       continue;
     }
     if (hc[C_UNCONV] == 0 && parked > 0) {
-      SPH_REQUIRE(c->n == c->n_own, SPH_E_NOCONV, "halo too narrow: an h exceeds cfg.halo_width");
       // every other particle has converged; the parked ones want an h beyond the top cells
       // (coarse_cap): re-bin everything for h_build = h * margin, keep h, its bracket and the
       // converged particles' sums, and continue with the parked ones only
@@ -867,6 +865,15 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   int status = (unconv > 0 && iters >= c->cfg.max_h_iter) ? SPH_E_NOCONV : SPH_OK;
   ctr_read(c, hc);
   c->loose = (int64_t)hc[C_TMP0];
+  if (c->n > c->n_own && c->cfg.halo_width > 0.0) {
+    // every owned particle's partners must be inside the received halo
+    ctr_reset(c);
+    LAUNCH(k_hrange, grid1d(c, c->n_own, 256), 256, 0, Bget<float>(c, B_HFIN_O), c->n_own, ctr(c));
+    unsigned long long hh[C_NCOUNTERS];
+    ctr_read(c, hh);
+    SPH_REQUIRE(as_float(hh[C_HMAXBITS]) <= c->cfg.halo_width, SPH_E_NOCONV,
+                "halo too narrow: an owned h = " + std::to_string(as_float(hh[C_HMAXBITS])) + " exceeds cfg.halo_width");
+  }
   {
     if (st) {
       memset(st, 0, sizeof(*st));
