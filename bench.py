@@ -10,9 +10,10 @@ the whole step's device time.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl sph|reference] [--config C4]
 
-N > 1 runs under torch.distributed.run: one process per GPU, each an independent
-replica of the workload (the path does not exchange data between replicas: "replicas
-only"); the time is the max over ranks, value = all ranks' pairs / that time.
+N > 1 runs under torch.distributed.run: one process per GPU, weak scaling over a slab
+decomposition of the C4 recipe in an (N,1,1) box with N x 2,097,152
+particles; two NCCL halo exchanges per step; the time is the max over ranks, value = all
+ranks' pairs / that time.
 --impl reference times the fp64 oracle (oracle/) on a bounded sample of the same
 workload on this host's CPU cores (rank 0 only).
 """
@@ -316,6 +317,115 @@ def run_sph(args, rank, world, local_rank):
     ctx.close()
 
 
+def run_slab(args, rank, world, local_rank):
+    """N > 1: weak scaling. The C4 recipe in a box (N,1,1) with N x 2,097,152 particles and
+    N x 64 clumps; ranks own count-quantile slabs along x (about one C4 each) and exchange
+    halos with their two neighbours over NCCL (paper_1404_2303_b200/slab.py)."""
+    import numpy as np
+    import torch
+    import torch.distributed as td
+
+    import paper_1404_2303_b200 as sph
+    import workloads
+    from paper_1404_2303_b200 import slab
+
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.current_stream(dev)
+    p = workloads.c4_weak(world)
+    Lx = p.box[0]
+    cfg0 = sph.default_config(p.box, **CONFIG_TUNING)
+    ctx0 = sph.Context(cfg0, device=local_rank, stream=stream.cuda_stream)
+    # count-quantile cuts from the global x histogram (each rank histograms its initial slab)
+    own0 = np.nonzero((p.x[:, 0] >= rank * Lx / world) & (p.x[:, 0] < (rank + 1) * Lx / world))[0]
+    hist = ctx0.x_histogram(torch.from_numpy(np.ascontiguousarray(p.x[own0])).to(dev), 0.0, Lx, 8192)
+    td.all_reduce(hist)
+    edges = slab.slab_cuts(hist.cpu().numpy(), 0.0, Lx, world)
+    lo, hi = edges[rank], edges[rank + 1]
+    own = np.nonzero((p.x[:, 0] >= lo) & (p.x[:, 0] < hi))[0]
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    x, v, m, u, h0 = t(p.x[own]), t(p.v[own]), t(p.m[own]), t(p.u[own]), t(p.h0[own])
+    # halo width: twice the largest occupancy guess of h anywhere (allreduce), <= slab width
+    gmax = torch.tensor([float(ctx0.guess_h(x).max())], dtype=torch.float64, device=dev)
+    td.all_reduce(gmax, op=td.ReduceOp.MAX)
+    wmin = torch.tensor([min(e1 - e0 for e0, e1 in zip(edges, edges[1:]))], dtype=torch.float64, device=dev)
+    width = float(min(2.0 * gmax.item(), wmin.item()))
+    ctx0.close()
+    cfg = sph.default_config(p.box, **CONFIG_TUNING, rank=rank, nranks=world, slab_lo=lo, slab_hi=hi,
+                             halo_width=width)
+    ctx = sph.Context(cfg, device=local_rank, stream=stream.cuda_stream)
+    tr = slab.DistTransport(rank, world)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step(inputs):
+        return slab.evaluate_rank(ctx, *inputs, lo, hi, width, tr)
+
+    for _ in range(args.warmup):
+        step((x, v, m, u, h0))
+    torch.cuda.synchronize()
+
+    def timed(make_inputs, fetch):
+        total, res = 0.0, None
+        td.barrier()
+        torch.cuda.synchronize()
+        l0 = ctx.kernel_launches
+        clk = Clocks(local_rank)
+        for _ in range(args.steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            res = step(make_inputs())
+            fetch(res)
+            e1.record(stream)
+            e1.synchronize()
+            total += e0.elapsed_time(e1)
+        clocks = clk.stop()
+        torch.cuda.synchronize()
+        td.barrier()
+        return total, res, ctx.kernel_launches - l0, clocks
+
+    total_ms, res, launches, clocks = timed(lambda: (x, v, m, u, h0), lambda r: None)
+    pairs = 2.0 * res.stats_force["n_pairs"] * args.steps
+    # e2e: owned inputs from pinned host memory, outputs back to the host, inside the region
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    hx, hv, hm, hu, hh0 = pin(p.x[own]), pin(p.v[own]), pin(p.m[own]), pin(p.u[own]), pin(p.h0[own])
+    outs = [torch.empty(len(own)).pin_memory(), torch.empty(len(own)).pin_memory(),
+            torch.empty(len(own), 3).pin_memory(), torch.empty(len(own)).pin_memory()]
+
+    def fetch(r):
+        for o, s_ in zip(outs, (r.h, r.rho, r.a, r.dudt)):
+            o.copy_(s_, non_blocking=True)
+
+    e2e_ms, _, _, _ = timed(lambda: tuple(a.to(dev, non_blocking=True) for a in (hx, hv, hm, hu, hh0)), fetch)
+    h2d = sum(a.numel() * 4 for a in (hx, hv, hm, hu, hh0))
+    d2h = sum(o.numel() * 4 for o in outs)
+    agg = torch.tensor([total_ms, e2e_ms, pairs, float(res.n_halo), float(len(own))], dtype=torch.float64, device=dev)
+    mx = agg.clone()
+    td.all_reduce(mx, op=td.ReduceOp.MAX)
+    sm = agg.clone()
+    td.all_reduce(sm)
+    if rank == 0:
+        t_max, e2e_max = float(mx[0]), float(mx[1])
+        line = {
+            "metric": METRIC, "value": float(sm[2]) / (t_max * 1e-3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": f"C4x{world}: C4 recipe in a ({world},1,1) box, {p.n} particles, "
+                                   f"{64 * world} clumps; count-quantile slabs along x, cold h0",
+                       "N": p.n, "parallelism": f"slab{world} (halo exchange over NCCL, 2 per step)",
+                       "halo_width": width, "halo_over_owned_mean": float(sm[3]) / float(sm[4]),
+                       "l2": "flushed (256 MiB write) before every timed step",
+                       "split_count": CONFIG_TUNING["split_count"]},
+            "roofline": None, "cpu_baseline": None,
+            "e2e": {"value": float(sm[2]) / (e2e_max * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": launches, "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -330,7 +440,10 @@ def main():
         torch.cuda.set_device(local_rank)
         td.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_sph(args, rank, world, local_rank)
+        if world > 1:
+            run_slab(args, rank, world, local_rank)
+        else:
+            run_sph(args, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as td

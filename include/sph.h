@@ -171,6 +171,11 @@ int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out,
  * of sph_density / sph_force cover the owned particles only. */
 int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const float* x, const float* h0);
 
+/* The library's initial guess of h from cell occupancy (the one sph_build_cells uses when
+ * h0 is NULL), h_out [n]: N_ngb = (4 pi/3) n h^3 for the local number density n of the
+ * smallest cell around the particle holding >= N_ngb particles. Used e.g. to size halos. */
+int sph_guess_h(sph_ctx* ctx, int64_t n, const float* x, float* h_out);
+
 /* Indices (ascending, caller order) of the particles within `width` of the lower face
  * (x - lo < width) and of the upper face (hi - x < width) of the slab [lo, hi).
  * idx_lo_out / idx_hi_out have room for n entries; counts_out[0..1] = their lengths. */

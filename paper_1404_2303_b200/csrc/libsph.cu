@@ -971,6 +971,34 @@ int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out, int3
   return SPH_OK;
 }
 
+int sph_guess_h(sph_ctx* ctx, int64_t n, const float* x, float* h_out) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(n > 0 && x && h_out, SPH_E_ARG, "bad argument");
+  c->n = n;
+  c->n_own = n;
+  c->state = 0;
+  float* xd = B<float>(c, B_XIN, 3 * n);
+  CUDA_TRY(cudaMemcpyAsync(xd, x, 3 * n * sizeof(float), cudaMemcpyDefault, c->stream));
+  float* hb = B<float>(c, B_HB_ORIG, n);
+  float* hcur = B<float>(c, B_HCUR_O, n);
+  float* lo = B<float>(c, B_LO_O, n);
+  float* hi = B<float>(c, B_HI_O, n);
+  LAUNCH(k_fill_f, grid1d(c, n, 256), 256, 0, hb, n, 1.0f);
+  LAUNCH(k_fill_f, grid1d(c, n, 256), 256, 0, hcur, n, 1.0f);
+  LAUNCH(k_fill_f, grid1d(c, n, 256), 256, 0, lo, n, 0.0f);
+  LAUNCH(k_fill_f, grid1d(c, n, 256), 256, 0, hi, n, 0.0f);
+  build_structure(c, true);
+  double Lmin = std::min(c->cfg.box[0], std::min(c->cfg.box[1], c->cfg.box[2]));
+  std::vector<OutMap> maps;
+  float* o = dev_out(c, h_out, n, B_OUT0, maps);
+  LAUNCH(k_guess_h, gridfull(c->n_nodes, 128), 128, 0, c->n_nodes, nodes(c), level_geom(c), Bget<uint32_t>(c, B_PERM),
+         c->cfg.n_ngb, (int)c->cfg.n_ngb, (float)(0.25 * Lmin), o);
+  flush_out(c, maps, c->ev[10]);
+  sync(c);
+  API_END
+  return SPH_OK;
+}
+
 int sph_halo_select(sph_ctx* ctx, int64_t n, const float* x, double lo, double hi, double width,
                     int32_t* idx_lo_out, int32_t* idx_hi_out, int64_t* counts_out) {
   API_BEGIN(ctx)

@@ -65,7 +65,7 @@ class Stats(ctypes.Structure):
 EXPORTS = ("sph_config_default", "sph_create", "sph_destroy", "sph_set_allocator",
            "sph_status_string", "sph_last_error", "sph_build_cells", "sph_density", "sph_force",
            "sph_kernel_launches", "sph_build_cells_halo", "sph_halo_select", "sph_export_state",
-           "sph_import_halo_state", "sph_x_histogram")
+           "sph_import_halo_state", "sph_x_histogram", "sph_guess_h")
 
 
 def load(path: str | None = None):
@@ -97,6 +97,7 @@ def load(path: str | None = None):
     lib.sph_export_state.argtypes = [P, i64, P, P]
     lib.sph_import_halo_state.argtypes = [P, P]
     lib.sph_x_histogram.argtypes = [P, i64, P, ctypes.c_double, ctypes.c_double, ctypes.c_int32, P]
+    lib.sph_guess_h.argtypes = [P, i64, P, P]
     if path == LIB or path is None:
         _lib = lib
     return lib
@@ -219,6 +220,12 @@ class Context:
 
     def import_halo_state(self, state):
         self._check(self.lib.sph_import_halo_state(self.h, _ptr(state) if state.shape[0] else None))
+
+    def guess_h(self, x):
+        import torch
+        out = torch.empty(int(x.shape[0]), dtype=torch.float32, device=x.device)
+        self._check(self.lib.sph_guess_h(self.h, int(x.shape[0]), _ptr(x), _ptr(out)))
+        return out
 
     def x_histogram(self, x, lo, hi, nbins):
         import torch

@@ -140,7 +140,7 @@ def c3(seed: int = 140423033, kl: int = 96, kr: int = 48, jitter: float = 0.1) -
 
 
 # ---------------------------------------------------------------- C4/C5 ---------
-def _clustered(name: str, seed: int, n: int, n_clumps: int) -> Particles:
+def _clustered(name: str, seed: int, n: int, n_clumps: int, box=(1.0, 1.0, 1.0)) -> Particles:
     """Clustered multi-resolution periodic unit box (SURVEY §8(d) C4 recipe):
     (1) floor(0.3N) uniform background; (2) centres U[0,1)^3; (3) scale radii
     a = exp(U(ln 0.002, ln 0.02)); (4) remaining particles split evenly, the
@@ -149,9 +149,10 @@ def _clustered(name: str, seed: int, n: int, n_clumps: int) -> Particles:
     (z = U(-1,1), phi = U(0, 2pi)); (6) wrap; (7) v ~ N(0, 0.1);
     (8) u = exp(U(ln 0.1, ln 10)); (9) m = 1/N; h0 = 0 (library guess)."""
     rng = np.random.default_rng(seed)
+    boxa = np.asarray(box, dtype=np.float64)
     nb = int(math.floor(0.3 * n))
-    xb = rng.random((nb, 3))
-    centres = rng.random((n_clumps, 3))
+    xb = rng.random((nb, 3)) * boxa
+    centres = rng.random((n_clumps, 3)) * boxa
     a = np.exp(rng.uniform(math.log(0.002), math.log(0.02), n_clumps))
     nc = n - nb
     per, rem = divmod(nc, n_clumps)
@@ -167,13 +168,20 @@ def _clustered(name: str, seed: int, n: int, n_clumps: int) -> Particles:
     x = np.concatenate([xb, xc])
     v = rng.normal(0.0, 0.1, (n, 3))
     u = np.exp(rng.uniform(math.log(0.1), math.log(10.0), n))
-    return _pack(name, (1.0, 1.0, 1.0), x, v, 1.0 / n, u, 0.0, seed=seed,
+    return _pack(name, box, x, v, float(np.prod(boxa)) / n, u, 0.0, seed=seed,
                  n_clumps=n_clumps, scale_radii=a.tolist())
 
 
 def c4(seed: int = 140423034, n: int = 2097152, n_clumps: int = 64) -> Particles:
     """BASELINE configs[3]: 2,097,152 particles, 30% background + 64 Plummer clumps."""
     return _clustered("C4", seed, n, n_clumps)
+
+
+def c4_weak(replicas: int, seed: int = 140423038) -> Particles:
+    """Weak-scaling version of C4 for `replicas` GPUs: box (replicas, 1, 1) with
+    replicas x 2,097,152 particles and replicas x 64 clumps (same density, same clump
+    statistics); slab decomposition along x gives each GPU about one C4."""
+    return _clustered(f"C4x{replicas}", seed, replicas * 2097152, replicas * 64, box=(float(replicas), 1.0, 1.0))
 
 
 def c5(seed: int = 140423035, n: int = 512 ** 3, n_clumps: int = 512) -> Particles:
