@@ -1,31 +1,21 @@
-// build.cuh — neighbour-finding structure on the device (section 3.2-3.3).
+// build.cuh — the cell hierarchy on the device (section 3.2).
 //
-//  a1  k_hrange / k_validate_x  : max/min h_build, domain checks
-//  a2  k_keys                   : key = top-cell index | Morton octants to `depth` levels,
-//                                 sorted by the radix sort (radix_sort.cuh)
-//  a3  k_gather_build           : particles packed in cell order (float4 {x,y,z,h})
-//  a4  k_level_split / k_make_children : recursive split, "more than some minimal number"
-//                                 and "a reasonable fraction" with h < edge/2 (P:510-518,
-//                                 constants P:1354-1356), one level per launch
-//  a5  k_top_slots / k_child_slots : every cell's 26 same-level neighbours (periodic at the
-//                                 top; children inherit them through their
-//                                 parent, which is the self refinement into 8 child selfs +
-//                                 28 sibling pairs of P:519-522 and the pair refinement of
-//                                 P:523-532).
-//      k_tau / k_level_counts / k_list_masks : the interaction level of each particle.
-//                                 tau_i = min(leaf level, deepest level with edge >= h_i).
-//                                 The pair {i,j} is enumerated exactly once, at level
-//                                 min(tau_i, tau_j), between the cells of i and j at that level
-//                                 (equal or adjacent since r < max(h) <= edge). This is the
-//                                 paper's refinement rule ("refine iff all h < edge/2")
-//                                 applied per particle instead of per cell pair: the large-h
-//                                 particles stay at the coarse level as a residue while the
-//                                 rest of the pair is refined. Per cell and level
-//                                 two source lists: A = {tau >= l} (targets with tau == l
-//                                 sweep them) and R = {tau == l} (deeper targets sweep them).
-//  a6  k_sort_warp / k_sort_block / big radix path : the A and R lists of each cell sorted
-//                                 along the 13 canonical axes where a neighbour needs them
-//                                 (P:687-698), plus an unsorted copy for the cell's own sweep
+//  a1  k_validate_x / k_hrange  : domain checks, max/min h
+//  a2  k_keys                   : key = top-cell index | Morton octants to `depth` levels;
+//                                 one radix sort (radix_sort.cuh) orders every level at once
+//                                 (particles of a cell contiguous in memory)
+//  a3  k_pack                   : particles copied into cell order (float4 {x, y, z, h})
+//  a4  k_level_split / k_make_children : recursive split of a cell into its 8 octants while
+//                                 it holds "more than some minimal number" of particles and
+//                                 "a reasonable fraction" of them has h < edge/2
+//                                 (constants P:1354-1356); one level per launch.
+//                                 split_fraction = 0 splits on the count alone.
+//  a6  k_sort_leaf_warp / k_sort_leaf_block : a leaf's particles presorted along the 13
+//                                 canonical pair directions, keys = projection of
+//                                 (x - cell corner) on the direction; used by the sorted
+//                                 sweeps of the list builder (lists.cuh).
+//      k_guess_h                : initial h from cell occupancy (cold start)
+//      k_leaf_groups            : targets in groups of <= 32 particles of one leaf (a warp each)
 #pragma once
 #include "common.cuh"
 
@@ -35,25 +25,16 @@ struct NodeArrays {
   int4* ijk;        // integer cell coordinates at its level, .w = level
   int* parent;
   int* child;       // [8*node + octant], -1 if empty / leaf
-  float* hmaxb;     // max h_build in the cell
   int* split;       // 1 if split into children
-  int* slot;        // [27*node + k] neighbour cell at offset k (same level), -1 if none
-  int* nA;          // #{i in cell : tau_i >= level}   (list A)
-  int* nR;          // #{i in cell : tau_i == level}   (list R)
-  int* amask;       // 14-bit: directions 0..12 (+ bit 13 unsorted) of list A that are needed
-  int* rmask;       // 14-bit, list R
-  int64_t* offA;    // offsets of the node's A / R blocks in the list array (see k_list_masks)
-  int64_t* offR;
-  float* hmaxA;     // max final h over list A / R (force window)
-  float* hmaxR;
+  float* hmax;      // max h in the cell (force reach of the sources it holds)
+  int4* rec;        // packed {first, count, first child, mask | level << 8} (k_node_rec)
+  int64_t* sortoff; // offset of the node's 13 sorted lists in the sorted-entry array, -1 if none
 };
-#define LIST_SELF 13  // "direction" of the unsorted copy used for the cell's own sweep
 
 struct LevelGeom {           // per-level edges (fp32), up to SPH_MAX_DEPTH+1 levels
   float E[SPH_MAX_DEPTH + 2][3];
-  float half_min[SPH_MAX_DEPTH + 2];   // min_k E_l,k / 2
-  int n[SPH_MAX_DEPTH + 2][3];         // cells per axis at level l (ntop << l)
   float L[3];
+  int ntop[3];
   int depth;
 };
 
@@ -75,9 +56,10 @@ __global__ void k_validate_x(const float* __restrict__ x, int64_t n, float Lx, f
   if ((threadIdx.x & 31) == 0 && err) atomicOr(&ctr[C_ERR], (unsigned long long)err);
 }
 
+// max / min positive h (float bits are monotone for h >= 0), zeros counted in C_TMP0
 __global__ void k_hrange(const float* __restrict__ h, int64_t n, unsigned long long* ctr) {
   unsigned mx = 0u, mn = 0x7f800000u;
-  int err = 0;
+  int err = 0, zeros = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     float v = h[i];
@@ -86,19 +68,24 @@ __global__ void k_hrange(const float* __restrict__ h, int64_t n, unsigned long l
       unsigned b = __float_as_uint(v);
       mx = max(mx, b);
       mn = min(mn, b);
+    } else {
+      ++zeros;
     }
   }
   mx = __reduce_max_sync(FULL_MASK, mx);
   mn = __reduce_min_sync(FULL_MASK, mn);
   err = __reduce_or_sync(FULL_MASK, err);
+  zeros = warp_sum_i(zeros);
   if ((threadIdx.x & 31) == 0) {
     atomicMax(&ctr[C_HMAXBITS], (unsigned long long)mx);
     atomicMin(&ctr[C_HMINBITS], (unsigned long long)mn);
     if (err) atomicOr(&ctr[C_ERR], (unsigned long long)err);
+    if (zeros) atomicAdd(&ctr[C_TMP0], (unsigned long long)zeros);
   }
 }
 
 // ---------------------------------------------------------------- a2 ---------
+// Binning in fp64 (R19): cell index floor(x * n_l / L) at the deepest level, clamped.
 __global__ void k_keys(const float* __restrict__ x, int64_t n, int nx, int ny, int nz, int depth,
                        double sx, double sy, double sz, uint64_t* __restrict__ keys,
                        uint32_t* __restrict__ vals) {
@@ -124,18 +111,13 @@ __global__ void k_keys(const float* __restrict__ x, int64_t n, int nx, int ny, i
 }
 
 // ---------------------------------------------------------------- a3 ---------
-__global__ void k_gather_build(const uint32_t* __restrict__ perm, int64_t n, const float* __restrict__ x,
-                               const float* __restrict__ hcur, const float* __restrict__ hb_o,
-                               const float* __restrict__ lo_o, const float* __restrict__ hi_o,
-                               float4* __restrict__ xh, float* __restrict__ hb, float* __restrict__ lo,
-                               float* __restrict__ hi) {
+// cell-order positions; h = h_in[perm] (caller order) or 0
+__global__ void k_pack(const uint32_t* __restrict__ perm, int64_t n, const float* __restrict__ x,
+                       const float* __restrict__ h_in, float4* __restrict__ xh) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n;
        s += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t p = perm[s];
-    xh[s] = make_float4(x[3 * (int64_t)p], x[3 * (int64_t)p + 1], x[3 * (int64_t)p + 2], hcur[p]);
-    hb[s] = hb_o[p];
-    if (lo) lo[s] = lo_o[p];
-    if (hi) hi[s] = hi_o[p];
+    const uint32_t p = perm[s];
+    xh[s] = make_float4(x[3 * (int64_t)p], x[3 * (int64_t)p + 1], x[3 * (int64_t)p + 2], h_in ? h_in[p] : 0.f);
   }
 }
 
@@ -168,31 +150,25 @@ __global__ void k_top_counts(int n0, int64_t n, NodeArrays N) {
 }
 
 // ---------------------------------------------------------------- a4 ---------
-// warp per node of one level: h_build max, fraction with h < edge/2, split decision
-// (P:510-518), child boundaries by binary search on the octant bits.
-__global__ void k_level_split(int a, int b, int level, int depth, const float* __restrict__ hb,
+// Warp per node of one level: split decision and child boundaries by binary
+// search on the octant bits of the sorted keys. hsplit == null: count rule alone.
+__global__ void k_level_split(int a, int b, int level, int depth, const float4* __restrict__ xh,
                               const uint64_t* __restrict__ keys, float half_edge, int split_count,
-                              float split_frac, int count_only, NodeArrays N, int* __restrict__ nch,
+                              float split_frac, NodeArrays N, int* __restrict__ nch,
                               int* __restrict__ chstart) {
   const int lane = threadIdx.x & 31;
   const int node = a + (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   if (node >= b) return;
   const int first = N.first[node], cnt = N.count[node];
-  float hm = 0.f;
-  int nsmall = 0;
-  for (int s = first + lane; s < first + cnt; s += 32) {
-    float h = hb[s];
-    hm = fmaxf(hm, h);
-    nsmall += (h < half_edge) ? 1 : 0;
+  bool frac_ok = true;
+  if (split_frac > 0.f && cnt > split_count && level < depth) {
+    int nsmall = 0;
+    for (int s = first + lane; s < first + cnt; s += 32) nsmall += (xh[s].w < half_edge) ? 1 : 0;
+    nsmall = warp_sum_i(nsmall);
+    frac_ok = (double)nsmall > (double)split_frac * (double)cnt;
   }
-  hm = warp_max_f(hm);
-  nsmall = warp_sum_i(nsmall);
-  int sp = (level < depth) && (cnt > split_count) &&
-           (count_only || (double)nsmall > (double)split_frac * (double)cnt);
-  if (lane == 0) {
-    N.hmaxb[node] = hm;
-    N.split[node] = sp;
-  }
+  const int sp = (level < depth) && (cnt > split_count) && frac_ok;
+  if (lane == 0) N.split[node] = sp;
   if (!sp) {
     if (lane == 0) nch[node - a] = 0;
     return;
@@ -250,136 +226,68 @@ __global__ void k_make_children(int a, int b, int64_t n_first_next, const int* _
   }
 }
 
-// ---------------------------------------------------------------- a5 ---------
-__global__ void k_top_slots(int n0, int nx, int ny, int nz, const int* __restrict__ topmap, NodeArrays N) {
-  int node = blockIdx.x * blockDim.x + threadIdx.x;
-  if (node >= n0) return;
-  int4 c = N.ijk[node];
-  for (int k = 0; k < 27; ++k) {
-    int y = -1;
-    if (k != 13) {
-      int ix = (c.x + off_x(k) + nx) % nx, iy = (c.y + off_y(k) + ny) % ny, iz = (c.z + off_z(k) + nz) % nz;
-      y = topmap[ix + (int64_t)nx * (iy + (int64_t)ny * iz)];
-    }
-    N.slot[27 * (int64_t)node + k] = y;
-  }
-}
-
-// slots of the nodes of level l >= 1 from their parent's slots (gather form: no atomics).
-// Every existing same-level neighbour is recorded; which pairs a level enumerates is
-// decided per particle by tau (k_tau), not per cell pair.
-__global__ void k_child_slots(int a, int b, NodeArrays N) {
-  int c = a + blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= b) return;
-  int X = N.parent[c];
-  int4 ijk = N.ijk[c];
-  int ax = ijk.x & 1, ay = ijk.y & 1, az = ijk.z & 1;
-  for (int k = 0; k < 27; ++k) {
-    int y = -1;
-    if (k != 13) {
-      int tx = ax + off_x(k), ty = ay + off_y(k), tz = az + off_z(k);
-      int Px = tx < 0 ? -1 : (tx >> 1), Py = ty < 0 ? -1 : (ty >> 1), Pz = tz < 0 ? -1 : (tz >> 1);
-      int bo = ((tx - 2 * Px) << 2) | ((ty - 2 * Py) << 1) | (tz - 2 * Pz);
-      if (Px == 0 && Py == 0 && Pz == 0) {
-        y = N.child[8 * (int64_t)X + bo];                          // sibling (self refinement)
-      } else {
-        int kp = (Px + 1) * 9 + (Py + 1) * 3 + (Pz + 1);
-        int Y = N.slot[27 * (int64_t)X + kp];
-        if (Y >= 0) y = N.child[8 * (int64_t)Y + bo];              // pair refinement
-      }
-    }
-    N.slot[27 * (int64_t)c + k] = y;
-  }
-}
-
-// tau_i = min(leaf level, deepest level l with min edge E_l >= h_build,i): at that level
-// every partner j with r < max(h_i, h_j) and tau_j >= tau_i lies in the 27 cells around i.
-__global__ void k_tau(int nnodes, NodeArrays N, LevelGeom g, const float* __restrict__ hb,
-                      uint8_t* __restrict__ tau) {
-  const int lane = threadIdx.x & 31;
-  const int node = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
-  if (node >= nnodes || N.split[node]) return;
-  const int first = N.first[node], cnt = N.count[node], L = N.ijk[node].w;
-  for (int s = first + lane; s < first + cnt; s += 32) {
-    const float h = hb[s] * 1.000001f;
-    int t = L;
-    while (t > 0 && 2.f * g.half_min[t] < h) --t;
-    tau[s] = (uint8_t)t;
-  }
-}
-
-__global__ void k_level_counts(int nnodes, NodeArrays N, const uint8_t* __restrict__ tau) {
+// per node max of a per-particle value (cell order), warp per node
+__global__ void k_node_hmax(int nnodes, NodeArrays N, const float* __restrict__ h) {
   const int lane = threadIdx.x & 31;
   const int node = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   if (node >= nnodes) return;
-  const int first = N.first[node], cnt = N.count[node], l = N.ijk[node].w;
-  int na = 0, nr = 0;
-  for (int s = first + lane; s < first + cnt; s += 32) {
-    const int t = tau[s];
-    na += t >= l;
-    nr += t == l;
-  }
-  na = warp_sum_i(na);
-  nr = warp_sum_i(nr);
-  if (lane == 0) {
-    N.nA[node] = na;
-    N.nR[node] = nr;
-  }
+  const int first = N.first[node], cnt = N.count[node];
+  float hm = 0.f;
+  for (int s = first + lane; s < first + cnt; s += 32) hm = fmaxf(hm, h[s]);
+  hm = warp_max_f(hm);
+  if (lane == 0) N.hmax[node] = hm;
 }
 
-// which lists a cell must provide as a source: its neighbour X (or itself, bit 13) sweeps
-// list A of this cell if X has targets with tau == l, list R if X has targets with tau > l.
-// A direction is stored presorted only if the list is longer than sort_min_len
-// and at least SORT_DEMAND_MIN targets sweep it; otherwise the sweeping warps read the whole
-// list with the box filter alone: a warp stages 32 sources at a time, so a sorted window
-// cannot save anything on a list of a few chunks, and sorting a list that one or two warps
-// visit costs more than it saves. An unsorted sweep reads a compacted copy (bit 13), or,
-// when every particle of the cell is a member (bit 14), the cell's own contiguous range.
-#define SORT_DEMAND_MIN 64
-#define LIST_RANGE 14
-__global__ void k_list_masks(int nnodes, NodeArrays N, int sort_min_len, int64_t* __restrict__ nsort /*[2*nnodes]*/) {
-  const int y = blockIdx.x * blockDim.x + threadIdx.x;
-  if (y >= nnodes) return;
-  const int na = N.nA[y], nr = N.nR[y], cnt = N.count[y];
-  (void)cnt;
-  int demA[14], demR[14];
-#pragma unroll
-  for (int d = 0; d < 14; ++d) demA[d] = demR[d] = 0;
-  for (int k = 0; k < 27; ++k) {
-    const int x = (k == 13) ? y : N.slot[27 * (int64_t)y + k];
-    if (x < 0) continue;
-    const int d = (k == 13) ? LIST_SELF : slot_dir(k);
-    demA[d] += N.nR[x];
-    demR[d] += N.nA[x] - N.nR[x];
-  }
-  const int uR = (nr == cnt) ? (1 << LIST_RANGE) : (1 << LIST_SELF);
-  int am = 0, rm = 0;
-#pragma unroll
-  for (int d = 0; d < 14; ++d) {
-    // list A (tau >= l) is never stored: it is swept as the cell's own range, culled down its
-    // sub-cells to the targets' reach and filtered by tau (cull_range) -- a 3D filter that
-    // beats a 1D projection window, so sorting it would not pay.
-    // With sort_min_len == 0 it is presorted along every swept direction (paper-literal).
-    if (na > 0 && demA[d] > 0) {
-      const bool srt = d != LIST_SELF && sort_min_len == 0;
-      am |= srt ? (1 << d) : (1 << LIST_RANGE);
+// initial guess from cell occupancy: N = (4 pi/3) n h^3 for a uniform number density n
+// (Eq. 3) -> h = cbrt(3 N_ngb / (4 pi n)). n is the largest number density among the leaf
+// and its ancestors holding >= GUESS_MIN_COUNT particles, up to the first ancestor holding
+// >= n_ngb: next to a dense clump a sparse cell's mean density hides the clump, and an
+// over-estimated h costs a long interaction list while an under-estimate costs one Newton
+// step. Written in cell order into xh[].w where h == 0.
+#define GUESS_MIN_COUNT 8
+__global__ void k_guess_h(int nnodes, NodeArrays N, LevelGeom g, float n_ngb, int min_count, float hcap,
+                          float4* __restrict__ xh) {
+  const int lane = threadIdx.x & 31;
+  const int x = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  if (x >= nnodes || N.split[x]) return;
+  double dens = 0.0;
+  int y = x;
+  while (true) {
+    const int cnt = N.count[y];
+    const int l = N.ijk[y].w;
+    if (cnt >= GUESS_MIN_COUNT) {
+      const double vol = (double)g.E[l][0] * g.E[l][1] * g.E[l][2];
+      dens = fmax(dens, (double)cnt / vol);
     }
-    if (nr > 0 && demR[d] > 0) {
-      const bool srt = d != LIST_SELF && (sort_min_len == 0 || (demR[d] >= SORT_DEMAND_MIN && nr > sort_min_len));
-      rm |= srt ? (1 << d) : uR;
+    if (cnt >= min_count || N.parent[y] < 0) {
+      if (dens == 0.0) dens = (double)cnt / ((double)g.E[l][0] * g.E[l][1] * g.E[l][2]);
+      break;
     }
+    y = N.parent[y];
   }
-  N.amask[y] = am;
-  N.rmask[y] = rm;
-  nsort[2 * (int64_t)y] = (int64_t)__popc(am & 0x3fff) * na;
-  nsort[2 * (int64_t)y + 1] = (int64_t)__popc(rm & 0x3fff) * nr;
+  float h = (float)cbrt(3.0 * n_ngb / (4.0 * 3.14159265358979323846 * dens));
+  h = fminf(h, hcap);
+  for (int s = N.first[x] + lane; s < N.first[x] + N.count[x]; s += 32)
+    if (xh[s].w == 0.f) xh[s].w = h;
 }
 
-__global__ void k_split_offsets(int nnodes, const int64_t* __restrict__ scan2, NodeArrays N) {
-  const int y = blockIdx.x * blockDim.x + threadIdx.x;
-  if (y >= nnodes) return;
-  N.offA[y] = scan2[2 * (int64_t)y];
-  N.offR[y] = scan2[2 * (int64_t)y + 1];
+// packed node records for the list walk: {first, count, first child (-1: none),
+// octant mask of the children | level << 8}; children are allocated contiguously in
+// octant order by k_make_children
+__global__ void k_node_rec(int nnodes, NodeArrays N, int4* __restrict__ rec) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= nnodes) return;
+  int base = -1, mask = 0;
+  if (N.split[x]) {
+    for (int o = 0; o < 8; ++o) {
+      const int ch = N.child[8 * (int64_t)x + o];
+      if (ch >= 0) {
+        if (base < 0) base = ch;
+        mask |= 1 << o;
+      }
+    }
+  }
+  rec[x] = make_int4(N.first[x], N.count[x], base, mask | (N.ijk[x].w << 8));
 }
 
 // ---------------------------------------------------------------- a6 ---------
@@ -392,45 +300,43 @@ struct SortEntry {  // 8 bytes: projection key and cell-order particle index
   int idx;
 };
 
-struct ListSeg {     // one (cell, kind) list family: members, directions, destination
-  int cnt, mask;
-  int64_t off;
-};
-__device__ __forceinline__ ListSeg list_seg(const NodeArrays& N, int node, int kind) {
-  ListSeg L;
-  L.cnt = kind ? N.nR[node] : N.nA[node];
-  L.mask = kind ? N.rmask[node] : N.amask[node];
-  L.off = kind ? N.offR[node] : N.offA[node];
-  return L;
+#define SORT_BLOCK_MAX 4096
+// number of sorted entries of each leaf: 13 * count if it is presorted
+__global__ void k_sort_sizes(int nnodes, NodeArrays N, int sort_min_len, int64_t* __restrict__ sz) {
+  const int y = blockIdx.x * blockDim.x + threadIdx.x;
+  if (y >= nnodes) return;
+  const int cnt = N.count[y];
+  const bool srt = !N.split[y] && cnt > sort_min_len && cnt <= SORT_BLOCK_MAX && cnt > 1;
+  sz[y] = srt ? 13 * (int64_t)cnt : 0;
 }
-__device__ __forceinline__ bool list_member(int t, int l, int kind) { return kind ? (t == l) : (t >= l); }
+__global__ void k_sort_offsets(int nnodes, const int64_t* __restrict__ sz, const int64_t* __restrict__ scan,
+                               NodeArrays N) {
+  const int y = blockIdx.x * blockDim.x + threadIdx.x;
+  if (y >= nnodes) return;
+  N.sortoff[y] = sz[y] > 0 ? scan[y] : -1;
+}
 
-// warp per (node, kind) with node count <= 32: one particle per lane, warp bitonic sort
-__global__ void k_sort_warp(int nnodes, const float4* __restrict__ xh, const uint8_t* __restrict__ tau,
-                            NodeArrays N, LevelGeom g, SortEntry* __restrict__ out) {
+// warp per leaf with count <= 32: warp bitonic sort of (key, lane) per direction
+__global__ void k_sort_leaf_warp(int nnodes, const float4* __restrict__ xh, NodeArrays N, LevelGeom g,
+                                 SortEntry* __restrict__ out) {
   const int lane = threadIdx.x & 31;
-  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int node = (int)(wid >> 1), kind = (int)(wid & 1);
+  const int node = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   if (node >= nnodes) return;
-  const ListSeg L = list_seg(N, node, kind);
-  const int cnt_node = N.count[node];
-  if ((L.mask & 0x3fff) == 0 || L.cnt == 0 || cnt_node > 32) return;
+  const int64_t off = N.sortoff[node];
+  const int cnt = N.count[node];
+  if (off < 0 || cnt > 32) return;
   const int first = N.first[node];
   const int4 c = N.ijk[node];
   float rx = 0.f, ry = 0.f, rz = 0.f;
-  bool mem = false;
-  if (lane < cnt_node) {
+  if (lane < cnt) {
     float4 p = xh[first + lane];
     rx = p.x - node_corner(c.x, c.w, 0, g);
     ry = p.y - node_corner(c.y, c.w, 1, g);
     rz = p.z - node_corner(c.z, c.w, 2, g);
-    mem = list_member(tau[first + lane], c.w, kind);
   }
-  int r = 0;
-  for (int d = 0; d < 14; ++d) {
-    if (!((L.mask >> d) & 1)) continue;
-    float key = (d == LIST_SELF) ? 0.f : proj(rx, ry, rz, dir_unit(d));
-    uint64_t v = mem ? (((uint64_t)float_ord(key) << 32) | (uint32_t)lane) : ~0ull;
+  for (int d = 0; d < 13; ++d) {
+    const float key = proj(rx, ry, rz, dir_unit(d));
+    uint64_t v = lane < cnt ? (((uint64_t)float_ord(key) << 32) | (uint32_t)lane) : ~0ull;
 #pragma unroll
     for (int size = 2; size <= 32; size <<= 1) {
 #pragma unroll
@@ -442,75 +348,34 @@ __global__ void k_sort_warp(int nnodes, const float4* __restrict__ xh, const uin
         v = (lower == up) ? mn : mx;
       }
     }
-    int li = (lane < L.cnt) ? (int)(uint32_t)v : 0;
-    float kk = __shfl_sync(FULL_MASK, key, li);
-    if (lane < L.cnt) out[L.off + (int64_t)r * L.cnt + lane] = SortEntry{kk, first + li};
-    ++r;
+    const int li = (lane < cnt) ? (int)(uint32_t)v : 0;
+    const float kk = __shfl_sync(FULL_MASK, key, li);
+    if (lane < cnt) out[off + (int64_t)d * cnt + lane] = SortEntry{kk, first + li};
   }
 }
 
-// deterministic block compaction of the members of (node, kind) into smem (cell order)
-__device__ __forceinline__ int block_compact_members(int first, int cnt_node, int l, int kind,
-                                                     const uint8_t* __restrict__ tau, int* mem, int cap,
-                                                     int* wsum) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  int total = 0;
-  for (int base = 0; base < cnt_node; base += blockDim.x) {
-    const int i = base + threadIdx.x;
-    const bool m = i < cnt_node && list_member(tau[first + i], l, kind);
-    const unsigned bal = __ballot_sync(FULL_MASK, m);
-    if (lane == 0) wsum[w] = __popc(bal);
-    __syncthreads();
-    int before = 0;
-    for (int ww = 0; ww < w; ++ww) before += wsum[ww];
-    int tot = 0;
-    for (int ww = 0; ww < nw; ++ww) tot += wsum[ww];
-    const int pos = total + before + __popc(bal & lanemask_lt());
-    if (m && pos < cap) mem[pos] = i;
-    total += tot;
-    __syncthreads();
-  }
-  return total;
-}
-
-#define SORT_BLOCK_MAX 4096
-// CTA per (node, kind) with 32 < node count and members <= SORT_BLOCK_MAX: shared-memory
-// bitonic sort per direction of (key, member index) composites
-__global__ void __launch_bounds__(512) k_sort_block(int nnodes, const float4* __restrict__ xh,
-                                                     const uint8_t* __restrict__ tau, NodeArrays N, LevelGeom g,
-                                                     SortEntry* __restrict__ out) {
+// CTA per leaf with 32 < count <= SORT_BLOCK_MAX: shared-memory bitonic sort per direction
+__global__ void __launch_bounds__(512) k_sort_leaf_block(int nnodes, const float4* __restrict__ xh, NodeArrays N,
+                                                         LevelGeom g, SortEntry* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char sb_raw[];
   uint64_t* sk = reinterpret_cast<uint64_t*>(sb_raw);
   float* skey = reinterpret_cast<float*>(sk + SORT_BLOCK_MAX);
-  int* mem = reinterpret_cast<int*>(skey + SORT_BLOCK_MAX);
-  __shared__ int wsum[32];
-  const int node = blockIdx.x >> 1, kind = blockIdx.x & 1;
+  const int node = blockIdx.x;
   if (node >= nnodes) return;
-  const ListSeg L = list_seg(N, node, kind);
-  const int cnt_node = N.count[node];
-  if ((L.mask & 0x3fff) == 0 || L.cnt == 0 || cnt_node <= 32 || L.cnt > SORT_BLOCK_MAX) return;
+  const int64_t off = N.sortoff[node];
+  const int cnt = N.count[node];
+  if (off < 0 || cnt <= 32) return;
   const int first = N.first[node];
   const int4 c = N.ijk[node];
-  block_compact_members(first, cnt_node, c.w, kind, tau, mem, SORT_BLOCK_MAX, wsum);
-  const int cnt = L.cnt;
-  const float cx = node_corner(c.x, c.w, 0, g), cy = node_corner(c.y, c.w, 1, g),
-              cz = node_corner(c.z, c.w, 2, g);
+  const float cx = node_corner(c.x, c.w, 0, g), cy = node_corner(c.y, c.w, 1, g), cz = node_corner(c.z, c.w, 2, g);
   int P = 64;
   while (P < cnt) P <<= 1;
-  int r = 0;
-  for (int d = 0; d < 14; ++d) {
-    if (!((L.mask >> d) & 1)) continue;
-    if (d == LIST_SELF) {
-      for (int i = threadIdx.x; i < cnt; i += blockDim.x)
-        out[L.off + (int64_t)r * cnt + i] = SortEntry{0.f, first + mem[i]};
-      ++r;
-      continue;
-    }
-    float3 dv = dir_unit(d);
+  for (int d = 0; d < 13; ++d) {
+    const float3 dv = dir_unit(d);
     for (int i = threadIdx.x; i < P; i += blockDim.x) {
       if (i < cnt) {
-        float4 p = xh[first + mem[i]];
-        float key = proj(p.x - cx, p.y - cy, p.z - cz, dv);
+        const float4 p = xh[first + i];
+        const float key = proj(p.x - cx, p.y - cy, p.z - cz, dv);
         skey[i] = key;
         sk[i] = ((uint64_t)float_ord(key) << 32) | (uint32_t)i;
       } else {
@@ -521,10 +386,10 @@ __global__ void __launch_bounds__(512) k_sort_block(int nnodes, const float4* __
     for (int size = 2; size <= P; size <<= 1) {
       for (int stride = size >> 1; stride > 0; stride >>= 1) {
         for (int i = threadIdx.x; i < P / 2; i += blockDim.x) {
-          int lo = 2 * i - (i & (stride - 1));
-          int hi = lo + stride;
-          bool up = ((lo & size) == 0);
-          uint64_t A = sk[lo], B = sk[hi];
+          const int lo = 2 * i - (i & (stride - 1));
+          const int hi = lo + stride;
+          const bool up = ((lo & size) == 0);
+          const uint64_t A = sk[lo], B = sk[hi];
           if ((A > B) == up) {
             sk[lo] = B;
             sk[hi] = A;
@@ -534,223 +399,78 @@ __global__ void __launch_bounds__(512) k_sort_block(int nnodes, const float4* __
       }
     }
     for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-      int li = (int)(uint32_t)sk[i];
-      out[L.off + (int64_t)r * cnt + i] = SortEntry{skey[li], first + mem[li]};
+      const int li = (int)(uint32_t)sk[i];
+      out[off + (int64_t)d * cnt + i] = SortEntry{skey[li], first + li};
     }
     __syncthreads();
-    ++r;
   }
 }
 
-// big lists (members > SORT_BLOCK_MAX): composite keys (segment, key) for the radix sort.
-// Segment ids grow with the destination offset, so the sorted order is the layout order.
-__global__ void __launch_bounds__(512) k_big_keys(int nbig, const int* __restrict__ bigseg,
-                                                  const int64_t* __restrict__ bigoff, const float4* __restrict__ xh,
-                                                  const uint8_t* __restrict__ tau, NodeArrays N, LevelGeom g,
-                                                  uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
-  __shared__ int wsum[32];
-  const int bi = blockIdx.x;
-  if (bi >= nbig) return;
-  const int node = bigseg[bi] >> 1, kind = bigseg[bi] & 1;
-  const ListSeg L = list_seg(N, node, kind);
-  const int first = N.first[node], cnt_node = N.count[node];
-  const int4 c = N.ijk[node];
-  const float cx = node_corner(c.x, c.w, 0, g), cy = node_corner(c.y, c.w, 1, g),
-              cz = node_corner(c.z, c.w, 2, g);
-  const int64_t base = bigoff[bi];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  int total = 0;
-  for (int b0 = 0; b0 < cnt_node; b0 += blockDim.x) {
-    const int i = b0 + threadIdx.x;
-    const bool m = i < cnt_node && list_member(tau[first + i], c.w, kind);
-    const unsigned bal = __ballot_sync(FULL_MASK, m);
-    if (lane == 0) wsum[w] = __popc(bal);
-    __syncthreads();
-    int before = 0, tot = 0;
-    for (int ww = 0; ww < nw; ++ww) {
-      if (ww < w) before += wsum[ww];
-      tot += wsum[ww];
-    }
-    if (m) {
-      const int pos = total + before + __popc(bal & lanemask_lt());
-      const float4 p = xh[first + i];
-      int r = 0;
-      for (int d = 0; d < 14; ++d) {
-        if (!((L.mask >> d) & 1)) continue;
-        const float key = (d == LIST_SELF) ? 0.f : proj(p.x - cx, p.y - cy, p.z - cz, dir_unit(d));
-        const uint64_t seg = (uint64_t)bi * 14 + r;
-        keys[base + (int64_t)r * L.cnt + pos] = (seg << 32) | float_ord(key);
-        vals[base + (int64_t)r * L.cnt + pos] = (uint32_t)(first + i);
-        ++r;
+// ---------------------------------------------------------------- groups -----
+// Targets in groups of <= SPH_GROUP particles (one warp each in the interaction kernels),
+// each a contiguous range of the cell order that lies inside one cell:
+//   * the children of a split cell that are leaves are packed greedily, in octant order,
+//     into runs of consecutive siblings holding <= SPH_GROUP particles (consecutive
+//     siblings are contiguous in memory, and they all lie inside the parent's box);
+//   * a leaf with more than SPH_GROUP particles (the paper's split rule keeps leaves of
+//     up to split_count particles; coincident particles at the deepest level) is cut into
+//     balanced chunks of consecutive particles (Morton order inside the leaf);
+//   * a top-level leaf is its own group.
+// int4 {node, first, count, -}.
+__device__ __forceinline__ int n_chunks(int cnt) { return (cnt + SPH_GROUP - 1) / SPH_GROUP; }
+
+template <bool WRITE>
+__device__ __forceinline__ int pack_children(const NodeArrays& N, int x, int4* out) {
+  int g = 0, acc = 0, first = 0;
+  for (int o = 0; o < 8; ++o) {
+    const int ch = N.child[8 * (int64_t)x + o];
+    if (ch < 0) continue;
+    const int cnt = N.count[ch];
+    if (N.split[ch] || cnt > SPH_GROUP) {            // handled at its own node
+      if (acc > 0) {
+        if (WRITE) out[g] = make_int4(x, first, acc, 0);
+        ++g;
+        acc = 0;
       }
+      continue;
     }
-    total += tot;
-    __syncthreads();
-  }
-}
-
-__device__ __forceinline__ float ord_float(uint32_t u) {
-  uint32_t b = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
-  return __uint_as_float(b);
-}
-
-__global__ void k_big_write(int nbig, const int* __restrict__ bigseg, const int64_t* __restrict__ bigoff,
-                            NodeArrays N, const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals,
-                            SortEntry* __restrict__ out) {
-  int bi = blockIdx.x;
-  if (bi >= nbig) return;
-  const ListSeg L = list_seg(N, bigseg[bi] >> 1, bigseg[bi] & 1);
-  int64_t n_ent = (int64_t)__popc(L.mask & 0x3fff) * L.cnt;
-  int64_t src = bigoff[bi];
-  for (int64_t i = threadIdx.x; i < n_ent; i += blockDim.x)
-    out[L.off + i] = SortEntry{ord_float((uint32_t)keys[src + i]), (int)vals[src + i]};
-}
-
-__global__ void k_mark_big(int nnodes, NodeArrays N, int* __restrict__ flag, int64_t* __restrict__ sz) {
-  int x = blockIdx.x * blockDim.x + threadIdx.x;
-  if (x >= 2 * nnodes) return;
-  const ListSeg L = list_seg(N, x >> 1, x & 1);
-  bool big = (L.mask & 0x3fff) != 0 && L.cnt > SORT_BLOCK_MAX;
-  flag[x] = big ? 1 : 0;
-  sz[x] = big ? (int64_t)__popc(L.mask & 0x3fff) * L.cnt : 0;
-}
-
-__global__ void k_compact_big(int nseg, const int* __restrict__ flag, const int* __restrict__ idx,
-                              const int64_t* __restrict__ szscan, int* __restrict__ bigseg,
-                              int64_t* __restrict__ bigoff) {
-  int x = blockIdx.x * blockDim.x + threadIdx.x;
-  if (x >= nseg || !flag[x]) return;
-  bigseg[idx[x]] = x;
-  bigoff[idx[x]] = szscan[x];
-}
-
-// Per target cell X and kind (0: A-lists for targets with tau == level, 1: R-lists for
-// deeper targets): the non-empty source lists of the 27 cells around X, as descriptors
-// with the list offset for the sweep direction, the periodic shift and Y's corner.
-struct SegDesc {   // 32 bytes
-  long long off;   // first entry of the list in the sweep direction
-  int cnt;         // entries
-  int meta;        // bits 0-4 k (slot), 5 flip, 6 self (k == 13), 7 swept whole (no window),
-                   // 8-13 shift codes (2 bits/axis: 1 = +1, 2 = -1), 14 list = cell range,
-                   // 15 range holds non-members (keep tau >= level only), 16-19 dir
-  float cx, cy, cz;  // Y's corner + source shift (frame of the keys)
-  int Y;
-};
-
-__device__ __forceinline__ bool seg_needed(const NodeArrays& N, int X, int kind) {
-  return kind ? (N.nA[X] - N.nR[X]) > 0 : N.nR[X] > 0;
-}
-
-__global__ void k_seg_count(int nnodes, NodeArrays N, int* __restrict__ cnt2) {
-  const int X = blockIdx.x * blockDim.x + threadIdx.x;
-  if (X >= nnodes) return;
-  for (int kind = 0; kind < 2; ++kind) {
-    int c = 0;
-    if (seg_needed(N, X, kind)) {
-      for (int k = 0; k < 27; ++k) {
-        const int Y = (k == 13) ? X : N.slot[27 * (int64_t)X + k];
-        if (Y >= 0 && (kind ? N.nR[Y] : N.nA[Y]) > 0) ++c;
-      }
+    if (acc + cnt > SPH_GROUP) {
+      if (WRITE) out[g] = make_int4(x, first, acc, 0);
+      ++g;
+      acc = 0;
     }
-    cnt2[2 * X + kind] = c;
+    if (acc == 0) first = N.first[ch];
+    acc += cnt;
   }
+  if (acc > 0) {
+    if (WRITE) out[g] = make_int4(x, first, acc, 0);
+    ++g;
+  }
+  return g;
 }
 
-__global__ void k_seg_fill(int nnodes, NodeArrays N, LevelGeom g, const int* __restrict__ off2,
-                           SegDesc* __restrict__ out) {
-  const int X = blockIdx.x * blockDim.x + threadIdx.x;
-  if (X >= nnodes) return;
-  const int4 cX = N.ijk[X];
-  const int l = cX.w;
-  for (int kind = 0; kind < 2; ++kind) {
-    if (!seg_needed(N, X, kind)) continue;
-    int o = off2[2 * X + kind];
-    for (int k = 0; k < 27; ++k) {
-      const int Y = (k == 13) ? X : N.slot[27 * (int64_t)X + k];
-      if (Y < 0) continue;
-      const ListSeg L = list_seg(N, Y, kind);
-      if (L.cnt == 0) continue;
-      int d = (k == 13) ? LIST_SELF : slot_dir(k);
-      const bool unsorted = (d == LIST_SELF) || !((L.mask >> d) & 1);   // swept whole, no window
-      const bool range = unsorted && ((L.mask >> LIST_RANGE) & 1);       // = the cell's own range
-      const bool tfilter = range && kind == 0 && N.nA[Y] != N.count[Y];  // range holds non-members
-      if (unsorted) d = LIST_SELF;
-      SegDesc sd;
-      sd.off = range ? (long long)N.first[Y] : L.off + (long long)__popc(L.mask & ((1 << d) - 1)) * L.cnt;
-      sd.cnt = range ? N.count[Y] : L.cnt;
-      sd.Y = Y;
-      int meta = k | (slot_flip(k) ? 32 : 0) | (k == 13 ? 64 : 0) | (unsorted ? 128 : 0) | (range ? (1 << 14) : 0) |
-                 (tfilter ? (1 << 15) : 0) | (d << 16);
-      float so[3] = {0.f, 0.f, 0.f};
-      if (k != 13) {
-        const int4 cY = N.ijk[Y];
-        const int dd[3] = {cX.x + off_x(k) - cY.x, cX.y + off_y(k) - cY.y, cX.z + off_z(k) - cY.z};
-        for (int a = 0; a < 3; ++a) {
-          const int sa = dd[a] > 1 ? 1 : (dd[a] < -1 ? -1 : 0);
-          meta |= (sa > 0 ? 1 : (sa < 0 ? 2 : 0)) << (8 + 2 * a);
-          so[a] = sa < 0 ? -g.L[a] : 0.f;
-        }
-        sd.cx = node_corner(cY.x, l, 0, g) + so[0];
-        sd.cy = node_corner(cY.y, l, 1, g) + so[1];
-        sd.cz = node_corner(cY.z, l, 2, g) + so[2];
-      } else {
-        sd.cx = sd.cy = sd.cz = 0.f;
-      }
-      sd.meta = meta;
-      out[o++] = sd;
-    }
-  }
-}
-
-// ---------------------------------------------------------------- tasks ------
-// Work unit of the interaction kernels: a leaf cell's particles in chunks of 32 (cell order).
-__global__ void k_leaf_chunks(int nnodes, NodeArrays N, int* __restrict__ nchunk) {
-  int x = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void k_group_count(int nnodes, NodeArrays N, int* __restrict__ ng) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= nnodes) return;
-  nchunk[x] = N.split[x] ? 0 : (N.count[x] + 31) >> 5;
+  const int cnt = N.count[x];
+  int g = 0;
+  if (N.split[x]) g = pack_children<false>(N, x, nullptr);
+  else if (N.parent[x] < 0 || cnt > SPH_GROUP) g = n_chunks(cnt);
+  ng[x] = g;
 }
 
-__global__ void k_write_tasks(int nnodes, NodeArrays N, const int* __restrict__ nchunk, const int* __restrict__ scan,
-                              int4* __restrict__ tasks) {
-  int x = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void k_group_write(int nnodes, NodeArrays N, const int* __restrict__ scan, int4* __restrict__ groups) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= nnodes) return;
-  const int c = nchunk[x], b = scan[x], first = N.first[x], cnt = N.count[x];
-  for (int i = 0; i < c; ++i) tasks[b + i] = make_int4(x, first + 32 * i, min(32, cnt - 32 * i), 0);
-}
-
-// per node max of the final h over lists A and R (force window)
-__global__ void k_node_hmax(int nnodes, NodeArrays N, const float4* __restrict__ xh, const uint8_t* __restrict__ tau) {
-  const int lane = threadIdx.x & 31;
-  const int node = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
-  if (node >= nnodes) return;
-  const int first = N.first[node], cnt = N.count[node], l = N.ijk[node].w;
-  float ha = 0.f, hr = 0.f;
-  for (int s = first + lane; s < first + cnt; s += 32) {
-    const int t = tau[s];
-    const float h = xh[s].w;
-    if (t >= l) ha = fmaxf(ha, h);
-    if (t == l) hr = fmaxf(hr, h);
+  const int cnt = N.count[x], first = N.first[x];
+  int4* out = groups + scan[x];
+  if (N.split[x]) {
+    pack_children<true>(N, x, out);
+  } else if (N.parent[x] < 0 || cnt > SPH_GROUP) {
+    const int c = n_chunks(cnt);
+    for (int i = 0; i < c; ++i) {      // balanced: 40 -> 20 + 20
+      const int s0 = (int)((int64_t)cnt * i / c), s1 = (int)((int64_t)cnt * (i + 1) / c);
+      out[i] = make_int4(x, first + s0, s1 - s0, 0);
+    }
   }
-  ha = warp_max_f(ha);
-  hr = warp_max_f(hr);
-  if (lane == 0) {
-    N.hmaxA[node] = ha;
-    N.hmaxR[node] = hr;
-  }
-}
-
-// initial guess from cell occupancy: N = (4 pi/3) n h^3 for uniform density n (Eq. 3)
-// -> h = cbrt(3 N_ngb / (4 pi n)); n from the leaf, or its parent if the leaf is sparse.
-__global__ void k_guess_h(int nnodes, NodeArrays N, LevelGeom g, const uint32_t* __restrict__ perm,
-                          float n_ngb, int min_count, float hcap, float* __restrict__ hguess_orig) {
-  int x = blockIdx.x * blockDim.x + threadIdx.x;
-  if (x >= nnodes || N.split[x]) return;
-  int y = x;
-  while (N.count[y] < min_count && N.parent[y] >= 0) y = N.parent[y];
-  int l = N.ijk[y].w;
-  double vol = (double)g.E[l][0] * g.E[l][1] * g.E[l][2];
-  double dens = (double)N.count[y] / vol;
-  float h = (float)cbrt(3.0 * n_ngb / (4.0 * 3.14159265358979323846 * dens));
-  h = fminf(h, hcap);
-  for (int s = N.first[x]; s < N.first[x] + N.count[x]; ++s) hguess_orig[perm[s]] = h;
 }

@@ -77,9 +77,11 @@ __device__ __forceinline__ float3 dir_unit(int d) { return make_float3(c_dirs[d]
 // ---------------------------------------------------------------- constants --
 #define SPH_PI_F 3.14159265358979323846f
 #define SPH_CNORM (8.0f / SPH_PI_F)   // 8/pi of W
-#define SPH_MAX_DEPTH 10              // Morton levels below the top grid
-#define SPH_NSLOT 27
-#define SPH_COLD_MARGIN 1.3f          // extra h_build margin when h0 is the occupancy guess
+#define SPH_MAX_DEPTH 12              // Morton levels below the top grid
+#define SPH_COLD_MARGIN 1.25f         // h_build / h when h0 is the occupancy guess
+#define SPH_IDX_BITS 27               // list entry = (periodic image code << 27) | source index
+#define SPH_IDX_MASK ((1u << SPH_IDX_BITS) - 1u)
+#define SPH_GROUP 32                  // targets per group (one warp, one lane per target)
 
 // ---------------------------------------------------------------- context ----
 struct DBuf {
@@ -101,62 +103,61 @@ struct sph_ctx {
 
   int64_t n = 0;        // particles in the structure: owned + halo
   int64_t n_own = 0;    // owned (targets); caller indices >= n_own are halo (sources only)
-  int64_t loose = 0;    // particles whose final h exceeds their cells' h_build
-  bool force_ready = false;
-  int state = 0;  // 0 nothing, 1 cells built, 2 density done
+  int state = 0;        // 0 nothing, 1 cells built, 2 density done
+  bool force_lists = false;
+  bool cold = false;       // h0 was the occupancy guess (wider list margin, N-only first pass)
 
-  // geometry of the current structure
+  // geometry of the current structure (built once per sph_build_cells)
   int ntop[3] = {0, 0, 0};
   double E0[3] = {0, 0, 0};
   int depth = 0;             // Morton levels below top (keys carry 3*depth bits)
   int top_bits = 0;
   std::vector<int> lev_off;  // node index offsets per level (size nlevels+1)
-  int n_nodes = 0, n_leaves = 0;
+  int n_nodes = 0, n_leaves = 0, n_groups = 0;
   int64_t n_sorted = 0;      // entries of all 13-direction lists
-  int64_t n_pair_slots = 0;
-  int64_t rebuilds = 0;
-  float margin_used = 1.1f;  // h_build / h of the current structure
+  int64_t pool_dens = 0;     // used entries of the density list pool
+  int64_t pool_force = 0;    // entries of the force lists
+  int64_t list_rebuilds = 0; // groups whose density list was rebuilt for a grown h
+  float hb_max = 0.f;        // largest h_build (density reach)
 
   // named device buffers
-  DBuf b[96];
+  DBuf b[64];
   cudaEvent_t ev[12];
   bool ev_ok = false;
 };
 
 enum BufId {
-  // caller-order inputs / iteration state
-  B_XIN = 0, B_HIN, B_HB_ORIG, B_HCUR_O, B_LO_O, B_HI_O, B_VIN, B_MIN, B_UIN,
+  // caller-order inputs / outputs kept between calls
+  B_XIN = 0, B_HIN, B_VIN, B_MIN, B_UIN, B_HFIN_O, B_GST_O,
   // sort scratch
   B_KEYS0, B_KEYS1, B_VALS0, B_VALS1, B_SORT_HIST, B_SORT_STATUS, B_SORT_CTR, B_SCAN_TMP,
   // cell-order particle arrays
-  B_PERM, B_XH, B_VM, B_U, B_HB, B_HLO, B_HHI, B_FLAG, B_DSUMF, B_DACC0, B_DACC1, B_FX, B_FS,
+  B_PERM, B_XH, B_VM, B_U, B_HB, B_HLO, B_HHI, B_STATE, B_DSUMF, B_DACC0, B_DACC1, B_DSUM2,
+  B_FX, B_FS,
   // nodes
-  B_N_FIRST, B_N_COUNT, B_N_IJK, B_N_PARENT, B_N_CHILD, B_N_HMAXB, B_N_SPLIT, B_N_SLOT, B_N_NA,
-  B_N_NR, B_N_AMASK, B_N_RMASK, B_N_OFFA, B_N_OFFR, B_N_HMAXA, B_N_HMAXR, B_N_NCH, B_N_CHBASE, B_N_NSORT,
-  B_TAU, B_DSUM2, B_HFIN_O, B_GST_O, B_STATE_O, B_SF_O, B_ACC0_O, B_ACC1_O, B_SEGCNT2, B_SEGOFF2, B_SEGDESC,
-  // lists / tasks
-  B_SORTED, B_TOPMAP, B_TASKS, B_TASKS2, B_TASKFLAG, B_TASKIDX, B_TMPI0, B_TMPI1, B_TMPL0, B_TMPL1,
-  B_BIGNODES, B_BIGOFF,
-  // misc
-  B_COUNTERS, B_OUT0, B_OUT1, B_OUT2, B_OUT3, B_OUT4, B_OUT5,
+  B_N_FIRST, B_N_COUNT, B_N_IJK, B_N_PARENT, B_N_CHILD, B_N_SPLIT, B_N_HMAX, B_N_SORTOFF, B_N_REC, B_N_NCH, B_N_CHBASE,
+  B_TOPMAP,
+  // 13-direction sorted lists
+  B_SORTED,
+  // groups and interaction lists
+  B_GROUPS, B_GOFF, B_GLEN, B_FOFF, B_FLEN, B_LISTD, B_LISTF, B_GFLAG, B_GIDX, B_GSEL,
+  // misc scratch
+  B_TMPI0, B_TMPI1, B_TMPL0, B_TMPL1, B_COUNTERS, B_OUT0, B_OUT1, B_OUT2, B_OUT3, B_OUT4, B_OUT5,
   B_COUNT
 };
-static_assert(B_COUNT <= 96, "too many buffers");
+static_assert(B_COUNT <= 64, "too many buffers");
 
 // device counters layout (int64 slots in B_COUNTERS)
 enum CounterId {
   C_ERR = 0,        // error bits (validation)
   C_UNCONV,         // unconverged particles after an h update
-  C_REBUILD,        // particles whose h wants to exceed its build h
-  C_CAND,           // candidate distance tests
+  C_REGROW,         // particles whose h outgrew their list reach (group list rebuild)
+  C_CAND,           // candidate distance tests (lane tests against staged sources)
   C_NDIR,           // D
   C_NFORCE,         // sum of force neighbour counts (2F)
   C_HMAXBITS,       // max h (float bits as int)
   C_HMINBITS,       // min positive h (float bits)
-  C_TASKS,          // active tasks
   C_TMP0, C_TMP1, C_TMP2,
-  C_MAXCH,          // max chunks of one warp (load balance diagnostics)
-  C_HEAVY,          // chunks of warps with > 2000 chunks
   C_NCOUNTERS
 };
 

@@ -12,6 +12,7 @@
 #include "radix_sort.cuh"
 #include "scan.cuh"
 #include "build.cuh"
+#include "lists.cuh"
 #include "interact.cuh"
 
 // =========================================================== memory =============
@@ -76,12 +77,8 @@ static int gridfull(int64_t n, int block) { return (int)std::max<int64_t>((n + b
 static void sync(sph_ctx* c) { CUDA_TRY(cudaStreamSynchronize(c->stream)); }
 
 static bool dbg_on() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SPH_DEBUG");
-    v = (e && e[0] && e[0] != '0') ? 1 : 0;
-  }
-  return v == 1;
+  const char* e = getenv("SPH_DEBUG");
+  return e && e[0] && e[0] != '0';
 }
 #define DBG(...) do { if (dbg_on()) { fprintf(stderr, "[sph] " __VA_ARGS__); fflush(stderr); } } while (0)
 // debug wall-clock of a region (device-synchronised), only when SPH_DEBUG is set
@@ -188,17 +185,10 @@ static NodeArrays nodes(sph_ctx* c) {
   N.ijk = Bget<int4>(c, B_N_IJK);
   N.parent = Bget<int>(c, B_N_PARENT);
   N.child = Bget<int>(c, B_N_CHILD);
-  N.hmaxb = Bget<float>(c, B_N_HMAXB);
   N.split = Bget<int>(c, B_N_SPLIT);
-  N.slot = Bget<int>(c, B_N_SLOT);
-  N.nA = Bget<int>(c, B_N_NA);
-  N.nR = Bget<int>(c, B_N_NR);
-  N.amask = Bget<int>(c, B_N_AMASK);
-  N.rmask = Bget<int>(c, B_N_RMASK);
-  N.offA = Bget<int64_t>(c, B_N_OFFA);
-  N.offR = Bget<int64_t>(c, B_N_OFFR);
-  N.hmaxA = Bget<float>(c, B_N_HMAXA);
-  N.hmaxR = Bget<float>(c, B_N_HMAXR);
+  N.hmax = Bget<float>(c, B_N_HMAX);
+  N.sortoff = Bget<int64_t>(c, B_N_SORTOFF);
+  N.rec = Bget<int4>(c, B_N_REC);
   return N;
 }
 
@@ -208,31 +198,26 @@ static void ensure_nodes(sph_ctx* c, int64_t cap) {
   B<int4>(c, B_N_IJK, cap, true);
   B<int>(c, B_N_PARENT, cap, true);
   B<int>(c, B_N_CHILD, 8 * cap, true);
-  B<float>(c, B_N_HMAXB, cap, true);
   B<int>(c, B_N_SPLIT, cap, true);
 }
 
 static LevelGeom level_geom(sph_ctx* c) {
   LevelGeom g;
   memset(&g, 0, sizeof(g));
-  for (int l = 0; l <= SPH_MAX_DEPTH + 1; ++l) {
-    float hm = 1e30f;
-    for (int k = 0; k < 3; ++k) {
-      g.E[l][k] = (float)(c->E0[k] / (double)(1 << l));
-      g.n[l][k] = c->ntop[k] << std::min(l, 20);
-      hm = std::min(hm, (float)(0.5 * c->E0[k] / (double)(1 << l)));
-    }
-    g.half_min[l] = hm;
+  for (int l = 0; l <= SPH_MAX_DEPTH + 1; ++l)
+    for (int k = 0; k < 3; ++k) g.E[l][k] = (float)(c->E0[k] / (double)(1 << l));
+  for (int k = 0; k < 3; ++k) {
+    g.L[k] = (float)c->cfg.box[k];
+    g.ntop[k] = c->ntop[k];
   }
-  for (int k = 0; k < 3; ++k) g.L[k] = (float)c->cfg.box[k];
   g.depth = c->depth;
   return g;
 }
 
-// largest h the cells may be built for: 3 top cells per axis (with rounding slack)
-static float hb_cap(sph_ctx* c) {
+// largest h the iteration may reach: below half the smallest box edge (minimum image, R19)
+static float h_cap(sph_ctx* c) {
   double Lmin = std::min(c->cfg.box[0], std::min(c->cfg.box[1], c->cfg.box[2]));
-  return (float)(Lmin / (3.0 * c->cfg.top_edge_factor) * (1.0 - 1e-5));
+  return (float)(0.5 * Lmin * (1.0 - 1e-4));
 }
 
 static float as_float(unsigned long long b) {
@@ -242,101 +227,93 @@ static float as_float(unsigned long long b) {
   return f;
 }
 
+static float3 box3(sph_ctx* c) {
+  return make_float3((float)c->cfg.box[0], (float)c->cfg.box[1], (float)c->cfg.box[2]);
+}
+
 // =========================================================== build ==============
-// Builds the structure for the caller-order state in B_XIN (positions) and B_HB_ORIG
-// (h_build), carrying B_HCUR_O / B_LO_O / B_HI_O into cell order. count_only: the
-// occupancy-only hierarchy used for the initial guess (no slots, no sorts).
-static void build_structure(sph_ctx* c, bool count_only) {
-  DbgTimer _t(c, count_only ? "build (count only)" : "build");
+// a2 + a3: top grid, keys, radix sort, cell-order positions (h from B_HIN or 0).
+// Top cell edge >= kappa * max h0 ("larger or equal" to h) and >= TOP_EDGE_HMEAN
+// times the mean-density h (Eq. 3 at the mean number density), so that top cells in
+// under-dense regions still hold enough particles to fill a warp; the hierarchy below
+// splits on occupancy (and on h with the paper's fraction rule, a4). The list walk
+// (lists.cuh) handles any h < L/2, so the top grid never has to be rebuilt when h grows.
+#define TOP_EDGE_HMEAN 4.0
+static void sort_particles(sph_ctx* c, float h0max, bool have_h) {
+  DbgTimer _t(c, "sort");
   const int64_t n = c->n;
-  const float* x = Bget<float>(c, B_XIN);
-  float* hb_o = Bget<float>(c, B_HB_ORIG);
-  double L[3] = {c->cfg.box[0], c->cfg.box[1], c->cfg.box[2]};
-  double Lmin = std::min(L[0], std::min(L[1], L[2]));
+  const double L[3] = {c->cfg.box[0], c->cfg.box[1], c->cfg.box[2]};
   const double V = L[0] * L[1] * L[2];
-  double hmax, hmin;
-  if (count_only) {
-    // top edge from the mean density; depth as deep as the key allows
-    hmax = cbrt(3.0 * c->cfg.n_ngb * V / (4.0 * M_PI * (double)n));
-    hmin = hmax / 1024.0;
-  } else {
-    ctr_reset(c);
-    LAUNCH(k_hrange, grid1d(c, n, 256), 256, 0, hb_o, n, ctr(c));
-    unsigned long long h[C_NCOUNTERS];
-    ctr_read(c, h);
-    SPH_REQUIRE(!(h[C_ERR] & ERRBIT_H), SPH_E_DOMAIN, "smoothing length negative or non-finite");
-    SPH_REQUIRE(h[C_HMAXBITS] != 0, SPH_E_DOMAIN, "all smoothing lengths are zero");
-    hmax = as_float(h[C_HMAXBITS]);
-    hmin = as_float(h[C_HMINBITS]);
-  }
+  const double hmean = cbrt(3.0 * c->cfg.n_ngb * V / (4.0 * M_PI * (double)n));
+  const double htop = std::max(TOP_EDGE_HMEAN * hmean, c->cfg.top_edge_factor * (double)h0max) * (1.0 + 1e-6);
   int64_t ntot = 1;
   for (int k = 0; k < 3; ++k) {
-    double nk = floor(L[k] / (c->cfg.top_edge_factor * hmax * (1.0 + 1e-6)));
-    if (count_only) nk = std::max(nk, 3.0);
-    SPH_REQUIRE(nk >= 3.0, SPH_E_DOMAIN,
-                "smoothing length >= L/3: fewer than 3 top cells per axis (h_build max = " +
-                    std::to_string(hmax) + ")");
-    nk = std::min(nk, 512.0);
+    double nk = floor(L[k] / htop);
+    nk = std::max(3.0, std::min(nk, 1024.0));
     c->ntop[k] = (int)nk;
     c->E0[k] = L[k] / nk;
     ntot *= (int64_t)nk;
   }
   int top_bits = 0;
   while ((1ll << top_bits) < ntot) ++top_bits;
-  double emin = std::min(c->E0[0], std::min(c->E0[1], c->E0[2]));
-  int depth = count_only ? SPH_MAX_DEPTH : (int)floor(log2(emin / (2.0 * hmin))) + 1;
-  depth = std::max(0, std::min(depth, SPH_MAX_DEPTH));
-  while (top_bits + 3 * depth > 63) --depth;
+  int depth = std::min(SPH_MAX_DEPTH, (63 - top_bits) / 3);
   c->depth = depth;
   c->top_bits = top_bits;
   const int kbits = top_bits + 3 * depth;
-
-  // ---- a2 keys + radix sort
   uint64_t* k0 = B<uint64_t>(c, B_KEYS0, n);
   uint64_t* k1 = B<uint64_t>(c, B_KEYS1, n);
   uint32_t* v0 = B<uint32_t>(c, B_VALS0, n);
   uint32_t* v1 = B<uint32_t>(c, B_VALS1, n);
   const double sc[3] = {(double)((int64_t)c->ntop[0] << depth) / L[0], (double)((int64_t)c->ntop[1] << depth) / L[1],
                         (double)((int64_t)c->ntop[2] << depth) / L[2]};
-  LAUNCH(k_keys, grid1d(c, n, 256), 256, 0, x, n, c->ntop[0], c->ntop[1], c->ntop[2], depth, sc[0], sc[1], sc[2],
-         k0, v0);
+  LAUNCH(k_keys, grid1d(c, n, 256), 256, 0, Bget<float>(c, B_XIN), n, c->ntop[0], c->ntop[1], c->ntop[2], depth,
+         sc[0], sc[1], sc[2], k0, v0);
   radix_sort(c, k0, v0, k1, v1, n, kbits);
-  uint64_t* keys = k0;
+  // sorted keys / permutation live in KEYS0/VALS0 from here on
+  if (k0 != Bget<uint64_t>(c, B_KEYS0)) {
+    CUDA_TRY(cudaMemcpyAsync(Bget<uint64_t>(c, B_KEYS0), k0, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, c->stream));
+  }
   uint32_t* perm = B<uint32_t>(c, B_PERM, n);
   CUDA_TRY(cudaMemcpyAsync(perm, v0, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, c->stream));
-
-  // ---- a3 cell-order pack
   float4* xh = B<float4>(c, B_XH, n);
-  float* hb = B<float>(c, B_HB, n);
-  float* lo = B<float>(c, B_HLO, n);
-  float* hi = B<float>(c, B_HHI, n);
-  LAUNCH(k_gather_build, grid1d(c, n, 256), 256, 0, perm, n, x, Bget<float>(c, B_HCUR_O), hb_o,
-         Bget<float>(c, B_LO_O), Bget<float>(c, B_HI_O), xh, hb, lo, hi);
+  LAUNCH(k_pack, grid1d(c, n, 256), 256, 0, perm, n, Bget<float>(c, B_XIN), have_h ? Bget<float>(c, B_HIN) : nullptr,
+         xh);
+}
 
-  // ---- a4 hierarchy: level 0 = runs of the top-cell index
+// a4: the hierarchy from the sorted keys. Split rule: count > split_count and (rule on)
+// more than split_fraction of the particles have h < edge/2; with
+// use_fraction false the count alone decides (occupancy tree of the cold start).
+static void build_nodes(sph_ctx* c, bool use_fraction) {
+  DbgTimer _t(c, "nodes");
+  const int64_t n = c->n;
+  const uint64_t* keys = Bget<uint64_t>(c, B_KEYS0);
+  const float4* xh = Bget<float4>(c, B_XH);
   int* flag = B<int>(c, B_TMPI0, n);
   int* idx = B<int>(c, B_TMPI1, n);
+  const int depth = c->depth;
   const int sh = 3 * depth;
   LAUNCH(k_mark_top, grid1d(c, n, 256), 256, 0, keys, n, sh, flag);
-  int n0 = scan_excl<int>(c, flag, idx, n);
-  ensure_nodes(c, std::max<int64_t>(2 * (int64_t)n0 + 1024, n / 16));
+  const int n0 = scan_excl<int>(c, flag, idx, n);
+  ensure_nodes(c, std::max<int64_t>(2 * (int64_t)n0 + 1024, n / 8));
+  const int64_t ntot = (int64_t)c->ntop[0] * c->ntop[1] * c->ntop[2];
   int* topmap = B<int>(c, B_TOPMAP, ntot);
   CUDA_TRY(cudaMemsetAsync(topmap, 0xff, ntot * sizeof(int), c->stream));
   NodeArrays N = nodes(c);
   LAUNCH(k_write_top, grid1d(c, n, 256), 256, 0, keys, n, sh, flag, idx, c->ntop[0], c->ntop[1], N, topmap);
   LAUNCH(k_top_counts, gridfull(n0, 256), 256, 0, n0, n, N);
   c->lev_off.assign({0, n0});
-  LevelGeom g = level_geom(c);
-  const int split_count = count_only ? 32 : c->cfg.split_count;
+  const LevelGeom g = level_geom(c);
+  const float frac = use_fraction ? c->cfg.split_fraction : 0.f;
   for (int l = 0;; ++l) {
     const int a = c->lev_off[l], b = c->lev_off[l + 1];
     const int nl = b - a;
     int* nch = B<int>(c, B_N_NCH, nl);
     int* chscan = B<int>(c, B_N_CHBASE, nl);
     N = nodes(c);
-    LAUNCH(k_level_split, gridfull((int64_t)nl * 32, 256), 256, 0, a, b, l, depth, hb, keys, g.half_min[l],
-           split_count, c->cfg.split_fraction, count_only ? 1 : 0, N, nch, N.child);
-    int nnext = scan_excl<int>(c, nch, chscan, nl);
+    const float half_edge = 0.5f * std::min(g.E[l][0], std::min(g.E[l][1], g.E[l][2]));
+    LAUNCH(k_level_split, gridfull((int64_t)nl * 32, 256), 256, 0, a, b, l, depth, xh, keys, half_edge,
+           c->cfg.split_count, frac, N, nch, N.child);
+    const int nnext = scan_excl<int>(c, nch, chscan, nl);
     ensure_nodes(c, (int64_t)b + nnext + 1);
     N = nodes(c);
     LAUNCH(k_make_children, gridfull(nl, 256), 256, 0, a, b, (int64_t)b, nch, chscan, N);
@@ -344,99 +321,129 @@ static void build_structure(sph_ctx* c, bool count_only) {
     c->lev_off.push_back(b + nnext);
   }
   c->n_nodes = c->lev_off.back();
-  const int nnodes = c->n_nodes;
-  const int nlev = (int)c->lev_off.size() - 1;
-  if (count_only) return;
-
-  // ---- a5 neighbour slots (27 per node; 13 = self), interaction levels, list sizes
-  B<int>(c, B_N_SLOT, 27 * (int64_t)nnodes);
-  B<int>(c, B_N_NA, nnodes);
-  B<int>(c, B_N_NR, nnodes);
-  B<int>(c, B_N_AMASK, nnodes);
-  B<int>(c, B_N_RMASK, nnodes);
-  B<int64_t>(c, B_N_OFFA, nnodes);
-  B<int64_t>(c, B_N_OFFR, nnodes);
-  B<float>(c, B_N_HMAXA, nnodes);
-  B<float>(c, B_N_HMAXR, nnodes);
-  uint8_t* tau = B<uint8_t>(c, B_TAU, n);
+  B<float>(c, B_N_HMAX, c->n_nodes);
+  B<int64_t>(c, B_N_SORTOFF, c->n_nodes);
+  B<int4>(c, B_N_REC, c->n_nodes);
   N = nodes(c);
-  LAUNCH(k_top_slots, gridfull(n0, 128), 128, 0, n0, c->ntop[0], c->ntop[1], c->ntop[2], topmap, N);
-  for (int l = 1; l < nlev; ++l) {
-    const int a = c->lev_off[l], b = c->lev_off[l + 1];
-    LAUNCH(k_child_slots, gridfull(b - a, 128), 128, 0, a, b, N);
-  }
-  LAUNCH(k_tau, gridfull((int64_t)nnodes * 32, 256), 256, 0, nnodes, N, g, hb, tau);
-  LAUNCH(k_level_counts, gridfull((int64_t)nnodes * 32, 256), 256, 0, nnodes, N, tau);
-  int64_t* nsort = B<int64_t>(c, B_N_NSORT, 2 * (int64_t)nnodes);
-  int64_t* sscan = B<int64_t>(c, B_TMPL1, 2 * (int64_t)nnodes);
-  LAUNCH(k_list_masks, gridfull(nnodes, 128), 128, 0, nnodes, N, c->cfg.sort_min_len, nsort);
-  c->n_sorted = scan_excl<int64_t>(c, nsort, sscan, 2 * (int64_t)nnodes);
-  LAUNCH(k_split_offsets, gridfull(nnodes, 256), 256, 0, nnodes, sscan, N);
-
-  // ---- a6 13-direction sorted lists (+ the unsorted self copy)
-  SortEntry* sorted = B<SortEntry>(c, B_SORTED, c->n_sorted);
-  LAUNCH(k_sort_warp, gridfull((int64_t)nnodes * 64, 256), 256, 0, nnodes, xh, tau, N, g, sorted);
-  {
-    static bool attr = false;
-    const int smem = SORT_BLOCK_MAX * (8 + 4 + 4);
-    if (!attr) {
-      CUDA_TRY(cudaFuncSetAttribute(k_sort_block, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      attr = true;
-    }
-    LAUNCH(k_sort_block, 2 * nnodes, 512, smem, nnodes, xh, tau, N, g, sorted);
-  }
-  {
-    const int nseg = 2 * nnodes;
-    int* bflag = B<int>(c, B_TASKFLAG, nseg);
-    int* bidx = B<int>(c, B_TASKIDX, nseg);
-    int64_t* bsz = B<int64_t>(c, B_TMPL0, nseg);
-    LAUNCH(k_mark_big, gridfull(nseg, 256), 256, 0, nnodes, N, bflag, bsz);
-    int nbig = scan_excl<int>(c, bflag, bidx, nseg);
-    if (nbig > 0) {
-      int64_t* bscan = B<int64_t>(c, B_TMPL1, nseg);
-      int64_t nent = scan_excl<int64_t>(c, bsz, bscan, nseg);
-      int* bigseg = B<int>(c, B_BIGNODES, nbig);
-      int64_t* bigoff = B<int64_t>(c, B_BIGOFF, nbig);
-      LAUNCH(k_compact_big, gridfull(nseg, 256), 256, 0, nseg, bflag, bidx, bscan, bigseg, bigoff);
-      uint64_t* bk0 = B<uint64_t>(c, B_KEYS0, nent);
-      uint64_t* bk1 = B<uint64_t>(c, B_KEYS1, nent);
-      uint32_t* bv0 = B<uint32_t>(c, B_VALS0, nent);
-      uint32_t* bv1 = B<uint32_t>(c, B_VALS1, nent);
-      N = nodes(c);
-      LAUNCH(k_big_keys, nbig, 512, 0, nbig, bigseg, bigoff, xh, tau, N, g, bk0, bv0);
-      int segbits = 0;
-      while ((1ll << segbits) < (int64_t)nbig * 14) ++segbits;
-      radix_sort(c, bk0, bv0, bk1, bv1, nent, 32 + segbits);
-      LAUNCH(k_big_write, nbig, 512, 0, nbig, bigseg, bigoff, N, bk0, bv0, sorted);
-    }
-  }
-  {
-    int* cnt2 = B<int>(c, B_SEGCNT2, 2 * (int64_t)nnodes);
-    int* off2 = B<int>(c, B_SEGOFF2, 2 * (int64_t)nnodes);
-    LAUNCH(k_seg_count, gridfull(nnodes, 128), 128, 0, nnodes, N, cnt2);
-    const int nseg = scan_excl<int>(c, cnt2, off2, 2 * (int64_t)nnodes);
-    SegDesc* seg = B<SegDesc>(c, B_SEGDESC, nseg);
-    LAUNCH(k_seg_fill, gridfull(nnodes, 128), 128, 0, nnodes, N, g, off2, seg);
-    c->n_pair_slots = nseg;
-  }
-
-  // ---- tasks: leaf cells in chunks of <= 32 particles
-  int ntasks;
-  {
-    int* nchunk = B<int>(c, B_TASKFLAG, nnodes);
-    int* cscan = B<int>(c, B_TASKIDX, nnodes);
-    N = nodes(c);
-    LAUNCH(k_leaf_chunks, gridfull(nnodes, 256), 256, 0, nnodes, N, nchunk);
-    ntasks = scan_excl<int>(c, nchunk, cscan, nnodes);
-    int4* tasks = B<int4>(c, B_TASKS, ntasks);
-    LAUNCH(k_write_tasks, gridfull(nnodes, 256), 256, 0, nnodes, N, nchunk, cscan, tasks);
-    c->n_leaves = ntasks;   // number of tasks (stats.n_leaves)
-  }
-  sync(c);
-  DBG("build: n %lld top %dx%dx%d depth %d levels %d nodes %d tasks %d sorted %lld big %s\n", (long long)n,
-      c->ntop[0], c->ntop[1], c->ntop[2], depth, nlev, nnodes, ntasks, (long long)c->n_sorted, "");
+  LAUNCH(k_node_rec, gridfull(c->n_nodes, 256), 256, 0, c->n_nodes, N, N.rec);
 }
 
+// a6: the 13 presorted directions of every leaf longer than sort_min_len
+static void build_sorted(sph_ctx* c) {
+  DbgTimer _t(c, "sorted lists");
+  const int nn = c->n_nodes;
+  int64_t* sz = B<int64_t>(c, B_TMPL0, nn);
+  int64_t* sc = B<int64_t>(c, B_TMPL1, nn);
+  NodeArrays N = nodes(c);
+  LAUNCH(k_sort_sizes, gridfull(nn, 256), 256, 0, nn, N, c->cfg.sort_min_len, sz);
+  c->n_sorted = scan_excl<int64_t>(c, sz, sc, nn);
+  LAUNCH(k_sort_offsets, gridfull(nn, 256), 256, 0, nn, sz, sc, N);
+  if (c->n_sorted == 0) return;
+  SortEntry* sorted = B<SortEntry>(c, B_SORTED, c->n_sorted);
+  const LevelGeom g = level_geom(c);
+  const float4* xh = Bget<float4>(c, B_XH);
+  LAUNCH(k_sort_leaf_warp, gridfull((int64_t)nn * 32, 256), 256, 0, nn, xh, N, g, sorted);
+  static bool attr = false;
+  const int smem = SORT_BLOCK_MAX * (8 + 4);
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(k_sort_leaf_block, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  LAUNCH(k_sort_leaf_block, nn, 512, smem, nn, xh, N, g, sorted);
+}
+
+static void build_groups(sph_ctx* c) {
+  const int nn = c->n_nodes;
+  int* nchunk = B<int>(c, B_TMPI0, nn);
+  int* cscan = B<int>(c, B_TMPI1, nn);
+  NodeArrays N = nodes(c);
+  LAUNCH(k_group_count, gridfull(nn, 256), 256, 0, nn, N, nchunk);
+  c->n_groups = scan_excl<int>(c, nchunk, cscan, nn);
+  int4* groups = B<int4>(c, B_GROUPS, c->n_groups);
+  LAUNCH(k_group_write, gridfull(nn, 256), 256, 0, nn, N, cscan, groups);
+}
+
+static WalkParams walk_params(sph_ctx* c, bool force) {
+  WalkParams P;
+  memset(&P, 0, sizeof(P));
+  P.groups = Bget<int4>(c, B_GROUPS);
+  P.xh = Bget<float4>(c, B_XH);
+  P.reach = force ? Bget<float>(c, B_HLO) : Bget<float>(c, B_HB);
+  P.perm = Bget<uint32_t>(c, B_PERM);
+  P.n_own = c->n_own;
+  P.N = nodes(c);
+  P.g = level_geom(c);
+  P.topmap = Bget<int>(c, B_TOPMAP);
+  P.sorted = Bget<SortEntry>(c, B_SORTED);
+  P.force = force ? 1 : 0;
+  float Lmax = (float)std::max(c->cfg.box[0], std::max(c->cfg.box[1], c->cfg.box[2]));
+  P.slack = 4e-7f * Lmax;
+  P.ctr = ctr(c);
+  return P;
+}
+
+// Interaction lists of the selected groups (sel == null: all), appended to the pool:
+// walk once to count, scan, walk again to fill (lists.cuh).
+static void build_lists(sph_ctx* c, bool force, int nsel, const int* sel) {
+  DbgTimer _t(c, force ? "force lists" : "density lists");
+  if (nsel == 0) return;
+  WalkParams P = walk_params(c, force);
+  const int ng = c->n_groups;
+  int64_t* off = B<int64_t>(c, force ? B_FOFF : B_GOFF, ng, true);
+  int* len = B<int>(c, force ? B_FLEN : B_GLEN, ng, true);
+  int* lsel = sel ? B<int>(c, B_TMPI0, nsel) : len;
+  int64_t* lscan = B<int64_t>(c, B_TMPL1, nsel);
+  int64_t* lsel64 = B<int64_t>(c, B_TMPL0, nsel);
+  float rmax = 0.f;
+  if (force) {
+    ctr_reset(c);
+    LAUNCH(k_hrange, grid1d(c, c->n, 256), 256, 0, P.reach, c->n, ctr(c));
+    unsigned long long h[C_NCOUNTERS];
+    ctr_read(c, h);
+    rmax = as_float(h[C_HMAXBITS]);
+  }
+  P.reach_max = rmax;
+  P.nsel = nsel;
+  P.sel = sel;
+  P.off = off;
+  P.len = len;
+  P.len_sel = sel ? lsel : nullptr;
+  LAUNCH(k_walk<false>, gridfull(nsel, WALK_WARPS), WALK_WARPS * 32, 0, P);
+  LAUNCH(k_widen_i32, grid1d(c, nsel, 256), 256, 0, lsel, (int64_t)nsel, lsel64);
+  const int64_t total = scan_excl<int64_t>(c, lsel64, lscan, nsel);
+  int64_t& used = force ? c->pool_force : c->pool_dens;
+  const int64_t base = used;
+  uint32_t* pool = B<uint32_t>(c, force ? B_LISTF : B_LISTD, base + total, true);
+  used = base + total;
+  LAUNCH(k_set_offsets, gridfull(nsel, 256), 256, 0, nsel, sel, lscan, base, off);
+  P = walk_params(c, force);
+  P.nsel = nsel;
+  P.sel = sel;
+  P.off = off;
+  P.len = len;
+  P.out = pool;
+  P.reach_max = rmax;
+  LAUNCH(k_walk<true>, gridfull(nsel, WALK_WARPS), WALK_WARPS * 32, 0, P);
+  if (dbg_on()) {
+    std::vector<int> h(nsel);
+    CUDA_TRY(cudaMemcpyAsync(h.data(), sel ? lsel : len, nsel * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    std::sort(h.begin(), h.end());
+    DBG("%s lists: %d groups, %lld entries (%.1f per group; p50 %d p99 %d max %d)\n", force ? "force" : "density",
+        nsel, (long long)total, (double)total / std::max(nsel, 1), h[nsel / 2], h[(int)(0.99 * (nsel - 1))],
+        h[nsel - 1]);
+  }
+}
+
+static GroupLists group_lists(sph_ctx* c, bool force) {
+  GroupLists G;
+  G.groups = Bget<int4>(c, B_GROUPS);
+  G.off = Bget<int64_t>(c, force ? B_FOFF : B_GOFF);
+  G.len = Bget<int>(c, force ? B_FLEN : B_GLEN);
+  G.list = Bget<uint32_t>(c, force ? B_LISTF : B_LISTD);
+  G.ngroups = c->n_groups;
+  return G;
+}
 // =========================================================== inputs =============
 static bool is_device_ptr(const void* p) {
   if (!p) return false;
@@ -478,29 +485,6 @@ static void flush_out(sph_ctx* c, std::vector<OutMap>& maps, cudaEvent_t done) {
   if (!maps.empty()) sync(c);
 }
 
-static TravParams trav(sph_ctx* c, const int4* tasks, int ntasks, const uint8_t* active) {
-  TravParams P;
-  P.tasks = tasks;
-  P.ntasks = ntasks;
-  P.N = nodes(c);
-  P.g = level_geom(c);
-  P.sorted = Bget<SortEntry>(c, B_SORTED);
-  P.tau = Bget<uint8_t>(c, B_TAU);
-  P.seg = Bget<SegDesc>(c, B_SEGDESC);
-  P.segoff2 = Bget<int>(c, B_SEGOFF2);
-  P.segcnt2 = Bget<int>(c, B_SEGCNT2);
-  P.active = active;
-  float Lmax = (float)std::max(c->cfg.box[0], std::max(c->cfg.box[1], c->cfg.box[2]));
-  P.slack = 4e-7f * Lmax;
-  {
-    const char* e = getenv("SPH_DEBUG_SKIP");
-    P.dbg_skip = e ? atoi(e) : 0;
-    const char* d = getenv("SPH_DESC_MIN");
-    P.desc_min = d ? atoi(d) : 32;
-  }
-  P.ctr = ctr(c);
-  return P;
-}
 
 // =========================================================== API ================
 #define API_BEGIN(ctx)                                                              \
@@ -539,7 +523,7 @@ void sph_config_default(sph_config* cfg, double lx, double ly, double lz) {
   cfg->split_fraction = 0.875f;
   cfg->top_edge_factor = 1.0f;
   cfg->h_margin = 1.1f;
-  cfg->sort_min_len = 96;
+  cfg->sort_min_len = 64;
   cfg->flags = SPH_F_SYNC;
   cfg->rank = 0;
   cfg->nranks = 1;
@@ -629,7 +613,7 @@ int sph_destroy(sph_ctx* c) {
   if (!c) return SPH_E_ARG;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
-  for (int i = 0; i < 96; ++i) dev_free(c, c->b[i].p);
+  for (int i = 0; i < 64; ++i) dev_free(c, c->b[i].p);
   if (c->ev_ok)
     for (int i = 0; i < 12; ++i) cudaEventDestroy(c->ev[i]);
   if (c->own_stream) cudaStreamDestroy(c->stream);
@@ -641,7 +625,7 @@ int sph_set_allocator(sph_ctx* c, void* (*alloc)(size_t, void*, void*), void (*r
                       void* user) {
   if (!c) return SPH_E_ARG;
   if ((alloc == nullptr) != (release == nullptr)) return SPH_E_ARG;
-  for (int i = 0; i < 96; ++i)
+  for (int i = 0; i < 64; ++i)
     if (c->b[i].p) return SPH_E_STATE;
   c->ualloc = alloc;
   c->urelease = release;
@@ -653,66 +637,75 @@ int sph_build_cells(sph_ctx* ctx, int64_t n, const float* x, const float* h0) {
   return sph_build_cells_halo(ctx, n, 0, x, h0);
 }
 
-int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const float* x, const float* h0) {
-  API_BEGIN(ctx)
-  SPH_REQUIRE(n_own > 0 && n_halo >= 0 && x, SPH_E_ARG, "n_own <= 0, n_halo < 0 or x == NULL");
-  const int64_t n = n_own + n_halo;
-  SPH_REQUIRE(n < (1ll << 30), SPH_E_ARG, "n >= 2^30");
-  c->n = n;
-  c->n_own = n_own;
-  c->force_ready = false;
-  c->state = 0;
-  c->rebuilds = 0;
-  CUDA_TRY(cudaEventRecord(c->ev[0], c->stream));
+// positions in, validated; h0 (optional) in, validated; returns whether a guess is needed
+static bool load_inputs(sph_ctx* c, const float* x, const float* h0, float* h0max) {
+  const int64_t n = c->n;
   float* xd = B<float>(c, B_XIN, 3 * n);
   CUDA_TRY(cudaMemcpyAsync(xd, x, 3 * n * sizeof(float), cudaMemcpyDefault, c->stream));
   ctr_reset(c);
   LAUNCH(k_validate_x, grid1d(c, n, 256), 256, 0, xd, n, (float)c->cfg.box[0], (float)c->cfg.box[1],
          (float)c->cfg.box[2], ctr(c));
-  float* hin = B<float>(c, B_HIN, n);
   if (h0) {
+    float* hin = B<float>(c, B_HIN, n);
     CUDA_TRY(cudaMemcpyAsync(hin, h0, n * sizeof(float), cudaMemcpyDefault, c->stream));
     LAUNCH(k_hrange, grid1d(c, n, 256), 256, 0, hin, n, ctr(c));
-    LAUNCH(k_count_zero, grid1d(c, n, 256), 256, 0, hin, n, ctr(c));
-  } else {
-    CUDA_TRY(cudaMemsetAsync(hin, 0, n * sizeof(float), c->stream));
   }
   unsigned long long hc[C_NCOUNTERS];
   ctr_read(c, hc);
   SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_NONFINITE), SPH_E_DOMAIN, "non-finite position");
   SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_XRANGE), SPH_E_DOMAIN, "position outside [0, L)");
   SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_H), SPH_E_DOMAIN, "h0 negative or non-finite");
-  const bool need_guess = !h0 || hc[C_TMP0] > 0;
-  float* hcur = B<float>(c, B_HCUR_O, n);
-  float* hb = B<float>(c, B_HB_ORIG, n);
-  float* lo = B<float>(c, B_LO_O, n);
-  float* hi = B<float>(c, B_HI_O, n);
+  *h0max = h0 ? as_float(hc[C_HMAXBITS]) : 0.f;
+  SPH_REQUIRE(*h0max < h_cap(c), SPH_E_DOMAIN,
+              "h0 >= min(L)/2: the minimum-image convention needs h < L/2 (h0 max = " + std::to_string(*h0max) + ")");
+  return !h0 || hc[C_TMP0] > 0;
+}
+
+int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const float* x, const float* h0) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(n_own > 0 && n_halo >= 0 && x, SPH_E_ARG, "n_own <= 0, n_halo < 0 or x == NULL");
+  const int64_t n = n_own + n_halo;
+  SPH_REQUIRE(n <= (1ll << SPH_IDX_BITS), SPH_E_ARG, "n > 2^27 particles in one context");
+  c->n = n;
+  c->n_own = n_own;
+  c->state = 0;
+  c->force_lists = false;
+  c->pool_dens = c->pool_force = 0;
+  c->list_rebuilds = 0;
+  CUDA_TRY(cudaEventRecord(c->ev[0], c->stream));
+  float h0max = 0.f;
+  const bool need_guess = load_inputs(c, x, h0, &h0max);
+  // a2 + a3: one sort for the whole evaluation
+  sort_particles(c, h0max, h0 != nullptr);
+  // a4: the hierarchy; the cold start guesses h from the occupancy of the count-rule tree
+  const bool frac = c->cfg.split_fraction > 0.f;
+  build_nodes(c, frac && !need_guess);
+  float margin = c->cfg.h_margin;
   if (need_guess) {
-    // occupancy-only hierarchy -> h from the particle number density of the leaf (or
-    // of its first ancestor holding >= n_ngb particles)
-    LAUNCH(k_fill_f, grid1d(c, n, 256), 256, 0, hb, n, 1.0f);
-    LAUNCH(k_fill_f, grid1d(c, n, 256), 256, 0, hcur, n, 1.0f);
-    LAUNCH(k_fill_f, grid1d(c, n, 256), 256, 0, lo, n, 0.0f);
-    LAUNCH(k_fill_f, grid1d(c, n, 256), 256, 0, hi, n, 0.0f);
-    build_structure(c, true);
-    LevelGeom g = level_geom(c);
-    double Lmin = std::min(c->cfg.box[0], std::min(c->cfg.box[1], c->cfg.box[2]));
-    LAUNCH(k_guess_h, gridfull(c->n_nodes, 128), 128, 0, c->n_nodes, nodes(c), g, Bget<uint32_t>(c, B_PERM),
-           c->cfg.n_ngb, (int)c->cfg.n_ngb, (float)(0.25 * Lmin), hcur);
-    if (h0) LAUNCH(k_merge_guess, grid1d(c, n, 256), 256, 0, hin, n, hcur);
-    // the occupancy guess is uncertain: bin for a wider margin so the first passes can
-    // bracket the root without a rebuild
-    LAUNCH(k_init_h, grid1d(c, n, 256), 256, 0, hcur, n, SPH_COLD_MARGIN * c->cfg.h_margin, hb_cap(c), hcur, hb,
-           lo, hi);
-    c->margin_used = SPH_COLD_MARGIN * c->cfg.h_margin;
-  } else {
-    LAUNCH(k_init_h, grid1d(c, n, 256), 256, 0, hin, n, c->cfg.h_margin, hb_cap(c), hcur, hb, lo, hi);
-    c->margin_used = c->cfg.h_margin;
+    LAUNCH(k_guess_h, gridfull((int64_t)c->n_nodes * 32, 256), 256, 0, c->n_nodes, nodes(c), level_geom(c),
+           c->cfg.n_ngb, (int)c->cfg.n_ngb, h_cap(c), Bget<float4>(c, B_XH));
+    margin = std::max(margin, SPH_COLD_MARGIN);
+    if (frac) build_nodes(c, true);     // the paper's split rule needs h
   }
-  build_structure(c, false);
+  c->cold = need_guess;
+  // a6 + groups + density lists for h_build = h * margin
+  build_sorted(c);
+  build_groups(c);
+  {
+    float* hb = B<float>(c, B_HB, n);
+    B<float>(c, B_HLO, n);
+    B<float>(c, B_HHI, n);
+    B<uint8_t>(c, B_STATE, n);
+    LAUNCH(k_init_iter, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, c->n_own, Bget<float4>(c, B_XH),
+           margin, h_cap(c), Bget<uint8_t>(c, B_STATE), hb, Bget<float>(c, B_HLO), Bget<float>(c, B_HHI));
+  }
+  build_lists(c, false, c->n_groups, nullptr);
   c->state = 1;
   CUDA_TRY(cudaEventRecord(c->ev[1], c->stream));
-  if (c->cfg.flags & SPH_F_SYNC) sync(c);
+  sync(c);
+  DBG("build: n %lld top %dx%dx%d depth %d levels %zu nodes %d groups %d sorted %lld list %lld\n", (long long)n,
+      c->ntop[0], c->ntop[1], c->ntop[2], c->depth, c->lev_off.size() - 1, c->n_nodes, c->n_groups,
+      (long long)c->n_sorted, (long long)c->pool_dens);
   API_END
   return SPH_OK;
 }
@@ -720,40 +713,23 @@ int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const floa
 static void fill_struct_stats(sph_ctx* c, sph_stats* st) {
   st->n_levels = (int)c->lev_off.size() - 1;
   st->n_cells = c->n_nodes;
-  st->n_leaves = c->n_leaves;
-  st->n_pair_slots = c->n_pair_slots;
-  st->n_rebuilds = c->rebuilds;
+  st->n_leaves = c->n_groups;
+  st->n_pair_slots = c->pool_dens;
+  st->n_rebuilds = c->list_rebuilds;
 }
 
-// re-bin for h_build = h * margin (parked particles: margin_parked), keeping h, its bracket,
-// the states and the converged particles' sums (permuted to the new cell order)
-static void rebuild_keep_sums(sph_ctx* c, const float* vd, const float* md, const float* ud, float margin_parked,
-                              float margin = -1.f) {
-  const int64_t n = c->n;
-  if (margin < 0.f) margin = c->cfg.h_margin;
-  uint8_t* active = Bget<uint8_t>(c, B_FLAG);
-  LAUNCH(k_scatter_state, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, Bget<float4>(c, B_XH),
-         Bget<float>(c, B_HLO), Bget<float>(c, B_HHI), active, margin, margin_parked, hb_cap(c),
-         Bget<float>(c, B_HCUR_O), Bget<float>(c, B_LO_O), Bget<float>(c, B_HI_O), Bget<float>(c, B_HB_ORIG));
-  uint8_t* st_o = B<uint8_t>(c, B_STATE_O, n);
-  double* sf_o = B<double>(c, B_SF_O, n);
-  float4* a0_o = B<float4>(c, B_ACC0_O, n);
-  float4* a1_o = B<float4>(c, B_ACC1_O, n);
-  LAUNCH(k_scatter_sums, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, active, Bget<double>(c, B_DSUMF),
-         Bget<float4>(c, B_DACC0), Bget<float4>(c, B_DACC1), st_o, sf_o, a0_o, a1_o);
-  build_structure(c, false);
-  c->rebuilds++;
-  c->margin_used = margin;
-  LAUNCH(k_gather_vmu, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, vd, md, ud, Bget<float4>(c, B_VM),
-         Bget<float>(c, B_U));
-  LAUNCH(k_gather_sums, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, st_o, sf_o, a0_o, a1_o, active,
-         Bget<double>(c, B_DSUMF), Bget<float4>(c, B_DACC0), Bget<float4>(c, B_DACC1));
-}
-
-// coarse mode covers any h below the top cell edge (the 27 top cells hold every partner)
-static float coarse_cap(sph_ctx* c) {
-  double cap = std::min(c->E0[0], std::min(c->E0[1], c->E0[2])) * (1.0 - 1e-5);
-  return (float)cap;
+// groups with a target whose h outgrew h_build: rebuild their density lists
+static void regrow_lists(sph_ctx* c) {
+  const int ng = c->n_groups;
+  int* flag = B<int>(c, B_GFLAG, ng);
+  int* scan = B<int>(c, B_TMPI1, ng);
+  LAUNCH(k_group_flags, gridfull((int64_t)ng * 32, 256), 256, 0, Bget<int4>(c, B_GROUPS), ng,
+         Bget<uint8_t>(c, B_STATE), flag);
+  const int nsel = scan_excl<int>(c, flag, scan, ng);
+  int* sel = B<int>(c, B_GSEL, std::max(nsel, 1));
+  LAUNCH(k_compact_idx, grid1d(c, ng, 256), 256, 0, flag, scan, (int64_t)ng, sel);
+  build_lists(c, false, nsel, sel);
+  c->list_rebuilds += nsel;
 }
 
 int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, float* h_out, float* rho_out,
@@ -763,82 +739,67 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   SPH_REQUIRE(v && m && u && h_out && rho_out, SPH_E_ARG, "required pointer is NULL");
   const int64_t n = c->n;
   CUDA_TRY(cudaEventRecord(c->ev[2], c->stream));
-  // copied: the force loop gathers v and m again after its rebuild
-  const float* vd = dev_in(c, v, 3 * n, B_VIN, true);
-  const float* md = dev_in(c, m, n, B_MIN, true);
-  const float* ud = dev_in(c, u, n, B_UIN, true);
+  const float* vd = dev_in(c, v, 3 * n, B_VIN);
+  const float* md = dev_in(c, m, n, B_MIN);
+  const float* ud = dev_in(c, u, n, B_UIN);
   ctr_reset(c);
   LAUNCH(k_validate_vmu, grid1d(c, n, 256), 256, 0, vd, md, ud, n, ctr(c));
+  float4* vm = B<float4>(c, B_VM, n);
+  float* uc = B<float>(c, B_U, n);
+  LAUNCH(k_gather_vmu, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, vd, md, ud, vm, uc);
   unsigned long long hc[C_NCOUNTERS];
   ctr_read(c, hc);
   SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_NONFINITE), SPH_E_DOMAIN, "non-finite velocity");
   SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_MASS), SPH_E_DOMAIN, "mass <= 0 or non-finite");
   SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_U), SPH_E_DOMAIN, "internal energy <= 0 or non-finite");
-  if (!is_device_ptr(v) || !is_device_ptr(m) || !is_device_ptr(u)) sync(c);
 
-  float4* vm = B<float4>(c, B_VM, n);
-  float* uc = B<float>(c, B_U, n);
-  uint8_t* active = B<uint8_t>(c, B_FLAG, n);
-  double* sf = B<double>(c, B_DSUMF, n);
-  float4* acc0 = B<float4>(c, B_DACC0, n);
-  float4* acc1 = B<float4>(c, B_DACC1, n);
-  float* s2 = B<float>(c, B_DSUM2, n);
-  LAUNCH(k_gather_vmu, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, vd, md, ud, vm, uc);
-  LAUNCH(k_init_state, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, c->n_own, active);
-
+  uint8_t* state = Bget<uint8_t>(c, B_STATE);
+  DensOut dout;
+  dout.sf = B<double>(c, B_DSUMF, n);
+  dout.acc0 = B<float4>(c, B_DACC0, n);
+  dout.acc1 = B<float4>(c, B_DACC1, n);
+  dout.s2 = B<float>(c, B_DSUM2, n);
+  if (c->state >= 2) {   // a repeated call: iterate again from the current h (lists stay valid)
+    LAUNCH(k_init_iter, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, c->n_own, Bget<float4>(c, B_XH),
+           1.0f, h_cap(c), state, (float*)nullptr, Bget<float>(c, B_HLO), Bget<float>(c, B_HHI));
+  }
+  const float margin = c->cold ? std::max(c->cfg.h_margin, SPH_COLD_MARGIN) : c->cfg.h_margin;
   int iters = 0;
   long long unconv = n;
-  long long cand_last = 0;
-  long long parked = 0;
+  long long cand_first = 0;
   while (true) {
-    // every task is launched; warps without an unconverged particle exit at once
-    const int ntasks = c->n_leaves;
-    const int4* tasks = Bget<int4>(c, B_TASKS);
-    // cold start: the first pass evaluates N, N', N'' only (nobody converges at the guess)
-    const int nonly = (iters == 0 && c->margin_used > 1.2f * c->cfg.h_margin && c->cfg.max_h_iter > 1) ? 1 : 0;
+    // cold start: nobody converges at the occupancy guess, so the first pass evaluates
+    // N(h) and its derivatives only
+    const bool nonly = iters == 0 && c->cold && c->cfg.max_h_iter > 1;
     ctr_reset(c);
-    if (ntasks > 0) {
+    {
       DbgTimer _t(c, "density kernel");
-      TravParams P = trav(c, tasks, ntasks, active);
       if (iters == 0) CUDA_TRY(cudaEventRecord(c->ev[6], c->stream));
-      LAUNCH(k_density, gridfull(ntasks, INTERACT_WARPS), INTERACT_WARPS * 32, 0, P, Bget<float4>(c, B_XH), vm,
-             Bget<uint8_t>(c, B_TAU), DensOut{nonly, sf, acc0, acc1, s2});
+      const GroupLists G = group_lists(c, false);
+      if (nonly)
+        LAUNCH(k_density<true>, gridfull(G.ngroups, DENS_WARPS), DENS_WARPS * 32, 0, G, Bget<float4>(c, B_XH), vm,
+               state, box3(c), dout, ctr(c));
+      else
+        LAUNCH(k_density<false>, gridfull(G.ngroups, DENS_WARPS), DENS_WARPS * 32, 0, G, Bget<float4>(c, B_XH), vm,
+               state, box3(c), dout, ctr(c));
       if (iters == 0) CUDA_TRY(cudaEventRecord(c->ev[7], c->stream));
     }
     ++iters;
-    const bool last = iters >= c->cfg.max_h_iter;
-    if (last) {
+    if (iters >= c->cfg.max_h_iter) {
       ctr_read(c, hc);
-      if (iters == 1) cand_last = (long long)hc[C_CAND];
+      if (iters == 1) cand_first = (long long)hc[C_CAND];
       break;  // sums are at the current h; unconverged particles are reported
     }
     LAUNCH(k_h_update, grid1d(c, n, 256), 256, 0, n, Bget<float4>(c, B_XH), Bget<float>(c, B_HB),
-           Bget<float>(c, B_HLO), Bget<float>(c, B_HHI), active, sf, acc0, s2, c->cfg.n_ngb, c->cfg.n_ngb_tol,
-           coarse_cap(c), nonly, ctr(c));
+           Bget<float>(c, B_HLO), Bget<float>(c, B_HHI), state, dout.sf, dout.acc0, dout.s2, c->cfg.n_ngb,
+           c->cfg.n_ngb_tol, margin, h_cap(c), nonly ? 1 : 0, ctr(c));
     ctr_read(c, hc);
-    if (iters == 1) cand_last = (long long)hc[C_CAND];
-    parked += (long long)hc[C_REBUILD];
-    unconv = (long long)hc[C_UNCONV] + parked;
-    DBG("density pass %d: cand %llu seg %llu chunks %llu (max/warp %llu, in heavy warps %llu) -> active %llu "
-        "(coarse %llu) parked %lld\n", iters, hc[C_CAND], hc[C_TMP1], hc[C_TMP2], hc[C_MAXCH], hc[C_HEAVY],
-        hc[C_UNCONV], hc[C_TMP0], parked);
+    if (iters == 1) cand_first = (long long)hc[C_CAND];
+    unconv = (long long)hc[C_UNCONV];
+    DBG("density pass %d%s: cand %llu -> unconverged %llu, regrow %llu\n", iters, nonly ? " (N only)" : "",
+        hc[C_CAND], hc[C_UNCONV], hc[C_REGROW]);
     if (unconv == 0) break;
-    if (iters == 1 && c->margin_used > 1.2f * c->cfg.h_margin) {
-      // cold start: the cells were binned for the occupancy guess with a wide margin; one
-      // Newton step later h is known to a few per cent, so re-bin for it with the normal margin
-      rebuild_keep_sums(c, vd, md, ud, 2.0f * c->cfg.h_margin);
-      parked = 0;
-      vm = Bget<float4>(c, B_VM);
-      continue;
-    }
-    if (hc[C_UNCONV] == 0 && parked > 0) {
-      // every other particle has converged; the parked ones want an h beyond the top cells
-      // (coarse_cap): re-bin everything for h_build = h * margin, keep h, its bracket and the
-      // converged particles' sums, and continue with the parked ones only
-      rebuild_keep_sums(c, vd, md, ud, 2.0f * c->cfg.h_margin);
-      parked = 0;
-      vm = Bget<float4>(c, B_VM);
-    }
+    if (hc[C_REGROW] > 0) regrow_lists(c);
   }
   // ghost: finalise and write the caller-order outputs
   std::vector<OutMap> maps;
@@ -854,17 +815,15 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   go.n_own = no;
   go.h_o = B<float>(c, B_HFIN_O, n);
   go.g_o = B<float4>(c, B_GST_O, n);
-  // particles whose final h exceeds the h their cells were built for (coarse mode)
   ctr_reset(c);
-  LAUNCH(k_count_loose, grid1d(c, n, 256), 256, 0, n, Bget<float4>(c, B_XH), Bget<float>(c, B_HB), ctr(c));
-  LAUNCH(k_ghost, grid1d(c, n, 256), 256, 0, n, Bget<float4>(c, B_XH), uc, sf, acc0, acc1, c->cfg.gamma,
+  LAUNCH(k_ghost, grid1d(c, n, 256), 256, 0, n, Bget<float4>(c, B_XH), uc, dout.acc0, dout.acc1, c->cfg.gamma,
          c->cfg.balsara_eps, go, ctr(c));
   flush_out(c, maps, c->ev[3]);
   c->state = 2;
-  c->force_ready = false;
-  int status = (unconv > 0 && iters >= c->cfg.max_h_iter) ? SPH_E_NOCONV : SPH_OK;
+  c->force_lists = false;
+  const bool noconv = unconv > 0 && iters >= c->cfg.max_h_iter;
   ctr_read(c, hc);
-  c->loose = (int64_t)hc[C_TMP0];
+  const long long ndir = (long long)hc[C_NDIR];
   if (c->n > c->n_own && c->cfg.halo_width > 0.0) {
     // every owned particle's partners must be inside the received halo
     ctr_reset(c);
@@ -872,58 +831,47 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
     unsigned long long hh[C_NCOUNTERS];
     ctr_read(c, hh);
     SPH_REQUIRE(as_float(hh[C_HMAXBITS]) <= c->cfg.halo_width, SPH_E_NOCONV,
-                "halo too narrow: an owned h = " + std::to_string(as_float(hh[C_HMAXBITS])) + " exceeds cfg.halo_width");
+                "halo too narrow: an owned h = " + std::to_string(as_float(hh[C_HMAXBITS])) +
+                    " exceeds cfg.halo_width");
   }
-  {
-    if (st) {
-      memset(st, 0, sizeof(*st));
-      fill_struct_stats(c, st);
-      st->n_directed = (int64_t)hc[C_NDIR];
-      st->n_candidates = cand_last;
-      st->n_candidates_density_full = cand_last;
-      st->n_unconverged = status == SPH_E_NOCONV ? unconv : 0;
-      st->h_iters = iters;
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
-      st->ms_build = ms;
-      cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]);
-      st->ms_density = ms;
-      cudaEventElapsedTime(&ms, c->ev[6], c->ev[7]);
-      st->ms_kernel_density_full = ms;
-    }
+  if (st) {
+    memset(st, 0, sizeof(*st));
+    fill_struct_stats(c, st);
+    st->n_directed = ndir;
+    st->n_candidates = cand_first;
+    st->n_candidates_density_full = cand_first;
+    st->n_unconverged = noconv ? unconv : 0;
+    st->h_iters = iters;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+    st->ms_build = ms;
+    cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]);
+    st->ms_density = ms;
+    cudaEventElapsedTime(&ms, c->ev[6], c->ev[7]);
+    st->ms_kernel_density_full = ms;
   }
-  if (status == SPH_E_NOCONV) {
+  if (noconv) {
     c->err = "h iteration did not converge in max_h_iter passes: " + std::to_string(unconv) + " particles";
-    return status;
+    return SPH_E_NOCONV;
   }
   API_END
   return SPH_OK;
 }
 
-// Force-loop structure: the density cells were built for h_build (cold-start margin, or
-// below the h of particles that finished in coarse mode) and without the halo particles'
-// final h; rebuild once, tight (h_build = h), from the caller-order state, then gather the
-// force inputs in the new cell order.
+// Force inputs in cell order (the hierarchy and the cell order are those of the build;
+// halo particles carry the imported state), node max h and the force lists for
+// r < max(h_i, h_j) at the final h.
 static void prepare_force(sph_ctx* c) {
   const int64_t n = c->n;
-  const bool rebuild = c->margin_used > 1.2f * c->cfg.h_margin || c->loose > 0 || c->n > c->n_own;
-  if (rebuild) {
-    DBG("force: tight rebuild (margin used %.3f, %lld loose, %lld halo)\n", c->margin_used, (long long)c->loose,
-        (long long)(c->n - c->n_own));
-    LAUNCH(k_force_hb, grid1d(c, n, 256), 256, 0, Bget<float>(c, B_HFIN_O), n, Bget<float>(c, B_HCUR_O),
-           Bget<float>(c, B_HB_ORIG));
-    build_structure(c, false);
-    c->rebuilds++;
-    c->margin_used = 1.0f;
-  }
   float4* fx = B<float4>(c, B_FX, n);
   float4* fs = B<float4>(c, B_FS, n);
-  float4* vm = B<float4>(c, B_VM, n);
+  float* hr = Bget<float>(c, B_HLO);
   LAUNCH(k_gather_force, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, Bget<float4>(c, B_XH),
-         Bget<float>(c, B_HFIN_O), Bget<float4>(c, B_GST_O), Bget<float>(c, B_VIN), Bget<float>(c, B_MIN), fx, fs, vm);
-  LAUNCH(k_node_hmax, gridfull((int64_t)c->n_nodes * 32, 256), 256, 0, c->n_nodes, nodes(c), Bget<float4>(c, B_XH),
-         Bget<uint8_t>(c, B_TAU));
-  c->force_ready = true;
+         Bget<float>(c, B_HFIN_O), Bget<float4>(c, B_GST_O), fx, fs, hr);
+  LAUNCH(k_node_hmax, gridfull((int64_t)c->n_nodes * 32, 256), 256, 0, c->n_nodes, nodes(c), hr);
+  c->pool_force = 0;
+  build_lists(c, true, c->n_groups, nullptr);
+  c->force_lists = true;
 }
 
 int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out, int32_t* n_nbr_force_out,
@@ -931,10 +879,10 @@ int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out, int3
   API_BEGIN(ctx)
   SPH_REQUIRE(c->state >= 2, SPH_E_STATE, "sph_force before sph_density");
   SPH_REQUIRE(a_out && dudt_out, SPH_E_ARG, "required pointer is NULL");
-  const int64_t n = c->n, no = c->n_own;
+  const int64_t no = c->n_own;
   CUDA_TRY(cudaEventRecord(c->ev[4], c->stream));
   DbgTimer _tf(c, "force call");
-  if (!c->force_ready) prepare_force(c);
+  if (!c->force_lists) prepare_force(c);
   std::vector<OutMap> maps;
   ForceOut fo;
   fo.a = dev_out(c, a_out, 3 * no, B_OUT0, maps);
@@ -944,28 +892,29 @@ int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out, int3
   fo.perm = Bget<uint32_t>(c, B_PERM);
   fo.n_own = no;
   ctr_reset(c);
-  TravParams P = trav(c, Bget<int4>(c, B_TASKS), c->n_leaves, nullptr);
+  const GroupLists G = group_lists(c, true);
   CUDA_TRY(cudaEventRecord(c->ev[8], c->stream));
-  LAUNCH(k_force, gridfull(c->n_leaves, INTERACT_WARPS), INTERACT_WARPS * 32, 0, P, Bget<float4>(c, B_FX),
-         Bget<float4>(c, B_VM), Bget<float4>(c, B_FS), c->cfg.alpha, Bget<uint8_t>(c, B_TAU), fo);
+  {
+    DbgTimer _t(c, "force kernel");
+    LAUNCH(k_force, gridfull(G.ngroups, FORCE_WARPS), FORCE_WARPS * 32, 0, G, Bget<float4>(c, B_FX),
+           Bget<float4>(c, B_VM), Bget<float4>(c, B_FS), c->cfg.alpha, box3(c), fo, ctr(c));
+  }
   CUDA_TRY(cudaEventRecord(c->ev[9], c->stream));
   flush_out(c, maps, c->ev[5]);
-  if (st || (c->cfg.flags & SPH_F_SYNC)) {
-    unsigned long long hc[C_NCOUNTERS];
-    ctr_read(c, hc);
-    if (st) {
-      memset(st, 0, sizeof(*st));
-      fill_struct_stats(c, st);
-      DBG("force: tasks %d cand %llu seg %llu chunks %llu (max/warp %llu heavy %llu) pairs %llu\n", c->n_leaves,
-          hc[C_CAND], hc[C_TMP1], hc[C_TMP2], hc[C_MAXCH], hc[C_HEAVY], hc[C_NFORCE] / 2);
-      st->n_pairs = (int64_t)(hc[C_NFORCE] / 2);
-      st->n_candidates = (int64_t)hc[C_CAND];
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, c->ev[4], c->ev[5]);
-      st->ms_force = ms;
-      cudaEventElapsedTime(&ms, c->ev[8], c->ev[9]);
-      st->ms_kernel_force = ms;
-    }
+  unsigned long long hc[C_NCOUNTERS];
+  ctr_read(c, hc);
+  SPH_REQUIRE(!(hc[C_ERR] & (1ull << 20)), SPH_E_CUDA, "interaction list count/fill mismatch");
+  DBG("force: groups %d cand %llu pairs %llu\n", c->n_groups, hc[C_CAND], hc[C_NFORCE] / 2);
+  if (st) {
+    memset(st, 0, sizeof(*st));
+    fill_struct_stats(c, st);
+    st->n_pairs = (int64_t)(hc[C_NFORCE] / 2);
+    st->n_candidates = (int64_t)hc[C_CAND];
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev[4], c->ev[5]);
+    st->ms_force = ms;
+    cudaEventElapsedTime(&ms, c->ev[8], c->ev[9]);
+    st->ms_kernel_force = ms;
   }
   API_END
   return SPH_OK;
@@ -974,25 +923,19 @@ int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out, int3
 int sph_guess_h(sph_ctx* ctx, int64_t n, const float* x, float* h_out) {
   API_BEGIN(ctx)
   SPH_REQUIRE(n > 0 && x && h_out, SPH_E_ARG, "bad argument");
+  SPH_REQUIRE(n <= (1ll << SPH_IDX_BITS), SPH_E_ARG, "n > 2^27 particles in one context");
   c->n = n;
   c->n_own = n;
   c->state = 0;
-  float* xd = B<float>(c, B_XIN, 3 * n);
-  CUDA_TRY(cudaMemcpyAsync(xd, x, 3 * n * sizeof(float), cudaMemcpyDefault, c->stream));
-  float* hb = B<float>(c, B_HB_ORIG, n);
-  float* hcur = B<float>(c, B_HCUR_O, n);
-  float* lo = B<float>(c, B_LO_O, n);
-  float* hi = B<float>(c, B_HI_O, n);
-  LAUNCH(k_fill_f, grid1d(c, n, 256), 256, 0, hb, n, 1.0f);
-  LAUNCH(k_fill_f, grid1d(c, n, 256), 256, 0, hcur, n, 1.0f);
-  LAUNCH(k_fill_f, grid1d(c, n, 256), 256, 0, lo, n, 0.0f);
-  LAUNCH(k_fill_f, grid1d(c, n, 256), 256, 0, hi, n, 0.0f);
-  build_structure(c, true);
-  double Lmin = std::min(c->cfg.box[0], std::min(c->cfg.box[1], c->cfg.box[2]));
+  float h0max = 0.f;
+  load_inputs(c, x, nullptr, &h0max);
+  sort_particles(c, 0.f, false);
+  build_nodes(c, false);
+  LAUNCH(k_guess_h, gridfull((int64_t)c->n_nodes * 32, 256), 256, 0, c->n_nodes, nodes(c), level_geom(c),
+         c->cfg.n_ngb, (int)c->cfg.n_ngb, h_cap(c), Bget<float4>(c, B_XH));
   std::vector<OutMap> maps;
   float* o = dev_out(c, h_out, n, B_OUT0, maps);
-  LAUNCH(k_guess_h, gridfull(c->n_nodes, 128), 128, 0, c->n_nodes, nodes(c), level_geom(c), Bget<uint32_t>(c, B_PERM),
-         c->cfg.n_ngb, (int)c->cfg.n_ngb, (float)(0.25 * Lmin), o);
+  LAUNCH(k_scatter_h, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, Bget<float4>(c, B_XH), o);
   flush_out(c, maps, c->ev[10]);
   sync(c);
   API_END
@@ -1007,8 +950,8 @@ int sph_halo_select(sph_ctx* ctx, int64_t n, const float* x, double lo, double h
   const float* xd = dev_in(c, x, 3 * n, B_XIN);
   int* flo = B<int>(c, B_TMPI0, n);
   int* fhi = B<int>(c, B_TMPI1, n);
-  int* slo = B<int>(c, B_TASKFLAG, n);
-  int* shi = B<int>(c, B_TASKIDX, n);
+  int* slo = B<int>(c, B_GFLAG, n);
+  int* shi = B<int>(c, B_GSEL, n);
   LAUNCH(k_halo_flags, grid1d(c, n, 256), 256, 0, xd, n, (float)lo, (float)hi, (float)width, flo, fhi);
   const int nlo = scan_excl<int>(c, flo, slo, n);
   const int nhi = scan_excl<int>(c, fhi, shi, n);
@@ -1050,7 +993,7 @@ int sph_import_halo_state(sph_ctx* ctx, const float* state) {
   const float* sd = dev_in(c, state, 5 * k, B_TMPL0);
   LAUNCH(k_import_state, grid1d(c, k, 256), 256, 0, sd, k, c->n_own, Bget<float>(c, B_HFIN_O),
          Bget<float4>(c, B_GST_O));
-  c->force_ready = false;
+  c->force_lists = false;
   sync(c);
   API_END
   return SPH_OK;
