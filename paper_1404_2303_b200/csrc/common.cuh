@@ -103,7 +103,7 @@ struct sph_ctx {
 
   int64_t n = 0;        // particles in the structure: owned + halo
   int64_t n_own = 0;    // owned (targets); caller indices >= n_own are halo (sources only)
-  int state = 0;        // 0 nothing, 1 cells built, 2 density done
+  int state = 0;        // 0 nothing, 1 cells built, 2 density done, 3 force inputs gathered
   bool force_lists = false;
   bool cold = false;       // h0 was the occupancy guess (wider list margin, N-only first pass)
 
@@ -115,9 +115,11 @@ struct sph_ctx {
   std::vector<int> lev_off;  // node index offsets per level (size nlevels+1)
   int n_nodes = 0, n_leaves = 0, n_groups = 0;
   int64_t n_sorted = 0;      // entries of all 13-direction lists
-  int64_t pool_dens = 0;     // used entries of the density list pool
-  int64_t pool_force = 0;    // entries of the force lists
-  int64_t list_rebuilds = 0; // groups whose density list was rebuilt for a grown h
+  int64_t pool = 0;          // entries of the interaction (UNION) lists
+  int nb_k = 192;            // capacity of a particle's neighbour list (NB walk)
+  int ucap = 768;            // capacity of a group's interaction list slab (UNION walk)
+  int64_t ovf_used = 0;      // entries of the neighbour-list overflow pool
+  int64_t list_rebuilds = 0; // groups re-walked for a particle whose h outgrew its list
   float hb_max = 0.f;        // largest h_build (density reach)
 
   // named device buffers
@@ -140,7 +142,7 @@ enum BufId {
   // 13-direction sorted lists
   B_SORTED,
   // groups and interaction lists
-  B_GROUPS, B_GOFF, B_GLEN, B_FOFF, B_FLEN, B_LISTD, B_LISTF, B_GFLAG, B_GIDX, B_GSEL,
+  B_GROUPS, B_GOFF, B_GLEN, B_LIST, B_NBR2, B_NBCNT, B_NBOFF, B_NBOVF, B_GFLAG, B_GSEL, B_HRCH,
   // misc scratch
   B_TMPI0, B_TMPI1, B_TMPL0, B_TMPL1, B_COUNTERS, B_OUT0, B_OUT1, B_OUT2, B_OUT3, B_OUT4, B_OUT5,
   B_COUNT

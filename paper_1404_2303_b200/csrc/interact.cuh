@@ -25,15 +25,6 @@ struct GroupLists {
   int ngroups;
 };
 
-// source position relative to the group origin o (oL = o - L), periodic image code c
-__device__ __forceinline__ float3 rel_pos(float4 p, uint32_t code, float3 o, float3 oL, const float* L) {
-  const int cx = code % 3, cy = (code / 3) % 3, cz = code / 9;
-  const float x = (cx == 1 ? p.x - L[0] : p.x) - (cx == 2 ? oL.x : o.x);
-  const float y = (cy == 1 ? p.y - L[1] : p.y) - (cy == 2 ? oL.y : o.y);
-  const float z = (cz == 1 ? p.z - L[2] : p.z) - (cz == 2 ? oL.z : o.z);
-  return make_float3(x, y, z);
-}
-
 // ------------------------------------------------------------------ kernel ------
 // f(q) of the cubic spline (W = (8/pi) h^-3 f), its first and second derivative
 __device__ __forceinline__ void spline(float q, float& f, float& fp, float& fpp) {
@@ -62,8 +53,8 @@ struct DensOut {
 template <bool NONLY>
 __global__ void __launch_bounds__(DENS_WARPS * 32) k_density(GroupLists G, const float4* __restrict__ xh,
                                                              const float4* __restrict__ vm,
-                                                             const uint8_t* __restrict__ state, float3 Lbox,
-                                                             DensOut out, unsigned long long* ctr) {
+                                                             const uint32_t* __restrict__ perm, int64_t n_own,
+                                                             float3 Lbox, DensOut out, unsigned long long* ctr) {
   __shared__ float4 sp[DENS_WARPS][32 * DENS_ST];   // x, y, z (group frame), m
   __shared__ float4 sv[DENS_WARPS][32 * DENS_ST];   // vx, vy, vz, j (int bits)
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -71,7 +62,7 @@ __global__ void __launch_bounds__(DENS_WARPS * 32) k_density(GroupLists G, const
   if (gid >= G.ngroups) return;
   const int4 grp = G.groups[gid];
   const int s = grp.y + lane;
-  const bool act = lane < grp.z && state[s] == HS_ACTIVE;
+  const bool act = lane < grp.z && perm[s] < (uint32_t)n_own;   // halo particles: sources only
   if (!__any_sync(FULL_MASK, act)) return;
   const float L[3] = {Lbox.x, Lbox.y, Lbox.z};
   const float4 o4 = xh[grp.y];
@@ -353,77 +344,134 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(GroupLists G, const 
   }
 }
 
-// ------------------------------------------------------------------ h update ------
-// Safeguarded Newton iteration for N_i(h) = (32/3) sum_j f(r_ij/h) = n_ngb (Eq. 3,
-// P:183-185; R3, R4), the step taken in log space (Halley's correction from the same
-// pass's second-derivative sum): x = ln h, g(x) = ln N - ln n_ngb, g' = h N'/N. Steps are
-// clamped to [h/2, 2h] and replaced by a bisection when they leave the bracket [lo, hi]
-// of evaluated points. Converged iff |N - n_ngb| <= tol. A particle whose next h exceeds
-// the reach its group's list was built for (h_build) gets h_build = h * margin and its
-// group's list is rebuilt before the next pass (state HS_REGROW, lists.cuh).
-__global__ void k_h_update(int64_t n, float4* __restrict__ xh, float* __restrict__ hb,
-                           float* __restrict__ lo, float* __restrict__ hi, uint8_t* __restrict__ state,
-                           const double* __restrict__ sf, const float4* __restrict__ acc0,
-                           const float* __restrict__ s2, float n_t, float tol, float margin, float hcap, int nonly,
-                           unsigned long long* ctr) {
-  int unconv = 0, regrow = 0;
-  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n;
-       s += (int64_t)gridDim.x * blockDim.x) {
-    if (state[s] != HS_ACTIVE) continue;
-    const float h = xh[s].w;
-    const double Nd = (32.0 / 3.0) * sf[s];
-    const float N = (float)Nd;
-    const float res = (float)(Nd - (double)n_t);
-    if (fabsf(res) <= tol) {
-      if (!nonly) state[s] = HS_DONE;            // N-only pass: keep h, evaluate the sums next pass
-      else ++unconv;
-      continue;
-    }
-    float l = lo[s], u = hi[s];
-    if (res < 0.f) l = h;
-    else u = h;
-    lo[s] = l;
-    hi[s] = u;
-    if (u - l <= 4.f * (h * 1.1920929e-7f)) {   // bracket at fp32 resolution: stop
-      if (!nonly) state[s] = HS_DONE;
-      else ++unconv;
-      continue;
-    }
-    // g(x) = ln N(e^x) - ln n_ngb with x = ln h:  g' = h N'/N,  g'' = g' + h^2 N''/N - g'^2,
-    // h N' = -(32/3) S1, h^2 N'' = (32/3)(2 S1 + S2), S1 = sum q f'(q), S2 = sum q^2 f''(q)
-    const float S1 = acc0[s].z, S2 = s2[s];
-    const float g = __logf(N / n_t);
-    const float g1 = -(32.f / 3.f) * S1 / N;
-    const float g2 = g1 + (32.f / 3.f) * (2.f * S1 + S2) / N - g1 * g1;
-    float dx;
-    if (g1 > 0.25f) {
-      dx = -g / g1;                                      // log-space Newton
-      const float den = 2.f * g1 * g1 - g * g2;           // Halley (cubic convergence)
-      if (den > 0.5f * g1 * g1) {
-        const float dh = -2.f * g * g1 / den;
-        if (fabsf(dh) <= 2.f * fabsf(dx)) dx = dh;
+// ------------------------------------------------------------------ h solve -------
+// The h iteration of Eq. 3 (R3, R4) for every particle on its own neighbour
+// list: the squared distances r^2 < h_build^2 recorded by the NB walk (lists.cuh). For any
+// h <= h_build, N(h) = (32/3) sum_{r < h} f(r/h) (self term included, R2) is exact on the
+// list, so the whole iteration runs here without further sweeps of the cells:
+//   x = ln h, g(x) = ln N - ln n_ngb, g' = h N'/N, g'' from the same sums;
+//   Newton step in log space with Halley's correction, clamped to [h/2, 2h] and replaced
+//   by a bisection when it leaves the bracket [lo, hi] of evaluated points;
+//   converged iff |N - n_ngb| <= tol (or the bracket is at fp32 resolution).
+// A step beyond h_build (the root lies outside the list) sets h_build = h * margin and
+// state HS_REGROW: the walk re-records this particle's list before the next round. A list
+// longer than K lives in the overflow pool (contiguous, exactly sized; lists.cuh).
+#define HSOLVE_WARPS 8
+__global__ void __launch_bounds__(HSOLVE_WARPS * 32) k_hsolve(const int4* __restrict__ groups, int ngroups,
+                                                              float4* __restrict__ xh, float* __restrict__ hb,
+                                                              float* __restrict__ lo_a, float* __restrict__ hi_a,
+                                                              uint8_t* __restrict__ state,
+                                                              const float* __restrict__ nb_r2,
+                                                              const int* __restrict__ nb_cnt, int K,
+                                                              const int64_t* __restrict__ ovf_off,
+                                                              const float* __restrict__ ovf, float n_t,
+                                                              float tol, float margin, float hcap, int max_iter,
+                                                              unsigned long long* ctr) {
+  const int lane = threadIdx.x & 31;
+  const int gid = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  if (gid >= ngroups) return;
+  const int4 grp = groups[gid];
+  const int s = grp.y + lane;
+  if (lane >= grp.z || state[s] != HS_ACTIVE) return;
+  const int cnt = nb_cnt[s];
+  const int64_t oo = ovf_off[s];
+  const float* __restrict__ r2l = oo >= 0 ? ovf + oo : nb_r2 + (int64_t)grp.y * K + lane;
+  const int gz = oo >= 0 ? 1 : grp.z;
+  float h = xh[s].w;
+  float hbs = hb[s];
+  float l = lo_a[s], u = hi_a[s];
+  uint8_t st = HS_ACTIVE;
+  int it = 0;
+  if (cnt > K && oo < 0) {
+    // not recorded (more than NB_POOL_MAX sources within h_build): the count alone says
+    // h_build is far beyond the root; shrink it to hold about K/2 sources, re-walk
+    hbs = hbs * cbrtf(0.5f * (float)K / (float)cnt);
+    h = fminf(h, hbs / margin);
+    st = HS_REGROW;
+  } else {
+    for (; it < max_iter; ++it) {
+      const float h2 = h * h, hinv = 1.0f / h;
+      double S0 = 0.0;
+      float S1 = 0.f, S2 = 0.f;
+      for (int e = 0; e < cnt; ++e) {
+        const float r2 = r2l[(int64_t)e * gz];
+        if (r2 < h2) {
+          const float q = (r2 > 0.f ? r2 * rsqrtf(r2) : 0.f) * hinv;
+          float f, fp, fpp;
+          spline(q, f, fp, fpp);
+          S0 += (double)f;
+          S1 = fmaf(q, fp, S1);
+          S2 = fmaf(q * q, fpp, S2);
+        }
       }
-    } else {
-      dx = (res < 0.f) ? 0.6931472f : -0.6931472f;       // (almost) no neighbour yet: double / halve
-    }
-    float hn = h * __expf(dx);
-    hn = fminf(fmaxf(hn, 0.5f * h), 2.f * h);
-    if (!(hn > l && hn < u)) hn = 0.5f * (l + fminf(u, 2.f * h));
-    hn = fminf(hn, hcap);
-    xh[s].w = hn;
-    ++unconv;
-    if (hn > hb[s]) {
-      hb[s] = fminf(hn * margin, hcap);
-      state[s] = HS_REGROW;
-      ++regrow;
+      const double Nd = (32.0 / 3.0) * S0;
+      const float N = (float)Nd;
+      const float res = (float)(Nd - (double)n_t);
+      if (fabsf(res) <= tol) {
+        st = HS_DONE;
+        break;
+      }
+      if (res < 0.f) l = h;
+      else u = h;
+      if (u - l <= 4.f * (h * 1.1920929e-7f)) {    // bracket at fp32 resolution
+        st = HS_DONE;
+        break;
+      }
+      // g' = h N'/N = -(32/3) S1 / N;  g'' = g' + (32/3)(2 S1 + S2)/N - g'^2
+      const float g = __logf(N / n_t);
+      const float g1 = -(32.f / 3.f) * S1 / N;
+      const float g2 = g1 + (32.f / 3.f) * (2.f * S1 + S2) / N - g1 * g1;
+      float dx;
+      if (g1 > 0.25f) {
+        dx = -g / g1;                                     // log-space Newton
+        const float den = 2.f * g1 * g1 - g * g2;          // Halley (cubic convergence)
+        if (den > 0.5f * g1 * g1) {
+          const float dh = -2.f * g * g1 / den;
+          if (fabsf(dh) <= 2.f * fabsf(dx)) dx = dh;
+        }
+      } else {
+        dx = (res < 0.f) ? 0.6931472f : -0.6931472f;      // (almost) no neighbour: double / halve
+      }
+      float hn = h * __expf(dx);
+      hn = fminf(fmaxf(hn, 0.5f * h), 2.f * h);
+      if (!(hn > l && hn < u)) hn = 0.5f * (l + fminf(u, 2.f * h));
+      hn = fminf(hn, hcap);
+      h = hn;
+      if (hn > hbs) {                                     // the root lies beyond the list
+        hbs = fminf(hn * margin, hcap);
+        st = HS_REGROW;
+        ++it;
+        break;
+      }
     }
   }
-  unconv = warp_sum_i(unconv);
-  regrow = warp_sum_i(regrow);
-  if ((threadIdx.x & 31) == 0) {
-    if (unconv) atomicAdd(&ctr[C_UNCONV], (unsigned long long)unconv);
-    if (regrow) atomicAdd(&ctr[C_REGROW], (unsigned long long)regrow);
+  xh[s].w = h;
+  hb[s] = hbs;
+  lo_a[s] = l;
+  hi_a[s] = u;
+  state[s] = st;
+  const unsigned regrow = __ballot_sync(__activemask(), st == HS_REGROW);
+  const unsigned unconv = __ballot_sync(__activemask(), st == HS_ACTIVE);
+  const int leader = __ffs(__activemask()) - 1;
+  if (lane == leader) {
+    if (regrow) atomicAdd(&ctr[C_REGROW], (unsigned long long)__popc(regrow));
+    if (unconv) atomicAdd(&ctr[C_UNCONV], (unsigned long long)__popc(unconv));
   }
+  const unsigned itmax = __reduce_max_sync(__activemask(), (unsigned)it);
+  if (lane == leader) atomicMax(&ctr[C_TMP1], (unsigned long long)itmax);
+}
+
+// UNION-walk reach in the density phase: the h of owned particles (halo h unknown: 0)
+__global__ void k_reach_owned(const uint32_t* __restrict__ perm, int64_t n, int64_t n_own,
+                              const float4* __restrict__ xh, float* __restrict__ hr) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x)
+    hr[s] = perm[s] < n_own ? xh[s].w : 0.f;
+}
+
+// HS_REGROW -> HS_ACTIVE once the new lists are recorded
+__global__ void k_state_swap(uint8_t* __restrict__ st, int64_t n, uint8_t from, uint8_t to) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x)
+    if (st[s] == from) st[s] = to;
 }
 
 // ------------------------------------------------------------------ ghost --------

@@ -363,87 +363,156 @@ static void build_groups(sph_ctx* c) {
   LAUNCH(k_group_write, gridfull(nn, 256), 256, 0, nn, N, cscan, groups);
 }
 
-static WalkParams walk_params(sph_ctx* c, bool force) {
+static WalkParams walk_params(sph_ctx* c, const float* reach) {
   WalkParams P;
   memset(&P, 0, sizeof(P));
   P.groups = Bget<int4>(c, B_GROUPS);
   P.xh = Bget<float4>(c, B_XH);
-  P.reach = force ? Bget<float>(c, B_HLO) : Bget<float>(c, B_HB);
+  P.reach = reach;
   P.perm = Bget<uint32_t>(c, B_PERM);
   P.n_own = c->n_own;
   P.N = nodes(c);
   P.g = level_geom(c);
   P.topmap = Bget<int>(c, B_TOPMAP);
   P.sorted = Bget<SortEntry>(c, B_SORTED);
-  P.force = force ? 1 : 0;
   float Lmax = (float)std::max(c->cfg.box[0], std::max(c->cfg.box[1], c->cfg.box[2]));
   P.slack = 4e-7f * Lmax;
   P.ctr = ctr(c);
   return P;
 }
 
-// Interaction lists of the selected groups (sel == null: all), appended to the pool:
-// walk once to count, scan, walk again to fill (lists.cuh).
-static void build_lists(sph_ctx* c, bool force, int nsel, const int* sel) {
-  DbgTimer _t(c, force ? "force lists" : "density lists");
+// NB walk: per target the squared distances r^2 < h_build^2 (lists.cuh, MODE_NB), for the
+// selected groups (sel == null: all) and the targets in state `tsel_val` (owned if < 0).
+// Lists longer than nb_k are recorded again, exactly sized, in the overflow pool.
+static void build_nb(sph_ctx* c, int nsel, const int* sel, int tsel_val) {
+  DbgTimer _t(c, "neighbour lists");
   if (nsel == 0) return;
-  WalkParams P = walk_params(c, force);
-  const int ng = c->n_groups;
-  int64_t* off = B<int64_t>(c, force ? B_FOFF : B_GOFF, ng, true);
-  int* len = B<int>(c, force ? B_FLEN : B_GLEN, ng, true);
-  int* lsel = sel ? B<int>(c, B_TMPI0, nsel) : len;
-  int64_t* lscan = B<int64_t>(c, B_TMPL1, nsel);
-  int64_t* lsel64 = B<int64_t>(c, B_TMPL0, nsel);
-  float rmax = 0.f;
-  if (force) {
-    ctr_reset(c);
-    LAUNCH(k_hrange, grid1d(c, c->n, 256), 256, 0, P.reach, c->n, ctr(c));
+  if (dbg_on()) ctr_reset(c);
+  const int64_t n = c->n;
+  WalkParams P = walk_params(c, Bget<float>(c, B_HB));
+  P.nsel = nsel;
+  P.sel = sel;
+  if (tsel_val >= 0) {
+    P.tsel = Bget<uint8_t>(c, B_STATE);
+    P.tsel_val = (uint8_t)tsel_val;
+  }
+  P.K = c->nb_k;
+  P.nb_r2 = B<float>(c, B_NBR2, (size_t)n * c->nb_k);
+  P.nb_cnt = B<int>(c, B_NBCNT, n);
+  LAUNCH(k_walk<MODE_NB>, gridfull(nsel, WALK_WARPS), WALK_WARPS * 32, 0, P);
+  if (dbg_on()) {
     unsigned long long h[C_NCOUNTERS];
     ctr_read(c, h);
-    rmax = as_float(h[C_HMAXBITS]);
+    DBG("NB walk: %d groups, raw sources %llu (%.0f per group, max %llu)\n", nsel, h[C_TMP2],
+        (double)h[C_TMP2] / nsel, h[C_TMP0]);
   }
+  // overflow: exact counts are known; record those lists contiguously
+  int64_t* oc = B<int64_t>(c, B_TMPL0, n);
+  int64_t* os = B<int64_t>(c, B_TMPL1, n);
+  int64_t* ooff = Bget<int64_t>(c, B_NBOFF);
+  uint8_t* state = Bget<uint8_t>(c, B_STATE);
+  LAUNCH(k_mark_overflow, gridfull((int64_t)c->n_groups * 32, 256), 256, 0, Bget<int4>(c, B_GROUPS), c->n_groups,
+         state, tsel_val, Bget<uint32_t>(c, B_PERM), c->n_own, P.nb_cnt, c->nb_k, state, oc, ooff);
+  const int64_t tot = scan_excl<int64_t>(c, oc, os, n);
+  if (tot == 0) return;
+  const int64_t base = c->ovf_used;
+  float* pool = B<float>(c, B_NBOVF, base + tot, true);
+  c->ovf_used = base + tot;
+  LAUNCH(k_ovf_offsets, grid1d(c, n, 256), 256, 0, n, oc, os, base, ooff);
+  const int ng = c->n_groups;
+  int* flag = B<int>(c, B_GFLAG, ng);
+  int* scan = B<int>(c, B_TMPI1, ng);
+  LAUNCH(k_group_flags, gridfull((int64_t)ng * 32, 256), 256, 0, Bget<int4>(c, B_GROUPS), ng, state, (uint8_t)HS_OVF,
+         flag);
+  const int no = scan_excl<int>(c, flag, scan, ng);
+  int* osel = B<int>(c, B_TMPI0, std::max(no, 1));
+  LAUNCH(k_compact_idx, grid1d(c, ng, 256), 256, 0, flag, scan, (int64_t)ng, osel);
+  WalkParams Q = walk_params(c, Bget<float>(c, B_HB));
+  Q.nsel = no;
+  Q.sel = osel;
+  Q.tsel = state;
+  Q.tsel_val = HS_OVF;
+  Q.K = c->nb_k;
+  Q.nb_cnt = P.nb_cnt;
+  Q.ovf = pool;
+  Q.ovf_off = ooff;
+  LAUNCH(k_walk<MODE_NB>, gridfull(no, WALK_WARPS), WALK_WARPS * 32, 0, Q);
+  LAUNCH(k_state_swap, grid1d(c, n, 256), 256, 0, state, n, (uint8_t)HS_OVF,
+         (uint8_t)(tsel_val >= 0 ? tsel_val : HS_ACTIVE));
+  DBG("neighbour lists: %lld entries of %d groups in the overflow pool\n", (long long)tot, no);
+}
+
+// UNION walk: per group the sources within reach max(h_i, h_j) of at least one target, with
+// h from `reach` (lists.cuh). One pass into fixed-capacity slabs (ucap entries per group);
+// groups beyond it are walked again into exactly sized space after the slabs.
+static void build_union(sph_ctx* c, const float* reach) {
+  DbgTimer _t(c, "interaction lists");
+  const int ng = c->n_groups;
+  if (ng == 0) return;
+  // node max of the reach (the walk's bound for sources with a large h)
+  LAUNCH(k_node_hmax, gridfull((int64_t)c->n_nodes * 32, 256), 256, 0, c->n_nodes, nodes(c), reach);
+  ctr_reset(c);
+  LAUNCH(k_hrange, grid1d(c, c->n, 256), 256, 0, reach, c->n, ctr(c));
+  unsigned long long h[C_NCOUNTERS];
+  ctr_read(c, h);
+  const float rmax = as_float(h[C_HMAXBITS]);
+  const int cap = c->ucap;
+  WalkParams P = walk_params(c, reach);
   P.reach_max = rmax;
-  P.nsel = nsel;
-  P.sel = sel;
-  P.off = off;
-  P.len = len;
-  P.len_sel = sel ? lsel : nullptr;
-  LAUNCH(k_walk<false>, gridfull(nsel, WALK_WARPS), WALK_WARPS * 32, 0, P);
-  LAUNCH(k_widen_i32, grid1d(c, nsel, 256), 256, 0, lsel, (int64_t)nsel, lsel64);
-  const int64_t total = scan_excl<int64_t>(c, lsel64, lscan, nsel);
-  int64_t& used = force ? c->pool_force : c->pool_dens;
-  const int64_t base = used;
-  uint32_t* pool = B<uint32_t>(c, force ? B_LISTF : B_LISTD, base + total, true);
-  used = base + total;
-  LAUNCH(k_set_offsets, gridfull(nsel, 256), 256, 0, nsel, sel, lscan, base, off);
-  P = walk_params(c, force);
-  P.nsel = nsel;
-  P.sel = sel;
-  P.off = off;
-  P.len = len;
-  P.out = pool;
-  P.reach_max = rmax;
-  LAUNCH(k_walk<true>, gridfull(nsel, WALK_WARPS), WALK_WARPS * 32, 0, P);
+  P.nsel = ng;
+  P.off = B<int64_t>(c, B_GOFF, ng);
+  P.len = B<int>(c, B_GLEN, ng);
+  P.ucap = cap;
+  const int64_t slab = (int64_t)ng * cap;
+  P.out = B<uint32_t>(c, B_LIST, slab);
+  LAUNCH(k_slab_offsets, gridfull(ng, 256), 256, 0, ng, cap, P.off);
+  LAUNCH(k_walk<MODE_FILL>, gridfull(ng, WALK_WARPS), WALK_WARPS * 32, 0, P);
+  int* flag = B<int>(c, B_GFLAG, ng);
+  int* scan = B<int>(c, B_TMPI1, ng);
+  LAUNCH(k_union_overflow, gridfull(ng, 256), 256, 0, ng, P.len, cap, flag);
+  const int no = scan_excl<int>(c, flag, scan, ng);
+  int64_t total = slab;
+  if (no > 0) {
+    int* sel = B<int>(c, B_GSEL, no);
+    LAUNCH(k_compact_idx, grid1d(c, ng, 256), 256, 0, flag, scan, (int64_t)ng, sel);
+    int64_t* l64 = B<int64_t>(c, B_TMPL0, no);
+    int64_t* lscan = B<int64_t>(c, B_TMPL1, no);
+    LAUNCH(k_gather_len, gridfull(no, 256), 256, 0, no, sel, P.len, l64);
+    const int64_t extra = scan_excl<int64_t>(c, l64, lscan, no);
+    P.out = B<uint32_t>(c, B_LIST, slab + extra, true);
+    total = slab + extra;
+    LAUNCH(k_set_offsets, gridfull(no, 256), 256, 0, no, sel, lscan, slab, P.off);
+    P.nsel = no;
+    P.sel = sel;
+    P.ucap = INT32_MAX;
+    P.check = 1;
+    LAUNCH(k_walk<MODE_FILL>, gridfull(no, WALK_WARPS), WALK_WARPS * 32, 0, P);
+  }
+  c->pool = total;
   if (dbg_on()) {
-    std::vector<int> h(nsel);
-    CUDA_TRY(cudaMemcpyAsync(h.data(), sel ? lsel : len, nsel * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    ctr_read(c, h);
+    std::vector<int> hl(ng);
+    CUDA_TRY(cudaMemcpyAsync(hl.data(), P.len, ng * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     sync(c);
-    std::sort(h.begin(), h.end());
-    DBG("%s lists: %d groups, %lld entries (%.1f per group; p50 %d p99 %d max %d)\n", force ? "force" : "density",
-        nsel, (long long)total, (double)total / std::max(nsel, 1), h[nsel / 2], h[(int)(0.99 * (nsel - 1))],
-        h[nsel - 1]);
+    int64_t ent = 0;
+    for (int v : hl) ent += v;
+    std::sort(hl.begin(), hl.end());
+    DBG("interaction lists: %d groups, %lld entries (%.1f per group; p50 %d p99 %d max %d), %d beyond the slab; "
+        "raw sources %llu (max %llu per group)\n", ng, (long long)ent, (double)ent / ng, hl[ng / 2],
+        hl[(int)(0.99 * (ng - 1))], hl[ng - 1], no, h[C_TMP2], h[C_TMP0]);
   }
 }
 
-static GroupLists group_lists(sph_ctx* c, bool force) {
+static GroupLists group_lists(sph_ctx* c) {
   GroupLists G;
   G.groups = Bget<int4>(c, B_GROUPS);
-  G.off = Bget<int64_t>(c, force ? B_FOFF : B_GOFF);
-  G.len = Bget<int>(c, force ? B_FLEN : B_GLEN);
-  G.list = Bget<uint32_t>(c, force ? B_LISTF : B_LISTD);
+  G.off = Bget<int64_t>(c, B_GOFF);
+  G.len = Bget<int>(c, B_GLEN);
+  G.list = Bget<uint32_t>(c, B_LIST);
   G.ngroups = c->n_groups;
   return G;
 }
+
 // =========================================================== inputs =============
 static bool is_device_ptr(const void* p) {
   if (!p) return false;
@@ -670,7 +739,7 @@ int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const floa
   c->n_own = n_own;
   c->state = 0;
   c->force_lists = false;
-  c->pool_dens = c->pool_force = 0;
+  c->pool = 0;
   c->list_rebuilds = 0;
   CUDA_TRY(cudaEventRecord(c->ev[0], c->stream));
   float h0max = 0.f;
@@ -695,17 +764,22 @@ int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const floa
     float* hb = B<float>(c, B_HB, n);
     B<float>(c, B_HLO, n);
     B<float>(c, B_HHI, n);
+    B<float>(c, B_HRCH, n);
     B<uint8_t>(c, B_STATE, n);
+    CUDA_TRY(cudaMemsetAsync(B<int64_t>(c, B_NBOFF, n), 0xff, n * sizeof(int64_t), c->stream));
+    B<float>(c, B_NBOVF, 1);
+    c->ovf_used = 0;
     LAUNCH(k_init_iter, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, c->n_own, Bget<float4>(c, B_XH),
            margin, h_cap(c), Bget<uint8_t>(c, B_STATE), hb, Bget<float>(c, B_HLO), Bget<float>(c, B_HHI));
   }
-  build_lists(c, false, c->n_groups, nullptr);
+  // neighbour lists of the h iteration: r^2 < h_build^2 per particle
+  build_nb(c, c->n_groups, nullptr, -1);
   c->state = 1;
   CUDA_TRY(cudaEventRecord(c->ev[1], c->stream));
   sync(c);
   DBG("build: n %lld top %dx%dx%d depth %d levels %zu nodes %d groups %d sorted %lld list %lld\n", (long long)n,
       c->ntop[0], c->ntop[1], c->ntop[2], c->depth, c->lev_off.size() - 1, c->n_nodes, c->n_groups,
-      (long long)c->n_sorted, (long long)c->pool_dens);
+      (long long)c->n_sorted, (long long)c->pool);
   API_END
   return SPH_OK;
 }
@@ -714,22 +788,25 @@ static void fill_struct_stats(sph_ctx* c, sph_stats* st) {
   st->n_levels = (int)c->lev_off.size() - 1;
   st->n_cells = c->n_nodes;
   st->n_leaves = c->n_groups;
-  st->n_pair_slots = c->pool_dens;
+  st->n_pair_slots = c->pool;
   st->n_rebuilds = c->list_rebuilds;
 }
 
-// groups with a target whose h outgrew h_build: rebuild their density lists
+// groups with a particle in state HS_REGROW: re-record those particles' neighbour lists
 static void regrow_lists(sph_ctx* c) {
   const int ng = c->n_groups;
   int* flag = B<int>(c, B_GFLAG, ng);
   int* scan = B<int>(c, B_TMPI1, ng);
   LAUNCH(k_group_flags, gridfull((int64_t)ng * 32, 256), 256, 0, Bget<int4>(c, B_GROUPS), ng,
-         Bget<uint8_t>(c, B_STATE), flag);
+         Bget<uint8_t>(c, B_STATE), (uint8_t)HS_REGROW, flag);
   const int nsel = scan_excl<int>(c, flag, scan, ng);
   int* sel = B<int>(c, B_GSEL, std::max(nsel, 1));
   LAUNCH(k_compact_idx, grid1d(c, ng, 256), 256, 0, flag, scan, (int64_t)ng, sel);
-  build_lists(c, false, nsel, sel);
+  build_nb(c, nsel, sel, HS_REGROW);
+  LAUNCH(k_state_swap, grid1d(c, c->n, 256), 256, 0, Bget<uint8_t>(c, B_STATE), c->n, (uint8_t)HS_REGROW,
+         (uint8_t)HS_ACTIVE);
   c->list_rebuilds += nsel;
+  DBG("regrow: %d groups re-walked\n", nsel);
 }
 
 int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, float* h_out, float* rho_out,
@@ -754,54 +831,62 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_U), SPH_E_DOMAIN, "internal energy <= 0 or non-finite");
 
   uint8_t* state = Bget<uint8_t>(c, B_STATE);
+  if (c->state >= 2) {   // a repeated call: iterate again from the current h (lists stay valid)
+    LAUNCH(k_init_iter, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, c->n_own, Bget<float4>(c, B_XH),
+           1.0f, h_cap(c), state, (float*)nullptr, Bget<float>(c, B_HLO), Bget<float>(c, B_HHI));
+  }
+  // a8: the h iteration, per particle on its neighbour list; re-walk particles whose root
+  // lies beyond their list, until every particle has converged
+  const float margin = c->cold ? std::max(c->cfg.h_margin, SPH_COLD_MARGIN) : c->cfg.h_margin;
+  int rounds = 0;
+  long long unconv = 0, itmax = 0;
+  CUDA_TRY(cudaEventRecord(c->ev[6], c->stream));
+  while (true) {
+    ctr_reset(c);
+    {
+      DbgTimer _t(c, "h solve");
+      LAUNCH(k_hsolve, gridfull((int64_t)c->n_groups * 32, HSOLVE_WARPS * 32), HSOLVE_WARPS * 32, 0,
+             Bget<int4>(c, B_GROUPS), c->n_groups, Bget<float4>(c, B_XH), Bget<float>(c, B_HB), Bget<float>(c, B_HLO),
+             Bget<float>(c, B_HHI), state, Bget<float>(c, B_NBR2), Bget<int>(c, B_NBCNT), c->nb_k,
+             Bget<int64_t>(c, B_NBOFF), Bget<float>(c, B_NBOVF), c->cfg.n_ngb,
+             c->cfg.n_ngb_tol, margin, h_cap(c), c->cfg.max_h_iter, ctr(c));
+    }
+    ctr_read(c, hc);
+    ++rounds;
+    unconv = (long long)hc[C_UNCONV];
+    itmax = std::max(itmax, (long long)hc[C_TMP1]);
+    DBG("h solve round %d: unconverged %llu, regrow %llu, max iterations %llu\n", rounds, hc[C_UNCONV],
+        hc[C_REGROW], hc[C_TMP1]);
+    if (hc[C_REGROW] == 0) break;
+    if (rounds >= c->cfg.max_h_iter) {
+      unconv += (long long)hc[C_REGROW];
+      break;
+    }
+    regrow_lists(c);
+  }
+  CUDA_TRY(cudaEventRecord(c->ev[7], c->stream));
+  // a7: the density loop at the final h over the interaction lists (reach max(h_i, h_j)
+  // with the owned particles' h; these are the force lists too when there is no halo)
+  float* hr = Bget<float>(c, B_HRCH);
+  LAUNCH(k_reach_owned, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, c->n_own, Bget<float4>(c, B_XH),
+         hr);
+  build_union(c, hr);
+  c->force_lists = c->n == c->n_own;
   DensOut dout;
   dout.sf = B<double>(c, B_DSUMF, n);
   dout.acc0 = B<float4>(c, B_DACC0, n);
   dout.acc1 = B<float4>(c, B_DACC1, n);
   dout.s2 = B<float>(c, B_DSUM2, n);
-  if (c->state >= 2) {   // a repeated call: iterate again from the current h (lists stay valid)
-    LAUNCH(k_init_iter, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, c->n_own, Bget<float4>(c, B_XH),
-           1.0f, h_cap(c), state, (float*)nullptr, Bget<float>(c, B_HLO), Bget<float>(c, B_HHI));
+  ctr_reset(c);
+  CUDA_TRY(cudaEventRecord(c->ev[8], c->stream));
+  {
+    DbgTimer _t(c, "density kernel");
+    const GroupLists G = group_lists(c);
+    LAUNCH(k_density<false>, gridfull(G.ngroups, DENS_WARPS), DENS_WARPS * 32, 0, G, Bget<float4>(c, B_XH), vm,
+           Bget<uint32_t>(c, B_PERM), c->n_own, box3(c), dout, ctr(c));
   }
-  const float margin = c->cold ? std::max(c->cfg.h_margin, SPH_COLD_MARGIN) : c->cfg.h_margin;
-  int iters = 0;
-  long long unconv = n;
-  long long cand_first = 0;
-  while (true) {
-    // cold start: nobody converges at the occupancy guess, so the first pass evaluates
-    // N(h) and its derivatives only
-    const bool nonly = iters == 0 && c->cold && c->cfg.max_h_iter > 1;
-    ctr_reset(c);
-    {
-      DbgTimer _t(c, "density kernel");
-      if (iters == 0) CUDA_TRY(cudaEventRecord(c->ev[6], c->stream));
-      const GroupLists G = group_lists(c, false);
-      if (nonly)
-        LAUNCH(k_density<true>, gridfull(G.ngroups, DENS_WARPS), DENS_WARPS * 32, 0, G, Bget<float4>(c, B_XH), vm,
-               state, box3(c), dout, ctr(c));
-      else
-        LAUNCH(k_density<false>, gridfull(G.ngroups, DENS_WARPS), DENS_WARPS * 32, 0, G, Bget<float4>(c, B_XH), vm,
-               state, box3(c), dout, ctr(c));
-      if (iters == 0) CUDA_TRY(cudaEventRecord(c->ev[7], c->stream));
-    }
-    ++iters;
-    if (iters >= c->cfg.max_h_iter) {
-      ctr_read(c, hc);
-      if (iters == 1) cand_first = (long long)hc[C_CAND];
-      break;  // sums are at the current h; unconverged particles are reported
-    }
-    LAUNCH(k_h_update, grid1d(c, n, 256), 256, 0, n, Bget<float4>(c, B_XH), Bget<float>(c, B_HB),
-           Bget<float>(c, B_HLO), Bget<float>(c, B_HHI), state, dout.sf, dout.acc0, dout.s2, c->cfg.n_ngb,
-           c->cfg.n_ngb_tol, margin, h_cap(c), nonly ? 1 : 0, ctr(c));
-    ctr_read(c, hc);
-    if (iters == 1) cand_first = (long long)hc[C_CAND];
-    unconv = (long long)hc[C_UNCONV];
-    DBG("density pass %d%s: cand %llu -> unconverged %llu, regrow %llu\n", iters, nonly ? " (N only)" : "",
-        hc[C_CAND], hc[C_UNCONV], hc[C_REGROW]);
-    if (unconv == 0) break;
-    if (hc[C_REGROW] > 0) regrow_lists(c);
-  }
-  // ghost: finalise and write the caller-order outputs
+  CUDA_TRY(cudaEventRecord(c->ev[9], c->stream));
+  // a9 ghost: finalise and write the caller-order outputs
   std::vector<OutMap> maps;
   GhostOut go;
   const int64_t no = c->n_own;
@@ -815,15 +900,14 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   go.n_own = no;
   go.h_o = B<float>(c, B_HFIN_O, n);
   go.g_o = B<float4>(c, B_GST_O, n);
-  ctr_reset(c);
   LAUNCH(k_ghost, grid1d(c, n, 256), 256, 0, n, Bget<float4>(c, B_XH), uc, dout.acc0, dout.acc1, c->cfg.gamma,
          c->cfg.balsara_eps, go, ctr(c));
   flush_out(c, maps, c->ev[3]);
   c->state = 2;
-  c->force_lists = false;
-  const bool noconv = unconv > 0 && iters >= c->cfg.max_h_iter;
+  const bool noconv = unconv > 0;
   ctr_read(c, hc);
   const long long ndir = (long long)hc[C_NDIR];
+  const long long cand = (long long)hc[C_CAND];
   if (c->n > c->n_own && c->cfg.halo_width > 0.0) {
     // every owned particle's partners must be inside the received halo
     ctr_reset(c);
@@ -838,39 +922,36 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
     memset(st, 0, sizeof(*st));
     fill_struct_stats(c, st);
     st->n_directed = ndir;
-    st->n_candidates = cand_first;
-    st->n_candidates_density_full = cand_first;
+    st->n_candidates = cand;
+    st->n_candidates_density_full = cand;
     st->n_unconverged = noconv ? unconv : 0;
-    st->h_iters = iters;
+    st->h_iters = (int)itmax;
     float ms = 0.f;
     cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
     st->ms_build = ms;
     cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]);
     st->ms_density = ms;
-    cudaEventElapsedTime(&ms, c->ev[6], c->ev[7]);
+    cudaEventElapsedTime(&ms, c->ev[8], c->ev[9]);
     st->ms_kernel_density_full = ms;
   }
   if (noconv) {
-    c->err = "h iteration did not converge in max_h_iter passes: " + std::to_string(unconv) + " particles";
+    c->err = "h iteration did not converge in max_h_iter iterations: " + std::to_string(unconv) + " particles";
     return SPH_E_NOCONV;
   }
   API_END
   return SPH_OK;
 }
 
-// Force inputs in cell order (the hierarchy and the cell order are those of the build;
-// halo particles carry the imported state), node max h and the force lists for
-// r < max(h_i, h_j) at the final h.
+// Force inputs in cell order (halo particles carry the imported state); the interaction
+// lists are rebuilt only when halo particles' h entered after the density loop.
 static void prepare_force(sph_ctx* c) {
   const int64_t n = c->n;
   float4* fx = B<float4>(c, B_FX, n);
   float4* fs = B<float4>(c, B_FS, n);
-  float* hr = Bget<float>(c, B_HLO);
+  float* hr = Bget<float>(c, B_HRCH);
   LAUNCH(k_gather_force, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, Bget<float4>(c, B_XH),
          Bget<float>(c, B_HFIN_O), Bget<float4>(c, B_GST_O), fx, fs, hr);
-  LAUNCH(k_node_hmax, gridfull((int64_t)c->n_nodes * 32, 256), 256, 0, c->n_nodes, nodes(c), hr);
-  c->pool_force = 0;
-  build_lists(c, true, c->n_groups, nullptr);
+  if (!c->force_lists) build_union(c, hr);
   c->force_lists = true;
 }
 
@@ -882,7 +963,10 @@ int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out, int3
   const int64_t no = c->n_own;
   CUDA_TRY(cudaEventRecord(c->ev[4], c->stream));
   DbgTimer _tf(c, "force call");
-  if (!c->force_lists) prepare_force(c);
+  if (c->state == 2) {
+    prepare_force(c);
+    c->state = 3;
+  }
   std::vector<OutMap> maps;
   ForceOut fo;
   fo.a = dev_out(c, a_out, 3 * no, B_OUT0, maps);
@@ -892,14 +976,14 @@ int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out, int3
   fo.perm = Bget<uint32_t>(c, B_PERM);
   fo.n_own = no;
   ctr_reset(c);
-  const GroupLists G = group_lists(c, true);
-  CUDA_TRY(cudaEventRecord(c->ev[8], c->stream));
+  const GroupLists G = group_lists(c);
+  CUDA_TRY(cudaEventRecord(c->ev[10], c->stream));
   {
     DbgTimer _t(c, "force kernel");
     LAUNCH(k_force, gridfull(G.ngroups, FORCE_WARPS), FORCE_WARPS * 32, 0, G, Bget<float4>(c, B_FX),
            Bget<float4>(c, B_VM), Bget<float4>(c, B_FS), c->cfg.alpha, box3(c), fo, ctr(c));
   }
-  CUDA_TRY(cudaEventRecord(c->ev[9], c->stream));
+  CUDA_TRY(cudaEventRecord(c->ev[11], c->stream));
   flush_out(c, maps, c->ev[5]);
   unsigned long long hc[C_NCOUNTERS];
   ctr_read(c, hc);
@@ -913,7 +997,7 @@ int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out, int3
     float ms = 0.f;
     cudaEventElapsedTime(&ms, c->ev[4], c->ev[5]);
     st->ms_force = ms;
-    cudaEventElapsedTime(&ms, c->ev[8], c->ev[9]);
+    cudaEventElapsedTime(&ms, c->ev[10], c->ev[11]);
     st->ms_kernel_force = ms;
   }
   API_END
@@ -994,6 +1078,7 @@ int sph_import_halo_state(sph_ctx* ctx, const float* state) {
   LAUNCH(k_import_state, grid1d(c, k, 256), 256, 0, sd, k, c->n_own, Bget<float>(c, B_HFIN_O),
          Bget<float4>(c, B_GST_O));
   c->force_lists = false;
+  if (c->state > 2) c->state = 2;   // force inputs must be gathered again
   sync(c);
   API_END
   return SPH_OK;

@@ -1,4 +1,5 @@
-// lists.cuh — interaction lists (neighbour finding, section 3.2-3.3).
+// lists.cuh — neighbour finding: the tree walk that builds the interaction lists
+// (section 3.2-3.3).
 //
 // The paper finds the interacting pairs through cell pairs: every particle sits in a cell
 // whose edge is at least its h, so its partners lie in the 26 neighbouring cells
@@ -7,182 +8,259 @@
 // onto the axis joining the cells, so the sweep stops at the first particle whose projected
 // distance exceeds h (P:644-698, 13 presorted directions per cell).
 //
-// On the GPU the same search is done ONCE per structure, per target group (<= 32
-// consecutive particles of one leaf, one warp), and its result -- the group's candidate
-// sources -- is stored as a flat list that every density pass (the h iteration) and the
-// force pass stream through (the paper reuses its sorts for both loops):
+// On the GPU the same search runs per target group (<= 32 consecutive particles of one
+// cell, one warp) and its result is stored, so the h iteration and the two interaction
+// loops reuse it (the paper reuses its sorts for both loops):
 //   1. the cells within reach of the group: the top cells around the group's bounding box
-//      (with their periodic images), refined recursively into their children
-//      while the child's box is within reach (the pair refinement of P:523-532, decided
-//      per child box instead of per cell pair);
-//   2. in a reached leaf, the sources are swept in the leaf's presorted order along the
+//      (with their periodic images), refined into their children while a
+//      child's box is within reach (the pair refinement of P:523-532, decided per child box
+//      instead of per cell pair), 32 cells per round (one per lane);
+//   2. in a reached leaf the sources are swept in the leaf's presorted order along the
 //      canonical direction joining the group and the leaf, stopping at the first source
 //      whose projection lies beyond the window (the sorted sweep of P:644-669, R6, R20);
-//      leaves without a sorted list are swept whole;
-//   3. every swept source is kept iff it lies within the reach of at least one target of
-//      the group (one distance test per lane of the warp; union of the targets' spheres).
-// Reach: density  r < h_build,i (list valid for every h <= h_build in the Newton iteration);
-//        force    r < max(h_i, h_j) with the final h.
-// List entry: (periodic image code << 27) | source index (cell order); image code
-// c = cx + 3 cy + 9 cz, c_a = 0 none, 1 source shifted by -L_a, 2 by +L_a.
+//      leaves without presorted lists are streamed whole, 32 sources per chunk;
+//   3. each swept source passes a box test against the group, then one exact distance test
+//      per target (lane), and is recorded:
+//        NB mode    per target i, the squared distances r^2 < h_build,i^2 (the neighbour
+//                   lists of the h iteration, k_hsolve);
+//        UNION mode per group, the sources within reach of at least one target, with
+//                   reach max(h_i, h_j) at the final h: the list the density and
+//                   force loops stream (interact.cuh). Counted, then filled.
+// Coordinates are relative to the group's first particle o with exact periodic images
+// (rel_pos), so the recorded r^2 are the ones the interaction kernels compute.
+// UNION entry: (periodic image code << 27) | source index (cell order); image code
+// c = cx + 3 cy + 9 cz, c_a = 0 none, 1 source at x - L_a, 2 source at x + L_a.
 #pragma once
 #include "build.cuh"
 
 #define WALK_WARPS 8
-#define WALK_STACK 160
 #define WALK_TAKE 32    // a node holding <= WALK_TAKE particles is swept whole (no descent)
+#define WALK_CAP 384    // frontier entries (node | image code << 27), LIFO
+#define WALK_DFS 112    // room for the depth-first fallback above the frontier
+#define WALK_RQ 64      // queued leaf ranges streamed together
+
+#define MODE_NB 0
+#define MODE_COUNT 1
+#define MODE_FILL 2
+
+// source position relative to the group origin o (oL = o - L), periodic image code c:
+// x - L is exact for a source near L, o - L for a group near L (Sterbenz; R19, H2)
+__device__ __forceinline__ float3 rel_pos(float4 p, uint32_t code, float3 o, float3 oL, const float* L) {
+  const int cx = code % 3, cy = (code / 3) % 3, cz = code / 9;
+  const float x = (cx == 1 ? p.x - L[0] : p.x) - (cx == 2 ? oL.x : o.x);
+  const float y = (cy == 1 ? p.y - L[1] : p.y) - (cy == 2 ? oL.y : o.y);
+  const float z = (cz == 1 ? p.z - L[2] : p.z) - (cz == 2 ? oL.z : o.z);
+  return make_float3(x, y, z);
+}
+__device__ __forceinline__ float shift_of(int c, float L) { return c == 1 ? -L : (c == 2 ? L : 0.f); }
+__device__ __forceinline__ float reach_eff(float r, float slack) { return fmaf(r, 1.00001f, slack); }
 
 struct WalkParams {
   const int4* groups;
   int nsel;                 // groups to walk
   const int* sel;           // their ids (null: 0..nsel-1)
   const float4* xh;         // cell-order positions
-  const float* reach;       // per particle: density h_build; force h (targets and sources)
-  const uint32_t* perm;     // cell order -> caller index; targets are perm < n_own
+  const float* reach;       // per particle: NB h_build; UNION the h used for the reach (0: none)
+  const uint8_t* tsel;      // NB: targets are the particles with tsel == tsel_val (null: owned)
+  uint8_t tsel_val;
+  const uint32_t* perm;     // cell order -> caller index; targets are owned (perm < n_own)
   int64_t n_own;
   NodeArrays N;
   LevelGeom g;
   const int* topmap;
   const SortEntry* sorted;
-  int force;
-  float reach_max;          // max reach over all particles (force: source reach bound)
-  float slack;              // absolute slack of the geometric tests (fp32 rounding)
+  float reach_max;          // UNION: max source reach (bound for the top-cell range)
+  float slack;              // absolute slack of the box tests (fp32 rounding of corners)
+  // UNION
   int64_t* off;             // per group: list offset (FILL reads)
   int* len;                 // per group: list length (COUNT writes)
   int* len_sel;             // per selected group: list length (COUNT writes, for the scan)
   uint32_t* out;            // list pool (FILL)
+  int ucap;                 // FILL: entries recorded per group (beyond: counted only)
+  int check;                // FILL: 1 = second pass into exact space, verify the length
+  // NB
+  float* nb_r2;             // [n * K]: particle s's entries at group_first*K + e*group_count + lane
+  int* nb_cnt;              // [n] sources with r^2 < h_build^2 (may exceed K: overflow)
+  int K;
+  const int64_t* ovf_off;   // NB overflow walk: the particle's list at ovf + ovf_off[s] (contiguous)
+  float* ovf;
   unsigned long long* ctr;
 };
 
-#define WALK_CAP 384    // frontier entries (node | image code << 27), LIFO
-#define WALK_DFS 112    // room for the depth-first fallback above the frontier
-#define WALK_RQ 64      // queued leaf ranges streamed together
 struct WalkSmem {
   int stk[WALK_CAP + WALK_DFS];
   int rq_first[WALK_RQ];
   int rq_code[WALK_RQ];
   int rq_pre[WALK_RQ + 1];  // exclusive prefix of the queued ranges' counts
-  float4 s[32];             // staged box survivors: shifted position, reach
+  float4 s[32];             // staged box survivors: relative position, source reach
 };
 
 struct WalkState {
-  float3 lo, hi;            // targets' bounding box
+  float3 o, oL;             // group origin, origin - L
+  float3 lo, hi;            // targets' bounding box (relative)
   float R;                  // max target reach
-  float xi, yi, zi, ri;     // this lane's target (ri = -1: not a target)
-  int64_t base;             // FILL: list offset of the group
-  int cur;                  // entries emitted so far
+  float xi, yi, zi, ri;     // this lane's target (relative; ri = -1: not a target)
+  int64_t base;             // FILL: list offset of the group / NB: column base
+  int cur;                  // UNION: entries emitted so far; NB: this lane's count
+  int gz, lane;
+  int raw;                  // sources streamed through the filters (diagnostics)
 };
 
-__device__ __forceinline__ float reach_eff(float r, float slack) { return fmaf(r, 1.00001f, slack); }
-
-// one chunk of <= 32 candidate sources (one per lane): keep those within reach of a target
-template <bool FILL>
+// one chunk of <= 32 candidate sources (one per lane, relative position p, reach hj)
+template <int MODE>
 __device__ __forceinline__ void emit_chunk(const WalkParams& P, WalkState& W, WalkSmem& S, bool valid, int j,
-                                           float px, float py, float pz, float hj, int code, int lane) {
+                                           float3 p, float hj, int code) {
+  const int lane = W.lane;
   // 1. box filter against the targets' bounding box
   bool keep = false;
   if (valid) {
-    const float ex = fmaxf(fmaxf(W.lo.x - px, px - W.hi.x), 0.f);
-    const float ey = fmaxf(fmaxf(W.lo.y - py, py - W.hi.y), 0.f);
-    const float ez = fmaxf(fmaxf(W.lo.z - pz, pz - W.hi.z), 0.f);
-    const float rr = reach_eff(P.force ? fmaxf(W.R, hj) : W.R, P.slack);
+    const float ex = fmaxf(fmaxf(W.lo.x - p.x, p.x - W.hi.x), 0.f);
+    const float ey = fmaxf(fmaxf(W.lo.y - p.y, p.y - W.hi.y), 0.f);
+    const float ez = fmaxf(fmaxf(W.lo.z - p.z, p.z - W.hi.z), 0.f);
+    const float rr = reach_eff(MODE == MODE_NB ? W.R : fmaxf(W.R, hj), P.slack);
     keep = fmaf(ex, ex, fmaf(ey, ey, ez * ez)) < rr * rr;
   }
+  W.raw += __popc(__ballot_sync(FULL_MASK, valid));
   const unsigned bal = __ballot_sync(FULL_MASK, keep);
   if (!bal) return;
   const int m = __popc(bal);
   const int pos = __popc(bal & lanemask_lt());
-  if (keep) S.s[pos] = make_float4(px, py, pz, P.force ? reach_eff(hj, P.slack) : 0.f);
+  if (keep) S.s[pos] = make_float4(p.x, p.y, p.z, MODE == MODE_NB ? 0.f : reach_eff(hj, 0.f));
   __syncwarp();
-  // 2. union of the targets' spheres: lane = target, tests every staged survivor
+  // 2. exact distance test per target (lane)
+  if (MODE == MODE_NB) {
+    if (W.ri >= 0.f) {
+      const float ri = reach_eff(W.ri, 0.f);
+      const float ri2 = ri * ri;
+      for (int t = 0; t < m; ++t) {
+        const float4 q = S.s[t];
+        const float dx = W.xi - q.x, dy = W.yi - q.y, dz = W.zi - q.z;
+        const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+        if (r2 < ri2) {
+          if (P.ovf) P.ovf[W.base + W.cur] = r2;
+          else if (W.cur < P.K) P.nb_r2[W.base + (int64_t)W.cur * W.gz] = r2;
+          ++W.cur;
+        }
+      }
+    }
+    __syncwarp();
+    return;
+  }
   unsigned hm = 0u;
   if (W.ri >= 0.f) {
-    const float ri = reach_eff(W.ri, P.slack);
+    const float ri = reach_eff(W.ri, 0.f);
     const float ri2 = ri * ri;
     for (int t = 0; t < m; ++t) {
       const float4 q = S.s[t];
       const float dx = W.xi - q.x, dy = W.yi - q.y, dz = W.zi - q.z;
       const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-      const float lim2 = P.force ? fmaxf(ri2, q.w * q.w) : ri2;
-      hm |= (unsigned)(r2 < lim2) << t;
+      hm |= (unsigned)(r2 < fmaxf(ri2, q.w * q.w)) << t;
     }
   }
   const unsigned km = __reduce_or_sync(FULL_MASK, hm);
   __syncwarp();
   const bool mine = keep && ((km >> pos) & 1u);
   const unsigned b2 = __ballot_sync(FULL_MASK, mine);
-  if (FILL && mine)
-    P.out[W.base + W.cur + __popc(b2 & lanemask_lt())] = ((uint32_t)code << SPH_IDX_BITS) | (uint32_t)j;
+  if (MODE == MODE_FILL && mine) {
+    const int idx = W.cur + __popc(b2 & lanemask_lt());
+    if (idx < P.ucap) P.out[W.base + idx] = ((uint32_t)code << SPH_IDX_BITS) | (uint32_t)j;
+  }
   W.cur += __popc(b2);
 }
 
-// shifted source position in the group's frame: x + k L (k in {-1, 0, 1} per axis)
-__device__ __forceinline__ float3 shifted(float4 p, int code, const LevelGeom& g) {
-  const int cx = code % 3, cy = (code / 3) % 3, cz = code / 9;
-  return make_float3(cx == 1 ? p.x - g.L[0] : (cx == 2 ? p.x + g.L[0] : p.x),
-                     cy == 1 ? p.y - g.L[1] : (cy == 2 ? p.y + g.L[1] : p.y),
-                     cz == 1 ? p.z - g.L[2] : (cz == 2 ? p.z + g.L[2] : p.z));
+__device__ __forceinline__ float3 node_corner_rel(const WalkParams& P, const WalkState& W, int4 c, int code) {
+  const int l = c.w;
+  return make_float3(node_corner(c.x, l, 0, P.g) + shift_of(code % 3, P.g.L[0]) - W.o.x,
+                     node_corner(c.y, l, 1, P.g) + shift_of((code / 3) % 3, P.g.L[1]) - W.o.y,
+                     node_corner(c.z, l, 2, P.g) + shift_of(code / 9, P.g.L[2]) - W.o.z);
 }
-__device__ __forceinline__ float shift_of(int c, float L) { return c == 1 ? -L : (c == 2 ? L : 0.f); }
 
-// node box (group frame) within reach of the targets' box
+// node box within reach of the targets' box
+template <int MODE>
 __device__ __forceinline__ bool node_in_reach(const WalkParams& P, const WalkState& W, int node, int code) {
   const int4 c = P.N.ijk[node];
   const int l = c.w;
-  const float sx = shift_of(code % 3, P.g.L[0]), sy = shift_of((code / 3) % 3, P.g.L[1]),
-              sz = shift_of(code / 9, P.g.L[2]);
-  const float cx = node_corner(c.x, l, 0, P.g) + sx, cy = node_corner(c.y, l, 1, P.g) + sy,
-              cz = node_corner(c.z, l, 2, P.g) + sz;
-  const float gx = fmaxf(fmaxf(cx - W.hi.x, W.lo.x - (cx + P.g.E[l][0])), 0.f);
-  const float gy = fmaxf(fmaxf(cy - W.hi.y, W.lo.y - (cy + P.g.E[l][1])), 0.f);
-  const float gz = fmaxf(fmaxf(cz - W.hi.z, W.lo.z - (cz + P.g.E[l][2])), 0.f);
-  const float rr = reach_eff(P.force ? fmaxf(W.R, P.N.hmax[node]) : W.R, P.slack);
+  const float3 cr = node_corner_rel(P, W, c, code);
+  const float gx = fmaxf(fmaxf(cr.x - W.hi.x, W.lo.x - (cr.x + P.g.E[l][0])), 0.f);
+  const float gy = fmaxf(fmaxf(cr.y - W.hi.y, W.lo.y - (cr.y + P.g.E[l][1])), 0.f);
+  const float gz = fmaxf(fmaxf(cr.z - W.hi.z, W.lo.z - (cr.z + P.g.E[l][2])), 0.f);
+  const float rr = reach_eff(MODE == MODE_NB ? W.R : fmaxf(W.R, P.N.hmax[node]), P.slack);
   return fmaf(gx, gx, fmaf(gy, gy, gz * gz)) < rr * rr;
 }
 
-// sweep a reached leaf (or small node): sorted window sweep if the leaf has presorted
-// lists and lies to one side of the group, else its whole contiguous range
-template <bool FILL>
-__device__ __forceinline__ void sweep_node(const WalkParams& P, WalkState& W, WalkSmem& S, int node, int code,
-                                           int lane) {
+// Refines the box test: the node (one per lane) is kept iff its box is within reach of at
+// least one target's own sphere (each target broadcast in turn), so a group whose targets'
+// h differ widely does not visit the cells only its bounding box reaches.
+template <int MODE>
+__device__ __forceinline__ bool node_in_spheres(const WalkParams& P, const WalkState& W, int node, int code,
+                                                bool coarse) {
+  unsigned tm = __ballot_sync(FULL_MASK, W.ri >= 0.f);
+  if (!__any_sync(FULL_MASK, coarse)) return false;
+  float3 lo = make_float3(0.f, 0.f, 0.f), hi = lo;
+  float hmn = 0.f;
+  if (coarse) {
+    const int4 c = P.N.ijk[node];
+    lo = node_corner_rel(P, W, c, code);
+    hi = make_float3(lo.x + P.g.E[c.w][0], lo.y + P.g.E[c.w][1], lo.z + P.g.E[c.w][2]);
+    if (MODE != MODE_NB) hmn = P.N.hmax[node];
+  }
+  bool hit = false;
+  while (tm) {
+    const int t = __ffs(tm) - 1;
+    tm &= tm - 1;
+    const float tx = __shfl_sync(FULL_MASK, W.xi, t), ty = __shfl_sync(FULL_MASK, W.yi, t),
+                tz = __shfl_sync(FULL_MASK, W.zi, t), tr = __shfl_sync(FULL_MASK, W.ri, t);
+    const float gx = fmaxf(fmaxf(lo.x - tx, tx - hi.x), 0.f);
+    const float gy = fmaxf(fmaxf(lo.y - ty, ty - hi.y), 0.f);
+    const float gz = fmaxf(fmaxf(lo.z - tz, tz - hi.z), 0.f);
+    const float rr = reach_eff(MODE == MODE_NB ? tr : fmaxf(tr, hmn), P.slack);
+    hit |= fmaf(gx, gx, fmaf(gy, gy, gz * gz)) < rr * rr;
+  }
+  return coarse && hit;
+}
+
+// sorted window sweep of a leaf with presorted lists that lies to one side of the group,
+// else its whole contiguous range
+template <int MODE>
+__device__ __forceinline__ void sweep_node(const WalkParams& P, WalkState& W, WalkSmem& S, int node, int code) {
+  const int lane = W.lane;
   const int first = P.N.first[node], cnt = P.N.count[node];
   const int64_t soff = P.N.sortoff[node];
+  const float* L = P.g.L;
   int k = 13;
-  float3 cnr;
+  float3 cr = make_float3(0.f, 0.f, 0.f);
   if (soff >= 0) {
     const int4 c = P.N.ijk[node];
     const int l = c.w;
-    cnr = make_float3(node_corner(c.x, l, 0, P.g) + shift_of(code % 3, P.g.L[0]),
-                      node_corner(c.y, l, 1, P.g) + shift_of((code / 3) % 3, P.g.L[1]),
-                      node_corner(c.z, l, 2, P.g) + shift_of(code / 9, P.g.L[2]));
-    const int ox = cnr.x > W.hi.x ? 1 : (cnr.x + P.g.E[l][0] < W.lo.x ? -1 : 0);
-    const int oy = cnr.y > W.hi.y ? 1 : (cnr.y + P.g.E[l][1] < W.lo.y ? -1 : 0);
-    const int oz = cnr.z > W.hi.z ? 1 : (cnr.z + P.g.E[l][2] < W.lo.z ? -1 : 0);
+    cr = node_corner_rel(P, W, c, code);
+    const int ox = cr.x > W.hi.x ? 1 : (cr.x + P.g.E[l][0] < W.lo.x ? -1 : 0);
+    const int oy = cr.y > W.hi.y ? 1 : (cr.y + P.g.E[l][1] < W.lo.y ? -1 : 0);
+    const int oz = cr.z > W.hi.z ? 1 : (cr.z + P.g.E[l][2] < W.lo.z ? -1 : 0);
     k = (ox + 1) * 9 + (oy + 1) * 3 + (oz + 1);
   }
-  if (k == 13) {                                   // whole range
+  if (k == 13) {
     for (int b0 = 0; b0 < cnt; b0 += 32) {
       const int e = b0 + lane;
       const bool v = e < cnt;
-      float3 ps = make_float3(0.f, 0.f, 0.f);
+      float3 p = make_float3(0.f, 0.f, 0.f);
       float hj = 0.f;
       if (v) {
-        ps = shifted(P.xh[first + e], code, P.g);
+        p = rel_pos(P.xh[first + e], code, W.o, W.oL, L);
         hj = P.reach[first + e];
       }
-      emit_chunk<FILL>(P, W, S, v, first + e, ps.x, ps.y, ps.z, hj, code, lane);
+      emit_chunk<MODE>(P, W, S, v, first + e, p, hj, code);
     }
     return;
   }
-  // sorted sweep along canonical direction d; the leaf lies on the +d side of the group
-  // (ascending keys, nearest first) or on the -d side (flip: descending)
+  // the leaf lies on the +d side of the group (ascending keys, nearest first) or on the
+  // -d side (flip: descending)
   const int d = slot_dir(k);
   const bool flip = slot_flip(k);
   const float3 du = dir_unit(d);
   const SortEntry* __restrict__ list = P.sorted + soff + (int64_t)d * cnt;
-  float pr = W.ri >= 0.f ? proj(W.xi - cnr.x, W.yi - cnr.y, W.zi - cnr.z, du) : (flip ? INFINITY : -INFINITY);
+  float pr = W.ri >= 0.f ? proj(W.xi - cr.x, W.yi - cr.y, W.zi - cr.z, du) : (flip ? INFINITY : -INFINITY);
   pr = flip ? warp_min_f(pr) : warp_max_f(pr);
-  const float win = reach_eff(P.force ? fmaxf(W.R, P.N.hmax[node]) : W.R, P.slack) + P.slack;
+  const float win = reach_eff(MODE == MODE_NB ? W.R : fmaxf(W.R, P.N.hmax[node]), P.slack) + P.slack;
   const float lim = flip ? pr - win : pr + win;
   for (int b0 = 0; b0 < cnt; b0 += 32) {
     const int e = b0 + lane;
@@ -194,27 +272,28 @@ __device__ __forceinline__ void sweep_node(const WalkParams& P, WalkState& W, Wa
       j = en.idx;
     }
     const unsigned inwin = __ballot_sync(FULL_MASK, v);
-    float3 ps = make_float3(0.f, 0.f, 0.f);
+    float3 p = make_float3(0.f, 0.f, 0.f);
     float hj = 0.f;
     if (v) {
-      ps = shifted(P.xh[j], code, P.g);
+      p = rel_pos(P.xh[j], code, W.o, W.oL, L);
       hj = P.reach[j];
     }
-    emit_chunk<FILL>(P, W, S, v, j, ps.x, ps.y, ps.z, hj, code, lane);
-    if (__popc(inwin) < min(32, cnt - b0)) break;  // early exit
+    emit_chunk<MODE>(P, W, S, v, j, p, hj, code);
+    if (__popc(inwin) < min(32, cnt - b0)) break;   // early exit
   }
 }
 
 // stream the queued leaf ranges as one sequence, 32 sources per chunk
-template <bool FILL>
-__device__ __forceinline__ void flush_ranges(const WalkParams& P, WalkState& W, WalkSmem& S, int& nq, int lane) {
+template <int MODE>
+__device__ __forceinline__ void flush_ranges(const WalkParams& P, WalkState& W, WalkSmem& S, int& nq) {
   if (nq == 0) return;
+  const int lane = W.lane;
   const int total = S.rq_pre[nq];
   for (int b0 = 0; b0 < total; b0 += 32) {
     const int gi = b0 + lane;
     const bool v = gi < total;
     int j = 0, code = 0;
-    float3 ps = make_float3(0.f, 0.f, 0.f);
+    float3 p = make_float3(0.f, 0.f, 0.f);
     float hj = 0.f;
     if (v) {
       int r = 0;                                    // rq_pre[r] <= gi < rq_pre[r+1]
@@ -223,18 +302,19 @@ __device__ __forceinline__ void flush_ranges(const WalkParams& P, WalkState& W, 
         if (r + step < nq && S.rq_pre[r + step] <= gi) r += step;
       j = S.rq_first[r] + (gi - S.rq_pre[r]);
       code = S.rq_code[r];
-      ps = shifted(P.xh[j], code, P.g);
+      p = rel_pos(P.xh[j], code, W.o, W.oL, P.g.L);
       hj = P.reach[j];
     }
-    emit_chunk<FILL>(P, W, S, v, j, ps.x, ps.y, ps.z, hj, code, lane);
+    emit_chunk<MODE>(P, W, S, v, j, p, hj, code);
   }
   __syncwarp();
   nq = 0;
 }
 
 // depth-first descent of one subtree (fallback when the frontier is full)
-template <bool FILL>
-__device__ void dfs_subtree(const WalkParams& P, WalkState& W, WalkSmem& S, int* stk, int entry, int& nq, int lane) {
+template <int MODE>
+__device__ void dfs_subtree(const WalkParams& P, WalkState& W, WalkSmem& S, int* stk, int entry, int& nq) {
+  const int lane = W.lane;
   if (lane == 0) stk[0] = entry;
   int top = 1;
   __syncwarp();
@@ -245,26 +325,28 @@ __device__ void dfs_subtree(const WalkParams& P, WalkState& W, WalkSmem& S, int*
     const int4 rec = P.N.rec[nd];
     if (rec.z >= 0 && rec.y > WALK_TAKE) {
       int ch = -1;
-      const int mask = rec.w & 0xff;
-      if (lane < __popc(mask)) {
+      bool rc = false;
+      if (lane < __popc(rec.w & 0xff)) {
         ch = rec.z + lane;
-        if (!node_in_reach(P, W, ch, code)) ch = -1;
+        rc = node_in_reach<MODE>(P, W, ch, code);
       }
+      rc = node_in_spheres<MODE>(P, W, ch, code, rc);
+      if (!rc) ch = -1;
       const unsigned ok = __ballot_sync(FULL_MASK, ch >= 0);
       if (ch >= 0) stk[top + __popc(ok & lanemask_lt())] = ch | (code << SPH_IDX_BITS);
       top += __popc(ok);
       __syncwarp();
     } else {
-      flush_ranges<FILL>(P, W, S, nq, lane);
-      sweep_node<FILL>(P, W, S, nd, code, lane);
+      flush_ranges<MODE>(P, W, S, nq);
+      sweep_node<MODE>(P, W, S, nd, code);
     }
   }
 }
 
 // Warp per group: the cells within reach, 32 nodes per round (each lane tests one node's
 // box; reached internal nodes push their children, reached leaves queue their ranges),
-// then the queued ranges streamed through the source filters.
-template <bool FILL>
+// and the queued ranges streamed through the source filters.
+template <int MODE>
 __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkParams P) {
   __shared__ WalkSmem smem[WALK_WARPS];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -275,34 +357,50 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkParams P) {
   const int4 grp = P.groups[gid];
   const int s = grp.y + lane;
   WalkState W;
+  W.lane = lane;
+  W.gz = grp.z;
+  const float4 o4 = P.xh[grp.y];
+  W.o = make_float3(o4.x, o4.y, o4.z);
+  W.oL = make_float3(o4.x - P.g.L[0], o4.y - P.g.L[1], o4.z - P.g.L[2]);
   W.ri = -1.f;
   W.xi = W.yi = W.zi = 0.f;
-  if (lane < grp.z && P.perm[s] < (uint32_t)P.n_own) {
-    const float4 p = P.xh[s];
-    W.xi = p.x;
-    W.yi = p.y;
-    W.zi = p.z;
-    W.ri = P.reach[s];
+  float ax = 0.f, ay = 0.f, az = 0.f;      // absolute target position (top-cell range)
+  bool tg = false;
+  if (lane < grp.z) {
+    tg = P.tsel ? P.tsel[s] == P.tsel_val : P.perm[s] < (uint32_t)P.n_own;
+    if (tg) {
+      const float4 p = P.xh[s];
+      ax = p.x;
+      ay = p.y;
+      az = p.z;
+      W.xi = p.x - W.o.x;
+      W.yi = p.y - W.o.y;
+      W.zi = p.z - W.o.z;
+      W.ri = P.reach[s];
+    }
   }
-  const bool tg = W.ri >= 0.f;
   W.lo = make_float3(warp_min_f(tg ? W.xi : INFINITY), warp_min_f(tg ? W.yi : INFINITY),
                      warp_min_f(tg ? W.zi : INFINITY));
   W.hi = make_float3(warp_max_f(tg ? W.xi : -INFINITY), warp_max_f(tg ? W.yi : -INFINITY),
                      warp_max_f(tg ? W.zi : -INFINITY));
+  const float alo[3] = {warp_min_f(tg ? ax : INFINITY), warp_min_f(tg ? ay : INFINITY), warp_min_f(tg ? az : INFINITY)};
+  const float ahi[3] = {warp_max_f(tg ? ax : -INFINITY), warp_max_f(tg ? ay : -INFINITY),
+                        warp_max_f(tg ? az : -INFINITY)};
   W.R = warp_max_f(tg ? W.ri : 0.f);
   W.cur = 0;
-  W.base = FILL ? P.off[gid] : 0;
+  W.raw = 0;
+  W.base = MODE == MODE_FILL ? P.off[gid] : (MODE == MODE_NB ? (int64_t)grp.y * P.K + lane : 0);
+  if (MODE == MODE_NB && P.ovf && tg) W.base = P.ovf_off[s];
   int nq = 0;
   if (__any_sync(FULL_MASK, tg)) {
     // top cells (unwrapped indices) overlapping the box grown by the largest possible reach
-    const float Rw = reach_eff(P.force ? fmaxf(W.R, P.reach_max) : W.R, P.slack) + P.slack;
+    const float Rw = reach_eff(MODE == MODE_NB ? W.R : fmaxf(W.R, P.reach_max), P.slack) + P.slack;
     int a0[3], na[3];
-    const float lo3[3] = {W.lo.x, W.lo.y, W.lo.z}, hi3[3] = {W.hi.x, W.hi.y, W.hi.z};
     int T = 1;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       const float E = P.g.E[0][a];
-      int lo_i = (int)floorf((lo3[a] - Rw) / E), hi_i = (int)floorf((hi3[a] + Rw) / E);
+      int lo_i = (int)floorf((alo[a] - Rw) / E), hi_i = (int)floorf((ahi[a] + Rw) / E);
       lo_i = max(lo_i, -P.g.ntop[a]);
       hi_i = min(hi_i, 2 * P.g.ntop[a] - 1);
       a0[a] = lo_i;
@@ -334,7 +432,7 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkParams P) {
           const int e = S.stk[top - 1];
           __syncwarp();
           --top;
-          dfs_subtree<FILL>(P, W, S, S.stk + top, e, nq, lane);
+          dfs_subtree<MODE>(P, W, S, S.stk + top, e, nq);
           continue;
         }
         int e = 0;
@@ -346,7 +444,10 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkParams P) {
         int4 rec = make_int4(0, 0, -1, 0);
         if (lane < k) {
           rec = P.N.rec[nd];
-          reach = node_in_reach(P, W, nd, code);
+          reach = node_in_reach<MODE>(P, W, nd, code);
+        }
+        reach = node_in_spheres<MODE>(P, W, nd, code, reach);
+        if (lane < k) {
           leaf = reach && !(rec.z >= 0 && rec.y > WALK_TAKE);
           srt = leaf && P.N.sortoff[nd] >= 0;
         }
@@ -364,39 +465,26 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkParams P) {
         // reached unsorted leaves: queue their ranges
         const bool ql = leaf && !srt;
         const unsigned qb = __ballot_sync(FULL_MASK, ql);
-        if (nq + __popc(qb) > WALK_RQ) flush_ranges<FILL>(P, W, S, nq, lane);
-        if (ql) {
-          const int q = nq + __popc(qb & lanemask_lt());
-          S.rq_first[q] = rec.x;
-          S.rq_code[q] = code;
-          S.rq_pre[q + 1] = rec.y;                  // counts; prefix below
-        }
-        __syncwarp();
+        if (nq + __popc(qb) > WALK_RQ) flush_ranges<MODE>(P, W, S, nq);
         if (qb) {
-          const int nn = nq + __popc(qb);
-          if (lane == 0) S.rq_pre[0] = 0;
-          __syncwarp();
-          // exclusive prefix over the queue (<= 64 entries): lanes own entries lane, lane+32
-          int c0 = (lane + 1 <= nn && lane >= nq) ? S.rq_pre[lane + 1] : 0;
-          int c1 = (lane + 33 <= nn && lane + 32 >= nq) ? S.rq_pre[lane + 33] : 0;
-          __syncwarp();
-          // recompute the whole prefix from the raw counts of the new entries
-          int v0 = c0, v1 = c1;
+          const int q = nq + __popc(qb & lanemask_lt());
+          if (ql) {
+            S.rq_first[q] = rec.x;
+            S.rq_code[q] = code;
+          }
+          // prefix of the new counts (one per queuing lane, in lane order)
+          int v0 = ql ? rec.y : 0;
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
-            const int y0 = __shfl_up_sync(FULL_MASK, v0, o), y1 = __shfl_up_sync(FULL_MASK, v1, o);
-            if (lane >= o) {
-              v0 += y0;
-              v1 += y1;
-            }
+            const int y = __shfl_up_sync(FULL_MASK, v0, o);
+            if (lane >= o) v0 += y;
           }
-          const int t0 = __shfl_sync(FULL_MASK, v0, 31);
-          const int basep = S.rq_pre[nq];
+          const int basep = nq == 0 ? 0 : S.rq_pre[nq];
           __syncwarp();
-          if (lane >= nq && lane + 1 <= nn) S.rq_pre[lane + 1] = basep + v0;
-          if (lane + 32 >= nq && lane + 33 <= nn) S.rq_pre[lane + 33] = basep + t0 + v1;
+          if (lane == 0 && nq == 0) S.rq_pre[0] = 0;
+          if (ql) S.rq_pre[q + 1] = basep + v0;
           __syncwarp();
-          nq = nn;
+          nq += __popc(qb);
         }
         // reached sorted leaves: windowed sweeps, one at a time
         unsigned sbm = __ballot_sync(FULL_MASK, srt);
@@ -404,17 +492,28 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkParams P) {
           const int src = __ffs(sbm) - 1;
           sbm &= sbm - 1;
           const int snd = __shfl_sync(FULL_MASK, nd, src), scode = __shfl_sync(FULL_MASK, code, src);
-          sweep_node<FILL>(P, W, S, snd, scode, lane);
+          flush_ranges<MODE>(P, W, S, nq);
+          sweep_node<MODE>(P, W, S, snd, scode);
         }
       }
     }
-    flush_ranges<FILL>(P, W, S, nq, lane);
+    flush_ranges<MODE>(P, W, S, nq);
   }
-  if (!FILL && lane == 0) {
-    P.len[gid] = W.cur;
-    if (P.len_sel) P.len_sel[w] = W.cur;
+  if (lane == 0) {
+    atomicAdd(&P.ctr[C_TMP2], (unsigned long long)W.raw);
+    atomicMax(&P.ctr[C_TMP0], (unsigned long long)W.raw);
   }
-  if (FILL && lane == 0 && W.cur != P.len[gid]) atomicOr(&P.ctr[C_ERR], 1ull << 20);   // count/fill mismatch
+  if (MODE == MODE_NB) {
+    if (tg && !P.ovf) P.nb_cnt[s] = W.cur;
+  } else if (MODE == MODE_COUNT) {
+    if (lane == 0) {
+      P.len[gid] = W.cur;
+      if (P.len_sel) P.len_sel[w] = W.cur;
+    }
+  } else if (lane == 0) {
+    if (!P.check) P.len[gid] = W.cur;
+    else if (W.cur != P.len[gid]) atomicOr(&P.ctr[C_ERR], 1ull << 20);   // pass mismatch
+  }
 }
 
 // list offsets of the selected groups: base + exclusive scan of their lengths
@@ -425,22 +524,19 @@ __global__ void k_set_offsets(int nsel, const int* __restrict__ sel, const int64
   off[sel ? sel[w] : w] = base + scan[w];
 }
 
-// groups flagged for a list rebuild (a target's h outgrew its h_build), compaction flags
+// per-particle states of the h iteration
 #define HS_DONE 0
 #define HS_ACTIVE 1
-#define HS_REGROW 2   // active; h_build grown: its group's density list is rebuilt before the next pass
-__global__ void k_group_flags(const int4* __restrict__ groups, int ngroups, uint8_t* __restrict__ state,
-                              int* __restrict__ flag) {
+#define HS_REGROW 2   // needs a neighbour list for a new h_build (grown, or shrunk after overflow)
+
+// groups holding a particle in state `val` (compaction flags)
+__global__ void k_group_flags(const int4* __restrict__ groups, int ngroups, const uint8_t* __restrict__ state,
+                              uint8_t val, int* __restrict__ flag) {
   const int lane = threadIdx.x & 31;
   const int gi = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   if (gi >= ngroups) return;
   const int4 g = groups[gi];
-  bool r = false;
-  if (lane < g.z) {
-    const int s = g.y + lane;
-    r = state[s] == HS_REGROW;
-    if (r) state[s] = HS_ACTIVE;
-  }
+  const bool r = lane < g.z && state[g.y + lane] == val;
   const bool any = __any_sync(FULL_MASK, r);
   if (lane == 0) flag[gi] = any ? 1 : 0;
 }
@@ -454,4 +550,45 @@ __global__ void k_compact_idx(const int* __restrict__ flag, const int* __restric
 __global__ void k_widen_i32(const int* __restrict__ in, int64_t n, int64_t* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = in[i];
+}
+
+// NB overflow: particles whose list exceeded K (count known) get an exactly sized list in the
+// overflow pool; state HS_OVF marks them for the second, contiguous-layout walk
+#define HS_OVF 3
+#define NB_POOL_MAX 4096   // longer lists (h_build far too large) are not recorded: h_build shrinks
+__global__ void k_mark_overflow(const int4* __restrict__ groups, int ngroups, const uint8_t* __restrict__ tsel,
+                                int tsel_val, const uint32_t* __restrict__ perm, int64_t n_own,
+                                const int* __restrict__ cnt, int K, uint8_t* __restrict__ state,
+                                int64_t* __restrict__ ovf_cnt, int64_t* __restrict__ ovf_off) {
+  const int lane = threadIdx.x & 31;
+  const int gi = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  if (gi >= ngroups) return;
+  const int4 g = groups[gi];
+  if (lane >= g.z) return;
+  const int s = g.y + lane;
+  const bool tg = tsel_val >= 0 ? tsel[s] == (uint8_t)tsel_val : perm[s] < (uint32_t)n_own;
+  const bool o = tg && cnt[s] > K && cnt[s] <= NB_POOL_MAX;
+  ovf_cnt[s] = o ? cnt[s] : 0;
+  if (o) state[s] = HS_OVF;
+  else if (tg) ovf_off[s] = -1;
+}
+__global__ void k_ovf_offsets(int64_t n, const int64_t* __restrict__ c, const int64_t* __restrict__ scan,
+                              int64_t base, int64_t* __restrict__ off) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x)
+    if (c[s] > 0) off[s] = base + scan[s];
+}
+
+// groups whose UNION list exceeded the slab capacity: compaction flags and their lengths
+__global__ void k_union_overflow(int ng, const int* __restrict__ len, int cap, int* __restrict__ flag) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < ng) flag[g] = len[g] > cap ? 1 : 0;
+}
+__global__ void k_gather_len(int nsel, const int* __restrict__ sel, const int* __restrict__ len,
+                             int64_t* __restrict__ out) {
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w < nsel) out[w] = len[sel[w]];
+}
+__global__ void k_slab_offsets(int ng, int cap, int64_t* __restrict__ off) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < ng) off[g] = (int64_t)g * cap;
 }

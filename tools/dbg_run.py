@@ -33,3 +33,5 @@ except AssertionError as e:
     print("rho rel worst", np.sort(rr)[-5:])
     ea = np.linalg.norm(g["a"][t] - orc["a"], axis=1) / orc["S_a"]
     print("a worst", np.sort(ea)[-5:])
+bad = np.argsort(-np.abs(g["h"][t] - h_or) / h_or)[:5]
+print("worst h:", [(int(t[b]), float(g["h"][t[b]]), float(h_or[b])) for b in bad])
