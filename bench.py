@@ -42,7 +42,7 @@ FLOP_DENS_PAIR, FLOP_DENS_DIR, FLOP_FORCE_PAIR = 27, 25, 74
 # (tools/fp32_peak.cu, profiles/round1/fp32_peak.json).
 FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 
-CONFIG_TUNING = dict(split_count=64, split_fraction=0.0)
+CONFIG_TUNING = dict(split_count=32, split_fraction=0.0)
 
 
 def parse():

@@ -78,7 +78,8 @@ __device__ __forceinline__ float3 dir_unit(int d) { return make_float3(c_dirs[d]
 #define SPH_PI_F 3.14159265358979323846f
 #define SPH_CNORM (8.0f / SPH_PI_F)   // 8/pi of W
 #define SPH_MAX_DEPTH 12              // Morton levels below the top grid
-#define SPH_COLD_MARGIN 1.25f         // h_build / h when h0 is the occupancy guess
+#define SPH_COLD_MARGIN 1.2f          // h_build / h when h0 is the occupancy guess
+#define SPH_REGROW_MARGIN 1.1f        // h_build / h after a Newton step left the list (tuned: tools/sweep.sh)
 #define SPH_IDX_BITS 27               // list entry = (periodic image code << 27) | source index
 #define SPH_IDX_MASK ((1u << SPH_IDX_BITS) - 1u)
 #define SPH_GROUP 32                  // targets per group (one warp, one lane per target)
@@ -116,14 +117,16 @@ struct sph_ctx {
   int n_nodes = 0, n_leaves = 0, n_groups = 0;
   int64_t n_sorted = 0;      // entries of all 13-direction lists
   int64_t pool = 0;          // entries of the interaction (UNION) lists
+  float cold_margin = SPH_COLD_MARGIN, regrow_margin = SPH_REGROW_MARGIN;
   int nb_k = 192;            // capacity of a particle's neighbour list (NB walk)
   int ucap = 768;            // capacity of a group's interaction list slab (UNION walk)
   int64_t ovf_used = 0;      // entries of the neighbour-list overflow pool
+  int64_t n_ovfidx = 0;      // particles that have a list in the pool (k_hsolve_pool)
   int64_t list_rebuilds = 0; // groups re-walked for a particle whose h outgrew its list
   float hb_max = 0.f;        // largest h_build (density reach)
 
   // named device buffers
-  DBuf b[64];
+  DBuf b[80];
   cudaEvent_t ev[12];
   bool ev_ok = false;
 };
@@ -142,12 +145,12 @@ enum BufId {
   // 13-direction sorted lists
   B_SORTED,
   // groups and interaction lists
-  B_GROUPS, B_GOFF, B_GLEN, B_LIST, B_NBR2, B_NBCNT, B_NBOFF, B_NBOVF, B_GFLAG, B_GSEL, B_HRCH,
+  B_GROUPS, B_GOFF, B_GLEN, B_LIST, B_NBR2, B_NBCNT, B_NBOFF, B_NBOVF, B_OVFIDX, B_GFLAG, B_GSEL, B_HRCH,
   // misc scratch
   B_TMPI0, B_TMPI1, B_TMPL0, B_TMPL1, B_COUNTERS, B_OUT0, B_OUT1, B_OUT2, B_OUT3, B_OUT4, B_OUT5,
   B_COUNT
 };
-static_assert(B_COUNT <= 64, "too many buffers");
+static_assert(B_COUNT <= 80, "too many buffers");
 
 // device counters layout (int64 slots in B_COUNTERS)
 enum CounterId {

@@ -419,6 +419,16 @@ static void build_nb(sph_ctx* c, int nsel, const int* sel, int tsel_val) {
   float* pool = B<float>(c, B_NBOVF, base + tot, true);
   c->ovf_used = base + tot;
   LAUNCH(k_ovf_offsets, grid1d(c, n, 256), 256, 0, n, oc, os, base, ooff);
+  {
+    // the pool particles' indices, appended to the list k_hsolve_pool walks
+    int* pf = B<int>(c, B_TMPI0, n);
+    int* ps = B<int>(c, B_TMPI1, n);
+    LAUNCH(k_flag_pos64, grid1d(c, n, 256), 256, 0, oc, n, pf);
+    const int np = scan_excl<int>(c, pf, ps, n);
+    int32_t* idx = B<int32_t>(c, B_OVFIDX, c->n_ovfidx + np, true);
+    LAUNCH(k_compact_append, grid1d(c, n, 256), 256, 0, pf, ps, n, idx + c->n_ovfidx);
+    c->n_ovfidx += np;
+  }
   const int ng = c->n_groups;
   int* flag = B<int>(c, B_GFLAG, ng);
   int* scan = B<int>(c, B_TMPI1, ng);
@@ -670,6 +680,11 @@ int sph_create(const sph_config* cfg, int dev, void* stream, sph_ctx** out) {
     dirs[13][0] = dirs[13][1] = dirs[13][2] = 0.f;
     CUDA_TRY(cudaMemcpyToSymbol(c_dirs, dirs, sizeof(dirs)));
     c->ev_ok = true;
+    // tuning overrides for experiments; defaults otherwise
+    if (const char* e = getenv("SPH_COLD_MARGIN")) c->cold_margin = (float)atof(e);
+    if (const char* e = getenv("SPH_REGROW_MARGIN")) c->regrow_margin = (float)atof(e);
+    if (const char* e = getenv("SPH_NBK")) c->nb_k = atoi(e);
+    if (const char* e = getenv("SPH_UCAP")) c->ucap = atoi(e);
   } catch (const SphError& e) {
     delete c;
     return e.status;
@@ -682,7 +697,7 @@ int sph_destroy(sph_ctx* c) {
   if (!c) return SPH_E_ARG;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
-  for (int i = 0; i < 64; ++i) dev_free(c, c->b[i].p);
+  for (int i = 0; i < 80; ++i) dev_free(c, c->b[i].p);
   if (c->ev_ok)
     for (int i = 0; i < 12; ++i) cudaEventDestroy(c->ev[i]);
   if (c->own_stream) cudaStreamDestroy(c->stream);
@@ -694,7 +709,7 @@ int sph_set_allocator(sph_ctx* c, void* (*alloc)(size_t, void*, void*), void (*r
                       void* user) {
   if (!c) return SPH_E_ARG;
   if ((alloc == nullptr) != (release == nullptr)) return SPH_E_ARG;
-  for (int i = 0; i < 64; ++i)
+  for (int i = 0; i < 80; ++i)
     if (c->b[i].p) return SPH_E_STATE;
   c->ualloc = alloc;
   c->urelease = release;
@@ -753,7 +768,7 @@ int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const floa
   if (need_guess) {
     LAUNCH(k_guess_h, gridfull((int64_t)c->n_nodes * 32, 256), 256, 0, c->n_nodes, nodes(c), level_geom(c),
            c->cfg.n_ngb, (int)c->cfg.n_ngb, h_cap(c), Bget<float4>(c, B_XH));
-    margin = std::max(margin, SPH_COLD_MARGIN);
+    margin = std::max(margin, c->cold_margin);
     if (frac) build_nodes(c, true);     // the paper's split rule needs h
   }
   c->cold = need_guess;
@@ -769,6 +784,7 @@ int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const floa
     CUDA_TRY(cudaMemsetAsync(B<int64_t>(c, B_NBOFF, n), 0xff, n * sizeof(int64_t), c->stream));
     B<float>(c, B_NBOVF, 1);
     c->ovf_used = 0;
+    c->n_ovfidx = 0;
     LAUNCH(k_init_iter, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, c->n_own, Bget<float4>(c, B_XH),
            margin, h_cap(c), Bget<uint8_t>(c, B_STATE), hb, Bget<float>(c, B_HLO), Bget<float>(c, B_HHI));
   }
@@ -837,7 +853,7 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   }
   // a8: the h iteration, per particle on its neighbour list; re-walk particles whose root
   // lies beyond their list, until every particle has converged
-  const float margin = c->cold ? std::max(c->cfg.h_margin, SPH_COLD_MARGIN) : c->cfg.h_margin;
+  const float margin = std::max(c->cfg.h_margin, c->regrow_margin);
   int rounds = 0;
   long long unconv = 0, itmax = 0;
   CUDA_TRY(cudaEventRecord(c->ev[6], c->stream));
@@ -850,6 +866,13 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
              Bget<float>(c, B_HHI), state, Bget<float>(c, B_NBR2), Bget<int>(c, B_NBCNT), c->nb_k,
              Bget<int64_t>(c, B_NBOFF), Bget<float>(c, B_NBOVF), c->cfg.n_ngb,
              c->cfg.n_ngb_tol, margin, h_cap(c), c->cfg.max_h_iter, ctr(c));
+    }
+    if (c->n_ovfidx > 0) {
+      DbgTimer _t(c, "h solve (pool)");
+      LAUNCH(k_hsolve_pool, gridfull((int64_t)c->n_ovfidx * 32, HSOLVE_WARPS * 32), HSOLVE_WARPS * 32, 0,
+             Bget<int32_t>(c, B_OVFIDX), (int)c->n_ovfidx, Bget<float4>(c, B_XH), Bget<float>(c, B_HB),
+             Bget<float>(c, B_HLO), Bget<float>(c, B_HHI), state, Bget<int>(c, B_NBCNT), Bget<int64_t>(c, B_NBOFF),
+             Bget<float>(c, B_NBOVF), c->cfg.n_ngb, c->cfg.n_ngb_tol, margin, h_cap(c), c->cfg.max_h_iter, ctr(c));
     }
     ctr_read(c, hc);
     ++rounds;

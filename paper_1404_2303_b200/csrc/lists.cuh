@@ -93,6 +93,7 @@ struct WalkSmem {
   int rq_code[WALK_RQ];
   int rq_pre[WALK_RQ + 1];  // exclusive prefix of the queued ranges' counts
   float4 s[32];             // staged box survivors: relative position, source reach
+  float4 tgt[32];           // the targets' spheres (relative position, reach), compacted
 };
 
 struct WalkState {
@@ -104,6 +105,8 @@ struct WalkState {
   int cur;                  // UNION: entries emitted so far; NB: this lane's count
   int gz, lane;
   int raw;                  // sources streamed through the filters (diagnostics)
+  int ntg;                  // targets (staged in WalkSmem::tgt)
+  bool spheres;             // refine node tests by the individual targets' spheres
 };
 
 // one chunk of <= 32 candidate sources (one per lane, relative position p, reach hj)
@@ -192,10 +195,9 @@ __device__ __forceinline__ bool node_in_reach(const WalkParams& P, const WalkSta
 // least one target's own sphere (each target broadcast in turn), so a group whose targets'
 // h differ widely does not visit the cells only its bounding box reaches.
 template <int MODE>
-__device__ __forceinline__ bool node_in_spheres(const WalkParams& P, const WalkState& W, int node, int code,
-                                                bool coarse) {
-  unsigned tm = __ballot_sync(FULL_MASK, W.ri >= 0.f);
-  if (!__any_sync(FULL_MASK, coarse)) return false;
+__device__ __forceinline__ bool node_in_spheres(const WalkParams& P, const WalkState& W, const WalkSmem& S, int node,
+                                                int code, bool coarse) {
+  if (!W.spheres || !__any_sync(FULL_MASK, coarse)) return coarse;
   float3 lo = make_float3(0.f, 0.f, 0.f), hi = lo;
   float hmn = 0.f;
   if (coarse) {
@@ -205,15 +207,12 @@ __device__ __forceinline__ bool node_in_spheres(const WalkParams& P, const WalkS
     if (MODE != MODE_NB) hmn = P.N.hmax[node];
   }
   bool hit = false;
-  while (tm) {
-    const int t = __ffs(tm) - 1;
-    tm &= tm - 1;
-    const float tx = __shfl_sync(FULL_MASK, W.xi, t), ty = __shfl_sync(FULL_MASK, W.yi, t),
-                tz = __shfl_sync(FULL_MASK, W.zi, t), tr = __shfl_sync(FULL_MASK, W.ri, t);
-    const float gx = fmaxf(fmaxf(lo.x - tx, tx - hi.x), 0.f);
-    const float gy = fmaxf(fmaxf(lo.y - ty, ty - hi.y), 0.f);
-    const float gz = fmaxf(fmaxf(lo.z - tz, tz - hi.z), 0.f);
-    const float rr = reach_eff(MODE == MODE_NB ? tr : fmaxf(tr, hmn), P.slack);
+  for (int t = 0; t < W.ntg; ++t) {
+    const float4 q = S.tgt[t];
+    const float gx = fmaxf(fmaxf(lo.x - q.x, q.x - hi.x), 0.f);
+    const float gy = fmaxf(fmaxf(lo.y - q.y, q.y - hi.y), 0.f);
+    const float gz = fmaxf(fmaxf(lo.z - q.z, q.z - hi.z), 0.f);
+    const float rr = MODE == MODE_NB ? q.w : fmaxf(q.w, reach_eff(hmn, P.slack));
     hit |= fmaf(gx, gx, fmaf(gy, gy, gz * gz)) < rr * rr;
   }
   return coarse && hit;
@@ -330,7 +329,7 @@ __device__ void dfs_subtree(const WalkParams& P, WalkState& W, WalkSmem& S, int*
         ch = rec.z + lane;
         rc = node_in_reach<MODE>(P, W, ch, code);
       }
-      rc = node_in_spheres<MODE>(P, W, ch, code, rc);
+      rc = node_in_spheres<MODE>(P, W, S, ch, code, rc);
       if (!rc) ch = -1;
       const unsigned ok = __ballot_sync(FULL_MASK, ch >= 0);
       if (ch >= 0) stk[top + __popc(ok & lanemask_lt())] = ch | (code << SPH_IDX_BITS);
@@ -387,6 +386,17 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkParams P) {
   const float ahi[3] = {warp_max_f(tg ? ax : -INFINITY), warp_max_f(tg ? ay : -INFINITY),
                         warp_max_f(tg ? az : -INFINITY)};
   W.R = warp_max_f(tg ? W.ri : 0.f);
+  {
+    // the targets' spheres, compacted, for the node tests; worth it only when the group's
+    // reach is uneven or its targets are spread wider than their reach
+    const unsigned tb = __ballot_sync(FULL_MASK, tg);
+    W.ntg = __popc(tb);
+    if (tg) S.tgt[__popc(tb & lanemask_lt())] = make_float4(W.xi, W.yi, W.zi, reach_eff(W.ri, P.slack));
+    __syncwarp();
+    const float rmin = warp_min_f(tg ? W.ri : INFINITY);
+    const float dx = W.hi.x - W.lo.x, dy = W.hi.y - W.lo.y, dz = W.hi.z - W.lo.z;
+    W.spheres = W.ntg <= 8 || rmin < 0.75f * W.R || fmaf(dx, dx, fmaf(dy, dy, dz * dz)) > 0.25f * W.R * W.R;
+  }
   W.cur = 0;
   W.raw = 0;
   W.base = MODE == MODE_FILL ? P.off[gid] : (MODE == MODE_NB ? (int64_t)grp.y * P.K + lane : 0);
@@ -446,7 +456,7 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkParams P) {
           rec = P.N.rec[nd];
           reach = node_in_reach<MODE>(P, W, nd, code);
         }
-        reach = node_in_spheres<MODE>(P, W, nd, code, reach);
+        reach = node_in_spheres<MODE>(P, W, S, nd, code, reach);
         if (lane < k) {
           leaf = reach && !(rec.z >= 0 && rec.y > WALK_TAKE);
           srt = leaf && P.N.sortoff[nd] >= 0;
@@ -503,6 +513,14 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkParams P) {
     atomicAdd(&P.ctr[C_TMP2], (unsigned long long)W.raw);
     atomicMax(&P.ctr[C_TMP0], (unsigned long long)W.raw);
   }
+#ifdef SPH_WALK_TRACE
+  if (W.raw > 10000) {
+    const int mc = __reduce_max_sync(FULL_MASK, tg ? W.cur : 0);
+    if (lane == 0)
+      printf("heavy walk mode %d group %d: targets %d R %.3g bbox %.3g %.3g %.3g spheres %d raw %d max list %d\n", MODE,
+             gid, W.ntg, W.R, W.hi.x - W.lo.x, W.hi.y - W.lo.y, W.hi.z - W.lo.z, (int)W.spheres, W.raw, mc);
+  }
+#endif
   if (MODE == MODE_NB) {
     if (tg && !P.ovf) P.nb_cnt[s] = W.cur;
   } else if (MODE == MODE_COUNT) {
@@ -555,7 +573,7 @@ __global__ void k_widen_i32(const int* __restrict__ in, int64_t n, int64_t* __re
 // NB overflow: particles whose list exceeded K (count known) get an exactly sized list in the
 // overflow pool; state HS_OVF marks them for the second, contiguous-layout walk
 #define HS_OVF 3
-#define NB_POOL_MAX 4096   // longer lists (h_build far too large) are not recorded: h_build shrinks
+#define NB_POOL_MAX (1 << 20)   // longer lists (h_build absurdly large) are not recorded: h_build shrinks
 __global__ void k_mark_overflow(const int4* __restrict__ groups, int ngroups, const uint8_t* __restrict__ tsel,
                                 int tsel_val, const uint32_t* __restrict__ perm, int64_t n_own,
                                 const int* __restrict__ cnt, int K, uint8_t* __restrict__ state,
@@ -591,4 +609,14 @@ __global__ void k_gather_len(int nsel, const int* __restrict__ sel, const int* _
 __global__ void k_slab_offsets(int ng, int cap, int64_t* __restrict__ off) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g < ng) off[g] = (int64_t)g * cap;
+}
+
+__global__ void k_flag_pos64(const int64_t* __restrict__ c, int64_t n, int* __restrict__ flag) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x)
+    flag[s] = c[s] > 0 ? 1 : 0;
+}
+__global__ void k_compact_append(const int* __restrict__ flag, const int* __restrict__ scan, int64_t n,
+                                 int32_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (flag[i]) out[scan[i]] = (int32_t)i;
 }

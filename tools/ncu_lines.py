@@ -16,7 +16,7 @@ for r in rows:
         func = r[1]; continue
     if r[0] == "Line No":
         continue
-    if func and func.startswith(kern) and r[0].isdigit():
+    if func and kern in func and r[0].isdigit():
         try:
             agg.append((int(r[4]), int(r[7]), fname, int(r[0]), r[1][:100]))
         except ValueError:
