@@ -363,6 +363,19 @@ static void build_groups(sph_ctx* c) {
   LAUNCH(k_group_write, gridfull(nn, 256), 256, 0, nn, N, cscan, groups);
 }
 
+// dynamic shared memory of the walk (WALK_WARPS x WalkSmem > the 48 KB static limit)
+static int walk_smem() {
+  static bool attr = false;
+  const int bytes = WALK_WARPS * (int)sizeof(WalkSmem);
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(k_walk<MODE_NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    CUDA_TRY(cudaFuncSetAttribute(k_walk<MODE_COUNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    CUDA_TRY(cudaFuncSetAttribute(k_walk<MODE_FILL>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    attr = true;
+  }
+  return bytes;
+}
+
 static WalkParams walk_params(sph_ctx* c, const float* reach) {
   WalkParams P;
   memset(&P, 0, sizeof(P));
@@ -399,7 +412,7 @@ static void build_nb(sph_ctx* c, int nsel, const int* sel, int tsel_val) {
   P.K = c->nb_k;
   P.nb_r2 = B<float>(c, B_NBR2, (size_t)n * c->nb_k);
   P.nb_cnt = B<int>(c, B_NBCNT, n);
-  LAUNCH(k_walk<MODE_NB>, gridfull(nsel, WALK_WARPS), WALK_WARPS * 32, 0, P);
+  LAUNCH(k_walk<MODE_NB>, gridfull(nsel, WALK_WARPS), WALK_WARPS * 32, walk_smem(), P);
   if (dbg_on()) {
     unsigned long long h[C_NCOUNTERS];
     ctr_read(c, h);
@@ -446,7 +459,7 @@ static void build_nb(sph_ctx* c, int nsel, const int* sel, int tsel_val) {
   Q.nb_cnt = P.nb_cnt;
   Q.ovf = pool;
   Q.ovf_off = ooff;
-  LAUNCH(k_walk<MODE_NB>, gridfull(no, WALK_WARPS), WALK_WARPS * 32, 0, Q);
+  LAUNCH(k_walk<MODE_NB>, gridfull(no, WALK_WARPS), WALK_WARPS * 32, walk_smem(), Q);
   LAUNCH(k_state_swap, grid1d(c, n, 256), 256, 0, state, n, (uint8_t)HS_OVF,
          (uint8_t)(tsel_val >= 0 ? tsel_val : HS_ACTIVE));
   DBG("neighbour lists: %lld entries of %d groups in the overflow pool\n", (long long)tot, no);
@@ -476,7 +489,7 @@ static void build_union(sph_ctx* c, const float* reach) {
   const int64_t slab = (int64_t)ng * cap;
   P.out = B<uint32_t>(c, B_LIST, slab);
   LAUNCH(k_slab_offsets, gridfull(ng, 256), 256, 0, ng, cap, P.off);
-  LAUNCH(k_walk<MODE_FILL>, gridfull(ng, WALK_WARPS), WALK_WARPS * 32, 0, P);
+  LAUNCH(k_walk<MODE_FILL>, gridfull(ng, WALK_WARPS), WALK_WARPS * 32, walk_smem(), P);
   int* flag = B<int>(c, B_GFLAG, ng);
   int* scan = B<int>(c, B_TMPI1, ng);
   LAUNCH(k_union_overflow, gridfull(ng, 256), 256, 0, ng, P.len, cap, flag);
@@ -496,7 +509,7 @@ static void build_union(sph_ctx* c, const float* reach) {
     P.sel = sel;
     P.ucap = INT32_MAX;
     P.check = 1;
-    LAUNCH(k_walk<MODE_FILL>, gridfull(no, WALK_WARPS), WALK_WARPS * 32, 0, P);
+    LAUNCH(k_walk<MODE_FILL>, gridfull(no, WALK_WARPS), WALK_WARPS * 32, walk_smem(), P);
   }
   c->pool = total;
   if (dbg_on()) {

@@ -91,6 +91,9 @@ struct WalkSmem {
   int stk[WALK_CAP + WALK_DFS];
   int rq_first[WALK_RQ];
   int rq_code[WALK_RQ];
+  float4 rq_so[WALK_RQ];    // per queued range: source pre-shift (x - L for a source near L)
+  float4 rq_oo[WALK_RQ];    //   and the origin it is taken relative to (o, or o - L)
+  float4 shf[27];           // image code -> shift vector
   int rq_pre[WALK_RQ + 1];  // exclusive prefix of the queued ranges' counts
   float4 s[32];             // staged box survivors: relative position, source reach
   float4 tgt[32];           // the targets' spheres (relative position, reach), compacted
@@ -171,19 +174,22 @@ __device__ __forceinline__ void emit_chunk(const WalkParams& P, WalkState& W, Wa
   W.cur += __popc(b2);
 }
 
-__device__ __forceinline__ float3 node_corner_rel(const WalkParams& P, const WalkState& W, int4 c, int code) {
+// node box corner in the group's frame (fp32; the box tests carry an absolute slack)
+__device__ __forceinline__ float3 node_corner_rel(const WalkParams& P, const WalkState& W, const WalkSmem& S, int4 c,
+                                                  int code) {
   const int l = c.w;
-  return make_float3(node_corner(c.x, l, 0, P.g) + shift_of(code % 3, P.g.L[0]) - W.o.x,
-                     node_corner(c.y, l, 1, P.g) + shift_of((code / 3) % 3, P.g.L[1]) - W.o.y,
-                     node_corner(c.z, l, 2, P.g) + shift_of(code / 9, P.g.L[2]) - W.o.z);
+  const float4 sh = S.shf[code];
+  return make_float3(fmaf((float)c.x, P.g.E[l][0], sh.x) - W.o.x, fmaf((float)c.y, P.g.E[l][1], sh.y) - W.o.y,
+                     fmaf((float)c.z, P.g.E[l][2], sh.z) - W.o.z);
 }
 
 // node box within reach of the targets' box
 template <int MODE>
-__device__ __forceinline__ bool node_in_reach(const WalkParams& P, const WalkState& W, int node, int code) {
+__device__ __forceinline__ bool node_in_reach(const WalkParams& P, const WalkState& W, const WalkSmem& S, int node,
+                                              int code) {
   const int4 c = P.N.ijk[node];
   const int l = c.w;
-  const float3 cr = node_corner_rel(P, W, c, code);
+  const float3 cr = node_corner_rel(P, W, S, c, code);
   const float gx = fmaxf(fmaxf(cr.x - W.hi.x, W.lo.x - (cr.x + P.g.E[l][0])), 0.f);
   const float gy = fmaxf(fmaxf(cr.y - W.hi.y, W.lo.y - (cr.y + P.g.E[l][1])), 0.f);
   const float gz = fmaxf(fmaxf(cr.z - W.hi.z, W.lo.z - (cr.z + P.g.E[l][2])), 0.f);
@@ -202,7 +208,7 @@ __device__ __forceinline__ bool node_in_spheres(const WalkParams& P, const WalkS
   float hmn = 0.f;
   if (coarse) {
     const int4 c = P.N.ijk[node];
-    lo = node_corner_rel(P, W, c, code);
+    lo = node_corner_rel(P, W, S, c, code);
     hi = make_float3(lo.x + P.g.E[c.w][0], lo.y + P.g.E[c.w][1], lo.z + P.g.E[c.w][2]);
     if (MODE != MODE_NB) hmn = P.N.hmax[node];
   }
@@ -231,7 +237,7 @@ __device__ __forceinline__ void sweep_node(const WalkParams& P, WalkState& W, Wa
   if (soff >= 0) {
     const int4 c = P.N.ijk[node];
     const int l = c.w;
-    cr = node_corner_rel(P, W, c, code);
+    cr = node_corner_rel(P, W, S, c, code);
     const int ox = cr.x > W.hi.x ? 1 : (cr.x + P.g.E[l][0] < W.lo.x ? -1 : 0);
     const int oy = cr.y > W.hi.y ? 1 : (cr.y + P.g.E[l][1] < W.lo.y ? -1 : 0);
     const int oz = cr.z > W.hi.z ? 1 : (cr.z + P.g.E[l][2] < W.lo.z ? -1 : 0);
@@ -301,7 +307,8 @@ __device__ __forceinline__ void flush_ranges(const WalkParams& P, WalkState& W, 
         if (r + step < nq && S.rq_pre[r + step] <= gi) r += step;
       j = S.rq_first[r] + (gi - S.rq_pre[r]);
       code = S.rq_code[r];
-      p = rel_pos(P.xh[j], code, W.o, W.oL, P.g.L);
+      const float4 q = P.xh[j], so = S.rq_so[r], oo = S.rq_oo[r];
+      p = make_float3((q.x + so.x) - oo.x, (q.y + so.y) - oo.y, (q.z + so.z) - oo.z);
       hj = P.reach[j];
     }
     emit_chunk<MODE>(P, W, S, v, j, p, hj, code);
@@ -327,7 +334,7 @@ __device__ void dfs_subtree(const WalkParams& P, WalkState& W, WalkSmem& S, int*
       bool rc = false;
       if (lane < __popc(rec.w & 0xff)) {
         ch = rec.z + lane;
-        rc = node_in_reach<MODE>(P, W, ch, code);
+        rc = node_in_reach<MODE>(P, W, S, ch, code);
       }
       rc = node_in_spheres<MODE>(P, W, S, ch, code, rc);
       if (!rc) ch = -1;
@@ -347,7 +354,8 @@ __device__ void dfs_subtree(const WalkParams& P, WalkState& W, WalkSmem& S, int*
 // and the queued ranges streamed through the source filters.
 template <int MODE>
 __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkParams P) {
-  __shared__ WalkSmem smem[WALK_WARPS];
+  extern __shared__ __align__(16) unsigned char walk_raw[];   // WALK_WARPS x WalkSmem (dynamic)
+  WalkSmem* smem = reinterpret_cast<WalkSmem*>(walk_raw);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int w = blockIdx.x * WALK_WARPS + wib;
   if (w >= P.nsel) return;
@@ -363,6 +371,9 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkParams P) {
   W.oL = make_float3(o4.x - P.g.L[0], o4.y - P.g.L[1], o4.z - P.g.L[2]);
   W.ri = -1.f;
   W.xi = W.yi = W.zi = 0.f;
+  if (lane < 27)
+    S.shf[lane] = make_float4(shift_of(lane % 3, P.g.L[0]), shift_of((lane / 3) % 3, P.g.L[1]),
+                              shift_of(lane / 9, P.g.L[2]), 0.f);
   float ax = 0.f, ay = 0.f, az = 0.f;      // absolute target position (top-cell range)
   bool tg = false;
   if (lane < grp.z) {
@@ -454,7 +465,7 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkParams P) {
         int4 rec = make_int4(0, 0, -1, 0);
         if (lane < k) {
           rec = P.N.rec[nd];
-          reach = node_in_reach<MODE>(P, W, nd, code);
+          reach = node_in_reach<MODE>(P, W, S, nd, code);
         }
         reach = node_in_spheres<MODE>(P, W, S, nd, code, reach);
         if (lane < k) {
@@ -481,6 +492,9 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkParams P) {
           if (ql) {
             S.rq_first[q] = rec.x;
             S.rq_code[q] = code;
+            const int cx = code % 3, cy = (code / 3) % 3, cz = code / 9;
+            S.rq_so[q] = make_float4(cx == 1 ? -P.g.L[0] : 0.f, cy == 1 ? -P.g.L[1] : 0.f, cz == 1 ? -P.g.L[2] : 0.f, 0.f);
+            S.rq_oo[q] = make_float4(cx == 2 ? W.oL.x : W.o.x, cy == 2 ? W.oL.y : W.o.y, cz == 2 ? W.oL.z : W.o.z, 0.f);
           }
           // prefix of the new counts (one per queuing lane, in lane order)
           int v0 = ql ? rec.y : 0;
