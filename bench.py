@@ -37,6 +37,9 @@ UNIT = "pair-interactions/s"
 # FLOP per unit: density 27 per unordered pair + 25 per directed
 # contribution (first full pass); force 74 per unordered pair.
 FLOP_DENS_PAIR, FLOP_DENS_DIR, FLOP_FORCE_PAIR = 27, 25, 74
+# neighbour finding: one distance test = 3 sub + 1 mul + 2 FMA = 8 FLOP per recorded entry;
+# h iteration: one evaluation of f, f', f'' and the three sums per entry ~ 20 FLOP
+FLOP_TEST, FLOP_HSOLVE = 8, 20
 # FP32 ALU peak derived from the unit counts and clock (B200_PROFILING.md: 148 SMs,
 # clocks.max.sm 1965 MHz; 128 FP32 lanes/SM, FMA = 2 FLOP). Measured: 72.6 TFLOP/s
 # (tools/fp32_peak.cu, profiles/round1/fp32_peak.json).
@@ -266,18 +269,30 @@ def run_sph(args, rank, world, local_rank):
     ms_force = med("ms_force", sfo)
     ms_build = med("ms_build", sd)
 
-    def roof(name, flop, ms):
+    def roof(name, flop, ms, what):
         ach = flop / (ms * 1e-3) / 1e12
         return {"kernel": name, "bound": "alu", "achieved": ach, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": ach / FP32_PEAK_TFLOPS, "traffic": traffic_from_profiles(name),
-                "flop_per_launch": flop, "ms_per_launch": ms,
+                "flop_per_step": flop, "ms_per_step": ms, "work": what,
                 "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (measured FFMA 72.6)"}
 
-    r_force = roof("k_force", flop_force, k_force_ms)
-    r_dens = roof("k_density", flop_dens, k_dens_ms)
-    # dominant kernel per step: all density passes vs the force launch
-    dens_kernels_ms = ms_density  # upper bound of the density kernels' share
-    dominant, secondary = (r_force, r_dens) if k_force_ms >= k_dens_ms else (r_dens, r_force)
+    # per-phase kernel time, CUDA events on the ctx stream around every launch of the phase
+    # (summed over the phase's launches within one step)
+    nb_entries = med("n_nb_entries", sd)
+    kern = {
+        "k_walk (neighbour lists)": roof("k_walk<MODE_NB>", FLOP_TEST * nb_entries, med("ms_kernel_walk_nb", sd),
+                                         f"{FLOP_TEST} FLOP per recorded neighbour entry (r^2 < h_build^2), "
+                                         f"{int(nb_entries)} entries"),
+        "k_force": roof("k_force", flop_force, k_force_ms, f"{FLOP_FORCE_PAIR} FLOP x F"),
+        "k_density": roof("k_density", flop_dens, k_dens_ms, f"{FLOP_DENS_PAIR} FLOP x F + {FLOP_DENS_DIR} x D"),
+        "k_walk (interaction lists)": roof("k_walk<MODE_FILL>", FLOP_TEST * sfo[-1]["n_pair_slots"],
+                                           med("ms_kernel_walk_union", sd),
+                                           f"{FLOP_TEST} FLOP per interaction-list entry"),
+        "k_hsolve": roof("k_hsolve", FLOP_HSOLVE * nb_entries, med("ms_kernel_hsolve", sd),
+                         f"{FLOP_HSOLVE} FLOP per neighbour entry (one Newton/Halley evaluation)"),
+    }
+    order = sorted(kern.values(), key=lambda r: -r["ms_per_step"])
+    dominant, secondary = order[0], order[1:]
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         n_s, one, _ = oracle_sample(args.cpu_budget_s)
@@ -298,7 +313,7 @@ def run_sph(args, rank, world, local_rank):
                    "split_count": CONFIG_TUNING["split_count"], "split_fraction": CONFIG_TUNING["split_fraction"],
                    "n_ngb": 48, "n_ngb_tol": cfg.n_ngb_tol},
         "roofline": dominant,
-        "roofline_secondary": secondary,
+        "roofline_others": secondary,
         "cpu_baseline": cpu,
         "e2e": ({"value": e2e_pairs / (e2e_tmax * 1e-3), "unit": UNIT,
                  "h2d_bytes_per_step": e2e["h2d_bytes_per_step"], "d2h_bytes_per_step": e2e["d2h_bytes_per_step"]}
@@ -308,7 +323,10 @@ def run_sph(args, rank, world, local_rank):
         "breakdown": {"F_pairs": F, "D_directed": D, "ms_build": ms_build, "ms_density": ms_density,
                       "ms_force": ms_force, "ms_kernel_density_full": k_dens_ms, "ms_kernel_force": k_force_ms,
                       "rate_loops_2F_over_tdens_plus_tforce": 2.0 * F / ((ms_density + ms_force) * 1e-3),
-                      "h_iters": sd[-1]["h_iters"], "rebuilds": sd[-1]["n_rebuilds"],
+                      "ms_kernel_walk_nb": med("ms_kernel_walk_nb", sd), "ms_kernel_hsolve": med("ms_kernel_hsolve", sd),
+                      "ms_kernel_walk_union": med("ms_kernel_walk_union", sd), "nb_entries": nb_entries,
+                      "walk_launches": sd[-1]["n_walk_launches"],
+                      "h_iters": sd[-1]["h_iters"], "regrow_groups": sd[-1]["n_rebuilds"],
                       "cand_density_full": sd[-1]["n_candidates_density_full"],
                       "cand_force": sfo[-1]["n_candidates"], "levels": sd[-1]["n_levels"],
                       "cells": sd[-1]["n_cells"]},

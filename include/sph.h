@@ -49,7 +49,7 @@ typedef enum {
                         (box <= 0, gamma <= 1, alpha < 0, n_ngb <= 32/3, tol <= 0,
                         top_edge_factor < 1, split_fraction outside [0,1)) */
   SPH_E_DOMAIN = -2, /* non-finite input; x outside [0,L); m <= 0; u <= 0; h0 < 0;
-                        a smoothing length >= min(L)/3 (fewer than 3 top cells per axis) */
+                        a smoothing length >= min(L)/2 (minimum image) */
   SPH_E_STATE = -3,  /* order violated: density before build_cells, force before density */
   SPH_E_NOCONV = -4, /* h iteration hit max_h_iter; all outputs written from the last iterate */
   SPH_E_CUDA = -5,
@@ -75,12 +75,12 @@ typedef struct {
   int32_t split_count;   /* split a cell only if it holds more particles: 300 */
   float split_fraction;  /* ... and more than this fraction has h < edge/2: 0.875 */
   float top_edge_factor; /* kappa >= 1: top cell edge >= kappa * max h ("larger or equal") */
-  float h_margin;        /* >= 1: cells are built for h_build = h * h_margin so the Newton
-                            iteration can grow h without a rebuild */
-  int32_t sort_min_len;  /* a cell's source list is kept presorted along a pair direction only
-                            if it is longer than this and enough targets sweep it; shorter lists
-                            are swept whole (box filter only). 0 = presort every swept
-                            direction (P:687-698 verbatim) */
+  float h_margin;        /* >= 1: neighbour lists are recorded for h_build = h * h_margin so the
+                            Newton iteration can grow h without a new walk */
+  int32_t sort_min_len;  /* leaves holding more particles than this are presorted along the 13
+                            pair directions and swept with the windowed early exit;
+                            smaller leaves are streamed whole through the box and distance
+                            filters. 0 = presort every leaf */
   uint32_t flags;        /* SPH_F_* */
   int32_t rank, nranks;  /* 0, 1 for a single GPU */
   double slab_lo, slab_hi; /* owned x-range of this rank (multi-GPU) */
@@ -94,16 +94,22 @@ typedef struct {         /* host struct, filled when non-NULL */
   int64_t n_candidates;  /* distance tests of the last density pass and the force pass
                             (SPH_F_COUNT_CANDIDATES) */
   int64_t n_unconverged; /* particles not converged when the density call returned */
-  int64_t n_rebuilds;    /* structure rebuilds triggered by h outgrowing its cells */
-  int32_t h_iters;       /* density passes executed */
+  int64_t n_rebuilds;    /* target groups re-walked because an h outgrew its neighbour list */
+  int32_t h_iters;       /* largest number of Newton/Halley iterations of one particle */
   int32_t n_levels;      /* depth of the cell hierarchy + 1 */
-  int64_t n_cells, n_leaves, n_pair_slots; /* hierarchy size; kept pair entries (directed) */
+  int64_t n_cells, n_leaves, n_pair_slots; /* cells; target groups; interaction-list entries */
   double ms_build, ms_density, ms_force, ms_halo; /* whole calls (CUDA events on the ctx stream) */
   int64_t halo_sent, halo_recv;
   /* kernel-only times (CUDA events bracketing the single launch on the ctx stream) */
-  double ms_kernel_density_full; /* first density pass: every particle active */
+  double ms_kernel_density_full; /* the density-sum kernel at the final h (one launch) */
   double ms_kernel_force;        /* the force kernel */
-  int64_t n_candidates_density_full; /* distance tests of that first full density pass */
+  int64_t n_candidates_density_full; /* distance tests of that density-sum launch */
+  /* per-phase kernel time (CUDA events around each launch, summed over launches) */
+  double ms_kernel_walk_nb;      /* neighbour-list walks (build + re-walks of the h iteration) */
+  double ms_kernel_hsolve;       /* the per-particle h iteration */
+  double ms_kernel_walk_union;   /* interaction-list walks */
+  int64_t n_nb_entries;          /* neighbour-list entries recorded (all walks) */
+  int64_t n_walk_launches;       /* neighbour-list walk launches */
 } sph_stats;
 
 /* Fill *cfg with the paper's defaults for the given box. */
@@ -126,18 +132,22 @@ const char* sph_last_error(const sph_ctx* ctx);
  *    x  [n][3]: positions in [0,L) (copied).
  *    h0 [n] or NULL: initial smoothing lengths (support radius); NULL or
  *       h0[i] == 0 -> library guess from cell occupancy.
- *    Bins particles into the top grid (edge >= kappa*max h), sorts them by
- *    cell key (device radix sort), splits cells recursively (P:510-518 with
- *    split_count / split_fraction), builds the self/pair interaction slots with the
- *    refinement rules of P:519-532, and the 13-direction sorted lists.
- *    Errors: SPH_E_ARG, SPH_E_DOMAIN, SPH_E_CUDA, SPH_E_OOM. */
+ *    Sorts the particles by cell key (top grid with edge >= kappa * max h0, P:471-474,
+ *    Morton octants below; device radix sort), splits cells recursively (P:510-518 with
+ *    split_count / split_fraction), presorts the leaves longer than sort_min_len along the
+ *    13 pair directions, groups the particles into warp-sized target groups and
+ *    records every particle's neighbour list (r^2 < h_build^2, h_build = h0 * margin) by a
+ *    walk of the hierarchy with the sorted sweeps.
+ *    Errors: SPH_E_ARG, SPH_E_DOMAIN (non-finite x, x outside [0,L), h0 < 0 or
+ *    h0 >= min(L)/2), SPH_E_CUDA, SPH_E_OOM. At most 2^27 particles per context. */
 int sph_build_cells(sph_ctx* ctx, int64_t n, const float* x, const float* h0);
 
 /* 2. Density loop (Eq. 2-3) with h_i solved to N_i = n_ngb +- tol by a
- *    bracketed Newton/bisection iteration (R3-R4); re-bins when an h
- *    outgrows the cells it was binned for. Then the "ghost" step:
- *    Omega, P, c, A = P/(Omega rho^2), div/curl v and Balsara f
- *    (P:1303-1310), kept inside ctx for sph_force.
+ *    bracketed Newton/Halley iteration (R3-R4) on each particle's recorded
+ *    neighbour list; particles whose root lies beyond their list are re-walked with a larger
+ *    h_build. Then the sums of Eq. 2 at the final h over the interaction lists (reach
+ *    max(h_i, h_j)) and the "ghost" step: Omega, P, c,
+ *    A = P/(Omega rho^2), div/curl v and Balsara f, kept inside ctx.
  *    v [n][3], m [n] (> 0), u [n] (> 0): copied.
  *    Outputs (caller order): h_out [n], rho_out [n]; optional (NULL to skip)
  *    omega_out [n], n_nbr_out [n] (#{j != i : r_ij < h_i}, R21), div_out [n],

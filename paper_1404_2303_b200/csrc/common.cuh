@@ -125,6 +125,16 @@ struct sph_ctx {
   int64_t list_rebuilds = 0; // groups re-walked for a particle whose h outgrew its list
   float hb_max = 0.f;        // largest h_build (density reach)
 
+  // phase timing: event pairs around kernel launches, resolved when the call syncs
+  struct Timed {
+    cudaEvent_t a, b;
+    int phase;
+  };
+  std::vector<Timed> timed;
+  size_t timed_used = 0;
+  double ms_phase[4] = {0, 0, 0, 0};   // 0 NB walks, 1 h solve, 2 union walks
+  int64_t nb_entries = 0, walk_launches = 0;
+
   // named device buffers
   DBuf b[80];
   cudaEvent_t ev[12];
@@ -145,7 +155,7 @@ enum BufId {
   // 13-direction sorted lists
   B_SORTED,
   // groups and interaction lists
-  B_GROUPS, B_GOFF, B_GLEN, B_LIST, B_NBR2, B_NBCNT, B_NBOFF, B_NBOVF, B_OVFIDX, B_GFLAG, B_GSEL, B_HRCH,
+  B_GROUPS, B_GOFF, B_GLEN, B_LIST, B_NBR2, B_NBCNT, B_NBOFF, B_NBOVF, B_OVFIDX, B_NBENT, B_GFLAG, B_GSEL, B_HRCH,
   // misc scratch
   B_TMPI0, B_TMPI1, B_TMPL0, B_TMPL1, B_COUNTERS, B_OUT0, B_OUT1, B_OUT2, B_OUT3, B_OUT4, B_OUT5,
   B_COUNT

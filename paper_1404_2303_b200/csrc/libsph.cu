@@ -105,6 +105,39 @@ struct DbgTimer {
   }
 };
 
+// =========================================================== phase timing =======
+// events around the launches of a phase; resolved (summed into ms_phase) after a sync
+struct PhaseTimer {
+  sph_ctx* c;
+  size_t k;
+  PhaseTimer(sph_ctx* c_, int phase) : c(c_) {
+    if (c->timed_used == c->timed.size()) {
+      sph_ctx::Timed t;
+      CUDA_TRY(cudaEventCreate(&t.a));
+      CUDA_TRY(cudaEventCreate(&t.b));
+      c->timed.push_back(t);
+    }
+    k = c->timed_used++;
+    c->timed[k].phase = phase;
+    CUDA_TRY(cudaEventRecord(c->timed[k].a, c->stream));
+  }
+  ~PhaseTimer() { cudaEventRecord(c->timed[k].b, c->stream); }
+};
+static void phase_resolve(sph_ctx* c) {
+  for (size_t k = 0; k < c->timed_used; ++k) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->timed[k].a, c->timed[k].b);
+    c->ms_phase[c->timed[k].phase] += ms;
+  }
+  c->timed_used = 0;
+}
+static void phase_reset(sph_ctx* c) {
+  c->timed_used = 0;
+  for (double& v : c->ms_phase) v = 0.0;
+  c->nb_entries = 0;
+  c->walk_launches = 0;
+}
+
 // =========================================================== counters ===========
 static unsigned long long* ctr(sph_ctx* c) { return B<unsigned long long>(c, B_COUNTERS, C_NCOUNTERS); }
 static void ctr_reset(sph_ctx* c) {
@@ -354,6 +387,12 @@ static void build_sorted(sph_ctx* c) {
 
 static void build_groups(sph_ctx* c) {
   const int nn = c->n_nodes;
+  if (getenv("SPH_GROUPS_FIXED")) {
+    c->n_groups = (int)((c->n + SPH_GROUP - 1) / SPH_GROUP);
+    int4* groups = B<int4>(c, B_GROUPS, c->n_groups);
+    LAUNCH(k_group_fixed, gridfull(c->n_groups, 256), 256, 0, c->n, groups);
+    return;
+  }
   int* nchunk = B<int>(c, B_TMPI0, nn);
   int* cscan = B<int>(c, B_TMPI1, nn);
   NodeArrays N = nodes(c);
@@ -410,9 +449,14 @@ static void build_nb(sph_ctx* c, int nsel, const int* sel, int tsel_val) {
     P.tsel_val = (uint8_t)tsel_val;
   }
   P.K = c->nb_k;
+  P.nb_entries = Bget<unsigned long long>(c, B_NBENT);
   P.nb_r2 = B<float>(c, B_NBR2, (size_t)n * c->nb_k);
   P.nb_cnt = B<int>(c, B_NBCNT, n);
-  LAUNCH(k_walk<MODE_NB>, gridfull(nsel, WALK_WARPS), WALK_WARPS * 32, walk_smem(), P);
+  {
+    PhaseTimer _p(c, 0);
+    LAUNCH(k_walk<MODE_NB>, gridfull(nsel, WALK_WARPS), WALK_WARPS * 32, walk_smem(), P);
+  }
+  c->walk_launches++;
   if (dbg_on()) {
     unsigned long long h[C_NCOUNTERS];
     ctr_read(c, h);
@@ -459,7 +503,12 @@ static void build_nb(sph_ctx* c, int nsel, const int* sel, int tsel_val) {
   Q.nb_cnt = P.nb_cnt;
   Q.ovf = pool;
   Q.ovf_off = ooff;
-  LAUNCH(k_walk<MODE_NB>, gridfull(no, WALK_WARPS), WALK_WARPS * 32, walk_smem(), Q);
+  Q.nb_entries = P.nb_entries;
+  {
+    PhaseTimer _p(c, 0);
+    LAUNCH(k_walk<MODE_NB>, gridfull(no, WALK_WARPS), WALK_WARPS * 32, walk_smem(), Q);
+  }
+  c->walk_launches++;
   LAUNCH(k_state_swap, grid1d(c, n, 256), 256, 0, state, n, (uint8_t)HS_OVF,
          (uint8_t)(tsel_val >= 0 ? tsel_val : HS_ACTIVE));
   DBG("neighbour lists: %lld entries of %d groups in the overflow pool\n", (long long)tot, no);
@@ -489,7 +538,10 @@ static void build_union(sph_ctx* c, const float* reach) {
   const int64_t slab = (int64_t)ng * cap;
   P.out = B<uint32_t>(c, B_LIST, slab);
   LAUNCH(k_slab_offsets, gridfull(ng, 256), 256, 0, ng, cap, P.off);
-  LAUNCH(k_walk<MODE_FILL>, gridfull(ng, WALK_WARPS), WALK_WARPS * 32, walk_smem(), P);
+  {
+    PhaseTimer _p(c, 2);
+    LAUNCH(k_walk<MODE_FILL>, gridfull(ng, WALK_WARPS), WALK_WARPS * 32, walk_smem(), P);
+  }
   int* flag = B<int>(c, B_GFLAG, ng);
   int* scan = B<int>(c, B_TMPI1, ng);
   LAUNCH(k_union_overflow, gridfull(ng, 256), 256, 0, ng, P.len, cap, flag);
@@ -509,6 +561,7 @@ static void build_union(sph_ctx* c, const float* reach) {
     P.sel = sel;
     P.ucap = INT32_MAX;
     P.check = 1;
+    PhaseTimer _p(c, 2);
     LAUNCH(k_walk<MODE_FILL>, gridfull(no, WALK_WARPS), WALK_WARPS * 32, walk_smem(), P);
   }
   c->pool = total;
@@ -770,6 +823,8 @@ int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const floa
   c->pool = 0;
   c->list_rebuilds = 0;
   CUDA_TRY(cudaEventRecord(c->ev[0], c->stream));
+  phase_reset(c);
+  CUDA_TRY(cudaMemsetAsync(B<unsigned long long>(c, B_NBENT, 1), 0, sizeof(unsigned long long), c->stream));
   float h0max = 0.f;
   const bool need_guess = load_inputs(c, x, h0, &h0max);
   // a2 + a3: one sort for the whole evaluation
@@ -874,6 +929,7 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
     ctr_reset(c);
     {
       DbgTimer _t(c, "h solve");
+      PhaseTimer _p(c, 1);
       LAUNCH(k_hsolve, gridfull((int64_t)c->n_groups * 32, HSOLVE_WARPS * 32), HSOLVE_WARPS * 32, 0,
              Bget<int4>(c, B_GROUPS), c->n_groups, Bget<float4>(c, B_XH), Bget<float>(c, B_HB), Bget<float>(c, B_HLO),
              Bget<float>(c, B_HHI), state, Bget<float>(c, B_NBR2), Bget<int>(c, B_NBCNT), c->nb_k,
@@ -882,6 +938,7 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
     }
     if (c->n_ovfidx > 0) {
       DbgTimer _t(c, "h solve (pool)");
+      PhaseTimer _p(c, 1);
       LAUNCH(k_hsolve_pool, gridfull((int64_t)c->n_ovfidx * 32, HSOLVE_WARPS * 32), HSOLVE_WARPS * 32, 0,
              Bget<int32_t>(c, B_OVFIDX), (int)c->n_ovfidx, Bget<float4>(c, B_XH), Bget<float>(c, B_HB),
              Bget<float>(c, B_HLO), Bget<float>(c, B_HHI), state, Bget<int>(c, B_NBCNT), Bget<int64_t>(c, B_NBOFF),
@@ -954,9 +1011,20 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
                 "halo too narrow: an owned h = " + std::to_string(as_float(hh[C_HMAXBITS])) +
                     " exceeds cfg.halo_width");
   }
+  phase_resolve(c);
+  {
+    unsigned long long ne = 0;
+    CUDA_TRY(cudaMemcpy(&ne, Bget<unsigned long long>(c, B_NBENT), sizeof(ne), cudaMemcpyDeviceToHost));
+    c->nb_entries = (int64_t)ne;
+  }
   if (st) {
     memset(st, 0, sizeof(*st));
     fill_struct_stats(c, st);
+    st->ms_kernel_walk_nb = c->ms_phase[0];
+    st->ms_kernel_hsolve = c->ms_phase[1];
+    st->ms_kernel_walk_union = c->ms_phase[2];
+    st->n_nb_entries = c->nb_entries;
+    st->n_walk_launches = c->walk_launches;
     st->n_directed = ndir;
     st->n_candidates = cand;
     st->n_candidates_density_full = cand;
@@ -1025,9 +1093,12 @@ int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out, int3
   ctr_read(c, hc);
   SPH_REQUIRE(!(hc[C_ERR] & (1ull << 20)), SPH_E_CUDA, "interaction list count/fill mismatch");
   DBG("force: groups %d cand %llu pairs %llu\n", c->n_groups, hc[C_CAND], hc[C_NFORCE] / 2);
+  c->ms_phase[2] = 0.0;
+  phase_resolve(c);
   if (st) {
     memset(st, 0, sizeof(*st));
     fill_struct_stats(c, st);
+    st->ms_kernel_walk_union = c->ms_phase[2];
     st->n_pairs = (int64_t)(hc[C_NFORCE] / 2);
     st->n_candidates = (int64_t)hc[C_CAND];
     float ms = 0.f;

@@ -82,6 +82,7 @@ struct WalkParams {
   float* nb_r2;             // [n * K]: particle s's entries at group_first*K + e*group_count + lane
   int* nb_cnt;              // [n] sources with r^2 < h_build^2 (may exceed K: overflow)
   int K;
+  unsigned long long* nb_entries;   // NB: running total of recorded entries
   const int64_t* ovf_off;   // NB overflow walk: the particle's list at ovf + ovf_off[s] (contiguous)
   float* ovf;
   unsigned long long* ctr;
@@ -537,6 +538,13 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkParams P) {
 #endif
   if (MODE == MODE_NB) {
     if (tg && !P.ovf) P.nb_cnt[s] = W.cur;
+    if (!P.ovf && P.nb_entries) {
+      const int tot = warp_sum_i(tg ? min(W.cur, P.K) : 0);
+      if (lane == 0 && tot) atomicAdd(P.nb_entries, (unsigned long long)tot);
+    } else if (P.ovf && P.nb_entries) {
+      const int tot = warp_sum_i(tg ? W.cur : 0);
+      if (lane == 0 && tot) atomicAdd(P.nb_entries, (unsigned long long)tot);
+    }
   } else if (MODE == MODE_COUNT) {
     if (lane == 0) {
       P.len[gid] = W.cur;

@@ -55,6 +55,9 @@ class Stats(ctypes.Structure):
         ("ms_force", ctypes.c_double), ("ms_halo", ctypes.c_double), ("halo_sent", ctypes.c_int64),
         ("halo_recv", ctypes.c_int64), ("ms_kernel_density_full", ctypes.c_double),
         ("ms_kernel_force", ctypes.c_double), ("n_candidates_density_full", ctypes.c_int64),
+        ("ms_kernel_walk_nb", ctypes.c_double), ("ms_kernel_hsolve", ctypes.c_double),
+        ("ms_kernel_walk_union", ctypes.c_double), ("n_nb_entries", ctypes.c_int64),
+        ("n_walk_launches", ctypes.c_int64),
     ]
 
     def as_dict(self):

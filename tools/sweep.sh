@@ -1,5 +1,9 @@
 #!/bin/bash
-# C4 timing sweep over tuning env vars: one line per variant (warm, no debug timers)
-run() { local name=$1; shift; env "$@" timeout 300 python tools/prof_run.py C4 4 > gpurun_out/sw_$name.log 2>&1; echo "$name $(python -c "import json;d=json.loads(open('gpurun_out/sw_$name.log').read().strip().splitlines()[-1]);print(round(d['ms_build'],2),round(d['ms_density'],2),round(d['ms_force'],2),round(d['ms_total_events'],2),d['list_rebuild_groups'])")"; }
-for rm in 1.05 1.1 1.15 1.2; do run rm$rm SPH_REGROW_MARGIN=$rm; done
-for cm in 1.1 1.2 1.3; do run cm${cm}_rm1.1 SPH_COLD_MARGIN=$cm SPH_REGROW_MARGIN=1.1; done
+run() { local name=$1; shift; local cfg=$1; shift; env "$@" timeout 300 python tools/prof_run.py C4 4 "$cfg" > gpurun_out/sw_$name.log 2>&1; echo "$name $(python -c "import json;d=json.loads(open('gpurun_out/sw_$name.log').read().strip().splitlines()[-1]);print(round(d['ms_build'],2),round(d['ms_density'],2),round(d['ms_force'],2),round(d['ms_total_events'],2),'kd',round(d['ms_kernel_density_full'],3),'kf',round(d['ms_kernel_force'],3),d['groups'],d['cells'],d['list_dens'])")"; }
+run s32 '{"split_count": 32, "split_fraction": 0.0}'
+run s64_sort32 '{"split_count": 64, "split_fraction": 0.0, "sort_min_len": 32}'
+run s64_nosort '{"split_count": 64, "split_fraction": 0.0, "sort_min_len": 100000}'
+run s128_sort32 '{"split_count": 128, "split_fraction": 0.0, "sort_min_len": 32}'
+run paper '{"split_count": 300, "split_fraction": 0.875}'
+run paper_sort0 '{"split_count": 300, "split_fraction": 0.875, "sort_min_len": 0}'
+run paper_nosort '{"split_count": 300, "split_fraction": 0.875, "sort_min_len": 100000}'
