@@ -36,12 +36,17 @@ __device__ __forceinline__ void spline(float q, float& f, float& fp, float& fpp)
 }
 __device__ __forceinline__ float spline_fp(float q) {
   const float t = 1.f - q;
-  return q <= 0.5f ? q * fmaf(18.f, q, -12.f) : -6.f * t * t;
+  const float a = q * fmaf(18.f, q, -12.f), b = -6.f * t * t;
+  return q <= 0.5f ? a : b;
 }
 
 // ------------------------------------------------------------------ density ------
+#ifndef DENS_WARPS
 #define DENS_WARPS 8
-#define DENS_ST 4          // staged sources per round: 32 * DENS_ST
+#endif
+#ifndef DENS_ST
+#define DENS_ST 1          // staged sources per round: 32 * DENS_ST (tuned, tools/sweep.sh)
+#endif
 
 struct DensOut {
   double* sf;     // sum f            (N_i = (32/3) sum f, Eq. 3)
@@ -92,10 +97,13 @@ __global__ void __launch_bounds__(DENS_WARPS * 32) k_density(GroupLists G, const
   const int len = G.len[gid];
   float4* __restrict__ SP = sp[wib];
   float4* __restrict__ SV = sv[wib];
-  for (int base = 0; base < len; base += 32 * DENS_ST) {
+  // stage s takes entries s, s + nst, s + 2 nst, ...: every stage samples the whole list, so
+  // the lanes' hit counts per stage are balanced (consecutive entries come from one cell)
+  const int nst = (len + 32 * DENS_ST - 1) / (32 * DENS_ST);
+  for (int stg = 0; stg < nst; ++stg) {
 #pragma unroll
     for (int k = 0; k < DENS_ST; ++k) {
-      const int e = base + 32 * k + lane;
+      const int e = stg + (32 * k + lane) * nst;
       float4 a = make_float4(1e30f, 1e30f, 1e30f, 0.f), b = make_float4(0.f, 0.f, 0.f, 0.f);
       if (e < len) {
         const uint32_t ent = G.list[off + e];
@@ -113,8 +121,7 @@ __global__ void __launch_bounds__(DENS_WARPS * 32) k_density(GroupLists G, const
       SV[32 * k + lane] = b;
     }
     __syncwarp();
-    const int nst = min(32 * DENS_ST, len - base);
-    ncand += act ? nst : 0;
+    ncand += act ? min(32 * DENS_ST, (len - stg + nst - 1) / nst) : 0;
     unsigned hm[DENS_ST];
 #pragma unroll
     for (int k = 0; k < DENS_ST; ++k) {
@@ -177,8 +184,12 @@ __global__ void __launch_bounds__(DENS_WARPS * 32) k_density(GroupLists G, const
 }
 
 // ------------------------------------------------------------------ force --------
-#define FORCE_WARPS 8
-#define FORCE_ST 2
+#ifndef FORCE_WARPS
+#define FORCE_WARPS 4
+#endif
+#ifndef FORCE_ST
+#define FORCE_ST 1
+#endif
 
 struct ForceOut {
   float* a;        // [n][3] caller order
@@ -241,10 +252,13 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(GroupLists G, const 
   float4* __restrict__ SB = sb[wib];
   float4* __restrict__ SC = sc[wib];
   int* __restrict__ SJ = sj[wib];
-  for (int base = 0; base < len; base += 32 * FORCE_ST) {
+  // stage s takes entries s, s + nst, s + 2 nst, ...: every stage samples the whole list, so
+  // the lanes' hit counts per stage are balanced (consecutive entries come from one cell)
+  const int nst = (len + 32 * FORCE_ST - 1) / (32 * FORCE_ST);
+  for (int stg = 0; stg < nst; ++stg) {
 #pragma unroll
     for (int k = 0; k < FORCE_ST; ++k) {
-      const int e = base + 32 * k + lane;
+      const int e = stg + (32 * k + lane) * nst;
       float4 a = make_float4(1e30f, 1e30f, 1e30f, 0.f), b = make_float4(0.f, 0.f, 0.f, 0.f), c = b;
       int jj = -1;
       if (e < len) {
@@ -263,8 +277,7 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(GroupLists G, const 
       SJ[32 * k + lane] = jj;
     }
     __syncwarp();
-    const int nst = min(32 * FORCE_ST, len - base);
-    ncand += act ? nst : 0;
+    ncand += act ? min(32 * FORCE_ST, (len - stg + nst - 1) / nst) : 0;
     unsigned hm[FORCE_ST];
 #pragma unroll
     for (int k = 0; k < FORCE_ST; ++k) {
