@@ -476,10 +476,8 @@ __global__ void __launch_bounds__(HSOLVE_WARPS * 32) k_hsolve(const int4* __rest
     u = hi_a[s];
     st = HS_ACTIVE;
     if (cnt > K && oo < 0) {
-      // not recorded (more than NB_POOL_MAX sources within h_build): the count alone says
-      // h_build is far beyond the root; shrink it to hold about K/2 sources, re-walk
-      // (> 2^20 sources within h_build: N(h_build) >> n_ngb, so h_build bounds the root)
-      u = fminf(u, hbs);
+      // not recorded (more than K sources within h_build, first time): the count alone says
+      // h_build is well beyond the root; shrink it to hold about K/2 sources and re-walk
       hbs = hbs * cbrtf(0.5f * (float)K / (float)cnt);
       h = fminf(h, hbs / margin);
       st = HS_REGROW;

@@ -484,7 +484,8 @@ static void build_nb(sph_ctx* c, int nsel, const int* sel, int tsel_val) {
   int64_t* ooff = Bget<int64_t>(c, B_NBOFF);
   uint8_t* state = Bget<uint8_t>(c, B_STATE);
   LAUNCH(k_mark_overflow, gridfull((int64_t)c->n_groups * 32, 256), 256, 0, Bget<int4>(c, B_GROUPS), c->n_groups,
-         state, tsel_val, Bget<uint32_t>(c, B_PERM), c->n_own, P.nb_cnt, c->nb_k, state, oc, ooff);
+         state, tsel_val, Bget<uint32_t>(c, B_PERM), c->n_own, P.nb_cnt, c->nb_k, state, oc, ooff,
+         Bget<uint8_t>(c, B_SHRUNK));
   const int64_t tot = scan_excl<int64_t>(c, oc, os, n);
   if (tot == 0) return;
   const int64_t base = c->ovf_used;
@@ -871,6 +872,7 @@ int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const floa
     B<float>(c, B_HRCH, n);
     B<uint8_t>(c, B_STATE, n);
     CUDA_TRY(cudaMemsetAsync(B<int64_t>(c, B_NBOFF, n), 0xff, n * sizeof(int64_t), c->stream));
+    CUDA_TRY(cudaMemsetAsync(B<uint8_t>(c, B_SHRUNK, n), 0, n, c->stream));
     B<float>(c, B_NBOVF, 1);
     c->ovf_used = 0;
     c->n_ovfidx = 0;

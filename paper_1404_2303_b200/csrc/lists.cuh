@@ -592,14 +592,18 @@ __global__ void k_widen_i32(const int* __restrict__ in, int64_t n, int64_t* __re
     out[i] = in[i];
 }
 
-// NB overflow: particles whose list exceeded K (count known) get an exactly sized list in the
-// overflow pool; state HS_OVF marks them for the second, contiguous-layout walk
+// NB overflow: a particle whose list exceeded K (count known) has its h_build shrunk on the
+// first overflow (k_hsolve re-walks it with a reach holding ~K/2 sources: no second walk of
+// the large region); a particle that overflows again gets an exactly sized list in the
+// overflow pool (state HS_OVF marks it for the second, contiguous-layout walk). The bit
+// `shrunk` remembers the first overflow.
 #define HS_OVF 3
-#define NB_POOL_MAX (1 << 20)   // longer lists (h_build absurdly large) are not recorded: h_build shrinks
+#define NB_POOL_MAX (1 << 24)   // longer lists are never recorded: h_build shrinks
 __global__ void k_mark_overflow(const int4* __restrict__ groups, int ngroups, const uint8_t* __restrict__ tsel,
                                 int tsel_val, const uint32_t* __restrict__ perm, int64_t n_own,
                                 const int* __restrict__ cnt, int K, uint8_t* __restrict__ state,
-                                int64_t* __restrict__ ovf_cnt, int64_t* __restrict__ ovf_off) {
+                                int64_t* __restrict__ ovf_cnt, int64_t* __restrict__ ovf_off,
+                                uint8_t* __restrict__ shrunk) {
   const int lane = threadIdx.x & 31;
   const int gi = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   if (gi >= ngroups) return;
@@ -607,7 +611,9 @@ __global__ void k_mark_overflow(const int4* __restrict__ groups, int ngroups, co
   if (lane >= g.z) return;
   const int s = g.y + lane;
   const bool tg = tsel_val >= 0 ? tsel[s] == (uint8_t)tsel_val : perm[s] < (uint32_t)n_own;
-  const bool o = tg && cnt[s] > K && cnt[s] <= NB_POOL_MAX;
+  const bool over = tg && cnt[s] > K;
+  const bool o = over && shrunk[s] && cnt[s] <= NB_POOL_MAX;
+  if (over && !shrunk[s]) shrunk[s] = 1;
   ovf_cnt[s] = o ? cnt[s] : 0;
   if (o) state[s] = HS_OVF;
   else if (tg) ovf_off[s] = -1;
