@@ -449,24 +449,35 @@ __device__ __forceinline__ int pack_children(const NodeArrays& N, int x, int4* o
   return g;
 }
 
-__global__ void k_group_count(int nnodes, NodeArrays N, int* __restrict__ ng) {
+// With cmax > 0 a group container is the deepest cell holding <= cmax particles (or a leaf
+// holding more): its particles, contiguous in Morton order, are cut into balanced chunks.
+__device__ __forceinline__ bool is_container(const NodeArrays& N, int x, int cmax) {
+  const int cnt = N.count[x];
+  if (cnt <= cmax) return N.parent[x] < 0 || N.count[N.parent[x]] > cmax;
+  return !N.split[x];
+}
+
+__global__ void k_group_count(int nnodes, NodeArrays N, int cmax, int* __restrict__ ng) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= nnodes) return;
   const int cnt = N.count[x];
   int g = 0;
-  if (N.split[x]) g = pack_children<false>(N, x, nullptr);
+  if (cmax > 0) g = is_container(N, x, cmax) ? n_chunks(cnt) : 0;
+  else if (N.split[x]) g = pack_children<false>(N, x, nullptr);
   else if (N.parent[x] < 0 || cnt > SPH_GROUP) g = n_chunks(cnt);
   ng[x] = g;
 }
 
-__global__ void k_group_write(int nnodes, NodeArrays N, const int* __restrict__ scan, int4* __restrict__ groups) {
+__global__ void k_group_write(int nnodes, NodeArrays N, int cmax, const int* __restrict__ scan,
+                              int4* __restrict__ groups) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= nnodes) return;
   const int cnt = N.count[x], first = N.first[x];
   int4* out = groups + scan[x];
-  if (N.split[x]) {
+  if (cmax > 0 ? !is_container(N, x, cmax) : false) return;
+  if (cmax <= 0 && N.split[x]) {
     pack_children<true>(N, x, out);
-  } else if (N.parent[x] < 0 || cnt > SPH_GROUP) {
+  } else if (cmax > 0 || N.parent[x] < 0 || cnt > SPH_GROUP) {
     const int c = n_chunks(cnt);
     for (int i = 0; i < c; ++i) {      // balanced: 40 -> 20 + 20
       const int s0 = (int)((int64_t)cnt * i / c), s1 = (int)((int64_t)cnt * (i + 1) / c);

@@ -120,6 +120,7 @@ struct sph_ctx {
   float cold_margin = SPH_COLD_MARGIN, regrow_margin = SPH_REGROW_MARGIN;
   int nb_k = 192;            // capacity of a particle's neighbour list (NB walk)
   int ucap = 768;            // capacity of a group's interaction list slab (UNION walk)
+  int group_cmax = 512;      // targets: balanced chunks of the deepest cells holding <= 512 (0: sibling packing)
   int64_t ovf_used = 0;      // entries of the neighbour-list overflow pool
   int64_t n_ovfidx = 0;      // particles that have a list in the pool (k_hsolve_pool)
   int64_t list_rebuilds = 0; // groups re-walked for a particle whose h outgrew its list

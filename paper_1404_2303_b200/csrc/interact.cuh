@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(GroupLists G, const 
       const float vdx = fmaf(vx, dx, fmaf(vy, dy, vz * dz));
       const float w = fminf(0.f, vdx * rinv);
       const float cs = ci + qc.z - 3.f * w;
-      const float Pi = -alpha * cs * w / (rhoi + qc.y);
+      const float Pi = __fdividef(-alpha * cs * w, rhoi + qc.y);
       const float V = Pi * (fi + qc.w) * (Gi + Gj);
       const float AGi = At * fpi * rinv;
       const float AGj = qc.x * fpj * rinv;
@@ -465,6 +465,7 @@ __global__ void __launch_bounds__(HSOLVE_WARPS * 32) k_hsolve(const int4* __rest
   float h = 0.f, hbs = 0.f, l = 0.f, u = 0.f;
   uint8_t st = HS_DONE;
   int it = 0;
+  bool fresh = false;
   if (act) {
     cnt = nb_cnt[s];
     oo = ovf_off[s];
@@ -475,6 +476,7 @@ __global__ void __launch_bounds__(HSOLVE_WARPS * 32) k_hsolve(const int4* __rest
     l = lo_a[s];
     u = hi_a[s];
     st = HS_ACTIVE;
+    fresh = true;
     if (cnt > K && oo < 0) {
       // not recorded (more than K sources within h_build, first time): the count alone says
       // h_build is well beyond the root; shrink it to hold about K/2 sources and re-walk
@@ -482,6 +484,13 @@ __global__ void __launch_bounds__(HSOLVE_WARPS * 32) k_hsolve(const int4* __rest
       h = fminf(h, hbs / margin);
       st = HS_REGROW;
     }
+  }
+  // first evaluation of a fresh list: start from the count within h_build, N(h) ~ C (h/h_build)^3
+  // for a locally uniform density (Eq. 3 with the kernel normalised), when that lies inside
+  // the bracket (saves the Newton steps from the cold guess)
+  if (st == HS_ACTIVE && cnt > 0) {
+    const float he = hbs * cbrtf(n_t / (float)cnt);
+    if (he > l && he < u && he <= hbs && fresh) h = he;
   }
   // short lists: one lane per particle
   const bool shortl = st == HS_ACTIVE && cnt <= HSOLVE_LONG;

@@ -74,7 +74,11 @@ static int grid1d(sph_ctx* c, int64_t n, int block) {
 }
 static int gridfull(int64_t n, int block) { return (int)std::max<int64_t>((n + block - 1) / block, 1); }
 
-static void sync(sph_ctx* c) { CUDA_TRY(cudaStreamSynchronize(c->stream)); }
+static int64_t g_syncs = 0;
+static void sync(sph_ctx* c) {
+  ++g_syncs;
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+}
 
 static bool dbg_on() {
   const char* e = getenv("SPH_DEBUG");
@@ -396,10 +400,12 @@ static void build_groups(sph_ctx* c) {
   int* nchunk = B<int>(c, B_TMPI0, nn);
   int* cscan = B<int>(c, B_TMPI1, nn);
   NodeArrays N = nodes(c);
-  LAUNCH(k_group_count, gridfull(nn, 256), 256, 0, nn, N, nchunk);
+  const char* ce = getenv("SPH_GROUP_CMAX");
+  const int cmax = ce ? atoi(ce) : c->group_cmax;
+  LAUNCH(k_group_count, gridfull(nn, 256), 256, 0, nn, N, cmax, nchunk);
   c->n_groups = scan_excl<int>(c, nchunk, cscan, nn);
   int4* groups = B<int4>(c, B_GROUPS, c->n_groups);
-  LAUNCH(k_group_write, gridfull(nn, 256), 256, 0, nn, N, cscan, groups);
+  LAUNCH(k_group_write, gridfull(nn, 256), 256, 0, nn, N, cmax, cscan, groups);
 }
 
 // dynamic shared memory of the walk (WALK_WARPS x WalkSmem > the 48 KB static limit)
@@ -1115,7 +1121,8 @@ int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out, int3
   unsigned long long hc[C_NCOUNTERS];
   ctr_read(c, hc);
   SPH_REQUIRE(!(hc[C_ERR] & (1ull << 20)), SPH_E_CUDA, "interaction list count/fill mismatch");
-  DBG("force: groups %d cand %llu pairs %llu\n", c->n_groups, hc[C_CAND], hc[C_NFORCE] / 2);
+  DBG("force: groups %d cand %llu pairs %llu; host syncs so far %lld, launches %lld\n", c->n_groups, hc[C_CAND],
+      hc[C_NFORCE] / 2, (long long)g_syncs, (long long)c->launches);
   c->ms_phase[2] = 0.0;
   phase_resolve(c);
   if (st) {

@@ -1,7 +1,6 @@
 #!/bin/bash
-run() { local name=$1; shift; env "$@" timeout 300 python tools/prof_run.py C4 4 > gpurun_out/sw_$name.log 2>&1; echo "$name $(python -c "import json;d=json.loads(open('gpurun_out/sw_$name.log').read().strip().splitlines()[-1]);print(round(d['ms_build'],2),round(d['ms_density'],2),round(d['ms_force'],2),round(d['ms_total_events'],2),'kd',round(d['ms_kernel_density_full'],3),'kf',round(d['ms_kernel_force'],3))")"; }
-run base
-run k320 SPH_NBK=320
-run k512 SPH_NBK=512
-run k1024 SPH_NBK=1024
-run k2048 SPH_NBK=2048
+run() { local name=$1; shift; env "$@" timeout 300 python tools/prof_run.py C4 4 > gpurun_out/sw_$name.log 2>&1; echo "$name $(python -c "import json;d=json.loads(open('gpurun_out/sw_$name.log').read().strip().splitlines()[-1]);print(round(d['ms_build'],2),round(d['ms_density'],2),round(d['ms_force'],2),round(d['ms_total_events'],2),'kd',round(d['ms_kernel_density_full'],3),'kf',round(d['ms_kernel_force'],3),d['groups'])")"; }
+run c1024 SPH_GROUP_CMAX=1024
+run c2048 SPH_GROUP_CMAX=2048
+run c8192 SPH_GROUP_CMAX=8192
+run c512 SPH_GROUP_CMAX=512
