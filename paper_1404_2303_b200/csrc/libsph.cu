@@ -844,9 +844,12 @@ int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const floa
   c->state = 0;
   c->force_lists = false;
   if (!getenv("SPH_NBK")) {
-    // neighbour-list slab: up to 1024 entries per particle within a ~24 GB budget (longer
-    // lists go to the exactly sized overflow pool)
-    c->nb_k = (int)std::max<int64_t>(64, std::min<int64_t>(1024, (int64_t)(24e9 / (4.0 * (double)n))));
+    // neighbour-list slab: up to 1024 entries per particle, within 40% of the free device
+    // memory (cold-start lists hold ~90 entries; longer ones shrink or go to the pool)
+    size_t fr = 0, tot = 0;
+    CUDA_TRY(cudaMemGetInfo(&fr, &tot));
+    const size_t have = fr + c->b[B_NBR2].bytes;   // the slab of a previous build is reused
+    c->nb_k = (int)std::max<int64_t>(64, std::min<int64_t>(1024, (int64_t)(0.4 * (double)have / (4.0 * (double)n))));
   }
   c->pool = 0;
   c->list_rebuilds = 0;
