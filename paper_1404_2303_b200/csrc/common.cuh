@@ -59,6 +59,25 @@ __device__ __forceinline__ uint32_t float_ord(float f) {
   return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
 
+// ---------------------------------------------------------------- packed fp32 -
+// sm_100 packed FP32 (FADD2 / FMUL2 / FFMA2): two candidate sources per instruction in the
+// distance tests. The operation order of the scalar r^2 = fma(dx, dx, fma(dy, dy, dz*dz)) is
+// kept, so the packed test and the interaction body agree bit for bit.
+__device__ __forceinline__ unsigned long long f2u(float2 v) { return *reinterpret_cast<unsigned long long*>(&v); }
+__device__ __forceinline__ float2 u2f(unsigned long long v) { return *reinterpret_cast<float2*>(&v); }
+// r^2 of two sources (x, y, z pairs) from one target (xi, yi, zi)
+__device__ __forceinline__ float2 r2_pair(float xi, float yi, float zi, float2 x, float2 y, float2 z) {
+  unsigned long long dx, dy, dz, r;
+  const unsigned long long X = f2u(make_float2(xi, xi)), Y = f2u(make_float2(yi, yi)), Z = f2u(make_float2(zi, zi));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dx) : "l"(X), "l"(f2u(x)));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dy) : "l"(Y), "l"(f2u(y)));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dz) : "l"(Z), "l"(f2u(z)));
+  asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(r) : "l"(dz));
+  asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(r) : "l"(dy));
+  asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(r) : "l"(dx));
+  return u2f(r);
+}
+
 // ---------------------------------------------------------------- geometry ---
 // 27 neighbour offsets o in {-1,0,1}^3, index k = (ox+1)*9 + (oy+1)*3 + (oz+1); k = 13 is
 // the cell itself. The 13 canonical sort directions are the offsets whose first non-zero

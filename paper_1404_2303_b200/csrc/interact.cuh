@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(DENS_WARPS * 32) k_density(GroupLists G, const
                                                              float3 Lbox, DensOut out, unsigned long long* ctr) {
   __shared__ float4 sp[DENS_WARPS][32 * DENS_ST];   // x, y, z (group frame), m
   __shared__ float4 sv[DENS_WARPS][32 * DENS_ST];   // vx, vy, vz, j (int bits)
+  __shared__ __align__(8) float sxyz[DENS_WARPS][3][32 * DENS_ST];   // x, y, z again (SoA, packed tests)
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int gid = blockIdx.x * DENS_WARPS + wib;
   if (gid >= G.ngroups) return;
@@ -119,6 +120,9 @@ __global__ void __launch_bounds__(DENS_WARPS * 32) k_density(GroupLists G, const
       }
       SP[32 * k + lane] = a;
       SV[32 * k + lane] = b;
+      sxyz[wib][0][32 * k + lane] = a.x;
+      sxyz[wib][1][32 * k + lane] = a.y;
+      sxyz[wib][2][32 * k + lane] = a.z;
     }
     __syncwarp();
     ncand += act ? min(32 * DENS_ST, (len - stg + nst - 1) / nst) : 0;
@@ -126,11 +130,13 @@ __global__ void __launch_bounds__(DENS_WARPS * 32) k_density(GroupLists G, const
 #pragma unroll
     for (int k = 0; k < DENS_ST; ++k) {
       unsigned m = 0u;
+      const float2* X2 = reinterpret_cast<const float2*>(sxyz[wib][0] + 32 * k);
+      const float2* Y2 = reinterpret_cast<const float2*>(sxyz[wib][1] + 32 * k);
+      const float2* Z2 = reinterpret_cast<const float2*>(sxyz[wib][2] + 32 * k);
 #pragma unroll 8
-      for (int t = 0; t < 32; ++t) {
-        const float4 q = SP[32 * k + t];
-        const float dx = xi - q.x, dy = yi - q.y, dz = zi - q.z;
-        m |= (unsigned)(fmaf(dx, dx, fmaf(dy, dy, dz * dz)) < hi2) << t;
+      for (int t = 0; t < 16; ++t) {
+        const float2 r2 = r2_pair(xi, yi, zi, X2[t], Y2[t], Z2[t]);
+        m |= ((unsigned)(r2.x < hi2) | ((unsigned)(r2.y < hi2) << 1)) << (2 * t);
       }
       hm[k] = m;
     }
@@ -212,6 +218,7 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(GroupLists G, const 
   __shared__ float4 sb[FORCE_WARPS][32 * FORCE_ST];   // v_j, m_j
   __shared__ float4 sc[FORCE_WARPS][32 * FORCE_ST];   // A~_j, rho_j, c_j, f_j
   __shared__ int sj[FORCE_WARPS][32 * FORCE_ST];
+  __shared__ __align__(8) float sxyzw[FORCE_WARPS][4][32 * FORCE_ST];   // x, y, z, 1/h (SoA, packed tests)
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int gid = blockIdx.x * FORCE_WARPS + wib;
   if (gid >= G.ngroups) return;
@@ -272,6 +279,10 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(GroupLists G, const 
         jj = (int)j;
       }
       SA[32 * k + lane] = a;
+      sxyzw[wib][0][32 * k + lane] = a.x;
+      sxyzw[wib][1][32 * k + lane] = a.y;
+      sxyzw[wib][2][32 * k + lane] = a.z;
+      sxyzw[wib][3][32 * k + lane] = a.w;
       SB[32 * k + lane] = b;
       SC[32 * k + lane] = c;
       SJ[32 * k + lane] = jj;
@@ -282,12 +293,17 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(GroupLists G, const 
 #pragma unroll
     for (int k = 0; k < FORCE_ST; ++k) {
       unsigned m = 0u;
+      const float2* X2 = reinterpret_cast<const float2*>(sxyzw[wib][0] + 32 * k);
+      const float2* Y2 = reinterpret_cast<const float2*>(sxyzw[wib][1] + 32 * k);
+      const float2* Z2 = reinterpret_cast<const float2*>(sxyzw[wib][2] + 32 * k);
+      const float2* W2 = reinterpret_cast<const float2*>(sxyzw[wib][3] + 32 * k);
 #pragma unroll 8
-      for (int t = 0; t < 32; ++t) {
-        const float4 q = SA[32 * k + t];
-        const float dx = xi - q.x, dy = yi - q.y, dz = zi - q.z;
-        const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-        m |= (unsigned)(r2 < hi2 || r2 * (q.w * q.w) < 1.0f) << t;
+      for (int t = 0; t < 16; ++t) {
+        const float2 r2 = r2_pair(xi, yi, zi, X2[t], Y2[t], Z2[t]);
+        const float2 hw = W2[t];
+        const bool a0 = r2.x < hi2 || r2.x * (hw.x * hw.x) < 1.0f;
+        const bool a1 = r2.y < hi2 || r2.y * (hw.y * hw.y) < 1.0f;
+        m |= ((unsigned)a0 | ((unsigned)a1 << 1)) << (2 * t);
       }
       hm[k] = act ? m : 0u;
     }
