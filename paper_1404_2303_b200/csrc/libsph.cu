@@ -454,17 +454,15 @@ static const int* group_order(sph_ctx* c, const float* reach) {
   return (const int*)va;
 }
 
-// NB walk: per target the squared distances r^2 < h_build^2 (lists.cuh, MODE_NB), for the
-// selected groups (sel == null: all) and the targets in state `tsel_val` (owned if < 0).
-// Lists longer than nb_k are recorded again, exactly sized, in the overflow pool.
-static void build_nb(sph_ctx* c, int nsel, const int* sel, int tsel_val) {
+// NB walk over all groups: per target (the owned particles if tsel_val < 0, else those in
+// state tsel_val) the squared distances r^2 < h_build^2 (lists.cuh, MODE_NB). Overflows are
+// marked on the device (k_mark_overflow) and counted in B_OVFCNT; no host round trip.
+static void nb_walk(sph_ctx* c, int tsel_val) {
   DbgTimer _t(c, "neighbour lists");
-  if (nsel == 0) return;
-  if (dbg_on()) ctr_reset(c);
   const int64_t n = c->n;
   WalkParams P = walk_params(c, Bget<float>(c, B_HB));
-  P.nsel = nsel;
-  P.sel = sel ? sel : group_order(c, Bget<float>(c, B_HB));
+  P.nsel = c->n_groups;
+  P.sel = group_order(c, Bget<float>(c, B_HB));
   if (tsel_val >= 0) {
     P.tsel = Bget<uint8_t>(c, B_STATE);
     P.tsel_val = (uint8_t)tsel_val;
@@ -475,23 +473,26 @@ static void build_nb(sph_ctx* c, int nsel, const int* sel, int tsel_val) {
   P.nb_cnt = B<int>(c, B_NBCNT, n);
   {
     PhaseTimer _p(c, 0);
-    LAUNCH(k_walk<MODE_NB>, gridfull(nsel, WALK_WARPS), WALK_WARPS * 32, walk_smem(), P);
+    LAUNCH(k_walk<MODE_NB>, gridfull(P.nsel, WALK_WARPS), WALK_WARPS * 32, walk_smem(), P);
   }
   c->walk_launches++;
-  if (dbg_on()) {
-    unsigned long long h[C_NCOUNTERS];
-    ctr_read(c, h);
-    DBG("NB walk: %d groups, raw sources %llu (%.0f per group, max %llu)\n", nsel, h[C_TMP2],
-        (double)h[C_TMP2] / nsel, h[C_TMP0]);
-  }
-  // overflow: exact counts are known; record those lists contiguously
-  int64_t* oc = B<int64_t>(c, B_TMPL0, n);
+  uint8_t* state = Bget<uint8_t>(c, B_STATE);
+  LAUNCH(k_mark_overflow, gridfull((int64_t)c->n_groups * 32, 256), 256, 0, Bget<int4>(c, B_GROUPS), c->n_groups,
+         state, tsel_val, Bget<uint32_t>(c, B_PERM), c->n_own, P.nb_cnt, c->nb_k, state, B<int64_t>(c, B_OVFC, n),
+         Bget<int64_t>(c, B_NBOFF), Bget<uint8_t>(c, B_SHRUNK), B<unsigned long long>(c, B_OVFCNT, 1));
+  if (tsel_val >= 0)
+    LAUNCH(k_state_swap, grid1d(c, n, 256), 256, 0, state, n, (uint8_t)tsel_val, (uint8_t)HS_ACTIVE);
+}
+
+// Particles in state HS_OVF (a repeat overflow): exactly sized lists in the overflow pool
+// (contiguous per particle), recorded by a second NB walk of their groups.
+static void nb_pool(sph_ctx* c) {
+  DbgTimer _t(c, "neighbour lists (pool)");
+  const int64_t n = c->n;
+  int64_t* oc = Bget<int64_t>(c, B_OVFC);
   int64_t* os = B<int64_t>(c, B_TMPL1, n);
   int64_t* ooff = Bget<int64_t>(c, B_NBOFF);
   uint8_t* state = Bget<uint8_t>(c, B_STATE);
-  LAUNCH(k_mark_overflow, gridfull((int64_t)c->n_groups * 32, 256), 256, 0, Bget<int4>(c, B_GROUPS), c->n_groups,
-         state, tsel_val, Bget<uint32_t>(c, B_PERM), c->n_own, P.nb_cnt, c->nb_k, state, oc, ooff,
-         Bget<uint8_t>(c, B_SHRUNK));
   const int64_t tot = scan_excl<int64_t>(c, oc, os, n);
   if (tot == 0) return;
   const int64_t base = c->ovf_used;
@@ -508,32 +509,23 @@ static void build_nb(sph_ctx* c, int nsel, const int* sel, int tsel_val) {
     LAUNCH(k_compact_append, grid1d(c, n, 256), 256, 0, pf, ps, n, idx + c->n_ovfidx);
     c->n_ovfidx += np;
   }
-  const int ng = c->n_groups;
-  int* flag = B<int>(c, B_GFLAG, ng);
-  int* scan = B<int>(c, B_TMPI1, ng);
-  LAUNCH(k_group_flags, gridfull((int64_t)ng * 32, 256), 256, 0, Bget<int4>(c, B_GROUPS), ng, state, (uint8_t)HS_OVF,
-         flag);
-  const int no = scan_excl<int>(c, flag, scan, ng);
-  int* osel = B<int>(c, B_TMPI0, std::max(no, 1));
-  LAUNCH(k_compact_idx, grid1d(c, ng, 256), 256, 0, flag, scan, (int64_t)ng, osel);
   WalkParams Q = walk_params(c, Bget<float>(c, B_HB));
-  Q.nsel = no;
-  Q.sel = osel;
+  Q.nsel = c->n_groups;
   Q.tsel = state;
   Q.tsel_val = HS_OVF;
   Q.K = c->nb_k;
-  Q.nb_cnt = P.nb_cnt;
+  Q.nb_cnt = Bget<int>(c, B_NBCNT);
   Q.ovf = pool;
   Q.ovf_off = ooff;
-  Q.nb_entries = P.nb_entries;
+  Q.nb_entries = Bget<unsigned long long>(c, B_NBENT);
   {
     PhaseTimer _p(c, 0);
-    LAUNCH(k_walk<MODE_NB>, gridfull(no, WALK_WARPS), WALK_WARPS * 32, walk_smem(), Q);
+    LAUNCH(k_walk<MODE_NB>, gridfull(Q.nsel, WALK_WARPS), WALK_WARPS * 32, walk_smem(), Q);
   }
   c->walk_launches++;
-  LAUNCH(k_state_swap, grid1d(c, n, 256), 256, 0, state, n, (uint8_t)HS_OVF,
-         (uint8_t)(tsel_val >= 0 ? tsel_val : HS_ACTIVE));
-  DBG("neighbour lists: %lld entries of %d groups in the overflow pool\n", (long long)tot, no);
+  LAUNCH(k_state_swap, grid1d(c, n, 256), 256, 0, state, n, (uint8_t)HS_OVF, (uint8_t)HS_ACTIVE);
+  CUDA_TRY(cudaMemsetAsync(oc, 0, n * sizeof(int64_t), c->stream));
+  DBG("neighbour lists: %lld entries in the overflow pool\n", (long long)tot);
 }
 
 // UNION walk: per group the sources within reach max(h_i, h_j) of at least one target, with
@@ -882,6 +874,7 @@ int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const floa
     B<uint8_t>(c, B_STATE, n);
     CUDA_TRY(cudaMemsetAsync(B<int64_t>(c, B_NBOFF, n), 0xff, n * sizeof(int64_t), c->stream));
     CUDA_TRY(cudaMemsetAsync(B<uint8_t>(c, B_SHRUNK, n), 0, n, c->stream));
+    CUDA_TRY(cudaMemsetAsync(B<int64_t>(c, B_OVFC, n), 0, n * sizeof(int64_t), c->stream));
     B<float>(c, B_NBOVF, 1);
     c->ovf_used = 0;
     c->n_ovfidx = 0;
@@ -889,7 +882,8 @@ int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const floa
            margin, h_cap(c), Bget<uint8_t>(c, B_STATE), hb, Bget<float>(c, B_HLO), Bget<float>(c, B_HHI));
   }
   // neighbour lists of the h iteration: r^2 < h_build^2 per particle
-  build_nb(c, c->n_groups, nullptr, -1);
+  CUDA_TRY(cudaMemsetAsync(B<unsigned long long>(c, B_OVFCNT, 1), 0, sizeof(unsigned long long), c->stream));
+  nb_walk(c, -1);
   c->state = 1;
   CUDA_TRY(cudaEventRecord(c->ev[1], c->stream));
   sync(c);
@@ -906,23 +900,6 @@ static void fill_struct_stats(sph_ctx* c, sph_stats* st) {
   st->n_leaves = c->n_groups;
   st->n_pair_slots = c->pool;
   st->n_rebuilds = c->list_rebuilds;
-}
-
-// groups with a particle in state HS_REGROW: re-record those particles' neighbour lists
-static void regrow_lists(sph_ctx* c) {
-  const int ng = c->n_groups;
-  int* flag = B<int>(c, B_GFLAG, ng);
-  int* scan = B<int>(c, B_TMPI1, ng);
-  LAUNCH(k_group_flags, gridfull((int64_t)ng * 32, 256), 256, 0, Bget<int4>(c, B_GROUPS), ng,
-         Bget<uint8_t>(c, B_STATE), (uint8_t)HS_REGROW, flag);
-  const int nsel = scan_excl<int>(c, flag, scan, ng);
-  int* sel = B<int>(c, B_GSEL, std::max(nsel, 1));
-  LAUNCH(k_compact_idx, grid1d(c, ng, 256), 256, 0, flag, scan, (int64_t)ng, sel);
-  build_nb(c, nsel, sel, HS_REGROW);
-  LAUNCH(k_state_swap, grid1d(c, c->n, 256), 256, 0, Bget<uint8_t>(c, B_STATE), c->n, (uint8_t)HS_REGROW,
-         (uint8_t)HS_ACTIVE);
-  c->list_rebuilds += nsel;
-  DBG("regrow: %d groups re-walked\n", nsel);
 }
 
 int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, float* h_out, float* rho_out,
@@ -976,18 +953,30 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
              Bget<float>(c, B_HLO), Bget<float>(c, B_HHI), state, Bget<int>(c, B_NBCNT), Bget<int64_t>(c, B_NBOFF),
              Bget<float>(c, B_NBOVF), c->cfg.n_ngb, c->cfg.n_ngb_tol, margin, h_cap(c), c->cfg.max_h_iter, ctr(c));
     }
+    // one host round trip per round: the solve's counters and the overflows of the last walk
+    unsigned long long novf = 0;
+    CUDA_TRY(cudaMemcpyAsync(&novf, Bget<unsigned long long>(c, B_OVFCNT), sizeof(novf), cudaMemcpyDeviceToHost,
+                             c->stream));
     ctr_read(c, hc);
     ++rounds;
     unconv = (long long)hc[C_UNCONV];
     itmax = std::max(itmax, (long long)hc[C_TMP1]);
-    DBG("h solve round %d: unconverged %llu, regrow %llu, max iterations %llu\n", rounds, hc[C_UNCONV],
-        hc[C_REGROW], hc[C_TMP1]);
-    if (hc[C_REGROW] == 0) break;
+    DBG("h solve round %d: unconverged %llu, regrow %llu, pool %llu, max iterations %llu\n", rounds, hc[C_UNCONV],
+        hc[C_REGROW], novf, hc[C_TMP1]);
+    if (hc[C_REGROW] == 0 && novf == 0) break;
     if (rounds >= c->cfg.max_h_iter) {
-      unconv += (long long)hc[C_REGROW];
+      unconv += (long long)(hc[C_REGROW] + novf);
       break;
     }
-    regrow_lists(c);
+    if (novf > 0) {
+      // repeat overflows of the last walk: record them in the pool, solve them next round
+      CUDA_TRY(cudaMemsetAsync(Bget<unsigned long long>(c, B_OVFCNT), 0, sizeof(unsigned long long), c->stream));
+      nb_pool(c);
+    }
+    if (hc[C_REGROW] > 0) {
+      nb_walk(c, HS_REGROW);
+      c->list_rebuilds += (int64_t)hc[C_REGROW];
+    }
   }
   CUDA_TRY(cudaEventRecord(c->ev[7], c->stream));
   // a7: the density loop at the final h over the interaction lists (reach max(h_i, h_j)

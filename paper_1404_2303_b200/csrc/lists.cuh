@@ -603,7 +603,7 @@ __global__ void k_mark_overflow(const int4* __restrict__ groups, int ngroups, co
                                 int tsel_val, const uint32_t* __restrict__ perm, int64_t n_own,
                                 const int* __restrict__ cnt, int K, uint8_t* __restrict__ state,
                                 int64_t* __restrict__ ovf_cnt, int64_t* __restrict__ ovf_off,
-                                uint8_t* __restrict__ shrunk) {
+                                uint8_t* __restrict__ shrunk, unsigned long long* __restrict__ novf) {
   const int lane = threadIdx.x & 31;
   const int gi = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   if (gi >= ngroups) return;
@@ -614,9 +614,13 @@ __global__ void k_mark_overflow(const int4* __restrict__ groups, int ngroups, co
   const bool over = tg && cnt[s] > K;
   const bool o = over && shrunk[s] && cnt[s] <= NB_POOL_MAX;
   if (over && !shrunk[s]) shrunk[s] = 1;
-  ovf_cnt[s] = o ? cnt[s] : 0;
-  if (o) state[s] = HS_OVF;
-  else if (tg) ovf_off[s] = -1;
+  if (tg) ovf_cnt[s] = o ? cnt[s] : 0;
+  if (o) {
+    state[s] = HS_OVF;
+    atomicAdd(novf, 1ull);
+  } else if (tg) {
+    ovf_off[s] = -1;
+  }
 }
 __global__ void k_ovf_offsets(int64_t n, const int64_t* __restrict__ c, const int64_t* __restrict__ scan,
                               int64_t base, int64_t* __restrict__ off) {
