@@ -390,6 +390,10 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkParams P) {
       W.ri = P.reach[s];
     }
   }
+  if (!__any_sync(FULL_MASK, tg)) {            // no target in this group (e.g. a re-walk round)
+    if (MODE != MODE_NB && lane == 0 && !P.check) P.len[gid] = 0;
+    return;
+  }
   W.lo = make_float3(warp_min_f(tg ? W.xi : INFINITY), warp_min_f(tg ? W.yi : INFINITY),
                      warp_min_f(tg ? W.zi : INFINITY));
   W.hi = make_float3(warp_max_f(tg ? W.xi : -INFINITY), warp_max_f(tg ? W.yi : -INFINITY),
