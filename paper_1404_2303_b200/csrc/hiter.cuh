@@ -1,0 +1,190 @@
+// hiter.cuh — the kernel function and the Newton/Halley step of the h iteration (Eq. 3,
+// P:176-185), shared by the fused walk + solve (lists.cuh) and the stand-alone solve
+// kernels (interact.cuh).
+#pragma once
+#include "common.cuh"
+
+// per-particle states of the h iteration
+#define HS_DONE 0
+#define HS_ACTIVE 1
+#define HS_REGROW 2   // needs a neighbour list for a new h_build (grown, or shrunk after overflow)
+
+#define HS_OVF 3   // repeat overflow: needs an exactly sized list in the overflow pool
+#define HSOLVE_LONG 96   // lists longer than this are solved by the whole warp
+
+// counters of a solve (device, read once per round): unconverged, re-walks, pool, max iterations
+#define HC_UNCONV 0
+#define HC_REGROW 1
+#define HC_OVF 2
+#define HC_ITMAX 3
+
+// ------------------------------------------------------------------ kernel ------
+// f(q) of the cubic spline (W = (8/pi) h^-3 f), its first and second derivative
+__device__ __forceinline__ void spline(float q, float& f, float& fp, float& fpp) {
+  const float t = 1.f - q;
+  const bool in = q <= 0.5f;
+  f = in ? fmaf(q * q, fmaf(6.f, q, -6.f), 1.f) : 2.f * t * t * t;
+  fp = in ? q * fmaf(18.f, q, -12.f) : -6.f * t * t;
+  fpp = in ? fmaf(36.f, q, -12.f) : 12.f * t;
+}
+__device__ __forceinline__ float spline_fp(float q) {
+  const float t = 1.f - q;
+  const float a = q * fmaf(18.f, q, -12.f), b = -6.f * t * t;
+  return q <= 0.5f ? a : b;
+}
+
+// one iteration's sums over a list: S0 = sum f (fp64), S1 = sum q f', S2 = sum q^2 f''.
+// Branch-free so the loads overlap: q is clamped to 1, where f = f' = f'' = 0 exactly.
+__device__ __forceinline__ void nsums(const float* __restrict__ r2l, int64_t stride, int e0, int e1, int estep,
+                                      float hinv, double& S0, float& S1, float& S2) {
+  int e = e0;
+  for (; e + 3 * estep < e1; e += 4 * estep) {
+    float r2[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) r2[k] = __ldg(r2l + (int64_t)(e + k * estep) * stride);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float q = fminf(r2[k] * rsqrtf(fmaxf(r2[k], 1e-37f)) * hinv, 1.f);
+      float f, fp, fpp;
+      spline(q, f, fp, fpp);
+      S0 += (double)f;
+      S1 = fmaf(q, fp, S1);
+      S2 = fmaf(q * q, fpp, S2);
+    }
+  }
+  for (; e < e1; e += estep) {
+    const float r2 = __ldg(r2l + (int64_t)e * stride);
+    const float q = fminf(r2 * rsqrtf(fmaxf(r2, 1e-37f)) * hinv, 1.f);
+    float f, fp, fpp;
+    spline(q, f, fp, fpp);
+    S0 += (double)f;
+    S1 = fmaf(q, fp, S1);
+    S2 = fmaf(q * q, fpp, S2);
+  }
+}
+
+// One Newton/Halley update from the sums at h. Returns the new state: HS_DONE (converged),
+// HS_ACTIVE (h updated, iterate), HS_REGROW (the new h lies beyond h_build).
+__device__ __forceinline__ uint8_t hstep(double S0, float S1, float S2, float& h, float& hbs, float& l, float& u,
+                                         float n_t, float tol, float margin, float hcap) {
+  const double Nd = (32.0 / 3.0) * S0;
+  const float N = (float)Nd;
+  const float res = (float)(Nd - (double)n_t);
+  if (fabsf(res) <= tol) return HS_DONE;
+  if (res < 0.f) l = h;
+  else u = h;
+  if (u - l <= 4.f * (h * 1.1920929e-7f)) return HS_DONE;   // bracket at fp32 resolution
+  // g' = h N'/N = -(32/3) S1 / N;  g'' = g' + (32/3)(2 S1 + S2)/N - g'^2
+  const float g = __logf(N / n_t);
+  const float g1 = -(32.f / 3.f) * S1 / N;
+  const float g2 = g1 + (32.f / 3.f) * (2.f * S1 + S2) / N - g1 * g1;
+  float dx;
+  if (g1 > 0.25f) {
+    dx = -g / g1;                                     // log-space Newton
+    const float den = 2.f * g1 * g1 - g * g2;          // Halley (cubic convergence)
+    if (den > 0.5f * g1 * g1) {
+      const float dh = -2.f * g * g1 / den;
+      if (fabsf(dh) <= 2.f * fabsf(dx)) dx = dh;
+    }
+  } else {
+    dx = (res < 0.f) ? 0.6931472f : -0.6931472f;      // (almost) no neighbour: double / halve
+  }
+  float hn = h * __expf(dx);
+  hn = fminf(fmaxf(hn, 0.5f * h), 2.f * h);
+  if (!(hn > l && hn < u)) hn = 0.5f * (l + fminf(u, 2.f * h));
+  hn = fminf(hn, hcap);
+  h = hn;
+  if (hn > hbs) {                                     // the root lies beyond the list
+    hbs = fminf(fminf(hn * margin, fmaxf(u, hn)), hcap);
+    return HS_REGROW;
+  }
+  return HS_ACTIVE;
+}
+
+
+// One solve of the h iteration for the lanes of a warp (warp-collective): each active lane
+// iterates on its own list (r2l, stride, cnt); lists longer than HSOLVE_LONG are summed by
+// the whole warp, one particle at a time. A list holding more than K sources that is not
+// in the pool was not recorded: h_build shrinks to hold ~K/2 sources and the particle is
+// re-walked. fresh: the list was just recorded for this h_build (count-based start).
+struct HLane {
+  float h, hbs, l, u;
+  uint8_t st;
+  int it;
+};
+
+__device__ __forceinline__ void warp_hsolve(bool act, const float* r2l, int64_t stride, int cnt, int K, bool pooled,
+                                            bool fresh, HLane& H, float n_t, float tol, float margin, float hcap,
+                                            int max_iter) {
+  const int lane = threadIdx.x & 31;
+  H.it = 0;
+  if (act) {
+    H.st = HS_ACTIVE;
+    if (cnt > K && !pooled) {
+      H.hbs = H.hbs * cbrtf(0.5f * (float)K / (float)cnt);
+      H.h = fminf(H.h, H.hbs / margin);
+      H.st = HS_REGROW;
+    } else if (fresh && cnt > 0) {
+      // start from the count within h_build: N(h) ~ C (h / h_build)^3 (locally uniform)
+      const float he = H.hbs * cbrtf(n_t / (float)cnt);
+      if (he > H.l && he < H.u && he <= H.hbs) H.h = he;
+    }
+  }
+  const bool shortl = act && H.st == HS_ACTIVE && cnt <= HSOLVE_LONG;
+  if (shortl) {
+    for (; H.it < max_iter && H.st == HS_ACTIVE; ++H.it) {
+      double S0 = 0.0;
+      float S1 = 0.f, S2 = 0.f;
+      nsums(r2l, stride, 0, cnt, 1, 1.0f / H.h, S0, S1, S2);
+      H.st = hstep(S0, S1, S2, H.h, H.hbs, H.l, H.u, n_t, tol, margin, hcap);
+      if (H.st == HS_REGROW) ++H.it;
+    }
+  }
+  unsigned lm = __ballot_sync(FULL_MASK, act && H.st == HS_ACTIVE && cnt > HSOLVE_LONG);
+  while (lm) {
+    const int t = __ffs(lm) - 1;
+    lm &= lm - 1;
+    const int tc = __shfl_sync(FULL_MASK, cnt, t);
+    const int64_t tstr = __shfl_sync(FULL_MASK, stride, t);
+    const float* tl = (const float*)__shfl_sync(FULL_MASK, (unsigned long long)r2l, t);
+    float th = __shfl_sync(FULL_MASK, H.h, t), thb = __shfl_sync(FULL_MASK, H.hbs, t);
+    float tlo = __shfl_sync(FULL_MASK, H.l, t), tu = __shfl_sync(FULL_MASK, H.u, t);
+    uint8_t tst = HS_ACTIVE;
+    int tit = 0;
+    for (; tit < max_iter && tst == HS_ACTIVE; ++tit) {
+      double S0 = 0.0;
+      float S1 = 0.f, S2 = 0.f;
+      nsums(tl, tstr, lane, tc, 32, 1.0f / th, S0, S1, S2);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        S0 += __shfl_xor_sync(FULL_MASK, S0, o);
+        S1 += __shfl_xor_sync(FULL_MASK, S1, o);
+        S2 += __shfl_xor_sync(FULL_MASK, S2, o);
+      }
+      tst = hstep(S0, S1, S2, th, thb, tlo, tu, n_t, tol, margin, hcap);
+      if (tst == HS_REGROW) ++tit;
+    }
+    if (lane == t) {
+      H.h = th;
+      H.hbs = thb;
+      H.l = tlo;
+      H.u = tu;
+      H.st = tst;
+      H.it = tit;
+    }
+  }
+}
+
+// warp totals of a solve into the round's counters
+__device__ __forceinline__ void hsolve_count(bool act, const HLane& H, unsigned long long* hc) {
+  const unsigned regrow = __ballot_sync(FULL_MASK, act && H.st == HS_REGROW);
+  const unsigned unconv = __ballot_sync(FULL_MASK, act && H.st == HS_ACTIVE);
+  const unsigned ovf = __ballot_sync(FULL_MASK, act && H.st == HS_OVF);
+  const unsigned itmax = __reduce_max_sync(FULL_MASK, act ? (unsigned)H.it : 0u);
+  if ((threadIdx.x & 31) == 0) {
+    if (regrow) atomicAdd(&hc[HC_REGROW], (unsigned long long)__popc(regrow));
+    if (unconv) atomicAdd(&hc[HC_UNCONV], (unsigned long long)__popc(unconv));
+    if (ovf) atomicAdd(&hc[HC_OVF], (unsigned long long)__popc(ovf));
+    if (itmax) atomicMax(&hc[HC_ITMAX], (unsigned long long)itmax);
+  }
+}

@@ -25,21 +25,6 @@ struct GroupLists {
   int ngroups;
 };
 
-// ------------------------------------------------------------------ kernel ------
-// f(q) of the cubic spline (W = (8/pi) h^-3 f), its first and second derivative
-__device__ __forceinline__ void spline(float q, float& f, float& fp, float& fpp) {
-  const float t = 1.f - q;
-  const bool in = q <= 0.5f;
-  f = in ? fmaf(q * q, fmaf(6.f, q, -6.f), 1.f) : 2.f * t * t * t;
-  fp = in ? q * fmaf(18.f, q, -12.f) : -6.f * t * t;
-  fpp = in ? fmaf(36.f, q, -12.f) : 12.f * t;
-}
-__device__ __forceinline__ float spline_fp(float q) {
-  const float t = 1.f - q;
-  const float a = q * fmaf(18.f, q, -12.f), b = -6.f * t * t;
-  return q <= 0.5f ? a : b;
-}
-
 // ------------------------------------------------------------------ density ------
 #ifndef DENS_WARPS
 #define DENS_WARPS 8
@@ -386,75 +371,6 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(GroupLists G, const 
 // state HS_REGROW: the walk re-records this particle's list before the next round. A list
 // longer than K lives in the overflow pool (contiguous, exactly sized; lists.cuh).
 #define HSOLVE_WARPS 8
-#define HSOLVE_LONG 96   // lists longer than this are solved by the whole warp
-
-// one iteration's sums over a list: S0 = sum f (fp64), S1 = sum q f', S2 = sum q^2 f''.
-// Branch-free so the loads overlap: q is clamped to 1, where f = f' = f'' = 0 exactly.
-__device__ __forceinline__ void nsums(const float* __restrict__ r2l, int64_t stride, int e0, int e1, int estep,
-                                      float hinv, double& S0, float& S1, float& S2) {
-  int e = e0;
-  for (; e + 3 * estep < e1; e += 4 * estep) {
-    float r2[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) r2[k] = __ldg(r2l + (int64_t)(e + k * estep) * stride);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float q = fminf(r2[k] * rsqrtf(fmaxf(r2[k], 1e-37f)) * hinv, 1.f);
-      float f, fp, fpp;
-      spline(q, f, fp, fpp);
-      S0 += (double)f;
-      S1 = fmaf(q, fp, S1);
-      S2 = fmaf(q * q, fpp, S2);
-    }
-  }
-  for (; e < e1; e += estep) {
-    const float r2 = __ldg(r2l + (int64_t)e * stride);
-    const float q = fminf(r2 * rsqrtf(fmaxf(r2, 1e-37f)) * hinv, 1.f);
-    float f, fp, fpp;
-    spline(q, f, fp, fpp);
-    S0 += (double)f;
-    S1 = fmaf(q, fp, S1);
-    S2 = fmaf(q * q, fpp, S2);
-  }
-}
-
-// One Newton/Halley update from the sums at h. Returns the new state: HS_DONE (converged),
-// HS_ACTIVE (h updated, iterate), HS_REGROW (the new h lies beyond h_build).
-__device__ __forceinline__ uint8_t hstep(double S0, float S1, float S2, float& h, float& hbs, float& l, float& u,
-                                         float n_t, float tol, float margin, float hcap) {
-  const double Nd = (32.0 / 3.0) * S0;
-  const float N = (float)Nd;
-  const float res = (float)(Nd - (double)n_t);
-  if (fabsf(res) <= tol) return HS_DONE;
-  if (res < 0.f) l = h;
-  else u = h;
-  if (u - l <= 4.f * (h * 1.1920929e-7f)) return HS_DONE;   // bracket at fp32 resolution
-  // g' = h N'/N = -(32/3) S1 / N;  g'' = g' + (32/3)(2 S1 + S2)/N - g'^2
-  const float g = __logf(N / n_t);
-  const float g1 = -(32.f / 3.f) * S1 / N;
-  const float g2 = g1 + (32.f / 3.f) * (2.f * S1 + S2) / N - g1 * g1;
-  float dx;
-  if (g1 > 0.25f) {
-    dx = -g / g1;                                     // log-space Newton
-    const float den = 2.f * g1 * g1 - g * g2;          // Halley (cubic convergence)
-    if (den > 0.5f * g1 * g1) {
-      const float dh = -2.f * g * g1 / den;
-      if (fabsf(dh) <= 2.f * fabsf(dx)) dx = dh;
-    }
-  } else {
-    dx = (res < 0.f) ? 0.6931472f : -0.6931472f;      // (almost) no neighbour: double / halve
-  }
-  float hn = h * __expf(dx);
-  hn = fminf(fmaxf(hn, 0.5f * h), 2.f * h);
-  if (!(hn > l && hn < u)) hn = 0.5f * (l + fminf(u, 2.f * h));
-  hn = fminf(hn, hcap);
-  h = hn;
-  if (hn > hbs) {                                     // the root lies beyond the list
-    hbs = fminf(fminf(hn * margin, fmaxf(u, hn)), hcap);
-    return HS_REGROW;
-  }
-  return HS_ACTIVE;
-}
 
 __global__ void __launch_bounds__(HSOLVE_WARPS * 32) k_hsolve(const int4* __restrict__ groups, int ngroups,
                                                               float4* __restrict__ xh, float* __restrict__ hb,
@@ -465,7 +381,7 @@ __global__ void __launch_bounds__(HSOLVE_WARPS * 32) k_hsolve(const int4* __rest
                                                               const int64_t* __restrict__ ovf_off,
                                                               const float* __restrict__ ovf, float n_t,
                                                               float tol, float margin, float hcap, int max_iter,
-                                                              unsigned long long* ctr) {
+                                                              unsigned long long* hc) {
   const int lane = threadIdx.x & 31;
   const int gid = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   if (gid >= ngroups) return;
@@ -474,100 +390,27 @@ __global__ void __launch_bounds__(HSOLVE_WARPS * 32) k_hsolve(const int4* __rest
   // particles with a list in the overflow pool are solved by k_hsolve_pool
   const bool act = lane < grp.z && state[s] == HS_ACTIVE && ovf_off[s] < 0;
   if (!__any_sync(FULL_MASK, act)) return;
+  HLane H;
+  H.h = H.hbs = H.l = H.u = 0.f;
+  H.st = HS_DONE;
   int cnt = 0;
-  int64_t oo = -1;
-  const float* r2l = nullptr;
-  int64_t stride = 1;
-  float h = 0.f, hbs = 0.f, l = 0.f, u = 0.f;
-  uint8_t st = HS_DONE;
-  int it = 0;
-  bool fresh = false;
   if (act) {
     cnt = nb_cnt[s];
-    oo = ovf_off[s];
-    r2l = oo >= 0 ? ovf + oo : nb_r2 + (int64_t)grp.y * K + lane;
-    stride = oo >= 0 ? 1 : grp.z;
-    h = xh[s].w;
-    hbs = hb[s];
-    l = lo_a[s];
-    u = hi_a[s];
-    st = HS_ACTIVE;
-    fresh = true;
-    if (cnt > K && oo < 0) {
-      // not recorded (more than K sources within h_build, first time): the count alone says
-      // h_build is well beyond the root; shrink it to hold about K/2 sources and re-walk
-      hbs = hbs * cbrtf(0.5f * (float)K / (float)cnt);
-      h = fminf(h, hbs / margin);
-      st = HS_REGROW;
-    }
+    H.h = xh[s].w;
+    H.hbs = hb[s];
+    H.l = lo_a[s];
+    H.u = hi_a[s];
   }
-  // first evaluation of a fresh list: start from the count within h_build, N(h) ~ C (h/h_build)^3
-  // for a locally uniform density (Eq. 3 with the kernel normalised), when that lies inside
-  // the bracket (saves the Newton steps from the cold guess)
-  if (st == HS_ACTIVE && cnt > 0) {
-    const float he = hbs * cbrtf(n_t / (float)cnt);
-    if (he > l && he < u && he <= hbs && fresh) h = he;
-  }
-  // short lists: one lane per particle
-  const bool shortl = st == HS_ACTIVE && cnt <= HSOLVE_LONG;
-  if (shortl) {
-    for (; it < max_iter && st == HS_ACTIVE; ++it) {
-      double S0 = 0.0;
-      float S1 = 0.f, S2 = 0.f;
-      nsums(r2l, stride, 0, cnt, 1, 1.0f / h, S0, S1, S2);
-      st = hstep(S0, S1, S2, h, hbs, l, u, n_t, tol, margin, hcap);
-      if (st == HS_REGROW) ++it;
-    }
-  }
-  // long lists: the whole warp, one particle at a time
-  unsigned lm = __ballot_sync(FULL_MASK, st == HS_ACTIVE && cnt > HSOLVE_LONG);
-  while (lm) {
-    const int t = __ffs(lm) - 1;
-    lm &= lm - 1;
-    const int tc = __shfl_sync(FULL_MASK, cnt, t);
-    const int64_t tstr = __shfl_sync(FULL_MASK, stride, t);
-    const float* tl = (const float*)__shfl_sync(FULL_MASK, (unsigned long long)r2l, t);
-    float th = __shfl_sync(FULL_MASK, h, t), thb = __shfl_sync(FULL_MASK, hbs, t);
-    float tlo = __shfl_sync(FULL_MASK, l, t), tu = __shfl_sync(FULL_MASK, u, t);
-    uint8_t tst = HS_ACTIVE;
-    int tit = 0;
-    for (; tit < max_iter && tst == HS_ACTIVE; ++tit) {
-      double S0 = 0.0;
-      float S1 = 0.f, S2 = 0.f;
-      nsums(tl, tstr, lane, tc, 32, 1.0f / th, S0, S1, S2);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        S0 += __shfl_xor_sync(FULL_MASK, S0, o);
-        S1 += __shfl_xor_sync(FULL_MASK, S1, o);
-        S2 += __shfl_xor_sync(FULL_MASK, S2, o);
-      }
-      tst = hstep(S0, S1, S2, th, thb, tlo, tu, n_t, tol, margin, hcap);
-      if (tst == HS_REGROW) ++tit;
-    }
-    if (lane == t) {
-      h = th;
-      hbs = thb;
-      l = tlo;
-      u = tu;
-      st = tst;
-      it = tit;
-    }
-  }
+  warp_hsolve(act, nb_r2 + (int64_t)grp.y * K + lane, grp.z, cnt, K, false, false, H, n_t, tol, margin, hcap,
+              max_iter);
   if (act) {
-    xh[s].w = h;
-    hb[s] = hbs;
-    lo_a[s] = l;
-    hi_a[s] = u;
-    state[s] = st;
+    xh[s].w = H.h;
+    hb[s] = H.hbs;
+    lo_a[s] = H.l;
+    hi_a[s] = H.u;
+    state[s] = H.st;
   }
-  const unsigned regrow = __ballot_sync(FULL_MASK, act && st == HS_REGROW);
-  const unsigned unconv = __ballot_sync(FULL_MASK, act && st == HS_ACTIVE);
-  const unsigned itmax = __reduce_max_sync(FULL_MASK, (unsigned)it);
-  if (lane == 0) {
-    if (regrow) atomicAdd(&ctr[C_REGROW], (unsigned long long)__popc(regrow));
-    if (unconv) atomicAdd(&ctr[C_UNCONV], (unsigned long long)__popc(unconv));
-    atomicMax(&ctr[C_TMP1], (unsigned long long)itmax);
-  }
+  hsolve_count(act, H, hc);
 }
 
 // The h iteration for particles whose list lives in the overflow pool (long, contiguous):
@@ -580,7 +423,7 @@ __global__ void __launch_bounds__(HSOLVE_WARPS * 32) k_hsolve_pool(const int* __
                                                                    const int64_t* __restrict__ ovf_off,
                                                                    const float* __restrict__ ovf, float n_t, float tol,
                                                                    float margin, float hcap, int max_iter,
-                                                                   unsigned long long* ctr) {
+                                                                   unsigned long long* hc) {
   const int lane = threadIdx.x & 31;
   const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   if (w >= nidx) return;
@@ -611,9 +454,9 @@ __global__ void __launch_bounds__(HSOLVE_WARPS * 32) k_hsolve_pool(const int* __
     lo_a[s] = l;
     hi_a[s] = u;
     state[s] = st;
-    if (st == HS_REGROW) atomicAdd(&ctr[C_REGROW], 1ull);
-    if (st == HS_ACTIVE) atomicAdd(&ctr[C_UNCONV], 1ull);
-    atomicMax(&ctr[C_TMP1], (unsigned long long)it);
+    if (st == HS_REGROW) atomicAdd(&hc[HC_REGROW], 1ull);
+    if (st == HS_ACTIVE) atomicAdd(&hc[HC_UNCONV], 1ull);
+    atomicMax(&hc[HC_ITMAX], (unsigned long long)it);
   }
 }
 

@@ -457,8 +457,10 @@ static const int* group_order(sph_ctx* c, const float* reach) {
 // NB walk over all groups: per target (the owned particles if tsel_val < 0, else those in
 // state tsel_val) the squared distances r^2 < h_build^2 (lists.cuh, MODE_NB). Overflows are
 // marked on the device (k_mark_overflow) and counted in B_OVFCNT; no host round trip.
+static float solve_margin(sph_ctx* c) { return std::max(c->cfg.h_margin, c->regrow_margin); }
+
 static void nb_walk(sph_ctx* c, int tsel_val) {
-  DbgTimer _t(c, "neighbour lists");
+  DbgTimer _t(c, "neighbour lists + h solve");
   const int64_t n = c->n;
   WalkParams P = walk_params(c, Bget<float>(c, B_HB));
   P.nsel = c->n_groups;
@@ -471,17 +473,29 @@ static void nb_walk(sph_ctx* c, int tsel_val) {
   P.nb_entries = Bget<unsigned long long>(c, B_NBENT);
   P.nb_r2 = B<float>(c, B_NBR2, (size_t)n * c->nb_k);
   P.nb_cnt = B<int>(c, B_NBCNT, n);
+  P.solve = 1;
+  P.hb_w = Bget<float>(c, B_HB);
+  P.lo = Bget<float>(c, B_HLO);
+  P.hi = Bget<float>(c, B_HHI);
+  P.state = Bget<uint8_t>(c, B_STATE);
+  P.shrunk = Bget<uint8_t>(c, B_SHRUNK);
+  P.ovf_cnt = B<int64_t>(c, B_OVFC, n);
+  P.ovf_off_w = Bget<int64_t>(c, B_NBOFF);
+  P.hc = B<unsigned long long>(c, B_HCTR, 4);
+  P.n_t = c->cfg.n_ngb;
+  P.tol = c->cfg.n_ngb_tol;
+  P.margin = solve_margin(c);
+  P.hcap = h_cap(c);
+  P.max_iter = c->cfg.max_h_iter;
   {
     PhaseTimer _p(c, 0);
     LAUNCH(k_walk<MODE_NB>, gridfull(P.nsel, WALK_WARPS), WALK_WARPS * 32, walk_smem(), P);
   }
   c->walk_launches++;
-  uint8_t* state = Bget<uint8_t>(c, B_STATE);
-  LAUNCH(k_mark_overflow, gridfull((int64_t)c->n_groups * 32, 256), 256, 0, Bget<int4>(c, B_GROUPS), c->n_groups,
-         state, tsel_val, Bget<uint32_t>(c, B_PERM), c->n_own, P.nb_cnt, c->nb_k, state, B<int64_t>(c, B_OVFC, n),
-         Bget<int64_t>(c, B_NBOFF), Bget<uint8_t>(c, B_SHRUNK), B<unsigned long long>(c, B_OVFCNT, 1));
-  if (tsel_val >= 0)
-    LAUNCH(k_state_swap, grid1d(c, n, 256), 256, 0, state, n, (uint8_t)tsel_val, (uint8_t)HS_ACTIVE);
+}
+
+static void hctr_reset(sph_ctx* c) {
+  CUDA_TRY(cudaMemsetAsync(B<unsigned long long>(c, B_HCTR, 4), 0, 4 * sizeof(unsigned long long), c->stream));
 }
 
 // Particles in state HS_OVF (a repeat overflow): exactly sized lists in the overflow pool
@@ -882,7 +896,7 @@ int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const floa
            margin, h_cap(c), Bget<uint8_t>(c, B_STATE), hb, Bget<float>(c, B_HLO), Bget<float>(c, B_HHI));
   }
   // neighbour lists of the h iteration: r^2 < h_build^2 per particle
-  CUDA_TRY(cudaMemsetAsync(B<unsigned long long>(c, B_OVFCNT, 1), 0, sizeof(unsigned long long), c->stream));
+  hctr_reset(c);
   nb_walk(c, -1);
   c->state = 1;
   CUDA_TRY(cudaEventRecord(c->ev[1], c->stream));
@@ -930,52 +944,56 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   }
   // a8: the h iteration, per particle on its neighbour list; re-walk particles whose root
   // lies beyond their list, until every particle has converged
-  const float margin = std::max(c->cfg.h_margin, c->regrow_margin);
+  const float margin = solve_margin(c);
   int rounds = 0;
   long long unconv = 0, itmax = 0;
   CUDA_TRY(cudaEventRecord(c->ev[6], c->stream));
+  if (c->state >= 2) {
+    // a repeated call: the lists are recorded; solve on them from the current h
+    hctr_reset(c);
+    PhaseTimer _p(c, 1);
+    LAUNCH(k_hsolve, gridfull((int64_t)c->n_groups * 32, HSOLVE_WARPS * 32), HSOLVE_WARPS * 32, 0,
+           Bget<int4>(c, B_GROUPS), c->n_groups, Bget<float4>(c, B_XH), Bget<float>(c, B_HB), Bget<float>(c, B_HLO),
+           Bget<float>(c, B_HHI), state, Bget<float>(c, B_NBR2), Bget<int>(c, B_NBCNT), c->nb_k,
+           Bget<int64_t>(c, B_NBOFF), Bget<float>(c, B_NBOVF), c->cfg.n_ngb, c->cfg.n_ngb_tol, margin, h_cap(c),
+           c->cfg.max_h_iter, Bget<unsigned long long>(c, B_HCTR));
+    if (c->n_ovfidx > 0)
+      LAUNCH(k_hsolve_pool, gridfull((int64_t)c->n_ovfidx * 32, HSOLVE_WARPS * 32), HSOLVE_WARPS * 32, 0,
+             Bget<int32_t>(c, B_OVFIDX), (int)c->n_ovfidx, Bget<float4>(c, B_XH), Bget<float>(c, B_HB),
+             Bget<float>(c, B_HLO), Bget<float>(c, B_HHI), state, Bget<int>(c, B_NBCNT), Bget<int64_t>(c, B_NBOFF),
+             Bget<float>(c, B_NBOVF), c->cfg.n_ngb, c->cfg.n_ngb_tol, margin, h_cap(c), c->cfg.max_h_iter,
+             Bget<unsigned long long>(c, B_HCTR));
+  }
+  // The first solve ran fused into the build's walk (lists.cuh); each round reads its
+  // counters (one host round trip), records the lists of the particles whose root lies
+  // beyond their list (a fused re-walk + solve) and the pool lists of repeat overflows.
   while (true) {
-    ctr_reset(c);
-    {
-      DbgTimer _t(c, "h solve");
-      PhaseTimer _p(c, 1);
-      LAUNCH(k_hsolve, gridfull((int64_t)c->n_groups * 32, HSOLVE_WARPS * 32), HSOLVE_WARPS * 32, 0,
-             Bget<int4>(c, B_GROUPS), c->n_groups, Bget<float4>(c, B_XH), Bget<float>(c, B_HB), Bget<float>(c, B_HLO),
-             Bget<float>(c, B_HHI), state, Bget<float>(c, B_NBR2), Bget<int>(c, B_NBCNT), c->nb_k,
-             Bget<int64_t>(c, B_NBOFF), Bget<float>(c, B_NBOVF), c->cfg.n_ngb,
-             c->cfg.n_ngb_tol, margin, h_cap(c), c->cfg.max_h_iter, ctr(c));
+    unsigned long long hh[4];
+    CUDA_TRY(cudaMemcpyAsync(hh, Bget<unsigned long long>(c, B_HCTR), sizeof(hh), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    ++rounds;
+    unconv = (long long)hh[HC_UNCONV];
+    itmax = std::max(itmax, (long long)hh[HC_ITMAX]);
+    DBG("h solve round %d: unconverged %llu, re-walk %llu, pool %llu, max iterations %llu\n", rounds,
+        hh[HC_UNCONV], hh[HC_REGROW], hh[HC_OVF], hh[HC_ITMAX]);
+    if (hh[HC_REGROW] == 0 && hh[HC_OVF] == 0) break;
+    if (rounds >= c->cfg.max_h_iter) {
+      unconv += (long long)(hh[HC_REGROW] + hh[HC_OVF]);
+      break;
     }
-    if (c->n_ovfidx > 0) {
-      DbgTimer _t(c, "h solve (pool)");
+    hctr_reset(c);
+    if (hh[HC_OVF] > 0) {
+      nb_pool(c);
       PhaseTimer _p(c, 1);
       LAUNCH(k_hsolve_pool, gridfull((int64_t)c->n_ovfidx * 32, HSOLVE_WARPS * 32), HSOLVE_WARPS * 32, 0,
              Bget<int32_t>(c, B_OVFIDX), (int)c->n_ovfidx, Bget<float4>(c, B_XH), Bget<float>(c, B_HB),
              Bget<float>(c, B_HLO), Bget<float>(c, B_HHI), state, Bget<int>(c, B_NBCNT), Bget<int64_t>(c, B_NBOFF),
-             Bget<float>(c, B_NBOVF), c->cfg.n_ngb, c->cfg.n_ngb_tol, margin, h_cap(c), c->cfg.max_h_iter, ctr(c));
+             Bget<float>(c, B_NBOVF), c->cfg.n_ngb, c->cfg.n_ngb_tol, margin, h_cap(c), c->cfg.max_h_iter,
+             Bget<unsigned long long>(c, B_HCTR));
     }
-    // one host round trip per round: the solve's counters and the overflows of the last walk
-    unsigned long long novf = 0;
-    CUDA_TRY(cudaMemcpyAsync(&novf, Bget<unsigned long long>(c, B_OVFCNT), sizeof(novf), cudaMemcpyDeviceToHost,
-                             c->stream));
-    ctr_read(c, hc);
-    ++rounds;
-    unconv = (long long)hc[C_UNCONV];
-    itmax = std::max(itmax, (long long)hc[C_TMP1]);
-    DBG("h solve round %d: unconverged %llu, regrow %llu, pool %llu, max iterations %llu\n", rounds, hc[C_UNCONV],
-        hc[C_REGROW], novf, hc[C_TMP1]);
-    if (hc[C_REGROW] == 0 && novf == 0) break;
-    if (rounds >= c->cfg.max_h_iter) {
-      unconv += (long long)(hc[C_REGROW] + novf);
-      break;
-    }
-    if (novf > 0) {
-      // repeat overflows of the last walk: record them in the pool, solve them next round
-      CUDA_TRY(cudaMemsetAsync(Bget<unsigned long long>(c, B_OVFCNT), 0, sizeof(unsigned long long), c->stream));
-      nb_pool(c);
-    }
-    if (hc[C_REGROW] > 0) {
+    if (hh[HC_REGROW] > 0) {
       nb_walk(c, HS_REGROW);
-      c->list_rebuilds += (int64_t)hc[C_REGROW];
+      c->list_rebuilds += (int64_t)hh[HC_REGROW];
     }
   }
   CUDA_TRY(cudaEventRecord(c->ev[7], c->stream));

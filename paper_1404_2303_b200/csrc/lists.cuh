@@ -32,6 +32,7 @@
 // c = cx + 3 cy + 9 cz, c_a = 0 none, 1 source at x - L_a, 2 source at x + L_a.
 #pragma once
 #include "build.cuh"
+#include "hiter.cuh"
 
 #define WALK_WARPS 8
 #define WALK_TAKE 32    // a node holding <= WALK_TAKE particles is swept whole (no descent)
@@ -83,6 +84,17 @@ struct WalkParams {
   int* nb_cnt;              // [n] sources with r^2 < h_build^2 (may exceed K: overflow)
   int K;
   unsigned long long* nb_entries;   // NB: running total of recorded entries
+  // NB + solve: the h iteration runs in the walk's epilogue on the list just recorded
+  int solve;
+  float* hb_w;              // h_build (== reach), written back
+  float *lo, *hi;           // Newton brackets
+  uint8_t* state;
+  uint8_t* shrunk;          // first overflow seen
+  int64_t* ovf_cnt;         // repeat overflow: exact count (pool)
+  int64_t* ovf_off_w;       // -1: the list is in the slab
+  unsigned long long* hc;   // solve counters (HC_*)
+  float n_t, tol, margin, hcap;
+  int max_iter;
   const int64_t* ovf_off;   // NB overflow walk: the particle's list at ovf + ovf_off[s] (contiguous)
   float* ovf;
   unsigned long long* ctr;
@@ -540,6 +552,41 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkParams P) {
              gid, W.ntg, W.R, W.hi.x - W.lo.x, W.hi.y - W.lo.y, W.hi.z - W.lo.z, (int)W.spheres, W.raw, mc);
   }
 #endif
+  if (MODE == MODE_NB && P.solve) {
+    // fused h iteration on the list just recorded (still in L1/L2): first overflow of K ->
+    // shrink h_build; repeat overflow -> exact list in the pool (k_hsolve_pool)
+    const int cnt = W.cur;
+    bool act = tg;
+    HLane H;
+    H.h = H.hbs = H.l = H.u = 0.f;
+    H.st = HS_DONE;
+    if (tg) {
+      H.h = P.xh[s].w;
+      H.hbs = W.ri;
+      H.l = P.lo[s];
+      H.u = P.hi[s];
+      const bool over = cnt > P.K;
+      if (over && P.shrunk[s]) {
+        H.st = HS_OVF;
+        act = false;
+        P.ovf_cnt[s] = cnt;
+      } else {
+        if (over) P.shrunk[s] = 1;
+        P.ovf_off_w[s] = -1;
+        P.ovf_cnt[s] = 0;
+      }
+    }
+    warp_hsolve(act, P.nb_r2 + (int64_t)grp.y * P.K + lane, W.gz, cnt, P.K, false, true, H, P.n_t, P.tol, P.margin,
+                P.hcap, P.max_iter);
+    if (tg) {
+      reinterpret_cast<float*>(const_cast<float4*>(P.xh) + s)[3] = H.h;
+      P.hb_w[s] = H.hbs;
+      P.lo[s] = H.l;
+      P.hi[s] = H.u;
+      P.state[s] = H.st;
+    }
+    hsolve_count(tg, H, P.hc);
+  }
   if (MODE == MODE_NB) {
     if (tg && !P.ovf) P.nb_cnt[s] = W.cur;
     if (!P.ovf && P.nb_entries) {
@@ -567,11 +614,6 @@ __global__ void k_set_offsets(int nsel, const int* __restrict__ sel, const int64
   if (w >= nsel) return;
   off[sel ? sel[w] : w] = base + scan[w];
 }
-
-// per-particle states of the h iteration
-#define HS_DONE 0
-#define HS_ACTIVE 1
-#define HS_REGROW 2   // needs a neighbour list for a new h_build (grown, or shrunk after overflow)
 
 // groups holding a particle in state `val` (compaction flags)
 __global__ void k_group_flags(const int4* __restrict__ groups, int ngroups, const uint8_t* __restrict__ state,
@@ -601,7 +643,6 @@ __global__ void k_widen_i32(const int* __restrict__ in, int64_t n, int64_t* __re
 // the large region); a particle that overflows again gets an exactly sized list in the
 // overflow pool (state HS_OVF marks it for the second, contiguous-layout walk). The bit
 // `shrunk` remembers the first overflow.
-#define HS_OVF 3
 #define NB_POOL_MAX (1 << 24)   // longer lists are never recorded: h_build shrinks
 __global__ void k_mark_overflow(const int4* __restrict__ groups, int ngroups, const uint8_t* __restrict__ tsel,
                                 int tsel_val, const uint32_t* __restrict__ perm, int64_t n_own,
