@@ -138,6 +138,7 @@ struct sph_ctx {
   int64_t pool = 0;          // entries of the interaction (UNION) lists
   float cold_margin = SPH_COLD_MARGIN, regrow_margin = SPH_REGROW_MARGIN;
   int nb_k = 192;            // capacity of a particle's neighbour list (NB walk)
+  int64_t nb_k_for = -1;     // particle count nb_k was sized for
   int ucap = 768;            // capacity of a group's interaction list slab (UNION walk)
   int group_cmax = 512;      // targets: balanced chunks of the deepest cells holding <= 512 (0: sibling packing)
   int64_t ovf_used = 0;      // entries of the neighbour-list overflow pool

@@ -849,13 +849,15 @@ int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const floa
   c->n_own = n_own;
   c->state = 0;
   c->force_lists = false;
-  if (!getenv("SPH_NBK")) {
+  if (!getenv("SPH_NBK") && n != c->nb_k_for) {
     // neighbour-list slab: up to 1024 entries per particle, within 40% of the free device
-    // memory (cold-start lists hold ~90 entries; longer ones shrink or go to the pool)
+    // memory (cold-start lists hold ~90 entries; longer ones shrink or go to the pool);
+    // sized once per particle count (cudaMemGetInfo stalls the host)
     size_t fr = 0, tot = 0;
     CUDA_TRY(cudaMemGetInfo(&fr, &tot));
     const size_t have = fr + c->b[B_NBR2].bytes;   // the slab of a previous build is reused
     c->nb_k = (int)std::max<int64_t>(64, std::min<int64_t>(1024, (int64_t)(0.4 * (double)have / (4.0 * (double)n))));
+    c->nb_k_for = n;
   }
   c->pool = 0;
   c->list_rebuilds = 0;
