@@ -159,6 +159,8 @@ struct sph_ctx {
   // named device buffers
   DBuf b[80];
   cudaEvent_t ev[12];
+  cudaStream_t stream2 = nullptr;   // side stream: host->device copies overlapped with the h iteration
+  cudaEvent_t ev_side[2];
   bool ev_ok = false;
 };
 

@@ -763,6 +763,8 @@ int sph_create(const sph_config* cfg, int dev, void* stream, sph_ctx** out) {
       c->own_stream = true;
     }
     for (int i = 0; i < 12; ++i) CUDA_TRY(cudaEventCreate(&c->ev[i]));
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) CUDA_TRY(cudaEventCreateWithFlags(&c->ev_side[i], cudaEventDisableTiming));
     float dirs[14][3];
     for (int d = 0; d < 13; ++d) {
       const int k = d + 14;
@@ -793,8 +795,15 @@ int sph_destroy(sph_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   for (int i = 0; i < 80; ++i) dev_free(c, c->b[i].p);
-  if (c->ev_ok)
+  if (c->ev_ok) {
     for (int i = 0; i < 12; ++i) cudaEventDestroy(c->ev[i]);
+    for (int i = 0; i < 2; ++i) cudaEventDestroy(c->ev_side[i]);
+    cudaStreamDestroy(c->stream2);
+  }
+  for (auto& t : c->timed) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
   return SPH_OK;
@@ -925,19 +934,31 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   SPH_REQUIRE(v && m && u && h_out && rho_out, SPH_E_ARG, "required pointer is NULL");
   const int64_t n = c->n;
   CUDA_TRY(cudaEventRecord(c->ev[2], c->stream));
-  const float* vd = dev_in(c, v, 3 * n, B_VIN);
-  const float* md = dev_in(c, m, n, B_MIN);
-  const float* ud = dev_in(c, u, n, B_UIN);
-  ctr_reset(c);
-  LAUNCH(k_validate_vmu, grid1d(c, n, 256), 256, 0, vd, md, ud, n, ctr(c));
-  float4* vm = B<float4>(c, B_VM, n);
-  float* uc = B<float>(c, B_U, n);
-  LAUNCH(k_gather_vmu, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, vd, md, ud, vm, uc);
+  // v, m, u are first needed after the h iteration: host arrays are copied on the side
+  // stream while the rounds run (joined before validation)
+  const float* vd = v;
+  const float* md = m;
+  const float* ud = u;
+  bool side = false;
+  {
+    const void* in[3] = {v, m, u};
+    const int ids[3] = {B_VIN, B_MIN, B_UIN};
+    const size_t cnt[3] = {(size_t)(3 * n), (size_t)n, (size_t)n};
+    const float** outp[3] = {&vd, &md, &ud};
+    for (int k = 0; k < 3; ++k) {
+      if (is_device_ptr(in[k])) continue;
+      if (!side) {
+        CUDA_TRY(cudaEventRecord(c->ev_side[0], c->stream));   // staging buffers free to overwrite
+        CUDA_TRY(cudaStreamWaitEvent(c->stream2, c->ev_side[0], 0));
+        side = true;
+      }
+      float* d = B<float>(c, ids[k], cnt[k]);
+      CUDA_TRY(cudaMemcpyAsync(d, in[k], cnt[k] * sizeof(float), cudaMemcpyHostToDevice, c->stream2));
+      *outp[k] = d;
+    }
+    if (side) CUDA_TRY(cudaEventRecord(c->ev_side[1], c->stream2));
+  }
   unsigned long long hc[C_NCOUNTERS];
-  ctr_read(c, hc);
-  SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_NONFINITE), SPH_E_DOMAIN, "non-finite velocity");
-  SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_MASS), SPH_E_DOMAIN, "mass <= 0 or non-finite");
-  SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_U), SPH_E_DOMAIN, "internal energy <= 0 or non-finite");
 
   uint8_t* state = Bget<uint8_t>(c, B_STATE);
   if (c->state >= 2) {   // a repeated call: iterate again from the current h (lists stay valid)
@@ -999,6 +1020,17 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
     }
   }
   CUDA_TRY(cudaEventRecord(c->ev[7], c->stream));
+  // join the side-stream copies; validate and gather v, m, u into cell order
+  if (side) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_side[1], 0));
+  ctr_reset(c);
+  LAUNCH(k_validate_vmu, grid1d(c, n, 256), 256, 0, vd, md, ud, n, ctr(c));
+  float4* vm = B<float4>(c, B_VM, n);
+  float* uc = B<float>(c, B_U, n);
+  LAUNCH(k_gather_vmu, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, vd, md, ud, vm, uc);
+  ctr_read(c, hc);
+  SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_NONFINITE), SPH_E_DOMAIN, "non-finite velocity");
+  SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_MASS), SPH_E_DOMAIN, "mass <= 0 or non-finite");
+  SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_U), SPH_E_DOMAIN, "internal energy <= 0 or non-finite");
   // a7: the density loop at the final h over the interaction lists (reach max(h_i, h_j)
   // with the owned particles' h; these are the force lists too when there is no halo)
   float* hr = Bget<float>(c, B_HRCH);
