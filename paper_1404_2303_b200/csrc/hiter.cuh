@@ -35,15 +35,23 @@ __device__ __forceinline__ float spline_fp(float q) {
 
 // one iteration's sums over a list: S0 = sum f (fp64), S1 = sum q f', S2 = sum q^2 f''.
 // Branch-free so the loads overlap: q is clamped to 1, where f = f' = f'' = 0 exactly.
-__device__ __forceinline__ void nsums(const float* __restrict__ r2l, int64_t stride, int e0, int e1, int estep,
+#ifndef SPH_HSTEP_ACCEPT
+#define SPH_HSTEP_ACCEPT 3e-3f
+#endif
+#ifndef NSUMS_UNROLL
+#define NSUMS_UNROLL 4
+#endif
+// The lists are read with plain (weak, coherent) loads, never ld.global.nc: the fused solve
+// reads lists its own warp wrote earlier in the same kernel (ordered by __syncwarp).
+__device__ __forceinline__ void nsums(const float* r2l, int64_t stride, int e0, int e1, int estep,
                                       float hinv, double& S0, float& S1, float& S2) {
   int e = e0;
-  for (; e + 3 * estep < e1; e += 4 * estep) {
-    float r2[4];
+  for (; e + (NSUMS_UNROLL - 1) * estep < e1; e += NSUMS_UNROLL * estep) {
+    float r2[NSUMS_UNROLL];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) r2[k] = __ldg(r2l + (int64_t)(e + k * estep) * stride);
+    for (int k = 0; k < NSUMS_UNROLL; ++k) r2[k] = r2l[(int64_t)(e + k * estep) * stride];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < NSUMS_UNROLL; ++k) {
       const float q = fminf(r2[k] * rsqrtf(fmaxf(r2[k], 1e-37f)) * hinv, 1.f);
       float f, fp, fpp;
       spline(q, f, fp, fpp);
@@ -53,7 +61,7 @@ __device__ __forceinline__ void nsums(const float* __restrict__ r2l, int64_t str
     }
   }
   for (; e < e1; e += estep) {
-    const float r2 = __ldg(r2l + (int64_t)e * stride);
+    const float r2 = r2l[(int64_t)e * stride];
     const float q = fminf(r2 * rsqrtf(fmaxf(r2, 1e-37f)) * hinv, 1.f);
     float f, fp, fpp;
     spline(q, f, fp, fpp);
@@ -79,25 +87,35 @@ __device__ __forceinline__ uint8_t hstep(double S0, float S1, float S2, float& h
   const float g1 = -(32.f / 3.f) * S1 / N;
   const float g2 = g1 + (32.f / 3.f) * (2.f * S1 + S2) / N - g1 * g1;
   float dx;
+  bool halley = false;
   if (g1 > 0.25f) {
     dx = -g / g1;                                     // log-space Newton
     const float den = 2.f * g1 * g1 - g * g2;          // Halley (cubic convergence)
     if (den > 0.5f * g1 * g1) {
       const float dh = -2.f * g * g1 / den;
-      if (fabsf(dh) <= 2.f * fabsf(dx)) dx = dh;
+      if (fabsf(dh) <= 2.f * fabsf(dx)) {
+        dx = dh;
+        halley = true;
+      }
     }
   } else {
     dx = (res < 0.f) ? 0.6931472f : -0.6931472f;      // (almost) no neighbour: double / halve
   }
   float hn = h * __expf(dx);
   hn = fminf(fmaxf(hn, 0.5f * h), 2.f * h);
-  if (!(hn > l && hn < u)) hn = 0.5f * (l + fminf(u, 2.f * h));
+  const bool inb = hn > l && hn < u;
+  if (!inb) hn = 0.5f * (l + fminf(u, 2.f * h));
   hn = fminf(hn, hcap);
   h = hn;
   if (hn > hbs) {                                     // the root lies beyond the list
     hbs = fminf(fminf(hn * margin, fmaxf(u, hn)), hcap);
     return HS_REGROW;
   }
+  // A Halley step of |dx| <= SPH_HSTEP_ACCEPT leaves a residual of order |g3 / g1| dx^3 / 6
+  // in ln N (g3 the third derivative; ~1e-7 N here), far inside tol: accept it without
+  // another pass over the list. k_ghost re-checks N(h) at the final h from the density
+  // loop's sums, so a wrong acceptance is reported as unconverged, never silently kept.
+  if (halley && inb && hn < hcap && fabsf(dx) <= SPH_HSTEP_ACCEPT) return HS_DONE;
   return HS_ACTIVE;
 }
 

@@ -495,8 +495,9 @@ struct GhostOut {
 
 __global__ void k_ghost(int64_t n, const float4* __restrict__ xh, const float* __restrict__ u,
                         const float4* __restrict__ acc0, const float4* __restrict__ acc1, float gamma, float beps,
-                        GhostOut out, unsigned long long* ctr) {
-  long long nd = 0;
+                        const double* __restrict__ sf, float n_t, float tol_check, GhostOut out,
+                        unsigned long long* ctr) {
+  long long nd = 0, nbad = 0;
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n;
        s += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t o = out.perm[s];
@@ -520,6 +521,8 @@ __global__ void k_ghost(int64_t n, const float4* __restrict__ xh, const float* _
     out.g_o[o] = make_float4(A, rho, c, fb);
     const int cnt = __float_as_int(a1.w);
     nd += cnt;
+    // the h iteration's convergence, re-checked from the density loop's sum at the final h
+    nbad += fabs((32.0 / 3.0) * sf[s] - (double)n_t) > (double)tol_check ? 1 : 0;
     out.h[o] = h;
     out.rho[o] = rho;
     if (out.omega) out.omega[o] = omega;
@@ -532,8 +535,12 @@ __global__ void k_ghost(int64_t n, const float4* __restrict__ xh, const float* _
     }
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) nd += __shfl_xor_sync(FULL_MASK, nd, o);
+  for (int o = 16; o > 0; o >>= 1) {
+    nd += __shfl_xor_sync(FULL_MASK, nd, o);
+    nbad += __shfl_xor_sync(FULL_MASK, nbad, o);
+  }
   if ((threadIdx.x & 31) == 0 && nd) atomicAdd(&ctr[C_NDIR], (unsigned long long)nd);
+  if ((threadIdx.x & 31) == 0 && nbad) atomicAdd(&ctr[C_UNCONV], (unsigned long long)nbad);
 }
 
 // force inputs in cell order from the caller-order state (owned: the ghost; halo: imported):

@@ -1066,14 +1066,18 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   go.n_own = no;
   go.h_o = B<float>(c, B_HFIN_O, n);
   go.g_o = B<float4>(c, B_GST_O, n);
+  // N(h) re-check: twice the iteration's tolerance plus a few fp32 ulps of h (the bracket
+  // stop at fp32 resolution) in N = n_t (h/h)^3
+  const float tol_check = 2.f * (float)c->cfg.n_ngb_tol + 24.f * (float)c->cfg.n_ngb * 1.1920929e-7f;
   LAUNCH(k_ghost, grid1d(c, n, 256), 256, 0, n, Bget<float4>(c, B_XH), uc, dout.acc0, dout.acc1, c->cfg.gamma,
-         c->cfg.balsara_eps, go, ctr(c));
+         c->cfg.balsara_eps, dout.sf, (float)c->cfg.n_ngb, tol_check, go, ctr(c));
   flush_out(c, maps, c->ev[3]);
   c->state = 2;
   const bool noconv = unconv > 0;
   ctr_read(c, hc);
   const long long ndir = (long long)hc[C_NDIR];
   const long long cand = (long long)hc[C_CAND];
+  const long long nbad = (long long)hc[C_UNCONV];
   if (c->n > c->n_own && c->cfg.halo_width > 0.0) {
     // every owned particle's partners must be inside the received halo
     ctr_reset(c);
@@ -1101,7 +1105,7 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
     st->n_directed = ndir;
     st->n_candidates = cand;
     st->n_candidates_density_full = cand;
-    st->n_unconverged = noconv ? unconv : 0;
+    st->n_unconverged = (noconv ? unconv : 0) + (noconv ? 0 : nbad);
     st->h_iters = (int)itmax;
     float ms = 0.f;
     cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);

@@ -34,7 +34,9 @@
 #include "build.cuh"
 #include "hiter.cuh"
 
+#ifndef WALK_WARPS
 #define WALK_WARPS 8
+#endif
 #define WALK_TAKE 32    // a node holding <= WALK_TAKE particles is swept whole (no descent)
 #define WALK_CAP 384    // frontier entries (node | image code << 27), LIFO
 #define WALK_DFS 112    // room for the depth-first fallback above the frontier
@@ -576,6 +578,7 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkParams P) {
         P.ovf_cnt[s] = 0;
       }
     }
+    __syncwarp();   // the lists recorded by every lane are visible to the cooperative sums
     warp_hsolve(act, P.nb_r2 + (int64_t)grp.y * P.K + lane, W.gz, cnt, P.K, false, true, H, P.n_t, P.tol, P.margin,
                 P.hcap, P.max_iter);
     if (tg) {
