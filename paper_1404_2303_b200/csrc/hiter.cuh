@@ -10,7 +10,9 @@
 #define HS_REGROW 2   // needs a neighbour list for a new h_build (grown, or shrunk after overflow)
 
 #define HS_OVF 3   // repeat overflow: needs an exactly sized list in the overflow pool
-#define HSOLVE_LONG 96   // lists longer than this are solved by the whole warp
+#ifndef HSOLVE_LONG
+#define HSOLVE_LONG 128  // lists longer than this are solved by the whole warp
+#endif
 
 // counters of a solve (device, read once per round): unconverged, re-walks, pool, max iterations
 #define HC_UNCONV 0

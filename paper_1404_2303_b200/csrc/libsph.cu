@@ -459,16 +459,32 @@ static const int* group_order(sph_ctx* c, const float* reach) {
 // marked on the device (k_mark_overflow) and counted in B_OVFCNT; no host round trip.
 static float solve_margin(sph_ctx* c) { return std::max(c->cfg.h_margin, c->regrow_margin); }
 
-static void nb_walk(sph_ctx* c, int tsel_val) {
+static void nb_walk(sph_ctx* c, int tsel_val, int64_t n_regrow = 0) {
   DbgTimer _t(c, "neighbour lists + h solve");
   const int64_t n = c->n;
   WalkParams P = walk_params(c, Bget<float>(c, B_HB));
   P.nsel = c->n_groups;
   P.sel = group_order(c, Bget<float>(c, B_HB));
+  const int ng = c->n_groups;
+  int* rgl = B<int>(c, B_RGL, 2 * (int64_t)std::max(ng, 1));
+  int* rgc = B<int>(c, B_RGCNT, 2);
   if (tsel_val >= 0) {
     P.tsel = Bget<uint8_t>(c, B_STATE);
     P.tsel_val = (uint8_t)tsel_val;
+    if (tsel_val == HS_REGROW && c->rg_valid && !getenv("SPH_REWALK_ALL")) {
+      // only the groups the last solve left with re-walking particles (at most one per particle)
+      P.sel = rgl + (int64_t)c->rg_cur * ng;
+      P.nsel_dev = rgc + c->rg_cur;
+      P.nsel = (int)std::min<int64_t>(ng, n_regrow);
+    }
   }
+  // this walk's solve appends its re-walk groups to the other list
+  const int nxt = P.nsel_dev ? 1 - c->rg_cur : c->rg_cur;
+  CUDA_TRY(cudaMemsetAsync(rgc + nxt, 0, sizeof(int), c->stream));
+  P.rg_out = rgl + (int64_t)nxt * ng;
+  P.rg_cnt = rgc + nxt;
+  c->rg_cur = nxt;
+  c->rg_valid = true;
   P.K = c->nb_k;
   P.nb_entries = Bget<unsigned long long>(c, B_NBENT);
   P.nb_r2 = B<float>(c, B_NBR2, (size_t)n * c->nb_k);
@@ -980,12 +996,14 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
            Bget<float>(c, B_HHI), state, Bget<float>(c, B_NBR2), Bget<int>(c, B_NBCNT), c->nb_k,
            Bget<int64_t>(c, B_NBOFF), Bget<float>(c, B_NBOVF), c->cfg.n_ngb, c->cfg.n_ngb_tol, margin, h_cap(c),
            c->cfg.max_h_iter, Bget<unsigned long long>(c, B_HCTR));
+    c->rg_valid = false;   // its re-walk particles are not in the group list
     if (c->n_ovfidx > 0)
       LAUNCH(k_hsolve_pool, gridfull((int64_t)c->n_ovfidx * 32, HSOLVE_WARPS * 32), HSOLVE_WARPS * 32, 0,
              Bget<int32_t>(c, B_OVFIDX), (int)c->n_ovfidx, Bget<float4>(c, B_XH), Bget<float>(c, B_HB),
              Bget<float>(c, B_HLO), Bget<float>(c, B_HHI), state, Bget<int>(c, B_NBCNT), Bget<int64_t>(c, B_NBOFF),
              Bget<float>(c, B_NBOVF), c->cfg.n_ngb, c->cfg.n_ngb_tol, margin, h_cap(c), c->cfg.max_h_iter,
              Bget<unsigned long long>(c, B_HCTR));
+      c->rg_valid = false;   // its re-walk particles are not in the group list
   }
   // The first solve ran fused into the build's walk (lists.cuh); each round reads its
   // counters (one host round trip), records the lists of the particles whose root lies
@@ -1013,9 +1031,10 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
              Bget<float>(c, B_HLO), Bget<float>(c, B_HHI), state, Bget<int>(c, B_NBCNT), Bget<int64_t>(c, B_NBOFF),
              Bget<float>(c, B_NBOVF), c->cfg.n_ngb, c->cfg.n_ngb_tol, margin, h_cap(c), c->cfg.max_h_iter,
              Bget<unsigned long long>(c, B_HCTR));
+      c->rg_valid = false;   // its re-walk particles are not in the group list
     }
     if (hh[HC_REGROW] > 0) {
-      nb_walk(c, HS_REGROW);
+      nb_walk(c, HS_REGROW, (int64_t)hh[HC_REGROW]);
       c->list_rebuilds += (int64_t)hh[HC_REGROW];
     }
   }

@@ -62,6 +62,9 @@ struct WalkParams {
   const int4* groups;
   int nsel;                 // groups to walk
   const int* sel;           // their ids (null: 0..nsel-1)
+  const int* nsel_dev;      // if set: the number of groups in sel (device; nsel is a bound)
+  int* rg_out;              // if set: groups with a lane left in HS_REGROW are appended here
+  int* rg_cnt;              //   (count, atomic; order is scheduling only, results do not depend on it)
   const float4* xh;         // cell-order positions
   const float* reach;       // per particle: NB h_build; UNION the h used for the reach (0: none)
   const uint8_t* tsel;      // NB: targets are the particles with tsel == tsel_val (null: owned)
@@ -373,7 +376,7 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkParams P) {
   WalkSmem* smem = reinterpret_cast<WalkSmem*>(walk_raw);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int w = blockIdx.x * WALK_WARPS + wib;
-  if (w >= P.nsel) return;
+  if (w >= P.nsel || (P.nsel_dev && w >= *P.nsel_dev)) return;
   WalkSmem& S = smem[wib];
   const int gid = P.sel ? P.sel[w] : w;
   const int4 grp = P.groups[gid];
@@ -589,6 +592,10 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkParams P) {
       P.state[s] = H.st;
     }
     hsolve_count(tg, H, P.hc);
+    if (P.rg_out) {
+      const unsigned rg = __ballot_sync(FULL_MASK, tg && H.st == HS_REGROW);
+      if (rg && lane == 0) P.rg_out[atomicAdd(P.rg_cnt, 1)] = gid;
+    }
   }
   if (MODE == MODE_NB) {
     if (tg && !P.ovf) P.nb_cnt[s] = W.cur;
