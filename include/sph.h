@@ -60,6 +60,8 @@ typedef enum {
 /* flags */
 #define SPH_F_SYNC 1u             /* synchronise at the end of each call (default on) */
 #define SPH_F_COUNT_CANDIDATES 2u /* count distance tests (stats.n_candidates) */
+#define SPH_F_DIAGNOSTICS 4u      /* count borderline and coincident pairs (stats.n_borderline,
+                                     n_borderline_force, n_coincident) */
 
 typedef struct {
   int32_t abi_version;   /* = SPH_ABI_VERSION */
@@ -110,6 +112,10 @@ typedef struct {         /* host struct, filled when non-NULL */
   double ms_kernel_walk_union;   /* interaction-list walks */
   int64_t n_nb_entries;          /* neighbour-list entries recorded (all walks) */
   int64_t n_walk_launches;       /* neighbour-list walk launches */
+  /* SPH_F_DIAGNOSTICS only (else 0), from the final density and force loops in fp32: */
+  int64_t n_borderline;          /* density (sph_density): directed (i, j), j != i, |r_ij/h_i - 1| <= 1e-6 (R5) */
+  int64_t n_borderline_force;    /* force (sph_force): unordered pairs, |r_ij/max(h_i,h_j) - 1| <= 1e-6 */
+  int64_t n_coincident;          /* density (sph_density): unordered pairs with r_ij = 0, i != j (R13) */
 } sph_stats;
 
 /* Fill *cfg with the paper's defaults for the given box. */

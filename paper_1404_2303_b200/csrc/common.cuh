@@ -99,6 +99,7 @@ __device__ __forceinline__ float3 dir_unit(int d) { return make_float3(c_dirs[d]
 #define SPH_MAX_DEPTH 12              // Morton levels below the top grid
 #define SPH_COLD_MARGIN 1.2f          // h_build / h when h0 is the occupancy guess
 #define SPH_REGROW_MARGIN 1.1f        // h_build / h after a Newton step left the list (tuned: tools/sweep.sh)
+#define SPH_BAND 1e-6f   // borderline band |r/h - 1| <= 1e-6 (north_star; R5)
 #define SPH_IDX_BITS 27               // list entry = (periodic image code << 27) | source index
 #define SPH_IDX_MASK ((1u << SPH_IDX_BITS) - 1u)
 #define SPH_GROUP 32                  // targets per group (one warp, one lane per target)
@@ -200,6 +201,9 @@ enum CounterId {
   C_HMAXBITS,       // max h (float bits as int)
   C_HMINBITS,       // min positive h (float bits)
   C_TMP0, C_TMP1, C_TMP2,
+  C_BORDER_D,       // SPH_F_DIAGNOSTICS: borderline directed density pairs
+  C_BORDER_F,       //   borderline directed force pairs
+  C_COINC,          //   coincident directed pairs (r = 0, j != i)
   C_NCOUNTERS
 };
 

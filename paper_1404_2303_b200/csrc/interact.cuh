@@ -40,7 +40,9 @@ struct DensOut {
   float* s2;      // sum q^2 f''      (second derivative of N for the Halley step)
 };
 
-template <bool NONLY>
+// DIAG: also count (O8) borderline directed pairs |r / h_i - 1| <= SPH_BAND and coincident
+// directed pairs (r = 0, j != i) into ctr[C_BORDER_D], ctr[C_COINC] (SPH_F_DIAGNOSTICS).
+template <bool NONLY, bool DIAG = false>
 __global__ void __launch_bounds__(DENS_WARPS * 32) k_density(GroupLists G, const float4* __restrict__ xh,
                                                              const float4* __restrict__ vm,
                                                              const uint32_t* __restrict__ perm, int64_t n_own,
@@ -78,7 +80,7 @@ __global__ void __launch_bounds__(DENS_WARPS * 32) k_density(GroupLists G, const
   double sf = 0.0;
   float sqfp = 0.f, sq2fpp = 0.f, smf = 0.f, smqfp = 0.f, divs = 0.f, crx = 0.f, cry = 0.f, crz = 0.f;
   int cnt = 0;
-  long long ncand = 0;
+  long long ncand = 0, nbord = 0, ncoin = 0;
   const int64_t off = G.off[gid];
   const int len = G.len[gid];
   float4* __restrict__ SP = sp[wib];
@@ -124,6 +126,16 @@ __global__ void __launch_bounds__(DENS_WARPS * 32) k_density(GroupLists G, const
         m |= ((unsigned)(r2.x < hi2) | ((unsigned)(r2.y < hi2) << 1)) << (2 * t);
       }
       hm[k] = m;
+    }
+    if (DIAG && act) {
+      // same r^2 as the hit loop; the band |r^2 - h^2| <= 2 SPH_BAND h^2 is |r/h - 1| <= SPH_BAND
+      for (int t = 0; t < 32 * DENS_ST; ++t) {
+        const float4 q = SP[t];
+        const float dx = xi - q.x, dy = yi - q.y, dz = zi - q.z;
+        const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+        nbord += fabsf(r2 - hi2) <= 2.f * SPH_BAND * hi2 ? 1 : 0;
+        ncoin += (r2 == 0.f && __float_as_int(SV[t].w) != s) ? 1 : 0;
+      }
     }
     // interaction body for this lane's hits
     while (true) {
@@ -172,6 +184,17 @@ __global__ void __launch_bounds__(DENS_WARPS * 32) k_density(GroupLists G, const
 #pragma unroll
   for (int o2 = 16; o2 > 0; o2 >>= 1) ncand += __shfl_xor_sync(FULL_MASK, ncand, o2);
   if (lane == 0 && ctr) atomicAdd(&ctr[C_CAND], (unsigned long long)ncand);
+  if (DIAG) {
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) {
+      nbord += __shfl_xor_sync(FULL_MASK, nbord, o2);
+      ncoin += __shfl_xor_sync(FULL_MASK, ncoin, o2);
+    }
+    if (lane == 0 && ctr) {
+      atomicAdd(&ctr[C_BORDER_D], (unsigned long long)nbord);
+      atomicAdd(&ctr[C_COINC], (unsigned long long)ncoin);
+    }
+  }
 }
 
 // ------------------------------------------------------------------ force --------
@@ -195,6 +218,8 @@ struct ForceOut {
 //   T = A_i G_i + A_j G_j + (1/4) Pi (f_i + f_j)(G_i + G_j),  G = W_r / r,
 //   a_i -= m_j T dx,  du_i += m_j (v_ij . dx) (A_i G_i + (1/8) Pi (f_i + f_j)(G_i + G_j)).
 // fx = {x, y, z, 1/h}; fs = {A (8/pi) h^-4, rho, c, f}; vm = {v, m}.
+// DIAG: also count borderline directed pairs |r / max(h_i, h_j) - 1| <= SPH_BAND (ctr[C_BORDER_F]).
+template <bool DIAG = false>
 __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(GroupLists G, const float4* __restrict__ fx,
                                                             const float4* __restrict__ vm,
                                                             const float4* __restrict__ fs, float alpha, float3 Lbox,
@@ -237,7 +262,7 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(GroupLists G, const 
   const float hhat = SPH_CNORM * h2i * h2i;
   float ax = 0.f, ay = 0.f, az = 0.f, du = 0.f, vsig = 0.f;
   int cnt = 0;
-  long long ncand = 0;
+  long long ncand = 0, nbord = 0;
   const int64_t off = G.off[gid];
   const int len = G.len[gid];
   float4* __restrict__ SA = sa[wib];
@@ -291,6 +316,16 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(GroupLists G, const 
         m |= ((unsigned)a0 | ((unsigned)a1 << 1)) << (2 * t);
       }
       hm[k] = act ? m : 0u;
+    }
+    if (DIAG && act) {
+      for (int t = 0; t < 32 * FORCE_ST; ++t) {
+        const float4 qa = SA[t];
+        if (SJ[t] < 0 || SJ[t] == s) continue;
+        const float dx = xi - qa.x, dy = yi - qa.y, dz = zi - qa.z;
+        const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+        const float hm = fmaxf(hi, 1.0f / qa.w), hm2 = hm * hm;
+        nbord += fabsf(r2 - hm2) <= 2.f * SPH_BAND * hm2 ? 1 : 0;
+      }
     }
     while (true) {
       int t = -1;
@@ -355,6 +390,11 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(GroupLists G, const 
   if (lane == 0 && ctr) {
     atomicAdd(&ctr[C_CAND], (unsigned long long)ncand);
     atomicAdd(&ctr[C_NFORCE], (unsigned long long)nf);
+  }
+  if (DIAG) {
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) nbord += __shfl_xor_sync(FULL_MASK, nbord, o2);
+    if (lane == 0 && ctr) atomicAdd(&ctr[C_BORDER_F], (unsigned long long)nbord);
   }
 }
 

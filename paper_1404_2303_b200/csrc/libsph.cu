@@ -1067,7 +1067,9 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   {
     DbgTimer _t(c, "density kernel");
     const GroupLists G = group_lists(c);
-    LAUNCH(k_density<false>, gridfull(G.ngroups, DENS_WARPS), DENS_WARPS * 32, 0, G, Bget<float4>(c, B_XH), vm,
+    const bool diag = (c->cfg.flags & SPH_F_DIAGNOSTICS) != 0;
+    auto kd = diag ? k_density<false, true> : k_density<false, false>;
+    LAUNCH(kd, gridfull(G.ngroups, DENS_WARPS), DENS_WARPS * 32, 0, G, Bget<float4>(c, B_XH), vm,
            Bget<uint32_t>(c, B_PERM), c->n_own, box3(c), dout, ctr(c));
   }
   CUDA_TRY(cudaEventRecord(c->ev[9], c->stream));
@@ -1096,6 +1098,7 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   ctr_read(c, hc);
   const long long ndir = (long long)hc[C_NDIR];
   const long long cand = (long long)hc[C_CAND];
+  const long long nbord_d = (long long)hc[C_BORDER_D], ncoinc = (long long)hc[C_COINC] / 2;
   const long long nbad = (long long)hc[C_UNCONV];
   if (c->n > c->n_own && c->cfg.halo_width > 0.0) {
     // every owned particle's partners must be inside the received halo
@@ -1122,6 +1125,8 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
     st->n_nb_entries = c->nb_entries;
     st->n_walk_launches = c->walk_launches;
     st->n_directed = ndir;
+    st->n_borderline = nbord_d;
+    st->n_coincident = ncoinc;
     st->n_candidates = cand;
     st->n_candidates_density_full = cand;
     st->n_unconverged = (noconv ? unconv : 0) + (noconv ? 0 : nbad);
@@ -1180,7 +1185,8 @@ int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out, int3
   CUDA_TRY(cudaEventRecord(c->ev[10], c->stream));
   {
     DbgTimer _t(c, "force kernel");
-    LAUNCH(k_force, gridfull(G.ngroups, FORCE_WARPS), FORCE_WARPS * 32, 0, G, Bget<float4>(c, B_FX),
+    auto kf = (c->cfg.flags & SPH_F_DIAGNOSTICS) ? k_force<true> : k_force<false>;
+    LAUNCH(kf, gridfull(G.ngroups, FORCE_WARPS), FORCE_WARPS * 32, 0, G, Bget<float4>(c, B_FX),
            Bget<float4>(c, B_VM), Bget<float4>(c, B_FS), c->cfg.alpha, box3(c), fo, ctr(c));
   }
   CUDA_TRY(cudaEventRecord(c->ev[11], c->stream));
@@ -1198,6 +1204,7 @@ int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out, int3
     st->ms_kernel_walk_union = c->ms_phase[2];
     st->n_pairs = (int64_t)(hc[C_NFORCE] / 2);
     st->n_candidates = (int64_t)hc[C_CAND];
+    st->n_borderline_force = (int64_t)(hc[C_BORDER_F] / 2);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, c->ev[4], c->ev[5]);
     st->ms_force = ms;

@@ -31,6 +31,7 @@ SPH_OK, SPH_E_ARG, SPH_E_DOMAIN, SPH_E_STATE, SPH_E_NOCONV, SPH_E_CUDA, SPH_E_NC
     0, -1, -2, -3, -4, -5, -6, -7)
 SPH_F_SYNC = 1
 SPH_F_COUNT_CANDIDATES = 2
+SPH_F_DIAGNOSTICS = 4
 ABI_VERSION = 1
 
 
@@ -57,7 +58,8 @@ class Stats(ctypes.Structure):
         ("ms_kernel_force", ctypes.c_double), ("n_candidates_density_full", ctypes.c_int64),
         ("ms_kernel_walk_nb", ctypes.c_double), ("ms_kernel_hsolve", ctypes.c_double),
         ("ms_kernel_walk_union", ctypes.c_double), ("n_nb_entries", ctypes.c_int64),
-        ("n_walk_launches", ctypes.c_int64),
+        ("n_walk_launches", ctypes.c_int64), ("n_borderline", ctypes.c_int64),
+        ("n_borderline_force", ctypes.c_int64), ("n_coincident", ctypes.c_int64),
     ]
 
     def as_dict(self):

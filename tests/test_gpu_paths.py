@@ -122,3 +122,30 @@ def test_repeated_calls_on_one_structure():
     assert torch.allclose(f2.a, a1, rtol=1e-4, atol=1e-6 * float(a1.abs().max()))
     assert torch.equal(f2.a, f3.a)
     ctx.close()
+
+
+@pytest.mark.parametrize("case", ["tiny_dups", "c1"])
+def test_diagnostic_counts(case):
+    """SPH_F_DIAGNOSTICS: coincident pairs (exact duplicates) equal the oracle's
+    count exactly; borderline pairs |r/h - 1| <= 1e-6 (density, h_i) and
+    |r/max(h_i,h_j) - 1| <= 1e-6 (force) agree with the oracle's fp64 counts at the GPU's h
+    up to pairs within fp32 rounding of the band edges."""
+    import paper_1404_2303_b200 as sph
+    if case == "tiny_dups":
+        p = workloads.tiny(8, n=3000, clump_frac=0.4, n_dup=25)
+        p.h0[:] = 0.0
+    else:
+        p = workloads.c1()
+    g = P.run_gpu(p, flags=sph.SPH_F_SYNC | sph.SPH_F_DIAGNOSTICS, **BENCH_CFG)
+    orc = P.oracle_given_h(p, g["h"])
+    sd, sf = g["stats_density"], g["stats_force"]
+    assert sd["n_coincident"] == int(orc["n_coincident"].sum()) // 2
+    if case == "tiny_dups":
+        assert sd["n_coincident"] > 0
+    nb_d, nb_f = int(orc["n_borderline"].sum()), int(orc["n_borderline_force"].sum()) // 2
+    assert abs(sd["n_borderline"] - nb_d) <= 2 + nb_d // 10, (sd["n_borderline"], nb_d)
+    assert abs(sf["n_borderline_force"] - nb_f) <= 2 + nb_f // 10, (sf["n_borderline_force"], nb_f)
+    # the diagnostic build computes the same results as the default one
+    g0 = P.run_gpu(p, **BENCH_CFG)
+    for k in ("h", "rho", "a", "dudt"):
+        assert np.array_equal(g[k], g0[k]), k
