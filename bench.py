@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-warm", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--transport", default="torch", choices=["torch", "libsph"],
+                    help="N > 1 halo exchange: torch.distributed P2P or libsph's NCCL communicator")
     return ap.parse_args()
 
 
@@ -391,7 +393,8 @@ def run_slab(args, rank, world, local_rank):
     cfg = sph.default_config(p.box, **CONFIG_TUNING, rank=rank, nranks=world, slab_lo=lo, slab_hi=hi,
                              halo_width=width)
     ctx = sph.Context(cfg, device=local_rank, stream=stream.cuda_stream)
-    tr = slab.DistTransport(rank, world)
+    # halo transport: torch.distributed P2P (NCCL) or libsph's own NCCL communicator
+    tr = slab.LibTransport(ctx, rank, world) if args.transport == "libsph" else slab.DistTransport(rank, world)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     def step(inputs):

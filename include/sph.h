@@ -175,8 +175,9 @@ int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out,
 
 /* ---- multi-GPU slab decomposition (the paper's proxy cells).
  * One process and one context per GPU; each rank owns the particles with x in its slab
- * [lo, hi). The transport (NCCL point-to-point over NVLink) is done by the caller, e.g.
- * through torch.distributed (paper_1404_2303_b200/slab.py); these calls do the device work.
+ * [lo, hi). The transport (NCCL point-to-point over NVLink) is either libsph's own
+ * (sph_comm_init, sph_halo_exchange below) or the caller's, e.g. torch.distributed
+ * (paper_1404_2303_b200/slab.py); the other calls do the device work.
  * Sequence per evaluation: sph_halo_select -> exchange x, v, m, u (+h0) of the selected
  * particles -> sph_build_cells_halo -> sph_density -> sph_export_state of the selected
  * particles -> exchange -> sph_import_halo_state -> sph_force. */
@@ -205,6 +206,35 @@ int sph_export_state(sph_ctx* ctx, int64_t k, const int32_t* idx, float* state_o
 
 /* Before sph_force: the halo particles' state [n_halo][5] (same layout, halo order). */
 int sph_import_halo_state(sph_ctx* ctx, const float* state);
+
+/* ---- NCCL transport of the slab ring. NCCL is loaded at run time
+ * (libnccl.so.2); SPH_E_NCCL if it is missing or a call fails. Rank r's neighbours are
+ * lower = r-1 and upper = r+1 (mod cfg.nranks). All buffers are device memory, enqueued on
+ * the context's stream (synchronised before return under SPH_F_SYNC); every rank of the
+ * communicator must make the same calls in the same order. */
+
+/* Rank 0: a new NCCL unique id (128 bytes) for sph_comm_init; broadcast it to the other ranks
+ * with any host transport (e.g. torch.distributed). */
+int sph_comm_unique_id(uint8_t* id_out);
+
+/* ncclCommInitRank(cfg.nranks, id, cfg.rank) on the context's device; collective. */
+int sph_comm_init(sph_ctx* ctx, const uint8_t* id);
+
+/* The counts of the next exchange: this rank sends n_lo rows to its lower and n_hi rows to
+ * its upper neighbour; returns the rows it will receive from each (host values). */
+int sph_halo_counts(sph_ctx* ctx, int64_t n_lo, int64_t n_hi, int64_t* m_lo, int64_t* m_hi);
+
+/* Ring exchange of fp32 rows of `cols` values: send_lo [n_lo][cols] -> lower neighbour,
+ * send_hi [n_hi][cols] -> upper neighbour; recv_lo [m_lo][cols] <- lower neighbour's send_hi,
+ * recv_hi [m_hi][cols] <- upper neighbour's send_lo (counts from sph_halo_counts). Used for
+ * the two halo exchanges of an evaluation: x, v, m, u, h0 of the sph_halo_select particles
+ * before sph_build_cells_halo, and the sph_export_state rows before sph_import_halo_state. */
+int sph_halo_exchange(sph_ctx* ctx, int32_t cols, const float* send_lo, int64_t n_lo, const float* send_hi,
+                      int64_t n_hi, float* recv_lo, int64_t m_lo, float* recv_hi, int64_t m_hi);
+
+/* In-place all-reduce of a device buffer over the communicator: dtype 0 = fp64, 1 = int64;
+ * op 0 = sum, 1 = max (slab-cut histograms, the global max h for the halo width). */
+int sph_allreduce(sph_ctx* ctx, void* buf, int64_t count, int32_t dtype, int32_t op);
 
 /* Histogram of x over [lo, hi) into nbins bins (for count-quantile slab cuts). */
 int sph_x_histogram(sph_ctx* ctx, int64_t n, const float* x, double lo, double hi, int32_t nbins,

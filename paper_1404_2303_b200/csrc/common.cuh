@@ -112,6 +112,7 @@ struct DBuf {
 
 struct sph_ctx {
   sph_config cfg;
+  void* comm = nullptr;   // ncclComm_t of the slab decomposition (sph_comm_init), or null
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;

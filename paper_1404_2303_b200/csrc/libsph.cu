@@ -14,6 +14,7 @@
 #include "build.cuh"
 #include "lists.cuh"
 #include "interact.cuh"
+#include "comm.cuh"
 
 // =========================================================== memory =============
 static void* dev_alloc(sph_ctx* c, size_t bytes) {
@@ -821,6 +822,7 @@ int sph_destroy(sph_ctx* c) {
     cudaEventDestroy(t.b);
   }
   if (c->own_stream) cudaStreamDestroy(c->stream);
+  if (c->comm) nccl().CommDestroy((ncclComm_t)c->comm);
   delete c;
   return SPH_OK;
 }
@@ -1315,3 +1317,94 @@ int sph_x_histogram(sph_ctx* ctx, int64_t n, const float* x, double lo, double h
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ NCCL transport ---
+// The ring of slabs: rank r exchanges with lower = r - 1 and upper = r + 1
+// (mod nranks). Messages to one peer match in posting order, so a rank sends its upper face
+// first and receives its lower halo first: with nranks <= 2 (one peer on both sides, or the
+// rank itself) the upper face of the lower neighbour still lands in the lower halo.
+
+int sph_comm_unique_id(uint8_t* id_out) {
+  if (!id_out) return SPH_E_ARG;
+  if (!nccl().ok) return SPH_E_NCCL;
+  ncclUniqueId id;
+  if (nccl().GetUniqueId(&id) != ncclSuccess) return SPH_E_NCCL;
+  memcpy(id_out, id.internal, NCCL_UNIQUE_ID_BYTES);
+  return SPH_OK;
+}
+
+int sph_comm_init(sph_ctx* ctx, const uint8_t* id) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(id != nullptr, SPH_E_ARG, "id == NULL");
+  SPH_REQUIRE(c->cfg.nranks >= 1 && c->cfg.rank >= 0 && c->cfg.rank < c->cfg.nranks, SPH_E_ARG,
+              "cfg.rank / cfg.nranks out of range");
+  SPH_REQUIRE(c->comm == nullptr, SPH_E_STATE, "communicator already initialised");
+  SPH_REQUIRE(nccl().ok, SPH_E_NCCL, nccl().why);
+  ncclUniqueId uid;
+  memcpy(uid.internal, id, NCCL_UNIQUE_ID_BYTES);
+  ncclComm_t comm = nullptr;
+  NCCL_TRY(nccl().CommInitRank(&comm, c->cfg.nranks, uid, c->cfg.rank));
+  c->comm = comm;
+  API_END
+  return SPH_OK;
+}
+
+static void ring_exchange(sph_ctx* c, const void* s_lo, size_t n_lo, const void* s_hi, size_t n_hi, void* r_lo,
+                          size_t m_lo, void* r_hi, size_t m_hi, ncclDataType_t t) {
+  const int P = c->cfg.nranks, r = c->cfg.rank;
+  const int lower = (r - 1 + P) % P, upper = (r + 1) % P;
+  ncclComm_t comm = (ncclComm_t)c->comm;
+  NCCL_TRY(nccl().GroupStart());
+  if (n_hi) NCCL_TRY(nccl().Send(s_hi, n_hi, t, upper, comm, c->stream));
+  if (n_lo) NCCL_TRY(nccl().Send(s_lo, n_lo, t, lower, comm, c->stream));
+  if (m_lo) NCCL_TRY(nccl().Recv(r_lo, m_lo, t, lower, comm, c->stream));
+  if (m_hi) NCCL_TRY(nccl().Recv(r_hi, m_hi, t, upper, comm, c->stream));
+  NCCL_TRY(nccl().GroupEnd());
+}
+
+int sph_halo_counts(sph_ctx* ctx, int64_t n_lo, int64_t n_hi, int64_t* m_lo, int64_t* m_hi) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(c->comm != nullptr, SPH_E_STATE, "sph_halo_counts before sph_comm_init");
+  SPH_REQUIRE(n_lo >= 0 && n_hi >= 0 && m_lo && m_hi, SPH_E_ARG, "bad argument");
+  int64_t* d = B<int64_t>(c, B_TMPL0, 4);
+  const int64_t h[2] = {n_lo, n_hi};
+  CUDA_TRY(cudaMemcpyAsync(d, h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
+  ring_exchange(c, d, 1, d + 1, 1, d + 2, 1, d + 3, 1, ncclInt64);
+  int64_t got[2];
+  CUDA_TRY(cudaMemcpyAsync(got, d + 2, sizeof(got), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  *m_lo = got[0];
+  *m_hi = got[1];
+  API_END
+  return SPH_OK;
+}
+
+int sph_halo_exchange(sph_ctx* ctx, int32_t cols, const float* send_lo, int64_t n_lo, const float* send_hi,
+                      int64_t n_hi, float* recv_lo, int64_t m_lo, float* recv_hi, int64_t m_hi) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(c->comm != nullptr, SPH_E_STATE, "sph_halo_exchange before sph_comm_init");
+  SPH_REQUIRE(cols > 0 && n_lo >= 0 && n_hi >= 0 && m_lo >= 0 && m_hi >= 0, SPH_E_ARG, "bad argument");
+  const void* ptrs[4] = {send_lo, send_hi, recv_lo, recv_hi};
+  const int64_t cnt[4] = {n_lo, n_hi, m_lo, m_hi};
+  for (int k = 0; k < 4; ++k)
+    if (cnt[k] > 0)
+      SPH_REQUIRE(ptrs[k] && is_device_ptr(ptrs[k]), SPH_E_ARG, "halo buffers must be device memory");
+  ring_exchange(c, send_lo, (size_t)n_lo * cols, send_hi, (size_t)n_hi * cols, recv_lo, (size_t)m_lo * cols, recv_hi,
+                (size_t)m_hi * cols, ncclFloat32);
+  if (c->cfg.flags & SPH_F_SYNC) sync(c);
+  API_END
+  return SPH_OK;
+}
+
+int sph_allreduce(sph_ctx* ctx, void* buf, int64_t count, int32_t dtype, int32_t op) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(c->comm != nullptr, SPH_E_STATE, "sph_allreduce before sph_comm_init");
+  SPH_REQUIRE(count >= 0 && (dtype == 0 || dtype == 1) && (op == 0 || op == 1), SPH_E_ARG, "bad argument");
+  if (count == 0) return SPH_OK;
+  SPH_REQUIRE(buf && is_device_ptr(buf), SPH_E_ARG, "buffer must be device memory");
+  NCCL_TRY(nccl().AllReduce(buf, buf, (size_t)count, dtype == 0 ? ncclFloat64 : ncclInt64, op == 0 ? ncclSum : ncclMax,
+                            (ncclComm_t)c->comm, c->stream));
+  if (c->cfg.flags & SPH_F_SYNC) sync(c);
+  API_END
+  return SPH_OK;
+}

@@ -110,6 +110,34 @@ class DistTransport:
         return t
 
 
+class LibTransport:
+    """The same ring exchange through libsph's own NCCL communicator (sph_comm_init,
+    sph_halo_exchange, sph_allreduce): the data path stays inside the C ABI; torch.distributed
+    only broadcasts the NCCL unique id. `ctx` is this rank's Context (cfg.rank, cfg.nranks)."""
+
+    def __init__(self, ctx, rank: int, world: int, group=None):
+        import torch
+        import torch.distributed as dist
+        self.ctx, self.rank, self.world = ctx, rank, world
+        self.lower, self.upper = neighbours(rank, world)
+        obj = [ctx.comm_unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0, group=group)
+        ctx.comm_init(obj[0])
+        self.device = torch.device("cuda", torch.cuda.current_device())
+
+    def exchange(self, send_lo, send_hi):
+        return self.ctx.halo_exchange(send_lo.contiguous(), send_hi.contiguous())
+
+    def allreduce_max(self, value: float) -> float:
+        import torch
+        t = torch.tensor([value], dtype=torch.float64, device=self.device)
+        return float(self.ctx.allreduce_(t, "max").item())
+
+    def allreduce_sum(self, t):
+        return self.ctx.allreduce_(t, "sum")
+
+
 PACK_COLS = 9   # x(3) v(3) m u h0
 
 

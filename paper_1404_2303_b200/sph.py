@@ -70,7 +70,8 @@ class Stats(ctypes.Structure):
 EXPORTS = ("sph_config_default", "sph_create", "sph_destroy", "sph_set_allocator",
            "sph_status_string", "sph_last_error", "sph_build_cells", "sph_density", "sph_force",
            "sph_kernel_launches", "sph_build_cells_halo", "sph_halo_select", "sph_export_state",
-           "sph_import_halo_state", "sph_x_histogram", "sph_guess_h")
+           "sph_import_halo_state", "sph_x_histogram", "sph_guess_h", "sph_comm_unique_id", "sph_comm_init",
+           "sph_halo_counts", "sph_halo_exchange", "sph_allreduce")
 
 
 def load(path: str | None = None):
@@ -103,6 +104,11 @@ def load(path: str | None = None):
     lib.sph_import_halo_state.argtypes = [P, P]
     lib.sph_x_histogram.argtypes = [P, i64, P, ctypes.c_double, ctypes.c_double, ctypes.c_int32, P]
     lib.sph_guess_h.argtypes = [P, i64, P, P]
+    lib.sph_comm_unique_id.argtypes = [P]
+    lib.sph_comm_init.argtypes = [P, P]
+    lib.sph_halo_counts.argtypes = [P, i64, i64, P, P]
+    lib.sph_halo_exchange.argtypes = [P, ctypes.c_int32, P, i64, P, i64, P, i64, P, i64]
+    lib.sph_allreduce.argtypes = [P, P, i64, ctypes.c_int32, ctypes.c_int32]
     if path == LIB or path is None:
         _lib = lib
     return lib
@@ -240,6 +246,44 @@ class Context:
         self._check(self.lib.sph_x_histogram(self.h, n, _ptr(x) if n else None, float(lo), float(hi), int(nbins),
                                              _ptr(out, np.int64)))
         return out
+
+    # -- NCCL transport of the slab ring (include/sph.h) ------------------------------
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        buf = (ctypes.c_uint8 * 128)()
+        st = load().sph_comm_unique_id(buf)
+        if st != SPH_OK:
+            raise SphError(st, "sph_comm_unique_id: " + load().sph_status_string(st).decode())
+        return bytes(buf)
+
+    def comm_init(self, uid: bytes):
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        self._check(self.lib.sph_comm_init(self.h, buf))
+
+    def halo_exchange(self, send_lo, send_hi):
+        """send_lo [n_lo, w] -> lower neighbour, send_hi [n_hi, w] -> upper neighbour (device
+        float32); returns (rows from the lower neighbour, rows from the upper neighbour)."""
+        import torch
+        w = int(send_lo.shape[1])
+        m = np.zeros(2, dtype=np.int64)
+        self._check(self.lib.sph_halo_counts(self.h, int(send_lo.shape[0]), int(send_hi.shape[0]), m.ctypes.data,
+                                             m.ctypes.data + 8))
+        r_lo = torch.empty(int(m[0]), w, dtype=torch.float32, device=send_lo.device)
+        r_hi = torch.empty(int(m[1]), w, dtype=torch.float32, device=send_lo.device)
+        p = lambda t: _ptr(t) if t.shape[0] else None
+        self._check(self.lib.sph_halo_exchange(self.h, w, p(send_lo), int(send_lo.shape[0]), p(send_hi),
+                                               int(send_hi.shape[0]), p(r_lo), int(m[0]), p(r_hi), int(m[1])))
+        return r_lo, r_hi
+
+    def allreduce_(self, t, op: str = "sum"):
+        """In-place all-reduce of a device float64 / int64 tensor (op "sum" or "max")."""
+        import torch
+        dt = {torch.float64: 0, torch.int64: 1}[t.dtype]
+        if not t.is_contiguous():
+            raise TypeError("expected a contiguous tensor")
+        self._check(self.lib.sph_allreduce(self.h, t.data_ptr() if t.numel() else None, int(t.numel()), dt,
+                                           {"sum": 0, "max": 1}[op]))
+        return t
 
     def density(self, v, m, u, out=None, stats: Stats | None = None, check=True):
         """out: dict of preallocated output arrays (h, rho, omega, n_nbr, div, curl)."""
