@@ -41,6 +41,9 @@
 #define WALK_CAP 384    // frontier entries (node | image code << 27), LIFO
 #define WALK_DFS 112    // room for the depth-first fallback above the frontier
 #define WALK_RQ 64      // queued leaf ranges streamed together
+#ifndef SPHERE_VOTE
+#define SPHERE_VOTE 8   // node-vs-target-sphere tests between warp votes for an early exit
+#endif
 
 #define MODE_NB 0
 #define MODE_COUNT 1
@@ -231,13 +234,18 @@ __device__ __forceinline__ bool node_in_spheres(const WalkParams& P, const WalkS
     if (MODE != MODE_NB) hmn = P.N.hmax[node];
   }
   bool hit = false;
-  for (int t = 0; t < W.ntg; ++t) {
-    const float4 q = S.tgt[t];
-    const float gx = fmaxf(fmaxf(lo.x - q.x, q.x - hi.x), 0.f);
-    const float gy = fmaxf(fmaxf(lo.y - q.y, q.y - hi.y), 0.f);
-    const float gz = fmaxf(fmaxf(lo.z - q.z, q.z - hi.z), 0.f);
-    const float rr = MODE == MODE_NB ? q.w : fmaxf(q.w, reach_eff(hmn, P.slack));
-    hit |= fmaf(gx, gx, fmaf(gy, gy, gz * gz)) < rr * rr;
+  for (int t0 = 0; t0 < W.ntg; t0 += SPHERE_VOTE) {
+#pragma unroll
+    for (int k = 0; k < SPHERE_VOTE; ++k) {
+      const int t = min(t0 + k, W.ntg - 1);   // (a repeated last target is harmless)
+      const float4 q = S.tgt[t];
+      const float gx = fmaxf(fmaxf(lo.x - q.x, q.x - hi.x), 0.f);
+      const float gy = fmaxf(fmaxf(lo.y - q.y, q.y - hi.y), 0.f);
+      const float gz = fmaxf(fmaxf(lo.z - q.z, q.z - hi.z), 0.f);
+      const float rr = MODE == MODE_NB ? q.w : fmaxf(q.w, reach_eff(hmn, P.slack));
+      hit |= fmaf(gx, gx, fmaf(gy, gy, gz * gz)) < rr * rr;
+    }
+    if (__all_sync(FULL_MASK, hit || !coarse)) break;   // every kept node already hit
   }
   return coarse && hit;
 }
