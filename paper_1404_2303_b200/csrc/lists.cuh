@@ -41,6 +41,9 @@
 #define WALK_CAP 384    // frontier entries (node | image code << 27), LIFO
 #define WALK_DFS 112    // room for the depth-first fallback above the frontier
 #define WALK_RQ 64      // queued leaf ranges streamed together
+#ifndef SPH_INWALK_PASSES
+#define SPH_INWALK_PASSES 6   // NB walk passes per group and launch (re-walks without a host round)
+#endif
 #ifndef SPHERE_VOTE
 #define SPHERE_VOTE 8   // node-vs-target-sphere tests between warp votes for an early exit
 #endif
@@ -419,6 +422,14 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkParams P) {
     if (MODE != MODE_NB && lane == 0 && !P.check) P.len[gid] = 0;
     return;
   }
+  // NB + solve: a target whose root lies beyond its new list is walked again right here
+  // (up to SPH_INWALK_PASSES passes) instead of waiting for a host round
+  HLane H;
+  H.h = H.hbs = H.l = H.u = 0.f;
+  H.st = HS_DONE;
+  H.it = 0;
+  int nb_tot = 0;
+  for (int pass = 0;; ++pass) {
   W.lo = make_float3(warp_min_f(tg ? W.xi : INFINITY), warp_min_f(tg ? W.yi : INFINITY),
                      warp_min_f(tg ? W.zi : INFINITY));
   W.hi = make_float3(warp_max_f(tg ? W.xi : -INFINITY), warp_max_f(tg ? W.yi : -INFINITY),
@@ -565,19 +576,19 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkParams P) {
              gid, W.ntg, W.R, W.hi.x - W.lo.x, W.hi.y - W.lo.y, W.hi.z - W.lo.z, (int)W.spheres, W.raw, mc);
   }
 #endif
+  if (MODE == MODE_NB && !P.ovf) nb_tot += tg ? min(W.cur, P.K) : 0;
   if (MODE == MODE_NB && P.solve) {
     // fused h iteration on the list just recorded (still in L1/L2): first overflow of K ->
     // shrink h_build; repeat overflow -> exact list in the pool (k_hsolve_pool)
     const int cnt = W.cur;
     bool act = tg;
-    HLane H;
-    H.h = H.hbs = H.l = H.u = 0.f;
-    H.st = HS_DONE;
     if (tg) {
-      H.h = P.xh[s].w;
+      if (pass == 0) {
+        H.h = P.xh[s].w;
+        H.l = P.lo[s];
+        H.u = P.hi[s];
+      }
       H.hbs = W.ri;
-      H.l = P.lo[s];
-      H.u = P.hi[s];
       const bool over = cnt > P.K;
       if (over && P.shrunk[s]) {
         H.st = HS_OVF;
@@ -598,6 +609,13 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkParams P) {
       P.lo[s] = H.l;
       P.hi[s] = H.u;
       P.state[s] = H.st;
+      P.nb_cnt[s] = cnt;
+    }
+    const bool again = tg && H.st == HS_REGROW && pass + 1 < SPH_INWALK_PASSES;
+    if (__any_sync(FULL_MASK, again)) {
+      tg = again;
+      W.ri = again ? H.hbs : -1.f;
+      continue;
     }
     hsolve_count(tg, H, P.hc);
     if (P.rg_out) {
@@ -605,10 +623,12 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkParams P) {
       if (rg && lane == 0) P.rg_out[atomicAdd(P.rg_cnt, 1)] = gid;
     }
   }
+  break;
+  }   // passes
   if (MODE == MODE_NB) {
-    if (tg && !P.ovf) P.nb_cnt[s] = W.cur;
+    if (tg && !P.ovf && !P.solve) P.nb_cnt[s] = W.cur;
     if (!P.ovf && P.nb_entries) {
-      const int tot = warp_sum_i(tg ? min(W.cur, P.K) : 0);
+      const int tot = warp_sum_i(nb_tot);
       if (lane == 0 && tot) atomicAdd(P.nb_entries, (unsigned long long)tot);
     } else if (P.ovf && P.nb_entries) {
       const int tot = warp_sum_i(tg ? W.cur : 0);
