@@ -162,16 +162,22 @@ __device__ __forceinline__ void emit_chunk(const WalkParams& P, WalkState& W, Wa
     if (W.ri >= 0.f) {
       const float ri = reach_eff(W.ri, 0.f);
       const float ri2 = ri * ri;
+      // running write pointer: the pool list is contiguous, the slab column strided by gz
+      const int step = P.ovf ? 1 : W.gz;
+      const int lim = P.ovf ? INT_MAX : P.K;
+      float* wp = P.ovf ? P.ovf + W.base + W.cur : P.nb_r2 + W.base + (int64_t)W.cur * W.gz;
+      int cur = W.cur;
       for (int t = 0; t < m; ++t) {
         const float4 q = S.s[t];
         const float dx = W.xi - q.x, dy = W.yi - q.y, dz = W.zi - q.z;
         const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
         if (r2 < ri2) {
-          if (P.ovf) P.ovf[W.base + W.cur] = r2;
-          else if (W.cur < P.K) P.nb_r2[W.base + (int64_t)W.cur * W.gz] = r2;
-          ++W.cur;
+          if (cur < lim) *wp = r2;
+          wp += step;
+          ++cur;
         }
       }
+      W.cur = cur;
     }
     __syncwarp();
     return;
