@@ -48,10 +48,12 @@ __device__ __forceinline__ float spline_fp(float q) {
 __device__ __forceinline__ void nsums(const float* r2l, int64_t stride, int e0, int e1, int estep,
                                       float hinv, double& S0, float& S1, float& S2) {
   int e = e0;
-  for (; e + (NSUMS_UNROLL - 1) * estep < e1; e += NSUMS_UNROLL * estep) {
+  const int64_t d = (int64_t)estep * stride;   // running pointer (no 64-bit product per load)
+  const float* rp = r2l + (int64_t)e0 * stride;
+  for (; e + (NSUMS_UNROLL - 1) * estep < e1; e += NSUMS_UNROLL * estep, rp += NSUMS_UNROLL * d) {
     float r2[NSUMS_UNROLL];
 #pragma unroll
-    for (int k = 0; k < NSUMS_UNROLL; ++k) r2[k] = r2l[(int64_t)(e + k * estep) * stride];
+    for (int k = 0; k < NSUMS_UNROLL; ++k) r2[k] = rp[k * d];
 #pragma unroll
     for (int k = 0; k < NSUMS_UNROLL; ++k) {
       const float q = fminf(r2[k] * rsqrtf(fmaxf(r2[k], 1e-37f)) * hinv, 1.f);
@@ -62,8 +64,8 @@ __device__ __forceinline__ void nsums(const float* r2l, int64_t stride, int e0, 
       S2 = fmaf(q * q, fpp, S2);
     }
   }
-  for (; e < e1; e += estep) {
-    const float r2 = r2l[(int64_t)e * stride];
+  for (; e < e1; e += estep, rp += d) {
+    const float r2 = *rp;
     const float q = fminf(r2 * rsqrtf(fmaxf(r2, 1e-37f)) * hinv, 1.f);
     float f, fp, fpp;
     spline(q, f, fp, fpp);
