@@ -75,6 +75,35 @@ __device__ __forceinline__ void nsums(const float* r2l, int64_t stride, int e0, 
   }
 }
 
+// nsums for a contiguous, 16-byte aligned list (the per-particle rows of the slab): float4
+// reads, same summation order as nsums.
+__device__ __forceinline__ void nsums_row(const float* r2l, int e1, float hinv, double& S0, float& S1, float& S2) {
+  const float4* r4 = reinterpret_cast<const float4*>(r2l);
+  int e = 0;
+  for (; e + 3 < e1; e += 4) {
+    const float4 v = r4[e >> 2];
+    const float r2[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float q = fminf(r2[k] * rsqrtf(fmaxf(r2[k], 1e-37f)) * hinv, 1.f);
+      float f, fp, fpp;
+      spline(q, f, fp, fpp);
+      S0 += (double)f;
+      S1 = fmaf(q, fp, S1);
+      S2 = fmaf(q * q, fpp, S2);
+    }
+  }
+  for (; e < e1; ++e) {
+    const float r2 = r2l[e];
+    const float q = fminf(r2 * rsqrtf(fmaxf(r2, 1e-37f)) * hinv, 1.f);
+    float f, fp, fpp;
+    spline(q, f, fp, fpp);
+    S0 += (double)f;
+    S1 = fmaf(q, fp, S1);
+    S2 = fmaf(q * q, fpp, S2);
+  }
+}
+
 // One Newton/Halley update from the sums at h. Returns the new state: HS_DONE (converged),
 // HS_ACTIVE (h updated, iterate), HS_REGROW (the new h lies beyond h_build).
 __device__ __forceinline__ uint8_t hstep(double S0, float S1, float S2, float& h, float& hbs, float& l, float& u,
@@ -157,7 +186,10 @@ __device__ __forceinline__ void warp_hsolve(bool act, const float* r2l, int64_t 
     for (; H.it < max_iter && H.st == HS_ACTIVE; ++H.it) {
       double S0 = 0.0;
       float S1 = 0.f, S2 = 0.f;
-      nsums(r2l, stride, 0, cnt, 1, 1.0f / H.h, S0, S1, S2);
+      if (stride == 1 && ((reinterpret_cast<uintptr_t>(r2l) & 15) == 0))
+        nsums_row(r2l, cnt, 1.0f / H.h, S0, S1, S2);
+      else
+        nsums(r2l, stride, 0, cnt, 1, 1.0f / H.h, S0, S1, S2);
       H.st = hstep(S0, S1, S2, H.h, H.hbs, H.l, H.u, n_t, tol, margin, hcap);
       if (H.st == HS_REGROW) ++H.it;
     }

@@ -441,7 +441,8 @@ __global__ void __launch_bounds__(HSOLVE_WARPS * 32) k_hsolve(const int4* __rest
     H.l = lo_a[s];
     H.u = hi_a[s];
   }
-  warp_hsolve(act, nb_r2 + (int64_t)grp.y * K + lane, grp.z, cnt, K, false, false, H, n_t, tol, margin, hcap,
+  warp_hsolve(act, nb_r2 + (NB_ROWS ? (int64_t)s * K : (int64_t)grp.y * K + lane), NB_ROWS ? 1 : grp.z, cnt, K, false,
+              false, H, n_t, tol, margin, hcap,
               max_iter);
   if (act) {
     xh[s].w = H.h;

@@ -797,7 +797,7 @@ int sph_create(const sph_config* cfg, int dev, void* stream, sph_ctx** out) {
     // tuning overrides for experiments; defaults otherwise
     if (const char* e = getenv("SPH_COLD_MARGIN")) c->cold_margin = (float)atof(e);
     if (const char* e = getenv("SPH_REGROW_MARGIN")) c->regrow_margin = (float)atof(e);
-    if (const char* e = getenv("SPH_NBK")) c->nb_k = atoi(e);
+    if (const char* e = getenv("SPH_NBK")) c->nb_k = std::max(4, atoi(e) & ~3);
     if (const char* e = getenv("SPH_UCAP")) c->ucap = atoi(e);
   } catch (const SphError& e) {
     delete c;
@@ -884,6 +884,7 @@ int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const floa
     CUDA_TRY(cudaMemGetInfo(&fr, &tot));
     const size_t have = fr + c->b[B_NBR2].bytes;   // the slab of a previous build is reused
     c->nb_k = (int)std::max<int64_t>(64, std::min<int64_t>(1024, (int64_t)(0.4 * (double)have / (4.0 * (double)n))));
+    c->nb_k &= ~3;   // rows of K floats stay 16-byte aligned (float4 reads in the h sums)
     c->nb_k_for = n;
   }
   c->pool = 0;

@@ -44,6 +44,9 @@
 #ifndef SPH_INWALK_PASSES
 #define SPH_INWALK_PASSES 6   // NB walk passes per group and launch (re-walks without a host round)
 #endif
+#ifndef NB_ROWS
+#define NB_ROWS 1       // neighbour-list slab: one contiguous row of K per particle (0: column-interleaved per group)
+#endif
 #ifndef SPHERE_VOTE
 #define SPHERE_VOTE 8   // node-vs-target-sphere tests between warp votes for an early exit
 #endif
@@ -163,9 +166,9 @@ __device__ __forceinline__ void emit_chunk(const WalkParams& P, WalkState& W, Wa
       const float ri = reach_eff(W.ri, 0.f);
       const float ri2 = ri * ri;
       // running write pointer: the pool list is contiguous, the slab column strided by gz
-      const int step = P.ovf ? 1 : W.gz;
+      const int step = (P.ovf || NB_ROWS) ? 1 : W.gz;
       const int lim = P.ovf ? INT_MAX : P.K;
-      float* wp = P.ovf ? P.ovf + W.base + W.cur : P.nb_r2 + W.base + (int64_t)W.cur * W.gz;
+      float* wp = P.ovf ? P.ovf + W.base + W.cur : P.nb_r2 + W.base + (int64_t)W.cur * step;
       int cur = W.cur;
       for (int t = 0; t < m; ++t) {
         const float4 q = S.s[t];
@@ -464,7 +467,11 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkParams P) {
   }
   W.cur = 0;
   W.raw = 0;
+#if NB_ROWS
+  W.base = MODE == MODE_FILL ? P.off[gid] : (MODE == MODE_NB ? (int64_t)s * P.K : 0);
+#else
   W.base = MODE == MODE_FILL ? P.off[gid] : (MODE == MODE_NB ? (int64_t)grp.y * P.K + lane : 0);
+#endif
   if (MODE == MODE_NB && P.ovf && tg) W.base = P.ovf_off[s];
   int nq = 0;
   if (__any_sync(FULL_MASK, tg)) {
@@ -614,7 +621,8 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkParams P) {
       }
     }
     __syncwarp();   // the lists recorded by every lane are visible to the cooperative sums
-    warp_hsolve(act, P.nb_r2 + (int64_t)grp.y * P.K + lane, W.gz, cnt, P.K, false, true, H, P.n_t, P.tol, P.margin,
+    warp_hsolve(act, P.nb_r2 + (NB_ROWS ? (int64_t)s * P.K : (int64_t)grp.y * P.K + lane), NB_ROWS ? 1 : W.gz, cnt, P.K,
+                false, true, H, P.n_t, P.tol, P.margin,
                 P.hcap, P.max_iter);
     if (tg) {
       reinterpret_cast<float*>(const_cast<float4*>(P.xh) + s)[3] = H.h;
