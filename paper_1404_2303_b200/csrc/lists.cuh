@@ -459,7 +459,15 @@ __global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkParams P) {
     // reach is uneven or its targets are spread wider than their reach
     const unsigned tb = __ballot_sync(FULL_MASK, tg);
     W.ntg = __popc(tb);
-    if (tg) S.tgt[__popc(tb & lanemask_lt())] = make_float4(W.xi, W.yi, W.zi, reach_eff(W.ri, P.slack));
+    if (tg) {
+      // stored in a stride-4 interleave of the (Morton-ordered) targets, so the first ones
+      // tested span the group and a reached node usually meets a hit within the first vote
+      const int pidx = __popc(tb & lanemask_lt()), q4 = (W.ntg + 3) >> 2;
+      const int r4 = pidx & 3, c4 = pidx >> 2;
+      const int full = W.ntg - 4 * (q4 - 1);   // rows 0..full-1 hold q4 entries, the rest q4 - 1
+      const int slot = r4 < full ? r4 * q4 + c4 : full * q4 + (r4 - full) * (q4 - 1) + c4;
+      S.tgt[slot] = make_float4(W.xi, W.yi, W.zi, reach_eff(W.ri, P.slack));
+    }
     __syncwarp();
     const float rmin = warp_min_f(tg ? W.ri : INFINITY);
     const float dx = W.hi.x - W.lo.x, dy = W.hi.y - W.lo.y, dz = W.hi.z - W.lo.z;
