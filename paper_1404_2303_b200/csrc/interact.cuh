@@ -220,7 +220,10 @@ struct ForceOut {
 // fx = {x, y, z, 1/h}; fs = {A (8/pi) h^-4, rho, c, f}; vm = {v, m}.
 // DIAG: also count borderline directed pairs |r / max(h_i, h_j) - 1| <= SPH_BAND (ctr[C_BORDER_F]).
 template <bool DIAG = false>
-__global__ void __launch_bounds__(FORCE_WARPS * 32) k_force(GroupLists G, const float4* __restrict__ fx,
+#ifndef FORCE_MINB
+#define FORCE_MINB 8    // 8 blocks of 4 warps: <= 64 registers, 32 resident warps
+#endif
+__global__ void __launch_bounds__(FORCE_WARPS * 32, FORCE_MINB) k_force(GroupLists G, const float4* __restrict__ fx,
                                                             const float4* __restrict__ vm,
                                                             const float4* __restrict__ fs, float alpha, float3 Lbox,
                                                             ForceOut out, unsigned long long* ctr) {
