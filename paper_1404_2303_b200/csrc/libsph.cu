@@ -181,21 +181,8 @@ static void radix_sort(sph_ctx* c, uint64_t*& keys, uint32_t*& vals, uint64_t*& 
   uint32_t* hist = B<uint32_t>(c, B_SORT_HIST, 16 * 256);
   CUDA_TRY(cudaMemsetAsync(hist, 0, 8 * 256 * sizeof(uint32_t), c->stream));
   LAUNCH(k_radix_hist, grid1d(c, n, 256), 256, 0, keys, n, npass, hist);
-  uint32_t h[8 * 256], g[8 * 256];
-  CUDA_TRY(cudaMemcpyAsync(h, hist, npass * 256 * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
-  sync(c);
-  bool trivial[8];
-  for (int p = 0; p < npass; ++p) {
-    uint32_t run = 0;
-    trivial[p] = false;
-    for (int d = 0; d < 256; ++d) {
-      g[p * 256 + d] = run;
-      run += h[p * 256 + d];
-      if (h[p * 256 + d] == (uint32_t)n) trivial[p] = true;
-    }
-  }
   uint32_t* gofs = hist + 8 * 256;
-  CUDA_TRY(cudaMemcpyAsync(gofs, g, npass * 256 * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
+  LAUNCH(k_radix_offsets, npass, 256, 0, hist, gofs);
   int64_t ntiles = (n + RS_TILE - 1) / RS_TILE;
   uint32_t* status = B<uint32_t>(c, B_SORT_STATUS, ntiles * 256);
   uint32_t* tctr = B<uint32_t>(c, B_SORT_CTR, 8);
@@ -205,14 +192,12 @@ static void radix_sort(sph_ctx* c, uint64_t*& keys, uint32_t*& vals, uint64_t*& 
   }
   CUDA_TRY(cudaMemsetAsync(tctr, 0, 8 * sizeof(uint32_t), c->stream));
   for (int p = 0; p < npass; ++p) {
-    if (trivial[p]) continue;
     CUDA_TRY(cudaMemsetAsync(status, 0, ntiles * 256 * sizeof(uint32_t), c->stream));
     LAUNCH(k_radix_pass, (int)ntiles, RS_THREADS, sizeof(RadixSmem), keys, vals, kalt, valt, n, 8 * p,
            gofs + 256 * p, status, tctr + p);
     std::swap(keys, kalt);
     std::swap(vals, valt);
   }
-  sync(c);  // the host arrays h/g above are stack buffers used by async copies
 }
 
 // =========================================================== nodes ==============

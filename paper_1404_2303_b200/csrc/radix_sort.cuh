@@ -4,8 +4,8 @@
 // single read of the keys; each 8-bit pass is then ONE kernel: tiles of 4096 items
 // ranked in-warp with __match_any_sync (stable), tile digit counts published with a
 // decoupled look-back (per-digit status words), items staged in shared memory in
-// digit order and written out in coalesced digit runs. Passes whose digit is constant
-// over all keys are skipped (known from the histogram).
+// digit order and written out in coalesced digit runs. Digit offsets are scanned on the
+// device (k_radix_offsets); every pass runs, so the sort has no host round trip.
 #pragma once
 #include "common.cuh"
 
@@ -32,6 +32,23 @@ __global__ void __launch_bounds__(256) k_radix_hist(const uint64_t* __restrict__
     uint32_t c = (&sh[0][0])[i];
     if (c) atomicAdd(&hist[i], c);
   }
+}
+
+// exclusive prefix of each pass's 256 digit counts (block p = pass p): the global digit
+// offsets, computed on the device so the sort needs no host round trip
+__global__ void __launch_bounds__(256) k_radix_offsets(const uint32_t* __restrict__ hist, uint32_t* __restrict__ gofs) {
+  __shared__ uint32_t s[256];
+  const int p = blockIdx.x, d = threadIdx.x;
+  const uint32_t v = hist[p * 256 + d];
+  s[d] = v;
+  __syncthreads();
+  for (int o = 1; o < 256; o <<= 1) {
+    const uint32_t y = d >= o ? s[d - o] : 0u;
+    __syncthreads();
+    s[d] += y;
+    __syncthreads();
+  }
+  gofs[p * 256 + d] = s[d] - v;
 }
 
 __device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
