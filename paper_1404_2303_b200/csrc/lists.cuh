@@ -35,7 +35,7 @@
 #include "hiter.cuh"
 
 #ifndef WALK_WARPS
-#define WALK_WARPS 8
+#define WALK_WARPS 4
 #endif
 #define WALK_TAKE 32    // a node holding <= WALK_TAKE particles is swept whole (no descent)
 #define WALK_CAP 384    // frontier entries (node | image code << 27), LIFO
