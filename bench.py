@@ -45,7 +45,7 @@ FLOP_TEST, FLOP_HSOLVE = 8, 20
 # (tools/fp32_peak.cu, profiles/round1/fp32_peak.json).
 FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 
-CONFIG_TUNING = dict(split_count=32, split_fraction=0.0)
+CONFIG_TUNING = dict(split_count=48, split_fraction=0.0)
 
 
 def parse():

@@ -37,7 +37,9 @@
 #ifndef WALK_WARPS
 #define WALK_WARPS 4
 #endif
-#define WALK_TAKE 32    // a node holding <= WALK_TAKE particles is swept whole (no descent)
+#ifndef WALK_TAKE
+#define WALK_TAKE 64    // a node holding <= WALK_TAKE particles is swept whole (no descent; 32: +0.08 ms, 128: +0.08)
+#endif
 #define WALK_CAP 384    // frontier entries (node | image code << 27), LIFO
 #define WALK_DFS 112    // room for the depth-first fallback above the frontier
 #define WALK_RQ 64      // queued leaf ranges streamed together

@@ -16,7 +16,7 @@ from . import parity as P
 pytestmark = pytest.mark.gpu
 
 # bench.py's tuning (the configuration the headline number is measured in)
-BENCH_CFG = dict(split_count=32, split_fraction=0.0)
+BENCH_CFG = dict(split_count=48, split_fraction=0.0)
 
 
 @pytest.fixture(scope="module", autouse=True)

@@ -3,7 +3,7 @@ sys.path.insert(0, "/root/repo")
 import numpy as np, torch
 import paper_1404_2303_b200 as sph, workloads
 p = workloads.c4(); N = p.n
-ctx = sph.Context(sph.default_config(p.box, split_count=32, split_fraction=0.0))
+ctx = sph.Context(sph.default_config(p.box, split_count=48, split_fraction=0.0))
 pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
 hx, hv, hm, hu = pin(p.x), pin(p.v), pin(p.m), pin(p.u)
 hod = dict(h=torch.empty(N).pin_memory(), rho=torch.empty(N).pin_memory())

@@ -7,7 +7,7 @@ name = sys.argv[1] if len(sys.argv) > 1 else "C4"
 p = workloads.make(name)
 dev = torch.device("cuda:0")
 t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
-ctx = sph.Context(sph.default_config(p.box, split_count=32, split_fraction=0.0))
+ctx = sph.Context(sph.default_config(p.box, split_count=48, split_fraction=0.0))
 x = t(p.x)
 g = ctx.guess_h(x).cpu().numpy()
 ctx.build_cells(x, None)

@@ -11,7 +11,7 @@ import workloads
 
 name = sys.argv[1] if len(sys.argv) > 1 else "C4"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-kw = dict(split_count=32, split_fraction=0.0)
+kw = dict(split_count=48, split_fraction=0.0)
 if len(sys.argv) > 3:
     kw.update(json.loads(sys.argv[3]))
 p = workloads.make(name)

@@ -16,7 +16,7 @@ tgen = time.time() - t0
 dev = torch.device("cuda:0")
 t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
 x, v, m, u = t(p.x), t(p.v), t(p.m), t(p.u)
-ctx = sph.Context(sph.default_config(p.box, split_count=32, split_fraction=0.0))
+ctx = sph.Context(sph.default_config(p.box, split_count=48, split_fraction=0.0))
 res = []
 for rep in range(2):
     torch.cuda.synchronize()
