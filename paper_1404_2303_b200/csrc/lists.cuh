@@ -50,7 +50,7 @@
 #define NB_ROWS 1       // neighbour-list slab: one contiguous row of K per particle (0: column-interleaved per group)
 #endif
 #ifndef SPHERE_VOTE
-#define SPHERE_VOTE 8   // node-vs-target-sphere tests between warp votes for an early exit
+#define SPHERE_VOTE 4   // node-vs-target-sphere tests between warp votes for an early exit
 #endif
 
 #define MODE_NB 0
@@ -400,7 +400,15 @@ __device__ void dfs_subtree(const WalkParams& P, WalkState& W, WalkSmem& S, int*
 // box; reached internal nodes push their children, reached leaves queue their ranges),
 // and the queued ranges streamed through the source filters.
 template <int MODE>
-__global__ void __launch_bounds__(WALK_WARPS * 32) k_walk(WalkParams P) {
+#ifndef WALK_MINB
+#define WALK_MINB 0     // min resident blocks for __launch_bounds__ (0: none; register use is then the compiler's)
+#endif
+#if WALK_MINB > 0
+#define WALK_BOUNDS __launch_bounds__(WALK_WARPS * 32, WALK_MINB)
+#else
+#define WALK_BOUNDS __launch_bounds__(WALK_WARPS * 32)
+#endif
+__global__ void WALK_BOUNDS k_walk(WalkParams P) {
   extern __shared__ __align__(16) unsigned char walk_raw[];   // WALK_WARPS x WalkSmem (dynamic)
   WalkSmem* smem = reinterpret_cast<WalkSmem*>(walk_raw);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
