@@ -403,7 +403,9 @@ template <int MODE>
 #ifndef WALK_MINB
 #define WALK_MINB 0     // min resident blocks for __launch_bounds__ (0: none; register use is then the compiler's)
 #endif
-#if WALK_MINB > 0
+#if defined(WALK_MAXNREG)
+#define WALK_BOUNDS __maxnreg__(WALK_MAXNREG)
+#elif WALK_MINB > 0
 #define WALK_BOUNDS __launch_bounds__(WALK_WARPS * 32, WALK_MINB)
 #else
 #define WALK_BOUNDS __launch_bounds__(WALK_WARPS * 32)
