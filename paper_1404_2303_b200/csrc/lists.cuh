@@ -49,6 +49,9 @@
 #ifndef NB_ROWS
 #define NB_ROWS 1       // neighbour-list slab: one contiguous row of K per particle (0: column-interleaved per group)
 #endif
+#ifndef UNION_PACKED
+#define UNION_PACKED 1  // interaction-list walk: packed FP32 pair tests (tools/sweep.sh)
+#endif
 #ifndef SPHERE_VOTE
 #define SPHERE_VOTE 4   // node-vs-target-sphere tests between warp votes for an early exit
 #endif
@@ -160,6 +163,24 @@ __device__ __forceinline__ void emit_chunk(const WalkParams& P, WalkState& W, Wa
   if (!bal) return;
   const int m = __popc(bal);
   const int pos = __popc(bal & lanemask_lt());
+#if UNION_PACKED
+  if (MODE != MODE_NB) {
+    // SoA planes x, y, z, reach^2 for packed FP32 pair tests; an odd count is padded with a
+    // far source
+    float* sx = reinterpret_cast<float*>(S.s);
+    if (keep) {
+      const float w = reach_eff(hj, 0.f);
+      sx[pos] = p.x;
+      sx[32 + pos] = p.y;
+      sx[64 + pos] = p.z;
+      sx[96 + pos] = w * w;
+    }
+    if (lane == 0 && (m & 1)) {
+      sx[m] = sx[32 + m] = sx[64 + m] = 1e30f;
+      sx[96 + m] = 0.f;
+    }
+  } else
+#endif
   if (keep) S.s[pos] = make_float4(p.x, p.y, p.z, MODE == MODE_NB ? 0.f : reach_eff(hj, 0.f));
   __syncwarp();
   // 2. exact distance test per target (lane)
@@ -191,12 +212,25 @@ __device__ __forceinline__ void emit_chunk(const WalkParams& P, WalkState& W, Wa
   if (W.ri >= 0.f) {
     const float ri = reach_eff(W.ri, 0.f);
     const float ri2 = ri * ri;
+#if UNION_PACKED
+    // two sources per packed instruction, the interaction kernels' r^2 operation order
+    const float2* X2 = reinterpret_cast<const float2*>(S.s);
+    const float2* Y2 = X2 + 16;
+    const float2* Z2 = X2 + 32;
+    const float2* R2 = X2 + 48;
+    for (int t = 0; t < (m + 1) >> 1; ++t) {
+      const float2 r2 = r2_pair(W.xi, W.yi, W.zi, X2[t], Y2[t], Z2[t]);
+      const float2 w2 = R2[t];
+      hm |= ((unsigned)(r2.x < fmaxf(ri2, w2.x)) | ((unsigned)(r2.y < fmaxf(ri2, w2.y)) << 1)) << (2 * t);
+    }
+#else
     for (int t = 0; t < m; ++t) {
       const float4 q = S.s[t];
       const float dx = W.xi - q.x, dy = W.yi - q.y, dz = W.zi - q.z;
       const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
       hm |= (unsigned)(r2 < fmaxf(ri2, q.w * q.w)) << t;
     }
+#endif
   }
   const unsigned km = __reduce_or_sync(FULL_MASK, hm);
   __syncwarp();
