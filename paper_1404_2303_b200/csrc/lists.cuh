@@ -49,6 +49,9 @@
 #ifndef NB_ROWS
 #define NB_ROWS 1       // neighbour-list slab: one contiguous row of K per particle (0: column-interleaved per group)
 #endif
+#ifndef NB_PREFETCH
+#define NB_PREFETCH 1   // prefetch each neighbour-list row into L1 before the h sums
+#endif
 #ifndef UNION_PACKED
 #define UNION_PACKED 1  // interaction-list walk: packed FP32 pair tests (tools/sweep.sh)
 #endif
@@ -674,6 +677,13 @@ __global__ void WALK_BOUNDS k_walk(WalkParams P) {
         P.ovf_cnt[s] = 0;
       }
     }
+#if NB_PREFETCH
+    if (act && NB_ROWS) {   // pull the row's lines into L1 at once (the sums then hit L1)
+      const char* rb = reinterpret_cast<const char*>(P.nb_r2 + (int64_t)s * P.K);
+      const int bytes = min(cnt, P.K) * 4;
+      for (int b = 0; b < bytes; b += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"(rb + b));
+    }
+#endif
     __syncwarp();   // the lists recorded by every lane are visible to the cooperative sums
     warp_hsolve(act, P.nb_r2 + (NB_ROWS ? (int64_t)s * P.K : (int64_t)grp.y * P.K + lane), NB_ROWS ? 1 : W.gz, cnt, P.K,
                 false, true, H, P.n_t, P.tol, P.margin,
