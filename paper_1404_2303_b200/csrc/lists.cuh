@@ -52,6 +52,9 @@
 #ifndef NB_PREFETCH
 #define NB_PREFETCH 1   // prefetch each neighbour-list row into L1 before the h sums
 #endif
+#ifndef SPHERE_HINT
+#define SPHERE_HINT 1   // interaction-list walk: test first the target that reached the node's parent
+#endif
 #ifndef UNION_PACKED
 #define UNION_PACKED 1  // interaction-list walk: packed FP32 pair tests (tools/sweep.sh)
 #endif
@@ -124,6 +127,7 @@ struct WalkParams {
 
 struct WalkSmem {
   int stk[WALK_CAP + WALK_DFS];
+  uint8_t hint[WALK_CAP];   // per frontier entry: a target that reached the parent
   int rq_first[WALK_RQ];
   int rq_code[WALK_RQ];
   float4 rq_so[WALK_RQ];    // per queued range: source pre-shift (x - L for a source near L)
@@ -272,9 +276,11 @@ __device__ __forceinline__ bool node_in_reach(const WalkParams& P, const WalkSta
 // Refines the box test: the node (one per lane) is kept iff its box is within reach of at
 // least one target's own sphere (each target broadcast in turn), so a group whose targets'
 // h differ widely does not visit the cells only its bounding box reaches.
+// hint: a target that reached the node's parent (tested first; children usually meet the
+// same target); *first_hit returns the target that reached this node, for its children.
 template <int MODE>
 __device__ __forceinline__ bool node_in_spheres(const WalkParams& P, const WalkState& W, const WalkSmem& S, int node,
-                                                int code, bool coarse) {
+                                                int code, bool coarse, int hint = 0, int* first_hit = nullptr) {
   if (!W.spheres || !__any_sync(FULL_MASK, coarse)) return coarse;
   float3 lo = make_float3(0.f, 0.f, 0.f), hi = lo;
   float hmn = 0.f;
@@ -285,6 +291,19 @@ __device__ __forceinline__ bool node_in_spheres(const WalkParams& P, const WalkS
     if (MODE != MODE_NB) hmn = P.N.hmax[node];
   }
   bool hit = false;
+  int ht = 0;
+#if SPHERE_HINT
+  if (MODE != MODE_NB) {
+    const float4 q = S.tgt[min(hint, W.ntg - 1)];
+    const float gx = fmaxf(fmaxf(lo.x - q.x, q.x - hi.x), 0.f);
+    const float gy = fmaxf(fmaxf(lo.y - q.y, q.y - hi.y), 0.f);
+    const float gz = fmaxf(fmaxf(lo.z - q.z, q.z - hi.z), 0.f);
+    const float rr = MODE == MODE_NB ? q.w : fmaxf(q.w, reach_eff(hmn, P.slack));
+    hit = fmaf(gx, gx, fmaf(gy, gy, gz * gz)) < rr * rr;
+    ht = min(hint, W.ntg - 1);
+  }
+  if (MODE == MODE_NB || !__all_sync(FULL_MASK, hit || !coarse))
+#endif
   for (int t0 = 0; t0 < W.ntg; t0 += SPHERE_VOTE) {
 #pragma unroll
     for (int k = 0; k < SPHERE_VOTE; ++k) {
@@ -294,10 +313,13 @@ __device__ __forceinline__ bool node_in_spheres(const WalkParams& P, const WalkS
       const float gy = fmaxf(fmaxf(lo.y - q.y, q.y - hi.y), 0.f);
       const float gz = fmaxf(fmaxf(lo.z - q.z, q.z - hi.z), 0.f);
       const float rr = MODE == MODE_NB ? q.w : fmaxf(q.w, reach_eff(hmn, P.slack));
-      hit |= fmaf(gx, gx, fmaf(gy, gy, gz * gz)) < rr * rr;
+      const bool h = fmaf(gx, gx, fmaf(gy, gy, gz * gz)) < rr * rr;
+      if (MODE != MODE_NB && h && !hit) ht = t;
+      hit |= h;
     }
     if (__all_sync(FULL_MASK, hit || !coarse)) break;   // every kept node already hit
   }
+  if (first_hit) *first_hit = ht;
   return coarse && hit;
 }
 
@@ -561,7 +583,10 @@ __global__ void WALK_BOUNDS k_walk(WalkParams P) {
         if (node >= 0) ent = node | (code << SPH_IDX_BITS);
       }
       const unsigned sb = __ballot_sync(FULL_MASK, ent != -1);
-      if (ent != -1) S.stk[__popc(sb & lanemask_lt())] = ent;
+      if (ent != -1) {
+        S.stk[__popc(sb & lanemask_lt())] = ent;
+        if (MODE != MODE_NB) S.hint[__popc(sb & lanemask_lt())] = 0;
+      }
       int top = __popc(sb);
       __syncwarp();
       while (top > 0) {
@@ -574,8 +599,11 @@ __global__ void WALK_BOUNDS k_walk(WalkParams P) {
           dfs_subtree<MODE>(P, W, S, S.stk + top, e, nq);
           continue;
         }
-        int e = 0;
-        if (lane < k) e = S.stk[top - k + lane];
+        int e = 0, hn = 0;
+        if (lane < k) {
+          e = S.stk[top - k + lane];
+          if (MODE != MODE_NB) hn = S.hint[top - k + lane];
+        }
         __syncwarp();
         top -= k;
         const int nd = e & SPH_IDX_MASK, code = (int)((unsigned)e >> SPH_IDX_BITS);
@@ -585,7 +613,8 @@ __global__ void WALK_BOUNDS k_walk(WalkParams P) {
           rec = P.N.rec[nd];
           reach = node_in_reach<MODE>(P, W, S, nd, code);
         }
-        reach = node_in_spheres<MODE>(P, W, S, nd, code, reach);
+        int fh = 0;
+        reach = node_in_spheres<MODE>(P, W, S, nd, code, reach, hn, &fh);
         if (lane < k) {
           leaf = reach && !(rec.z >= 0 && rec.y > WALK_TAKE);
           srt = leaf && P.N.sortoff[nd] >= 0;
@@ -599,7 +628,10 @@ __global__ void WALK_BOUNDS k_walk(WalkParams P) {
           if (lane >= o) pre += y;
         }
         const int tot = __shfl_sync(FULL_MASK, pre, 31);
-        for (int c2 = 0; c2 < nch; ++c2) S.stk[top + pre - nch + c2] = (rec.z + c2) | (code << SPH_IDX_BITS);
+        for (int c2 = 0; c2 < nch; ++c2) {
+          S.stk[top + pre - nch + c2] = (rec.z + c2) | (code << SPH_IDX_BITS);
+          if (MODE != MODE_NB) S.hint[top + pre - nch + c2] = (uint8_t)fh;
+        }
         top += tot;
         // reached unsorted leaves: queue their ranges
         const bool ql = leaf && !srt;
