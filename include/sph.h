@@ -116,6 +116,10 @@ typedef struct {         /* host struct, filled when non-NULL */
   int64_t n_borderline;          /* density (sph_density): directed (i, j), j != i, |r_ij/h_i - 1| <= 1e-6 (R5) */
   int64_t n_borderline_force;    /* force (sph_force): unordered pairs, |r_ij/max(h_i,h_j) - 1| <= 1e-6 */
   int64_t n_coincident;          /* density (sph_density): unordered pairs with r_ij = 0, i != j (R13) */
+  /* SPH_F_COUNT_CANDIDATES only (else 0), sph_density: sources the walks streamed through their
+     box filters (after the sorted windows where leaves are presorted) */
+  int64_t n_nb_sources;          /* neighbour-list walks since the last build (incl. re-walks) */
+  int64_t n_union_sources;       /* interaction-list walks of this call */
 } sph_stats;
 
 /* Fill *cfg with the paper's defaults for the given box. */

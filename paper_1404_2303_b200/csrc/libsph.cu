@@ -410,6 +410,8 @@ static int walk_smem() {
 static WalkParams walk_params(sph_ctx* c, const float* reach) {
   WalkParams P;
   memset(&P, 0, sizeof(P));
+  // [0] neighbour-list walks since the build, [1] interaction-list walks of the last density call
+  if (c->cfg.flags & SPH_F_COUNT_CANDIDATES) P.raw_out = Bget<unsigned long long>(c, B_WALKRAW);
   P.groups = Bget<int4>(c, B_GROUPS);
   P.xh = Bget<float4>(c, B_XH);
   P.reach = reach;
@@ -560,6 +562,10 @@ static void build_union(sph_ctx* c, const float* reach) {
   const float rmax = as_float(h[C_HMAXBITS]);
   const int cap = c->ucap;
   WalkParams P = walk_params(c, reach);
+  if (P.raw_out) {
+    P.raw_out += 1;
+    CUDA_TRY(cudaMemsetAsync(P.raw_out, 0, sizeof(unsigned long long), c->stream));
+  }
   P.reach_max = rmax;
   P.nsel = ng;
   P.sel = group_order(c, reach);
@@ -914,6 +920,7 @@ int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const floa
   }
   // neighbour lists of the h iteration: r^2 < h_build^2 per particle
   hctr_reset(c);
+  CUDA_TRY(cudaMemsetAsync(B<unsigned long long>(c, B_WALKRAW, 2), 0, 2 * sizeof(unsigned long long), c->stream));
   nb_walk(c, -1);
   c->state = 1;
   CUDA_TRY(cudaEventRecord(c->ev[1], c->stream));
@@ -1114,6 +1121,12 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
     st->ms_kernel_walk_union = c->ms_phase[2];
     st->n_nb_entries = c->nb_entries;
     st->n_walk_launches = c->walk_launches;
+    if (c->cfg.flags & SPH_F_COUNT_CANDIDATES) {
+      unsigned long long wr[2];
+      CUDA_TRY(cudaMemcpy(wr, Bget<unsigned long long>(c, B_WALKRAW), sizeof(wr), cudaMemcpyDeviceToHost));
+      st->n_nb_sources = (int64_t)wr[0];
+      st->n_union_sources = (int64_t)wr[1];
+    }
     st->n_directed = ndir;
     st->n_borderline = nbord_d;
     st->n_coincident = ncoinc;

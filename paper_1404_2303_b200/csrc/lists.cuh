@@ -85,6 +85,7 @@ struct WalkParams {
   const int* nsel_dev;      // if set: the number of groups in sel (device; nsel is a bound)
   int* rg_out;              // if set: groups with a lane left in HS_REGROW are appended here
   int* rg_cnt;              //   (count, atomic; order is scheduling only, results do not depend on it)
+  unsigned long long* raw_out;  // if set: sources streamed through the filters, summed (SPH_F_COUNT_CANDIDATES)
   const float4* xh;         // cell-order positions
   const float* reach;       // per particle: NB h_build; UNION the h used for the reach (0: none)
   const uint8_t* tsel;      // NB: targets are the particles with tsel == tsel_val (null: owned)
@@ -676,6 +677,7 @@ __global__ void WALK_BOUNDS k_walk(WalkParams P) {
   if (lane == 0) {
     atomicAdd(&P.ctr[C_TMP2], (unsigned long long)W.raw);
     atomicMax(&P.ctr[C_TMP0], (unsigned long long)W.raw);
+    if (P.raw_out) atomicAdd(P.raw_out, (unsigned long long)W.raw);
   }
 #ifdef SPH_WALK_TRACE
   if (W.raw > 10000) {

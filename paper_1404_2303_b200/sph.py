@@ -60,6 +60,7 @@ class Stats(ctypes.Structure):
         ("ms_kernel_walk_union", ctypes.c_double), ("n_nb_entries", ctypes.c_int64),
         ("n_walk_launches", ctypes.c_int64), ("n_borderline", ctypes.c_int64),
         ("n_borderline_force", ctypes.c_int64), ("n_coincident", ctypes.c_int64),
+        ("n_nb_sources", ctypes.c_int64), ("n_union_sources", ctypes.c_int64),
     ]
 
     def as_dict(self):
