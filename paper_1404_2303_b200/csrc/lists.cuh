@@ -40,9 +40,15 @@
 #ifndef WALK_TAKE
 #define WALK_TAKE 64    // a node holding <= WALK_TAKE particles is swept whole (no descent; 32: +0.08 ms, 128: +0.08)
 #endif
+#ifndef WALK_CAP
 #define WALK_CAP 384    // frontier entries (node | image code << 27), LIFO
+#endif
+#ifndef WALK_DFS
 #define WALK_DFS 112    // room for the depth-first fallback above the frontier
+#endif
+#ifndef WALK_RQ
 #define WALK_RQ 64      // queued leaf ranges streamed together
+#endif
 #ifndef SPH_INWALK_PASSES
 #define SPH_INWALK_PASSES 6   // NB walk passes per group and launch (re-walks without a host round)
 #endif
