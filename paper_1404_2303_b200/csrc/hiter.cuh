@@ -138,7 +138,10 @@ __device__ __forceinline__ uint8_t hstep(double S0, float S1, float S2, float& h
   hn = fminf(fmaxf(hn, 0.5f * h), 2.f * h);
   const bool inb = hn > l && hn < u;
   if (!inb) hn = 0.5f * (l + fminf(u, 2.f * h));
-  hn = fminf(hn, hcap);
+  // floor at 2^-19 of the cap (~1e-6 L, below the fp32 resolution of distances in the box):
+  // with more than 4 coincident particles N(h) > n_t for every h > 0 (no root);
+  // such a particle stops here and is reported unconverged instead of underflowing
+  hn = fminf(fmaxf(hn, hcap * 1.9073486e-6f), hcap);
   h = hn;
   if (hn > hbs) {                                     // the root lies beyond the list
     hbs = fminf(fminf(hn * margin, fmaxf(u, hn)), hcap);

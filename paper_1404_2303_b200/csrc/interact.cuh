@@ -555,7 +555,9 @@ __global__ void k_ghost(int64_t n, const float4* __restrict__ xh, const float* _
     const float uu = u[s];
     const float P = (gamma - 1.f) * rho * uu;
     const float c = sqrtf(gamma * (gamma - 1.f) * uu);
-    const float A = P / (omega * rho * rho);
+    // Omega = 0 only without a neighbour at r > 0 inside h (R17): every G_i is then 0 and the
+    // oracle's convention A_i G_i = 0 is kept by A_i = 0
+    const float A = omega > 0.f ? P / (omega * rho * rho) : 0.f;
     const float nrm = 1.0f / (h * smf);
     const float div = a0.w * nrm;
     const float cx = -a1.x * nrm, cy = -a1.y * nrm, cz = -a1.z * nrm;

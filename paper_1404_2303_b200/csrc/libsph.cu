@@ -1010,7 +1010,7 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
     CUDA_TRY(cudaMemcpyAsync(hh, Bget<unsigned long long>(c, B_HCTR), sizeof(hh), cudaMemcpyDeviceToHost, c->stream));
     sync(c);
     ++rounds;
-    unconv = (long long)hh[HC_UNCONV];
+    unconv += (long long)hh[HC_UNCONV];   // disjoint per round: an unconverged particle is never re-walked
     itmax = std::max(itmax, (long long)hh[HC_ITMAX]);
     DBG("h solve round %d: unconverged %llu, re-walk %llu, pool %llu, max iterations %llu\n", rounds,
         hh[HC_UNCONV], hh[HC_REGROW], hh[HC_OVF], hh[HC_ITMAX]);
@@ -1091,12 +1091,16 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
          c->cfg.balsara_eps, dout.sf, (float)c->cfg.n_ngb, tol_check, go, ctr(c));
   flush_out(c, maps, c->ev[3]);
   c->state = 2;
-  const bool noconv = unconv > 0;
+  bool noconv = unconv > 0;
   ctr_read(c, hc);
   const long long ndir = (long long)hc[C_NDIR];
   const long long cand = (long long)hc[C_CAND];
   const long long nbord_d = (long long)hc[C_BORDER_D], ncoinc = (long long)hc[C_COINC] / 2;
   const long long nbad = (long long)hc[C_UNCONV];
+  if (nbad > 0 && !noconv) {   // an accepted step failed the N(h) re-check (R4): not converged
+    noconv = true;
+    unconv = nbad;
+  }
   if (c->n > c->n_own && c->cfg.halo_width > 0.0) {
     // every owned particle's partners must be inside the received halo
     ctr_reset(c);
@@ -1132,7 +1136,7 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
     st->n_coincident = ncoinc;
     st->n_candidates = cand;
     st->n_candidates_density_full = cand;
-    st->n_unconverged = (noconv ? unconv : 0) + (noconv ? 0 : nbad);
+    st->n_unconverged = noconv ? unconv : 0;
     st->h_iters = (int)itmax;
     float ms = 0.f;
     cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);

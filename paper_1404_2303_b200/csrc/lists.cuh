@@ -737,12 +737,14 @@ __global__ void WALK_BOUNDS k_walk(WalkParams P) {
       P.nb_cnt[s] = cnt;
     }
     const bool again = tg && H.st == HS_REGROW && pass + 1 < SPH_INWALK_PASSES;
+    // lanes that finish in this pass (converged, unconverged, overflowed, or out of passes)
+    // are counted now; the re-walked ones in the pass that finishes them
+    hsolve_count(tg && !again, H, P.hc);
     if (__any_sync(FULL_MASK, again)) {
       tg = again;
       W.ri = again ? H.hbs : -1.f;
       continue;
     }
-    hsolve_count(tg, H, P.hc);
     if (P.rg_out) {
       const unsigned rg = __ballot_sync(FULL_MASK, tg && H.st == HS_REGROW);
       if (rg && lane == 0) P.rg_out[atomicAdd(P.rg_cnt, 1)] = gid;
