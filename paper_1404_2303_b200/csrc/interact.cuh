@@ -33,12 +33,62 @@ struct GroupLists {
 #define DENS_ST 1          // staged sources per round: 32 * DENS_ST (tuned, tools/sweep.sh)
 #endif
 
+struct GhostOut {
+  float* h;
+  float* rho;
+  float* omega;
+  int* nnbr;
+  float* div;
+  float* curl;
+  const uint32_t* perm;
+  int64_t n_own;       // caller indices >= n_own are halo (source-only) particles
+  float* h_o;          // caller-order state kept for the force loop: h
+  float4* g_o;         //   {A, rho, c, f}
+};
+
 struct DensOut {
   double* sf;     // sum f            (N_i = (32/3) sum f, Eq. 3)
   float4* acc0;   // sum m f, sum m q f', sum q f', sum m (f'/r) dv.dx
   float4* acc1;   // sum m (f'/r) dv x dx (xyz), neighbour count (int bits)
   float* s2;      // sum q^2 f''      (second derivative of N for the Halley step)
+  // ghost fused into the epilogue (a9): the sums above are then not
+  // written; the caller-order outputs and the force state are
+  bool ghost;
+  const float* u;
+  float gamma, beps, n_t, tol_check;
+  GhostOut g;
 };
+
+// a9 for one target from its density sums (k_density's epilogue and k_ghost)
+__device__ __forceinline__ void ghost_one(const GhostOut& out, uint32_t o, float h, float uu, float smf, float smqfp,
+                                          float divs, float crx, float cry, float crz, int cnt, float gamma,
+                                          float beps) {
+  const float hinv = 1.0f / h;
+  const float rho = SPH_CNORM * hinv * hinv * hinv * smf;
+  const float omega = -smqfp / (3.f * smf);
+  const float P = (gamma - 1.f) * rho * uu;
+  const float c = sqrtf(gamma * (gamma - 1.f) * uu);
+  // Omega = 0 only without a neighbour at r > 0 inside h (R17): every G_i is then 0 and the
+  // oracle's convention A_i G_i = 0 is kept by A_i = 0
+  const float A = omega > 0.f ? P / (omega * rho * rho) : 0.f;
+  const float nrm = 1.0f / (h * smf);
+  const float div = divs * nrm;
+  const float cx = -crx * nrm, cy = -cry * nrm, cz = -crz * nrm;
+  const float cn = sqrtf(cx * cx + cy * cy + cz * cz);
+  const float fb = cn / (fabsf(div) + cn + beps * c * hinv);
+  out.h_o[o] = h;
+  out.g_o[o] = make_float4(A, rho, c, fb);
+  out.h[o] = h;
+  out.rho[o] = rho;
+  if (out.omega) out.omega[o] = omega;
+  if (out.nnbr) out.nnbr[o] = cnt;
+  if (out.div) out.div[o] = div;
+  if (out.curl) {
+    out.curl[3 * (int64_t)o] = cx;
+    out.curl[3 * (int64_t)o + 1] = cy;
+    out.curl[3 * (int64_t)o + 2] = cz;
+  }
+}
 
 // DIAG: also count (O8) borderline directed pairs |r / h_i - 1| <= SPH_BAND and coincident
 // directed pairs (r = 0, j != i) into ctr[C_BORDER_D], ctr[C_COINC] (SPH_F_DIAGNOSTICS).
@@ -175,15 +225,31 @@ __global__ void __launch_bounds__(DENS_WARPS * 32) k_density(GroupLists G, const
     }
     __syncwarp();
   }
+  long long nd = 0, nbad = 0;
   if (act) {
-    out.sf[s] = sf;
-    out.s2[s] = sq2fpp;
-    out.acc0[s] = make_float4(smf, smqfp, sqfp, divs);
-    out.acc1[s] = make_float4(crx, cry, crz, __int_as_float(cnt));
+    if (!NONLY && out.ghost) {
+      ghost_one(out.g, perm[s], hi, out.u[s], smf, smqfp, divs, crx, cry, crz, cnt, out.gamma, out.beps);
+      nd = cnt;
+      // the h iteration's convergence, re-checked from this loop's sum at the final h (R4)
+      nbad = fabs((32.0 / 3.0) * sf - (double)out.n_t) > (double)out.tol_check ? 1 : 0;
+    } else {
+      out.sf[s] = sf;
+      out.s2[s] = sq2fpp;
+      out.acc0[s] = make_float4(smf, smqfp, sqfp, divs);
+      out.acc1[s] = make_float4(crx, cry, crz, __int_as_float(cnt));
+    }
   }
 #pragma unroll
-  for (int o2 = 16; o2 > 0; o2 >>= 1) ncand += __shfl_xor_sync(FULL_MASK, ncand, o2);
-  if (lane == 0 && ctr) atomicAdd(&ctr[C_CAND], (unsigned long long)ncand);
+  for (int o2 = 16; o2 > 0; o2 >>= 1) {
+    ncand += __shfl_xor_sync(FULL_MASK, ncand, o2);
+    nd += __shfl_xor_sync(FULL_MASK, nd, o2);
+    nbad += __shfl_xor_sync(FULL_MASK, nbad, o2);
+  }
+  if (lane == 0 && ctr) {
+    atomicAdd(&ctr[C_CAND], (unsigned long long)ncand);
+    if (nd) atomicAdd(&ctr[C_NDIR], (unsigned long long)nd);
+    if (nbad) atomicAdd(&ctr[C_UNCONV], (unsigned long long)nbad);
+  }
   if (DIAG) {
 #pragma unroll
     for (int o2 = 16; o2 > 0; o2 >>= 1) {
@@ -524,18 +590,6 @@ __global__ void k_state_swap(uint8_t* __restrict__ st, int64_t n, uint8_t from, 
 //   P = (gamma-1) rho u,  c = sqrt(gamma (gamma-1) u),  A = P/(Omega rho^2)
 //   div = sum m (f'/r) dv.dx / (h sum m f),  curl = -sum m (f'/r) dv x dx / (h sum m f)
 //   f = |curl| / (|div| + |curl| + eps c/h)       (R10)
-struct GhostOut {
-  float* h;
-  float* rho;
-  float* omega;
-  int* nnbr;
-  float* div;
-  float* curl;
-  const uint32_t* perm;
-  int64_t n_own;       // caller indices >= n_own are halo (source-only) particles
-  float* h_o;          // caller-order state kept for the force loop: h
-  float4* g_o;         //   {A, rho, c, f}
-};
 
 __global__ void k_ghost(int64_t n, const float4* __restrict__ xh, const float* __restrict__ u,
                         const float4* __restrict__ acc0, const float4* __restrict__ acc1, float gamma, float beps,
@@ -546,39 +600,12 @@ __global__ void k_ghost(int64_t n, const float4* __restrict__ xh, const float* _
        s += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t o = out.perm[s];
     if (o >= out.n_own) continue;            // halo particle: its owner computes it
-    const float4 p = xh[s];
-    const float h = p.w, hinv = 1.0f / h;
     const float4 a0 = acc0[s], a1 = acc1[s];
-    const float smf = a0.x;
-    const float rho = SPH_CNORM * hinv * hinv * hinv * smf;
-    const float omega = -a0.y / (3.f * smf);
-    const float uu = u[s];
-    const float P = (gamma - 1.f) * rho * uu;
-    const float c = sqrtf(gamma * (gamma - 1.f) * uu);
-    // Omega = 0 only without a neighbour at r > 0 inside h (R17): every G_i is then 0 and the
-    // oracle's convention A_i G_i = 0 is kept by A_i = 0
-    const float A = omega > 0.f ? P / (omega * rho * rho) : 0.f;
-    const float nrm = 1.0f / (h * smf);
-    const float div = a0.w * nrm;
-    const float cx = -a1.x * nrm, cy = -a1.y * nrm, cz = -a1.z * nrm;
-    const float cn = sqrtf(cx * cx + cy * cy + cz * cz);
-    const float fb = cn / (fabsf(div) + cn + beps * c * hinv);
-    out.h_o[o] = h;
-    out.g_o[o] = make_float4(A, rho, c, fb);
     const int cnt = __float_as_int(a1.w);
+    ghost_one(out, o, xh[s].w, u[s], a0.x, a0.y, a0.w, a1.x, a1.y, a1.z, cnt, gamma, beps);
     nd += cnt;
     // the h iteration's convergence, re-checked from the density loop's sum at the final h
     nbad += fabs((32.0 / 3.0) * sf[s] - (double)n_t) > (double)tol_check ? 1 : 0;
-    out.h[o] = h;
-    out.rho[o] = rho;
-    if (out.omega) out.omega[o] = omega;
-    if (out.nnbr) out.nnbr[o] = cnt;
-    if (out.div) out.div[o] = div;
-    if (out.curl) {
-      out.curl[3 * (int64_t)o] = cx;
-      out.curl[3 * (int64_t)o + 1] = cy;
-      out.curl[3 * (int64_t)o + 2] = cz;
-    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {

@@ -1054,23 +1054,7 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
          hr);
   build_union(c, hr);
   c->force_lists = c->n == c->n_own;
-  DensOut dout;
-  dout.sf = B<double>(c, B_DSUMF, n);
-  dout.acc0 = B<float4>(c, B_DACC0, n);
-  dout.acc1 = B<float4>(c, B_DACC1, n);
-  dout.s2 = B<float>(c, B_DSUM2, n);
-  ctr_reset(c);
-  CUDA_TRY(cudaEventRecord(c->ev[8], c->stream));
-  {
-    DbgTimer _t(c, "density kernel");
-    const GroupLists G = group_lists(c);
-    const bool diag = (c->cfg.flags & SPH_F_DIAGNOSTICS) != 0;
-    auto kd = diag ? k_density<false, true> : k_density<false, false>;
-    LAUNCH(kd, gridfull(G.ngroups, DENS_WARPS), DENS_WARPS * 32, 0, G, Bget<float4>(c, B_XH), vm,
-           Bget<uint32_t>(c, B_PERM), c->n_own, box3(c), dout, ctr(c));
-  }
-  CUDA_TRY(cudaEventRecord(c->ev[9], c->stream));
-  // a9 ghost: finalise and write the caller-order outputs
+  // a9 ghost fused into the density kernel: the caller-order outputs and the force state
   std::vector<OutMap> maps;
   GhostOut go;
   const int64_t no = c->n_own;
@@ -1084,11 +1068,28 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   go.n_own = no;
   go.h_o = B<float>(c, B_HFIN_O, n);
   go.g_o = B<float4>(c, B_GST_O, n);
+  DensOut dout;
+  memset(&dout, 0, sizeof(dout));
+  dout.ghost = true;
+  dout.g = go;
+  dout.u = uc;
+  dout.gamma = c->cfg.gamma;
+  dout.beps = c->cfg.balsara_eps;
+  dout.n_t = (float)c->cfg.n_ngb;
   // N(h) re-check: twice the iteration's tolerance plus a few fp32 ulps of h (the bracket
   // stop at fp32 resolution) in N = n_t (h/h)^3
-  const float tol_check = 2.f * (float)c->cfg.n_ngb_tol + 24.f * (float)c->cfg.n_ngb * 1.1920929e-7f;
-  LAUNCH(k_ghost, grid1d(c, n, 256), 256, 0, n, Bget<float4>(c, B_XH), uc, dout.acc0, dout.acc1, c->cfg.gamma,
-         c->cfg.balsara_eps, dout.sf, (float)c->cfg.n_ngb, tol_check, go, ctr(c));
+  dout.tol_check = 2.f * (float)c->cfg.n_ngb_tol + 24.f * (float)c->cfg.n_ngb * 1.1920929e-7f;
+  ctr_reset(c);
+  CUDA_TRY(cudaEventRecord(c->ev[8], c->stream));
+  {
+    DbgTimer _t(c, "density kernel");
+    const GroupLists G = group_lists(c);
+    const bool diag = (c->cfg.flags & SPH_F_DIAGNOSTICS) != 0;
+    auto kd = diag ? k_density<false, true> : k_density<false, false>;
+    LAUNCH(kd, gridfull(G.ngroups, DENS_WARPS), DENS_WARPS * 32, 0, G, Bget<float4>(c, B_XH), vm,
+           Bget<uint32_t>(c, B_PERM), c->n_own, box3(c), dout, ctr(c));
+  }
+  CUDA_TRY(cudaEventRecord(c->ev[9], c->stream));
   flush_out(c, maps, c->ev[3]);
   c->state = 2;
   bool noconv = unconv > 0;
