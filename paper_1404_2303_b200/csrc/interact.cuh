@@ -93,7 +93,10 @@ __device__ __forceinline__ void ghost_one(const GhostOut& out, uint32_t o, float
 // DIAG: also count (O8) borderline directed pairs |r / h_i - 1| <= SPH_BAND and coincident
 // directed pairs (r = 0, j != i) into ctr[C_BORDER_D], ctr[C_COINC] (SPH_F_DIAGNOSTICS).
 template <bool NONLY, bool DIAG = false>
-__global__ void __launch_bounds__(DENS_WARPS * 32) k_density(GroupLists G, const float4* __restrict__ xh,
+#ifndef DENS_MINB
+#define DENS_MINB 4     // 4 resident blocks of 8 warps: <= 64 registers (free: 72, 1: 89; both slower)
+#endif
+__global__ void __launch_bounds__(DENS_WARPS * 32, DENS_MINB) k_density(GroupLists G, const float4* __restrict__ xh,
                                                              const float4* __restrict__ vm,
                                                              const uint32_t* __restrict__ perm, int64_t n_own,
                                                              float3 Lbox, DensOut out, unsigned long long* ctr) {
