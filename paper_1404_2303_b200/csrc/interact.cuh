@@ -300,6 +300,7 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FORCE_MINB) k_force(GroupLis
   __shared__ float4 sb[FORCE_WARPS][32 * FORCE_ST];   // v_j, m_j
   __shared__ float4 sc[FORCE_WARPS][32 * FORCE_ST];   // A~_j, rho_j, c_j, f_j
   __shared__ int sj[FORCE_WARPS][32 * FORCE_ST];
+  __shared__ int sself[FORCE_WARPS][32];   // per target lane: its own particle's staged slot, or -1
   __shared__ __align__(8) float sxyzw[FORCE_WARPS][4][32 * FORCE_ST];   // x, y, z, 1/h (SoA, packed tests)
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int gid = blockIdx.x * FORCE_WARPS + wib;
@@ -345,6 +346,8 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FORCE_MINB) k_force(GroupLis
   // the lanes' hit counts per stage are balanced (consecutive entries come from one cell)
   const int nst = (len + 32 * FORCE_ST - 1) / (32 * FORCE_ST);
   for (int stg = 0; stg < nst; ++stg) {
+    sself[wib][lane] = -1;
+    __syncwarp();
 #pragma unroll
     for (int k = 0; k < FORCE_ST; ++k) {
       const int e = stg + (32 * k + lane) * nst;
@@ -353,6 +356,10 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FORCE_MINB) k_force(GroupLis
       if (e < len) {
         const uint32_t ent = G.list[off + e];
         const uint32_t j = ent & SPH_IDX_MASK;
+        // the target's own particle (in its group's list with image code 0): its slot, so
+        // the hit mask drops it once instead of a check per hit
+        const int tl = (int)j - grp.y;
+        if ((ent >> SPH_IDX_BITS) == 0 && tl >= 0 && tl < grp.z) sself[wib][tl] = 32 * k + lane;
         const float4 p = fx[j];
         const float3 r = rel_pos(p, ent >> SPH_IDX_BITS, o, oL, L);
         a = make_float4(r.x, r.y, r.z, p.w);
@@ -389,6 +396,16 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FORCE_MINB) k_force(GroupLis
       }
       hm[k] = act ? m : 0u;
     }
+    {
+      const int sl = sself[wib][lane];
+#if FORCE_ST == 1
+      if (sl >= 0) hm[0] &= ~(1u << sl);
+#else
+#pragma unroll
+      for (int k = 0; k < FORCE_ST; ++k)
+        if (sl >= 0 && (sl >> 5) == k) hm[k] &= ~(1u << (sl & 31));
+#endif
+    }
     if (DIAG && act) {
       for (int t = 0; t < 32 * FORCE_ST; ++t) {
         const float4 qa = SA[t];
@@ -409,7 +426,6 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FORCE_MINB) k_force(GroupLis
         }
       }
       if (t < 0) break;
-      if (SJ[t] == s) continue;
       const float4 qa = SA[t], qb = SB[t], qc = SC[t];
       const float dx = xi - qa.x, dy = yi - qa.y, dz = zi - qa.z;
       const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
