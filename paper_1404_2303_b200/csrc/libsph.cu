@@ -556,17 +556,15 @@ static void build_union(sph_ctx* c, const float* reach) {
   // node max of the reach (the walk's bound for sources with a large h)
   LAUNCH(k_node_hmax, gridfull((int64_t)c->n_nodes * 32, 256), 256, 0, c->n_nodes, nodes(c), reach);
   ctr_reset(c);
-  LAUNCH(k_hrange, grid1d(c, c->n, 256), 256, 0, reach, c->n, ctr(c));
+  LAUNCH(k_hrange, grid1d(c, c->n, 256), 256, 0, reach, c->n, ctr(c));   // max reach, read by the walk
   unsigned long long h[C_NCOUNTERS];
-  ctr_read(c, h);
-  const float rmax = as_float(h[C_HMAXBITS]);
   const int cap = c->ucap;
   WalkParams P = walk_params(c, reach);
   if (P.raw_out) {
     P.raw_out += 1;
     CUDA_TRY(cudaMemsetAsync(P.raw_out, 0, sizeof(unsigned long long), c->stream));
   }
-  P.reach_max = rmax;
+  P.reach_max_bits = ctr(c) + C_HMAXBITS;
   P.nsel = ng;
   P.sel = group_order(c, reach);
   P.off = B<int64_t>(c, B_GOFF, ng);

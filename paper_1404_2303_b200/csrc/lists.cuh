@@ -103,6 +103,7 @@ struct WalkParams {
   const int* topmap;
   const SortEntry* sorted;
   float reach_max;          // UNION: max source reach (bound for the top-cell range)
+  const unsigned long long* reach_max_bits;   // if set: reach_max as float bits on the device
   float slack;              // absolute slack of the box tests (fp32 rounding of corners)
   // UNION
   int64_t* off;             // per group: list offset (FILL reads)
@@ -562,7 +563,8 @@ __global__ void WALK_BOUNDS k_walk(WalkParams P) {
   int nq = 0;
   if (__any_sync(FULL_MASK, tg)) {
     // top cells (unwrapped indices) overlapping the box grown by the largest possible reach
-    const float Rw = reach_eff(MODE == MODE_NB ? W.R : fmaxf(W.R, P.reach_max), P.slack) + P.slack;
+    const float rmax = P.reach_max_bits ? __uint_as_float((unsigned)*P.reach_max_bits) : P.reach_max;
+    const float Rw = reach_eff(MODE == MODE_NB ? W.R : fmaxf(W.R, rmax), P.slack) + P.slack;
     int a0[3], na[3];
     int T = 1;
 #pragma unroll
