@@ -149,7 +149,7 @@ __device__ __forceinline__ uint8_t hstep(double S0, float S1, float S2, float& h
   }
   // A Halley step of |dx| <= SPH_HSTEP_ACCEPT leaves a residual of order |g3 / g1| dx^3 / 6
   // in ln N (g3 the third derivative; ~1e-7 N here), far inside tol: accept it without
-  // another pass over the list. k_ghost re-checks N(h) at the final h from the density
+  // another pass over the list. The density kernel re-checks N(h) at the final h from its
   // loop's sums, so a wrong acceptance is reported as unconverged, never silently kept.
   if (halley && inb && hn < hcap && fabsf(dx) <= SPH_HSTEP_ACCEPT) return HS_DONE;
   return HS_ACTIVE;

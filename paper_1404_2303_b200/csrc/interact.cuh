@@ -59,7 +59,7 @@ struct DensOut {
   GhostOut g;
 };
 
-// a9 for one target from its density sums (k_density's epilogue and k_ghost)
+// a9 for one target from its density sums (k_density's epilogue)
 __device__ __forceinline__ void ghost_one(const GhostOut& out, uint32_t o, float h, float uu, float smf, float smqfp,
                                           float divs, float crx, float cry, float crz, int cnt, float gamma,
                                           float beps) {
@@ -609,31 +609,6 @@ __global__ void k_state_swap(uint8_t* __restrict__ st, int64_t n, uint8_t from, 
 //   P = (gamma-1) rho u,  c = sqrt(gamma (gamma-1) u),  A = P/(Omega rho^2)
 //   div = sum m (f'/r) dv.dx / (h sum m f),  curl = -sum m (f'/r) dv x dx / (h sum m f)
 //   f = |curl| / (|div| + |curl| + eps c/h)       (R10)
-
-__global__ void k_ghost(int64_t n, const float4* __restrict__ xh, const float* __restrict__ u,
-                        const float4* __restrict__ acc0, const float4* __restrict__ acc1, float gamma, float beps,
-                        const double* __restrict__ sf, float n_t, float tol_check, GhostOut out,
-                        unsigned long long* ctr) {
-  long long nd = 0, nbad = 0;
-  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n;
-       s += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t o = out.perm[s];
-    if (o >= out.n_own) continue;            // halo particle: its owner computes it
-    const float4 a0 = acc0[s], a1 = acc1[s];
-    const int cnt = __float_as_int(a1.w);
-    ghost_one(out, o, xh[s].w, u[s], a0.x, a0.y, a0.w, a1.x, a1.y, a1.z, cnt, gamma, beps);
-    nd += cnt;
-    // the h iteration's convergence, re-checked from the density loop's sum at the final h
-    nbad += fabs((32.0 / 3.0) * sf[s] - (double)n_t) > (double)tol_check ? 1 : 0;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    nd += __shfl_xor_sync(FULL_MASK, nd, o);
-    nbad += __shfl_xor_sync(FULL_MASK, nbad, o);
-  }
-  if ((threadIdx.x & 31) == 0 && nd) atomicAdd(&ctr[C_NDIR], (unsigned long long)nd);
-  if ((threadIdx.x & 31) == 0 && nbad) atomicAdd(&ctr[C_UNCONV], (unsigned long long)nbad);
-}
 
 // force inputs in cell order from the caller-order state (owned: the ghost; halo: imported):
 //   fx = {x, y, z, 1/h},  fs = {A (8/pi) h^-4, rho, c, f},  hr = h (the force list reach)
