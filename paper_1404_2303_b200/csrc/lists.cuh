@@ -35,7 +35,7 @@
 #include "hiter.cuh"
 
 #ifndef WALK_WARPS
-#define WALK_WARPS 4
+#define WALK_WARPS 2
 #endif
 #ifndef WALK_TAKE
 #define WALK_TAKE 64    // a node holding <= WALK_TAKE particles is swept whole (no descent; 32: +0.08 ms, 128: +0.08)
