@@ -244,6 +244,23 @@ int sph_allreduce(sph_ctx* ctx, void* buf, int64_t count, int32_t dtype, int32_t
 int sph_x_histogram(sph_ctx* ctx, int64_t n, const float* x, double lo, double hi, int32_t nbins,
                     int64_t* hist_out);
 
+/* ---- the step around the hot path (first part). Device arrays in the
+ * caller's order; enqueued on the context's stream (synchronised under SPH_F_SYNC).
+ * Velocity-Verlet: kick(dt/2), drift(dt), build + density + force, kick(dt/2). */
+
+/* v[n][3] += a[n][3] dt; u[n] += dudt[n] dt (u and dudt may both be NULL). */
+int sph_kick(sph_ctx* ctx, int64_t n, float* v, float* u, const float* a, const float* dudt, float dt);
+
+/* x[n][3] += v[n][3] dt, wrapped back into [0, L) per axis (requires |v dt| < L). */
+int sph_drift(sph_ctx* ctx, int64_t n, float* x, const float* v, float dt);
+
+/* Eq. 6: dt_i = c_cfl 2 h_i / vsig_i with vsig_i = max_j (c_i + c_j
+ * + max{0, -3 r_ij . v_ij / r_ij}) from sph_force's vsig_out (+inf where vsig = 0).
+ * dt_out [n] (device, or NULL); *dt_min_out (host) = min_i dt_i. The paper uses c_cfl = 1/4
+ * (P:1353). */
+int sph_timestep(sph_ctx* ctx, int64_t n, const float* h, const float* vsig, float c_cfl, float* dt_out,
+                 float* dt_min_out);
+
 /* Number of CUDA kernel launches libsph issued on this context since creation
  * (evidence for the bench's gpu_launches). */
 int64_t sph_kernel_launches(const sph_ctx* ctx);

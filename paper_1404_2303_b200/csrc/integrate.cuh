@@ -1,0 +1,46 @@
+// integrate.cuh — the step around the hot path (first part): velocity-Verlet
+// kick and drift of the particles ("integrated using a velocity-Verlet
+// integrator") and the per-particle time step of Eq. 6,
+//   dt_i = C_CFL 2 h_i / max_j (c_i + c_j + max{0, -3 r_ij . v_ij / r_ij}) = C_CFL 2 h_i / vsig_i,
+// with vsig from the force loop (k_force). Arrays in the caller's order, device memory.
+#pragma once
+#include "common.cuh"
+
+// kick: v += a dt, u += du/dt dt
+__global__ void k_kick(int64_t n, float* __restrict__ v, float* __restrict__ u, const float* __restrict__ a,
+                       const float* __restrict__ dudt, float dt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    v[3 * i] = fmaf(a[3 * i], dt, v[3 * i]);
+    v[3 * i + 1] = fmaf(a[3 * i + 1], dt, v[3 * i + 1]);
+    v[3 * i + 2] = fmaf(a[3 * i + 2], dt, v[3 * i + 2]);
+    if (u) u[i] = fmaf(dudt[i], dt, u[i]);
+  }
+}
+
+// drift: x += v dt, wrapped back into [0, L) (periodic box); |v dt| < L
+__device__ __forceinline__ float wrap1(float x, float L) {
+  if (x >= L) x -= L;
+  if (x < 0.f) x += L;
+  return (x >= L || x < 0.f) ? 0.f : x;   // a rounding onto L itself lands on 0
+}
+__global__ void k_drift(int64_t n, float* __restrict__ x, const float* __restrict__ v, float dt, float Lx, float Ly,
+                        float Lz) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[3 * i] = wrap1(fmaf(v[3 * i], dt, x[3 * i]), Lx);
+    x[3 * i + 1] = wrap1(fmaf(v[3 * i + 1], dt, x[3 * i + 1]), Ly);
+    x[3 * i + 2] = wrap1(fmaf(v[3 * i + 2], dt, x[3 * i + 2]), Lz);
+  }
+}
+
+// Eq. 6 per particle (optional output) and its minimum (float bits, atomicMin on positives)
+__global__ void k_timestep(int64_t n, const float* __restrict__ h, const float* __restrict__ vsig, float c_cfl,
+                           float* __restrict__ dt_out, unsigned* __restrict__ dt_min_bits) {
+  unsigned mn = 0x7f800000u;   // +inf
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float dt = vsig[i] > 0.f ? c_cfl * 2.f * h[i] / vsig[i] : INFINITY;
+    if (dt_out) dt_out[i] = dt;
+    mn = min(mn, __float_as_uint(dt));
+  }
+  mn = __reduce_min_sync(FULL_MASK, mn);
+  if ((threadIdx.x & 31) == 0) atomicMin(dt_min_bits, mn);
+}

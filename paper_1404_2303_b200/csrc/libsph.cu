@@ -15,6 +15,7 @@
 #include "lists.cuh"
 #include "interact.cuh"
 #include "comm.cuh"
+#include "integrate.cuh"
 
 // =========================================================== memory =============
 static void* dev_alloc(sph_ctx* c, size_t bytes) {
@@ -1321,6 +1322,51 @@ int sph_x_histogram(sph_ctx* ctx, int64_t n, const float* x, double lo, double h
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ time step ---------
+// SURVEY 8(f) f1 (first part): velocity-Verlet kick / drift and the Eq. 6 time step on the
+// caller's device arrays; the density and force calls in between are the hot path.
+
+int sph_kick(sph_ctx* ctx, int64_t n, float* v, float* u, const float* a, const float* dudt, float dt) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(n >= 0 && (n == 0 || (v && a)) && (!u || dudt), SPH_E_ARG, "bad argument");
+  SPH_REQUIRE(n == 0 || (is_device_ptr(v) && is_device_ptr(a) && (!u || (is_device_ptr(u) && is_device_ptr(dudt)))),
+              SPH_E_ARG, "sph_kick: arrays must be device memory");
+  if (n > 0) LAUNCH(k_kick, grid1d(c, n, 256), 256, 0, n, v, u, a, dudt, dt);
+  if (c->cfg.flags & SPH_F_SYNC) sync(c);
+  API_END
+  return SPH_OK;
+}
+
+int sph_drift(sph_ctx* ctx, int64_t n, float* x, const float* v, float dt) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(n >= 0 && (n == 0 || (x && v)), SPH_E_ARG, "bad argument");
+  SPH_REQUIRE(n == 0 || (is_device_ptr(x) && is_device_ptr(v)), SPH_E_ARG, "sph_drift: arrays must be device memory");
+  if (n > 0)
+    LAUNCH(k_drift, grid1d(c, n, 256), 256, 0, n, x, v, dt, (float)c->cfg.box[0], (float)c->cfg.box[1],
+           (float)c->cfg.box[2]);
+  if (c->cfg.flags & SPH_F_SYNC) sync(c);
+  API_END
+  return SPH_OK;
+}
+
+int sph_timestep(sph_ctx* ctx, int64_t n, const float* h, const float* vsig, float c_cfl, float* dt_out,
+                 float* dt_min_out) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(n > 0 && h && vsig && dt_min_out && c_cfl > 0.f, SPH_E_ARG, "bad argument");
+  SPH_REQUIRE(is_device_ptr(h) && is_device_ptr(vsig) && (!dt_out || is_device_ptr(dt_out)), SPH_E_ARG,
+              "sph_timestep: arrays must be device memory");
+  unsigned* mb = B<unsigned>(c, B_TSTEP, 1);
+  const unsigned inf = 0x7f800000u;
+  CUDA_TRY(cudaMemcpyAsync(mb, &inf, sizeof(unsigned), cudaMemcpyHostToDevice, c->stream));
+  LAUNCH(k_timestep, grid1d(c, n, 256), 256, 0, n, h, vsig, c_cfl, dt_out, mb);
+  unsigned r = 0;
+  CUDA_TRY(cudaMemcpyAsync(&r, mb, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  memcpy(dt_min_out, &r, 4);
+  API_END
+  return SPH_OK;
+}
 
 // ------------------------------------------------------------------ NCCL transport ---
 // The ring of slabs: rank r exchanges with lower = r - 1 and upper = r + 1

@@ -72,7 +72,7 @@ EXPORTS = ("sph_config_default", "sph_create", "sph_destroy", "sph_set_allocator
            "sph_status_string", "sph_last_error", "sph_build_cells", "sph_density", "sph_force",
            "sph_kernel_launches", "sph_build_cells_halo", "sph_halo_select", "sph_export_state",
            "sph_import_halo_state", "sph_x_histogram", "sph_guess_h", "sph_comm_unique_id", "sph_comm_init",
-           "sph_halo_counts", "sph_halo_exchange", "sph_allreduce")
+           "sph_halo_counts", "sph_halo_exchange", "sph_allreduce", "sph_kick", "sph_drift", "sph_timestep")
 
 
 def load(path: str | None = None):
@@ -110,6 +110,9 @@ def load(path: str | None = None):
     lib.sph_halo_counts.argtypes = [P, i64, i64, P, P]
     lib.sph_halo_exchange.argtypes = [P, ctypes.c_int32, P, i64, P, i64, P, i64, P, i64]
     lib.sph_allreduce.argtypes = [P, P, i64, ctypes.c_int32, ctypes.c_int32]
+    lib.sph_kick.argtypes = [P, i64, P, P, P, P, ctypes.c_float]
+    lib.sph_drift.argtypes = [P, i64, P, P, ctypes.c_float]
+    lib.sph_timestep.argtypes = [P, i64, P, P, ctypes.c_float, P, P]
     if path == LIB or path is None:
         _lib = lib
     return lib
@@ -285,6 +288,22 @@ class Context:
         self._check(self.lib.sph_allreduce(self.h, t.data_ptr() if t.numel() else None, int(t.numel()), dt,
                                            {"sum": 0, "max": 1}[op]))
         return t
+
+    # -- the step around the hot path (include/sph.h sph_kick / sph_drift / sph_timestep) ----
+    def kick(self, v, a, dt, u=None, dudt=None):
+        self._check(self.lib.sph_kick(self.h, int(v.shape[0]), _ptr(v), _ptr(u), _ptr(a), _ptr(dudt), float(dt)))
+
+    def drift(self, x, v, dt):
+        self._check(self.lib.sph_drift(self.h, int(x.shape[0]), _ptr(x), _ptr(v), float(dt)))
+
+    def timestep(self, h, vsig, c_cfl=0.25, per_particle=False):
+        """Eq. 6: min_i C_CFL 2 h_i / vsig_i (and the per-particle dt if asked)."""
+        import torch
+        out = torch.empty_like(h) if per_particle else None
+        dmin = ctypes.c_float()
+        self._check(self.lib.sph_timestep(self.h, int(h.shape[0]), _ptr(h), _ptr(vsig), float(c_cfl), _ptr(out),
+                                          ctypes.byref(dmin)))
+        return (dmin.value, out) if per_particle else dmin.value
 
     def density(self, v, m, u, out=None, stats: Stats | None = None, check=True):
         """out: dict of preallocated output arrays (h, rho, omega, n_nbr, div, curl)."""
