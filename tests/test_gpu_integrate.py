@@ -97,3 +97,23 @@ def test_leapfrog_energy_error_is_second_order():
     e1 = abs(_run(p, 0.1, t_end=t_end)["dE"])
     e2 = abs(_run(p, 0.05, t_end=t_end)["dE"])
     assert e1 / e2 >= 2.8, (e1, e2)
+
+
+def test_sod_shock_against_exact_solution():
+    """The paper's Sod-shock test (rho 4 / 1, P 1 / 0.1795) in a 2x1x1 periodic
+    box of two cubic lattices, evolved to t = 0.1 with the velocity-Verlet loop: the SPH
+    density at both interfaces (one mirrored through the periodic wrap) matches the exact
+    Riemann solution (tests/sod_exact.py, pinned in test_sod_exact.py) to a few percent in
+    L1, the error falls with resolution, and mass, momentum and energy are conserved."""
+    import sys, os
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import sod_run
+    lo = sod_run.run(24, 0.1)
+    hi = sod_run.run(48, 0.1)
+    for r in (lo, hi):
+        assert abs(r["L1_rho_interface_1"] - r["L1_rho_interface_0"]) < 1e-3    # periodic symmetry
+        assert abs(r["dE_over_E"]) < 1e-3
+        assert r["dP_max"] < 1e-6
+    assert lo["L1_rho_interface_1"] < 0.04
+    assert hi["L1_rho_interface_1"] < 0.025
+    assert hi["L1_rho_interface_1"] < 0.8 * lo["L1_rho_interface_1"]
