@@ -166,7 +166,7 @@ struct sph_ctx {
   DBuf b[80];
   cudaEvent_t ev[12];
   cudaStream_t stream2 = nullptr;   // side stream: host->device copies overlapped with the h iteration
-  cudaEvent_t ev_side[2];
+  cudaEvent_t ev_side[4];   // [0] side stream may start, [1] v, m, u copied, [2] h ready, [3] h copied back
   bool ev_ok = false;
 };
 

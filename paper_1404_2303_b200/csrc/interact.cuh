@@ -78,7 +78,7 @@ __device__ __forceinline__ void ghost_one(const GhostOut& out, uint32_t o, float
   const float fb = cn / (fabsf(div) + cn + beps * c * hinv);
   out.h_o[o] = h;
   out.g_o[o] = make_float4(A, rho, c, fb);
-  out.h[o] = h;
+  if (out.h) out.h[o] = h;
   out.rho[o] = rho;
   if (out.omega) out.omega[o] = omega;
   if (out.nnbr) out.nnbr[o] = cnt;
@@ -707,6 +707,15 @@ __global__ void k_gather_vmu(const uint32_t* __restrict__ perm, int64_t n, const
     const uint32_t p = perm[s];
     vm[s] = make_float4(v[3 * (int64_t)p], v[3 * (int64_t)p + 1], v[3 * (int64_t)p + 2], m[p]);
     uc[s] = u[p];
+  }
+}
+
+// h of the owned particles in caller order (the early copy-back of sph_density)
+__global__ void k_scatter_h_own(const uint32_t* __restrict__ perm, int64_t n, int64_t n_own,
+                                const float4* __restrict__ xh, float* __restrict__ h_o) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t o = perm[s];
+    if (o < n_own) h_o[o] = xh[s].w;
   }
 }
 

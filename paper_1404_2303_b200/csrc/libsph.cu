@@ -626,6 +626,17 @@ static GroupLists group_lists(sph_ctx* c) {
 }
 
 // =========================================================== inputs =============
+// page-locked host memory (cudaMallocHost / cudaHostRegister): copies to it are asynchronous
+static bool is_pinned_host_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 static bool is_device_ptr(const void* p) {
   if (!p) return false;
   cudaPointerAttributes a;
@@ -771,7 +782,7 @@ int sph_create(const sph_config* cfg, int dev, void* stream, sph_ctx** out) {
     }
     for (int i = 0; i < 12; ++i) CUDA_TRY(cudaEventCreate(&c->ev[i]));
     CUDA_TRY(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
-    for (int i = 0; i < 2; ++i) CUDA_TRY(cudaEventCreateWithFlags(&c->ev_side[i], cudaEventDisableTiming));
+    for (int i = 0; i < 4; ++i) CUDA_TRY(cudaEventCreateWithFlags(&c->ev_side[i], cudaEventDisableTiming));
     float dirs[14][3];
     for (int d = 0; d < 13; ++d) {
       const int k = d + 14;
@@ -804,7 +815,7 @@ int sph_destroy(sph_ctx* c) {
   for (int i = 0; i < 80; ++i) dev_free(c, c->b[i].p);
   if (c->ev_ok) {
     for (int i = 0; i < 12; ++i) cudaEventDestroy(c->ev[i]);
-    for (int i = 0; i < 2; ++i) cudaEventDestroy(c->ev_side[i]);
+    for (int i = 0; i < 4; ++i) cudaEventDestroy(c->ev_side[i]);
     cudaStreamDestroy(c->stream2);
   }
   for (auto& t : c->timed) {
@@ -1035,7 +1046,27 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
     }
   }
   CUDA_TRY(cudaEventRecord(c->ev[7], c->stream));
-  // join the side-stream copies; validate and gather v, m, u into cell order
+  // a7 (first half): the interaction lists need only x and the final h (reach max(h_i, h_j)
+  // with the owned particles' h; these are the force lists too when there is no halo), so
+  // they are built while the side stream still copies v, m, u from the host
+  float* hr = Bget<float>(c, B_HRCH);
+  LAUNCH(k_reach_owned, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, c->n_own, Bget<float4>(c, B_XH),
+         hr);
+  build_union(c, hr);
+  c->force_lists = c->n == c->n_own;
+  // h is final: a pinned host h_out is copied back on the side stream during the density
+  // loop (the ghost then skips h; a pageable copy would block the host)
+  const bool h_early = is_pinned_host_ptr(h_out);
+  if (h_early) {
+    float* hs = B<float>(c, B_OUT0, c->n_own);
+    LAUNCH(k_scatter_h_own, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, c->n_own, Bget<float4>(c, B_XH),
+           hs);
+    CUDA_TRY(cudaEventRecord(c->ev_side[2], c->stream));
+    CUDA_TRY(cudaStreamWaitEvent(c->stream2, c->ev_side[2], 0));
+    CUDA_TRY(cudaMemcpyAsync(h_out, hs, c->n_own * sizeof(float), cudaMemcpyDeviceToHost, c->stream2));
+    CUDA_TRY(cudaEventRecord(c->ev_side[3], c->stream2));
+  }
+  // join the side-stream copies of v, m, u; validate and gather them into cell order
   if (side) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_side[1], 0));
   ctr_reset(c);
   LAUNCH(k_validate_vmu, grid1d(c, n, 256), 256, 0, vd, md, ud, n, ctr(c));
@@ -1046,18 +1077,11 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_NONFINITE), SPH_E_DOMAIN, "non-finite velocity");
   SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_MASS), SPH_E_DOMAIN, "mass <= 0 or non-finite");
   SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_U), SPH_E_DOMAIN, "internal energy <= 0 or non-finite");
-  // a7: the density loop at the final h over the interaction lists (reach max(h_i, h_j)
-  // with the owned particles' h; these are the force lists too when there is no halo)
-  float* hr = Bget<float>(c, B_HRCH);
-  LAUNCH(k_reach_owned, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, c->n_own, Bget<float4>(c, B_XH),
-         hr);
-  build_union(c, hr);
-  c->force_lists = c->n == c->n_own;
   // a9 ghost fused into the density kernel: the caller-order outputs and the force state
   std::vector<OutMap> maps;
   GhostOut go;
   const int64_t no = c->n_own;
-  go.h = dev_out(c, h_out, no, B_OUT0, maps);
+  go.h = h_early ? nullptr : dev_out(c, h_out, no, B_OUT0, maps);
   go.rho = dev_out(c, rho_out, no, B_OUT1, maps);
   go.omega = dev_out(c, omega_out, no, B_OUT2, maps);
   go.nnbr = dev_out(c, n_nbr_out, no, B_OUT3, maps);
@@ -1089,7 +1113,9 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
            Bget<uint32_t>(c, B_PERM), c->n_own, box3(c), dout, ctr(c));
   }
   CUDA_TRY(cudaEventRecord(c->ev[9], c->stream));
+  if (h_early) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_side[3], 0));   // the call ends after the h copy
   flush_out(c, maps, c->ev[3]);
+  if (h_early) CUDA_TRY(cudaStreamSynchronize(c->stream2));
   c->state = 2;
   bool noconv = unconv > 0;
   ctr_read(c, hc);
