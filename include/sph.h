@@ -51,7 +51,10 @@ typedef enum {
   SPH_E_DOMAIN = -2, /* non-finite input; x outside [0,L); m <= 0; u <= 0; h0 < 0;
                         a smoothing length >= min(L)/2 (minimum image) */
   SPH_E_STATE = -3,  /* order violated: density before build_cells, force before density */
-  SPH_E_NOCONV = -4, /* h iteration hit max_h_iter; all outputs written from the last iterate */
+  SPH_E_NOCONV = -4, /* h iteration did not converge: it hit max_h_iter, Eq. 3 has no root for a
+                        particle (more than 4 coincident particles, or too few within L/2: R23),
+                        or the density loop's re-check of N(h) failed (R4); every output is
+                        written (finite) from the last iterate; stats.n_unconverged counts them */
   SPH_E_CUDA = -5,
   SPH_E_NCCL = -6,
   SPH_E_OOM = -7
@@ -154,8 +157,9 @@ int sph_build_cells(sph_ctx* ctx, int64_t n, const float* x, const float* h0);
 
 /* 2. Density loop (Eq. 2-3) with h_i solved to N_i = n_ngb +- tol by a
  *    bracketed Newton/Halley iteration (R3-R4) on each particle's recorded
- *    neighbour list; particles whose root lies beyond their list are re-walked with a larger
- *    h_build. Then the sums of Eq. 2 at the final h over the interaction lists (reach
+ *    neighbour list (run inside the build's walk; particles whose root lies beyond their
+ *    list are re-walked with a larger h_build). Then the sums of Eq. 2 at the final h over
+ *    the interaction lists (reach
  *    max(h_i, h_j)) and the "ghost" step: Omega, P, c,
  *    A = P/(Omega rho^2), div/curl v and Balsara f, kept inside ctx.
  *    v [n][3], m [n] (> 0), u [n] (> 0): copied.
