@@ -251,6 +251,29 @@ class Context:
                                              _ptr(out, np.int64)))
         return out
 
+    # -- allocator hook (include/sph.h sph_set_allocator) ---------------------------
+    def use_torch_allocator(self):
+        """Route libsph's device buffers through torch's caching allocator (before the first
+        build). The callbacks count allocations and releases (self.alloc_counts)."""
+        import torch
+        dev = torch.cuda.current_device()
+        self.alloc_counts = {"alloc": 0, "free": 0, "bytes": 0}
+        AF = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+        RF = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
+
+        def _alloc(nbytes, stream, user):
+            self.alloc_counts["alloc"] += 1
+            self.alloc_counts["bytes"] += int(nbytes)
+            return torch.cuda.caching_allocator_alloc(int(nbytes), dev, int(stream or 0))
+
+        def _free(ptr, stream, user):
+            self.alloc_counts["free"] += 1
+            torch.cuda.caching_allocator_delete(int(ptr))
+
+        self._alloc_cbs = (AF(_alloc), RF(_free))            # kept alive with the context
+        self._check(self.lib.sph_set_allocator(self.h, ctypes.cast(self._alloc_cbs[0], ctypes.c_void_p),
+                                               ctypes.cast(self._alloc_cbs[1], ctypes.c_void_p), None))
+
     # -- NCCL transport of the slab ring (include/sph.h) ------------------------------
     @staticmethod
     def comm_unique_id() -> bytes:

@@ -149,3 +149,32 @@ def test_diagnostic_counts(case):
     g0 = P.run_gpu(p, **BENCH_CFG)
     for k in ("h", "rho", "a", "dudt"):
         assert np.array_equal(g[k], g0[k]), k
+
+
+def test_torch_caching_allocator_hook():
+    """sph_set_allocator: every libsph device buffer through torch's caching
+    allocator gives bit-identical results, and every allocation is released at close."""
+    import torch
+
+    import paper_1404_2303_b200 as sph
+    p = workloads.c1()
+    dev = torch.device("cuda:0")
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+    def run(hook):
+        ctx = sph.Context(sph.default_config(p.box, n_ngb_tol=1e-4, **BENCH_CFG))
+        if hook:
+            ctx.use_torch_allocator()
+        ctx.build_cells(t(p.x))
+        d = ctx.density(t(p.v), t(p.m), t(p.u))
+        f = ctx.force(t(p.v))
+        out = (d.h.clone(), d.rho.clone(), f.a.clone())
+        counts = getattr(ctx, "alloc_counts", None)
+        ctx.close()
+        return out, counts
+
+    ref, _ = run(False)
+    got, counts = run(True)
+    for a, b in zip(ref, got):
+        assert torch.equal(a, b)
+    assert counts["alloc"] > 10 and counts["free"] == counts["alloc"]
