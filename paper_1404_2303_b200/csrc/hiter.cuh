@@ -11,7 +11,7 @@
 
 #define HS_OVF 3   // repeat overflow: needs an exactly sized list in the overflow pool
 #ifndef HSOLVE_LONG
-#define HSOLVE_LONG 128  // lists longer than this are solved by the whole warp
+#define HSOLVE_LONG 256  // lists longer than this are solved by the whole warp
 #endif
 
 // counters of a solve (device, read once per round): unconverged, re-walks, pool, max iterations
