@@ -183,6 +183,10 @@ __device__ __forceinline__ void warp_hsolve(bool act, const float* r2l, int64_t 
       const float he = H.hbs * cbrtf(n_t / (float)cnt);
       if (he > H.l && he < H.u && he <= H.hbs) H.h = he;
     }
+    // N(h) is exact on the list only for h <= h_build: never start beyond it (a list
+    // recorded below the initial h, e.g. a cold margin < 1, would otherwise set a false
+    // lower bracket from a truncated sum)
+    H.h = fminf(H.h, H.hbs);
   }
   const bool shortl = act && H.st == HS_ACTIVE && cnt <= HSOLVE_LONG;
   if (shortl) {

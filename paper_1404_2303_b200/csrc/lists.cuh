@@ -64,6 +64,9 @@
 #ifndef UNION_PACKED
 #define UNION_PACKED 1  // interaction-list walk: packed FP32 pair tests (tools/sweep.sh)
 #endif
+#ifndef RANGE_MASK
+#define RANGE_MASK 1
+#endif
 #ifndef SPHERE_VOTE
 #define SPHERE_VOTE 4   // node-vs-target-sphere tests between warp votes for an early exit
 #endif
@@ -407,6 +410,7 @@ __device__ __forceinline__ void flush_ranges(const WalkParams& P, WalkState& W, 
     const bool v = gi < total;
     // range starts inside [b0, b0 + 32) as a bit mask (queued ranges are never empty, so
     // starts are distinct): lane gi lies in range rs + #{starts <= gi}
+#if RANGE_MASK
     unsigned bm = 0u;
     if (rs + 1 + lane < nq) {
       const int B = S.rq_pre[rs + 1 + lane];
@@ -415,6 +419,12 @@ __device__ __forceinline__ void flush_ranges(const WalkParams& P, WalkState& W, 
     bm = __reduce_or_sync(FULL_MASK, bm);
     const int r = rs + __popc(bm & (lanemask_lt() | (1u << lane)));
     rs += __popc(bm);
+#else
+    int r = 0;                                    // rq_pre[r] <= gi < rq_pre[r+1]
+#pragma unroll
+    for (int step = 32; step > 0; step >>= 1)
+      if (r + step < nq && S.rq_pre[r + step] <= gi) r += step;
+#endif
     int j = 0, code = 0;
     float3 p = make_float3(0.f, 0.f, 0.f);
     float hj = 0.f;

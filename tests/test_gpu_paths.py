@@ -178,3 +178,13 @@ def test_torch_caching_allocator_hook():
     for a, b in zip(ref, got):
         assert torch.equal(a, b)
     assert counts["alloc"] > 10 and counts["free"] == counts["alloc"]
+
+
+@pytest.mark.parametrize("margin", ["0.8", "1.3"])
+def test_cold_margin_below_and_above_the_guess(margin):
+    """Neighbour lists recorded below the initial guess (cold margin < 1: most particles
+    re-walk) or well above it: the h iteration never evaluates N(h) beyond a recorded list,
+    and every particle converges to the oracle's root."""
+    p = workloads.tiny(12, n=6000, clump_frac=0.4, n_dup=2)
+    p.h0[:] = 0.0
+    _check(p, env={"SPH_COLD_MARGIN": margin}, **BENCH_CFG)
