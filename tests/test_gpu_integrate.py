@@ -117,3 +117,24 @@ def test_sod_shock_against_exact_solution():
     assert lo["L1_rho_interface_1"] < 0.04
     assert hi["L1_rho_interface_1"] < 0.025
     assert hi["L1_rho_interface_1"] < 0.8 * lo["L1_rho_interface_1"]
+
+
+def test_sedov_blast_self_similar_radius():
+    """The paper's Sedov blast on a 32^3-cell FCC lattice (131,072 particles,
+    rho = 1, cold background, E = 1 in the ~30 central particles), evolved to t = 0.05 with
+    the velocity-Verlet loop. The shock radius (leading edge of the radially binned SPH
+    density) follows the Sedov-Taylor law R = xi0 (E t^2 / rho)^(1/5), xi0 = 1.152 for
+    gamma = 5/3 (the published Sedov constant), within 8 % at the end, and grows as t^(2/5)
+    (dimensional analysis) late in the run; the peak compression stays below the
+    strong-shock limit (gamma+1)/(gamma-1) = 4; energy is conserved."""
+    import os, sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import sedov_run
+    r = sedov_run.run(32, 0.05)
+    T, R, peak = r["snapshots"][-1]
+    assert 0.95 <= R / (1.152 * (T * T) ** 0.2) <= 1.08
+    late = r["snapshots"][2:]
+    slope = np.polyfit(np.log([s[0] for s in late]), np.log([s[1] for s in late]), 1)[0]
+    assert 0.36 <= slope <= 0.46, slope
+    assert all(1.5 < s[2] < 4.0 for s in r["snapshots"])
+    assert abs(r["dE_over_E"]) < 3e-3
