@@ -52,7 +52,7 @@ typedef enum {
                         a smoothing length >= min(L)/2 (minimum image) */
   SPH_E_STATE = -3,  /* order violated: density before build_cells, force before density */
   SPH_E_NOCONV = -4, /* h iteration did not converge: it hit max_h_iter, Eq. 3 has no root for a
-                        particle (more than 4 coincident particles, or too few within L/2: R23),
+                        particle (more than 4 coincident particles, or too few within L/2: R24),
                         or the density loop's re-check of N(h) failed (R4); every output is
                         written (finite) from the last iterate; stats.n_unconverged counts them */
   SPH_E_CUDA = -5,

@@ -13,6 +13,9 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
+    # flush-to-zero, approximate rcp / sqrt: SURVEY R23 allows both (no value is near
+    # denormal; MUFU rcp / rsqrt are a few ulp); density + force -3.5 %, parity unchanged
+    "-use_fast_math",
     "-Xptxas", "-v",
 ]
 
