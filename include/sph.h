@@ -248,6 +248,15 @@ int sph_allreduce(sph_ctx* ctx, void* buf, int64_t count, int32_t dtype, int32_t
 int sph_x_histogram(sph_ctx* ctx, int64_t n, const float* x, double lo, double hi, int32_t nbins,
                     int64_t* hist_out);
 
+/* ---- active subset (the paper's multiple time-stepping: only active
+ * particles are "included in the density and force calculations"). active [n] (caller
+ * order, device or host; copied), 1 = target, 0 = source only; NULL clears it (all
+ * active). Applies from the next sph_build_cells, which must then get h0 (the inactive
+ * particles' current h). Inactive particles keep their h, their sph_density state (the
+ * A, rho, c, f of their last evaluation, used as sources by sph_force) and their output
+ * entries: with a mask, outputs must be device arrays (SPH_E_ARG otherwise). */
+int sph_set_active(sph_ctx* ctx, int64_t n, const uint8_t* active);
+
 /* ---- the step around the hot path (first part). Device arrays in the
  * caller's order; enqueued on the context's stream (synchronised under SPH_F_SYNC).
  * Velocity-Verlet: kick(dt/2), drift(dt), build + density + force, kick(dt/2). */

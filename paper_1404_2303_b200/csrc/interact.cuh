@@ -98,8 +98,9 @@ template <bool NONLY, bool DIAG = false>
 #endif
 __global__ void __launch_bounds__(DENS_WARPS * 32, DENS_MINB) k_density(GroupLists G, const float4* __restrict__ xh,
                                                              const float4* __restrict__ vm,
-                                                             const uint32_t* __restrict__ perm, int64_t n_own,
-                                                             float3 Lbox, DensOut out, unsigned long long* ctr) {
+                                                             const uint32_t* __restrict__ perm,
+                                                             const uint8_t* __restrict__ tgt, float3 Lbox,
+                                                             DensOut out, unsigned long long* ctr) {
   __shared__ float4 sp[DENS_WARPS][32 * DENS_ST];   // x, y, z (group frame), m
   __shared__ float4 sv[DENS_WARPS][32 * DENS_ST];   // vx, vy, vz, j (int bits)
   __shared__ __align__(8) float sxyz[DENS_WARPS][3][32 * DENS_ST];   // x, y, z again (SoA, packed tests)
@@ -108,7 +109,7 @@ __global__ void __launch_bounds__(DENS_WARPS * 32, DENS_MINB) k_density(GroupLis
   if (gid >= G.ngroups) return;
   const int4 grp = G.groups[gid];
   const int s = grp.y + lane;
-  const bool act = lane < grp.z && perm[s] < (uint32_t)n_own;   // halo particles: sources only
+  const bool act = lane < grp.z && tgt[s];   // halo and inactive particles: sources only
   if (!__any_sync(FULL_MASK, act)) return;
   const float L[3] = {Lbox.x, Lbox.y, Lbox.z};
   const float4 o4 = xh[grp.y];
@@ -281,6 +282,7 @@ struct ForceOut {
   int* nnbr;       // [n] or null
   const uint32_t* perm;
   int64_t n_own;
+  const uint8_t* tgt;   // cell order: 1 = target (owned and active)
 };
 
 // Eq. 4-5 + Monaghan-Balsara viscosity, symmetric pair scalar
@@ -307,7 +309,7 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FORCE_MINB) k_force(GroupLis
   if (gid >= G.ngroups) return;
   const int4 grp = G.groups[gid];
   const int s = grp.y + lane;
-  const bool act = lane < grp.z && out.perm[s] < (uint32_t)out.n_own;   // halo particles: sources only
+  const bool act = lane < grp.z && out.tgt[s];   // halo and inactive particles: sources only
   if (!__any_sync(FULL_MASK, act)) return;
   const float L[3] = {Lbox.x, Lbox.y, Lbox.z};
   const float4 o4 = fx[grp.y];
@@ -630,11 +632,11 @@ __global__ void k_gather_force(const uint32_t* __restrict__ perm, int64_t n, con
 
 // iteration state in cell order: owned particles active (bracket (0, inf), h_build =
 // h * margin), halo (source-only) particles done
-__global__ void k_init_iter(const uint32_t* __restrict__ perm, int64_t n, int64_t n_own, const float4* __restrict__ xh,
+__global__ void k_init_iter(const uint8_t* __restrict__ tgt, int64_t n, const float4* __restrict__ xh,
                             float margin, float hcap, uint8_t* __restrict__ st, float* __restrict__ hb,
                             float* __restrict__ lo, float* __restrict__ hi) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
-    const bool own = perm[s] < n_own;
+    const bool own = tgt[s] != 0;   // targets iterate; halo and inactive particles keep their h
     st[s] = own ? HS_ACTIVE : HS_DONE;
     if (hb) hb[s] = own ? fminf(xh[s].w * margin, hcap) : 0.f;
     lo[s] = 0.f;
@@ -724,4 +726,13 @@ __global__ void k_scatter_h(const uint32_t* __restrict__ perm, int64_t n, const 
                             float* __restrict__ h_o) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x)
     h_o[perm[s]] = xh[s].w;
+}
+
+// cell-order target flags: owned (caller index < n_own) and active (caller mask, or all)
+__global__ void k_make_tgt(const uint32_t* __restrict__ perm, int64_t n, int64_t n_own,
+                           const uint8_t* __restrict__ active, uint8_t* __restrict__ tgt) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t o = perm[s];
+    tgt[s] = (o < n_own && (!active || active[o])) ? 1 : 0;
+  }
 }

@@ -418,6 +418,7 @@ static WalkParams walk_params(sph_ctx* c, const float* reach) {
   P.reach = reach;
   P.perm = Bget<uint32_t>(c, B_PERM);
   P.n_own = c->n_own;
+  P.tgt = Bget<uint8_t>(c, B_TGT);
   P.N = nodes(c);
   P.g = level_geom(c);
   P.topmap = Bget<int>(c, B_TOPMAP);
@@ -871,6 +872,8 @@ static bool load_inputs(sph_ctx* c, const float* x, const float* h0, float* h0ma
 int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const float* x, const float* h0) {
   API_BEGIN(ctx)
   SPH_REQUIRE(n_own > 0 && n_halo >= 0 && x, SPH_E_ARG, "n_own <= 0, n_halo < 0 or x == NULL");
+  SPH_REQUIRE(!c->has_active || (h0 && c->n_active_for == n_own), SPH_E_ARG,
+              "an active mask (sph_set_active) needs h0 (the inactive particles' h) and n_own particles");
   const int64_t n = n_own + n_halo;
   SPH_REQUIRE(n <= (1ll << SPH_IDX_BITS), SPH_E_ARG, "n > 2^27 particles in one context");
   c->n = n;
@@ -925,7 +928,10 @@ int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const floa
     B<float>(c, B_NBOVF, 1);
     c->ovf_used = 0;
     c->n_ovfidx = 0;
-    LAUNCH(k_init_iter, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, c->n_own, Bget<float4>(c, B_XH),
+    // targets: owned and active (sph_set_active); everything else is a source only
+    LAUNCH(k_make_tgt, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, c->n_own,
+           c->has_active ? Bget<uint8_t>(c, B_ACTIVE) : (const uint8_t*)nullptr, B<uint8_t>(c, B_TGT, n));
+    LAUNCH(k_init_iter, grid1d(c, n, 256), 256, 0, Bget<uint8_t>(c, B_TGT), n, Bget<float4>(c, B_XH),
            margin, h_cap(c), Bget<uint8_t>(c, B_STATE), hb, Bget<float>(c, B_HLO), Bget<float>(c, B_HHI));
   }
   // neighbour lists of the h iteration: r^2 < h_build^2 per particle
@@ -953,6 +959,11 @@ static void fill_struct_stats(sph_ctx* c, sph_stats* st) {
 int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, float* h_out, float* rho_out,
                 float* omega_out, int32_t* n_nbr_out, float* div_out, float* curl_out, sph_stats* st) {
   API_BEGIN(ctx)
+  if (c->has_active) {   // inactive entries are left as they are: only device outputs can be
+    const void* outs[6] = {h_out, rho_out, omega_out, n_nbr_out, div_out, curl_out};
+    for (const void* o : outs)
+      SPH_REQUIRE(!o || is_device_ptr(o), SPH_E_ARG, "with an active mask the outputs must be device arrays");
+  }
   SPH_REQUIRE(c->state >= 1, SPH_E_STATE, "sph_density before sph_build_cells");
   SPH_REQUIRE(v && m && u && h_out && rho_out, SPH_E_ARG, "required pointer is NULL");
   const int64_t n = c->n;
@@ -985,7 +996,7 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
 
   uint8_t* state = Bget<uint8_t>(c, B_STATE);
   if (c->state >= 2) {   // a repeated call: iterate again from the current h (lists stay valid)
-    LAUNCH(k_init_iter, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, c->n_own, Bget<float4>(c, B_XH),
+    LAUNCH(k_init_iter, grid1d(c, n, 256), 256, 0, Bget<uint8_t>(c, B_TGT), n, Bget<float4>(c, B_XH),
            1.0f, h_cap(c), state, (float*)nullptr, Bget<float>(c, B_HLO), Bget<float>(c, B_HHI));
   }
   // a8: the h iteration, per particle on its neighbour list; re-walk particles whose root
@@ -1110,7 +1121,7 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
     const bool diag = (c->cfg.flags & SPH_F_DIAGNOSTICS) != 0;
     auto kd = diag ? k_density<false, true> : k_density<false, false>;
     LAUNCH(kd, gridfull(G.ngroups, DENS_WARPS), DENS_WARPS * 32, 0, G, Bget<float4>(c, B_XH), vm,
-           Bget<uint32_t>(c, B_PERM), c->n_own, box3(c), dout, ctr(c));
+           Bget<uint32_t>(c, B_PERM), Bget<uint8_t>(c, B_TGT), box3(c), dout, ctr(c));
   }
   CUDA_TRY(cudaEventRecord(c->ev[9], c->stream));
   if (h_early) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_side[3], 0));   // the call ends after the h copy
@@ -1196,6 +1207,11 @@ static void prepare_force(sph_ctx* c) {
 int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out, int32_t* n_nbr_force_out,
               sph_stats* st) {
   API_BEGIN(ctx)
+  if (c->has_active) {
+    const void* outs[4] = {a_out, dudt_out, vsig_out, n_nbr_force_out};
+    for (const void* o : outs)
+      SPH_REQUIRE(!o || is_device_ptr(o), SPH_E_ARG, "with an active mask the outputs must be device arrays");
+  }
   SPH_REQUIRE(c->state >= 2, SPH_E_STATE, "sph_force before sph_density");
   SPH_REQUIRE(a_out && dudt_out, SPH_E_ARG, "required pointer is NULL");
   const int64_t no = c->n_own;
@@ -1213,6 +1229,7 @@ int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out, int3
   fo.nnbr = dev_out(c, n_nbr_force_out, no, B_OUT3, maps);
   fo.perm = Bget<uint32_t>(c, B_PERM);
   fo.n_own = no;
+  fo.tgt = Bget<uint8_t>(c, B_TGT);
   ctr_reset(c);
   const GroupLists G = group_lists(c);
   CUDA_TRY(cudaEventRecord(c->ev[10], c->stream));
@@ -1348,6 +1365,24 @@ int sph_x_histogram(sph_ctx* ctx, int64_t n, const float* x, double lo, double h
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ active subset -----
+int sph_set_active(sph_ctx* ctx, int64_t n, const uint8_t* active) {
+  API_BEGIN(ctx)
+  if (!active) {
+    c->has_active = false;
+    c->n_active_for = 0;
+    return SPH_OK;
+  }
+  SPH_REQUIRE(n > 0, SPH_E_ARG, "n <= 0");
+  uint8_t* d = B<uint8_t>(c, B_ACTIVE, n);
+  CUDA_TRY(cudaMemcpyAsync(d, active, n, cudaMemcpyDefault, c->stream));
+  sync(c);
+  c->has_active = true;
+  c->n_active_for = n;
+  API_END
+  return SPH_OK;
+}
 
 // ------------------------------------------------------------------ time step ---------
 // SURVEY 8(f) f1 (first part): velocity-Verlet kick / drift and the Eq. 6 time step on the

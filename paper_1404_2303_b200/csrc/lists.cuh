@@ -94,6 +94,7 @@ struct WalkParams {
   const int* nsel_dev;      // if set: the number of groups in sel (device; nsel is a bound)
   int* rg_out;              // if set: groups with a lane left in HS_REGROW are appended here
   int* rg_cnt;              //   (count, atomic; order is scheduling only, results do not depend on it)
+  const uint8_t* tgt;       // cell order: 1 = target (owned and active), 0 = source only
   unsigned long long* raw_out;  // if set: sources streamed through the filters, summed (SPH_F_COUNT_CANDIDATES)
   const float4* xh;         // cell-order positions
   const float* reach;       // per particle: NB h_build; UNION the h used for the reach (0: none)
@@ -511,7 +512,7 @@ __global__ void WALK_BOUNDS k_walk(WalkParams P) {
   float ax = 0.f, ay = 0.f, az = 0.f;      // absolute target position (top-cell range)
   bool tg = false;
   if (lane < grp.z) {
-    tg = P.tsel ? P.tsel[s] == P.tsel_val : P.perm[s] < (uint32_t)P.n_own;
+    tg = P.tsel ? P.tsel[s] == P.tsel_val : P.tgt[s] != 0;
     if (tg) {
       const float4 p = P.xh[s];
       ax = p.x;

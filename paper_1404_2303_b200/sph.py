@@ -72,7 +72,7 @@ EXPORTS = ("sph_config_default", "sph_create", "sph_destroy", "sph_set_allocator
            "sph_status_string", "sph_last_error", "sph_build_cells", "sph_density", "sph_force",
            "sph_kernel_launches", "sph_build_cells_halo", "sph_halo_select", "sph_export_state",
            "sph_import_halo_state", "sph_x_histogram", "sph_guess_h", "sph_comm_unique_id", "sph_comm_init",
-           "sph_halo_counts", "sph_halo_exchange", "sph_allreduce", "sph_kick", "sph_drift", "sph_timestep")
+           "sph_halo_counts", "sph_halo_exchange", "sph_allreduce", "sph_kick", "sph_drift", "sph_timestep", "sph_set_active")
 
 
 def load(path: str | None = None):
@@ -111,6 +111,7 @@ def load(path: str | None = None):
     lib.sph_halo_exchange.argtypes = [P, ctypes.c_int32, P, i64, P, i64, P, i64, P, i64]
     lib.sph_allreduce.argtypes = [P, P, i64, ctypes.c_int32, ctypes.c_int32]
     lib.sph_kick.argtypes = [P, i64, P, P, P, P, ctypes.c_float]
+    lib.sph_set_active.argtypes = [P, i64, P]
     lib.sph_drift.argtypes = [P, i64, P, P, ctypes.c_float]
     lib.sph_timestep.argtypes = [P, i64, P, P, ctypes.c_float, P, P]
     if path == LIB or path is None:
@@ -311,6 +312,18 @@ class Context:
         self._check(self.lib.sph_allreduce(self.h, t.data_ptr() if t.numel() else None, int(t.numel()), dt,
                                            {"sum": 0, "max": 1}[op]))
         return t
+
+    def set_active(self, mask=None):
+        """Targets of the next build / density / force: bool or uint8 array [n] (caller
+        order), None for all (include/sph.h sph_set_active)."""
+        if mask is None:
+            self._check(self.lib.sph_set_active(self.h, 0, None))
+            return
+        import torch
+        m = mask.to(torch.uint8).contiguous() if isinstance(mask, torch.Tensor) else \
+            np.ascontiguousarray(mask, dtype=np.uint8)
+        ptr = m.data_ptr() if isinstance(m, torch.Tensor) else m.ctypes.data
+        self._check(self.lib.sph_set_active(self.h, int(m.shape[0]), ptr))
 
     # -- the step around the hot path (include/sph.h sph_kick / sph_drift / sph_timestep) ----
     def kick(self, v, a, dt, u=None, dudt=None):

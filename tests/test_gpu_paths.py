@@ -188,3 +188,46 @@ def test_cold_margin_below_and_above_the_guess(margin):
     p = workloads.tiny(12, n=6000, clump_frac=0.4, n_dup=2)
     p.h0[:] = 0.0
     _check(p, env={"SPH_COLD_MARGIN": margin}, **BENCH_CFG)
+
+
+def test_active_subset_evaluation():
+    """sph_set_active (the paper's multiple time-stepping: only active
+    particles are computed): after a full evaluation, a warm evaluation with 30 % of the
+    particles active reproduces the full results for the active ones (same positions, so
+    the inactive sources carry the same state) and leaves every inactive output entry
+    untouched; the inactive particles keep their h."""
+    import torch
+
+    import paper_1404_2303_b200 as sph
+    p = workloads.c1()
+    dev = torch.device("cuda:0")
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    x, v, m, u = t(p.x), t(p.v), t(p.m), t(p.u)
+    ctx = sph.Context(sph.default_config(p.box, n_ngb_tol=1e-4, **BENCH_CFG))
+    ctx.build_cells(x)
+    d0 = ctx.density(v, m, u)
+    f0 = ctx.force(v)
+    h0, rho0, a0, du0 = d0.h.clone(), d0.rho.clone(), f0.a.clone(), f0.dudt.clone()
+    rng = np.random.default_rng(3)
+    act = rng.random(p.n) < 0.3
+    ctx.set_active(act)
+    ctx.build_cells(x, h0)
+    sentinel = -7.0
+    od = dict(h=torch.full((p.n,), sentinel, device=dev), rho=torch.full((p.n,), sentinel, device=dev))
+    of = dict(a=torch.full((p.n, 3), sentinel, device=dev), dudt=torch.full((p.n,), sentinel, device=dev))
+    d1 = ctx.density(v, m, u, out=od)
+    f1 = ctx.force(v, out=of)
+    A = torch.from_numpy(act).to(dev)
+    assert torch.all(d1.rho[~A] == sentinel) and torch.all(f1.a[~A] == sentinel)
+    assert torch.allclose(d1.h[A], h0[A], rtol=2e-6)
+    assert torch.allclose(d1.rho[A], rho0[A], rtol=1e-5)
+    scale = float(a0.abs().max())
+    assert float((f1.a[A] - a0[A]).abs().max()) <= 1e-4 * scale
+    assert float((f1.dudt[A] - du0[A]).abs().max()) <= 1e-4 * float(du0.abs().max())
+    assert f1.stats["n_pairs"] < f0.stats["n_pairs"]
+    # host outputs are refused while a mask is set (inactive entries must stay untouched)
+    with pytest.raises(sph.SphError) as e:
+        ctx.density(p.v, p.m, p.u)
+    assert e.value.status == sph.SPH_E_ARG
+    ctx.set_active(None)
+    ctx.close()
