@@ -123,6 +123,7 @@ typedef struct {         /* host struct, filled when non-NULL */
      box filters (after the sorted windows where leaves are presorted) */
   int64_t n_nb_sources;          /* neighbour-list walks since the last build (incl. re-walks) */
   int64_t n_union_sources;       /* interaction-list walks of this call */
+  int32_t cells_reused;          /* 1 if the last build kept the cells (sph_update_cells) */
 } sph_stats;
 
 /* Fill *cfg with the paper's defaults for the given box. */
@@ -247,6 +248,14 @@ int sph_allreduce(sph_ctx* ctx, void* buf, int64_t count, int32_t dtype, int32_t
 /* Histogram of x over [lo, hi) into nbins bins (for count-quantile slab cuts). */
 int sph_x_histogram(sph_ctx* ctx, int64_t n, const float* x, double lo, double hi, int32_t nbins,
                     int64_t* hist_out);
+
+/* Pseudo-Verlet reuse of the cells: new positions x [n][3] and smoothing
+ * lengths h0 [n] (> 0) of the particles of the last sph_build_cells (same n, no halo). When
+ * no particle moved by more than a tenth of the smallest h0 since that build (and no leaf
+ * is presorted), the sort, the hierarchy and the target groups are kept and every node
+ * test is widened by the drift; otherwise this is sph_build_cells(x, h0). Then the
+ * neighbour lists as in sph_build_cells. stats.cells_reused (sph_density) tells which. */
+int sph_update_cells(sph_ctx* ctx, const float* x, const float* h0);
 
 /* ---- active subset (the paper's multiple time-stepping: only active
  * particles are "included in the density and force calculations"). active [n] (caller

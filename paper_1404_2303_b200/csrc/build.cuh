@@ -493,3 +493,32 @@ __global__ void k_group_fixed(int64_t n, int4* __restrict__ groups) {
   const int64_t ng = (n + SPH_GROUP - 1) / SPH_GROUP;
   if (g < ng) groups[g] = make_int4(-1, (int)(g * SPH_GROUP), (int)min((int64_t)SPH_GROUP, n - g * SPH_GROUP), 0);
 }
+
+// Pseudo-Verlet reuse of the cells: the new positions of the same particles
+// in the cell order of the last full build, each kept as ref + its minimum-image
+// displacement (so it stays next to the cell it was sorted into, even across the periodic
+// boundary), h from h_in; the largest displacement component into ctr[C_HMAXBITS].
+__global__ void k_update_pos(const uint32_t* __restrict__ perm, int64_t n, const float* __restrict__ x_in,
+                             const float* __restrict__ h_in, const float4* __restrict__ xref, float Lx, float Ly,
+                             float Lz, float4* __restrict__ xh, unsigned long long* ctr) {
+  unsigned mx = 0u;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t o = perm[s];
+    const float4 r = xref[s];
+    const float L[3] = {Lx, Ly, Lz};
+    const float xn[3] = {x_in[3 * (int64_t)o], x_in[3 * (int64_t)o + 1], x_in[3 * (int64_t)o + 2]};
+    const float rr[3] = {r.x, r.y, r.z};
+    float y[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      float d = xn[k] - rr[k];
+      if (d > 0.5f * L[k]) d -= L[k];
+      if (d < -0.5f * L[k]) d += L[k];
+      y[k] = rr[k] + d;
+      mx = max(mx, __float_as_uint(fabsf(d)));
+    }
+    xh[s] = make_float4(y[0], y[1], y[2], h_in[o]);
+  }
+  mx = __reduce_max_sync(FULL_MASK, mx);
+  if ((threadIdx.x & 31) == 0) atomicMax(&ctr[C_HMAXBITS], (unsigned long long)mx);
+}

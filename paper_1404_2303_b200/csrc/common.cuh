@@ -132,6 +132,8 @@ struct sph_ctx {
   int rg_cur = 0;
   bool has_active = false;   // sph_set_active: a caller-order mask in B_ACTIVE applies to the next build
   int64_t n_active_for = 0;
+  float skin = 0.f;            // drift since the cells were sorted (sph_update_cells)
+  bool cells_reused = false;
   bool rg_valid = false;
   bool cold = false;       // h0 was the occupancy guess (wider list margin, N-only first pass)
 
@@ -186,7 +188,7 @@ enum BufId {
   // 13-direction sorted lists
   B_SORTED,
   // groups and interaction lists
-  B_GROUPS, B_GOFF, B_GLEN, B_LIST, B_NBR2, B_NBCNT, B_NBOFF, B_NBOVF, B_OVFIDX, B_NBENT, B_GKEYS, B_GORDER, B_SHRUNK, B_OVFC, B_OVFCNT, B_HCTR, B_RGL, B_RGCNT, B_TGT, B_ACTIVE, B_TSTEP, B_WALKRAW, B_GFLAG, B_GSEL, B_HRCH,
+  B_GROUPS, B_GOFF, B_GLEN, B_LIST, B_NBR2, B_NBCNT, B_NBOFF, B_NBOVF, B_OVFIDX, B_NBENT, B_GKEYS, B_GORDER, B_SHRUNK, B_OVFC, B_OVFCNT, B_HCTR, B_RGL, B_RGCNT, B_XREF, B_TGT, B_ACTIVE, B_TSTEP, B_WALKRAW, B_GFLAG, B_GSEL, B_HRCH,
   // misc scratch
   B_TMPI0, B_TMPI1, B_TMPL0, B_TMPL1, B_COUNTERS, B_OUT0, B_OUT1, B_OUT2, B_OUT3, B_OUT4, B_OUT5,
   B_COUNT

@@ -302,6 +302,9 @@ static void sort_particles(sph_ctx* c, float h0max, bool have_h) {
   float4* xh = B<float4>(c, B_XH, n);
   LAUNCH(k_pack, grid1d(c, n, 256), 256, 0, perm, n, Bget<float>(c, B_XIN), have_h ? Bget<float>(c, B_HIN) : nullptr,
          xh);
+  // the cell-order positions of this sort: the reference of a later pseudo-Verlet update
+  CUDA_TRY(cudaMemcpyAsync(B<float4>(c, B_XREF, n), xh, n * sizeof(float4), cudaMemcpyDeviceToDevice, c->stream));
+  c->skin = 0.f;
 }
 
 // a4: the hierarchy from the sorted keys. Split rule: count > split_count and (rule on)
@@ -424,7 +427,7 @@ static WalkParams walk_params(sph_ctx* c, const float* reach) {
   P.topmap = Bget<int>(c, B_TOPMAP);
   P.sorted = Bget<SortEntry>(c, B_SORTED);
   float Lmax = (float)std::max(c->cfg.box[0], std::max(c->cfg.box[1], c->cfg.box[2]));
-  P.slack = 4e-7f * Lmax;
+  P.slack = 4e-7f * Lmax + c->skin;   // + the drift since the cells were sorted (sph_update_cells)
   P.ctr = ctr(c);
   return P;
 }
@@ -913,6 +916,7 @@ int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const floa
     if (frac) build_nodes(c, true);     // the paper's split rule needs h
   }
   c->cold = need_guess;
+  c->cells_reused = false;
   // a6 + groups + density lists for h_build = h * margin
   build_sorted(c);
   build_groups(c);
@@ -1162,6 +1166,7 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
     st->ms_kernel_walk_union = c->ms_phase[2];
     st->n_nb_entries = c->nb_entries;
     st->n_walk_launches = c->walk_launches;
+    st->cells_reused = c->cells_reused ? 1 : 0;
     if (c->cfg.flags & SPH_F_COUNT_CANDIDATES) {
       unsigned long long wr[2];
       CUDA_TRY(cudaMemcpy(wr, Bget<unsigned long long>(c, B_WALKRAW), sizeof(wr), cudaMemcpyDeviceToHost));
@@ -1365,6 +1370,69 @@ int sph_x_histogram(sph_ctx* ctx, int64_t n, const float* x, double lo, double h
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ pseudo-Verlet -------
+// sph_update_cells: new positions (and h) of the same particles; when no particle moved by
+// more than a tenth of the smallest h since the last full build, the sort, hierarchy and
+// groups are kept and every node test is widened by that drift; else a full
+// build. Then the neighbour lists and h iteration as in sph_build_cells.
+int sph_update_cells(sph_ctx* ctx, const float* x, const float* h0) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(x && h0, SPH_E_ARG, "x or h0 NULL");
+  const bool can = c->state >= 1 && c->n == c->n_own && c->n_sorted == 0 && c->b[B_XREF].p;
+  if (!can) {
+    c->cells_reused = false;
+    return sph_build_cells_halo(ctx, c->n_own, 0, x, h0);
+  }
+  const int64_t n = c->n;
+  float h0max = 0.f;
+  const bool need_guess = load_inputs(c, x, h0, &h0max);
+  SPH_REQUIRE(!need_guess, SPH_E_ARG, "sph_update_cells needs every h0 > 0");
+  unsigned long long hc[C_NCOUNTERS];
+  ctr_reset(c);
+  LAUNCH(k_hrange, grid1d(c, n, 256), 256, 0, Bget<float>(c, B_HIN), n, ctr(c));
+  ctr_read(c, hc);
+  const float hmin = as_float(hc[C_HMINBITS]);
+  ctr_reset(c);
+  LAUNCH(k_update_pos, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, Bget<float>(c, B_XIN),
+         Bget<float>(c, B_HIN), Bget<float4>(c, B_XREF), (float)c->cfg.box[0], (float)c->cfg.box[1],
+         (float)c->cfg.box[2], Bget<float4>(c, B_XH), ctr(c));
+  ctr_read(c, hc);
+  const float drift = as_float(hc[C_HMAXBITS]);
+  if (!(drift <= 0.1f * hmin)) {
+    c->cells_reused = false;
+    return sph_build_cells_halo(ctx, c->n_own, 0, x, h0);
+  }
+  c->cells_reused = true;
+  c->skin = 1.7320508f * drift * 1.0001f;   // |d| <= sqrt(3) max component
+  c->state = 0;
+  c->force_lists = false;
+  c->pool = 0;
+  c->list_rebuilds = 0;
+  CUDA_TRY(cudaEventRecord(c->ev[0], c->stream));
+  phase_reset(c);
+  CUDA_TRY(cudaMemsetAsync(B<unsigned long long>(c, B_NBENT, 1), 0, sizeof(unsigned long long), c->stream));
+  {
+    float* hb = B<float>(c, B_HB, n);
+    CUDA_TRY(cudaMemsetAsync(B<int64_t>(c, B_NBOFF, n), 0xff, n * sizeof(int64_t), c->stream));
+    CUDA_TRY(cudaMemsetAsync(B<uint8_t>(c, B_SHRUNK, n), 0, n, c->stream));
+    CUDA_TRY(cudaMemsetAsync(B<int64_t>(c, B_OVFC, n), 0, n * sizeof(int64_t), c->stream));
+    c->ovf_used = 0;
+    c->n_ovfidx = 0;
+    LAUNCH(k_make_tgt, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, c->n_own,
+           c->has_active ? Bget<uint8_t>(c, B_ACTIVE) : (const uint8_t*)nullptr, B<uint8_t>(c, B_TGT, n));
+    LAUNCH(k_init_iter, grid1d(c, n, 256), 256, 0, Bget<uint8_t>(c, B_TGT), n, Bget<float4>(c, B_XH),
+           c->cfg.h_margin, h_cap(c), Bget<uint8_t>(c, B_STATE), hb, Bget<float>(c, B_HLO), Bget<float>(c, B_HHI));
+  }
+  hctr_reset(c);
+  CUDA_TRY(cudaMemsetAsync(B<unsigned long long>(c, B_WALKRAW, 2), 0, 2 * sizeof(unsigned long long), c->stream));
+  nb_walk(c, -1);
+  c->state = 1;
+  CUDA_TRY(cudaEventRecord(c->ev[1], c->stream));
+  sync(c);
+  API_END
+  return SPH_OK;
+}
 
 // ------------------------------------------------------------------ active subset -----
 int sph_set_active(sph_ctx* ctx, int64_t n, const uint8_t* active) {

@@ -3,9 +3,11 @@ first part; "integrated using a velocity-Verlet integrator") with th
 time step of Eq. 6 (C_CFL = 1/4 as in P:1353). Every arithmetic step runs in
 libsph (sph_kick, sph_drift, sph_timestep, and the three hot-path calls); this class holds
 the device arrays and the order of the calls. Each step rebuilds the cells from the moved
-positions and warm-starts h from the previous step (the regime SURVEY 8(d) calls warm).
-Not here yet: multiple time-stepping and pseudo-Verlet reuse of the cells
-(P:1281-1289)."""
+positions (or reuses them) and warm-starts h from the previous step (the regime SURVEY
+8(d) calls warm).
+Each step keeps the cells of the last full sort while the particles moved little
+(sph_update_cells, the pseudo-Verlet reuse of P:1281-1289). Not here yet: the multiple
+time-stepping integrator (the library side is sph_set_active)."""
 from __future__ import annotations
 
 from .sph import Context
@@ -23,7 +25,10 @@ class Leapfrog:
         ctx = self.ctx
         v = self.v if v is None else v
         u = self.u if u is None else u
-        ctx.build_cells(self.x, h0)
+        if h0 is None:
+            ctx.build_cells(self.x, None)
+        else:                                 # pseudo-Verlet: the cells are kept while they are valid
+            ctx.update_cells(self.x, h0)
         d = ctx.density(v, self.m, u)
         f = ctx.force(v)
         self.h, self.rho, self.a, self.dudt, self.vsig = d.h, d.rho, f.a, f.dudt, f.vsig

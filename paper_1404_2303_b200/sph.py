@@ -60,7 +60,7 @@ class Stats(ctypes.Structure):
         ("ms_kernel_walk_union", ctypes.c_double), ("n_nb_entries", ctypes.c_int64),
         ("n_walk_launches", ctypes.c_int64), ("n_borderline", ctypes.c_int64),
         ("n_borderline_force", ctypes.c_int64), ("n_coincident", ctypes.c_int64),
-        ("n_nb_sources", ctypes.c_int64), ("n_union_sources", ctypes.c_int64),
+        ("n_nb_sources", ctypes.c_int64), ("n_union_sources", ctypes.c_int64), ("cells_reused", ctypes.c_int32),
     ]
 
     def as_dict(self):
@@ -72,7 +72,7 @@ EXPORTS = ("sph_config_default", "sph_create", "sph_destroy", "sph_set_allocator
            "sph_status_string", "sph_last_error", "sph_build_cells", "sph_density", "sph_force",
            "sph_kernel_launches", "sph_build_cells_halo", "sph_halo_select", "sph_export_state",
            "sph_import_halo_state", "sph_x_histogram", "sph_guess_h", "sph_comm_unique_id", "sph_comm_init",
-           "sph_halo_counts", "sph_halo_exchange", "sph_allreduce", "sph_kick", "sph_drift", "sph_timestep", "sph_set_active")
+           "sph_halo_counts", "sph_halo_exchange", "sph_allreduce", "sph_kick", "sph_drift", "sph_timestep", "sph_set_active", "sph_update_cells")
 
 
 def load(path: str | None = None):
@@ -112,6 +112,7 @@ def load(path: str | None = None):
     lib.sph_allreduce.argtypes = [P, P, i64, ctypes.c_int32, ctypes.c_int32]
     lib.sph_kick.argtypes = [P, i64, P, P, P, P, ctypes.c_float]
     lib.sph_set_active.argtypes = [P, i64, P]
+    lib.sph_update_cells.argtypes = [P, P, P]
     lib.sph_drift.argtypes = [P, i64, P, P, ctypes.c_float]
     lib.sph_timestep.argtypes = [P, i64, P, P, ctypes.c_float, P, P]
     if path == LIB or path is None:
@@ -207,6 +208,11 @@ class Context:
         n = int(x.shape[0])
         self._check(self.lib.sph_build_cells(self.h, n, _ptr(x), _ptr(h0)))
         self.n = n
+
+    def update_cells(self, x, h0):
+        """New positions and h of the same particles; keeps the cells when they moved little
+        (include/sph.h sph_update_cells)."""
+        self._check(self.lib.sph_update_cells(self.h, _ptr(x), _ptr(h0)))
 
     def build_cells_halo(self, x, n_own, h0=None):
         """x holds n_own owned particles followed by halo (source-only) particles."""

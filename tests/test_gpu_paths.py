@@ -231,3 +231,37 @@ def test_active_subset_evaluation():
     assert e.value.status == sph.SPH_E_ARG
     ctx.set_active(None)
     ctx.close()
+
+
+@pytest.mark.parametrize("drift_frac,reused", [(0.05, 1), (0.5, 0)])
+def test_update_cells_pseudo_verlet(drift_frac, reused):
+    """sph_update_cells: after a small drift the cells are kept (node tests
+    widened by the drift) and the results equal a fresh build at the new positions and the
+    oracle's; a large drift falls back to a full build."""
+    import torch
+
+    import paper_1404_2303_b200 as sph
+    p = workloads.tiny(13, n=6000, clump_frac=0.4, n_dup=0)
+    dev = torch.device("cuda:0")
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    ctx = sph.Context(sph.default_config(p.box, n_ngb_tol=1e-4, **BENCH_CFG))
+    ctx.build_cells(t(p.x))
+    h1 = ctx.density(t(p.v), t(p.m), t(p.u)).h.clone()
+    rng = np.random.default_rng(17)
+    step = drift_frac * float(h1.min()) / np.sqrt(3.0)
+    L = np.asarray(p.box, dtype=np.float64)
+    x2 = np.mod(p.x.astype(np.float64) + rng.uniform(-step, step, p.x.shape), L)
+    x2 = np.where(x2 >= L, 0.0, x2).astype(np.float32)
+    q = workloads.generators.Particles(p.name, p.box, x2, p.v, p.m, p.u, p.h0)
+    ctx.update_cells(t(x2), h1)
+    d = ctx.density(t(p.v), t(p.m), t(p.u))
+    f = ctx.force(t(p.v))
+    assert d.stats["cells_reused"] == reused
+    fresh = P.run_gpu(q)
+    assert np.allclose(d.h.cpu().numpy(), fresh["h"], rtol=3e-6)
+    assert np.allclose(d.rho.cpu().numpy(), fresh["rho"], rtol=1e-5)
+    a = f.a.cpu().numpy()
+    assert np.abs(a - fresh["a"]).max() <= 1e-4 * np.abs(fresh["a"]).max()
+    h_or = oracle.solve_h(q.x, q.box)
+    assert np.abs(d.h.cpu().numpy() / h_or - 1).max() <= P.TOL_H
+    ctx.close()
