@@ -273,6 +273,10 @@ int sph_set_active(sph_ctx* ctx, int64_t n, const uint8_t* active);
 /* v[n][3] += a[n][3] dt; u[n] += dudt[n] dt (u and dudt may both be NULL). */
 int sph_kick(sph_ctx* ctx, int64_t n, float* v, float* u, const float* a, const float* dudt, float dt);
 
+/* Individual time steps: v[n][3] += a[n][3] dt[i], u[n] += dudt[n] dt[i] with
+ * dt [n] (device); dt[i] = 0 leaves particle i unchanged. */
+int sph_kick_each(sph_ctx* ctx, int64_t n, float* v, float* u, const float* a, const float* dudt, const float* dt);
+
 /* x[n][3] += v[n][3] dt, wrapped back into [0, L) per axis (requires |v dt| < L). */
 int sph_drift(sph_ctx* ctx, int64_t n, float* x, const float* v, float dt);
 

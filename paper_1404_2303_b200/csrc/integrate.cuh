@@ -17,6 +17,20 @@ __global__ void k_kick(int64_t n, float* __restrict__ v, float* __restrict__ u, 
   }
 }
 
+// kick with a per-particle step (individual time steps): v += a dt_i,
+// u += du/dt dt_i; dt_i = 0 leaves a particle as it is
+__global__ void k_kick_each(int64_t n, float* __restrict__ v, float* __restrict__ u, const float* __restrict__ a,
+                            const float* __restrict__ dudt, const float* __restrict__ dt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float d = dt[i];
+    if (d == 0.f) continue;
+    v[3 * i] = fmaf(a[3 * i], d, v[3 * i]);
+    v[3 * i + 1] = fmaf(a[3 * i + 1], d, v[3 * i + 1]);
+    v[3 * i + 2] = fmaf(a[3 * i + 2], d, v[3 * i + 2]);
+    if (u) u[i] = fmaf(dudt[i], d, u[i]);
+  }
+}
+
 // drift: x += v dt, wrapped back into [0, L) (periodic box); |v dt| < L
 __device__ __forceinline__ float wrap1(float x, float L) {
   if (x >= L) x -= L;

@@ -1467,6 +1467,18 @@ int sph_kick(sph_ctx* ctx, int64_t n, float* v, float* u, const float* a, const 
   return SPH_OK;
 }
 
+int sph_kick_each(sph_ctx* ctx, int64_t n, float* v, float* u, const float* a, const float* dudt, const float* dt) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(n >= 0 && (n == 0 || (v && a && dt)) && (!u || dudt), SPH_E_ARG, "bad argument");
+  SPH_REQUIRE(n == 0 || (is_device_ptr(v) && is_device_ptr(a) && is_device_ptr(dt) &&
+                         (!u || (is_device_ptr(u) && is_device_ptr(dudt)))),
+              SPH_E_ARG, "sph_kick_each: arrays must be device memory");
+  if (n > 0) LAUNCH(k_kick_each, grid1d(c, n, 256), 256, 0, n, v, u, a, dudt, dt);
+  if (c->cfg.flags & SPH_F_SYNC) sync(c);
+  API_END
+  return SPH_OK;
+}
+
 int sph_drift(sph_ctx* ctx, int64_t n, float* x, const float* v, float dt) {
   API_BEGIN(ctx)
   SPH_REQUIRE(n >= 0 && (n == 0 || (x && v)), SPH_E_ARG, "bad argument");

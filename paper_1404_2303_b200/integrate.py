@@ -58,3 +58,88 @@ class Leapfrog:
     def energy(self) -> float:
         m, v, u = self.m.double(), self.v.double(), self.u.double()
         return float((0.5 * m * (v * v).sum(1) + m * u).sum())
+
+
+class MultiStep:
+    """Individual power-of-two time steps (as in Gadget-2): particle i moves
+    with a step 2^k dt_min <= its Eq. 6 step, kick-drift-kick per particle; at each
+    synchronisation point only the particles whose step ends there are the targets of the
+    density and force loops (sph_set_active), the others stay sources with their last state.
+    The loops see every particle's v and u predicted to the current time. No time-step
+    limiter (neighbours' steps may differ by more than 2x): meant for mild flows."""
+
+    def __init__(self, ctx: Context, x, v, m, u, dt_max: float, n_bins: int = 6, c_cfl: float = 0.25):
+        import torch
+        self.ctx, self.c_cfl, self.n_bins = ctx, c_cfl, n_bins
+        self.dt_min = dt_max / (1 << n_bins)
+        self.x, self.v, self.m, self.u = x.clone(), v.clone(), m.clone(), u.clone()
+        n = x.shape[0]
+        dev = x.device
+        self.h = torch.empty(n, device=dev)
+        self.rho = torch.empty(n, device=dev)
+        self.a = torch.empty(n, 3, device=dev)
+        self.dudt = torch.empty(n, device=dev)
+        self.vsig = torch.empty(n, device=dev)
+        self.ti = 0
+        self.ti_begin = torch.zeros(n, dtype=torch.int64, device=dev)
+        ctx.set_active(None)
+        ctx.build_cells(self.x, None)
+        ctx.density(self.v, self.m, self.u, out=dict(h=self.h, rho=self.rho))
+        ctx.force(self.v, out=dict(a=self.a, dudt=self.dudt, vsig=self.vsig))
+        self.step_ticks = self._ticks(torch.ones(n, dtype=torch.bool, device=dev), 0)
+        self._kick(self.step_ticks.float() * 0.5 * self.dt_min)
+        self.evaluations = n
+
+    def _ticks(self, sel, ti):
+        """Power-of-two step (in dt_min ticks) <= the Eq. 6 step, dividing ti."""
+        import torch
+        _, dt = self.ctx.timestep(self.h, self.vsig, self.c_cfl, per_particle=True)
+        k = torch.floor(torch.log2(torch.clamp(dt / self.dt_min, min=1.0))).clamp(max=self.n_bins).long()
+        s = torch.pow(2, k)
+        while True:                             # a new step has to start on its own grid
+            bad = (ti % s) != 0
+            if not bool(bad.any()):
+                break
+            s = torch.where(bad, s // 2, s)
+        return torch.where(sel, s, getattr(self, "step_ticks", s))
+
+    def _kick(self, dt):
+        self.ctx.kick_each(self.v, self.a, dt.float().contiguous(), self.u, self.dudt)
+
+    def step(self) -> float:
+        import torch
+        ctx = self.ctx
+        end = self.ti_begin + self.step_ticks
+        ti_end = int(end.min())
+        dt = (ti_end - self.ti) * self.dt_min
+        ctx.drift(self.x, self.v, dt)
+        active = end == ti_end
+        # v and u predicted to ti_end: v holds the mid-step value of each particle's step
+        pred = ((ti_end - (self.ti_begin + self.step_ticks // 2)).float() * self.dt_min).contiguous()
+        vp, up = self.v.clone(), self.u.clone()
+        ctx.kick_each(vp, self.a, pred, up, self.dudt)
+        ctx.set_active(active)
+        ctx.update_cells(self.x, self.h)
+        ctx.density(vp, self.m, up, out=dict(h=self.h, rho=self.rho))
+        ctx.force(vp, out=dict(a=self.a, dudt=self.dudt, vsig=self.vsig))
+        self.evaluations += int(active.sum())
+        zero = torch.zeros_like(self.h)
+        self._kick(torch.where(active, self.step_ticks.float() * 0.5 * self.dt_min, zero))   # close the step
+        self.step_ticks = self._ticks(active, ti_end)
+        self._kick(torch.where(active, self.step_ticks.float() * 0.5 * self.dt_min, zero))   # open the next
+        self.ti_begin = torch.where(active, torch.full_like(self.ti_begin, ti_end), self.ti_begin)
+        self.ti = ti_end
+        return dt
+
+    def time(self) -> float:
+        return self.ti * self.dt_min
+
+    def synced_energy(self) -> float:
+        """Total energy at the current time when every particle starts a step here."""
+        import torch
+        assert bool((self.ti_begin == self.ti).all()), "not a synchronisation point"
+        half = (self.step_ticks.float() * 0.5 * self.dt_min)[:, None]
+        v = self.v.double() - self.a.double() * half.double()
+        u = self.u.double() - self.dudt.double() * half[:, 0].double()
+        m = self.m.double()
+        return float((0.5 * m * (v * v).sum(1) + m * u).sum())
