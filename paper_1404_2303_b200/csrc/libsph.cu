@@ -404,7 +404,6 @@ static int walk_smem() {
   const int bytes = WALK_WARPS * (int)sizeof(WalkSmem);
   if (!attr) {
     CUDA_TRY(cudaFuncSetAttribute(k_walk<MODE_NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    CUDA_TRY(cudaFuncSetAttribute(k_walk<MODE_COUNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     CUDA_TRY(cudaFuncSetAttribute(k_walk<MODE_FILL>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     attr = true;
   }

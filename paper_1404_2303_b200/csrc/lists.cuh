@@ -793,27 +793,10 @@ __global__ void k_set_offsets(int nsel, const int* __restrict__ sel, const int64
   off[sel ? sel[w] : w] = base + scan[w];
 }
 
-// groups holding a particle in state `val` (compaction flags)
-__global__ void k_group_flags(const int4* __restrict__ groups, int ngroups, const uint8_t* __restrict__ state,
-                              uint8_t val, int* __restrict__ flag) {
-  const int lane = threadIdx.x & 31;
-  const int gi = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
-  if (gi >= ngroups) return;
-  const int4 g = groups[gi];
-  const bool r = lane < g.z && state[g.y + lane] == val;
-  const bool any = __any_sync(FULL_MASK, r);
-  if (lane == 0) flag[gi] = any ? 1 : 0;
-}
-
 __global__ void k_compact_idx(const int* __restrict__ flag, const int* __restrict__ scan, int64_t n,
                               int32_t* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     if (flag[i]) out[scan[i]] = (int32_t)i;
-}
-
-__global__ void k_widen_i32(const int* __restrict__ in, int64_t n, int64_t* __restrict__ out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = in[i];
 }
 
 // NB overflow: a particle whose list exceeded K (count known) has its h_build shrunk on the
