@@ -265,3 +265,32 @@ def test_update_cells_pseudo_verlet(drift_frac, reused):
     h_or = oracle.solve_h(q.x, q.box)
     assert np.abs(d.h.cpu().numpy() / h_or - 1).max() <= P.TOL_H
     ctx.close()
+
+
+def test_active_subset_edge_cases():
+    """No active particle: nothing evaluated, every output untouched; a mask of the wrong
+    length is refused (SPH_E_ARG); clearing the mask restores the full evaluation bit for bit."""
+    import torch
+
+    import paper_1404_2303_b200 as sph
+    p = workloads.c1()
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    ctx = sph.Context(sph.default_config(p.box, **BENCH_CFG))
+    ctx.build_cells(t(p.x))
+    d = ctx.density(t(p.v), t(p.m), t(p.u))
+    h = d.h.clone()
+    ctx.set_active(np.zeros(p.n, bool))
+    ctx.build_cells(t(p.x), h)
+    od = dict(h=torch.full((p.n,), -1.0, device="cuda"), rho=torch.full((p.n,), -1.0, device="cuda"))
+    of = dict(a=torch.full((p.n, 3), -1.0, device="cuda"), dudt=torch.full((p.n,), -1.0, device="cuda"))
+    d2 = ctx.density(t(p.v), t(p.m), t(p.u), out=od)
+    f2 = ctx.force(t(p.v), out=of)
+    assert bool((d2.rho == -1).all()) and bool((f2.a == -1).all()) and f2.stats["n_pairs"] == 0
+    ctx.set_active(np.ones(p.n - 1, bool))
+    with pytest.raises(sph.SphError) as e:
+        ctx.build_cells(t(p.x), h)
+    assert e.value.status == sph.SPH_E_ARG
+    ctx.set_active(None)
+    ctx.build_cells(t(p.x))
+    assert torch.equal(ctx.density(t(p.v), t(p.m), t(p.u)).h, d.h)
+    ctx.close()
