@@ -277,6 +277,11 @@ int sph_kick(sph_ctx* ctx, int64_t n, float* v, float* u, const float* a, const 
  * dt [n] (device); dt[i] = 0 leaves particle i unchanged. */
 int sph_kick_each(sph_ctx* ctx, int64_t n, float* v, float* u, const float* a, const float* dudt, const float* dt);
 
+/* Time-step limiter support: after sph_force, for every target i of that call and every j
+ * with r_ij < max(h_i, h_j), out[j] = min(out[j], val[i]). val, out [n] caller order,
+ * device, positive values (out is read and updated). Deterministic (min). */
+int sph_neighbour_min(sph_ctx* ctx, const float* val, float* out);
+
 /* x[n][3] += v[n][3] dt, wrapped back into [0, L) per axis (requires |v dt| < L). */
 int sph_drift(sph_ctx* ctx, int64_t n, float* x, const float* v, float dt);
 

@@ -736,3 +736,70 @@ __global__ void k_make_tgt(const uint32_t* __restrict__ perm, int64_t n, int64_t
     tgt[s] = (o < n_own && (!active || active[o])) ? 1 : 0;
   }
 }
+
+// Neighbour minimum for the time-step limiter (individual time steps): for
+// every target i of the last force loop and every j in its interaction list with
+// r_ij < max(h_i, h_j) (the force pairs): out[j] = min(out[j], val[i]) in the
+// caller's order (positive floats as bits: atomicMin is order-independent, so the result is
+// deterministic). Warp per group, lane = target; sources staged 32 at a time.
+__global__ void __launch_bounds__(256) k_scatter_min(GroupLists G, const float4* __restrict__ fx,
+                                                     const uint32_t* __restrict__ perm,
+                                                     const uint8_t* __restrict__ tgt, const float* __restrict__ val,
+                                                     float3 Lbox, unsigned* __restrict__ out_bits) {
+  __shared__ float4 sa[8][32];
+  __shared__ unsigned so[8][32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int gid = blockIdx.x * 8 + wib;
+  if (gid >= G.ngroups) return;
+  const int4 grp = G.groups[gid];
+  const int s = grp.y + lane;
+  const bool act = lane < grp.z && tgt[s];
+  if (!__any_sync(FULL_MASK, act)) return;
+  const float L[3] = {Lbox.x, Lbox.y, Lbox.z};
+  const float4 o4 = fx[grp.y];
+  const float3 o = make_float3(o4.x, o4.y, o4.z);
+  const float3 oL = make_float3(o4.x - L[0], o4.y - L[1], o4.z - L[2]);
+  float xi = 0.f, yi = 0.f, zi = 0.f, hi2 = -1.f;
+  unsigned vi = 0x7f800000u;
+  if (act) {
+    const float4 p = fx[s];
+    xi = p.x - o.x;
+    yi = p.y - o.y;
+    zi = p.z - o.z;
+    const float hi = 1.0f / p.w;
+    hi2 = hi * hi;
+    vi = __float_as_uint(val[perm[s]]);
+  }
+  const int64_t off = G.off[gid];
+  const int len = G.len[gid];
+  for (int b0 = 0; b0 < len; b0 += 32) {
+    const int e = b0 + lane;
+    float4 a = make_float4(1e30f, 1e30f, 1e30f, 0.f);
+    unsigned oj = 0xffffffffu;
+    if (e < len) {
+      const uint32_t ent = G.list[off + e];
+      const uint32_t j = ent & SPH_IDX_MASK;
+      const float4 p = fx[j];
+      const float3 r = rel_pos(p, ent >> SPH_IDX_BITS, o, oL, L);
+      a = make_float4(r.x, r.y, r.z, p.w);
+      oj = perm[j];
+    }
+    sa[wib][lane] = a;
+    so[wib][lane] = oj;
+    __syncwarp();
+    // per source (lane = source): the smallest value of the targets that reach it
+    unsigned best = 0x7f800000u;
+    const float4 q = sa[wib][lane];
+    for (int t = 0; t < 32; ++t) {
+      const float tx = __shfl_sync(FULL_MASK, xi, t), ty = __shfl_sync(FULL_MASK, yi, t);
+      const float tz = __shfl_sync(FULL_MASK, zi, t), th2 = __shfl_sync(FULL_MASK, hi2, t);
+      const unsigned tv = __shfl_sync(FULL_MASK, vi, t);
+      const float dx = tx - q.x, dy = ty - q.y, dz = tz - q.z;
+      const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+      if (th2 >= 0.f && (r2 < th2 || r2 * (q.w * q.w) < 1.0f)) best = min(best, tv);
+    }
+    const unsigned ob = so[wib][lane];
+    if (ob != 0xffffffffu && best != 0x7f800000u) atomicMin(&out_bits[ob], best);
+    __syncwarp();
+  }
+}

@@ -1433,6 +1433,20 @@ int sph_update_cells(sph_ctx* ctx, const float* x, const float* h0) {
   return SPH_OK;
 }
 
+// ------------------------------------------------------------------ time-step limiter --
+int sph_neighbour_min(sph_ctx* ctx, const float* val, float* out) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(c->state >= 3, SPH_E_STATE, "sph_neighbour_min before sph_force");
+  SPH_REQUIRE(val && out && is_device_ptr(val) && is_device_ptr(out), SPH_E_ARG,
+              "sph_neighbour_min: val and out must be device arrays");
+  const GroupLists G = group_lists(c);
+  LAUNCH(k_scatter_min, gridfull(G.ngroups, 8), 256, 0, G, Bget<float4>(c, B_FX), Bget<uint32_t>(c, B_PERM),
+         Bget<uint8_t>(c, B_TGT), val, box3(c), reinterpret_cast<unsigned*>(out));
+  if (c->cfg.flags & SPH_F_SYNC) sync(c);
+  API_END
+  return SPH_OK;
+}
+
 // ------------------------------------------------------------------ active subset -----
 int sph_set_active(sph_ctx* ctx, int64_t n, const uint8_t* active) {
   API_BEGIN(ctx)

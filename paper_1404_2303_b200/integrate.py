@@ -65,12 +65,14 @@ class MultiStep:
     with a step 2^k dt_min <= its Eq. 6 step, kick-drift-kick per particle; at each
     synchronisation point only the particles whose step ends there are the targets of the
     density and force loops (sph_set_active), the others stay sources with their last state.
-    The loops see every particle's v and u predicted to the current time. No time-step
-    limiter (neighbours' steps may differ by more than 2x): meant for mild flows."""
+    The loops see every particle's v and u predicted to the current time. Limiter (Saitoh &
+    Makino style): a step grows at most 2x at a time, and a particle whose step exceeds 4x a
+    force neighbour's new step is woken (sph_neighbour_min), its step ending early."""
 
-    def __init__(self, ctx: Context, x, v, m, u, dt_max: float, n_bins: int = 6, c_cfl: float = 0.25):
+    def __init__(self, ctx: Context, x, v, m, u, dt_max: float, n_bins: int = 6, c_cfl: float = 0.25,
+                 limiter: bool = True):
         import torch
-        self.ctx, self.c_cfl, self.n_bins = ctx, c_cfl, n_bins
+        self.ctx, self.c_cfl, self.n_bins, self.limiter = ctx, c_cfl, n_bins, limiter
         self.dt_min = dt_max / (1 << n_bins)
         self.x, self.v, self.m, self.u = x.clone(), v.clone(), m.clone(), u.clone()
         n = x.shape[0]
@@ -125,7 +127,24 @@ class MultiStep:
         self.evaluations += int(active.sum())
         zero = torch.zeros_like(self.h)
         self._kick(torch.where(active, self.step_ticks.float() * 0.5 * self.dt_min, zero))   # close the step
+        old_ticks = self.step_ticks
         self.step_ticks = self._ticks(active, ti_end)
+        if self.limiter:
+            # a step grows at most 2x at a time ...
+            self.step_ticks = torch.where(active, torch.minimum(self.step_ticks, 2 * old_ticks), self.step_ticks)
+            # ... and no particle keeps a step above 4x a force neighbour's new one: such a
+            # particle is woken, its current step ending at the next point of the shorter
+            # grid (its opening half kick corrected to the shortened step)
+            lim = torch.full_like(self.h, float("inf"))
+            ctx.neighbour_min(torch.where(active, self.step_ticks.float(), torch.full_like(self.h, float("inf"))), lim)
+            wake = (~active) & (self.step_ticks.float() > 4 * lim)
+            if bool(wake.any()):
+                s2 = torch.pow(2, torch.floor(torch.log2(torch.clamp(4 * lim, min=1.0))).long())
+                new_end = (ti_end // s2 + 1) * s2
+                new_len = torch.where(wake, new_end - self.ti_begin, self.step_ticks)
+                corr = torch.where(wake, (new_len - self.step_ticks).float() * 0.5 * self.dt_min, zero)
+                self._kick(corr)
+                self.step_ticks = new_len
         self._kick(torch.where(active, self.step_ticks.float() * 0.5 * self.dt_min, zero))   # open the next
         self.ti_begin = torch.where(active, torch.full_like(self.ti_begin, ti_end), self.ti_begin)
         self.ti = ti_end

@@ -72,7 +72,7 @@ EXPORTS = ("sph_config_default", "sph_create", "sph_destroy", "sph_set_allocator
            "sph_status_string", "sph_last_error", "sph_build_cells", "sph_density", "sph_force",
            "sph_kernel_launches", "sph_build_cells_halo", "sph_halo_select", "sph_export_state",
            "sph_import_halo_state", "sph_x_histogram", "sph_guess_h", "sph_comm_unique_id", "sph_comm_init",
-           "sph_halo_counts", "sph_halo_exchange", "sph_allreduce", "sph_kick", "sph_drift", "sph_timestep", "sph_set_active", "sph_update_cells", "sph_kick_each")
+           "sph_halo_counts", "sph_halo_exchange", "sph_allreduce", "sph_kick", "sph_drift", "sph_timestep", "sph_set_active", "sph_update_cells", "sph_kick_each", "sph_neighbour_min")
 
 
 def load(path: str | None = None):
@@ -114,6 +114,7 @@ def load(path: str | None = None):
     lib.sph_set_active.argtypes = [P, i64, P]
     lib.sph_update_cells.argtypes = [P, P, P]
     lib.sph_kick_each.argtypes = [P, i64, P, P, P, P, P]
+    lib.sph_neighbour_min.argtypes = [P, P, P]
     lib.sph_drift.argtypes = [P, i64, P, P, ctypes.c_float]
     lib.sph_timestep.argtypes = [P, i64, P, P, ctypes.c_float, P, P]
     if path == LIB or path is None:
@@ -339,6 +340,12 @@ class Context:
     def kick_each(self, v, a, dt, u=None, dudt=None):
         """Per-particle kick: dt is a device float32 array [n] (0 = unchanged)."""
         self._check(self.lib.sph_kick_each(self.h, int(v.shape[0]), _ptr(v), _ptr(u), _ptr(a), _ptr(dudt), _ptr(dt)))
+
+    def neighbour_min(self, val, out):
+        """out[j] = min(out[j], val[i]) over the last force call's targets i and their force
+        neighbours j (device float32 arrays, caller order)."""
+        self._check(self.lib.sph_neighbour_min(self.h, _ptr(val), _ptr(out)))
+        return out
 
     def drift(self, x, v, dt):
         self._check(self.lib.sph_drift(self.h, int(x.shape[0]), _ptr(x), _ptr(v), float(dt)))
