@@ -9,8 +9,12 @@
 #pragma once
 #include "common.cuh"
 
+#ifndef RS_THREADS
 #define RS_THREADS 256
+#endif
+#ifndef RS_ITEMS
 #define RS_ITEMS 16
+#endif
 #define RS_TILE (RS_THREADS * RS_ITEMS)
 #define RS_WARPS (RS_THREADS / 32)
 #define RS_FLAG_INC 0x80000000u
