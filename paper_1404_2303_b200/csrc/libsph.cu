@@ -446,9 +446,11 @@ static const int* group_order(sph_ctx* c, const float* reach) {
   return (const int*)va;
 }
 
-// NB walk over all groups: per target (the owned particles if tsel_val < 0, else those in
-// state tsel_val) the squared distances r^2 < h_build^2 (lists.cuh, MODE_NB). Overflows are
-// marked on the device (k_mark_overflow) and counted in B_OVFCNT; no host round trip.
+// NB walk: per target (the owned, active particles if tsel_val < 0, else those in state
+// tsel_val, over only the groups the last solve listed) the squared distances
+// r^2 < h_build^2 (lists.cuh, MODE_NB), with the h iteration fused into the walk's epilogue
+// and the re-walks of its particles in the same warp; overflows and leftovers are counted
+// on the device (B_HCTR), read once per host round.
 static float solve_margin(sph_ctx* c) { return std::max(c->cfg.h_margin, c->regrow_margin); }
 
 static void nb_walk(sph_ctx* c, int tsel_val, int64_t n_regrow = 0) {

@@ -798,36 +798,6 @@ __global__ void k_compact_idx(const int* __restrict__ flag, const int* __restric
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     if (flag[i]) out[scan[i]] = (int32_t)i;
 }
-
-// NB overflow: a particle whose list exceeded K (count known) has its h_build shrunk on the
-// first overflow (k_hsolve re-walks it with a reach holding ~K/2 sources: no second walk of
-// the large region); a particle that overflows again gets an exactly sized list in the
-// overflow pool (state HS_OVF marks it for the second, contiguous-layout walk). The bit
-// `shrunk` remembers the first overflow.
-#define NB_POOL_MAX (1 << 24)   // longer lists are never recorded: h_build shrinks
-__global__ void k_mark_overflow(const int4* __restrict__ groups, int ngroups, const uint8_t* __restrict__ tsel,
-                                int tsel_val, const uint32_t* __restrict__ perm, int64_t n_own,
-                                const int* __restrict__ cnt, int K, uint8_t* __restrict__ state,
-                                int64_t* __restrict__ ovf_cnt, int64_t* __restrict__ ovf_off,
-                                uint8_t* __restrict__ shrunk, unsigned long long* __restrict__ novf) {
-  const int lane = threadIdx.x & 31;
-  const int gi = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
-  if (gi >= ngroups) return;
-  const int4 g = groups[gi];
-  if (lane >= g.z) return;
-  const int s = g.y + lane;
-  const bool tg = tsel_val >= 0 ? tsel[s] == (uint8_t)tsel_val : perm[s] < (uint32_t)n_own;
-  const bool over = tg && cnt[s] > K;
-  const bool o = over && shrunk[s] && cnt[s] <= NB_POOL_MAX;
-  if (over && !shrunk[s]) shrunk[s] = 1;
-  if (tg) ovf_cnt[s] = o ? cnt[s] : 0;
-  if (o) {
-    state[s] = HS_OVF;
-    atomicAdd(novf, 1ull);
-  } else if (tg) {
-    ovf_off[s] = -1;
-  }
-}
 __global__ void k_ovf_offsets(int64_t n, const int64_t* __restrict__ c, const int64_t* __restrict__ scan,
                               int64_t base, int64_t* __restrict__ off) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x)
