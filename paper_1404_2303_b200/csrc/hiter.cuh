@@ -35,6 +35,16 @@ __device__ __forceinline__ float spline_fp(float q) {
   return q <= 0.5f ? a : b;
 }
 
+// The neighbour lists hold r (NB_STORE_R = 1: the square root is taken once, when the walk
+// records the entry, instead of once per entry in every iteration) or r^2 (NB_STORE_R = 0).
+// Both give the same fp32 r = r^2 * rsqrt(r^2), so the two layouts agree bit for bit.
+#ifndef NB_STORE_R
+#define NB_STORE_R 1
+#endif
+__device__ __forceinline__ float nb_dist_of_r2(float r2) { return r2 * rsqrtf(fmaxf(r2, 1e-37f)); }
+__device__ __forceinline__ float nb_stored(float r2) { return NB_STORE_R ? nb_dist_of_r2(r2) : r2; }
+__device__ __forceinline__ float nb_r(float e) { return NB_STORE_R ? e : nb_dist_of_r2(e); }
+
 // one iteration's sums over a list: S0 = sum f (fp64), S1 = sum q f', S2 = sum q^2 f''.
 // Branch-free so the loads overlap: q is clamped to 1, where f = f' = f'' = 0 exactly.
 #ifndef SPH_HSTEP_ACCEPT
@@ -56,7 +66,7 @@ __device__ __forceinline__ void nsums(const float* r2l, int64_t stride, int e0, 
     for (int k = 0; k < NSUMS_UNROLL; ++k) r2[k] = rp[k * d];
 #pragma unroll
     for (int k = 0; k < NSUMS_UNROLL; ++k) {
-      const float q = fminf(r2[k] * rsqrtf(fmaxf(r2[k], 1e-37f)) * hinv, 1.f);
+      const float q = fminf(nb_r(r2[k]) * hinv, 1.f);
       float f, fp, fpp;
       spline(q, f, fp, fpp);
       S0 += (double)f;
@@ -66,7 +76,7 @@ __device__ __forceinline__ void nsums(const float* r2l, int64_t stride, int e0, 
   }
   for (; e < e1; e += estep, rp += d) {
     const float r2 = *rp;
-    const float q = fminf(r2 * rsqrtf(fmaxf(r2, 1e-37f)) * hinv, 1.f);
+    const float q = fminf(nb_r(r2) * hinv, 1.f);
     float f, fp, fpp;
     spline(q, f, fp, fpp);
     S0 += (double)f;
@@ -85,7 +95,7 @@ __device__ __forceinline__ void nsums_row(const float* r2l, int e1, float hinv, 
     const float r2[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const float q = fminf(r2[k] * rsqrtf(fmaxf(r2[k], 1e-37f)) * hinv, 1.f);
+      const float q = fminf(nb_r(r2[k]) * hinv, 1.f);
       float f, fp, fpp;
       spline(q, f, fp, fpp);
       S0 += (double)f;
@@ -95,7 +105,7 @@ __device__ __forceinline__ void nsums_row(const float* r2l, int e1, float hinv, 
   }
   for (; e < e1; ++e) {
     const float r2 = r2l[e];
-    const float q = fminf(r2 * rsqrtf(fmaxf(r2, 1e-37f)) * hinv, 1.f);
+    const float q = fminf(nb_r(r2) * hinv, 1.f);
     float f, fp, fpp;
     spline(q, f, fp, fpp);
     S0 += (double)f;

@@ -117,7 +117,7 @@ struct WalkParams {
   int ucap;                 // FILL: entries recorded per group (beyond: counted only)
   int check;                // FILL: 1 = second pass into exact space, verify the length
   // NB
-  float* nb_r2;             // [n * K]: particle s's entries at group_first*K + e*group_count + lane
+  float* nb_r2;             // [n * K]: particle s's entries (r, or r^2 if !NB_STORE_R; hiter.cuh), row s (NB_ROWS)
   int* nb_cnt;              // [n] sources with r^2 < h_build^2 (may exceed K: overflow)
   int K;
   unsigned long long* nb_entries;   // NB: running total of recorded entries
@@ -217,7 +217,7 @@ __device__ __forceinline__ void emit_chunk(const WalkParams& P, WalkState& W, Wa
         const float dx = W.xi - q.x, dy = W.yi - q.y, dz = W.zi - q.z;
         const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
         if (r2 < ri2) {
-          if (cur < lim) *wp = r2;
+          if (cur < lim) *wp = nb_stored(r2);
           wp += step;
           ++cur;
         }
