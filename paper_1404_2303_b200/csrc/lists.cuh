@@ -207,7 +207,7 @@ __device__ __forceinline__ void emit_chunk(const WalkParams& P, WalkState& W, Wa
     if (W.ri >= 0.f) {
       const float ri = reach_eff(W.ri, 0.f);
       const float ri2 = ri * ri;
-      // running write pointer: the pool list is contiguous, the slab column strided by gz
+      // the pool list and the slab rows are contiguous, the slab columns (!NB_ROWS) strided by gz
       const int step = (P.ovf || NB_ROWS) ? 1 : W.gz;
       const int lim = P.ovf ? INT_MAX : P.K;
       float* wp = P.ovf ? P.ovf + W.base + W.cur : P.nb_r2 + W.base + (int64_t)W.cur * step;
@@ -216,11 +216,13 @@ __device__ __forceinline__ void emit_chunk(const WalkParams& P, WalkState& W, Wa
         const float4 q = S.s[t];
         const float dx = W.xi - q.x, dy = W.yi - q.y, dz = W.zi - q.z;
         const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-        if (r2 < ri2) {
-          if (cur < lim) *wp = nb_stored(r2);
-          wp += step;
-          ++cur;
-        }
+        // every lane computes the entry, the store and the pointer step are predicated: no
+        // reconvergence block per source (the hits diverge across the warp)
+        const float e = nb_stored(r2);
+        const bool hit = r2 < ri2;
+        if (hit && cur < lim) *wp = e;
+        wp += hit ? step : 0;
+        cur += hit ? 1 : 0;
       }
       W.cur = cur;
     }
