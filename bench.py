@@ -167,6 +167,23 @@ def traffic_from_profiles(kernel: str):
         return None
 
 
+ISSUE_PEAK_GINST = 148 * 4 * 1.965   # warp-instructions per ns: 148 SMs x 4 schedulers x 1/clock
+
+
+def issue_from_profiles(kernel: str, ms: float):
+    """Issue-rate utilisation: the kernel's executed warp instructions (ncu, profiles/issue.json)
+    over its live launch time, against one warp-instruction per scheduler per clock."""
+    try:
+        inst = json.load(open(os.path.join(ROOT, "profiles", "issue.json"))).get(kernel)
+    except (OSError, ValueError):
+        return None
+    if not inst or ms <= 0:
+        return None
+    ach = inst / (ms * 1e6)
+    return {"warp_inst_per_launch": inst, "achieved_ginst_s": ach, "peak_ginst_s": ISSUE_PEAK_GINST,
+            "frac": ach / ISSUE_PEAK_GINST, "source": "profiles/issue.json (ncu executed instructions, v18)"}
+
+
 def run_sph(args, rank, world, local_rank):
     import numpy as np
     import torch
@@ -291,7 +308,7 @@ def run_sph(args, rank, world, local_rank):
         ach = flop / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
         return {"kernel": name, "bound": "alu", "achieved": ach, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": ach / FP32_PEAK_TFLOPS, "traffic": traffic_from_profiles(name),
-                "flop_per_step": flop, "ms_per_step": ms, "work": what,
+                "flop_per_step": flop, "ms_per_step": ms, "work": what, "issue": issue_from_profiles(name, ms),
                 "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (measured FFMA 72.6)"}
 
     # per-phase kernel time, CUDA events on the ctx stream around every launch of the phase
