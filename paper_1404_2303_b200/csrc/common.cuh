@@ -102,7 +102,9 @@ __device__ __forceinline__ float3 dir_unit(int d) { return make_float3(c_dirs[d]
 #define SPH_BAND 1e-6f   // borderline band |r/h - 1| <= 1e-6 (north_star; R5)
 #define SPH_IDX_BITS 27               // list entry = (periodic image code << 27) | source index
 #define SPH_IDX_MASK ((1u << SPH_IDX_BITS) - 1u)
-#define SPH_GROUP 32                  // targets per group (one warp, one lane per target)
+#ifndef SPH_GROUP
+#define SPH_GROUP 32                  // targets per group (one warp, one lane per target; <= 32)
+#endif
 
 // ---------------------------------------------------------------- context ----
 struct DBuf {
