@@ -169,8 +169,11 @@ def density_at(x, v, m, h, box, targets=None, tree=None):
     div = S(mj * np.einsum("ij,ij->i", dv, gradW)) / rho
     cr = np.cross(dv, gradW)
     curl = -np.stack([S(mj * cr[:, k]) for k in range(3)], axis=1) / rho[:, None]
+    # magnitude scale of the div / curl sums (O8, like S_a): (1/rho_i) sum_j m_j |v_j - v_i|
+    # |grad W|, so that |div_i| <= S_dv,i and |curl_i| <= S_dv,i (Cauchy-Schwarz)
+    S_dv = S(mj * np.linalg.norm(dv, axis=1) * np.abs(G) * r) / rho
     return dict(rho=rho, drho_dh=drho_dh, omega=omega, omega_identity=omega_identity,
-                N=N, dN_dh=dN, n_nbr=n_nbr, div=div, curl=curl,
+                N=N, dN_dh=dN, n_nbr=n_nbr, div=div, curl=curl, S_dv=S_dv,
                 n_borderline=n_border, n_coincident=n_coinc)
 
 

@@ -105,6 +105,7 @@ __device__ __forceinline__ float3 dir_unit(int d) { return make_float3(c_dirs[d]
 #ifndef SPH_GROUP
 #define SPH_GROUP 32                  // targets per group (one warp, one lane per target; <= 32)
 #endif
+static_assert(SPH_GROUP >= 1 && SPH_GROUP <= 32, "a target group is one warp: 1 <= SPH_GROUP <= 32");
 
 // ---------------------------------------------------------------- context ----
 struct DBuf {

@@ -7,6 +7,9 @@
 #include <exception>
 #include <cstdlib>
 #include <ctime>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "common.cuh"
 #include "radix_sort.cuh"
@@ -171,8 +174,20 @@ static T scan_excl(sph_ctx* c, const T* in, T* out, int64_t n) {
   return total;
 }
 
+// =========================================================== kernel attributes ==
+// cudaFuncSetAttribute acts on the current device: remember (device, kernel) pairs, so a
+// second context on another GPU of the same process raises the limit there too.
+static std::mutex g_attr_mu;
+static std::set<std::pair<int, const void*>> g_attr_done;
+static void ensure_smem_attr(sph_ctx* c, const void* func, int bytes) {
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  const auto key = std::make_pair(c->device, func);
+  if (g_attr_done.count(key)) return;
+  CUDA_TRY(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  g_attr_done.insert(key);
+}
+
 // =========================================================== radix sort =========
-static bool g_radix_attr = false;
 static void radix_sort(sph_ctx* c, uint64_t*& keys, uint32_t*& vals, uint64_t*& kalt, uint32_t*& valt,
                        int64_t n, int bits) {
   if (n <= 1) return;
@@ -187,10 +202,7 @@ static void radix_sort(sph_ctx* c, uint64_t*& keys, uint32_t*& vals, uint64_t*& 
   int64_t ntiles = (n + RS_TILE - 1) / RS_TILE;
   uint32_t* status = B<uint32_t>(c, B_SORT_STATUS, ntiles * 256);
   uint32_t* tctr = B<uint32_t>(c, B_SORT_CTR, 8);
-  if (!g_radix_attr) {
-    CUDA_TRY(cudaFuncSetAttribute(k_radix_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RadixSmem)));
-    g_radix_attr = true;
-  }
+  ensure_smem_attr(c, (const void*)k_radix_pass, (int)sizeof(RadixSmem));
   CUDA_TRY(cudaMemsetAsync(tctr, 0, 8 * sizeof(uint32_t), c->stream));
   for (int p = 0; p < npass; ++p) {
     CUDA_TRY(cudaMemsetAsync(status, 0, ntiles * 256 * sizeof(uint32_t), c->stream));
@@ -370,12 +382,8 @@ static void build_sorted(sph_ctx* c) {
   const LevelGeom g = level_geom(c);
   const float4* xh = Bget<float4>(c, B_XH);
   LAUNCH(k_sort_leaf_warp, gridfull((int64_t)nn * 32, 256), 256, 0, nn, xh, N, g, sorted);
-  static bool attr = false;
   const int smem = SORT_BLOCK_MAX * (8 + 4);
-  if (!attr) {
-    CUDA_TRY(cudaFuncSetAttribute(k_sort_leaf_block, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
+  ensure_smem_attr(c, (const void*)k_sort_leaf_block, smem);
   LAUNCH(k_sort_leaf_block, nn, 512, smem, nn, xh, N, g, sorted);
 }
 
@@ -399,14 +407,10 @@ static void build_groups(sph_ctx* c) {
 }
 
 // dynamic shared memory of the walk (WALK_WARPS x WalkSmem > the 48 KB static limit)
-static int walk_smem() {
-  static bool attr = false;
+static int walk_smem(sph_ctx* c) {
   const int bytes = WALK_WARPS * (int)sizeof(WalkSmem);
-  if (!attr) {
-    CUDA_TRY(cudaFuncSetAttribute(k_walk<MODE_NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    CUDA_TRY(cudaFuncSetAttribute(k_walk<MODE_FILL>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    attr = true;
-  }
+  ensure_smem_attr(c, (const void*)k_walk<MODE_NB>, bytes);
+  ensure_smem_attr(c, (const void*)k_walk<MODE_FILL>, bytes);
   return bytes;
 }
 
@@ -499,7 +503,7 @@ static void nb_walk(sph_ctx* c, int tsel_val, int64_t n_regrow = 0) {
   P.max_iter = c->cfg.max_h_iter;
   {
     PhaseTimer _p(c, 0);
-    LAUNCH(k_walk<MODE_NB>, gridfull(P.nsel, WALK_WARPS), WALK_WARPS * 32, walk_smem(), P);
+    LAUNCH(k_walk<MODE_NB>, gridfull(P.nsel, WALK_WARPS), WALK_WARPS * 32, walk_smem(c), P);
   }
   c->walk_launches++;
 }
@@ -544,7 +548,7 @@ static void nb_pool(sph_ctx* c) {
   Q.nb_entries = Bget<unsigned long long>(c, B_NBENT);
   {
     PhaseTimer _p(c, 0);
-    LAUNCH(k_walk<MODE_NB>, gridfull(Q.nsel, WALK_WARPS), WALK_WARPS * 32, walk_smem(), Q);
+    LAUNCH(k_walk<MODE_NB>, gridfull(Q.nsel, WALK_WARPS), WALK_WARPS * 32, walk_smem(c), Q);
   }
   c->walk_launches++;
   LAUNCH(k_state_swap, grid1d(c, n, 256), 256, 0, state, n, (uint8_t)HS_OVF, (uint8_t)HS_ACTIVE);
@@ -581,7 +585,7 @@ static void build_union(sph_ctx* c, const float* reach) {
   LAUNCH(k_slab_offsets, gridfull(ng, 256), 256, 0, ng, cap, P.off);
   {
     PhaseTimer _p(c, 2);
-    LAUNCH(k_walk<MODE_FILL>, gridfull(ng, WALK_WARPS), WALK_WARPS * 32, walk_smem(), P);
+    LAUNCH(k_walk<MODE_FILL>, gridfull(ng, WALK_WARPS), WALK_WARPS * 32, walk_smem(c), P);
   }
   int* flag = B<int>(c, B_GFLAG, ng);
   int* scan = B<int>(c, B_TMPI1, ng);
@@ -603,7 +607,7 @@ static void build_union(sph_ctx* c, const float* reach) {
     P.ucap = INT32_MAX;
     P.check = 1;
     PhaseTimer _p(c, 2);
-    LAUNCH(k_walk<MODE_FILL>, gridfull(no, WALK_WARPS), WALK_WARPS * 32, walk_smem(), P);
+    LAUNCH(k_walk<MODE_FILL>, gridfull(no, WALK_WARPS), WALK_WARPS * 32, walk_smem(c), P);
   }
   c->pool = total;
   if (dbg_on()) {
@@ -782,7 +786,9 @@ int sph_create(const sph_config* cfg, int dev, void* stream, sph_ctx** out) {
     if (stream) {
       c->stream = (cudaStream_t)stream;
     } else {
-      CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      // a blocking stream: ordered after work on the legacy default stream (e.g. torch's
+      // tensors produced there), so a caller that passes no stream gets no race
+      CUDA_TRY(cudaStreamCreate(&c->stream));
       c->own_stream = true;
     }
     for (int i = 0; i < 12; ++i) CUDA_TRY(cudaEventCreate(&c->ev[i]));
@@ -1380,6 +1386,8 @@ int sph_x_histogram(sph_ctx* ctx, int64_t n, const float* x, double lo, double h
 int sph_update_cells(sph_ctx* ctx, const float* x, const float* h0) {
   API_BEGIN(ctx)
   SPH_REQUIRE(x && h0, SPH_E_ARG, "x or h0 NULL");
+  SPH_REQUIRE(!c->has_active || c->n_active_for == c->n_own, SPH_E_ARG,
+              "an active mask (sph_set_active) must cover the n_own particles of the last build");
   const bool can = c->state >= 1 && c->n == c->n_own && c->n_sorted == 0 && c->b[B_XREF].p;
   if (!can) {
     c->cells_reused = false;

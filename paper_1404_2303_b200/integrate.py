@@ -139,8 +139,13 @@ class MultiStep:
             ctx.neighbour_min(torch.where(active, self.step_ticks.float(), torch.full_like(self.h, float("inf"))), lim)
             wake = (~active) & (self.step_ticks.float() > 4 * lim)
             if bool(wake.any()):
-                s2 = torch.pow(2, torch.floor(torch.log2(torch.clamp(4 * lim, min=1.0))).long())
-                new_end = (ti_end // s2 + 1) * s2
+                # the shorter grid's step, only where woken (lim is finite there)
+                lim4 = torch.where(wake, 4 * lim, torch.ones_like(lim))
+                s2 = torch.pow(2, torch.floor(torch.log2(torch.clamp(lim4, min=1.0))).long())
+                old_end = self.ti_begin + self.step_ticks
+                # the next point of that grid, never later than the current end of the step
+                new_end = torch.minimum((ti_end // s2 + 1) * s2, old_end)
+                wake = wake & (new_end < old_end)
                 new_len = torch.where(wake, new_end - self.ti_begin, self.step_ticks)
                 corr = torch.where(wake, (new_len - self.step_ticks).float() * 0.5 * self.dt_min, zero)
                 self._kick(corr)

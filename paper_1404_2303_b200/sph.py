@@ -177,6 +177,13 @@ class Context:
     def __init__(self, config: Config | None = None, device: int = 0, stream: int | None = None, **kw):
         self.lib = load()
         self.cfg = config if config is not None else default_config(**kw)
+        if stream is None:
+            # order the context after torch's work: its current stream on that device (a
+            # legacy default stream has handle 0, and libsph then creates a blocking stream,
+            # which is ordered after the legacy stream too)
+            import torch
+            if torch.cuda.is_available():
+                stream = torch.cuda.current_stream(torch.device("cuda", int(device))).cuda_stream or None
         h = ctypes.c_void_p()
         st = self.lib.sph_create(ctypes.byref(self.cfg), int(device), stream, ctypes.byref(h))
         if st != SPH_OK:

@@ -155,3 +155,25 @@ def test_errors():
         ctx.force(v)
     assert e.value.status == sph.SPH_E_STATE
     ctx.close()
+
+
+def test_paper_mode_membership():
+    """n_ngb_tol = 1 (the paper's "e.g. +-1"): several h are correct, so h parity is
+    replaced by membership (SURVEY 8(c) "paper" mode): for every particle the oracle's
+    N(h_gpu) lies in [47, 49]; then mode B at the GPU's h."""
+    p = workloads.tiny(3, n=4000, clump_frac=0.3, n_dup=0)
+    p.h0[:] = 0.0
+    g = P.run_gpu(p, n_ngb_tol=1.0)
+    assert g["stats_density"]["n_unconverged"] == 0
+    d = oracle.density_at(p.x, p.v, p.m, g["h"].astype(np.float64), p.box)
+    assert np.all(np.abs(d["N"] - 48.0) <= 1.0 + 1e-4), float(np.abs(d["N"] - 48.0).max())
+    orc = P.oracle_given_h(p, g["h"])
+    P.compare(g, orc, np.arange(p.n))
+
+
+@pytest.mark.parametrize("t", [0, 1])
+def test_unquantised_positions_at_the_faces(t):
+    """arbitrary fp32 positions (off the 2^-24 grid) crowded against every periodic face,
+    including 0 and the largest fp32 below L; all particles compared, modes A and B."""
+    p = workloads.edges_unquantised(t, n=4000)
+    _modes(p)

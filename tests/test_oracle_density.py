@@ -223,3 +223,16 @@ def test_galilean_invariance_of_div_curl():
     d1 = oracle.density_at(x, p.v.astype(np.float64) + np.array([3.0, -2.0, 1.0]), p.m, h, p.box)
     assert np.allclose(d0["div"], d1["div"], rtol=1e-9, atol=1e-9)
     assert np.allclose(d0["curl"], d1["curl"], rtol=1e-9, atol=1e-9)
+
+
+@pytest.mark.parametrize("t", [0, 1])
+def test_div_curl_bounded_by_their_scale(t):
+    """|div_i| <= S_dv,i and |curl_i| <= S_dv,i (Cauchy-Schwarz on each term), with equality
+    impossible to exceed by more than rounding; S_dv = 0 only without a neighbour at r > 0."""
+    p = workloads.tiny(t, n=500)
+    h = p.h0.astype(np.float64) * 1.5
+    d = oracle.density_at(p.x, p.v, p.m, h, p.box)
+    assert np.all(np.abs(d["div"]) <= d["S_dv"] * (1 + 1e-12))
+    assert np.all(np.linalg.norm(d["curl"], axis=1) <= d["S_dv"] * (1 + 1e-12))
+    # S_dv = 0 only where particle i has no neighbour at r > 0 inside h_i
+    assert np.all((d["S_dv"] > 0) | (d["n_nbr"] - d["n_coincident"] == 0))

@@ -156,6 +156,46 @@ def test_two_particles_by_hand():
     assert fo["dudt"][0] == pytest.approx(du_i, rel=1e-12)
     assert fo["dudt"][1] == pytest.approx(du_j, rel=1e-12)
     assert fo["vsig"][0] == pytest.approx(c_i + c_j - 3 * w, rel=1e-14)
+    # magnitude scales (O8), written out: the one pair's |T| r and |v_ij.dx| terms
+    # (they set the force tolerance band, so they are pinned from above too)
+    T = A_i * G_i + 0.25 * Pi * (f_i + f_j) * G_i
+    assert fo["S_a"][0] == pytest.approx(mj * abs(T) * r, rel=1e-12)
+    assert fo["S_a"][1] == pytest.approx(mi * abs(T) * r, rel=1e-12)
+    assert fo["S_a"][0] == pytest.approx(np.linalg.norm(fo["a"][0]), rel=1e-12)   # one term: |a| = S_a
+    vdx = np.dot(vij, dx)
+    assert fo["S_u"][0] == pytest.approx(mj * abs(vdx) * (abs(A_i * G_i) + 0.125 * abs(Pi) * (f_i + f_j) * abs(G_i)),
+                                         rel=1e-12)
+    assert fo["S_u"][1] == pytest.approx(mi * abs(vdx) * (0.125 * abs(Pi) * (f_i + f_j) * abs(G_i)), rel=1e-12)
+    # div / curl scale of i: (1/rho_i) m_j |v_j - v_i| |grad W|; j has no neighbour (0)
+    assert d["S_dv"][0] == pytest.approx(mj * np.linalg.norm(vj - vi) * abs(_dWdr(r, hi)) / rho_i, rel=1e-12)
+    assert d["S_dv"][1] == 0.0
     assert list(fo["n_nbr_force"]) == [1, 1]
     # pressure pushes i away from j (repulsive): a_i . (x_i - x_j) > 0
     assert np.dot(fo["a"][0], dx) > 0
+
+
+@pytest.mark.parametrize("eps,border", [(5e-7, 1), (-5e-7, 1), (2e-6, 0), (-2e-6, 0)])
+def test_borderline_bands(eps, border):
+    """The borderline band |r/h - 1| <= 1e-6 (north_star, R5) by construction: a pair at
+    r = (1 + eps) h counts as borderline iff |eps| <= 1e-6, for the density band (h_i) and
+    the force band (max(h_i, h_j), here set by the larger h_j). Pins the band from both
+    sides: a band twice as wide, or half as wide, fails one of the cases."""
+    L = 1.0
+    r = 0.0371
+    x = np.array([[0.40, 0.50, 0.50], [0.40 + r, 0.50, 0.50]])
+    v = np.zeros((2, 3))
+    m = np.array([1e-3, 2e-3])
+    u = np.ones(2)
+    h_at = r / (1.0 + eps)                          # r / h - 1 = eps (fp64)
+    h = np.array([h_at, 0.5 * r])
+    assert abs(abs(r / h[0] - 1.0) - abs(eps)) < 1e-15
+    d = oracle.density_at(x, v, m, h, (L, L, L))
+    assert list(d["n_borderline"]) == [border, 0]
+    assert d["n_nbr"][0] == (1 if eps < 0 else 0)   # strict r < h (R5)
+    # force band: max(h_i, h_j) = h_j for particle 0 with a small own h
+    hf = np.array([0.5 * r, h_at])
+    df = oracle.density_at(x, v, m, hf, (L, L, L))
+    st = oracle.particle_state(df["rho"], df["omega"], u, hf, df["div"], df["curl"])
+    fo = oracle.force_at(x, v, m, hf, df["rho"], np.nan_to_num(st["A"], posinf=0.0), st["c"], st["f"], (L, L, L))
+    assert list(fo["n_borderline"]) == [border, border]
+    assert list(fo["n_nbr_force"]) == ([1, 1] if eps < 0 else [0, 0])

@@ -216,6 +216,32 @@ def tiny(t: int, n: int = 600, clump_frac: float = 0.4, n_dup: int = 3,
     return _pack(f"tiny{t}", (1.0, 1.0, 1.0), x, v, m, u, h, seed=140423100 + t)
 
 
+def edges_unquantised(t: int = 0, n: int = 4000) -> Particles:
+    """Arbitrary fp32 positions (NOT snapped to the 2^-24 grid) crowded against the periodic
+    faces: 40% of the particles within 2e-3 of x, y or z = 0 or L, including the exact values
+    0 and the largest fp32 below L, the rest uniform; unequal masses, random v and u. The
+    minimum-image differences across the wrap are then inexact in fp32 (H2): the GPU must
+    still match the fp64 oracle within the tolerances."""
+    rng = np.random.default_rng(140423200 + t)
+    x = rng.random((n, 3))
+    k = int(0.4 * n)
+    idx = rng.choice(n, k, replace=False)
+    ax = rng.integers(0, 3, k)
+    side = rng.integers(0, 2, k)
+    d = rng.random(k) * 2e-3
+    x[idx, ax] = np.where(side == 0, d, 1.0 - d)
+    xf = x.astype(np.float32)
+    top = np.nextafter(np.float32(1.0), np.float32(0.0))
+    xf[idx[:8], ax[:8]] = np.where(side[:8] == 0, np.float32(0.0), top)
+    xf = np.where(xf >= np.float32(1.0), top, xf).astype(np.float32)
+    v = rng.normal(0.0, 0.2, (n, 3))
+    u = np.exp(rng.uniform(math.log(0.5), math.log(2.0), n))
+    m = rng.uniform(0.5, 1.5, n) / n
+    return Particles(f"edges{t}", (1.0, 1.0, 1.0), np.ascontiguousarray(xf),
+                     v.astype(np.float32), m.astype(np.float32), u.astype(np.float32),
+                     np.zeros(n, dtype=np.float32), {"seed": 140423200 + t})
+
+
 CONFIGS = {
     "C1": c1, "C2": c2, "C2-exact": c2_exact, "SC-exact": c2_exact,
     "FCC-exact": fcc_exact, "C3": c3, "C4": c4, "C5": c5,
