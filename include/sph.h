@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 1
+#define SPH_ABI_VERSION 2
 
 typedef struct sph_ctx sph_ctx;
 
@@ -91,6 +91,17 @@ typedef struct {
   double slab_lo, slab_hi; /* owned x-range of this rank (multi-GPU) */
   double halo_width;     /* multi-GPU: width of the halo received at each slab face; an h beyond
                             it cannot be evaluated (SPH_E_NOCONV "halo too narrow"). 0 = none */
+  /* capacities and tuning of the neighbour-finding structures (results do not depend on them) */
+  int32_t row_cap;       /* entries of a particle's neighbour row (the h iteration's distances);
+                            longer rows shrink h_build once, then go to an exactly sized pool.
+                            0 = sized from free device memory (<= 1024) */
+  int32_t list_cap;      /* interaction-list slab entries per target group; longer lists are walked
+                            again into exactly sized space. 0 = 768 */
+  int32_t group_container; /* target groups: chunks of <= 32 consecutive particles of the deepest
+                            cells holding <= group_container particles. 0 = 512; -1 = pack sibling
+                            leaves instead */
+  float cold_margin;     /* h0 == 0 (library guess): rows are recorded for h_build = guess x this.
+                            0 = 1.0 */
 } sph_config;
 
 typedef struct {         /* host struct, filled when non-NULL */
@@ -291,6 +302,30 @@ int sph_drift(sph_ctx* ctx, int64_t n, float* x, const float* v, float dt);
  * (P:1353). */
 int sph_timestep(sph_ctx* ctx, int64_t n, const float* h, const float* vsig, float c_cfl, float* dt_out,
                  float* dt_min_out);
+
+/* ---- structure introspection (tests and tools; not on the hot path). Copies one of the
+ * context's internal arrays to the HOST buffer `out` (room for `cap` elements) and sets
+ * *count to its element count (nothing is copied when cap < count). `what`:
+ *   SPH_X_PERM     uint32 [n]        cell order -> caller index (the sort's permutation)
+ *   SPH_X_GROUPS   int32 [ng][4]     target groups {node, first, count, 0} (cell order)
+ *   SPH_X_LIST_OFF int64 [ng]        interaction-list offset of each group
+ *   SPH_X_LIST_LEN int32 [ng]        interaction-list length of each group
+ *   SPH_X_LIST     uint32 [entries]  interaction-list entries (image code << 27) | source
+ *   SPH_X_NODES    int32 [nodes][4]  {first, count, first child or -1, octant mask | level << 8}
+ *   SPH_X_SORTOFF  int64 [nodes]     offset of a node's 13 presorted lists, -1 if none
+ *   SPH_X_SORTED   {float key, int32 idx} [entries]  presorted lists, 13 per node
+ *   SPH_X_XH       float [n][4]      cell-order positions and current h
+ * Errors: SPH_E_ARG (unknown `what`, count or out NULL), SPH_E_STATE (no build yet). */
+#define SPH_X_PERM 0
+#define SPH_X_GROUPS 1
+#define SPH_X_LIST_OFF 2
+#define SPH_X_LIST_LEN 3
+#define SPH_X_LIST 4
+#define SPH_X_NODES 5
+#define SPH_X_SORTOFF 6
+#define SPH_X_SORTED 7
+#define SPH_X_XH 8
+int sph_debug_export(sph_ctx* ctx, int32_t what, void* out, int64_t cap, int64_t* count);
 
 /* Number of CUDA kernel launches libsph issued on this context since creation
  * (evidence for the bench's gpu_launches). */

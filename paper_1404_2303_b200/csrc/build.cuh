@@ -486,14 +486,6 @@ __global__ void k_group_write(int nnodes, NodeArrays N, int cmax, const int* __r
   }
 }
 
-// alternative grouping (experiments): fixed chunks of SPH_GROUP consecutive particles in
-// cell (Morton) order, regardless of cell boundaries
-__global__ void k_group_fixed(int64_t n, int4* __restrict__ groups) {
-  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t ng = (n + SPH_GROUP - 1) / SPH_GROUP;
-  if (g < ng) groups[g] = make_int4(-1, (int)(g * SPH_GROUP), (int)min((int64_t)SPH_GROUP, n - g * SPH_GROUP), 0);
-}
-
 // Pseudo-Verlet reuse of the cells: the new positions of the same particles
 // in the cell order of the last full build, each kept as ref + its minimum-image
 // displacement (so it stays next to the cell it was sorted into, even across the periodic

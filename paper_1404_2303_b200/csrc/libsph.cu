@@ -389,17 +389,10 @@ static void build_sorted(sph_ctx* c) {
 
 static void build_groups(sph_ctx* c) {
   const int nn = c->n_nodes;
-  if (getenv("SPH_GROUPS_FIXED")) {
-    c->n_groups = (int)((c->n + SPH_GROUP - 1) / SPH_GROUP);
-    int4* groups = B<int4>(c, B_GROUPS, c->n_groups);
-    LAUNCH(k_group_fixed, gridfull(c->n_groups, 256), 256, 0, c->n, groups);
-    return;
-  }
   int* nchunk = B<int>(c, B_TMPI0, nn);
   int* cscan = B<int>(c, B_TMPI1, nn);
   NodeArrays N = nodes(c);
-  const char* ce = getenv("SPH_GROUP_CMAX");
-  const int cmax = ce ? atoi(ce) : c->group_cmax;
+  const int cmax = c->group_cmax;
   LAUNCH(k_group_count, gridfull(nn, 256), 256, 0, nn, N, cmax, nchunk);
   c->n_groups = scan_excl<int>(c, nchunk, cscan, nn);
   int4* groups = B<int4>(c, B_GROUPS, c->n_groups);
@@ -435,21 +428,6 @@ static WalkParams walk_params(sph_ctx* c, const float* reach) {
   return P;
 }
 
-// the groups in longest-first order (estimated walk work, k_group_cost) for a full walk
-static const int* group_order(sph_ctx* c, const float* reach) {
-  if (!getenv("SPH_LPT")) return nullptr;   // off: spatial order keeps tree nodes and particles in cache (ablation: +1.3 ms on C4)
-  const int ng = c->n_groups;
-  uint64_t* k0 = B<uint64_t>(c, B_KEYS1, ng);
-  uint32_t* v0 = B<uint32_t>(c, B_VALS1, ng);
-  uint64_t* k1 = B<uint64_t>(c, B_GKEYS, ng);
-  uint32_t* v1 = B<uint32_t>(c, B_GORDER, ng);
-  LAUNCH(k_group_cost, gridfull(ng, 256), 256, 0, Bget<int4>(c, B_GROUPS), ng, reach, nodes(c), level_geom(c), k0, v0);
-  uint64_t *ka = k0, *kb = k1;
-  uint32_t *va = v0, *vb = v1;
-  radix_sort(c, ka, va, kb, vb, ng, 32);
-  return (const int*)va;
-}
-
 // NB walk: per target (the owned, active particles if tsel_val < 0, else those in state
 // tsel_val, over only the groups the last solve listed) the squared distances
 // r^2 < h_build^2 (lists.cuh, MODE_NB), with the h iteration fused into the walk's epilogue
@@ -462,14 +440,13 @@ static void nb_walk(sph_ctx* c, int tsel_val, int64_t n_regrow = 0) {
   const int64_t n = c->n;
   WalkParams P = walk_params(c, Bget<float>(c, B_HB));
   P.nsel = c->n_groups;
-  P.sel = group_order(c, Bget<float>(c, B_HB));
   const int ng = c->n_groups;
   int* rgl = B<int>(c, B_RGL, 2 * (int64_t)std::max(ng, 1));
   int* rgc = B<int>(c, B_RGCNT, 2);
   if (tsel_val >= 0) {
     P.tsel = Bget<uint8_t>(c, B_STATE);
     P.tsel_val = (uint8_t)tsel_val;
-    if (tsel_val == HS_REGROW && c->rg_valid && !getenv("SPH_REWALK_ALL")) {
+    if (tsel_val == HS_REGROW && c->rg_valid) {
       // only the groups the last solve left with re-walking particles (at most one per particle)
       P.sel = rgl + (int64_t)c->rg_cur * ng;
       P.nsel_dev = rgc + c->rg_cur;
@@ -576,7 +553,6 @@ static void build_union(sph_ctx* c, const float* reach) {
   }
   P.reach_max_bits = ctr(c) + C_HMAXBITS;
   P.nsel = ng;
-  P.sel = group_order(c, reach);
   P.off = B<int64_t>(c, B_GOFF, ng);
   P.len = B<int>(c, B_GLEN, ng);
   P.ucap = cap;
@@ -765,6 +741,10 @@ static bool cfg_ok(const sph_config* f, std::string& why) {
   if (!(f->split_fraction >= 0.f && f->split_fraction < 1.f)) { why = "split_fraction outside [0,1)"; return false; }
   if (f->split_count < 1) { why = "split_count < 1"; return false; }
   if (f->max_h_iter < 1) { why = "max_h_iter < 1"; return false; }
+  if (f->row_cap < 0 || f->list_cap < 0 || f->cold_margin < 0.f || f->group_container < -1) {
+    why = "negative capacity or margin";
+    return false;
+  }
   if (f->nranks < 1 || f->rank < 0 || f->rank >= f->nranks) { why = "bad rank/nranks"; return false; }
   return true;
 }
@@ -806,11 +786,10 @@ int sph_create(const sph_config* cfg, int dev, void* stream, sph_ctx** out) {
     dirs[13][0] = dirs[13][1] = dirs[13][2] = 0.f;
     CUDA_TRY(cudaMemcpyToSymbol(c_dirs, dirs, sizeof(dirs)));
     c->ev_ok = true;
-    // tuning overrides for experiments; defaults otherwise
-    if (const char* e = getenv("SPH_COLD_MARGIN")) c->cold_margin = (float)atof(e);
-    if (const char* e = getenv("SPH_REGROW_MARGIN")) c->regrow_margin = (float)atof(e);
-    if (const char* e = getenv("SPH_NBK")) c->nb_k = std::max(4, atoi(e) & ~3);
-    if (const char* e = getenv("SPH_UCAP")) c->ucap = atoi(e);
+    // capacities and tuning from the config (include/sph.h); defaults otherwise
+    if (cfg->cold_margin > 0.f) c->cold_margin = cfg->cold_margin;
+    if (cfg->list_cap > 0) c->ucap = cfg->list_cap;
+    if (cfg->group_container != 0) c->group_cmax = cfg->group_container < 0 ? 0 : cfg->group_container;
   } catch (const SphError& e) {
     delete c;
     return e.status;
@@ -890,7 +869,9 @@ int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const floa
   c->n_own = n_own;
   c->state = 0;
   c->force_lists = false;
-  if (!getenv("SPH_NBK") && n != c->nb_k_for) {
+  if (c->cfg.row_cap > 0) {
+    c->nb_k = std::max(4, c->cfg.row_cap & ~3);
+  } else if (n != c->nb_k_for) {
     // neighbour-list slab: up to 1024 entries per particle, within 40% of the free device
     // memory (cold-start lists hold ~90 entries; longer ones shrink or go to the pool);
     // sized once per particle count (cudaMemGetInfo stalls the host)
@@ -1439,6 +1420,36 @@ int sph_update_cells(sph_ctx* ctx, const float* x, const float* h0) {
   c->state = 1;
   CUDA_TRY(cudaEventRecord(c->ev[1], c->stream));
   sync(c);
+  API_END
+  return SPH_OK;
+}
+
+// ------------------------------------------------------------------ introspection -----
+int sph_debug_export(sph_ctx* ctx, int32_t what, void* out, int64_t cap, int64_t* count) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(count != nullptr, SPH_E_ARG, "count == NULL");
+  SPH_REQUIRE(c->state >= 1, SPH_E_STATE, "sph_debug_export before sph_build_cells");
+  int id = -1;
+  int64_t cnt = 0;
+  size_t esz = 0;
+  switch (what) {
+    case SPH_X_PERM: id = B_PERM; cnt = c->n; esz = 4; break;
+    case SPH_X_GROUPS: id = B_GROUPS; cnt = c->n_groups; esz = 16; break;
+    case SPH_X_LIST_OFF: id = B_GOFF; cnt = c->state >= 2 ? c->n_groups : 0; esz = 8; break;
+    case SPH_X_LIST_LEN: id = B_GLEN; cnt = c->state >= 2 ? c->n_groups : 0; esz = 4; break;
+    case SPH_X_LIST: id = B_LIST; cnt = c->state >= 2 ? c->pool : 0; esz = 4; break;
+    case SPH_X_NODES: id = B_N_REC; cnt = c->n_nodes; esz = 16; break;
+    case SPH_X_SORTOFF: id = B_N_SORTOFF; cnt = c->n_nodes; esz = 8; break;
+    case SPH_X_SORTED: id = B_SORTED; cnt = c->n_sorted; esz = sizeof(SortEntry); break;
+    case SPH_X_XH: id = B_XH; cnt = c->n; esz = 16; break;
+    default: SPH_REQUIRE(false, SPH_E_ARG, "unknown sph_debug_export item");
+  }
+  *count = cnt;
+  if (cnt > 0 && cap >= cnt) {
+    SPH_REQUIRE(out != nullptr, SPH_E_ARG, "out == NULL");
+    CUDA_TRY(cudaMemcpyAsync(out, c->b[id].p, (size_t)cnt * esz, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+  }
   API_END
   return SPH_OK;
 }

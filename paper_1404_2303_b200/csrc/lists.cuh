@@ -830,24 +830,3 @@ __global__ void k_compact_append(const int* __restrict__ flag, const int* __rest
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     if (flag[i]) out[scan[i]] = (int32_t)i;
 }
-
-// Longest-first order of the groups for a walk: estimated work = particles of the group's
-// cell density inside the reach (R_group / edge)^3 x count; launching the heavy groups first
-// hides their latency behind the light ones. Key = ~float_ord(est) (descending), value = id.
-__global__ void k_group_cost(const int4* __restrict__ groups, int ngroups, const float* __restrict__ reach,
-                             NodeArrays N, LevelGeom g, uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
-  const int gi = blockIdx.x * blockDim.x + threadIdx.x;
-  if (gi >= ngroups) return;
-  const int4 grp = groups[gi];
-  float R = 0.f;
-  for (int k = 0; k < grp.z; ++k) R = fmaxf(R, reach[grp.y + k]);
-  float est = (float)grp.z;
-  if (grp.x >= 0) {
-    const int4 c = N.ijk[grp.x];
-    const float E = fminf(g.E[c.w][0], fminf(g.E[c.w][1], g.E[c.w][2]));
-    const float q = R / E;
-    est = (float)N.count[grp.x] * fmaxf(q * q * q, 1.f);
-  }
-  keys[gi] = (uint64_t)(~float_ord(est));
-  vals[gi] = (uint32_t)gi;
-}

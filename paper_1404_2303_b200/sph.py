@@ -32,7 +32,7 @@ SPH_OK, SPH_E_ARG, SPH_E_DOMAIN, SPH_E_STATE, SPH_E_NOCONV, SPH_E_CUDA, SPH_E_NC
 SPH_F_SYNC = 1
 SPH_F_COUNT_CANDIDATES = 2
 SPH_F_DIAGNOSTICS = 4
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 
 class Config(ctypes.Structure):
@@ -43,7 +43,8 @@ class Config(ctypes.Structure):
         ("split_fraction", ctypes.c_float), ("top_edge_factor", ctypes.c_float),
         ("h_margin", ctypes.c_float), ("sort_min_len", ctypes.c_int32), ("flags", ctypes.c_uint32), ("rank", ctypes.c_int32),
         ("nranks", ctypes.c_int32), ("slab_lo", ctypes.c_double), ("slab_hi", ctypes.c_double),
-        ("halo_width", ctypes.c_double),
+        ("halo_width", ctypes.c_double), ("row_cap", ctypes.c_int32), ("list_cap", ctypes.c_int32),
+        ("group_container", ctypes.c_int32), ("cold_margin", ctypes.c_float),
     ]
 
 
@@ -72,7 +73,8 @@ EXPORTS = ("sph_config_default", "sph_create", "sph_destroy", "sph_set_allocator
            "sph_status_string", "sph_last_error", "sph_build_cells", "sph_density", "sph_force",
            "sph_kernel_launches", "sph_build_cells_halo", "sph_halo_select", "sph_export_state",
            "sph_import_halo_state", "sph_x_histogram", "sph_guess_h", "sph_comm_unique_id", "sph_comm_init",
-           "sph_halo_counts", "sph_halo_exchange", "sph_allreduce", "sph_kick", "sph_drift", "sph_timestep", "sph_set_active", "sph_update_cells", "sph_kick_each", "sph_neighbour_min")
+           "sph_halo_counts", "sph_halo_exchange", "sph_allreduce", "sph_kick", "sph_drift", "sph_timestep", "sph_set_active", "sph_update_cells", "sph_kick_each", "sph_neighbour_min",
+           "sph_debug_export")
 
 
 def load(path: str | None = None):
@@ -115,6 +117,7 @@ def load(path: str | None = None):
     lib.sph_update_cells.argtypes = [P, P, P]
     lib.sph_kick_each.argtypes = [P, i64, P, P, P, P, P]
     lib.sph_neighbour_min.argtypes = [P, P, P]
+    lib.sph_debug_export.argtypes = [P, ctypes.c_int32, P, i64, P]
     lib.sph_drift.argtypes = [P, i64, P, P, ctypes.c_float]
     lib.sph_timestep.argtypes = [P, i64, P, P, ctypes.c_float, P, P]
     if path == LIB or path is None:
@@ -327,6 +330,21 @@ class Context:
         self._check(self.lib.sph_allreduce(self.h, t.data_ptr() if t.numel() else None, int(t.numel()), dt,
                                            {"sum": 0, "max": 1}[op]))
         return t
+
+    _EXPORT = {"perm": (0, np.uint32, 1), "groups": (1, np.int32, 4), "list_off": (2, np.int64, 1),
+               "list_len": (3, np.int32, 1), "list": (4, np.uint32, 1), "nodes": (5, np.int32, 4),
+               "sortoff": (6, np.int64, 1), "sorted": (7, np.dtype([("key", np.float32), ("idx", np.int32)]), 1),
+               "xh": (8, np.float32, 4)}
+
+    def export(self, what: str) -> np.ndarray:
+        """A copy of one of the context's internal arrays (include/sph.h sph_debug_export)."""
+        code, dt, w = self._EXPORT[what]
+        cnt = ctypes.c_int64()
+        self._check(self.lib.sph_debug_export(self.h, code, None, 0, ctypes.byref(cnt)))
+        out = np.zeros((cnt.value, w) if w > 1 else cnt.value, dtype=dt)
+        if cnt.value:
+            self._check(self.lib.sph_debug_export(self.h, code, out.ctypes.data, cnt.value, ctypes.byref(cnt)))
+        return out
 
     def set_active(self, mask=None):
         """Targets of the next build / density / force: bool or uint8 array [n] (caller

@@ -40,7 +40,7 @@ def test_exports_every_declared_symbol(lib):
 
 def test_config_default_matches_paper_constants(lib):
     cfg = sphlib.default_config((2.0, 1.0, 1.0))
-    assert cfg.abi_version == 1 and list(cfg.box) == [2.0, 1.0, 1.0]
+    assert cfg.abi_version == 2 and list(cfg.box) == [2.0, 1.0, 1.0]
     assert cfg.n_ngb == 48.0 and cfg.alpha == pytest.approx(0.8)
     assert cfg.gamma == pytest.approx(5 / 3)
     assert cfg.split_count == 300 and cfg.split_fraction == pytest.approx(0.875)

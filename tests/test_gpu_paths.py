@@ -3,8 +3,6 @@ configuration at C4's full size, the paper-literal presort of every leaf (P:687-
 neighbour-list overflow (shrink on first overflow, exact pool on a repeat), interaction-
 list slab overflow, and repeated calls on one structure. Each case is compared with the
 fp64 oracle (tests/parity.py, north_star tolerances)."""
-import os
-
 import numpy as np
 import pytest
 
@@ -28,19 +26,8 @@ def _cuda():
     build.build()
 
 
-def _check(p, targets=None, env=None, **cfg):
-    old = {}
-    for k, v in (env or {}).items():
-        old[k] = os.environ.get(k)
-        os.environ[k] = str(v)
-    try:
-        g = P.run_gpu(p, **cfg)
-    finally:
-        for k, v in old.items():
-            if v is None:
-                os.environ.pop(k, None)
-            else:
-                os.environ[k] = v
+def _check(p, targets=None, **cfg):
+    g = P.run_gpu(p, **cfg)
     t = np.arange(p.n) if targets is None else targets
     h_or = oracle.solve_h(p.x, p.box, targets=t)
     rel_h = np.abs(g["h"][t] - h_or) / h_or
@@ -83,20 +70,20 @@ def test_neighbour_list_overflow_paths():
     re-walked, and repeat overflows go to the exact pool."""
     p = workloads.tiny(6, n=5000, clump_frac=0.4, n_dup=2)
     p.h0[:] = 0.0
-    g, _ = _check(p, env={"SPH_NBK": 64}, **BENCH_CFG)
+    g, _ = _check(p, row_cap=64, **BENCH_CFG)
     assert g["stats_density"]["n_rebuilds"] > 0
 
 
 def test_interaction_list_slab_overflow():
     """A 64-entry interaction-list slab: every group's list is re-walked into exact space."""
     p = workloads.c1()
-    _check(p, env={"SPH_UCAP": 64}, **BENCH_CFG)
+    _check(p, list_cap=64, **BENCH_CFG)
 
 
 def test_sibling_packing_groups():
     p = workloads.tiny(7, n=4000, clump_frac=0.3, n_dup=2)
     p.h0[:] = 0.0
-    _check(p, env={"SPH_GROUP_CMAX": 0}, **BENCH_CFG)
+    _check(p, group_container=-1, **BENCH_CFG)
 
 
 def test_repeated_calls_on_one_structure():
@@ -180,14 +167,14 @@ def test_torch_caching_allocator_hook():
     assert counts["alloc"] > 10 and counts["free"] == counts["alloc"]
 
 
-@pytest.mark.parametrize("margin", ["0.8", "1.3"])
+@pytest.mark.parametrize("margin", [0.8, 1.3])
 def test_cold_margin_below_and_above_the_guess(margin):
     """Neighbour lists recorded below the initial guess (cold margin < 1: most particles
     re-walk) or well above it: the h iteration never evaluates N(h) beyond a recorded list,
     and every particle converges to the oracle's root."""
     p = workloads.tiny(12, n=6000, clump_frac=0.4, n_dup=2)
     p.h0[:] = 0.0
-    _check(p, env={"SPH_COLD_MARGIN": margin}, **BENCH_CFG)
+    _check(p, cold_margin=margin, **BENCH_CFG)
 
 
 def test_active_subset_evaluation():
