@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-warm", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--cpu-frac", type=float, default=0.02, help="cpu_baseline: fraction of the particles timed as targets")
     ap.add_argument("--transport", default="torch", choices=["torch", "libsph"],
                     help="N > 1 halo exchange: torch.distributed P2P or libsph's NCCL communicator")
     return ap.parse_args()
@@ -123,6 +124,97 @@ def oracle_sample(budget_s: float):
     n = int(8192 * max(1.0, budget_s / max(t_cal, 1e-3)))
     n = int(2 ** math.floor(math.log2(max(8192, min(n, 1 << 20)))))
     return n, one, np
+
+
+# ---- cpu_baseline: the oracle on a seeded 2% subset of the headline input itself ----------
+_G = {}   # inherited by the forked pool workers (x, v, m, box, tree, h and state of all particles)
+
+
+def _w_density(idx):
+    """Pool worker, phase 1: the oracle's own h root (Eq. 3), density (Eq. 2) and particle
+    state for a chunk of targets. Returns (idx, h, rho, A, c, f, seconds)."""
+    import numpy as np
+
+    import oracle
+    import oracle.neighbours as nb
+    nb.WORKERS = 1
+    g = _G
+    t0 = time.perf_counter()
+    hT = oracle.solve_h(g["x"], g["box"], targets=idx, tree=g["tree"])
+    h = g["h"].copy()
+    h[idx] = hT
+    den = oracle.density_at(g["x"], g["v"], g["m"], h, g["box"], targets=idx, tree=g["tree"])
+    st = oracle.particle_state(den["rho"], den["omega"], g["u"][idx], hT, den["div"], den["curl"])
+    return idx, hT, den["rho"], st["A"], st["c"], st["f"], time.perf_counter() - t0
+
+
+def _w_force(idx):
+    """Pool worker, phase 2: the oracle's force (Eq. 4-5 + viscosity) for a chunk of targets.
+    Returns (directed force pairs, seconds)."""
+    import oracle
+    import oracle.neighbours as nb
+    nb.WORKERS = 1
+    g = _G
+    t0 = time.perf_counter()
+    fo = oracle.force_at(g["x"], g["v"], g["m"], g["h"], g["rho"], g["A"], g["c"], g["f"], g["box"], targets=idx,
+                         tree=g["tree"])
+    return int(fo["n_nbr_force"].sum()), time.perf_counter() - t0
+
+
+def oracle_subset_rate(p, gpu, frac=0.02, procs=None, seed=140423098):
+    """Time the fp64 oracle (as it stands, oracle/) on the headline input itself: a seeded
+    `frac` subset of its particles as targets, every particle a source. Per target the oracle
+    does its full work: h root of Eq. 3, density, particle state, force. Neighbours outside the
+    subset take their h and state (rho, A, c, f) from the GPU run's outputs (they are inputs of
+    the targets' force sums, not timed work). Targets are split over a process pool (fork, one
+    cKDTree thread per process); the rate is directed force pairs of the targets (their share
+    of 2F) over the wall time of the two pool phases. Also a 1-process figure on one chunk."""
+    import multiprocessing as mp
+
+    import numpy as np
+    from scipy.spatial import cKDTree
+
+    import oracle
+    procs = procs or cores_used()
+    x = p.x.astype(np.float64)
+    box = np.asarray(p.box, np.float64)
+    st = oracle.particle_state(gpu["rho"], gpu["omega"], p.u, gpu["h"], gpu["div"], gpu["curl"])
+    _G.clear()
+    _G.update(x=x, v=p.v.astype(np.float64), m=p.m.astype(np.float64), u=p.u.astype(np.float64), box=box,
+              tree=cKDTree(x, boxsize=box), h=gpu["h"].astype(np.float64), rho=gpu["rho"].astype(np.float64),
+              A=np.nan_to_num(st["A"], posinf=0.0), c=st["c"], f=st["f"])
+    rng = np.random.default_rng(seed)
+    T = np.sort(rng.choice(p.n, int(frac * p.n), replace=False))
+    chunks = np.array_split(T, procs * 2)
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(procs) as pool:
+        res = pool.map(_w_density, chunks)
+    for idx, hT, rho, A, c, f, _ in res:
+        _G["h"][idx], _G["rho"][idx], _G["A"][idx], _G["c"][idx], _G["f"][idx] = hT, rho, np.nan_to_num(A), c, f
+    with ctx.Pool(procs) as pool:
+        res2 = pool.map(_w_force, chunks)
+    wall = time.perf_counter() - t0
+    pairs = sum(r[0] for r in res2)
+    # one process, one chunk: the single-thread figure
+    _, _, _, _, _, _, t1a = _w_density(chunks[0])
+    p1, t1b = _w_force(chunks[0])
+    cpu = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                cpu = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"value": pairs / wall, "unit": UNIT, "cores": procs, "kind": "oracle",
+            "sample": (f"{p.name} itself ({p.n} particles, every one a source): seeded {frac:.0%} subset of "
+                       f"{T.size} targets (seed {seed}), full oracle work per target (h root + density + state + "
+                       f"force, fp64 numpy/scipy), {procs} processes x 1 thread, wall {wall:.1f} s; neighbours' h "
+                       f"and state from the GPU outputs (inputs, untimed); rate = the targets' directed force "
+                       f"pairs / wall"),
+            "one_thread": {"value": p1 / (t1a + t1b), "targets": int(chunks[0].size), "seconds": t1a + t1b},
+            "cpu_model": cpu}
 
 
 def cores_used():
@@ -333,12 +425,10 @@ def run_sph(args, rank, world, local_rank):
     dominant, secondary = order[0], order[1:]
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        n_s, one, _ = oracle_sample(args.cpu_budget_s)
-        t_s, F_s = one(n_s)
-        cpu = {"value": 2.0 * F_s / t_s, "unit": UNIT, "cores": cores_used(), "kind": "oracle",
-               "sample": (f"C4 generator (64 clumps, seed 140423034) at N={n_s}: one full oracle evaluation "
-                          f"(h root + density + force) in {t_s:.1f} s, fp64 numpy/scipy (cKDTree queries "
-                          f"threaded, sums single-threaded)")}
+        # every output of one more (untimed) evaluation: the neighbours' state for the oracle
+        d = ctx.density(v, m, u)
+        gpu = {k: getattr(d, k).cpu().numpy().astype(np.float64) for k in ("h", "rho", "omega", "div", "curl")}
+        cpu = oracle_subset_rate(p, gpu, frac=args.cpu_frac)
     value = pairs_all / (t_max * 1e-3)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -135,6 +135,10 @@ typedef struct {         /* host struct, filled when non-NULL */
   int64_t n_nb_sources;          /* neighbour-list walks since the last build (incl. re-walks) */
   int64_t n_union_sources;       /* interaction-list walks of this call */
   int32_t cells_reused;          /* 1 if the last build kept the cells (sph_update_cells) */
+  /* binning + sort of the last build (a1-a3): keys, radix passes, permute + pack */
+  double ms_kernel_sort;         /* CUDA events around those launches */
+  int32_t sort_key_bits;         /* top-cell index bits + 3 x Morton levels */
+  int32_t sort_passes;           /* 8-bit radix passes */
 } sph_stats;
 
 /* Fill *cfg with the paper's defaults for the given box. */

@@ -16,6 +16,9 @@ import itertools
 import numpy as np
 from scipy.spatial import cKDTree
 
+#: threads of the cKDTree queries (-1 = all; a process pool sets 1 per process)
+WORKERS = -1
+
 
 def min_image(dx: np.ndarray, box) -> np.ndarray:
     box = np.asarray(box, dtype=np.float64)
@@ -50,7 +53,7 @@ def ball_pairs(x, box, centers_x, radii, tree=None, chunk=200_000):
         cx = centers_x[s:s + chunk]
         rr = radii[s:s + chunk]
         # candidate superset: the tree's own distance may differ from ours by an ulp
-        lists = tree.query_ball_point(cx, rr * (1.0 + 1e-9) + 1e-300, workers=-1,
+        lists = tree.query_ball_point(cx, rr * (1.0 + 1e-9) + 1e-300, workers=WORKERS,
                                       return_sorted=True)
         lens = np.fromiter(map(len, lists), dtype=np.int64, count=len(lists))
         j = np.fromiter(itertools.chain.from_iterable(lists), dtype=np.int64,
@@ -88,7 +91,7 @@ def knn_sorted_distances(x, box, centers_x, k, tree=None):
     if tree is None:
         tree = cKDTree(x, boxsize=np.asarray(box, dtype=np.float64))
     k = min(k, x.shape[0])
-    _, idx = tree.query(centers_x, k=k, workers=-1)
+    _, idx = tree.query(centers_x, k=k, workers=WORKERS)
     idx = idx.reshape(centers_x.shape[0], k)
     dx = min_image(centers_x[:, None, :] - x[idx], box)
     d = np.sqrt((dx * dx).sum(axis=2))

@@ -113,11 +113,13 @@ __global__ void k_keys(const float* __restrict__ x, int64_t n, int nx, int ny, i
 // ---------------------------------------------------------------- a3 ---------
 // cell-order positions; h = h_in[perm] (caller order) or 0
 __global__ void k_pack(const uint32_t* __restrict__ perm, int64_t n, const float* __restrict__ x,
-                       const float* __restrict__ h_in, float4* __restrict__ xh) {
+                       const float* __restrict__ h_in, float4* __restrict__ xh, float4* __restrict__ xref) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n;
        s += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t p = perm[s];
-    xh[s] = make_float4(x[3 * (int64_t)p], x[3 * (int64_t)p + 1], x[3 * (int64_t)p + 2], h_in ? h_in[p] : 0.f);
+    const float4 q = make_float4(x[3 * (int64_t)p], x[3 * (int64_t)p + 1], x[3 * (int64_t)p + 2], h_in ? h_in[p] : 0.f);
+    xh[s] = q;
+    xref[s] = q;
   }
 }
 

@@ -166,7 +166,8 @@ struct sph_ctx {
   };
   std::vector<Timed> timed;
   size_t timed_used = 0;
-  double ms_phase[4] = {0, 0, 0, 0};   // 0 NB walks, 1 h solve, 2 union walks
+  double ms_phase[4] = {0, 0, 0, 0};   // 0 NB walks, 1 h solve, 2 union walks, 3 binning + sort
+  int sort_bits = 0, sort_passes = 0;
   int64_t nb_entries = 0, walk_launches = 0;
 
   // named device buffers

@@ -275,8 +275,15 @@ static float3 box3(sph_ctx* c) {
 // splits on occupancy (and on h with the paper's fraction rule, a4). The list walk
 // (lists.cuh) handles any h < L/2, so the top grid never has to be rebuilt when h grows.
 #define TOP_EDGE_HMEAN 4.0
+// Morton levels keyed below the top grid: at least SORT_DEPTH_MIN (C4 uses 8 below its
+// 14^3 top cells), and as many more as fit in the same number of 8-bit radix passes; a leaf
+// at the deepest keyed level just stays larger (results do not depend on the depth)
+#ifndef SORT_DEPTH_MIN
+#define SORT_DEPTH_MIN 9
+#endif
 static void sort_particles(sph_ctx* c, float h0max, bool have_h) {
   DbgTimer _t(c, "sort");
+  PhaseTimer _p(c, 3);
   const int64_t n = c->n;
   const double L[3] = {c->cfg.box[0], c->cfg.box[1], c->cfg.box[2]};
   const double V = L[0] * L[1] * L[2];
@@ -292,30 +299,33 @@ static void sort_particles(sph_ctx* c, float h0max, bool have_h) {
   }
   int top_bits = 0;
   while ((1ll << top_bits) < ntot) ++top_bits;
-  int depth = std::min(SPH_MAX_DEPTH, (63 - top_bits) / 3);
+  const int passes = (top_bits + 3 * SORT_DEPTH_MIN + 7) / 8;
+  int depth = std::min(SPH_MAX_DEPTH, (8 * passes - top_bits) / 3);
+  depth = std::min(depth, (63 - top_bits) / 3);
   c->depth = depth;
   c->top_bits = top_bits;
   const int kbits = top_bits + 3 * depth;
+  c->sort_bits = kbits;
+  c->sort_passes = (kbits + 7) / 8;
   uint64_t* k0 = B<uint64_t>(c, B_KEYS0, n);
   uint64_t* k1 = B<uint64_t>(c, B_KEYS1, n);
   uint32_t* v0 = B<uint32_t>(c, B_VALS0, n);
   uint32_t* v1 = B<uint32_t>(c, B_VALS1, n);
+  B<uint32_t>(c, B_PERM, n);
   const double sc[3] = {(double)((int64_t)c->ntop[0] << depth) / L[0], (double)((int64_t)c->ntop[1] << depth) / L[1],
                         (double)((int64_t)c->ntop[2] << depth) / L[2]};
   LAUNCH(k_keys, grid1d(c, n, 256), 256, 0, Bget<float>(c, B_XIN), n, c->ntop[0], c->ntop[1], c->ntop[2], depth,
          sc[0], sc[1], sc[2], k0, v0);
   radix_sort(c, k0, v0, k1, v1, n, kbits);
-  // sorted keys / permutation live in KEYS0/VALS0 from here on
-  if (k0 != Bget<uint64_t>(c, B_KEYS0)) {
-    CUDA_TRY(cudaMemcpyAsync(Bget<uint64_t>(c, B_KEYS0), k0, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, c->stream));
-  }
-  uint32_t* perm = B<uint32_t>(c, B_PERM, n);
-  CUDA_TRY(cudaMemcpyAsync(perm, v0, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, c->stream));
+  // the sorted keys / permutation: the buffers holding the result take the names KEYS0 and
+  // PERM (slot swaps, no copies)
+  if (k0 != Bget<uint64_t>(c, B_KEYS0)) std::swap(c->b[B_KEYS0], c->b[B_KEYS1]);
+  if (v0 == Bget<uint32_t>(c, B_VALS0)) std::swap(c->b[B_PERM], c->b[B_VALS0]);
+  else std::swap(c->b[B_PERM], c->b[B_VALS1]);
   float4* xh = B<float4>(c, B_XH, n);
-  LAUNCH(k_pack, grid1d(c, n, 256), 256, 0, perm, n, Bget<float>(c, B_XIN), have_h ? Bget<float>(c, B_HIN) : nullptr,
-         xh);
-  // the cell-order positions of this sort: the reference of a later pseudo-Verlet update
-  CUDA_TRY(cudaMemcpyAsync(B<float4>(c, B_XREF, n), xh, n * sizeof(float4), cudaMemcpyDeviceToDevice, c->stream));
+  // cell-order positions, and the reference of a later pseudo-Verlet update, in one pass
+  LAUNCH(k_pack, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, Bget<float>(c, B_XIN),
+         have_h ? Bget<float>(c, B_HIN) : nullptr, xh, B<float4>(c, B_XREF, n));
   c->skin = 0.f;
 }
 
@@ -1075,7 +1085,10 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   LAUNCH(k_validate_vmu, grid1d(c, n, 256), 256, 0, vd, md, ud, n, ctr(c));
   float4* vm = B<float4>(c, B_VM, n);
   float* uc = B<float>(c, B_U, n);
-  LAUNCH(k_gather_vmu, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, vd, md, ud, vm, uc);
+  {
+    PhaseTimer _p(c, 3);   // the rest of a3 (permute + pack): v, m, u into cell order
+    LAUNCH(k_gather_vmu, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, vd, md, ud, vm, uc);
+  }
   ctr_read(c, hc);
   SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_NONFINITE), SPH_E_DOMAIN, "non-finite velocity");
   SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_MASS), SPH_E_DOMAIN, "mass <= 0 or non-finite");
@@ -1155,6 +1168,9 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
     st->n_nb_entries = c->nb_entries;
     st->n_walk_launches = c->walk_launches;
     st->cells_reused = c->cells_reused ? 1 : 0;
+    st->ms_kernel_sort = c->ms_phase[3];
+    st->sort_key_bits = c->sort_bits;
+    st->sort_passes = c->sort_passes;
     if (c->cfg.flags & SPH_F_COUNT_CANDIDATES) {
       unsigned long long wr[2];
       CUDA_TRY(cudaMemcpy(wr, Bget<unsigned long long>(c, B_WALKRAW), sizeof(wr), cudaMemcpyDeviceToHost));
