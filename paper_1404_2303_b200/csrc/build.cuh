@@ -1,9 +1,10 @@
 // build.cuh — the cell hierarchy on the device (section 3.2).
 //
-//  a1  k_validate_x / k_hrange  : domain checks, max/min h
-//  a2  k_keys                   : key = top-cell index | Morton octants to `depth` levels;
-//                                 one radix sort (radix_sort.cuh) orders every level at once
-//                                 (particles of a cell contiguous in memory)
+//  a1  k_hrange                 : h0 checks, max/min h; x checks in k_keys
+//  a2  k_keys                   : key = top-cell index | Morton octants to `depth` levels,
+//                                 and the radix histograms; one radix sort (radix_sort.cuh)
+//                                 orders every level at once (particles of a cell
+//                                 contiguous in memory)
 //  a3  k_pack                   : particles copied into cell order (float4 {x, y, z, h})
 //  a4  k_level_split / k_make_children : recursive split of a cell into its 8 octants while
 //                                 it holds "more than some minimal number" of particles and
@@ -43,6 +44,7 @@ __host__ __device__ __forceinline__ float node_corner(int i, int l, int axis, co
 }
 
 // ---------------------------------------------------------------- a1 ---------
+// positions finite and inside [0, L) (sph_update_cells; a build validates inside k_keys)
 __global__ void k_validate_x(const float* __restrict__ x, int64_t n, float Lx, float Ly, float Lz,
                              unsigned long long* ctr) {
   int err = 0;
@@ -85,39 +87,69 @@ __global__ void k_hrange(const float* __restrict__ h, int64_t n, unsigned long l
 }
 
 // ---------------------------------------------------------------- a2 ---------
-// Binning in fp64 (R19): cell index floor(x * n_l / L) at the deepest level, clamped.
-__global__ void k_keys(const float* __restrict__ x, int64_t n, int nx, int ny, int nz, int depth,
-                       double sx, double sy, double sz, uint64_t* __restrict__ keys,
-                       uint32_t* __restrict__ vals) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t fx = ((int64_t)nx << depth) - 1, fy = ((int64_t)ny << depth) - 1,
-                  fz = ((int64_t)nz << depth) - 1;
-    int64_t cx = (int64_t)floor((double)x[3 * i] * sx);
-    int64_t cy = (int64_t)floor((double)x[3 * i + 1] * sy);
-    int64_t cz = (int64_t)floor((double)x[3 * i + 2] * sz);
+// bits of v (< 2^21) to every third bit (bit b -> bit 3b): the Morton interleave
+__device__ __forceinline__ uint64_t spread3(uint64_t v) {
+  v &= 0x1fffffull;
+  v = (v | v << 32) & 0x1f00000000ffffull;
+  v = (v | v << 16) & 0x1f0000ff0000ffull;
+  v = (v | v << 8) & 0x100f00f00f00f00full;
+  v = (v | v << 4) & 0x10c30c30c30c30c3ull;
+  v = (v | v << 2) & 0x1249249249249249ull;
+  return v;
+}
+
+// One pass over the caller's positions (a1 + a2): validation (finite, inside [0, L)), the
+// cell key = top-cell index | Morton octants to `depth` levels, binned in fp64 (R19):
+// cell index floor(x * n_l / L) at the deepest level, clamped; the (key, index) pairs; the
+// positions packed as float4 {x, y, z, h0} in caller order (so the permute gathers one
+// 16-byte record per particle); and every radix pass's digit histogram (shared-memory
+// counts, one global add per block and digit).
+__global__ void __launch_bounds__(256) k_keys(const float* __restrict__ x, const float* __restrict__ h0, int64_t n,
+                                              float Lx, float Ly, float Lz, int nx, int ny, int nz, int depth, double sx,
+                                              double sy, double sz, int npass, uint64_t* __restrict__ keys,
+                                              uint32_t* __restrict__ vals, float4* __restrict__ xc,
+                                              uint32_t* __restrict__ hist, unsigned long long* ctr) {
+  __shared__ uint32_t sh[8][256];
+  for (int i = threadIdx.x; i < npass * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
+  __syncthreads();
+  int err = 0;
+  const int64_t fx = ((int64_t)nx << depth) - 1, fy = ((int64_t)ny << depth) - 1, fz = ((int64_t)nz << depth) - 1;
+  const uint64_t lowm = (1ull << depth) - 1ull;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float a = x[3 * i], b = x[3 * i + 1], c = x[3 * i + 2];
+    if (!isfinite(a) || !isfinite(b) || !isfinite(c)) err |= ERRBIT_NONFINITE;
+    else if (a < 0.f || a >= Lx || b < 0.f || b >= Ly || c < 0.f || c >= Lz) err |= ERRBIT_XRANGE;
+    int64_t cx = (int64_t)floor((double)a * sx);
+    int64_t cy = (int64_t)floor((double)b * sy);
+    int64_t cz = (int64_t)floor((double)c * sz);
     cx = min(max(cx, (int64_t)0), fx);
     cy = min(max(cy, (int64_t)0), fy);
     cz = min(max(cz, (int64_t)0), fz);
-    uint64_t t = (uint64_t)((cx >> depth) + (int64_t)nx * ((cy >> depth) + (int64_t)ny * (cz >> depth)));
-    uint64_t m = 0;
-    for (int b = depth - 1; b >= 0; --b) {
-      uint64_t oct = (((cx >> b) & 1) << 2) | (((cy >> b) & 1) << 1) | ((cz >> b) & 1);
-      m = (m << 3) | oct;
-    }
-    keys[i] = (t << (3 * depth)) | m;
+    const uint64_t t = (uint64_t)((cx >> depth) + (int64_t)nx * ((cy >> depth) + (int64_t)ny * (cz >> depth)));
+    const uint64_t m = (spread3((uint64_t)cx & lowm) << 2) | (spread3((uint64_t)cy & lowm) << 1) |
+                       spread3((uint64_t)cz & lowm);
+    const uint64_t k = (t << (3 * depth)) | m;
+    keys[i] = k;
     vals[i] = (uint32_t)i;
+    xc[i] = make_float4(a, b, c, h0 ? h0[i] : 0.f);
+    for (int p = 0; p < npass; ++p) atomicAdd(&sh[p][(k >> (8 * p)) & 255u], 1u);
+  }
+  err = __reduce_or_sync(FULL_MASK, err);
+  if ((threadIdx.x & 31) == 0 && err) atomicOr(&ctr[C_ERR], (unsigned long long)err);
+  __syncthreads();
+  for (int i = threadIdx.x; i < npass * 256; i += blockDim.x) {
+    const uint32_t v = (&sh[0][0])[i];
+    if (v) atomicAdd(&hist[i], v);
   }
 }
 
 // ---------------------------------------------------------------- a3 ---------
-// cell-order positions; h = h_in[perm] (caller order) or 0
-__global__ void k_pack(const uint32_t* __restrict__ perm, int64_t n, const float* __restrict__ x,
-                       const float* __restrict__ h_in, float4* __restrict__ xh, float4* __restrict__ xref) {
+// cell-order positions (and the pseudo-Verlet reference) from the packed caller-order records
+__global__ void k_pack(const uint32_t* __restrict__ perm, int64_t n, const float4* __restrict__ xc,
+                       float4* __restrict__ xh, float4* __restrict__ xref) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n;
        s += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t p = perm[s];
-    const float4 q = make_float4(x[3 * (int64_t)p], x[3 * (int64_t)p + 1], x[3 * (int64_t)p + 2], h_in ? h_in[p] : 0.f);
+    const float4 q = xc[perm[s]];
     xh[s] = q;
     xref[s] = q;
   }

@@ -168,6 +168,8 @@ struct sph_ctx {
   size_t timed_used = 0;
   double ms_phase[4] = {0, 0, 0, 0};   // 0 NB walks, 1 h solve, 2 union walks, 3 binning + sort
   int sort_bits = 0, sort_passes = 0;
+  const float* xin = nullptr;   // this call's positions (caller's device array or a staged copy)
+  const float* hin = nullptr;   // this call's h0 (or null)
   int64_t nb_entries = 0, walk_launches = 0;
 
   // named device buffers
@@ -182,7 +184,7 @@ enum BufId {
   // caller-order inputs / outputs kept between calls
   B_XIN = 0, B_HIN, B_VIN, B_MIN, B_UIN, B_HFIN_O, B_GST_O,
   // sort scratch
-  B_KEYS0, B_KEYS1, B_VALS0, B_VALS1, B_SORT_HIST, B_SORT_STATUS, B_SORT_CTR, B_SCAN_TMP,
+  B_KEYS0, B_KEYS1, B_VALS0, B_VALS1, B_SORT_HIST, B_SORT_STATUS, B_SORT_CTR, B_SCAN_TMP, B_XC,
   // cell-order particle arrays
   B_PERM, B_XH, B_VM, B_U, B_HB, B_HLO, B_HHI, B_STATE, B_DSUMF, B_DACC0, B_DACC1, B_DSUM2,
   B_FX, B_FS,

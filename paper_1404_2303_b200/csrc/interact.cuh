@@ -688,26 +688,30 @@ __global__ void k_x_hist(const float* __restrict__ x, int64_t n, float lo, float
 }
 
 // ------------------------------------------------------------------ misc ---------
-__global__ void k_validate_vmu(const float* __restrict__ v, const float* __restrict__ m, const float* __restrict__ u,
-                               int64_t n, unsigned long long* ctr) {
+// v, m, u checked (finite; m, u > 0) and packed in caller order as float4 {v, m} and u in
+// one coalesced pass, so the permute below gathers one 16-byte record (+ u) per particle
+__global__ void k_validate_pack_vmu(const float* __restrict__ v, const float* __restrict__ m,
+                                    const float* __restrict__ u, int64_t n, float4* __restrict__ vmc,
+                                    unsigned long long* ctr) {
   int err = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    if (!isfinite(v[3 * i]) || !isfinite(v[3 * i + 1]) || !isfinite(v[3 * i + 2])) err |= ERRBIT_NONFINITE;
-    if (!(m[i] > 0.f) || !isfinite(m[i])) err |= ERRBIT_MASS;
-    if (!(u[i] > 0.f) || !isfinite(u[i])) err |= ERRBIT_U;
+    const float a = v[3 * i], b = v[3 * i + 1], c = v[3 * i + 2], mm = m[i], uu = u[i];
+    if (!isfinite(a) || !isfinite(b) || !isfinite(c)) err |= ERRBIT_NONFINITE;
+    if (!(mm > 0.f) || !isfinite(mm)) err |= ERRBIT_MASS;
+    if (!(uu > 0.f) || !isfinite(uu)) err |= ERRBIT_U;
+    vmc[i] = make_float4(a, b, c, mm);
   }
   err = __reduce_or_sync(FULL_MASK, err);
   if ((threadIdx.x & 31) == 0 && err) atomicOr(&ctr[C_ERR], (unsigned long long)err);
 }
 
-__global__ void k_gather_vmu(const uint32_t* __restrict__ perm, int64_t n, const float* __restrict__ v,
-                             const float* __restrict__ m, const float* __restrict__ u, float4* __restrict__ vm,
-                             float* __restrict__ uc) {
+__global__ void k_gather_vmu(const uint32_t* __restrict__ perm, int64_t n, const float4* __restrict__ vmc,
+                             const float* __restrict__ u, float4* __restrict__ vm, float* __restrict__ uc) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n;
        s += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t p = perm[s];
-    vm[s] = make_float4(v[3 * (int64_t)p], v[3 * (int64_t)p + 1], v[3 * (int64_t)p + 2], m[p]);
+    vm[s] = vmc[p];
     uc[s] = u[p];
   }
 }

@@ -188,15 +188,18 @@ static void ensure_smem_attr(sph_ctx* c, const void* func, int bytes) {
 }
 
 // =========================================================== radix sort =========
+// hist_ready: B_SORT_HIST already holds every pass's digit counts (k_keys computes them)
 static void radix_sort(sph_ctx* c, uint64_t*& keys, uint32_t*& vals, uint64_t*& kalt, uint32_t*& valt,
-                       int64_t n, int bits) {
+                       int64_t n, int bits, bool hist_ready = false) {
   if (n <= 1) return;
   int npass = std::max(1, (bits + 7) / 8);
   SPH_REQUIRE(npass <= 8, SPH_E_ARG, "radix sort: more than 64 key bits");
   SPH_REQUIRE(n < (1ll << 30), SPH_E_ARG, "radix sort: n >= 2^30");
   uint32_t* hist = B<uint32_t>(c, B_SORT_HIST, 16 * 256);
-  CUDA_TRY(cudaMemsetAsync(hist, 0, 8 * 256 * sizeof(uint32_t), c->stream));
-  LAUNCH(k_radix_hist, grid1d(c, n, 256), 256, 0, keys, n, npass, hist);
+  if (!hist_ready) {
+    CUDA_TRY(cudaMemsetAsync(hist, 0, 8 * 256 * sizeof(uint32_t), c->stream));
+    LAUNCH(k_radix_hist, grid1d(c, n, 256), 256, 0, keys, n, npass, hist);
+  }
   uint32_t* gofs = hist + 8 * 256;
   LAUNCH(k_radix_offsets, npass, 256, 0, hist, gofs);
   int64_t ntiles = (n + RS_TILE - 1) / RS_TILE;
@@ -314,9 +317,13 @@ static void sort_particles(sph_ctx* c, float h0max, bool have_h) {
   B<uint32_t>(c, B_PERM, n);
   const double sc[3] = {(double)((int64_t)c->ntop[0] << depth) / L[0], (double)((int64_t)c->ntop[1] << depth) / L[1],
                         (double)((int64_t)c->ntop[2] << depth) / L[2]};
-  LAUNCH(k_keys, grid1d(c, n, 256), 256, 0, Bget<float>(c, B_XIN), n, c->ntop[0], c->ntop[1], c->ntop[2], depth,
-         sc[0], sc[1], sc[2], k0, v0);
-  radix_sort(c, k0, v0, k1, v1, n, kbits);
+  uint32_t* hist = B<uint32_t>(c, B_SORT_HIST, 16 * 256);
+  CUDA_TRY(cudaMemsetAsync(hist, 0, 8 * 256 * sizeof(uint32_t), c->stream));
+  float4* xc = B<float4>(c, B_XC, n);
+  LAUNCH(k_keys, grid1d(c, n, 256), 256, 0, c->xin, have_h ? c->hin : nullptr, n, (float)L[0], (float)L[1],
+         (float)L[2], c->ntop[0], c->ntop[1], c->ntop[2], depth, sc[0], sc[1], sc[2], c->sort_passes, k0, v0, xc, hist,
+         ctr(c));
+  radix_sort(c, k0, v0, k1, v1, n, kbits, true);
   // the sorted keys / permutation: the buffers holding the result take the names KEYS0 and
   // PERM (slot swaps, no copies)
   if (k0 != Bget<uint64_t>(c, B_KEYS0)) std::swap(c->b[B_KEYS0], c->b[B_KEYS1]);
@@ -324,9 +331,13 @@ static void sort_particles(sph_ctx* c, float h0max, bool have_h) {
   else std::swap(c->b[B_PERM], c->b[B_VALS1]);
   float4* xh = B<float4>(c, B_XH, n);
   // cell-order positions, and the reference of a later pseudo-Verlet update, in one pass
-  LAUNCH(k_pack, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, Bget<float>(c, B_XIN),
-         have_h ? Bget<float>(c, B_HIN) : nullptr, xh, B<float4>(c, B_XREF, n));
+  LAUNCH(k_pack, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, xc, xh, B<float4>(c, B_XREF, n));
   c->skin = 0.f;
+  // the position checks of k_keys (the sort itself is harmless on invalid input)
+  unsigned long long hc[C_NCOUNTERS];
+  ctr_read(c, hc);
+  SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_NONFINITE), SPH_E_DOMAIN, "non-finite position");
+  SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_XRANGE), SPH_E_DOMAIN, "position outside [0, L)");
 }
 
 // a4: the hierarchy from the sorted keys. Split rule: count > split_count and (rule on)
@@ -845,26 +856,45 @@ int sph_build_cells(sph_ctx* ctx, int64_t n, const float* x, const float* h0) {
 }
 
 // positions in, validated; h0 (optional) in, validated; returns whether a guess is needed
-static bool load_inputs(sph_ctx* c, const float* x, const float* h0, float* h0max) {
+// Positions and h0 for this call: device arrays are used in place (they are consumed inside
+// the call), host arrays copied in. h0 is validated here (its largest value sets the top grid);
+// the positions are validated by k_keys (or k_validate_x, validate_x = true). Returns whether
+// a guess is needed.
+static bool load_inputs(sph_ctx* c, const float* x, const float* h0, float* h0max, bool validate_x = false) {
   const int64_t n = c->n;
-  float* xd = B<float>(c, B_XIN, 3 * n);
-  CUDA_TRY(cudaMemcpyAsync(xd, x, 3 * n * sizeof(float), cudaMemcpyDefault, c->stream));
-  ctr_reset(c);
-  LAUNCH(k_validate_x, grid1d(c, n, 256), 256, 0, xd, n, (float)c->cfg.box[0], (float)c->cfg.box[1],
-         (float)c->cfg.box[2], ctr(c));
-  if (h0) {
-    float* hin = B<float>(c, B_HIN, n);
-    CUDA_TRY(cudaMemcpyAsync(hin, h0, n * sizeof(float), cudaMemcpyDefault, c->stream));
-    LAUNCH(k_hrange, grid1d(c, n, 256), 256, 0, hin, n, ctr(c));
+  if (is_device_ptr(x)) {
+    c->xin = x;
+  } else {
+    float* xd = B<float>(c, B_XIN, 3 * n);
+    CUDA_TRY(cudaMemcpyAsync(xd, x, 3 * n * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    c->xin = xd;
   }
+  ctr_reset(c);
+  if (validate_x)
+    LAUNCH(k_validate_x, grid1d(c, n, 256), 256, 0, c->xin, n, (float)c->cfg.box[0], (float)c->cfg.box[1],
+           (float)c->cfg.box[2], ctr(c));
+  c->hin = nullptr;
   unsigned long long hc[C_NCOUNTERS];
-  ctr_read(c, hc);
-  SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_NONFINITE), SPH_E_DOMAIN, "non-finite position");
-  SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_XRANGE), SPH_E_DOMAIN, "position outside [0, L)");
-  SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_H), SPH_E_DOMAIN, "h0 negative or non-finite");
+  if (h0) {
+    if (is_device_ptr(h0)) {
+      c->hin = h0;
+    } else {
+      float* hd = B<float>(c, B_HIN, n);
+      CUDA_TRY(cudaMemcpyAsync(hd, h0, n * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+      c->hin = hd;
+    }
+    LAUNCH(k_hrange, grid1d(c, n, 256), 256, 0, c->hin, n, ctr(c));
+  }
+  if (h0 || validate_x) {
+    ctr_read(c, hc);
+    SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_NONFINITE), SPH_E_DOMAIN, "non-finite position");
+    SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_XRANGE), SPH_E_DOMAIN, "position outside [0, L)");
+    SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_H), SPH_E_DOMAIN, "h0 negative or non-finite");
+  }
   *h0max = h0 ? as_float(hc[C_HMAXBITS]) : 0.f;
   SPH_REQUIRE(*h0max < h_cap(c), SPH_E_DOMAIN,
               "h0 >= min(L)/2: the minimum-image convention needs h < L/2 (h0 max = " + std::to_string(*h0max) + ")");
+  if (h0) ctr_reset(c);
   return !h0 || hc[C_TMP0] > 0;
 }
 
@@ -1082,12 +1112,13 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   // join the side-stream copies of v, m, u; validate and gather them into cell order
   if (side) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_side[1], 0));
   ctr_reset(c);
-  LAUNCH(k_validate_vmu, grid1d(c, n, 256), 256, 0, vd, md, ud, n, ctr(c));
   float4* vm = B<float4>(c, B_VM, n);
   float* uc = B<float>(c, B_U, n);
   {
-    PhaseTimer _p(c, 3);   // the rest of a3 (permute + pack): v, m, u into cell order
-    LAUNCH(k_gather_vmu, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, vd, md, ud, vm, uc);
+    PhaseTimer _p(c, 3);   // the rest of a3 (permute + pack): v, m, u checked, into cell order
+    float4* vmc = B<float4>(c, B_XC, n);   // caller-order {v, m} (the positions' staging is free again)
+    LAUNCH(k_validate_pack_vmu, grid1d(c, n, 256), 256, 0, vd, md, ud, n, vmc, ctr(c));
+    LAUNCH(k_gather_vmu, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, vmc, ud, vm, uc);
   }
   ctr_read(c, hc);
   SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_NONFINITE), SPH_E_DOMAIN, "non-finite velocity");
@@ -1392,16 +1423,16 @@ int sph_update_cells(sph_ctx* ctx, const float* x, const float* h0) {
   }
   const int64_t n = c->n;
   float h0max = 0.f;
-  const bool need_guess = load_inputs(c, x, h0, &h0max);
+  const bool need_guess = load_inputs(c, x, h0, &h0max, true);
   SPH_REQUIRE(!need_guess, SPH_E_ARG, "sph_update_cells needs every h0 > 0");
   unsigned long long hc[C_NCOUNTERS];
   ctr_reset(c);
-  LAUNCH(k_hrange, grid1d(c, n, 256), 256, 0, Bget<float>(c, B_HIN), n, ctr(c));
+  LAUNCH(k_hrange, grid1d(c, n, 256), 256, 0, c->hin, n, ctr(c));
   ctr_read(c, hc);
   const float hmin = as_float(hc[C_HMINBITS]);
   ctr_reset(c);
-  LAUNCH(k_update_pos, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, Bget<float>(c, B_XIN),
-         Bget<float>(c, B_HIN), Bget<float4>(c, B_XREF), (float)c->cfg.box[0], (float)c->cfg.box[1],
+  LAUNCH(k_update_pos, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, c->xin, c->hin,
+         Bget<float4>(c, B_XREF), (float)c->cfg.box[0], (float)c->cfg.box[1],
          (float)c->cfg.box[2], Bget<float4>(c, B_XH), ctr(c));
   ctr_read(c, hc);
   const float drift = as_float(hc[C_HMAXBITS]);

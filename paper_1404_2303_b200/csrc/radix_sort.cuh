@@ -1,8 +1,9 @@
 // radix_sort.cuh — hand-written LSD radix sort of (u64 key, u32 value) pairs for sm_100a.
 //
 // Onesweep structure: one histogram kernel computes every pass's digit counts in a
-// single read of the keys; each 8-bit pass is then ONE kernel: tiles of 4096 items
-// ranked in-warp with __match_any_sync (stable), tile digit counts published with a
+// single read of the keys (fused into k_keys, build.cuh); each 8-bit pass is then ONE
+// kernel: tiles of 2048 items
+// ranked in-warp from digit-bit ballots (stable), tile digit counts published with a
 // decoupled look-back (per-digit status words), items staged in shared memory in
 // digit order and written out in coalesced digit runs. Digit offsets are scanned on the
 // device (k_radix_offsets); every pass runs, so the sort has no host round trip.
@@ -13,9 +14,12 @@
 #define RS_THREADS 256
 #endif
 #ifndef RS_ITEMS
-#define RS_ITEMS 16
-#endif
+#define RS_ITEMS 8      // 2048-item tiles: <= 64 registers, 4 blocks per SM (16 items: 128 registers,
+#endif                  // 2 blocks, +36% on the 16.8M binning run; profiles/round2/binning_*.txt)
 #define RS_TILE (RS_THREADS * RS_ITEMS)
+#ifndef RS_LB
+#define RS_LB 8         // predecessor statuses loaded together in the look-back
+#endif
 #define RS_WARPS (RS_THREADS / 32)
 #define RS_FLAG_INC 0x80000000u
 #define RS_FLAG_AGG 0x40000000u
@@ -71,7 +75,10 @@ struct RadixSmem {
   uint32_t vals[RS_TILE];
 };
 
-__global__ void __launch_bounds__(RS_THREADS) k_radix_pass(
+#ifndef RS_MINB
+#define RS_MINB 4
+#endif
+__global__ void __launch_bounds__(RS_THREADS, RS_MINB) k_radix_pass(
     const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint64_t* __restrict__ kout,
     uint32_t* __restrict__ vout, int64_t n, int shift, const uint32_t* __restrict__ gofs,
     uint32_t* status, uint32_t* tile_ctr) {
@@ -102,11 +109,19 @@ __global__ void __launch_bounds__(RS_THREADS) k_radix_pass(
       dg[it] = 256u;
     }
   }
-  // stable in-warp ranking: items visited in position order (it major, lane minor)
+  // stable in-warp ranking: items visited in position order (it major, lane minor); the
+  // lanes holding the same digit from 9 ballots (8 digit bits + the invalid flag), cheaper
+  // than __match_any_sync
 #pragma unroll
   for (int it = 0; it < RS_ITEMS; ++it) {
     uint32_t d = dg[it];
-    unsigned peers = __match_any_sync(FULL_MASK, d);
+    unsigned peers = FULL_MASK;
+#pragma unroll
+    for (int b = 0; b < 9; ++b) {
+      const bool bit = (d >> b) & 1u;
+      const unsigned bb = __ballot_sync(FULL_MASK, bit);
+      peers &= bit ? bb : ~bb;
+    }
     uint32_t cnt_before = 0;
     if (d < 256u) cnt_before = S.wcnt[w][d];
     __syncwarp();
@@ -134,16 +149,25 @@ __global__ void __launch_bounds__(RS_THREADS) k_radix_pass(
       S.gbase[d] = gofs[d];
     } else {
       atomicExch(st, RS_FLAG_AGG | tcnt);
+      // look back RS_LB predecessors at a time (independent loads in flight): the tiles of
+      // the first wave all publish their aggregates at about the same time, and a serial
+      // walk would pay one L2 round trip per predecessor
       uint32_t excl = 0;
       int64_t pt = (int64_t)tile - 1;
-      while (pt >= 0) {
-        uint32_t s;
-        do {
-          s = ld_volatile_u32(status + (size_t)pt * 256 + d);
-        } while ((s & (RS_FLAG_INC | RS_FLAG_AGG)) == 0);
-        excl += s & RS_VAL_MASK;
-        if (s & RS_FLAG_INC) break;
-        --pt;
+      bool done = false;
+      while (!done) {
+        uint32_t sv[RS_LB];
+#pragma unroll
+        for (int k = 0; k < RS_LB; ++k)
+          sv[k] = pt - k >= 0 ? ld_volatile_u32(status + (size_t)(pt - k) * 256 + d) : RS_FLAG_INC;
+#pragma unroll
+        for (int k = 0; k < RS_LB; ++k) {
+          if (done) break;
+          while ((sv[k] & (RS_FLAG_INC | RS_FLAG_AGG)) == 0) sv[k] = ld_volatile_u32(status + (size_t)(pt - k) * 256 + d);
+          excl += sv[k] & RS_VAL_MASK;
+          if (sv[k] & RS_FLAG_INC) done = true;
+        }
+        pt -= RS_LB;
       }
       atomicExch(st, RS_FLAG_INC | (excl + tcnt));
       S.gbase[d] = gofs[d] + excl;
