@@ -217,6 +217,15 @@ def oracle_subset_rate(p, gpu, frac=0.02, procs=None, seed=140423098):
             "cpu_model": cpu}
 
 
+def measured_hbm():
+    """HBM copy bandwidth (GB/s) from MEASURED_PEAKS.json (driver-written), else the profiling
+    guide's fallback."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, ValueError, KeyError):
+        return 6550.7, "fallback (B200_PROFILING.md)"
+
+
 def cores_used():
     try:
         return len(os.sched_getaffinity(0))
@@ -429,6 +438,19 @@ def run_sph(args, rank, world, local_rank):
         d = ctx.density(v, m, u)
         gpu = {k: getattr(d, k).cpu().numpy().astype(np.float64) for k in ("h", "rho", "omega", "div", "curl")}
         cpu = oracle_subset_rate(p, gpu, frac=args.cpu_frac)
+    # a1-a3 (binning + sort + permute) against HBM: SURVEY 8(d)'s algorithmic bytes per particle,
+    # (28 + 24 x passes + 8 + 80), over the CUDA-event time of those kernels in the step
+    passes = sd[-1]["sort_passes"]
+    bpp = 28 + 24 * passes + 8 + 80
+    ms_sort = med("ms_kernel_sort", sd)
+    hbm = measured_hbm()
+    ach_bin = N * bpp / (ms_sort * 1e-3) / 1e9 if ms_sort > 0 else 0.0
+    roof_bin = {"kernels": "k_keys + k_radix_pass x passes + k_pack + k_validate_pack_vmu + k_gather_vmu",
+                "bound": "hbm", "achieved": ach_bin, "peak": hbm[0], "unit": "GB/s", "frac": ach_bin / hbm[0],
+                "traffic": None, "bytes_per_particle": bpp, "sort_passes": passes,
+                "sort_key_bits": sd[-1]["sort_key_bits"], "ms_per_step": ms_sort, "peak_source": hbm[1],
+                "note": ("C4's 2.1M-particle arrays are L2-resident per pass (126 MB L2), so this is not an HBM "
+                         "measurement; the shard-size run is tools/binning_run.py (profiles/round2/binning_16M.md)")}
     value = pairs_all / (t_max * 1e-3)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -442,6 +464,7 @@ def run_sph(args, rank, world, local_rank):
                    "n_ngb": 48, "n_ngb_tol": cfg.n_ngb_tol},
         "roofline": dominant,
         "roofline_others": secondary,
+        "roofline_binning": roof_bin,
         "cpu_baseline": cpu,
         "e2e": ({"value": e2e_pairs / (e2e_tmax * 1e-3), "unit": UNIT,
                  "h2d_bytes_per_step": e2e["h2d_bytes_per_step"], "d2h_bytes_per_step": e2e["d2h_bytes_per_step"]}

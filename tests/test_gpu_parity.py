@@ -177,3 +177,51 @@ def test_unquantised_positions_at_the_faces(t):
     including 0 and the largest fp32 below L; all particles compared, modes A and B."""
     p = workloads.edges_unquantised(t, n=4000)
     _modes(p)
+
+def test_c5_full_size_sampled():
+    """C5 (BASELINE configs[4]: 512^3 = 134,217,728 clustered particles, 512 clumps) on one
+    B200 in one context: 2,000 seeded targets plus the 100 largest and 100 smallest h, modes A
+    and B. The oracle runs on the particles within 2 h_max of a target (every source of their
+    density and force sums, and of their neighbours' densities: the sums are exact), found by a
+    grid hash of cell edge 2 h_max."""
+    import torch
+
+    import paper_1404_2303_b200 as sph
+    p = workloads.c5()
+    dev = torch.device("cuda:0")
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    ctx = sph.Context(sph.default_config(p.box, n_ngb_tol=1e-4, split_count=48, split_fraction=0.0))
+    ctx.build_cells(t(p.x), None)
+    d = ctx.density(t(p.v), t(p.m), t(p.u))
+    f = ctx.force(t(p.v))
+    g = {k: getattr(d, k).cpu().numpy() for k in ("h", "rho", "omega", "n_nbr", "div", "curl")}
+    g.update({k: getattr(f, k).cpu().numpy() for k in ("a", "dudt", "vsig", "n_nbr_force")})
+    assert d.stats["n_unconverged"] == 0
+    ctx.close()
+    del d, f
+    torch.cuda.empty_cache()
+    rng = np.random.default_rng(5)
+    order = np.argsort(g["h"])
+    T = np.unique(np.concatenate([rng.choice(p.n, 2000, replace=False), order[:100], order[-100:]]))
+    # local particle set: every particle in the grid cells (edge 2 h_max) around a target's cell
+    R = 2.0 * float(g["h"].max()) * 1.001
+    nc = max(3, int(1.0 / R))
+    cell = np.minimum((p.x * nc).astype(np.int64), nc - 1)
+    cid = (cell[:, 0] * nc + cell[:, 1]) * nc + cell[:, 2]
+    tc = cell[T]
+    near = set()
+    for ox in (-1, 0, 1):
+        for oy in (-1, 0, 1):
+            for oz in (-1, 0, 1):
+                q = (tc + np.array([ox, oy, oz])) % nc
+                near.update(((q[:, 0] * nc + q[:, 1]) * nc + q[:, 2]).tolist())
+    sel = np.nonzero(np.isin(cid, np.fromiter(near, np.int64)))[0]
+    del cell, cid
+    loc = p.take(sel)
+    tl = np.searchsorted(sel, T)
+    h_or = oracle.solve_h(loc.x, loc.box, targets=tl)
+    rel_h = np.abs(g["h"][T] - h_or) / h_or
+    assert rel_h.max() <= P.TOL_H, float(rel_h.max())
+    gl = {k: v[sel] for k, v in g.items()}
+    orc = P.oracle_given_h(loc, gl["h"], targets=tl)
+    P.compare(gl, orc, tl)
