@@ -65,6 +65,10 @@ typedef enum {
 #define SPH_F_COUNT_CANDIDATES 2u /* count distance tests (stats.n_candidates) */
 #define SPH_F_DIAGNOSTICS 4u      /* count borderline and coincident pairs (stats.n_borderline,
                                      n_borderline_force, n_coincident) */
+#define SPH_F_SYMMETRIC 8u        /* sph_force evaluates every unordered pair once and updates both
+                                     particles (j side by shared-memory then global float
+                                     reductions: not bitwise deterministic). Default: gather form,
+                                     every pair from both sides, deterministic */
 
 typedef struct {
   int32_t abi_version;   /* = SPH_ABI_VERSION */

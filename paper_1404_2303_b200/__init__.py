@@ -7,5 +7,5 @@ fallback.
 from .sph import (  # noqa: F401
     Context, Config, Stats, SphError, default_config, load, EXPORTS,
     SPH_OK, SPH_E_ARG, SPH_E_DOMAIN, SPH_E_STATE, SPH_E_NOCONV, SPH_E_CUDA, SPH_E_NCCL, SPH_E_OOM,
-    SPH_F_SYNC, SPH_F_COUNT_CANDIDATES, SPH_F_DIAGNOSTICS,
+    SPH_F_SYNC, SPH_F_COUNT_CANDIDATES, SPH_F_DIAGNOSTICS, SPH_F_SYMMETRIC,
 )

@@ -173,7 +173,7 @@ struct sph_ctx {
   int64_t nb_entries = 0, walk_launches = 0;
 
   // named device buffers
-  DBuf b[80];
+  DBuf b[96];
   cudaEvent_t ev[12];
   cudaStream_t stream2 = nullptr;   // side stream: host->device copies overlapped with the h iteration
   cudaEvent_t ev_side[4];   // [0] side stream may start, [1] v, m, u copied, [2] h ready, [3] h copied back
@@ -196,10 +196,11 @@ enum BufId {
   // groups and interaction lists
   B_GROUPS, B_GOFF, B_GLEN, B_LIST, B_NBR2, B_NBCNT, B_NBOFF, B_NBOVF, B_OVFIDX, B_NBENT, B_GKEYS, B_GORDER, B_SHRUNK, B_OVFC, B_OVFCNT, B_HCTR, B_RGL, B_RGCNT, B_XREF, B_TGT, B_ACTIVE, B_TSTEP, B_WALKRAW, B_GFLAG, B_GSEL, B_HRCH,
   // misc scratch
+  B_PGROUP, B_SYM_IA, B_SYM_IVS, B_SYM_ICNT, B_SYM_JA, B_SYM_JVS, B_SYM_JCNT,
   B_TMPI0, B_TMPI1, B_TMPL0, B_TMPL1, B_COUNTERS, B_OUT0, B_OUT1, B_OUT2, B_OUT3, B_OUT4, B_OUT5,
   B_COUNT
 };
-static_assert(B_COUNT <= 80, "too many buffers");
+static_assert(B_COUNT <= 96, "too many buffers");
 
 // device counters layout (int64 slots in B_COUNTERS)
 enum CounterId {

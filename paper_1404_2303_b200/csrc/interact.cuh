@@ -488,6 +488,243 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FORCE_MINB) k_force(GroupLis
   }
 }
 
+// ------------------------------------------------------------------ symmetric force --
+// The paper's pair update ("a pair ... updates both particles"; north_star item 4):
+// every unordered pair {i, j} is evaluated ONCE, by its owner, and both particles are updated.
+// Owner of the pair: the target group with the smaller index (a pair inside one group: the
+// lower cell-order index; a pair with a source that is not a target, e.g. halo or inactive:
+// the target's group). Each pair lies in both groups' interaction lists (the union criterion
+// r < max(h_i, h_j) is symmetric), so every pair is found by its owner.
+//   i side (the owner's lane): registers, written once per target (ia, idu, ivs, icnt);
+//   j side: shared-memory slots per staged source (red.shared across the lanes that hit it),
+//   one global red.add per slot and stage into ja / jdu / jvs / jcnt (cell order).
+// k_force_sym_finish adds the two sides in the caller's order. Global float reductions are
+// order-dependent, so unlike the gather kernel k_force this one is not bitwise deterministic.
+struct ForceSym {
+  const int* pgroup;   // cell order -> target group
+  float4* ia;          // i side: a (xyz), du/dt
+  float* ivs;
+  int* icnt;
+  float4* ja;          // j side (reductions)
+  unsigned* jvs;       // v_sig bits (positive floats: integer max)
+  int* jcnt;
+};
+
+template <bool DIAG>
+__global__ void __launch_bounds__(FORCE_WARPS * 32, FORCE_MINB)
+    k_force_sym(GroupLists G, const float4* __restrict__ fx, const float4* __restrict__ vm,
+                const float4* __restrict__ fs, float alpha, float3 Lbox, ForceOut out, ForceSym Y,
+                unsigned long long* ctr) {
+  __shared__ float4 sa[FORCE_WARPS][32];   // x, y, z (group frame), 1/h_j
+  __shared__ float4 sb[FORCE_WARPS][32];   // v_j, m_j
+  __shared__ float4 sc[FORCE_WARPS][32];   // A~_j, rho_j, c_j, f_j
+  __shared__ int sj[FORCE_WARPS][32];      // source index (cell order), -1 none
+  __shared__ int sown[FORCE_WARPS][32];    // 1: the pair with this source is owned by any target of the group
+  __shared__ float4 jacc[FORCE_WARPS][32]; // j-side sums of this stage
+  __shared__ unsigned jvsm[FORCE_WARPS][32];
+  __shared__ int jcn[FORCE_WARPS][32];
+  __shared__ __align__(8) float sxyzw[FORCE_WARPS][4][32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int gid = blockIdx.x * FORCE_WARPS + wib;
+  if (gid >= G.ngroups) return;
+  const int4 grp = G.groups[gid];
+  const int s = grp.y + lane;
+  const bool act = lane < grp.z && out.tgt[s];
+  if (!__any_sync(FULL_MASK, act)) return;
+  const float L[3] = {Lbox.x, Lbox.y, Lbox.z};
+  const float4 o4 = fx[grp.y];
+  const float3 o = make_float3(o4.x, o4.y, o4.z);
+  const float3 oL = make_float3(o4.x - L[0], o4.y - L[1], o4.z - L[2]);
+  float xi = 0.f, yi = 0.f, zi = 0.f, hinv = 0.f, vxi = 0.f, vyi = 0.f, vzi = 0.f, mi = 0.f;
+  float At = 0.f, rhoi = 0.f, ci = 0.f, fi = 0.f;
+  if (act) {
+    const float4 p = fx[s], q = vm[s], w = fs[s];
+    xi = p.x - o.x;
+    yi = p.y - o.y;
+    zi = p.z - o.z;
+    hinv = p.w;
+    vxi = q.x;
+    vyi = q.y;
+    vzi = q.z;
+    mi = q.w;
+    At = w.x;
+    rhoi = w.y;
+    ci = w.z;
+    fi = w.w;
+  }
+  const float hi = act ? 1.0f / hinv : 0.f;
+  const float hi2 = act ? hi * hi : -1.f;
+  const float h2i = hinv * hinv;
+  const float hhat = SPH_CNORM * h2i * h2i;
+  float ax = 0.f, ay = 0.f, az = 0.f, du = 0.f, vsig = 0.f;
+  int cnt = 0;
+  long long ncand = 0, nbord = 0;
+  const int64_t off = G.off[gid];
+  const int len = G.len[gid];
+  const int nst = (len + 31) / 32;
+  for (int stg = 0; stg < nst; ++stg) {
+    const int e = stg + lane * nst;
+    float4 a = make_float4(1e30f, 1e30f, 1e30f, 0.f), b = make_float4(0.f, 0.f, 0.f, 0.f), c = b;
+    int jj = -1, own = 0;
+    if (e < len) {
+      const uint32_t ent = G.list[off + e];
+      const uint32_t j = ent & SPH_IDX_MASK;
+      const float4 p = fx[j];
+      const float3 r = rel_pos(p, ent >> SPH_IDX_BITS, o, oL, L);
+      a = make_float4(r.x, r.y, r.z, p.w);
+      b = vm[j];
+      c = fs[j];
+      jj = (int)j;
+      // 2: every pair with j owned here; 1: owned for the targets below j in this group; 0: by j's group
+      const int pj = Y.pgroup[j];
+      own = (!out.tgt[j] || pj > gid) ? 2 : (pj == gid ? 1 : 0);
+    }
+    sa[wib][lane] = a;
+    sxyzw[wib][0][lane] = a.x;
+    sxyzw[wib][1][lane] = a.y;
+    sxyzw[wib][2][lane] = a.z;
+    sxyzw[wib][3][lane] = a.w;
+    sb[wib][lane] = b;
+    sc[wib][lane] = c;
+    sj[wib][lane] = jj;
+    sown[wib][lane] = own;
+    jacc[wib][lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+    jvsm[wib][lane] = 0u;
+    jcn[wib][lane] = 0;
+    __syncwarp();
+    ncand += act ? min(32, (len - stg + nst - 1) / nst) : 0;
+    unsigned hm = 0u;
+    {
+      const float2* X2 = reinterpret_cast<const float2*>(sxyzw[wib][0]);
+      const float2* Y2 = reinterpret_cast<const float2*>(sxyzw[wib][1]);
+      const float2* Z2 = reinterpret_cast<const float2*>(sxyzw[wib][2]);
+      const float2* W2 = reinterpret_cast<const float2*>(sxyzw[wib][3]);
+#pragma unroll 8
+      for (int t = 0; t < 16; ++t) {
+        const float2 r2 = r2_pair(xi, yi, zi, X2[t], Y2[t], Z2[t]);
+        const float2 hw = W2[t];
+        const bool a0 = r2.x < hi2 || r2.x * (hw.x * hw.x) < 1.0f;
+        const bool a1 = r2.y < hi2 || r2.y * (hw.y * hw.y) < 1.0f;
+        hm |= ((unsigned)a0 | ((unsigned)a1 << 1)) << (2 * t);
+      }
+      hm = act ? hm : 0u;
+    }
+    if (DIAG && act) {
+      for (int t = 0; t < 32; ++t) {
+        const float4 qa = sa[wib][t];
+        if (sj[wib][t] < 0 || sj[wib][t] == s) continue;
+        const float dx = xi - qa.x, dy = yi - qa.y, dz = zi - qa.z;
+        const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+        const float hmx = fmaxf(hi, 1.0f / qa.w), hm2 = hmx * hmx;
+        nbord += fabsf(r2 - hm2) <= 2.f * SPH_BAND * hm2 ? 1 : 0;
+      }
+    }
+    while (hm) {
+      const int t = __ffs(hm) - 1;
+      hm &= hm - 1;
+      const int jt = sj[wib][t];
+      const int ow = sown[wib][t];
+      if (jt == s || ow == 0 || (ow == 1 && jt < s)) continue;   // self, or owned elsewhere
+      const float4 qa = sa[wib][t], qb = sb[wib][t], qc = sc[wib][t];
+      const float dx = xi - qa.x, dy = yi - qa.y, dz = zi - qa.z;
+      const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+      const float hjinv = qa.w;
+      const float hj2i = hjinv * hjinv;
+      const bool in_i = r2 < hi2;
+      const bool in_j = r2 * hj2i < 1.0f;
+      const float rinv = r2 > 0.f ? rsqrtf(r2) : 0.f;
+      const float r = r2 * rinv;
+      const float fpi = in_i ? spline_fp(r * hinv) : 0.f;
+      const float fpj = in_j ? spline_fp(r * hjinv) : 0.f;
+      const float hhatj = SPH_CNORM * hj2i * hj2i;
+      const float Gi = hhat * fpi * rinv;
+      const float Gj = hhatj * fpj * rinv;
+      const float vx = vxi - qb.x, vy = vyi - qb.y, vz = vzi - qb.z;
+      const float vdx = fmaf(vx, dx, fmaf(vy, dy, vz * dz));
+      const float w = fminf(0.f, vdx * rinv);
+      const float cs = ci + qc.z - 3.f * w;
+      const float Pi = __fdividef(-alpha * cs * w, rhoi + qc.y);
+      const float V = Pi * (fi + qc.w) * (Gi + Gj);
+      const float AGi = At * fpi * rinv;
+      const float AGj = qc.x * fpj * rinv;
+      const float T = AGi + AGj + 0.25f * V;
+      const float mj = qb.w;
+      const float mT = mj * T;
+      ax = fmaf(-mT, dx, ax);
+      ay = fmaf(-mT, dy, ay);
+      az = fmaf(-mT, dz, az);
+      du = fmaf(mj * vdx, AGi + 0.125f * V, du);
+      vsig = fmaxf(vsig, cs);
+      cnt += 1;
+      // j side: a_j += m_i T dx, du_j += m_i (v_ij . dx)(A_j G_j + V/8)
+      const float miT = mi * T;
+      atomicAdd(&jacc[wib][t].x, miT * dx);
+      atomicAdd(&jacc[wib][t].y, miT * dy);
+      atomicAdd(&jacc[wib][t].z, miT * dz);
+      atomicAdd(&jacc[wib][t].w, mi * vdx * (AGj + 0.125f * V));
+      atomicMax(&jvsm[wib][t], __float_as_uint(cs));
+      atomicAdd(&jcn[wib][t], 1);
+    }
+    __syncwarp();
+    // one global reduction per source slot of the stage that received a contribution
+    if (jcn[wib][lane] > 0) {
+      const int j = sj[wib][lane];
+      const float4 q = jacc[wib][lane];
+      atomicAdd(&Y.ja[j].x, q.x);
+      atomicAdd(&Y.ja[j].y, q.y);
+      atomicAdd(&Y.ja[j].z, q.z);
+      atomicAdd(&Y.ja[j].w, q.w);
+      atomicMax(&Y.jvs[j], jvsm[wib][lane]);
+      atomicAdd(&Y.jcnt[j], jcn[wib][lane]);
+    }
+    __syncwarp();
+  }
+  if (act) {
+    Y.ia[s] = make_float4(ax, ay, az, du);
+    Y.ivs[s] = vsig;
+    Y.icnt[s] = cnt;
+  }
+  long long nf = act ? cnt : 0;
+#pragma unroll
+  for (int o2 = 16; o2 > 0; o2 >>= 1) {
+    ncand += __shfl_xor_sync(FULL_MASK, ncand, o2);
+    nf += __shfl_xor_sync(FULL_MASK, nf, o2);
+  }
+  if (lane == 0 && ctr) {
+    atomicAdd(&ctr[C_CAND], (unsigned long long)ncand);
+    atomicAdd(&ctr[C_NFORCE], 2ull * (unsigned long long)nf);   // each evaluated pair counts for both
+  }
+  if (DIAG) {
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) nbord += __shfl_xor_sync(FULL_MASK, nbord, o2);
+    if (lane == 0 && ctr) atomicAdd(&ctr[C_BORDER_F], (unsigned long long)nbord);
+  }
+}
+
+// both sides of the symmetric force into the caller's order (targets only)
+__global__ void k_force_sym_finish(const uint32_t* __restrict__ perm, int64_t n, const uint8_t* __restrict__ tgt,
+                                   ForceSym Y, ForceOut out) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+    if (!tgt[s]) continue;
+    const uint32_t p = perm[s];
+    const float4 a = Y.ia[s], b = Y.ja[s];
+    out.a[3 * (int64_t)p] = a.x + b.x;
+    out.a[3 * (int64_t)p + 1] = a.y + b.y;
+    out.a[3 * (int64_t)p + 2] = a.z + b.z;
+    out.dudt[p] = a.w + b.w;
+    if (out.vsig) out.vsig[p] = fmaxf(Y.ivs[s], __uint_as_float(Y.jvs[s]));
+    if (out.nnbr) out.nnbr[p] = Y.icnt[s] + Y.jcnt[s];
+  }
+}
+
+__global__ void k_pgroup(const int4* __restrict__ groups, int ng, int* __restrict__ pgroup) {
+  const int lane = threadIdx.x & 31;
+  const int g = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  if (g >= ng) return;
+  const int4 gr = groups[g];
+  if (lane < gr.z) pgroup[gr.y + lane] = g;
+}
+
 // ------------------------------------------------------------------ h solve -------
 // The h iteration of Eq. 3 (R3, R4) for every particle on its own neighbour
 // list: the squared distances r^2 < h_build^2 recorded by the NB walk (lists.cuh). For any

@@ -1275,9 +1275,31 @@ int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out, int3
   CUDA_TRY(cudaEventRecord(c->ev[10], c->stream));
   {
     DbgTimer _t(c, "force kernel");
-    auto kf = (c->cfg.flags & SPH_F_DIAGNOSTICS) ? k_force<true> : k_force<false>;
-    LAUNCH(kf, gridfull(G.ngroups, FORCE_WARPS), FORCE_WARPS * 32, 0, G, Bget<float4>(c, B_FX),
-           Bget<float4>(c, B_VM), Bget<float4>(c, B_FS), c->cfg.alpha, box3(c), fo, ctr(c));
+    if (c->cfg.flags & SPH_F_SYMMETRIC) {
+      // every unordered pair once, both particles updated (interact.cuh k_force_sym)
+      const int64_t n = c->n;
+      ForceSym Y;
+      Y.pgroup = B<int>(c, B_PGROUP, n);
+      LAUNCH(k_pgroup, gridfull((int64_t)G.ngroups * 32, 256), 256, 0, G.groups, G.ngroups, B<int>(c, B_PGROUP, n));
+      Y.ia = B<float4>(c, B_SYM_IA, n);
+      Y.ivs = B<float>(c, B_SYM_IVS, n);
+      Y.icnt = B<int>(c, B_SYM_ICNT, n);
+      Y.ja = B<float4>(c, B_SYM_JA, n);
+      Y.jvs = B<unsigned>(c, B_SYM_JVS, n);
+      Y.jcnt = B<int>(c, B_SYM_JCNT, n);
+      CUDA_TRY(cudaMemsetAsync(Y.ja, 0, n * sizeof(float4), c->stream));
+      CUDA_TRY(cudaMemsetAsync(Y.jvs, 0, n * sizeof(unsigned), c->stream));
+      CUDA_TRY(cudaMemsetAsync(Y.jcnt, 0, n * sizeof(int), c->stream));
+      auto ks = (c->cfg.flags & SPH_F_DIAGNOSTICS) ? k_force_sym<true> : k_force_sym<false>;
+      LAUNCH(ks, gridfull(G.ngroups, FORCE_WARPS), FORCE_WARPS * 32, 0, G, Bget<float4>(c, B_FX), Bget<float4>(c, B_VM),
+             Bget<float4>(c, B_FS), c->cfg.alpha, box3(c), fo, Y, ctr(c));
+      LAUNCH(k_force_sym_finish, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, Bget<uint8_t>(c, B_TGT), Y,
+             fo);
+    } else {
+      auto kf = (c->cfg.flags & SPH_F_DIAGNOSTICS) ? k_force<true> : k_force<false>;
+      LAUNCH(kf, gridfull(G.ngroups, FORCE_WARPS), FORCE_WARPS * 32, 0, G, Bget<float4>(c, B_FX),
+             Bget<float4>(c, B_VM), Bget<float4>(c, B_FS), c->cfg.alpha, box3(c), fo, ctr(c));
+    }
   }
   CUDA_TRY(cudaEventRecord(c->ev[11], c->stream));
   flush_out(c, maps, c->ev[5]);

@@ -32,6 +32,7 @@ SPH_OK, SPH_E_ARG, SPH_E_DOMAIN, SPH_E_STATE, SPH_E_NOCONV, SPH_E_CUDA, SPH_E_NC
 SPH_F_SYNC = 1
 SPH_F_COUNT_CANDIDATES = 2
 SPH_F_DIAGNOSTICS = 4
+SPH_F_SYMMETRIC = 8
 ABI_VERSION = 2
 
 

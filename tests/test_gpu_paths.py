@@ -281,3 +281,21 @@ def test_active_subset_edge_cases():
     ctx.build_cells(t(p.x))
     assert torch.equal(ctx.density(t(p.v), t(p.m), t(p.u)).h, d.h)
     ctx.close()
+
+
+@pytest.mark.parametrize("case", ["tiny", "c1"])
+def test_symmetric_force(case):
+    """SPH_F_SYMMETRIC: every unordered pair evaluated once by its owner group and both
+    particles updated: a, du/dt, v_sig and n_nbr_force against the oracle (north_star
+    tolerances), and against the default gather form."""
+    import paper_1404_2303_b200 as sph
+    if case == "tiny":
+        p = workloads.tiny(14, n=5000, clump_frac=0.4, n_dup=3)
+        p.h0[:] = 0.0
+    else:
+        p = workloads.c1()
+    g, _ = _check(p, flags=sph.SPH_F_SYNC | sph.SPH_F_SYMMETRIC, **BENCH_CFG)
+    g0 = P.run_gpu(p, **BENCH_CFG)
+    assert g["stats_force"]["n_pairs"] == g0["stats_force"]["n_pairs"]
+    assert np.array_equal(g["n_nbr_force"], g0["n_nbr_force"])
+    assert np.array_equal(g["vsig"], g0["vsig"])
