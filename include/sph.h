@@ -335,6 +335,18 @@ int sph_timestep(sph_ctx* ctx, int64_t n, const float* h, const float* vsig, flo
 #define SPH_X_XH 8
 int sph_debug_export(sph_ctx* ctx, int32_t what, void* out, int64_t cap, int64_t* count);
 
+/* ---- the paper's cell-pair loops, for the sorted-vs-naive ablation (not
+ * the hot path). After sph_density: a uniform periodic grid of edge >= max h, each
+ * cell with itself and its 13 forward neighbours, the density sums of Eq. 2 by the naive
+ * double loop (sorted = 0) or the sorted sweeps with early exit (sorted = 1,
+ * P:644-669 with R6/R7, 13 presorted directions per cell). rho_out [n] (caller order, device or
+ * host, or NULL) gets rho = (8/pi) h^-3 sum m f at the context's h. counts_out (host, 16 int64):
+ * [0] distance tests, [1] directed contributions found, [2..4] particle pairs n_A n_B of face /
+ * edge / corner cell pairs, [5..7] their sweep-1 window passes (naive: all pairs), [8..10] their
+ * sweep-1 pairs within h_i, [11] cells per axis (x), [12] pair-loop kernel time in ns, [13]
+ * presort time in ns. Errors: SPH_E_STATE (no sph_density yet), SPH_E_ARG. */
+int sph_pair_ablation(sph_ctx* ctx, int32_t sorted, float* rho_out, int64_t* counts_out);
+
 /* Number of CUDA kernel launches libsph issued on this context since creation
  * (evidence for the bench's gpu_launches). */
 int64_t sph_kernel_launches(const sph_ctx* ctx);

@@ -19,6 +19,7 @@
 #include "interact.cuh"
 #include "comm.cuh"
 #include "integrate.cuh"
+#include "ablation.cuh"
 
 // =========================================================== memory =============
 static void* dev_alloc(sph_ctx* c, size_t bytes) {
@@ -1519,6 +1520,99 @@ int sph_debug_export(sph_ctx* ctx, int32_t what, void* out, int64_t cap, int64_t
     CUDA_TRY(cudaMemcpyAsync(out, c->b[id].p, (size_t)cnt * esz, cudaMemcpyDeviceToHost, c->stream));
     sync(c);
   }
+  API_END
+  return SPH_OK;
+}
+
+// ------------------------------------------------------------------ f2 ablation ----------
+int sph_pair_ablation(sph_ctx* ctx, int32_t sorted, float* rho_out, int64_t* counts_out) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(c->state >= 2, SPH_E_STATE, "sph_pair_ablation before sph_density");
+  SPH_REQUIRE(counts_out && (sorted == 0 || sorted == 1), SPH_E_ARG, "bad argument");
+  const int64_t n = c->n;
+  // grid edge >= the largest h, with a relative slack for the fp32 binning (R19)
+  ctr_reset(c);
+  LAUNCH(k_hrange, grid1d(c, n, 256), 256, 0, Bget<float>(c, B_HRCH), n, ctr(c));
+  unsigned long long hc[C_NCOUNTERS];
+  ctr_read(c, hc);
+  const double hmax = (double)as_float(hc[C_HMAXBITS]) * (1.0 + 1e-5);
+  int nc[3];
+  for (int k = 0; k < 3; ++k) nc[k] = std::max(3, (int)floor(c->cfg.box[k] / hmax));
+  const int ncell = nc[0] * nc[1] * nc[2];
+  int* cell = B<int>(c, B_TMPI0, n);
+  int* ccount = B<int>(c, B_GFLAG, ncell);
+  int* cstart = B<int>(c, B_GSEL, ncell);
+  int* cfill = B<int>(c, B_RGL, std::max<int64_t>(ncell, 2 * (int64_t)std::max(c->n_groups, 1)));
+  int* order = B<int>(c, B_TMPI1, n);
+  CUDA_TRY(cudaMemsetAsync(ccount, 0, ncell * sizeof(int), c->stream));
+  const float4* xh = Bget<float4>(c, B_XH);
+  LAUNCH(k_ab_cells, grid1d(c, n, 256), 256, 0, xh, n, nc[0], nc[1], nc[2], (float)(nc[0] / c->cfg.box[0]),
+         (float)(nc[1] / c->cfg.box[1]), (float)(nc[2] / c->cfg.box[2]), cell, ccount);
+  scan_excl<int>(c, ccount, cstart, ncell);
+  CUDA_TRY(cudaMemsetAsync(cfill, 0, ncell * sizeof(int), c->stream));
+  LAUNCH(k_ab_scatter, grid1d(c, n, 256), 256, 0, cell, n, cstart, cfill, order);
+  AbParams P;
+  memset(&P, 0, sizeof(P));
+  P.nx = nc[0];
+  P.ny = nc[1];
+  P.nz = nc[2];
+  for (int k = 0; k < 3; ++k) P.L[k] = (float)c->cfg.box[k];
+  P.cstart = cstart;
+  P.ccount = ccount;
+  P.xh = xh;
+  P.vm = Bget<float4>(c, B_VM);
+  P.order = order;
+  P.mode = sorted;
+  float presort_ms = 0.f;
+  if (sorted) {
+    // the 13 presorted directions of every cell: one radix sort per direction of
+    // (cell, projection) keys
+    uint32_t* ls = B<uint32_t>(c, B_ABLIST, (size_t)13 * n * 2);   // [13][n] lists then [13][n] projections
+    float* lp = reinterpret_cast<float*>(ls + (size_t)13 * n);
+    int cbits = 0;
+    while ((1 << cbits) < ncell) ++cbits;
+    CUDA_TRY(cudaEventRecord(c->ev[10], c->stream));
+    for (int d = 0; d < 13; ++d) {
+      uint64_t* k0 = B<uint64_t>(c, B_KEYS0, n);
+      uint64_t* k1 = B<uint64_t>(c, B_KEYS1, n);
+      uint32_t* v0 = B<uint32_t>(c, B_VALS0, n);
+      uint32_t* v1 = B<uint32_t>(c, B_VALS1, n);
+      LAUNCH(k_ab_keys, grid1d(c, n, 256), 256, 0, xh, order, n, cell, nc[0], nc[1], (float)(c->cfg.box[0] / nc[0]),
+             (float)(c->cfg.box[1] / nc[1]), (float)(c->cfg.box[2] / nc[2]), d, k0, v0);
+      radix_sort(c, k0, v0, k1, v1, n, 32 + cbits);
+      LAUNCH(k_ab_unpack, grid1d(c, n, 256), 256, 0, k0, v0, n, ls + (size_t)d * n, lp + (size_t)d * n);
+    }
+    CUDA_TRY(cudaEventRecord(c->ev[11], c->stream));
+    sync(c);
+    cudaEventElapsedTime(&presort_ms, c->ev[10], c->ev[11]);
+    P.sorted = ls;
+    P.proj = lp;
+  }
+  float* rs = B<float>(c, B_OUT4, n);
+  CUDA_TRY(cudaMemsetAsync(rs, 0, n * sizeof(float), c->stream));
+  P.rho_sum = rs;
+  unsigned long long* ac = B<unsigned long long>(c, B_TMPL0, 16);
+  CUDA_TRY(cudaMemsetAsync(ac, 0, 16 * sizeof(unsigned long long), c->stream));
+  P.ctr = ac;
+  CUDA_TRY(cudaEventRecord(c->ev[10], c->stream));
+  LAUNCH(k_ab_pairs, gridfull((int64_t)ncell * 14 * 32, 256), 256, 0, P, ncell);
+  CUDA_TRY(cudaEventRecord(c->ev[11], c->stream));
+  std::vector<OutMap> maps;
+  if (rho_out) {
+    float* ro = dev_out(c, rho_out, c->n_own, B_OUT5, maps);
+    LAUNCH(k_ab_finish, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, c->n_own, xh, P.vm, rs, ro);
+  }
+  flush_out(c, maps, c->ev[5]);
+  unsigned long long h[16];
+  CUDA_TRY(cudaMemcpyAsync(h, ac, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, c->ev[10], c->ev[11]);
+  for (int k = 0; k < AB_N; ++k) counts_out[k] = (int64_t)h[k];
+  counts_out[11] = nc[0];
+  counts_out[12] = (int64_t)(ms * 1e6);
+  counts_out[13] = (int64_t)(presort_ms * 1e6);
+  counts_out[14] = counts_out[15] = 0;
   API_END
   return SPH_OK;
 }

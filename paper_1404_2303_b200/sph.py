@@ -76,7 +76,7 @@ EXPORTS = ("sph_config_default", "sph_create", "sph_destroy", "sph_set_allocator
            "sph_kernel_launches", "sph_build_cells_halo", "sph_halo_select", "sph_export_state",
            "sph_import_halo_state", "sph_x_histogram", "sph_guess_h", "sph_comm_unique_id", "sph_comm_init",
            "sph_halo_counts", "sph_halo_exchange", "sph_allreduce", "sph_kick", "sph_drift", "sph_timestep", "sph_set_active", "sph_update_cells", "sph_kick_each", "sph_neighbour_min",
-           "sph_debug_export")
+           "sph_debug_export", "sph_pair_ablation")
 
 
 def load(path: str | None = None):
@@ -120,6 +120,7 @@ def load(path: str | None = None):
     lib.sph_kick_each.argtypes = [P, i64, P, P, P, P, P]
     lib.sph_neighbour_min.argtypes = [P, P, P]
     lib.sph_debug_export.argtypes = [P, ctypes.c_int32, P, i64, P]
+    lib.sph_pair_ablation.argtypes = [P, ctypes.c_int32, P, P]
     lib.sph_drift.argtypes = [P, i64, P, P, ctypes.c_float]
     lib.sph_timestep.argtypes = [P, i64, P, P, ctypes.c_float, P, P]
     if path == LIB or path is None:
@@ -347,6 +348,15 @@ class Context:
         if cnt.value:
             self._check(self.lib.sph_debug_export(self.h, code, out.ctypes.data, cnt.value, ctypes.byref(cnt)))
         return out
+
+    def pair_ablation(self, sorted: bool, rho_out=None) -> dict:
+        """The paper's cell-pair density loops on a uniform grid (include/sph.h
+        sph_pair_ablation): naive double loop or the presorted sweeps."""
+        c = np.zeros(16, dtype=np.int64)
+        self._check(self.lib.sph_pair_ablation(self.h, int(bool(sorted)), _ptr(rho_out), c.ctypes.data))
+        keys = ("tests", "hits", "pairs_face", "pairs_edge", "pairs_corner", "pass_face", "pass_edge",
+                "pass_corner", "inrange_face", "inrange_edge", "inrange_corner", "cells_x", "ns_loop", "ns_presort")
+        return {k: int(v) for k, v in zip(keys, c)}
 
     def set_active(self, mask=None):
         """Targets of the next build / density / force: bool or uint8 array [n] (caller
