@@ -10,9 +10,9 @@ the whole step's device time.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl sph|reference] [--config C4]
 
-N > 1 runs under torch.distributed.run: one process per GPU, weak scaling over a slab
-decomposition of the C4 recipe in an (N,1,1) box with N x 2,097,152
-particles; two NCCL halo exchanges per step; the time is the max over ranks, value = all
+N > 1 runs under torch.distributed.run: one process per GPU, strong scaling of C5
+(134,217,728 clustered particles, BASELINE configs[4]) over a slab decomposition (SURVEY
+§8(e)); two NCCL halo exchanges per step; the time is the max over ranks, value = all
 ranks' pairs / that time.
 --impl reference times the fp64 oracle (oracle/) on a bounded sample of the same
 workload on this host's CPU cores (rank 0 only).
@@ -60,6 +60,7 @@ def parse():
     ap.add_argument("--no-warm", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--cpu-frac", type=float, default=0.02, help="cpu_baseline: fraction of the particles timed as targets")
+    ap.add_argument("--scale-config", default="C5", help="N > 1 workload: C5 (strong scaling) or C4xN (weak)")
     ap.add_argument("--transport", default="torch", choices=["torch", "libsph"],
                     help="N > 1 halo exchange: torch.distributed P2P or libsph's NCCL communicator")
     return ap.parse_args()
@@ -488,9 +489,12 @@ def run_sph(args, rank, world, local_rank):
 
 
 def run_slab(args, rank, world, local_rank):
-    """N > 1: weak scaling. The C4 recipe in a box (N,1,1) with N x 2,097,152 particles and
-    N x 64 clumps; ranks own count-quantile slabs along x (about one C4 each) and exchange
-    halos with their two neighbours over NCCL (paper_1404_2303_b200/slab.py)."""
+    """N > 1: strong scaling on BASELINE configs[4] (north_star: "measured at 1, 2, 4 and 8
+    GPUs on the 134M-particle case"): C5, 134,217,728 clustered particles (512 clumps), split
+    into N count-quantile slabs along x; each rank exchanges halos with its two neighbours over
+    NCCL before the density and before the force loop (paper_1404_2303_b200/slab.py; the send
+    rows packed by libsph's k_halo_pack). --scale-config C4xN selects the former weak-scaling
+    workload (the C4 recipe in an (N,1,1) box)."""
     import numpy as np
     import torch
     import torch.distributed as td
@@ -501,7 +505,8 @@ def run_slab(args, rank, world, local_rank):
 
     dev = torch.device("cuda", local_rank)
     stream = torch.cuda.current_stream(dev)
-    p = workloads.c4_weak(world)
+    p = workloads.c4_weak(world) if args.scale_config == "C4xN" else workloads.make(args.scale_config)
+    strong = args.scale_config != "C4xN"
     Lx = p.box[0]
     cfg0 = sph.default_config(p.box, **CONFIG_TUNING)
     ctx0 = sph.Context(cfg0, device=local_rank, stream=stream.cuda_stream)
@@ -580,10 +585,10 @@ def run_slab(args, rank, world, local_rank):
         line = {
             "metric": METRIC, "value": float(sm[2]) / (t_max * 1e-3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic",
-            "config": {"workload": f"C4x{world}: C4 recipe in a ({world},1,1) box, {p.n} particles, "
-                                   f"{64 * world} clumps; count-quantile slabs along x, cold h0",
+            "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": (f"{p.name}: {p.n} particles ({p.meta.get('n_clumps')} clumps), "
+                                    f"{world} count-quantile slabs along x, cold h0"),
                        "N": p.n, "parallelism": f"slab{world} (halo exchange over NCCL, 2 per step)",
                        "halo_width": width, "halo_over_owned_mean": float(sm[3]) / float(sm[4]),
                        "l2": "flushed (256 MiB write) before every timed step",

@@ -227,6 +227,12 @@ int sph_guess_h(sph_ctx* ctx, int64_t n, const float* x, float* h_out);
 int sph_halo_select(sph_ctx* ctx, int64_t n, const float* x, double lo, double hi, double width,
                     int32_t* idx_lo_out, int32_t* idx_hi_out, int64_t* counts_out);
 
+/* The rows sent in the first halo exchange, in one kernel: out [k][9] = {x, y, z, vx, vy, vz, m,
+ * u, h0} of the owned particles idx [k] (caller order, as returned by sph_halo_select; h0 may be
+ * NULL: 0). All device arrays. */
+int sph_halo_pack(sph_ctx* ctx, const float* x, const float* v, const float* m, const float* u, const float* h0,
+                  int64_t k, const int32_t* idx, float* out);
+
 /* After sph_density: per listed owned particle, the state its halo copies need for the force
  * loop ("densities and friends"): state_out [k][5] = {h, A = P/(Omega rho^2),
  * rho, c, Balsara f}. */

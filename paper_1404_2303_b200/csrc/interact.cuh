@@ -894,6 +894,26 @@ __global__ void k_halo_flags(const float* __restrict__ x, int64_t n, float lo, f
   }
 }
 
+// first-exchange rows {x, v, m, u, h0} of the listed owned particles (the
+// particles a proxy cell needs)
+__global__ void k_halo_pack(const float* __restrict__ x, const float* __restrict__ v, const float* __restrict__ m,
+                            const float* __restrict__ u, const float* __restrict__ h0, const int32_t* __restrict__ idx,
+                            int64_t k, float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = idx[i];
+    float* r = out + 9 * i;
+    r[0] = x[3 * o];
+    r[1] = x[3 * o + 1];
+    r[2] = x[3 * o + 2];
+    r[3] = v[3 * o];
+    r[4] = v[3 * o + 1];
+    r[5] = v[3 * o + 2];
+    r[6] = m[o];
+    r[7] = u[o];
+    r[8] = h0 ? h0[o] : 0.f;
+  }
+}
+
 __global__ void k_export_state(const int32_t* __restrict__ idx, int64_t k, const float* __restrict__ h_o,
                                const float4* __restrict__ g_o, float* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {

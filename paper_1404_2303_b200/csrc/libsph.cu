@@ -824,7 +824,7 @@ int sph_destroy(sph_ctx* c) {
   if (!c) return SPH_E_ARG;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
-  for (int i = 0; i < 80; ++i) dev_free(c, c->b[i].p);
+  for (int i = 0; i < B_COUNT; ++i) dev_free(c, c->b[i].p);
   if (c->ev_ok) {
     for (int i = 0; i < 12; ++i) cudaEventDestroy(c->ev[i]);
     for (int i = 0; i < 4; ++i) cudaEventDestroy(c->ev_side[i]);
@@ -844,7 +844,7 @@ int sph_set_allocator(sph_ctx* c, void* (*alloc)(size_t, void*, void*), void (*r
                       void* user) {
   if (!c) return SPH_E_ARG;
   if ((alloc == nullptr) != (release == nullptr)) return SPH_E_ARG;
-  for (int i = 0; i < 80; ++i)
+  for (int i = 0; i < B_COUNT; ++i)
     if (c->b[i].p) return SPH_E_STATE;
   c->ualloc = alloc;
   c->urelease = release;
@@ -1373,6 +1373,21 @@ int sph_halo_select(sph_ctx* ctx, int64_t n, const float* x, double lo, double h
   sync(c);
   counts_out[0] = nlo;
   counts_out[1] = nhi;
+  API_END
+  return SPH_OK;
+}
+
+int sph_halo_pack(sph_ctx* ctx, const float* x, const float* v, const float* m, const float* u, const float* h0,
+                  int64_t k, const int32_t* idx, float* out) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(k >= 0, SPH_E_ARG, "k < 0");
+  if (k == 0) return SPH_OK;
+  SPH_REQUIRE(x && v && m && u && idx && out, SPH_E_ARG, "required pointer is NULL");
+  const void* ptrs[7] = {x, v, m, u, idx, out, h0};
+  for (int i = 0; i < 7; ++i)
+    SPH_REQUIRE(!ptrs[i] || is_device_ptr(ptrs[i]), SPH_E_ARG, "sph_halo_pack: arrays must be device memory");
+  LAUNCH(k_halo_pack, grid1d(c, k, 256), 256, 0, x, v, m, u, h0, idx, k, out);
+  if (c->cfg.flags & SPH_F_SYNC) sync(c);
   API_END
   return SPH_OK;
 }

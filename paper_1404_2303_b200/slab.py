@@ -183,7 +183,10 @@ class SlabRank:
             # both faces border the same rank: send a particle near both faces only once
             keep = ~torch.isin(self.idx_hi, self.idx_lo)
             self.idx_hi = self.idx_hi[keep].contiguous()
-        pk = pack(self.x, self.v, self.m, self.u, self.h0)
+        if self.x.is_cuda:   # one libsph kernel per face (k_halo_pack)
+            return (self.ctx.halo_pack(self.x, self.v, self.m, self.u, self.h0, self.idx_lo),
+                    self.ctx.halo_pack(self.x, self.v, self.m, self.u, self.h0, self.idx_hi))
+        pk = pack(self.x, self.v, self.m, self.u, self.h0)   # CPU tensors (gloo tests of the host logic)
         return pk[self.idx_lo.long()].contiguous(), pk[self.idx_hi.long()].contiguous()
 
     def density(self, recv_lo, recv_hi):

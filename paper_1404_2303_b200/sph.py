@@ -76,7 +76,7 @@ EXPORTS = ("sph_config_default", "sph_create", "sph_destroy", "sph_set_allocator
            "sph_kernel_launches", "sph_build_cells_halo", "sph_halo_select", "sph_export_state",
            "sph_import_halo_state", "sph_x_histogram", "sph_guess_h", "sph_comm_unique_id", "sph_comm_init",
            "sph_halo_counts", "sph_halo_exchange", "sph_allreduce", "sph_kick", "sph_drift", "sph_timestep", "sph_set_active", "sph_update_cells", "sph_kick_each", "sph_neighbour_min",
-           "sph_debug_export", "sph_pair_ablation")
+           "sph_debug_export", "sph_pair_ablation", "sph_halo_pack")
 
 
 def load(path: str | None = None):
@@ -121,6 +121,7 @@ def load(path: str | None = None):
     lib.sph_neighbour_min.argtypes = [P, P, P]
     lib.sph_debug_export.argtypes = [P, ctypes.c_int32, P, i64, P]
     lib.sph_pair_ablation.argtypes = [P, ctypes.c_int32, P, P]
+    lib.sph_halo_pack.argtypes = [P, P, P, P, P, P, i64, P, P]
     lib.sph_drift.argtypes = [P, i64, P, P, ctypes.c_float]
     lib.sph_timestep.argtypes = [P, i64, P, P, ctypes.c_float, P, P]
     if path == LIB or path is None:
@@ -246,6 +247,16 @@ class Context:
         self._check(self.lib.sph_halo_select(self.h, n, _ptr(x), float(lo), float(hi), float(width),
                                              _ptr(ilo, np.int32), _ptr(ihi, np.int32), cnt.ctypes.data))
         return ilo[: int(cnt[0])], ihi[: int(cnt[1])]
+
+    def halo_pack(self, x, v, m, u, h0, idx):
+        """[k, 9] rows {x, v, m, u, h0} of the owned particles idx (device), one libsph kernel."""
+        import torch
+        k = int(idx.shape[0])
+        out = torch.empty(k, 9, dtype=torch.float32, device=idx.device)
+        if k:
+            self._check(self.lib.sph_halo_pack(self.h, _ptr(x), _ptr(v), _ptr(m), _ptr(u), _ptr(h0), k,
+                                               _ptr(idx, np.int32), _ptr(out)))
+        return out
 
     def export_state(self, idx):
         import torch
