@@ -1,6 +1,7 @@
 """Per-kernel summary of ncu --set full reports: duration, DRAM bytes, IPC, occupancy,
-FP32 pipe utilisation; optionally merges DRAM traffic per launch into profiles/traffic.json.
-  python tools/ncu_summary.py rep1.ncu-rep [rep2 ...] [--traffic profiles/traffic.json]"""
+FP32 pipe utilisation; optionally merges DRAM traffic per launch into profiles/traffic.json and
+executed warp instructions per launch into profiles/issue.json.
+  python tools/ncu_summary.py rep1.ncu-rep [rep2 ...] [--traffic profiles/traffic.json] [--issue profiles/issue.json]"""
 import csv, json, subprocess, sys
 
 WANT = {"gpu__time_duration.sum": "ns", "dram__bytes_read.sum": "B", "dram__bytes_write.sum": "B",
@@ -10,11 +11,15 @@ WANT = {"gpu__time_duration.sum": "ns", "dram__bytes_read.sum": "B", "dram__byte
         "smsp__thread_inst_executed_per_inst_executed.ratio": "thr/inst",
         "sm__sass_thread_inst_executed_op_ffma_pred_on.sum": "ffma",
         "sm__sass_thread_inst_executed_op_fadd_pred_on.sum": "fadd",
-        "sm__sass_thread_inst_executed_op_fmul_pred_on.sum": "fmul"}
+        "sm__sass_thread_inst_executed_op_fmul_pred_on.sum": "fmul",
+        "smsp__inst_executed.sum": "warp_inst"}
 args = [a for a in sys.argv[1:] if not a.startswith("--")]
 traffic_path = sys.argv[sys.argv.index("--traffic") + 1] if "--traffic" in sys.argv else None
 if traffic_path:
     args = [a for a in args if a != traffic_path]
+issue_path = sys.argv[sys.argv.index("--issue") + 1] if "--issue" in sys.argv else None
+if issue_path:
+    args = [a for a in args if a != issue_path]
 rows_out = []
 for rep in args:
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -44,6 +49,15 @@ for rep in args:
         rows_out.append(rec)
 for r in rows_out:
     print(json.dumps({k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()}))
+if issue_path:
+    try:
+        t = json.load(open(issue_path))
+    except (OSError, ValueError):
+        t = {}
+    for r in rows_out:
+        if r.get("warp_inst"):
+            t[r["kernel"]] = int(r["warp_inst"])
+    json.dump(t, open(issue_path, "w"), indent=1)
 if traffic_path:
     try:
         t = json.load(open(traffic_path))
