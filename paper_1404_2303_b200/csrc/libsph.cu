@@ -970,10 +970,26 @@ int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const floa
   // neighbour lists of the h iteration: r^2 < h_build^2 per particle
   hctr_reset(c);
   CUDA_TRY(cudaMemsetAsync(B<unsigned long long>(c, B_WALKRAW, 2), 0, 2 * sizeof(unsigned long long), c->stream));
+#ifdef SPH_WALK_STATS
+  {
+    unsigned long long z[8][5] = {};
+    CUDA_TRY(cudaMemcpyToSymbolAsync(g_walkstats, z, sizeof(z), 0, cudaMemcpyHostToDevice, c->stream));
+  }
+#endif
   nb_walk(c, -1);
   c->state = 1;
   CUDA_TRY(cudaEventRecord(c->ev[1], c->stream));
   sync(c);
+#ifdef SPH_WALK_STATS
+  {
+    unsigned long long z[8][5];
+    CUDA_TRY(cudaMemcpyFromSymbol(z, g_walkstats, sizeof(z)));
+    for (int p = 0; p < 8; ++p)
+      if (z[p][0])
+        fprintf(stderr, "[walkstats] pass %d: warp-passes %llu active lanes %llu survivors %llu recorded %llu chunks %llu\n",
+                p, z[p][0], z[p][1], z[p][2], z[p][3], z[p][4]);
+  }
+#endif
   DBG("build: n %lld top %dx%dx%d depth %d levels %zu nodes %d groups %d sorted %lld list %lld\n", (long long)n,
       c->ntop[0], c->ntop[1], c->ntop[2], c->depth, c->lev_off.size() - 1, c->n_nodes, c->n_groups,
       (long long)c->n_sorted, (long long)c->pool);

@@ -75,6 +75,13 @@
 #define MODE_COUNT 1
 #define MODE_FILL 2
 
+#ifdef SPH_WALK_STATS
+// instrumentation (build with -DSPH_WALK_STATS; printed by sph_build_cells): per NB-walk pass,
+// [0] warp passes, [1] active target lanes, [2] staged box survivors (warp level),
+// [3] recorded entries, [4] staged chunks
+__device__ unsigned long long g_walkstats[8][5];
+#endif
+
 // source position relative to the group origin o (oL = o - L), periodic image code c:
 // x - L is exact for a source near L, o - L for a group near L (Sterbenz; R19, H2)
 __device__ __forceinline__ float3 rel_pos(float4 p, uint32_t code, float3 o, float3 oL, const float* L) {
@@ -160,6 +167,9 @@ struct WalkState {
   int gz, lane;
   int raw;                  // sources streamed through the filters (diagnostics)
   int ntg;                  // targets (staged in WalkSmem::tgt)
+#ifdef SPH_WALK_STATS
+  long long st_surv, st_calls;
+#endif
   bool spheres;             // refine node tests by the individual targets' spheres
 };
 
@@ -181,6 +191,12 @@ __device__ __forceinline__ void emit_chunk(const WalkParams& P, WalkState& W, Wa
   const unsigned bal = __ballot_sync(FULL_MASK, keep);
   if (!bal) return;
   const int m = __popc(bal);
+#ifdef SPH_WALK_STATS
+  if (MODE == MODE_NB) {
+    W.st_surv += m;
+    W.st_calls += 1;
+  }
+#endif
   const int pos = __popc(bal & lanemask_lt());
 #if UNION_PACKED
   if (MODE != MODE_NB) {
@@ -567,6 +583,10 @@ __global__ void WALK_BOUNDS k_walk(WalkParams P) {
   }
   W.cur = 0;
   W.raw = 0;
+#ifdef SPH_WALK_STATS
+  W.st_surv = 0;
+  W.st_calls = 0;
+#endif
 #if NB_ROWS
   W.base = MODE == MODE_FILL ? P.off[gid] : (MODE == MODE_NB ? (int64_t)s * P.K : 0);
 #else
@@ -706,6 +726,20 @@ __global__ void WALK_BOUNDS k_walk(WalkParams P) {
     if (lane == 0)
       printf("heavy walk mode %d group %d: targets %d R %.3g bbox %.3g %.3g %.3g spheres %d raw %d max list %d\n", MODE,
              gid, W.ntg, W.R, W.hi.x - W.lo.x, W.hi.y - W.lo.y, W.hi.z - W.lo.z, (int)W.spheres, W.raw, mc);
+  }
+#endif
+#ifdef SPH_WALK_STATS
+  if (MODE == MODE_NB && P.solve) {
+    const int act = __popc(__ballot_sync(FULL_MASK, tg));
+    const int rec = warp_sum_i(tg ? min(W.cur, P.K) : 0);
+    if (lane == 0) {
+      const int pp = min(pass, 7);
+      atomicAdd(&g_walkstats[pp][0], 1ull);
+      atomicAdd(&g_walkstats[pp][1], (unsigned long long)act);
+      atomicAdd(&g_walkstats[pp][2], (unsigned long long)W.st_surv);
+      atomicAdd(&g_walkstats[pp][3], (unsigned long long)rec);
+      atomicAdd(&g_walkstats[pp][4], (unsigned long long)W.st_calls);
+    }
   }
 #endif
   if (MODE == MODE_NB && !P.ovf) nb_tot += tg ? min(W.cur, P.K) : 0;
