@@ -307,6 +307,25 @@ int sph_kick_each(sph_ctx* ctx, int64_t n, float* v, float* u, const float* a, c
  * device, positive values (out is read and updated). Deterministic (min). */
 int sph_neighbour_min(sph_ctx* ctx, const float* val, float* out);
 
+/* Individual power-of-two time steps, the bin arithmetic of a multiple
+ * time-stepping integrator, in integer ticks of dt_min. For every particle with active[i] != 0
+ * (all if active is NULL): ticks_out[i] = the largest power of two s <= min(dt_i / dt_min,
+ * 2^n_bins) (dt_i of Eq. 6 from h and vsig, c_cfl) that divides ti (a new step starts on its
+ * own grid), and with cap2 != 0 at most 2 ticks_in[i] (a step grows at most 2x at a time);
+ * inactive particles keep ticks_in[i] (ticks_in is required when active is given). All arrays
+ * device memory; ticks int64. */
+int sph_timebins(sph_ctx* ctx, int64_t n, const float* h, const float* vsig, float c_cfl, double dt_min,
+                 int32_t n_bins, int64_t ti, const uint8_t* active, const int64_t* ticks_in, int32_t cap2,
+                 int64_t* ticks_out);
+
+/* Time-step limiter wake-up: an inactive particle whose step exceeds 4 lim[i] ticks (lim: the
+ * smallest new step of a force neighbour, from sph_neighbour_min) ends its step at the next
+ * point of the grid of the largest power of two <= 4 lim[i] after ti_end, never later than its
+ * current end ti_begin[i] + ticks[i]. ticks[i] is shortened in place; kick[i] = (new - old)
+ * ticks x dt_min / 2 (the correction of its opening half kick), else 0. Device arrays. */
+int sph_timebins_wake(sph_ctx* ctx, int64_t n, const uint8_t* active, const float* lim, int64_t ti_end,
+                      const int64_t* ti_begin, int64_t* ticks, double dt_min, float* kick);
+
 /* x[n][3] += v[n][3] dt, wrapped back into [0, L) per axis (requires |v dt| < L). */
 int sph_drift(sph_ctx* ctx, int64_t n, float* x, const float* v, float dt);
 

@@ -58,3 +58,46 @@ __global__ void k_timestep(int64_t n, const float* __restrict__ h, const float* 
   mn = __reduce_min_sync(FULL_MASK, mn);
   if ((threadIdx.x & 31) == 0) atomicMin(dt_min_bits, mn);
 }
+
+// Individual time steps: power-of-two step in dt_min ticks <= the Eq. 6 step,
+// dividing ti, at most 2x the previous one (include/sph.h sph_timebins)
+__global__ void k_timebins(int64_t n, const float* __restrict__ h, const float* __restrict__ vsig, float c_cfl,
+                           double dt_min, int n_bins, long long ti, const uint8_t* __restrict__ active,
+                           const long long* __restrict__ tin, int cap2, long long* __restrict__ tout) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (active && !active[i]) {
+      tout[i] = tin ? tin[i] : 1;
+      continue;
+    }
+    const double dt = vsig[i] > 0.f ? (double)(c_cfl * 2.f * h[i] / vsig[i]) : INFINITY;
+    const double q = fmax(dt / dt_min, 1.0);
+    int k = q >= (double)(1ll << n_bins) ? n_bins : (int)floor(log2(q));
+    k = min(max(k, 0), n_bins);
+    long long s = 1ll << k;
+    while (s > 1 && ti % s != 0) s >>= 1;                         // on its own grid
+    if (tin && cap2) s = min(s, 2 * tin[i]);                       // grows at most 2x
+    tout[i] = s;
+  }
+}
+
+// limiter wake-up (include/sph.h sph_timebins_wake)
+__global__ void k_timebins_wake(int64_t n, const uint8_t* __restrict__ active, const float* __restrict__ lim,
+                                long long ti_end, const long long* __restrict__ begin, long long* __restrict__ ticks,
+                                double dt_min, float* __restrict__ kick) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float corr = 0.f;
+    const long long st = ticks[i];
+    if (!(active && active[i]) && (float)st > 4.f * lim[i]) {       // lim is finite here
+      const double l4 = fmax((double)(4.f * lim[i]), 1.0);
+      const long long s2 = 1ll << (int)floor(log2(l4));
+      const long long old_end = begin[i] + st;
+      const long long new_end = min((ti_end / s2 + 1) * s2, old_end);
+      if (new_end < old_end) {
+        const long long nl = new_end - begin[i];
+        corr = (float)((double)(nl - st) * 0.5 * dt_min);
+        ticks[i] = nl;
+      }
+    }
+    kick[i] = corr;
+  }
+}

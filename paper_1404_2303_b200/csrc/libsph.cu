@@ -1707,6 +1707,40 @@ int sph_kick_each(sph_ctx* ctx, int64_t n, float* v, float* u, const float* a, c
   return SPH_OK;
 }
 
+int sph_timebins(sph_ctx* ctx, int64_t n, const float* h, const float* vsig, float c_cfl, double dt_min,
+                 int32_t n_bins, int64_t ti, const uint8_t* active, const int64_t* ticks_in, int32_t cap2,
+                 int64_t* ticks_out) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(n >= 0 && (n == 0 || (h && vsig && ticks_out)) && c_cfl > 0.f && dt_min > 0.0 && n_bins >= 0 &&
+                  n_bins < 62 && ti >= 0 && (!active || ticks_in),
+              SPH_E_ARG, "bad argument");
+  const void* ptrs[5] = {h, vsig, ticks_out, active, ticks_in};
+  for (int i = 0; i < 5; ++i)
+    SPH_REQUIRE(!ptrs[i] || n == 0 || is_device_ptr(ptrs[i]), SPH_E_ARG, "sph_timebins: arrays must be device memory");
+  if (n > 0)
+    LAUNCH(k_timebins, grid1d(c, n, 256), 256, 0, n, h, vsig, c_cfl, dt_min, n_bins, (long long)ti, active,
+           reinterpret_cast<const long long*>(ticks_in), cap2, reinterpret_cast<long long*>(ticks_out));
+  if (c->cfg.flags & SPH_F_SYNC) sync(c);
+  API_END
+  return SPH_OK;
+}
+
+int sph_timebins_wake(sph_ctx* ctx, int64_t n, const uint8_t* active, const float* lim, int64_t ti_end,
+                      const int64_t* ti_begin, int64_t* ticks, double dt_min, float* kick) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(n >= 0 && (n == 0 || (lim && ti_begin && ticks && kick)) && dt_min > 0.0, SPH_E_ARG, "bad argument");
+  const void* ptrs[5] = {active, lim, ti_begin, ticks, kick};
+  for (int i = 0; i < 5; ++i)
+    SPH_REQUIRE(!ptrs[i] || n == 0 || is_device_ptr(ptrs[i]), SPH_E_ARG,
+                "sph_timebins_wake: arrays must be device memory");
+  if (n > 0)
+    LAUNCH(k_timebins_wake, grid1d(c, n, 256), 256, 0, n, active, lim, (long long)ti_end,
+           reinterpret_cast<const long long*>(ti_begin), reinterpret_cast<long long*>(ticks), dt_min, kick);
+  if (c->cfg.flags & SPH_F_SYNC) sync(c);
+  API_END
+  return SPH_OK;
+}
+
 int sph_drift(sph_ctx* ctx, int64_t n, float* x, const float* v, float dt) {
   API_BEGIN(ctx)
   SPH_REQUIRE(n >= 0 && (n == 0 || (x && v)), SPH_E_ARG, "bad argument");

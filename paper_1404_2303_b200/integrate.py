@@ -88,22 +88,17 @@ class MultiStep:
         ctx.build_cells(self.x, None)
         ctx.density(self.v, self.m, self.u, out=dict(h=self.h, rho=self.rho))
         ctx.force(self.v, out=dict(a=self.a, dudt=self.dudt, vsig=self.vsig))
-        self.step_ticks = self._ticks(torch.ones(n, dtype=torch.bool, device=dev), 0)
+        self.step_ticks = self._ticks(None, 0)
         self._kick(self.step_ticks.float() * 0.5 * self.dt_min)
         self.evaluations = n
 
-    def _ticks(self, sel, ti):
-        """Power-of-two step (in dt_min ticks) <= the Eq. 6 step, dividing ti."""
-        import torch
-        _, dt = self.ctx.timestep(self.h, self.vsig, self.c_cfl, per_particle=True)
-        k = torch.floor(torch.log2(torch.clamp(dt / self.dt_min, min=1.0))).clamp(max=self.n_bins).long()
-        s = torch.pow(2, k)
-        while True:                             # a new step has to start on its own grid
-            bad = (ti % s) != 0
-            if not bool(bad.any()):
-                break
-            s = torch.where(bad, s // 2, s)
-        return torch.where(sel, s, getattr(self, "step_ticks", s))
+    def _ticks(self, sel, ti, cap2=False):
+        """Power-of-two step (in dt_min ticks) <= the Eq. 6 step, dividing ti, for the particles
+        in `sel` (the others keep theirs); at most 2x the previous one with cap2 (libsph
+        sph_timebins)."""
+        old = getattr(self, "step_ticks", None)
+        return self.ctx.timebins(self.h, self.vsig, self.c_cfl, self.dt_min, self.n_bins, ti,
+                                 active=sel if old is not None else None, ticks_in=old, cap2=cap2)
 
     def _kick(self, dt):
         self.ctx.kick_each(self.v, self.a, dt.float().contiguous(), self.u, self.dudt)
@@ -127,29 +122,16 @@ class MultiStep:
         self.evaluations += int(active.sum())
         zero = torch.zeros_like(self.h)
         self._kick(torch.where(active, self.step_ticks.float() * 0.5 * self.dt_min, zero))   # close the step
-        old_ticks = self.step_ticks
-        self.step_ticks = self._ticks(active, ti_end)
+        # a step grows at most 2x at a time (the limiter) ...
+        self.step_ticks = self._ticks(active, ti_end, cap2=self.limiter)
         if self.limiter:
-            # a step grows at most 2x at a time ...
-            self.step_ticks = torch.where(active, torch.minimum(self.step_ticks, 2 * old_ticks), self.step_ticks)
             # ... and no particle keeps a step above 4x a force neighbour's new one: such a
-            # particle is woken, its current step ending at the next point of the shorter
-            # grid (its opening half kick corrected to the shortened step)
+            # particle is woken, its current step ending at the next point of the shorter grid
+            # (never later than its current end), its opening half kick corrected (libsph
+            # sph_neighbour_min + sph_timebins_wake)
             lim = torch.full_like(self.h, float("inf"))
             ctx.neighbour_min(torch.where(active, self.step_ticks.float(), torch.full_like(self.h, float("inf"))), lim)
-            wake = (~active) & (self.step_ticks.float() > 4 * lim)
-            if bool(wake.any()):
-                # the shorter grid's step, only where woken (lim is finite there)
-                lim4 = torch.where(wake, 4 * lim, torch.ones_like(lim))
-                s2 = torch.pow(2, torch.floor(torch.log2(torch.clamp(lim4, min=1.0))).long())
-                old_end = self.ti_begin + self.step_ticks
-                # the next point of that grid, never later than the current end of the step
-                new_end = torch.minimum((ti_end // s2 + 1) * s2, old_end)
-                wake = wake & (new_end < old_end)
-                new_len = torch.where(wake, new_end - self.ti_begin, self.step_ticks)
-                corr = torch.where(wake, (new_len - self.step_ticks).float() * 0.5 * self.dt_min, zero)
-                self._kick(corr)
-                self.step_ticks = new_len
+            self._kick(ctx.timebins_wake(active, lim, ti_end, self.ti_begin, self.step_ticks, self.dt_min))
         self._kick(torch.where(active, self.step_ticks.float() * 0.5 * self.dt_min, zero))   # open the next
         self.ti_begin = torch.where(active, torch.full_like(self.ti_begin, ti_end), self.ti_begin)
         self.ti = ti_end

@@ -76,7 +76,7 @@ EXPORTS = ("sph_config_default", "sph_create", "sph_destroy", "sph_set_allocator
            "sph_kernel_launches", "sph_build_cells_halo", "sph_halo_select", "sph_export_state",
            "sph_import_halo_state", "sph_x_histogram", "sph_guess_h", "sph_comm_unique_id", "sph_comm_init",
            "sph_halo_counts", "sph_halo_exchange", "sph_allreduce", "sph_kick", "sph_drift", "sph_timestep", "sph_set_active", "sph_update_cells", "sph_kick_each", "sph_neighbour_min",
-           "sph_debug_export", "sph_pair_ablation", "sph_halo_pack")
+           "sph_debug_export", "sph_pair_ablation", "sph_halo_pack", "sph_timebins", "sph_timebins_wake")
 
 
 def load(path: str | None = None):
@@ -122,6 +122,9 @@ def load(path: str | None = None):
     lib.sph_debug_export.argtypes = [P, ctypes.c_int32, P, i64, P]
     lib.sph_pair_ablation.argtypes = [P, ctypes.c_int32, P, P]
     lib.sph_halo_pack.argtypes = [P, P, P, P, P, P, i64, P, P]
+    lib.sph_timebins.argtypes = [P, i64, P, P, ctypes.c_float, ctypes.c_double, ctypes.c_int32, i64, P, P,
+                                 ctypes.c_int32, P]
+    lib.sph_timebins_wake.argtypes = [P, i64, P, P, i64, P, P, ctypes.c_double, P]
     lib.sph_drift.argtypes = [P, i64, P, P, ctypes.c_float]
     lib.sph_timestep.argtypes = [P, i64, P, P, ctypes.c_float, P, P]
     if path == LIB or path is None:
@@ -394,6 +397,26 @@ class Context:
         neighbours j (device float32 arrays, caller order)."""
         self._check(self.lib.sph_neighbour_min(self.h, _ptr(val), _ptr(out)))
         return out
+
+    def timebins(self, h, vsig, c_cfl, dt_min, n_bins, ti, active=None, ticks_in=None, cap2=False, out=None):
+        """Power-of-two steps in dt_min ticks (include/sph.h sph_timebins); int64 device arrays."""
+        import torch
+        out = out if out is not None else torch.empty(int(h.shape[0]), dtype=torch.int64, device=h.device)
+        a = active.to(torch.uint8).contiguous() if active is not None else None
+        self._check(self.lib.sph_timebins(self.h, int(h.shape[0]), _ptr(h), _ptr(vsig), float(c_cfl), float(dt_min),
+                                          int(n_bins), int(ti), a.data_ptr() if a is not None else None,
+                                          _ptr(ticks_in, np.int64), int(bool(cap2)), _ptr(out, np.int64)))
+        return out
+
+    def timebins_wake(self, active, lim, ti_end, ti_begin, ticks, dt_min):
+        """Limiter wake-up in place on `ticks`; returns the opening-kick corrections (include/sph.h)."""
+        import torch
+        kick = torch.empty(int(ticks.shape[0]), dtype=torch.float32, device=ticks.device)
+        a = active.to(torch.uint8).contiguous() if active is not None else None
+        self._check(self.lib.sph_timebins_wake(self.h, int(ticks.shape[0]), a.data_ptr() if a is not None else None,
+                                               _ptr(lim), int(ti_end), _ptr(ti_begin, np.int64), _ptr(ticks, np.int64),
+                                               float(dt_min), _ptr(kick)))
+        return kick
 
     def drift(self, x, v, dt):
         self._check(self.lib.sph_drift(self.h, int(x.shape[0]), _ptr(x), _ptr(v), float(dt)))

@@ -9,7 +9,7 @@ import workloads
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("P", [2, 3])
+@pytest.mark.parametrize("P", [2, 3, 4])
 def test_slabs_match_single_context(P):
     import torch
 
@@ -47,3 +47,24 @@ def test_slabs_match_single_context(P):
         assert np.abs(a - ref["a"][own]).max() <= 1e-4 * scale
     for rk in ranks:
         rk.ctx.close()
+
+
+def test_halo_pack_kernel_equals_the_row_layout():
+    """sph_halo_pack (k_halo_pack) writes exactly the rows slab.pack builds: {x, v, m, u, h0} of
+    the selected owned particles."""
+    import torch
+
+    import paper_1404_2303_b200 as sph
+    from paper_1404_2303_b200 import slab
+
+    p = workloads.tiny(1, n=3000)
+    dev = torch.device("cuda:0")
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    ctx = sph.Context(sph.default_config(p.box))
+    x, v, m, u, h0 = t(p.x), t(p.v), t(p.m), t(p.u), t(p.h0)
+    lo_idx, hi_idx = ctx.halo_select(x, 0.25, 0.75, 0.1)
+    assert lo_idx.numel() > 0 and hi_idx.numel() > 0
+    ref = slab.pack(x, v, m, u, h0)
+    for idx in (lo_idx, hi_idx):
+        assert torch.equal(ctx.halo_pack(x, v, m, u, h0, idx), ref[idx.long()])
+    ctx.close()
