@@ -38,8 +38,11 @@ UNIT = "pair-interactions/s"
 # contribution (first full pass); force 74 per unordered pair.
 FLOP_DENS_PAIR, FLOP_DENS_DIR, FLOP_FORCE_PAIR = 27, 25, 74
 # neighbour finding: one distance test = 3 sub + 1 mul + 2 FMA = 8 FLOP per recorded entry;
-# h iteration: one evaluation of f, f', f'' and the three sums per entry ~ 20 FLOP
-FLOP_TEST, FLOP_HSOLVE = 8, 20
+# h iteration (Eq. 3 and its h-derivatives), per list entry per evaluation of N(h): q = r/h 1,
+# f, f', f'' of the spline 7 (outer branch; the inner one is 10, credit the smaller), the
+# sums S0 += f 1, S1 += q f' 2 (FMA), S2 += q^2 f'' 3 -> 14 FLOP, times the device-counted
+# entry evaluations (sph_stats.n_h_evals)
+FLOP_TEST, FLOP_HEVAL = 8, 14
 # FP32 ALU peak derived from the unit counts and clock (B200_PROFILING.md: 148 SMs,
 # clocks.max.sm 1965 MHz; 128 FP32 lanes/SM, FMA = 2 FLOP). Measured: 72.6 TFLOP/s
 # (tools/fp32_peak.cu, profiles/round1/fp32_peak.json).
@@ -416,21 +419,24 @@ def run_sph(args, rank, world, local_rank):
     # per-phase kernel time, CUDA events on the ctx stream around every launch of the phase
     # (summed over the phase's launches within one step)
     nb_entries = med("n_nb_entries", sd)
+    h_evals = med("n_h_evals", sd)
+    # the h iteration runs fused in the NB walk's epilogue; stand-alone solves (pool lists,
+    # repeated calls) add k_hsolve time, so the phase is credited over both kernels' time
+    ms_nb = med("ms_kernel_walk_nb", sd) + med("ms_kernel_hsolve", sd)
     kern = {
-        "k_walk (neighbour lists + h solve)": roof("k_walk<MODE_NB>", FLOP_TEST * nb_entries,
-                                                   med("ms_kernel_walk_nb", sd),
+        "k_walk (neighbour lists + h solve)": roof("k_walk<MODE_NB>", FLOP_TEST * nb_entries + FLOP_HEVAL * h_evals,
+                                                   ms_nb,
                                                    f"{FLOP_TEST} FLOP per recorded neighbour entry (r^2 < h_build^2), "
-                                                   f"{int(nb_entries)} entries; the h iteration runs fused in the "
-                                                   f"walk's epilogue (not credited)"),
+                                                   f"{int(nb_entries)} entries, + {FLOP_HEVAL} FLOP per entry "
+                                                   f"evaluation of the h iteration (fused in the walk's epilogue), "
+                                                   f"{int(h_evals)} evaluations "
+                                                   f"({h_evals / max(nb_entries, 1):.2f} per entry)"),
         "k_force": roof("k_force", flop_force, k_force_ms, f"{FLOP_FORCE_PAIR} FLOP x F"),
         "k_density": roof("k_density", flop_dens, k_dens_ms, f"{FLOP_DENS_PAIR} FLOP x F + {FLOP_DENS_DIR} x D"),
         "k_walk (interaction lists)": roof("k_walk<MODE_FILL>", FLOP_TEST * sfo[-1]["n_pair_slots"],
                                            med("ms_kernel_walk_union", sd),
                                            f"{FLOP_TEST} FLOP per interaction-list entry"),
     }
-    if med("ms_kernel_hsolve", sd) > 0:   # stand-alone solves (pool lists, repeated calls)
-        kern["k_hsolve"] = roof("k_hsolve", FLOP_HSOLVE * nb_entries, med("ms_kernel_hsolve", sd),
-                                f"{FLOP_HSOLVE} FLOP per neighbour entry (one Newton/Halley evaluation)")
     order = sorted(kern.values(), key=lambda r: -r["ms_per_step"])
     dominant, secondary = order[0], order[1:]
     cpu = None

@@ -149,6 +149,9 @@ typedef struct {         /* host struct, filled when non-NULL */
   double ms_kernel_sort;         /* CUDA events around those launches */
   int32_t sort_key_bits;         /* top-cell index bits + 3 x Morton levels */
   int32_t sort_passes;           /* 8-bit radix passes */
+  /* sph_density: neighbour-list entries summed by the h iteration, over every evaluation of
+     N(h) and its derivatives (Eq. 3; the build's fused solve and all re-walk rounds) */
+  int64_t n_h_evals;
 } sph_stats;
 
 /* Fill *cfg with the paper's defaults for the given box. */

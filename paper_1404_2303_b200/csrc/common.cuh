@@ -170,7 +170,7 @@ struct sph_ctx {
   int sort_bits = 0, sort_passes = 0;
   const float* xin = nullptr;   // this call's positions (caller's device array or a staged copy)
   const float* hin = nullptr;   // this call's h0 (or null)
-  int64_t nb_entries = 0, walk_launches = 0;
+  int64_t nb_entries = 0, walk_launches = 0, h_evals = 0;
 
   // named device buffers
   DBuf b[96];

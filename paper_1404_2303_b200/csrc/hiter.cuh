@@ -19,6 +19,8 @@
 #define HC_REGROW 1
 #define HC_OVF 2
 #define HC_ITMAX 3
+#define HC_EVALS 4   // entries summed by the h iteration (all evaluations, all rounds)
+#define HC_N 5
 
 // ------------------------------------------------------------------ kernel ------
 // f(q) of the cubic spline (W = (8/pi) h^-3 f), its first and second derivative
@@ -175,6 +177,7 @@ struct HLane {
   float h, hbs, l, u;
   uint8_t st;
   int it;
+  long long ev;   // entries summed over all evaluations of N(h) (work of the iteration, Eq. 3)
 };
 
 __device__ __forceinline__ void warp_hsolve(bool act, const float* r2l, int64_t stride, int cnt, int K, bool pooled,
@@ -207,6 +210,7 @@ __device__ __forceinline__ void warp_hsolve(bool act, const float* r2l, int64_t 
         nsums_row(r2l, cnt, 1.0f / H.h, S0, S1, S2);
       else
         nsums(r2l, stride, 0, cnt, 1, 1.0f / H.h, S0, S1, S2);
+      H.ev += cnt;
       H.st = hstep(S0, S1, S2, H.h, H.hbs, H.l, H.u, n_t, tol, margin, hcap);
       if (H.st == HS_REGROW) ++H.it;
     }
@@ -222,10 +226,12 @@ __device__ __forceinline__ void warp_hsolve(bool act, const float* r2l, int64_t 
     float tlo = __shfl_sync(FULL_MASK, H.l, t), tu = __shfl_sync(FULL_MASK, H.u, t);
     uint8_t tst = HS_ACTIVE;
     int tit = 0;
+    long long tev = 0;
     for (; tit < max_iter && tst == HS_ACTIVE; ++tit) {
       double S0 = 0.0;
       float S1 = 0.f, S2 = 0.f;
       nsums(tl, tstr, lane, tc, 32, 1.0f / th, S0, S1, S2);
+      tev += tc;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         S0 += __shfl_xor_sync(FULL_MASK, S0, o);
@@ -242,6 +248,7 @@ __device__ __forceinline__ void warp_hsolve(bool act, const float* r2l, int64_t 
       H.u = tu;
       H.st = tst;
       H.it = tit;
+      H.ev += tev;
     }
   }
 }
@@ -252,7 +259,11 @@ __device__ __forceinline__ void hsolve_count(bool act, const HLane& H, unsigned 
   const unsigned unconv = __ballot_sync(FULL_MASK, act && H.st == HS_ACTIVE);
   const unsigned ovf = __ballot_sync(FULL_MASK, act && H.st == HS_OVF);
   const unsigned itmax = __reduce_max_sync(FULL_MASK, act ? (unsigned)H.it : 0u);
+  unsigned long long ev = act ? (unsigned long long)H.ev : 0ull;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ev += __shfl_xor_sync(FULL_MASK, ev, o);
   if ((threadIdx.x & 31) == 0) {
+    if (ev) atomicAdd(&hc[HC_EVALS], ev);
     if (regrow) atomicAdd(&hc[HC_REGROW], (unsigned long long)__popc(regrow));
     if (unconv) atomicAdd(&hc[HC_UNCONV], (unsigned long long)__popc(unconv));
     if (ovf) atomicAdd(&hc[HC_OVF], (unsigned long long)__popc(ovf));

@@ -759,6 +759,7 @@ __global__ void __launch_bounds__(HSOLVE_WARPS * 32) k_hsolve(const int4* __rest
   if (!__any_sync(FULL_MASK, act)) return;
   HLane H;
   H.h = H.hbs = H.l = H.u = 0.f;
+  H.ev = 0;
   H.st = HS_DONE;
   int cnt = 0;
   if (act) {
@@ -803,10 +804,12 @@ __global__ void __launch_bounds__(HSOLVE_WARPS * 32) k_hsolve_pool(const int* __
   float h = xh[s].w, hbs = hb[s], l = lo_a[s], u = hi_a[s];
   uint8_t st = HS_ACTIVE;
   int it = 0;
+  unsigned long long ev = 0;
   for (; it < max_iter && st == HS_ACTIVE; ++it) {
     double S0 = 0.0;
     float S1 = 0.f, S2 = 0.f;
     nsums(r2l, 1, lane, cnt, 32, 1.0f / h, S0, S1, S2);
+    ev += cnt;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       S0 += __shfl_xor_sync(FULL_MASK, S0, o);
@@ -825,6 +828,7 @@ __global__ void __launch_bounds__(HSOLVE_WARPS * 32) k_hsolve_pool(const int* __
     if (st == HS_REGROW) atomicAdd(&hc[HC_REGROW], 1ull);
     if (st == HS_ACTIVE) atomicAdd(&hc[HC_UNCONV], 1ull);
     atomicMax(&hc[HC_ITMAX], (unsigned long long)it);
+    atomicAdd(&hc[HC_EVALS], ev);
   }
 }
 

@@ -494,7 +494,7 @@ static void nb_walk(sph_ctx* c, int tsel_val, int64_t n_regrow = 0) {
   P.shrunk = Bget<uint8_t>(c, B_SHRUNK);
   P.ovf_cnt = B<int64_t>(c, B_OVFC, n);
   P.ovf_off_w = Bget<int64_t>(c, B_NBOFF);
-  P.hc = B<unsigned long long>(c, B_HCTR, 4);
+  P.hc = B<unsigned long long>(c, B_HCTR, HC_N);
   P.n_t = c->cfg.n_ngb;
   P.tol = c->cfg.n_ngb_tol;
   P.margin = solve_margin(c);
@@ -507,8 +507,13 @@ static void nb_walk(sph_ctx* c, int tsel_val, int64_t n_regrow = 0) {
   c->walk_launches++;
 }
 
+// per-round counters (HC_EVALS accumulates over the rounds of a call: zeroed by hctr_zero)
 static void hctr_reset(sph_ctx* c) {
-  CUDA_TRY(cudaMemsetAsync(B<unsigned long long>(c, B_HCTR, 4), 0, 4 * sizeof(unsigned long long), c->stream));
+  CUDA_TRY(cudaMemsetAsync(B<unsigned long long>(c, B_HCTR, HC_N), 0, HC_EVALS * sizeof(unsigned long long),
+                           c->stream));
+}
+static void hctr_zero(sph_ctx* c) {
+  CUDA_TRY(cudaMemsetAsync(B<unsigned long long>(c, B_HCTR, HC_N), 0, HC_N * sizeof(unsigned long long), c->stream));
 }
 
 // Particles in state HS_OVF (a repeat overflow): exactly sized lists in the overflow pool
@@ -968,7 +973,7 @@ int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const floa
            margin, h_cap(c), Bget<uint8_t>(c, B_STATE), hb, Bget<float>(c, B_HLO), Bget<float>(c, B_HHI));
   }
   // neighbour lists of the h iteration: r^2 < h_build^2 per particle
-  hctr_reset(c);
+  hctr_zero(c);
   CUDA_TRY(cudaMemsetAsync(B<unsigned long long>(c, B_WALKRAW, 2), 0, 2 * sizeof(unsigned long long), c->stream));
 #ifdef SPH_WALK_STATS
   {
@@ -1056,7 +1061,7 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   CUDA_TRY(cudaEventRecord(c->ev[6], c->stream));
   if (c->state >= 2) {
     // a repeated call: the lists are recorded; solve on them from the current h
-    hctr_reset(c);
+    hctr_zero(c);
     PhaseTimer _p(c, 1);
     LAUNCH(k_hsolve, gridfull((int64_t)c->n_groups * 32, HSOLVE_WARPS * 32), HSOLVE_WARPS * 32, 0,
            Bget<int4>(c, B_GROUPS), c->n_groups, Bget<float4>(c, B_XH), Bget<float>(c, B_HB), Bget<float>(c, B_HLO),
@@ -1076,12 +1081,13 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   // counters (one host round trip), records the lists of the particles whose root lies
   // beyond their list (a fused re-walk + solve) and the pool lists of repeat overflows.
   while (true) {
-    unsigned long long hh[4];
+    unsigned long long hh[HC_N];
     CUDA_TRY(cudaMemcpyAsync(hh, Bget<unsigned long long>(c, B_HCTR), sizeof(hh), cudaMemcpyDeviceToHost, c->stream));
     sync(c);
     ++rounds;
     unconv += (long long)hh[HC_UNCONV];   // disjoint per round: an unconverged particle is never re-walked
     itmax = std::max(itmax, (long long)hh[HC_ITMAX]);
+    c->h_evals = (int64_t)hh[HC_EVALS];   // cumulative over the build's walk and every round
     DBG("h solve round %d: unconverged %llu, re-walk %llu, pool %llu, max iterations %llu\n", rounds,
         hh[HC_UNCONV], hh[HC_REGROW], hh[HC_OVF], hh[HC_ITMAX]);
     if (hh[HC_REGROW] == 0 && hh[HC_OVF] == 0) break;
@@ -1214,6 +1220,7 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
     st->ms_kernel_hsolve = c->ms_phase[1];
     st->ms_kernel_walk_union = c->ms_phase[2];
     st->n_nb_entries = c->nb_entries;
+    st->n_h_evals = c->h_evals;
     st->n_walk_launches = c->walk_launches;
     st->cells_reused = c->cells_reused ? 1 : 0;
     st->ms_kernel_sort = c->ms_phase[3];
@@ -1515,7 +1522,7 @@ int sph_update_cells(sph_ctx* ctx, const float* x, const float* h0) {
     LAUNCH(k_init_iter, grid1d(c, n, 256), 256, 0, Bget<uint8_t>(c, B_TGT), n, Bget<float4>(c, B_XH),
            c->cfg.h_margin, h_cap(c), Bget<uint8_t>(c, B_STATE), hb, Bget<float>(c, B_HLO), Bget<float>(c, B_HHI));
   }
-  hctr_reset(c);
+  hctr_zero(c);
   CUDA_TRY(cudaMemsetAsync(B<unsigned long long>(c, B_WALKRAW, 2), 0, 2 * sizeof(unsigned long long), c->stream));
   nb_walk(c, -1);
   c->state = 1;

@@ -550,6 +550,7 @@ __global__ void WALK_BOUNDS k_walk(WalkParams P) {
   // (up to SPH_INWALK_PASSES passes) instead of waiting for a host round
   HLane H;
   H.h = H.hbs = H.l = H.u = 0.f;
+  H.ev = 0;
   H.st = HS_DONE;
   H.it = 0;
   int nb_tot = 0;

@@ -64,6 +64,7 @@ class Stats(ctypes.Structure):
         ("n_borderline_force", ctypes.c_int64), ("n_coincident", ctypes.c_int64),
         ("n_nb_sources", ctypes.c_int64), ("n_union_sources", ctypes.c_int64), ("cells_reused", ctypes.c_int32),
         ("ms_kernel_sort", ctypes.c_double), ("sort_key_bits", ctypes.c_int32), ("sort_passes", ctypes.c_int32),
+        ("n_h_evals", ctypes.c_int64),
     ]
 
     def as_dict(self):

@@ -299,3 +299,40 @@ def test_symmetric_force(case):
     assert g["stats_force"]["n_pairs"] == g0["stats_force"]["n_pairs"]
     assert np.array_equal(g["n_nbr_force"], g0["n_nbr_force"])
     assert np.array_equal(g["vsig"], g0["vsig"])
+
+
+@pytest.mark.parametrize("case", ["c1", "overflow"])
+def test_h_iteration_work_counter(case):
+    """sph_stats.n_h_evals (the entries the h iteration summed, the NB walk's credited Eq. 3
+    work in bench.py's roofline): every target's final evaluation summed at least its n_nbr
+    neighbours, and no entry is summed more than max_h_iter times per recorded list."""
+    if case == "c1":
+        p, cfg = workloads.c1(), dict(BENCH_CFG)
+    else:
+        p = workloads.tiny(6, n=5000, clump_frac=0.4, n_dup=2)
+        p.h0[:] = 0.0
+        cfg = dict(row_cap=64, **BENCH_CFG)
+    g = P.run_gpu(p, **cfg)
+    sd = g["stats_density"]
+    ev, ne = sd["n_h_evals"], sd["n_nb_entries"]
+    assert ev >= int(g["n_nbr"].astype(np.int64).sum()) > 0, (ev, int(g["n_nbr"].sum()))
+    assert ev <= 64 * ne, (ev, ne)           # max_h_iter default 64
+    assert ev <= 12 * ne                     # Newton/Halley from the count-based start: few passes
+
+
+def test_h_iteration_work_counter_repeated_call():
+    """A repeated density call re-solves from the converged h on the recorded lists: about one
+    evaluation per entry, counted afresh (not accumulated over calls)."""
+    import torch
+
+    import paper_1404_2303_b200 as sph
+    p = workloads.c1()
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    ctx = sph.Context(sph.default_config(p.box, n_ngb_tol=1e-4, **BENCH_CFG))
+    ctx.build_cells(t(p.x))
+    d1 = ctx.density(t(p.v), t(p.m), t(p.u))
+    d2 = ctx.density(t(p.v), t(p.m), t(p.u))
+    e1, e2 = d1.stats["n_h_evals"], d2.stats["n_h_evals"]
+    n_nbr = int(d2.n_nbr.sum().item())
+    ctx.close()
+    assert n_nbr <= e2 < e1, (n_nbr, e2, e1)
