@@ -99,8 +99,9 @@ typedef struct {
   uint32_t flags;        /* SPH_F_* */
   int32_t rank, nranks;  /* 0, 1 for a single GPU */
   double slab_lo, slab_hi; /* owned x-range of this rank (multi-GPU) */
-  double halo_width;     /* multi-GPU: width of the halo received at each slab face; an h beyond
-                            it cannot be evaluated (SPH_E_NOCONV "halo too narrow"). 0 = none */
+  double halo_width;     /* multi-GPU: width of the halo received at each slab face; an owned
+                            particle within h of a face with h beyond it cannot be evaluated
+                            (SPH_E_NOCONV "halo too narrow"; sph_halo_required). 0 = none */
   /* capacities and tuning of the neighbour-finding structures (results do not depend on them) */
   int32_t row_cap;       /* entries of a particle's neighbour row (the h iteration's distances);
                             longer rows shrink h_build once, then go to an exactly sized pool.
@@ -278,6 +279,29 @@ int sph_halo_exchange(sph_ctx* ctx, int32_t cols, const float* send_lo, int64_t 
 /* In-place all-reduce of a device buffer over the communicator: dtype 0 = fp64, 1 = int64;
  * op 0 = sum, 1 = max (slab-cut histograms, the global max h for the halo width). */
 int sph_allreduce(sph_ctx* ctx, void* buf, int64_t count, int32_t dtype, int32_t op);
+
+/* Work-weighted histogram (NEXT-f3, work-weighted partition; the paper weights its cell
+ * graph by the cost of the pair tasks): hist_out[b] = sum of w[i] (int32 work
+ * units, negative counted as 0) over the particles with x in bin b of [lo, hi). Integer
+ * sums, so the cuts taken from it are reproducible. */
+int sph_x_histogram_weighted(sph_ctx* ctx, int64_t n, const float* x, const int32_t* w, double lo, double hi,
+                             int32_t nbins, int64_t* hist_out);
+
+/* Particles that left the slab [lo, hi) (re-partition / drift): idx_lo_out = ascending
+ * indices with x < lo (to the lower neighbour), idx_hi_out = those with x >= hi (to the
+ * upper one); each has room for n entries, counts_out[0..1] their lengths. */
+int sph_slab_leavers(sph_ctx* ctx, int64_t n, const float* x, double lo, double hi, int32_t* idx_lo_out,
+                     int32_t* idx_hi_out, int64_t* counts_out);
+
+/* The halo width the last sph_density call on a context with a halo needs: the largest h of
+ * an owned particle lying within h of a slab face (every partner of an owned particle, and
+ * every foreign particle whose h reaches one, then lies within that distance of the face).
+ * Set also when the call returned SPH_E_NOCONV because it exceeded cfg.halo_width: the caller
+ * sends the missing band [width, h_max) of its faces and evaluates again (slab.py). */
+int sph_halo_required(sph_ctx* ctx, double* h_max);
+
+/* Replace cfg.halo_width (after the band of a wider halo was received). width >= 0. */
+int sph_set_halo_width(sph_ctx* ctx, double width);
 
 /* Histogram of x over [lo, hi) into nbins bins (for count-quantile slab cuts). */
 int sph_x_histogram(sph_ctx* ctx, int64_t n, const float* x, double lo, double hi, int32_t nbins,

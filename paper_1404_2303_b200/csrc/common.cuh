@@ -171,6 +171,7 @@ struct sph_ctx {
   const float* xin = nullptr;   // this call's positions (caller's device array or a staged copy)
   const float* hin = nullptr;   // this call's h0 (or null)
   int64_t nb_entries = 0, walk_launches = 0, h_evals = 0;
+  double h_own_max = 0.0;   // largest owned h of the last density call (sph_halo_required)
 
   // named device buffers
   DBuf b[96];
@@ -196,7 +197,7 @@ enum BufId {
   // groups and interaction lists
   B_GROUPS, B_GOFF, B_GLEN, B_LIST, B_NBR2, B_NBCNT, B_NBOFF, B_NBOVF, B_OVFIDX, B_NBENT, B_GKEYS, B_GORDER, B_SHRUNK, B_OVFC, B_OVFCNT, B_HCTR, B_RGL, B_RGCNT, B_XREF, B_TGT, B_ACTIVE, B_TSTEP, B_WALKRAW, B_GFLAG, B_GSEL, B_HRCH,
   // misc scratch
-  B_ABLIST, B_PGROUP, B_SYM_IA, B_SYM_IVS, B_SYM_ICNT, B_SYM_JA, B_SYM_JVS, B_SYM_JCNT,
+  B_ABLIST, B_WIN, B_PGROUP, B_SYM_IA, B_SYM_IVS, B_SYM_ICNT, B_SYM_JA, B_SYM_JVS, B_SYM_JCNT,
   B_TMPI0, B_TMPI1, B_TMPL0, B_TMPL1, B_COUNTERS, B_OUT0, B_OUT1, B_OUT2, B_OUT3, B_OUT4, B_OUT5,
   B_COUNT
 };

@@ -889,12 +889,18 @@ __global__ void k_init_iter(const uint8_t* __restrict__ tgt, int64_t n, const fl
 // owned particles within `width` of the lower / upper face of the slab
 // [lo, hi) (in x) are sent to the lower / upper neighbour rank as its halo (proxy cells of
 // P:1065-1105). Flags here; compaction by scan keeps caller order.
+// width > 0: within width of the faces (halo); width == 0: outside [lo, hi) (slab leavers)
 __global__ void k_halo_flags(const float* __restrict__ x, int64_t n, float lo, float hi, float width,
                              int* __restrict__ flo, int* __restrict__ fhi) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const float xi = x[3 * i];
-    flo[i] = (xi - lo < width) ? 1 : 0;
-    fhi[i] = (hi - xi < width) ? 1 : 0;
+    if (width > 0.f) {
+      flo[i] = (xi - lo < width) ? 1 : 0;
+      fhi[i] = (hi - xi < width) ? 1 : 0;
+    } else {
+      flo[i] = (xi < lo) ? 1 : 0;
+      fhi[i] = (xi >= hi) ? 1 : 0;
+    }
   }
 }
 
@@ -945,6 +951,33 @@ __global__ void k_x_hist(const float* __restrict__ x, int64_t n, float lo, float
     int b = (int)floorf((x[3 * i] - lo) / (hi - lo) * nb);
     b = min(max(b, 0), nb - 1);
     atomicAdd(&hist[b], 1ull);
+  }
+}
+
+// the halo width the owned particles need (a proxy cell holds every foreign
+// particle an owned one interacts with): the largest h of an owned particle within h of a
+// slab face. A foreign j must be in the halo iff some owned i has r_ij < max(h_i, h_j); both
+// cases put the particle with the larger h within that h of the face, so the max over both
+// ranks of this quantity bounds the distance beyond the face any partner lies at.
+__global__ void k_hface(const uint32_t* __restrict__ perm, const float4* __restrict__ xh, int64_t n, int64_t n_own,
+                        float lo, float hi, unsigned long long* ctr) {
+  unsigned mx = 0u;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+    if (perm[s] >= n_own) continue;
+    const float4 p = xh[s];
+    if (p.x - lo < p.w || hi - p.x < p.w) mx = max(mx, __float_as_uint(p.w));
+  }
+  mx = __reduce_max_sync(FULL_MASK, mx);
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(&ctr[C_HMAXBITS], (unsigned long long)mx);
+}
+
+// work-weighted histogram (integer work units: exact, order-independent sums)
+__global__ void k_x_hist_w(const float* __restrict__ x, const int32_t* __restrict__ w, int64_t n, float lo, float hi,
+                           int nb, unsigned long long* __restrict__ hist) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int b = (int)floorf((x[3 * i] - lo) / (hi - lo) * nb);
+    b = min(max(b, 0), nb - 1);
+    atomicAdd(&hist[b], (unsigned long long)max(w[i], 0));
   }
 }
 

@@ -1198,14 +1198,17 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
     unconv = nbad;
   }
   if (c->n > c->n_own && c->cfg.halo_width > 0.0) {
-    // every owned particle's partners must be inside the received halo
+    // every owned particle's partners must be inside the received halo: the largest h of an
+    // owned particle within h of a face must not exceed the halo width (k_hface)
     ctr_reset(c);
-    LAUNCH(k_hrange, grid1d(c, c->n_own, 256), 256, 0, Bget<float>(c, B_HFIN_O), c->n_own, ctr(c));
+    LAUNCH(k_hface, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), Bget<float4>(c, B_XH), n, c->n_own,
+           (float)c->cfg.slab_lo, (float)c->cfg.slab_hi, ctr(c));
     unsigned long long hh[C_NCOUNTERS];
     ctr_read(c, hh);
+    c->h_own_max = as_float(hh[C_HMAXBITS]);
     SPH_REQUIRE(as_float(hh[C_HMAXBITS]) <= c->cfg.halo_width, SPH_E_NOCONV,
                 "halo too narrow: an owned h = " + std::to_string(as_float(hh[C_HMAXBITS])) +
-                    " exceeds cfg.halo_width");
+                    " within h of a slab face exceeds cfg.halo_width");
   }
   phase_resolve(c);
   {
@@ -1373,11 +1376,74 @@ int sph_guess_h(sph_ctx* ctx, int64_t n, const float* x, float* h_out) {
   return SPH_OK;
 }
 
+// the two face selections of sph_halo_select (width > 0) and sph_slab_leavers (width == 0)
+static void face_select(sph_ctx* c, int64_t n, const float* x, double lo, double hi, double width,
+                        int32_t* idx_lo_out, int32_t* idx_hi_out, int64_t* counts_out);
+
 int sph_halo_select(sph_ctx* ctx, int64_t n, const float* x, double lo, double hi, double width,
                     int32_t* idx_lo_out, int32_t* idx_hi_out, int64_t* counts_out) {
   API_BEGIN(ctx)
   SPH_REQUIRE(n > 0 && x && idx_lo_out && idx_hi_out && counts_out, SPH_E_ARG, "bad argument");
   SPH_REQUIRE(hi > lo && width > 0.0, SPH_E_ARG, "need hi > lo and width > 0");
+  face_select(c, n, x, lo, hi, width, idx_lo_out, idx_hi_out, counts_out);
+  API_END
+  return SPH_OK;
+}
+
+int sph_slab_leavers(sph_ctx* ctx, int64_t n, const float* x, double lo, double hi, int32_t* idx_lo_out,
+                     int32_t* idx_hi_out, int64_t* counts_out) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(n >= 0 && idx_lo_out && idx_hi_out && counts_out && (n == 0 || x), SPH_E_ARG, "bad argument");
+  SPH_REQUIRE(hi > lo, SPH_E_ARG, "need hi > lo");
+  if (n == 0) {
+    counts_out[0] = counts_out[1] = 0;
+    return SPH_OK;
+  }
+  face_select(c, n, x, lo, hi, 0.0, idx_lo_out, idx_hi_out, counts_out);
+  API_END
+  return SPH_OK;
+}
+
+int sph_halo_required(sph_ctx* ctx, double* h_max) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(h_max, SPH_E_ARG, "h_max is NULL");
+  *h_max = c->h_own_max;
+  API_END
+  return SPH_OK;
+}
+
+int sph_set_halo_width(sph_ctx* ctx, double width) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(width >= 0.0 && std::isfinite(width), SPH_E_ARG, "width must be finite and >= 0");
+  c->cfg.halo_width = width;
+  API_END
+  return SPH_OK;
+}
+
+int sph_x_histogram_weighted(sph_ctx* ctx, int64_t n, const float* x, const int32_t* w, double lo, double hi,
+                             int32_t nbins, int64_t* hist_out) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(n >= 0 && nbins > 0 && hist_out && (n == 0 || (x && w)) && hi > lo, SPH_E_ARG, "bad argument");
+  unsigned long long* hd = B<unsigned long long>(c, B_TMPL1, nbins);
+  CUDA_TRY(cudaMemsetAsync(hd, 0, nbins * sizeof(unsigned long long), c->stream));
+  if (n > 0) {
+    const float* xd = dev_in(c, x, 3 * n, B_XIN);
+    const int32_t* wd = dev_in(c, w, n, B_WIN);
+    LAUNCH(k_x_hist_w, grid1d(c, n, 256), 256, 0, xd, wd, n, (float)lo, (float)hi, nbins, hd);
+  }
+  std::vector<OutMap> maps;
+  int64_t* o = dev_out(c, hist_out, nbins, B_OUT3, maps);
+  CUDA_TRY(cudaMemcpyAsync(o, hd, nbins * sizeof(int64_t), cudaMemcpyDeviceToDevice, c->stream));
+  flush_out(c, maps, c->ev[10]);
+  sync(c);
+  API_END
+  return SPH_OK;
+}
+
+}  // extern "C"
+
+static void face_select(sph_ctx* c, int64_t n, const float* x, double lo, double hi, double width,
+                        int32_t* idx_lo_out, int32_t* idx_hi_out, int64_t* counts_out) {
   const float* xd = dev_in(c, x, 3 * n, B_XIN);
   int* flo = B<int>(c, B_TMPI0, n);
   int* fhi = B<int>(c, B_TMPI1, n);
@@ -1396,9 +1462,9 @@ int sph_halo_select(sph_ctx* ctx, int64_t n, const float* x, double lo, double h
   sync(c);
   counts_out[0] = nlo;
   counts_out[1] = nhi;
-  API_END
-  return SPH_OK;
 }
+
+extern "C" {
 
 int sph_halo_pack(sph_ctx* ctx, const float* x, const float* v, const float* m, const float* u, const float* h0,
                   int64_t k, const int32_t* idx, float* out) {

@@ -8,7 +8,14 @@ Per evaluation, two halo exchanges with the two slab neighbours (periodic ring):
   2. before the force loop: their h, A, rho, c, f (`sph_export_state` /
      `sph_import_halo_state`).
 Halo particles are sources only; owned-halo pairs are computed on both ranks, each updating
-its own particle (no reverse exchange).
+its own particle (no reverse exchange). When an owned h comes out wider than the halo
+(libsph returns SPH_E_NOCONV and `sph_halo_required` the width needed), every rank sends the
+missing band [width, need) of its faces and evaluates again (`evaluate_rank`).
+
+Partition (NEXT-f3): the cuts sit at quantiles of a global x histogram, of
+particle counts (`slab_cuts` of `sph_x_histogram`) or of per-particle work units from the
+previous evaluation (`work_weights`, `sph_x_histogram_weighted`); `migrate` moves the
+particles that a new cut puts on the other side of a face to the neighbouring rank.
 
 All device work is in libsph; this module moves buffers between ranks through
 torch.distributed (NCCL point-to-point over NVLink on GPUs, gloo in CPU tests) and picks
@@ -42,6 +49,25 @@ def slab_cuts(hist, lo: float, hi: float, world: int) -> list[float]:
         if not b > a:
             raise ValueError("degenerate slab cut")
     return edges
+
+
+#: fixed work units per particle in the weighted partition (sort, tree, walk traversal), beside
+#: its density and force neighbours (tools/balance_run.py fits the ratio on C5 slabs)
+WORK_FIXED = 32
+
+
+def work_weights(n_nbr, n_nbr_force, fixed: int = WORK_FIXED):
+    """int32 work units per owned particle from the previous evaluation's neighbour counts:
+    the paper weights its cell graph by the cost of the pair tasks."""
+    return (n_nbr + n_nbr_force + fixed).to(dtype=n_nbr.dtype)
+
+
+def partition(ctx, transport, x, lo: float, hi: float, world: int, w=None, nbins: int = 8192) -> list[float]:
+    """Global cuts of [lo, hi) into `world` slabs: quantiles of the all-reduced x histogram of
+    every rank's particles, counts (w None) or work units w (int32, `work_weights`)."""
+    hist = ctx.x_histogram(x, lo, hi, nbins) if w is None else ctx.x_histogram_weighted(x, w, lo, hi, nbins)
+    hist = transport.allreduce_sum(hist)
+    return slab_cuts(hist.cpu().numpy(), lo, hi, world)
 
 
 def neighbours(rank: int, world: int) -> tuple[int, int]:
@@ -183,15 +209,16 @@ class SlabRank:
             # both faces border the same rank: send a particle near both faces only once
             keep = ~torch.isin(self.idx_hi, self.idx_lo)
             self.idx_hi = self.idx_hi[keep].contiguous()
-        if self.x.is_cuda:   # one libsph kernel per face (k_halo_pack)
-            return (self.ctx.halo_pack(self.x, self.v, self.m, self.u, self.h0, self.idx_lo),
-                    self.ctx.halo_pack(self.x, self.v, self.m, self.u, self.h0, self.idx_hi))
-        pk = pack(self.x, self.v, self.m, self.u, self.h0)   # CPU tensors (gloo tests of the host logic)
-        return pk[self.idx_lo.long()].contiguous(), pk[self.idx_hi.long()].contiguous()
+        # CUDA: one libsph kernel per face (k_halo_pack); CPU tensors: the gloo tests of the host logic
+        return self._pack(self.idx_lo), self._pack(self.idx_hi)
 
-    def density(self, recv_lo, recv_hi):
-        """Phase 2: build over owned + halo particles, h iteration and density loop."""
+    def density(self, recv_lo, recv_hi) -> float:
+        """Phase 2: build over owned + halo particles, h iteration and density loop. Returns
+        0 when every owned h fits the halo, else the width it needs (the evaluation must be
+        repeated with the band up to that width: `extend`)."""
         import torch
+
+        from .sph import SPH_E_NOCONV, SphError
         halo = torch.cat([recv_lo, recv_hi])
         self.n_halo = int(halo.shape[0])
         hx, hv, hm, hu, hh0 = unpack(halo)
@@ -201,8 +228,38 @@ class SlabRank:
         U = torch.cat([self.u, hu]).contiguous()
         H0 = torch.cat([self.h0, hh0]).contiguous()
         self.ctx.build_cells_halo(X, self.n_own, H0 if bool((H0 > 0).all()) else None)
-        self.d = self.ctx.density(V, M, U)
-        return self.d
+        self.d = None
+        try:
+            self.d = self.ctx.density(V, M, U)
+        except SphError as e:
+            need = self.ctx.halo_required() if e.status == SPH_E_NOCONV else 0.0
+            if not need > self.width:
+                raise
+            return need
+        return 0.0
+
+    def extend(self, width):
+        """The band of the faces between the current halo width and `width`, packed like
+        `select` (to lower, to upper); the band rows follow the first ones in the halo order."""
+        import torch
+        if not (width <= self.hi - self.lo):
+            raise ValueError("an owned h exceeds the slab width (next-nearest slabs would be needed)")
+        lo2, hi2 = self.ctx.halo_select(self.x, self.lo, self.hi, width)
+        sent = torch.cat([self.idx_lo, self.idx_hi])
+        b_lo = lo2[~torch.isin(lo2, sent)].contiguous()
+        if self.world == 2:   # one peer: a particle goes to it once
+            sent = torch.cat([sent, b_lo])
+        b_hi = hi2[~torch.isin(hi2, sent)].contiguous()
+        self.idx_lo = torch.cat([self.idx_lo, b_lo])
+        self.idx_hi = torch.cat([self.idx_hi, b_hi])
+        self.width = float(width)
+        self.ctx.set_halo_width(self.width)
+        return self._pack(b_lo), self._pack(b_hi)
+
+    def _pack(self, idx):
+        if self.x.is_cuda:
+            return self.ctx.halo_pack(self.x, self.v, self.m, self.u, self.h0, idx)
+        return pack(self.x, self.v, self.m, self.u, self.h0)[idx.long()].contiguous()
 
     def export(self):
         """Phase 3: state of the particles sent in phase 1 (same order)."""
@@ -218,11 +275,29 @@ class SlabRank:
                           f.stats)
 
 
+#: band rounds before giving up (one suffices: a wider halo only lowers the owned h)
+MAX_BAND_ROUNDS = 3
+
+
+def _grow(need):
+    return need * (1.0 + 1e-6)
+
+
 def evaluate_rank(ctx, x, v, m, u, h0, lo, hi, width, transport):
-    """One rank's evaluation with a live transport (DistTransport)."""
+    """One rank's evaluation with a live transport (DistTransport / LibTransport)."""
+    import torch
     r = SlabRank(ctx, x, v, m, u, h0, lo, hi, width, transport.world)
     s_lo, s_hi = r.select()
-    r.density(*transport.exchange(s_lo, s_hi))
+    got_lo, got_hi = transport.exchange(s_lo, s_hi)
+    for _ in range(MAX_BAND_ROUNDS + 1):
+        need = transport.allreduce_max(r.density(got_lo, got_hi))
+        if not need > r.width:
+            break
+        b_lo, b_hi = r.extend(_grow(need))
+        e_lo, e_hi = transport.exchange(b_lo, b_hi)
+        got_lo, got_hi = torch.cat([got_lo, e_lo]), torch.cat([got_hi, e_hi])
+    else:
+        raise RuntimeError("halo band rounds did not converge")
     e_lo, e_hi = r.export()
     return r.force(*transport.exchange(e_lo, e_hi))
 
@@ -230,14 +305,57 @@ def evaluate_rank(ctx, x, v, m, u, h0, lo, hi, width, transport):
 def evaluate_ring_sequential(ranks):
     """Evaluate a list of SlabRank (ranks 0..P-1 of one ring) one after another in ONE
     process, passing the halo buffers directly (single-GPU tests of the decomposition)."""
+    import torch
     P = len(ranks)
     sent = [r.select() for r in ranks]                       # (to lower, to upper)
-    for k, r in enumerate(ranks):
-        lower, upper = neighbours(k, P)
-        r.density(sent[lower][1], sent[upper][0])            # from lower: its upper face
+    # from lower: its upper face; from upper: its lower face
+    got = [[sent[neighbours(k, P)[0]][1], sent[neighbours(k, P)[1]][0]] for k in range(P)]
+    for _ in range(MAX_BAND_ROUNDS + 1):
+        need = max(r.density(*got[k]) for k, r in enumerate(ranks))
+        if not need > ranks[0].width:
+            break
+        band = [r.extend(_grow(need)) for r in ranks]
+        for k in range(P):
+            lower, upper = neighbours(k, P)
+            got[k] = [torch.cat([got[k][0], band[lower][1]]), torch.cat([got[k][1], band[upper][0]])]
+    else:
+        raise RuntimeError("halo band rounds did not converge")
     ex = [r.export() for r in ranks]
     out = []
     for k, r in enumerate(ranks):
         lower, upper = neighbours(k, P)
         out.append(r.force(ex[lower][1], ex[upper][0]))
+    return out
+
+
+def migrate(ctx, transport, lo, hi, arrays):
+    """Move the particles outside this rank's new slab [lo, hi) to the neighbour across the
+    face they crossed (a re-partition moves each cut by less than a neighbouring slab; checked
+    on the receiving side). `arrays`: dict of per-particle tensors, `x` [n, 3] first; returns
+    the dict of this rank's particles (kept ones first, then those from the lower and the
+    upper neighbour)."""
+    import torch
+    x = arrays["x"]
+    i_lo, i_hi = ctx.slab_leavers(x, lo, hi)
+    n = int(x.shape[0])
+    keep = torch.ones(n, dtype=torch.bool, device=x.device)
+    keep[i_lo.long()] = False
+    keep[i_hi.long()] = False
+    names = list(arrays)
+    cols = [arrays[k].reshape(n, -1) for k in names]
+    widths = [c.shape[1] for c in cols]
+    dtypes = [c.dtype for c in cols]
+    # one float32 row per particle (integer columns travel as their float32 value: exact below 2^24)
+    rows = torch.cat([c.to(torch.float32) for c in cols], dim=1)
+    got_lo, got_hi = transport.exchange(rows[i_lo.long()].contiguous(), rows[i_hi.long()].contiguous())
+    new = torch.cat([rows[keep], got_lo, got_hi])
+    xin = new[:, 0]
+    if new.shape[0] and not bool(((xin >= lo) & (xin < hi)).all()):
+        raise ValueError("a cut moved by more than one slab: a particle arrived outside the new slab")
+    out = {}
+    c0 = 0
+    for k, w, dt in zip(names, widths, dtypes):
+        col = new[:, c0:c0 + w].to(dt)
+        out[k] = col.reshape((-1,) + tuple(arrays[k].shape[1:])).contiguous()
+        c0 += w
     return out

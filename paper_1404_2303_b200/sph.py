@@ -77,7 +77,8 @@ EXPORTS = ("sph_config_default", "sph_create", "sph_destroy", "sph_set_allocator
            "sph_kernel_launches", "sph_build_cells_halo", "sph_halo_select", "sph_export_state",
            "sph_import_halo_state", "sph_x_histogram", "sph_guess_h", "sph_comm_unique_id", "sph_comm_init",
            "sph_halo_counts", "sph_halo_exchange", "sph_allreduce", "sph_kick", "sph_drift", "sph_timestep", "sph_set_active", "sph_update_cells", "sph_kick_each", "sph_neighbour_min",
-           "sph_debug_export", "sph_pair_ablation", "sph_halo_pack", "sph_timebins", "sph_timebins_wake")
+           "sph_debug_export", "sph_pair_ablation", "sph_halo_pack", "sph_timebins", "sph_timebins_wake",
+           "sph_x_histogram_weighted", "sph_slab_leavers", "sph_halo_required", "sph_set_halo_width")
 
 
 def load(path: str | None = None):
@@ -110,6 +111,10 @@ def load(path: str | None = None):
     lib.sph_import_halo_state.argtypes = [P, P]
     lib.sph_x_histogram.argtypes = [P, i64, P, ctypes.c_double, ctypes.c_double, ctypes.c_int32, P]
     lib.sph_guess_h.argtypes = [P, i64, P, P]
+    lib.sph_x_histogram_weighted.argtypes = [P, i64, P, P, ctypes.c_double, ctypes.c_double, ctypes.c_int32, P]
+    lib.sph_slab_leavers.argtypes = [P, i64, P, ctypes.c_double, ctypes.c_double, P, P, P]
+    lib.sph_halo_required.argtypes = [P, P]
+    lib.sph_set_halo_width.argtypes = [P, ctypes.c_double]
     lib.sph_comm_unique_id.argtypes = [P]
     lib.sph_comm_init.argtypes = [P, P]
     lib.sph_halo_counts.argtypes = [P, i64, i64, P, P]
@@ -251,6 +256,37 @@ class Context:
         self._check(self.lib.sph_halo_select(self.h, n, _ptr(x), float(lo), float(hi), float(width),
                                              _ptr(ilo, np.int32), _ptr(ihi, np.int32), cnt.ctypes.data))
         return ilo[: int(cnt[0])], ihi[: int(cnt[1])]
+
+    def slab_leavers(self, x, lo, hi):
+        """Indices of the particles outside [lo, hi): (x < lo, x >= hi)."""
+        import torch
+        n = int(x.shape[0])
+        dev = x.device if isinstance(x, torch.Tensor) else torch.device("cpu")
+        ilo = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        ihi = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+        cnt = np.zeros(2, dtype=np.int64)
+        self._check(self.lib.sph_slab_leavers(self.h, n, _ptr(x) if n else None, float(lo), float(hi),
+                                              _ptr(ilo, np.int32), _ptr(ihi, np.int32), cnt.ctypes.data))
+        return ilo[: int(cnt[0])], ihi[: int(cnt[1])]
+
+    def halo_required(self) -> float:
+        """The largest owned h of the last density call (the halo width it needs)."""
+        v = ctypes.c_double(0.0)
+        self._check(self.lib.sph_halo_required(self.h, ctypes.byref(v)))
+        return float(v.value)
+
+    def set_halo_width(self, width: float):
+        self._check(self.lib.sph_set_halo_width(self.h, float(width)))
+
+    def x_histogram_weighted(self, x, w, lo, hi, nbins):
+        import torch
+        dev = x.device if isinstance(x, torch.Tensor) else torch.device("cpu")
+        out = torch.zeros(nbins, dtype=torch.int64, device=dev)
+        n = int(x.shape[0])
+        self._check(self.lib.sph_x_histogram_weighted(self.h, n, _ptr(x) if n else None,
+                                                      _ptr(w, np.int32) if n else None, float(lo), float(hi),
+                                                      int(nbins), _ptr(out, np.int64)))
+        return out
 
     def halo_pack(self, x, v, m, u, h0, idx):
         """[k, 9] rows {x, v, m, u, h0} of the owned particles idx (device), one libsph kernel."""
