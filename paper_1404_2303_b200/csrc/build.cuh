@@ -6,7 +6,7 @@
 //                                 orders every level at once (particles of a cell
 //                                 contiguous in memory)
 //  a3  k_pack                   : particles copied into cell order (float4 {x, y, z, h})
-//  a4  k_level_split / k_make_children : recursive split of a cell into its 8 octants while
+//  a4  k_build_levels           : recursive split of a cell into its 8 octants while
 //                                 it holds "more than some minimal number" of particles and
 //                                 "a reasonable fraction" of them has h < edge/2
 //                                 (constants P:1354-1356); one level per launch.
@@ -184,79 +184,199 @@ __global__ void k_top_counts(int n0, int64_t n, NodeArrays N) {
 }
 
 // ---------------------------------------------------------------- a4 ---------
-// Warp per node of one level: split decision and child boundaries by binary
-// search on the octant bits of the sorted keys. hsplit == null: count rule alone.
-__global__ void k_level_split(int a, int b, int level, int depth, const float4* __restrict__ xh,
-                              const uint64_t* __restrict__ keys, float half_edge, int split_count,
-                              float split_frac, NodeArrays N, int* __restrict__ nch,
-                              int* __restrict__ chstart) {
-  const int lane = threadIdx.x & 31;
-  const int node = a + (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
-  if (node >= b) return;
-  const int first = N.first[node], cnt = N.count[node];
-  bool frac_ok = true;
-  if (split_frac > 0.f && cnt > split_count && level < depth) {
-    int nsmall = 0;
-    for (int s = first + lane; s < first + cnt; s += 32) nsmall += (xh[s].w < half_edge) ? 1 : 0;
-    nsmall = warp_sum_i(nsmall);
-    frac_ok = (double)nsmall > (double)split_frac * (double)cnt;
-  }
-  const int sp = (level < depth) && (cnt > split_count) && frac_ok;
-  if (lane == 0) N.split[node] = sp;
-  if (!sp) {
-    if (lane == 0) nch[node - a] = 0;
-    return;
-  }
-  const int shift = 3 * (depth - level - 1);
-  int start = first + cnt;
-  if (lane < 8) {
-    int lo = first, hi = first + cnt;
-    while (lo < hi) {
-      int mid = (lo + hi) >> 1;
-      int oct = (int)((keys[mid] >> shift) & 7ull);
-      if (oct < lane) lo = mid + 1;
-      else hi = mid;
-    }
-    start = lo;
-  }
-  int nxt = __shfl_down_sync(FULL_MASK, start, 1);
-  int ne = (lane < 8 && nxt - start > 0) ? 1 : 0;
-  unsigned bal = __ballot_sync(FULL_MASK, ne);
-  if (lane < 8) chstart[8 * (int64_t)node + lane] = start;
-  if (lane == 0) nch[node - a] = __popc(bal);
+// ---- a4 in one launch: every level of the hierarchy without a host round trip ------------
+// A cooperative (co-resident) grid runs the level loop on the device: per level, (A) warp per
+// node: split decision and octant boundaries (binary search on the keys' octant bits); (B) per-block sums of the
+// children counts; (C) each block's exclusive offset from the block sums, the scan of its
+// contiguous chunk of nodes and their children written. Node numbering: level by level,
+// children in parent order, octant order. A level
+// that would exceed the node capacity stops the loop (status[1] = 1: the host grows the
+// arrays and runs it again).
+struct LevelBuild {
+  int* lev_off;      // [SPH_MAX_DEPTH + 4]: level offsets; [0], [1] set by the host
+  int* status;       // [0] levels processed, [1] 1 = node capacity exceeded, 2 = barrier timeout
+  unsigned* bar;     // grid barrier: arrivals, generation (zeroed before the launch)
+  int* part;         // [gridDim.x] block sums
+  int* nch;          // [cap] children per node of the level being built (index node - a)
+  int cap;           // node capacity
+};
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 
-__global__ void k_make_children(int a, int b, int64_t n_first_next, const int* __restrict__ nch,
-                                 const int* __restrict__ chscan, NodeArrays N) {
-  int p = a + blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= b) return;
-  int* ch = N.child + 8 * (int64_t)p;
-  if (nch[p - a] == 0) {
-#pragma unroll
-    for (int o = 0; o < 8; ++o) ch[o] = -1;
-    return;
-  }
-  int st[9];
-#pragma unroll
-  for (int o = 0; o < 8; ++o) st[o] = ch[o];
-  st[8] = N.first[p] + N.count[p];
-  int4 pijk = N.ijk[p];
-  int k = 0;
-  int base = (int)(n_first_next + chscan[p - a]);
-#pragma unroll
-  for (int o = 0; o < 8; ++o) {
-    int c = st[o + 1] - st[o];
-    if (c > 0) {
-      int cn = base + k++;
-      N.first[cn] = st[o];
-      N.count[cn] = c;
-      N.ijk[cn] = make_int4(2 * pijk.x + ((o >> 2) & 1), 2 * pijk.y + ((o >> 1) & 1),
-                            2 * pijk.z + (o & 1), pijk.w + 1);
-      N.parent[cn] = p;
-      ch[o] = cn;
+// all blocks of a co-resident grid meet here; false if the wait timed out (a stalled grid
+// exits with an error instead of hanging the device)
+__device__ __forceinline__ bool grid_sync(unsigned* bar, int* status) {
+  __shared__ int ok;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ok = 1;
+    volatile unsigned* gen = bar + 1;
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
     } else {
-      ch[o] = -1;
+      const unsigned long long t0 = globaltimer_ns();
+      while (*gen == g) {
+        __nanosleep(100);
+        if (globaltimer_ns() - t0 > 2000000000ull) {
+          ok = 0;
+          atomicExch(status + 1, 2);
+          break;
+        }
+      }
     }
+    __threadfence();
+  }
+  __syncthreads();
+  return ok;
+}
+
+__device__ __forceinline__ int block_sum_i(int v, int* red) {
+  v = warp_sum_i(v);
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  int t = 0;
+  for (int k = 0; k < nw; ++k) t += red[k];
+  return t;
+}
+
+#define LEVEL_THREADS 256
+__global__ void __launch_bounds__(LEVEL_THREADS) k_build_levels(LevelBuild L, const float4* __restrict__ xh,
+                                                                const uint64_t* __restrict__ keys, LevelGeom g,
+                                                                int depth, int split_count, float split_frac,
+                                                                NodeArrays N) {
+  __shared__ int red[LEVEL_THREADS / 32];
+  __shared__ int wsc[LEVEL_THREADS / 32];
+  const int lane = threadIdx.x & 31;
+  const int gw = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int nwarps = (int)(gridDim.x * (blockDim.x >> 5));
+  volatile int* lev = L.lev_off;
+  for (int l = 0;; ++l) {
+    const int a = lev[l], b = lev[l + 1];
+    const float half_edge = 0.5f * fminf(g.E[l][0], fminf(g.E[l][1], g.E[l][2]));
+    // (A) split decision + octant boundaries, warp per node
+    for (int node = a + gw; node < b; node += nwarps) {
+      const int first = __ldcg(N.first + node), cnt = __ldcg(N.count + node);
+      bool frac_ok = true;
+      if (split_frac > 0.f && cnt > split_count && l < depth) {
+        int nsmall = 0;
+        for (int s = first + lane; s < first + cnt; s += 32) nsmall += (xh[s].w < half_edge) ? 1 : 0;
+        nsmall = warp_sum_i(nsmall);
+        frac_ok = (double)nsmall > (double)split_frac * (double)cnt;
+      }
+      const int sp = (l < depth) && (cnt > split_count) && frac_ok;
+      if (lane == 0) N.split[node] = sp;
+      if (!sp) {
+        if (lane == 0) L.nch[node - a] = 0;
+        continue;
+      }
+      const int shift = 3 * (depth - l - 1);
+      int start = first + cnt;
+      if (lane < 8) {
+        int lo = first, hi = first + cnt;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          const int oct = (int)((keys[mid] >> shift) & 7ull);
+          if (oct < lane) lo = mid + 1;
+          else hi = mid;
+        }
+        start = lo;
+      }
+      const int nxt = __shfl_down_sync(FULL_MASK, start, 1);
+      const unsigned bal = __ballot_sync(FULL_MASK, lane < 8 && nxt - start > 0);
+      if (lane < 8) N.child[8 * (int64_t)node + lane] = start;
+      if (lane == 0) L.nch[node - a] = __popc(bal);
+    }
+    if (!grid_sync(L.bar, L.status)) return;
+    // (B) block sums over contiguous chunks of the level
+    const int nl = b - a;
+    const int chunk = (nl + gridDim.x - 1) / gridDim.x;
+    const int c0 = a + min(nl, (int)blockIdx.x * chunk), c1 = a + min(nl, ((int)blockIdx.x + 1) * chunk);
+    int v = 0;
+    for (int p = c0 + threadIdx.x; p < c1; p += blockDim.x) v += __ldcg(L.nch + (p - a));
+    v = block_sum_i(v, red);
+    if (threadIdx.x == 0) L.part[blockIdx.x] = v;
+    if (!grid_sync(L.bar, L.status)) return;
+    // (C) offsets, scan of the chunk, children
+    int before = 0, total = 0;
+    for (int k = threadIdx.x; k < (int)gridDim.x; k += blockDim.x) {
+      const int pk = __ldcg(L.part + k);
+      total += pk;
+      if (k < (int)blockIdx.x) before += pk;
+    }
+    before = block_sum_i(before, red);
+    total = block_sum_i(total, red);
+    const int next = b + total;
+    if (next > L.cap) {   // the same decision in every block: no block waits at a barrier below
+      if (blockIdx.x == 0 && threadIdx.x == 0) L.status[1] = 1;
+      return;
+    }
+    int carry = b + before;
+    for (int t0 = c0; t0 < c1; t0 += blockDim.x) {
+      const int p = t0 + threadIdx.x;
+      const int nc = p < c1 ? __ldcg(L.nch + (p - a)) : 0;
+      // block exclusive scan of nc
+      int incl = nc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL_MASK, incl, o);
+        if (lane >= o) incl += y;
+      }
+      __syncthreads();
+      if (lane == 31) wsc[threadIdx.x >> 5] = incl;
+      __syncthreads();
+      int wpre = 0, ttot = 0;
+      for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+        if (k < (int)(threadIdx.x >> 5)) wpre += wsc[k];
+        ttot += wsc[k];
+      }
+      if (p < c1) {
+        int* ch = N.child + 8 * (int64_t)p;
+        if (nc == 0) {
+#pragma unroll
+          for (int o = 0; o < 8; ++o) ch[o] = -1;
+        } else {
+          int st[9];
+#pragma unroll
+          for (int o = 0; o < 8; ++o) st[o] = __ldcg(ch + o);
+          st[8] = __ldcg(N.first + p) + __ldcg(N.count + p);
+          const int4 pijk = __ldcg(N.ijk + p);
+          const int base = carry + wpre + incl - nc;
+          int k = 0;
+#pragma unroll
+          for (int o = 0; o < 8; ++o) {
+            const int cc = st[o + 1] - st[o];
+            if (cc > 0) {
+              const int cn = base + k++;
+              N.first[cn] = st[o];
+              N.count[cn] = cc;
+              N.ijk[cn] = make_int4(2 * pijk.x + ((o >> 2) & 1), 2 * pijk.y + ((o >> 1) & 1), 2 * pijk.z + (o & 1),
+                                    pijk.w + 1);
+              N.parent[cn] = p;
+              ch[o] = cn;
+            } else {
+              ch[o] = -1;
+            }
+          }
+        }
+      }
+      carry += ttot;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      L.lev_off[l + 2] = next;
+      L.status[0] = l + 1;
+    }
+    if (total == 0) return;
+    if (!grid_sync(L.bar, L.status)) return;
   }
 }
 
@@ -307,7 +427,7 @@ __global__ void k_guess_h(int nnodes, NodeArrays N, LevelGeom g, float n_ngb, in
 
 // packed node records for the list walk: {first, count, first child (-1: none),
 // octant mask of the children | level << 8}; children are allocated contiguously in
-// octant order by k_make_children
+// octant order by k_build_levels
 __global__ void k_node_rec(int nnodes, NodeArrays N, int4* __restrict__ rec) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= nnodes) return;

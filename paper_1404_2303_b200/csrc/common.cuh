@@ -190,7 +190,7 @@ enum BufId {
   B_PERM, B_XH, B_VM, B_U, B_HB, B_HLO, B_HHI, B_STATE, B_DSUMF, B_DACC0, B_DACC1, B_DSUM2,
   B_FX, B_FS,
   // nodes
-  B_N_FIRST, B_N_COUNT, B_N_IJK, B_N_PARENT, B_N_CHILD, B_N_SPLIT, B_N_HMAX, B_N_SORTOFF, B_N_REC, B_N_NCH, B_N_CHBASE,
+  B_N_FIRST, B_N_COUNT, B_N_IJK, B_N_PARENT, B_N_CHILD, B_N_SPLIT, B_N_HMAX, B_N_SORTOFF, B_N_REC, B_N_NCH, B_N_CHBASE, B_N_LEV,
   B_TOPMAP,
   // 13-direction sorted lists
   B_SORTED,

@@ -363,23 +363,51 @@ static void build_nodes(sph_ctx* c, bool use_fraction) {
   LAUNCH(k_write_top, grid1d(c, n, 256), 256, 0, keys, n, sh, flag, idx, c->ntop[0], c->ntop[1], N, topmap);
   LAUNCH(k_top_counts, gridfull(n0, 256), 256, 0, n0, n, N);
   c->lev_off.assign({0, n0});
+  // the levels in one cooperative launch (k_build_levels); grown and re-run if the nodes
+  // outgrow the arrays (they keep their size across builds)
   const LevelGeom g = level_geom(c);
   const float frac = use_fraction ? c->cfg.split_fraction : 0.f;
-  for (int l = 0;; ++l) {
-    const int a = c->lev_off[l], b = c->lev_off[l + 1];
-    const int nl = b - a;
-    int* nch = B<int>(c, B_N_NCH, nl);
-    int* chscan = B<int>(c, B_N_CHBASE, nl);
+  int grid = 0;
+  {
+    int per_sm = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_build_levels, LEVEL_THREADS, 0));
+    grid = std::max(1, per_sm) * c->num_sms;
+  }
+  int* lev = B<int>(c, B_N_LEV, SPH_MAX_DEPTH + 8);
+  int* part = B<int>(c, B_N_CHBASE, grid);
+  for (int attempt = 0;; ++attempt) {
+    const int64_t cap = std::min({(int64_t)(c->b[B_N_FIRST].bytes / sizeof(int)),
+                                  (int64_t)(c->b[B_N_COUNT].bytes / sizeof(int)),
+                                  (int64_t)(c->b[B_N_IJK].bytes / sizeof(int4)),
+                                  (int64_t)(c->b[B_N_PARENT].bytes / sizeof(int)),
+                                  (int64_t)(c->b[B_N_CHILD].bytes / (8 * sizeof(int))),
+                                  (int64_t)(c->b[B_N_SPLIT].bytes / sizeof(int))});
+    LevelBuild Lb;
+    Lb.lev_off = lev;
+    Lb.status = lev + SPH_MAX_DEPTH + 4;
+    Lb.bar = reinterpret_cast<unsigned*>(lev + SPH_MAX_DEPTH + 6);
+    Lb.part = part;
+    Lb.nch = B<int>(c, B_N_NCH, cap);
+    Lb.cap = (int)std::min<int64_t>(cap, INT_MAX);
+    const int h0[2] = {0, n0};
+    CUDA_TRY(cudaMemsetAsync(lev, 0, (SPH_MAX_DEPTH + 8) * sizeof(int), c->stream));
+    CUDA_TRY(cudaMemcpyAsync(lev, h0, sizeof(h0), cudaMemcpyHostToDevice, c->stream));
     N = nodes(c);
-    const float half_edge = 0.5f * std::min(g.E[l][0], std::min(g.E[l][1], g.E[l][2]));
-    LAUNCH(k_level_split, gridfull((int64_t)nl * 32, 256), 256, 0, a, b, l, depth, xh, keys, half_edge,
-           c->cfg.split_count, frac, N, nch, N.child);
-    const int nnext = scan_excl<int>(c, nch, chscan, nl);
-    ensure_nodes(c, (int64_t)b + nnext + 1);
-    N = nodes(c);
-    LAUNCH(k_make_children, gridfull(nl, 256), 256, 0, a, b, (int64_t)b, nch, chscan, N);
-    if (nnext == 0) break;
-    c->lev_off.push_back(b + nnext);
+    void* args[] = {&Lb, (void*)&xh, (void*)&keys, (void*)&g, (void*)&depth, &c->cfg.split_count, (void*)&frac, &N};
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_build_levels, grid, LEVEL_THREADS, args, 0, c->stream));
+    c->launches++;
+    int hl[SPH_MAX_DEPTH + 6];
+    CUDA_TRY(cudaMemcpyAsync(hl, lev, sizeof(hl), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    SPH_REQUIRE(hl[SPH_MAX_DEPTH + 5] != 2, SPH_E_CUDA, "k_build_levels: grid barrier timed out");
+    if (hl[SPH_MAX_DEPTH + 5] == 1) {   // node capacity exceeded: grow and run again
+      SPH_REQUIRE(attempt < 8, SPH_E_OOM, "node arrays keep overflowing");
+      ensure_nodes(c, 2 * cap);
+      continue;
+    }
+    c->lev_off.assign({0, n0});
+    for (int l = 0; l + 2 < SPH_MAX_DEPTH + 4 && hl[l + 2] > hl[l + 1]; ++l) c->lev_off.push_back(hl[l + 2]);
+    break;
   }
   c->n_nodes = c->lev_off.back();
   B<float>(c, B_N_HMAX, c->n_nodes);

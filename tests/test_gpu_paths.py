@@ -336,3 +336,13 @@ def test_h_iteration_work_counter_repeated_call():
     n_nbr = int(d2.n_nbr.sum().item())
     ctx.close()
     assert n_nbr <= e2 < e1, (n_nbr, e2, e1)
+
+
+def test_node_arrays_grow_inside_the_level_build():
+    """split_count 4 on a clustered input: the hierarchy outgrows the initial node arrays
+    (2 n0 + 1024 or n / 8 nodes), k_build_levels reports the overflow, the arrays grow and
+    the levels are built again; results as in every other configuration."""
+    p = workloads.tiny(9, n=6000, clump_frac=0.5, n_dup=2)
+    p.h0[:] = 0.0
+    g, _ = _check(p, split_count=4, split_fraction=0.0)
+    assert g["stats_density"]["n_cells"] > 6000 // 8 + 1024
