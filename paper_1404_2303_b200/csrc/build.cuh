@@ -381,7 +381,8 @@ __global__ void __launch_bounds__(LEVEL_THREADS) k_build_levels(LevelBuild L, co
 }
 
 // per node max of a per-particle value (cell order), warp per node
-__global__ void k_node_hmax(int nnodes, NodeArrays N, const float* __restrict__ h) {
+// (values >= 0); the top cells' maxima also give the global max (ctr[C_HMAXBITS], if set)
+__global__ void k_node_hmax(int nnodes, NodeArrays N, const float* __restrict__ h, unsigned long long* ctr) {
   const int lane = threadIdx.x & 31;
   const int node = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   if (node >= nnodes) return;
@@ -389,7 +390,10 @@ __global__ void k_node_hmax(int nnodes, NodeArrays N, const float* __restrict__ 
   float hm = 0.f;
   for (int s = first + lane; s < first + cnt; s += 32) hm = fmaxf(hm, h[s]);
   hm = warp_max_f(hm);
-  if (lane == 0) N.hmax[node] = hm;
+  if (lane == 0) {
+    N.hmax[node] = hm;
+    if (ctr && N.parent[node] < 0) atomicMax(&ctr[C_HMAXBITS], (unsigned long long)__float_as_uint(hm));
+  }
 }
 
 // initial guess from cell occupancy: N = (4 pi/3) n h^3 for a uniform number density n

@@ -595,10 +595,10 @@ static void build_union(sph_ctx* c, const float* reach) {
   DbgTimer _t(c, "interaction lists");
   const int ng = c->n_groups;
   if (ng == 0) return;
-  // node max of the reach (the walk's bound for sources with a large h)
-  LAUNCH(k_node_hmax, gridfull((int64_t)c->n_nodes * 32, 256), 256, 0, c->n_nodes, nodes(c), reach);
+  // node max of the reach (the walk's bound for sources with a large h); the top cells' maxima
+  // give the global max, read by the walk
   ctr_reset(c);
-  LAUNCH(k_hrange, grid1d(c, c->n, 256), 256, 0, reach, c->n, ctr(c));   // max reach, read by the walk
+  LAUNCH(k_node_hmax, gridfull((int64_t)c->n_nodes * 32, 256), 256, 0, c->n_nodes, nodes(c), reach, ctr(c));
   unsigned long long h[C_NCOUNTERS];
   const int cap = c->ucap;
   WalkParams P = walk_params(c, reach);
