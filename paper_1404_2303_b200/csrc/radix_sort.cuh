@@ -110,15 +110,21 @@ __global__ void __launch_bounds__(RS_THREADS, RS_MINB) k_radix_pass(
     }
   }
   // stable in-warp ranking: items visited in position order (it major, lane minor); the
-  // lanes holding the same digit from 9 ballots (8 digit bits + the invalid flag), cheaper
-  // than __match_any_sync
+  // lanes holding the same digit from ballots of the 8 digit bits (+ the invalid flag in a
+  // partial tile), cheaper than __match_any_sync
+  const bool full = tile_n == RS_TILE;
 #pragma unroll
   for (int it = 0; it < RS_ITEMS; ++it) {
     uint32_t d = dg[it];
     unsigned peers = FULL_MASK;
 #pragma unroll
-    for (int b = 0; b < 9; ++b) {
+    for (int b = 0; b < 8; ++b) {
       const bool bit = (d >> b) & 1u;
+      const unsigned bb = __ballot_sync(FULL_MASK, bit);
+      peers &= bit ? bb : ~bb;
+    }
+    if (!full) {
+      const bool bit = d >> 8;
       const unsigned bb = __ballot_sync(FULL_MASK, bit);
       peers &= bit ? bb : ~bb;
     }
@@ -130,10 +136,12 @@ __global__ void __launch_bounds__(RS_THREADS, RS_MINB) k_radix_pass(
     __syncwarp();
   }
   __syncthreads();
-  // per digit: exclusive over warps, tile total
+  // per digit (thread d): exclusive over warps, the tile total published at once as the
+  // tile's aggregate, and the tile-local exclusive prefix over digits
+  const int d = tid;  // RS_THREADS == 256
   uint32_t tcnt = 0;
+  uint32_t* st = status + (size_t)tile * 256 + d;
   {
-    const int d = tid;  // RS_THREADS == 256
     uint32_t run = 0;
 #pragma unroll
     for (int ww = 0; ww < RS_WARPS; ++ww) {
@@ -142,37 +150,12 @@ __global__ void __launch_bounds__(RS_THREADS, RS_MINB) k_radix_pass(
       run += c;
     }
     tcnt = run;
-    // decoupled look-back over previous tiles for digit d
-    uint32_t* st = status + (size_t)tile * 256 + d;
     if (tile == 0) {
       atomicExch(st, RS_FLAG_INC | tcnt);
       S.gbase[d] = gofs[d];
     } else {
       atomicExch(st, RS_FLAG_AGG | tcnt);
-      // look back RS_LB predecessors at a time (independent loads in flight): the tiles of
-      // the first wave all publish their aggregates at about the same time, and a serial
-      // walk would pay one L2 round trip per predecessor
-      uint32_t excl = 0;
-      int64_t pt = (int64_t)tile - 1;
-      bool done = false;
-      while (!done) {
-        uint32_t sv[RS_LB];
-#pragma unroll
-        for (int k = 0; k < RS_LB; ++k)
-          sv[k] = pt - k >= 0 ? ld_volatile_u32(status + (size_t)(pt - k) * 256 + d) : RS_FLAG_INC;
-#pragma unroll
-        for (int k = 0; k < RS_LB; ++k) {
-          if (done) break;
-          while ((sv[k] & (RS_FLAG_INC | RS_FLAG_AGG)) == 0) sv[k] = ld_volatile_u32(status + (size_t)(pt - k) * 256 + d);
-          excl += sv[k] & RS_VAL_MASK;
-          if (sv[k] & RS_FLAG_INC) done = true;
-        }
-        pt -= RS_LB;
-      }
-      atomicExch(st, RS_FLAG_INC | (excl + tcnt));
-      S.gbase[d] = gofs[d] + excl;
     }
-    // tile-local exclusive prefix over digits (block scan of tcnt)
     uint32_t x = tcnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -186,20 +169,51 @@ __global__ void __launch_bounds__(RS_THREADS, RS_MINB) k_radix_pass(
     S.dpre[d] = x - tcnt + add;
   }
   __syncthreads();
+  // the tile sorted by digit in shared memory: this work sits between the tile's aggregate
+  // and its look-back, so the predecessors have mostly published their inclusive prefix by
+  // the time it is read
 #pragma unroll
   for (int it = 0; it < RS_ITEMS; ++it) {
-    uint32_t d = dg[it];
-    if (d < 256u) {
-      uint32_t pos = S.dpre[d] + S.wcnt[w][d] + rank[it];
+    uint32_t dd = dg[it];
+    if (dd < 256u) {
+      uint32_t pos = S.dpre[dd] + S.wcnt[w][dd] + rank[it];
       S.keys[pos] = k[it];
       S.vals[pos] = v[it];
     }
   }
+  // decoupled look-back over the previous tiles for digit d: the predecessor first (usually
+  // inclusive by now), then RS_LB statuses at a time
+  if (tile != 0) {
+    uint32_t excl = 0;
+    int64_t pt = (int64_t)tile - 1;
+    uint32_t s0 = ld_volatile_u32(status + (size_t)pt * 256 + d);
+    while ((s0 & (RS_FLAG_INC | RS_FLAG_AGG)) == 0) s0 = ld_volatile_u32(status + (size_t)pt * 256 + d);
+    excl = s0 & RS_VAL_MASK;
+    bool done = (s0 & RS_FLAG_INC) != 0;
+    --pt;
+    while (!done) {
+      uint32_t sv[RS_LB];
+#pragma unroll
+      for (int k2 = 0; k2 < RS_LB; ++k2)
+        sv[k2] = pt - k2 >= 0 ? ld_volatile_u32(status + (size_t)(pt - k2) * 256 + d) : RS_FLAG_INC;
+#pragma unroll
+      for (int k2 = 0; k2 < RS_LB; ++k2) {
+        if (done) break;
+        while ((sv[k2] & (RS_FLAG_INC | RS_FLAG_AGG)) == 0)
+          sv[k2] = ld_volatile_u32(status + (size_t)(pt - k2) * 256 + d);
+        excl += sv[k2] & RS_VAL_MASK;
+        if (sv[k2] & RS_FLAG_INC) done = true;
+      }
+      pt -= RS_LB;
+    }
+    atomicExch(st, RS_FLAG_INC | (excl + tcnt));
+    S.gbase[d] = gofs[d] + excl;
+  }
   __syncthreads();
   for (int i = tid; i < tile_n; i += RS_THREADS) {
     uint64_t kk = S.keys[i];
-    uint32_t d = (uint32_t)(kk >> shift) & 255u;
-    uint32_t g = S.gbase[d] + (uint32_t)i - S.dpre[d];
+    uint32_t dd = (uint32_t)(kk >> shift) & 255u;
+    uint32_t g = S.gbase[dd] + (uint32_t)i - S.dpre[dd];
     kout[g] = kk;
     vout[g] = S.vals[i];
   }
