@@ -184,6 +184,8 @@ __global__ void k_top_counts(int n0, int64_t n, NodeArrays N) {
 }
 
 // ---------------------------------------------------------------- a4 ---------
+#define GUESS_MIN_COUNT 8   // a cell counts for the occupancy guess from this many particles
+
 // ---- a4 in one launch: every level of the hierarchy without a host round trip ------------
 // A cooperative (co-resident) grid runs the level loop on the device: per level, (A) warp per
 // node: split decision and octant boundaries (binary search on the keys' octant bits); (B) per-block sums of the
@@ -250,10 +252,13 @@ __device__ __forceinline__ int block_sum_i(int v, int* red) {
 }
 
 #define LEVEL_THREADS 256
+// guess_n > 0: a cold start; each leaf, once decided, writes the occupancy guess of h (as
+// k_guess_h, n_ngb = guess_n, ancestors up to guess_min particles) into xh_w[].w where 0.
 __global__ void __launch_bounds__(LEVEL_THREADS) k_build_levels(LevelBuild L, const float4* __restrict__ xh,
                                                                 const uint64_t* __restrict__ keys, LevelGeom g,
                                                                 int depth, int split_count, float split_frac,
-                                                                NodeArrays N) {
+                                                                NodeArrays N, float guess_n, int guess_min,
+                                                                float hcap, float4* xh_w) {
   __shared__ int red[LEVEL_THREADS / 32];
   __shared__ int wsc[LEVEL_THREADS / 32];
   const int lane = threadIdx.x & 31;
@@ -277,6 +282,25 @@ __global__ void __launch_bounds__(LEVEL_THREADS) k_build_levels(LevelBuild L, co
       if (lane == 0) N.split[node] = sp;
       if (!sp) {
         if (lane == 0) L.nch[node - a] = 0;
+        if (guess_n > 0.f) {
+          double dens = 0.0;
+          int y = node;
+          while (true) {
+            const int cy = __ldcg(N.count + y);
+            const int ly = __ldcg(N.ijk + y).w;
+            const double vol = (double)g.E[ly][0] * g.E[ly][1] * g.E[ly][2];
+            if (cy >= GUESS_MIN_COUNT) dens = fmax(dens, (double)cy / vol);
+            const int py = __ldcg(N.parent + y);
+            if (cy >= guess_min || py < 0) {
+              if (dens == 0.0) dens = (double)cy / vol;
+              break;
+            }
+            y = py;
+          }
+          const float hg = fminf((float)cbrt(3.0 * guess_n / (4.0 * 3.14159265358979323846 * dens)), hcap);
+          for (int s = first + lane; s < first + cnt; s += 32)
+            if (xh_w[s].w == 0.f) xh_w[s].w = hg;
+        }
         continue;
       }
       const int shift = 3 * (depth - l - 1);
@@ -402,7 +426,6 @@ __global__ void k_node_hmax(int nnodes, NodeArrays N, const float* __restrict__ 
 // >= n_ngb: next to a dense clump a sparse cell's mean density hides the clump, and an
 // over-estimated h costs a long interaction list while an under-estimate costs one Newton
 // step. Written in cell order into xh[].w where h == 0.
-#define GUESS_MIN_COUNT 8
 __global__ void k_guess_h(int nnodes, NodeArrays N, LevelGeom g, float n_ngb, int min_count, float hcap,
                           float4* __restrict__ xh) {
   const int lane = threadIdx.x & 31;

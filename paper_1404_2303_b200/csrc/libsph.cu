@@ -344,7 +344,7 @@ static void sort_particles(sph_ctx* c, float h0max, bool have_h) {
 // a4: the hierarchy from the sorted keys. Split rule: count > split_count and (rule on)
 // more than split_fraction of the particles have h < edge/2; with
 // use_fraction false the count alone decides (occupancy tree of the cold start).
-static void build_nodes(sph_ctx* c, bool use_fraction) {
+static void build_nodes(sph_ctx* c, bool use_fraction, bool guess = false) {
   DbgTimer _t(c, "nodes");
   const int64_t n = c->n;
   const uint64_t* keys = Bget<uint64_t>(c, B_KEYS0);
@@ -393,7 +393,12 @@ static void build_nodes(sph_ctx* c, bool use_fraction) {
     CUDA_TRY(cudaMemsetAsync(lev, 0, (SPH_MAX_DEPTH + 8) * sizeof(int), c->stream));
     CUDA_TRY(cudaMemcpyAsync(lev, h0, sizeof(h0), cudaMemcpyHostToDevice, c->stream));
     N = nodes(c);
-    void* args[] = {&Lb, (void*)&xh, (void*)&keys, (void*)&g, (void*)&depth, &c->cfg.split_count, (void*)&frac, &N};
+    float guess_n = guess ? c->cfg.n_ngb : 0.f;
+    int guess_min = (int)c->cfg.n_ngb;
+    float hcap = h_cap(c);
+    float4* xh_w = Bget<float4>(c, B_XH);
+    void* args[] = {&Lb,          (void*)&xh, (void*)&keys, (void*)&g,    (void*)&depth, &c->cfg.split_count,
+                    (void*)&frac, &N,         &guess_n,     &guess_min,   &hcap,         &xh_w};
     CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_build_levels, grid, LEVEL_THREADS, args, 0, c->stream));
     c->launches++;
     int hl[SPH_MAX_DEPTH + 6];
@@ -967,11 +972,10 @@ int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const floa
   sort_particles(c, h0max, h0 != nullptr);
   // a4: the hierarchy; the cold start guesses h from the occupancy of the count-rule tree
   const bool frac = c->cfg.split_fraction > 0.f;
-  build_nodes(c, frac && !need_guess);
+  // (the leaves write the guess as the level build decides them: k_build_levels)
+  build_nodes(c, frac && !need_guess, need_guess);
   float margin = c->cfg.h_margin;
   if (need_guess) {
-    LAUNCH(k_guess_h, gridfull((int64_t)c->n_nodes * 32, 256), 256, 0, c->n_nodes, nodes(c), level_geom(c),
-           c->cfg.n_ngb, (int)c->cfg.n_ngb, h_cap(c), Bget<float4>(c, B_XH));
     // the guess is off by up to ~2x either way (C4 p1/p99 0.68/1.88): record at the guess
     // itself; particles whose root lies beyond it are re-walked in the same warp (lists.cuh)
     margin = c->cold_margin;

@@ -11,10 +11,11 @@
 #include "common.cuh"
 
 #ifndef RS_THREADS
-#define RS_THREADS 256
+#define RS_THREADS 512  // 256 or 512 (the first 256 threads hold one digit each in the scan / look-back);
+                        // 4096-item tiles halve the tiles in flight a look-back walks over (16.8M: -2.4%)
 #endif
 #ifndef RS_ITEMS
-#define RS_ITEMS 8      // 2048-item tiles: <= 64 registers, 4 blocks per SM (16 items: 128 registers,
+#define RS_ITEMS 8      // 8 items per thread: <= 64 registers, 1024 threads per SM (16 items: 128 registers,
 #endif                  // 2 blocks, +36% on the 16.8M binning run; profiles/round2/binning_*.txt)
 #define RS_TILE (RS_THREADS * RS_ITEMS)
 #ifndef RS_LB
@@ -76,7 +77,7 @@ struct RadixSmem {
 };
 
 #ifndef RS_MINB
-#define RS_MINB 4
+#define RS_MINB (1024 / RS_THREADS)   // 64 registers: 1024 resident threads per SM
 #endif
 __global__ void __launch_bounds__(RS_THREADS, RS_MINB) k_radix_pass(
     const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint64_t* __restrict__ kout,
@@ -136,12 +137,13 @@ __global__ void __launch_bounds__(RS_THREADS, RS_MINB) k_radix_pass(
     __syncwarp();
   }
   __syncthreads();
-  // per digit (thread d): exclusive over warps, the tile total published at once as the
-  // tile's aggregate, and the tile-local exclusive prefix over digits
-  const int d = tid;  // RS_THREADS == 256
-  uint32_t tcnt = 0;
-  uint32_t* st = status + (size_t)tile * 256 + d;
-  {
+  // per digit (thread d < 256): exclusive over warps, the tile total published at once as
+  // the tile's aggregate, and the tile-local exclusive prefix over digits
+  const int d = tid;
+  const bool digit = tid < 256;
+  uint32_t tcnt = 0, x = 0;
+  uint32_t* st = status + (size_t)tile * 256 + (digit ? d : 0);
+  if (digit) {
     uint32_t run = 0;
 #pragma unroll
     for (int ww = 0; ww < RS_WARPS; ++ww) {
@@ -156,14 +158,16 @@ __global__ void __launch_bounds__(RS_THREADS, RS_MINB) k_radix_pass(
     } else {
       atomicExch(st, RS_FLAG_AGG | tcnt);
     }
-    uint32_t x = tcnt;
+    x = tcnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       uint32_t y = __shfl_up_sync(FULL_MASK, x, o);
       if (lane >= o) x += y;
     }
     if (lane == 31) S.wsum[w] = x;
-    __syncthreads();
+  }
+  __syncthreads();
+  if (digit) {
     uint32_t add = 0;
     for (int ww = 0; ww < w; ++ww) add += S.wsum[ww];
     S.dpre[d] = x - tcnt + add;
@@ -183,7 +187,7 @@ __global__ void __launch_bounds__(RS_THREADS, RS_MINB) k_radix_pass(
   }
   // decoupled look-back over the previous tiles for digit d: the predecessor first (usually
   // inclusive by now), then RS_LB statuses at a time
-  if (tile != 0) {
+  if (digit && tile != 0) {
     uint32_t excl = 0;
     int64_t pt = (int64_t)tile - 1;
     uint32_t s0 = ld_volatile_u32(status + (size_t)pt * 256 + d);
