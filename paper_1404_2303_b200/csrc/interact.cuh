@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FORCE_MINB) k_force(GroupLis
   __shared__ float4 sc[FORCE_WARPS][32 * FORCE_ST];   // A~_j, rho_j, c_j, f_j
   __shared__ int sj[FORCE_WARPS][32 * FORCE_ST];
   __shared__ int sself[FORCE_WARPS][32];   // per target lane: its own particle's staged slot, or -1
-  __shared__ __align__(8) float sxyzw[FORCE_WARPS][4][32 * FORCE_ST];   // x, y, z, 1/h (SoA, packed tests)
+  __shared__ __align__(8) float sxyzw[FORCE_WARPS][4][32 * FORCE_ST];   // x, y, z, 1/h^2 (SoA, packed tests)
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int gid = blockIdx.x * FORCE_WARPS + wib;
   if (gid >= G.ngroups) return;
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FORCE_MINB) k_force(GroupLis
       sxyzw[wib][0][32 * k + lane] = a.x;
       sxyzw[wib][1][32 * k + lane] = a.y;
       sxyzw[wib][2][32 * k + lane] = a.z;
-      sxyzw[wib][3][32 * k + lane] = a.w;
+      sxyzw[wib][3][32 * k + lane] = a.w * a.w;   // 1/h_j^2: the same product the hit body forms
       SB[32 * k + lane] = b;
       SC[32 * k + lane] = c;
       SJ[32 * k + lane] = jj;
@@ -391,9 +391,9 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FORCE_MINB) k_force(GroupLis
 #pragma unroll 8
       for (int t = 0; t < 16; ++t) {
         const float2 r2 = r2_pair(xi, yi, zi, X2[t], Y2[t], Z2[t]);
-        const float2 hw = W2[t];
-        const bool a0 = r2.x < hi2 || r2.x * (hw.x * hw.x) < 1.0f;
-        const bool a1 = r2.y < hi2 || r2.y * (hw.y * hw.y) < 1.0f;
+        const float2 hw2 = W2[t];
+        const bool a0 = r2.x < hi2 || r2.x * hw2.x < 1.0f;
+        const bool a1 = r2.y < hi2 || r2.y * hw2.y < 1.0f;
         m |= ((unsigned)a0 | ((unsigned)a1 << 1)) << (2 * t);
       }
       hm[k] = act ? m : 0u;
@@ -602,9 +602,9 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FORCE_MINB)
 #pragma unroll 8
       for (int t = 0; t < 16; ++t) {
         const float2 r2 = r2_pair(xi, yi, zi, X2[t], Y2[t], Z2[t]);
-        const float2 hw = W2[t];
-        const bool a0 = r2.x < hi2 || r2.x * (hw.x * hw.x) < 1.0f;
-        const bool a1 = r2.y < hi2 || r2.y * (hw.y * hw.y) < 1.0f;
+        const float2 hw2 = W2[t];
+        const bool a0 = r2.x < hi2 || r2.x * hw2.x < 1.0f;
+        const bool a1 = r2.y < hi2 || r2.y * hw2.y < 1.0f;
         hm |= ((unsigned)a0 | ((unsigned)a1 << 1)) << (2 * t);
       }
       hm = act ? hm : 0u;
