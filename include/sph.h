@@ -226,6 +226,17 @@ int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out,
  * of sph_density / sph_force cover the owned particles only. */
 int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const float* x, const float* h0);
 
+/* One whole evaluation, sph_build_cells(n, x, h0) + sph_density(v, m, u, h_out, rho_out) +
+ * sph_force(a_out, dudt_out), with the host <-> device copies of host arrays overlapped with
+ * the work: v, m, u are copied up on a side stream while the cells and neighbour lists are
+ * built, and h, rho come down on the side stream while the force loop runs (page-locked host
+ * arrays make these copies asynchronous). Same results, statuses and stats as the three calls;
+ * every output is complete on return. st_density / st_force may be NULL. The first call on a
+ * context (or one with a new n) stages v, m, u inside the density call instead. */
+int sph_step(sph_ctx* ctx, int64_t n, const float* x, const float* h0, const float* v, const float* m,
+             const float* u, float* h_out, float* rho_out, float* a_out, float* dudt_out, sph_stats* st_density,
+             sph_stats* st_force);
+
 /* The library's initial guess of h from cell occupancy (the one sph_build_cells uses when
  * h0 is NULL), h_out [n]: N_ngb = (4 pi/3) n h^3 for the local number density n of the
  * smallest cell around the particle holding >= N_ngb particles. Used e.g. to size halos. */

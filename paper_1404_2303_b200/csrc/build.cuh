@@ -195,7 +195,7 @@ __global__ void k_top_counts(int n0, int64_t n, NodeArrays N) {
 // that would exceed the node capacity stops the loop (status[1] = 1: the host grows the
 // arrays and runs it again).
 struct LevelBuild {
-  int* lev_off;      // [SPH_MAX_DEPTH + 4]: level offsets; [0], [1] set by the host
+  int* lev_off;      // [SPH_MAX_DEPTH + 4]: level offsets (zeroed by the host; [1] = n0 written here)
   int* status;       // [0] levels processed, [1] 1 = node capacity exceeded, 2 = barrier timeout
   unsigned* bar;     // grid barrier: arrivals, generation (zeroed before the launch)
   int* part;         // [gridDim.x] block sums
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(LEVEL_THREADS) k_build_levels(LevelBuild L, co
                                                                 const uint64_t* __restrict__ keys, LevelGeom g,
                                                                 int depth, int split_count, float split_frac,
                                                                 NodeArrays N, float guess_n, int guess_min,
-                                                                float hcap, float4* xh_w) {
+                                                                float hcap, float4* xh_w, int n0) {
   __shared__ int red[LEVEL_THREADS / 32];
   __shared__ int wsc[LEVEL_THREADS / 32];
   const int lane = threadIdx.x & 31;
@@ -266,7 +266,8 @@ __global__ void __launch_bounds__(LEVEL_THREADS) k_build_levels(LevelBuild L, co
   const int nwarps = (int)(gridDim.x * (blockDim.x >> 5));
   volatile int* lev = L.lev_off;
   for (int l = 0;; ++l) {
-    const int a = lev[l], b = lev[l + 1];
+    // level 0 (the top cells, 0..n0) from the argument: lev[] is written only under barriers
+    const int a = l == 0 ? 0 : lev[l], b = l == 0 ? n0 : lev[l + 1];
     const float half_edge = 0.5f * fminf(g.E[l][0], fminf(g.E[l][1], g.E[l][2]));
     // (A) split decision + octant boundaries, warp per node
     for (int node = a + gw; node < b; node += nwarps) {
@@ -283,26 +284,27 @@ __global__ void __launch_bounds__(LEVEL_THREADS) k_build_levels(LevelBuild L, co
       if (!sp) {
         if (lane == 0) L.nch[node - a] = 0;
         if (guess_n > 0.f) {
-          double dens = 0.0;
+          float dens = 0.f;
           int y = node;
           while (true) {
             const int cy = __ldcg(N.count + y);
             const int ly = __ldcg(N.ijk + y).w;
-            const double vol = (double)g.E[ly][0] * g.E[ly][1] * g.E[ly][2];
-            if (cy >= GUESS_MIN_COUNT) dens = fmax(dens, (double)cy / vol);
+            const float vol = g.E[ly][0] * g.E[ly][1] * g.E[ly][2];
+            if (cy >= GUESS_MIN_COUNT) dens = fmaxf(dens, (float)cy / vol);
             const int py = __ldcg(N.parent + y);
             if (cy >= guess_min || py < 0) {
-              if (dens == 0.0) dens = (double)cy / vol;
+              if (dens == 0.f) dens = (float)cy / vol;
               break;
             }
             y = py;
           }
-          const float hg = fminf((float)cbrt(3.0 * guess_n / (4.0 * 3.14159265358979323846 * dens)), hcap);
+          const float hg = fminf(cbrtf(3.f * guess_n / (4.f * 3.14159265f * dens)), hcap);
           for (int s = first + lane; s < first + cnt; s += 32)
             if (xh_w[s].w == 0.f) xh_w[s].w = hg;
         }
         continue;
       }
+      // octant boundaries: a binary search per octant on the sorted keys (lanes 0..7)
       const int shift = 3 * (depth - l - 1);
       int start = first + cnt;
       if (lane < 8) {
@@ -396,6 +398,7 @@ __global__ void __launch_bounds__(LEVEL_THREADS) k_build_levels(LevelBuild L, co
       carry += ttot;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
+      if (l == 0) L.lev_off[1] = n0;
       L.lev_off[l + 2] = next;
       L.status[0] = l + 1;
     }

@@ -115,6 +115,16 @@ struct DBuf {
 
 struct sph_ctx {
   sph_config cfg;
+  // page-locked scratch for the small device -> host reads (counters, scan totals), so each
+  // is one stream-ordered copy + sync instead of a staged pageable copy
+  unsigned long long* hpin = nullptr;
+  bool ctr_init_ready = false;   // B_CTRINIT holds the counters' initial values
+  // sph_step: v, m, u staged on the side stream before the build (pre_in: the caller's
+  // pointers, pre_dev: their device views), and the density's host outputs copied on the side
+  // stream while the force loop runs (defer_out)
+  const float* pre_in[3] = {nullptr, nullptr, nullptr};
+  const float* pre_dev[3] = {nullptr, nullptr, nullptr};
+  bool pre_pending = false, pre_ready = false, pre_side = false, defer_out = false;
   void* comm = nullptr;   // ncclComm_t of the slab decomposition (sph_comm_init), or null
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -197,8 +207,9 @@ enum BufId {
   // groups and interaction lists
   B_GROUPS, B_GOFF, B_GLEN, B_LIST, B_NBR2, B_NBCNT, B_NBOFF, B_NBOVF, B_OVFIDX, B_NBENT, B_GKEYS, B_GORDER, B_SHRUNK, B_OVFC, B_OVFCNT, B_HCTR, B_RGL, B_RGCNT, B_XREF, B_TGT, B_ACTIVE, B_TSTEP, B_WALKRAW, B_GFLAG, B_GSEL, B_HRCH,
   // misc scratch
-  B_ABLIST, B_WIN, B_PGROUP, B_SYM_IA, B_SYM_IVS, B_SYM_ICNT, B_SYM_JA, B_SYM_JVS, B_SYM_JCNT,
+  B_ABLIST, B_WIN, B_CTRINIT, B_PGROUP, B_SYM_IA, B_SYM_IVS, B_SYM_ICNT, B_SYM_JA, B_SYM_JVS, B_SYM_JCNT,
   B_TMPI0, B_TMPI1, B_TMPL0, B_TMPL1, B_COUNTERS, B_OUT0, B_OUT1, B_OUT2, B_OUT3, B_OUT4, B_OUT5,
+  B_FOUT0, B_FOUT1, B_FOUT2, B_FOUT3,
   B_COUNT
 };
 static_assert(B_COUNT <= 96, "too many buffers");

@@ -583,7 +583,7 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FORCE_MINB)
     sxyzw[wib][0][lane] = a.x;
     sxyzw[wib][1][lane] = a.y;
     sxyzw[wib][2][lane] = a.z;
-    sxyzw[wib][3][lane] = a.w;
+    sxyzw[wib][3][lane] = a.w * a.w;   // 1/h_j^2, as in k_force
     sb[wib][lane] = b;
     sc[wib][lane] = c;
     sj[wib][lane] = jj;

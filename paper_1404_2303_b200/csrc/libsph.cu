@@ -150,14 +150,27 @@ static void phase_reset(sph_ctx* c) {
 
 // =========================================================== counters ===========
 static unsigned long long* ctr(sph_ctx* c) { return B<unsigned long long>(c, B_COUNTERS, C_NCOUNTERS); }
+// a small device -> host read through the context's page-locked scratch (<= 64 words)
+static void read_dev(sph_ctx* c, void* host, const void* dev, size_t bytes) {
+  SPH_REQUIRE(bytes <= 64 * sizeof(unsigned long long), SPH_E_ARG, "read_dev: more than the pinned scratch");
+  CUDA_TRY(cudaMemcpyAsync(c->hpin, dev, bytes, cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  memcpy(host, c->hpin, bytes);
+}
+// counters back to their initial values by a device-to-device copy (a host-to-device copy from
+// pageable memory may wait for the stream)
 static void ctr_reset(sph_ctx* c) {
   static const unsigned long long init[C_NCOUNTERS] = {0, 0, 0, 0, 0, 0, 0, 0x7f800000ull};   // C_HMINBITS = +inf
   static_assert(C_HMINBITS == 7, "counter layout");
-  CUDA_TRY(cudaMemcpyAsync(ctr(c), init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+  unsigned long long* d0 = B<unsigned long long>(c, B_CTRINIT, C_NCOUNTERS);
+  if (!c->ctr_init_ready) {
+    CUDA_TRY(cudaMemcpy(d0, init, sizeof(init), cudaMemcpyHostToDevice));
+    c->ctr_init_ready = true;
+  }
+  CUDA_TRY(cudaMemcpyAsync(ctr(c), d0, sizeof(init), cudaMemcpyDeviceToDevice, c->stream));
 }
 static void ctr_read(sph_ctx* c, unsigned long long* h) {
-  CUDA_TRY(cudaMemcpyAsync(h, ctr(c), sizeof(unsigned long long) * C_NCOUNTERS, cudaMemcpyDeviceToHost, c->stream));
-  sync(c);
+  read_dev(c, h, ctr(c), sizeof(unsigned long long) * C_NCOUNTERS);
 }
 
 // =========================================================== scan ===============
@@ -170,8 +183,7 @@ static T scan_excl(sph_ctx* c, const T* in, T* out, int64_t n) {
   LAUNCH(k_scan_blocksums<T>, 1, SCAN_THREADS, 0, sums, nb, sums + nb);
   LAUNCH(k_scan_final<T>, (int)nb, SCAN_THREADS, 0, in, n, sums, out);
   T total;
-  CUDA_TRY(cudaMemcpyAsync(&total, sums + nb, sizeof(T), cudaMemcpyDeviceToHost, c->stream));
-  sync(c);
+  read_dev(c, &total, sums + nb, sizeof(T));
   return total;
 }
 
@@ -389,21 +401,19 @@ static void build_nodes(sph_ctx* c, bool use_fraction, bool guess = false) {
     Lb.part = part;
     Lb.nch = B<int>(c, B_N_NCH, cap);
     Lb.cap = (int)std::min<int64_t>(cap, INT_MAX);
-    const int h0[2] = {0, n0};
     CUDA_TRY(cudaMemsetAsync(lev, 0, (SPH_MAX_DEPTH + 8) * sizeof(int), c->stream));
-    CUDA_TRY(cudaMemcpyAsync(lev, h0, sizeof(h0), cudaMemcpyHostToDevice, c->stream));
     N = nodes(c);
     float guess_n = guess ? c->cfg.n_ngb : 0.f;
     int guess_min = (int)c->cfg.n_ngb;
     float hcap = h_cap(c);
     float4* xh_w = Bget<float4>(c, B_XH);
-    void* args[] = {&Lb,          (void*)&xh, (void*)&keys, (void*)&g,    (void*)&depth, &c->cfg.split_count,
-                    (void*)&frac, &N,         &guess_n,     &guess_min,   &hcap,         &xh_w};
+    int n0_arg = n0;
+    void* args[] = {&Lb,  (void*)&xh, (void*)&keys, (void*)&g,  (void*)&depth, &c->cfg.split_count, (void*)&frac,
+                    &N,   &guess_n,   &guess_min,   &hcap,      &xh_w,         &n0_arg};
     CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_build_levels, grid, LEVEL_THREADS, args, 0, c->stream));
     c->launches++;
     int hl[SPH_MAX_DEPTH + 6];
-    CUDA_TRY(cudaMemcpyAsync(hl, lev, sizeof(hl), cudaMemcpyDeviceToHost, c->stream));
-    sync(c);
+    read_dev(c, hl, lev, sizeof(hl));
     SPH_REQUIRE(hl[SPH_MAX_DEPTH + 5] != 2, SPH_E_CUDA, "k_build_levels: grid barrier timed out");
     if (hl[SPH_MAX_DEPTH + 5] == 1) {   // node capacity exceeded: grow and run again
       SPH_REQUIRE(attempt < 8, SPH_E_OOM, "node arrays keep overflowing");
@@ -823,6 +833,7 @@ int sph_create(const sph_config* cfg, int dev, void* stream, sph_ctx** out) {
     int ns = 0;
     CUDA_TRY(cudaDeviceGetAttribute(&ns, cudaDevAttrMultiProcessorCount, dev));
     c->num_sms = ns;
+    CUDA_TRY(cudaMallocHost((void**)&c->hpin, 64 * sizeof(unsigned long long)));
     if (stream) {
       c->stream = (cudaStream_t)stream;
     } else {
@@ -851,6 +862,7 @@ int sph_create(const sph_config* cfg, int dev, void* stream, sph_ctx** out) {
     if (cfg->list_cap > 0) c->ucap = cfg->list_cap;
     if (cfg->group_container != 0) c->group_cmax = cfg->group_container < 0 ? 0 : cfg->group_container;
   } catch (const SphError& e) {
+    if (c->hpin) cudaFreeHost(c->hpin);
     delete c;
     return e.status;
   }
@@ -863,6 +875,7 @@ int sph_destroy(sph_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   for (int i = 0; i < B_COUNT; ++i) dev_free(c, c->b[i].p);
+  if (c->hpin) cudaFreeHost(c->hpin);
   if (c->ev_ok) {
     for (int i = 0; i < 12; ++i) cudaEventDestroy(c->ev[i]);
     for (int i = 0; i < 4; ++i) cudaEventDestroy(c->ev_side[i]);
@@ -889,6 +902,8 @@ int sph_set_allocator(sph_ctx* c, void* (*alloc)(size_t, void*, void*), void (*r
   c->uuser = user;
   return SPH_OK;
 }
+
+static bool stage_vmu(sph_ctx* c, const float* v, const float* m, const float* u, const float* dv[3]);
 
 int sph_build_cells(sph_ctx* ctx, int64_t n, const float* x, const float* h0) {
   return sph_build_cells_halo(ctx, n, 0, x, h0);
@@ -968,6 +983,13 @@ int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const floa
   CUDA_TRY(cudaMemsetAsync(B<unsigned long long>(c, B_NBENT, 1), 0, sizeof(unsigned long long), c->stream));
   float h0max = 0.f;
   const bool need_guess = load_inputs(c, x, h0, &h0max);
+  if (c->pre_pending) {   // sph_step: v, m, u up on the side stream behind x, during the build
+    const float* dv[3];
+    c->pre_side = stage_vmu(c, c->pre_in[0], c->pre_in[1], c->pre_in[2], dv);
+    for (int k = 0; k < 3; ++k) c->pre_dev[k] = dv[k];
+    c->pre_pending = false;
+    c->pre_ready = true;
+  }
   // a2 + a3: one sort for the whole evaluation
   sort_particles(c, h0max, h0 != nullptr);
   // a4: the hierarchy; the cold start guesses h from the occupancy of the count-rule tree
@@ -1042,6 +1064,30 @@ static void fill_struct_stats(sph_ctx* c, sph_stats* st) {
   st->n_rebuilds = c->list_rebuilds;
 }
 
+// v, m, u of host arrays copied on the side stream (device arrays used in place): dv = their
+// device views; returns whether a side-stream copy was issued (joined by ev_side[1])
+static bool stage_vmu(sph_ctx* c, const float* v, const float* m, const float* u, const float* dv[3]) {
+  const int64_t n = c->n;
+  const float* in[3] = {v, m, u};
+  const int ids[3] = {B_VIN, B_MIN, B_UIN};
+  const size_t cnt[3] = {(size_t)(3 * n), (size_t)n, (size_t)n};
+  bool side = false;
+  for (int k = 0; k < 3; ++k) {
+    dv[k] = in[k];
+    if (is_device_ptr(in[k])) continue;
+    if (!side) {
+      CUDA_TRY(cudaEventRecord(c->ev_side[0], c->stream));   // staging buffers free to overwrite
+      CUDA_TRY(cudaStreamWaitEvent(c->stream2, c->ev_side[0], 0));
+      side = true;
+    }
+    float* d = B<float>(c, ids[k], cnt[k]);
+    CUDA_TRY(cudaMemcpyAsync(d, in[k], cnt[k] * sizeof(float), cudaMemcpyHostToDevice, c->stream2));
+    dv[k] = d;
+  }
+  if (side) CUDA_TRY(cudaEventRecord(c->ev_side[1], c->stream2));
+  return side;
+}
+
 int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, float* h_out, float* rho_out,
                 float* omega_out, int32_t* n_nbr_out, float* div_out, float* curl_out, sph_stats* st) {
   API_BEGIN(ctx)
@@ -1060,23 +1106,20 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   const float* md = m;
   const float* ud = u;
   bool side = false;
-  {
-    const void* in[3] = {v, m, u};
-    const int ids[3] = {B_VIN, B_MIN, B_UIN};
-    const size_t cnt[3] = {(size_t)(3 * n), (size_t)n, (size_t)n};
-    const float** outp[3] = {&vd, &md, &ud};
-    for (int k = 0; k < 3; ++k) {
-      if (is_device_ptr(in[k])) continue;
-      if (!side) {
-        CUDA_TRY(cudaEventRecord(c->ev_side[0], c->stream));   // staging buffers free to overwrite
-        CUDA_TRY(cudaStreamWaitEvent(c->stream2, c->ev_side[0], 0));
-        side = true;
-      }
-      float* d = B<float>(c, ids[k], cnt[k]);
-      CUDA_TRY(cudaMemcpyAsync(d, in[k], cnt[k] * sizeof(float), cudaMemcpyHostToDevice, c->stream2));
-      *outp[k] = d;
-    }
-    if (side) CUDA_TRY(cudaEventRecord(c->ev_side[1], c->stream2));
+  if (c->pre_ready && c->pre_in[0] == v && c->pre_in[1] == m && c->pre_in[2] == u) {
+    // staged by sph_step before the build
+    vd = c->pre_dev[0];
+    md = c->pre_dev[1];
+    ud = c->pre_dev[2];
+    side = c->pre_side;
+    c->pre_ready = false;
+  } else {
+    c->pre_ready = false;
+    const float* dv[3];
+    side = stage_vmu(c, v, m, u, dv);
+    vd = dv[0];
+    md = dv[1];
+    ud = dv[2];
   }
   unsigned long long hc[C_NCOUNTERS];
 
@@ -1114,8 +1157,7 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   // beyond their list (a fused re-walk + solve) and the pool lists of repeat overflows.
   while (true) {
     unsigned long long hh[HC_N];
-    CUDA_TRY(cudaMemcpyAsync(hh, Bget<unsigned long long>(c, B_HCTR), sizeof(hh), cudaMemcpyDeviceToHost, c->stream));
-    sync(c);
+    read_dev(c, hh, Bget<unsigned long long>(c, B_HCTR), sizeof(hh));
     ++rounds;
     unconv += (long long)hh[HC_UNCONV];   // disjoint per round: an unconverged particle is never re-walked
     itmax = std::max(itmax, (long long)hh[HC_ITMAX]);
@@ -1175,10 +1217,7 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
     LAUNCH(k_validate_pack_vmu, grid1d(c, n, 256), 256, 0, vd, md, ud, n, vmc, ctr(c));
     LAUNCH(k_gather_vmu, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, vmc, ud, vm, uc);
   }
-  ctr_read(c, hc);
-  SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_NONFINITE), SPH_E_DOMAIN, "non-finite velocity");
-  SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_MASS), SPH_E_DOMAIN, "mass <= 0 or non-finite");
-  SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_U), SPH_E_DOMAIN, "internal energy <= 0 or non-finite");
+  // (their error bits are read with the density kernel's counters below: one host round trip)
   // a9 ghost fused into the density kernel: the caller-order outputs and the force state
   std::vector<OutMap> maps;
   GhostOut go;
@@ -1204,7 +1243,6 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   // N(h) re-check: twice the iteration's tolerance plus a few fp32 ulps of h (the bracket
   // stop at fp32 resolution) in N = n_t (h/h)^3
   dout.tol_check = 2.f * (float)c->cfg.n_ngb_tol + 24.f * (float)c->cfg.n_ngb * 1.1920929e-7f;
-  ctr_reset(c);
   CUDA_TRY(cudaEventRecord(c->ev[8], c->stream));
   {
     DbgTimer _t(c, "density kernel");
@@ -1215,12 +1253,26 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
            Bget<uint32_t>(c, B_PERM), Bget<uint8_t>(c, B_TGT), box3(c), dout, ctr(c));
   }
   CUDA_TRY(cudaEventRecord(c->ev[9], c->stream));
-  if (h_early) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_side[3], 0));   // the call ends after the h copy
-  flush_out(c, maps, c->ev[3]);
-  if (h_early) CUDA_TRY(cudaStreamSynchronize(c->stream2));
-  c->state = 2;
+  if (c->defer_out) {
+    // sph_step: the host copies run on the side stream behind the density kernel while the
+    // force loop runs (its staging buffers are others); sph_step joins them at its end
+    CUDA_TRY(cudaEventRecord(c->ev[3], c->stream));
+    CUDA_TRY(cudaStreamWaitEvent(c->stream2, c->ev[3], 0));
+    for (auto& mp : maps)
+      CUDA_TRY(cudaMemcpyAsync(mp.user, mp.dev, mp.bytes, cudaMemcpyDeviceToHost, c->stream2));
+  } else {
+    if (h_early) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_side[3], 0));   // the call ends after the h copy
+    flush_out(c, maps, c->ev[3]);
+    if (h_early) CUDA_TRY(cudaStreamSynchronize(c->stream2));
+  }
   bool noconv = unconv > 0;
   ctr_read(c, hc);
+  if ((hc[C_ERR] & (ERRBIT_NONFINITE | ERRBIT_MASS | ERRBIT_U)) && c->defer_out)
+    cudaStreamSynchronize(c->stream2);   // no copy may outlive the failed call
+  SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_NONFINITE), SPH_E_DOMAIN, "non-finite velocity");
+  SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_MASS), SPH_E_DOMAIN, "mass <= 0 or non-finite");
+  SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_U), SPH_E_DOMAIN, "internal energy <= 0 or non-finite");
+  c->state = 2;
   const long long ndir = (long long)hc[C_NDIR];
   const long long cand = (long long)hc[C_CAND];
   const long long nbord_d = (long long)hc[C_BORDER_D], ncoinc = (long long)hc[C_COINC] / 2;
@@ -1245,7 +1297,7 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   phase_resolve(c);
   {
     unsigned long long ne = 0;
-    CUDA_TRY(cudaMemcpy(&ne, Bget<unsigned long long>(c, B_NBENT), sizeof(ne), cudaMemcpyDeviceToHost));
+    read_dev(c, &ne, Bget<unsigned long long>(c, B_NBENT), sizeof(ne));
     c->nb_entries = (int64_t)ne;
   }
   if (st) {
@@ -1263,7 +1315,7 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
     st->sort_passes = c->sort_passes;
     if (c->cfg.flags & SPH_F_COUNT_CANDIDATES) {
       unsigned long long wr[2];
-      CUDA_TRY(cudaMemcpy(wr, Bget<unsigned long long>(c, B_WALKRAW), sizeof(wr), cudaMemcpyDeviceToHost));
+      read_dev(c, wr, Bget<unsigned long long>(c, B_WALKRAW), sizeof(wr));
       st->n_nb_sources = (int64_t)wr[0];
       st->n_union_sources = (int64_t)wr[1];
     }
@@ -1322,10 +1374,10 @@ int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out, int3
   }
   std::vector<OutMap> maps;
   ForceOut fo;
-  fo.a = dev_out(c, a_out, 3 * no, B_OUT0, maps);
-  fo.dudt = dev_out(c, dudt_out, no, B_OUT1, maps);
-  fo.vsig = dev_out(c, vsig_out, no, B_OUT2, maps);
-  fo.nnbr = dev_out(c, n_nbr_force_out, no, B_OUT3, maps);
+  fo.a = dev_out(c, a_out, 3 * no, B_FOUT0, maps);
+  fo.dudt = dev_out(c, dudt_out, no, B_FOUT1, maps);
+  fo.vsig = dev_out(c, vsig_out, no, B_FOUT2, maps);
+  fo.nnbr = dev_out(c, n_nbr_force_out, no, B_FOUT3, maps);
   fo.perm = Bget<uint32_t>(c, B_PERM);
   fo.n_own = no;
   fo.tgt = Bget<uint8_t>(c, B_TGT);
@@ -1384,6 +1436,45 @@ int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out, int3
   }
   API_END
   return SPH_OK;
+}
+
+// One evaluation with the host <-> device copies overlapped (include/sph.h): v, m, u go up on
+// the side stream while the cells and neighbour lists are built; the density's host outputs
+// come down on the side stream while the force loop runs.
+int sph_step(sph_ctx* ctx, int64_t n, const float* x, const float* h0, const float* v, const float* m,
+             const float* u, float* h_out, float* rho_out, float* a_out, float* dudt_out, sph_stats* st_density,
+             sph_stats* st_force) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(n > 0 && x && v && m && u && h_out && rho_out && a_out && dudt_out, SPH_E_ARG,
+              "required pointer is NULL");
+  SPH_REQUIRE(c->n == 0 || n == c->n, SPH_E_ARG, "n changed between calls");
+  // v, m, u are staged by the build right after it enqueued x (copies queued before x would
+  // delay the build: one copy engine serves both streams in order)
+  c->pre_in[0] = v;
+  c->pre_in[1] = m;
+  c->pre_in[2] = u;
+  c->pre_pending = true;
+  c->pre_ready = false;
+  API_END
+  int rc = sph_build_cells(ctx, n, x, h0);
+  ctx->pre_pending = false;
+  if (rc != SPH_OK) {
+    ctx->pre_ready = false;
+    return rc;
+  }
+  ctx->defer_out = true;
+  const int rd = sph_density(ctx, v, m, u, h_out, rho_out, nullptr, nullptr, nullptr, nullptr, st_density);
+  ctx->defer_out = false;
+  if (rd != SPH_OK && rd != SPH_E_NOCONV) {
+    cudaStreamSynchronize(ctx->stream2);
+    return rd;
+  }
+  const int rf = sph_force(ctx, a_out, dudt_out, nullptr, nullptr, st_force);
+  if (cudaStreamSynchronize(ctx->stream2) != cudaSuccess && rf == SPH_OK) {   // the density's host outputs
+    ctx->err = std::string("sph_step: ") + cudaGetErrorString(cudaGetLastError());
+    return SPH_E_CUDA;
+  }
+  return rf != SPH_OK ? rf : rd;
 }
 
 int sph_guess_h(sph_ctx* ctx, int64_t n, const float* x, float* h_out) {

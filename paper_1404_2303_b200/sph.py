@@ -78,7 +78,7 @@ EXPORTS = ("sph_config_default", "sph_create", "sph_destroy", "sph_set_allocator
            "sph_import_halo_state", "sph_x_histogram", "sph_guess_h", "sph_comm_unique_id", "sph_comm_init",
            "sph_halo_counts", "sph_halo_exchange", "sph_allreduce", "sph_kick", "sph_drift", "sph_timestep", "sph_set_active", "sph_update_cells", "sph_kick_each", "sph_neighbour_min",
            "sph_debug_export", "sph_pair_ablation", "sph_halo_pack", "sph_timebins", "sph_timebins_wake",
-           "sph_x_histogram_weighted", "sph_slab_leavers", "sph_halo_required", "sph_set_halo_width")
+           "sph_x_histogram_weighted", "sph_slab_leavers", "sph_halo_required", "sph_set_halo_width", "sph_step")
 
 
 def load(path: str | None = None):
@@ -115,6 +115,7 @@ def load(path: str | None = None):
     lib.sph_slab_leavers.argtypes = [P, i64, P, ctypes.c_double, ctypes.c_double, P, P, P]
     lib.sph_halo_required.argtypes = [P, P]
     lib.sph_set_halo_width.argtypes = [P, ctypes.c_double]
+    lib.sph_step.argtypes = [P, i64, P, P, P, P, P, P, P, P, P, ctypes.POINTER(Stats), ctypes.POINTER(Stats)]
     lib.sph_comm_unique_id.argtypes = [P]
     lib.sph_comm_init.argtypes = [P, P]
     lib.sph_halo_counts.argtypes = [P, i64, i64, P, P]
@@ -233,6 +234,20 @@ class Context:
         n = int(x.shape[0])
         self._check(self.lib.sph_build_cells(self.h, n, _ptr(x), _ptr(h0)))
         self.n = n
+
+    def step(self, x, v, m, u, h0=None, out=None):
+        """build_cells + density + force in one call (include/sph.h sph_step: the host <-> device
+        copies of host arrays overlap the work). out: dict of preallocated h, rho, a, dudt
+        (host or device, like x). Returns (DensityResult, ForceResult) with those outputs."""
+        n = int(x.shape[0])
+        self.n = n
+        out = out if out is not None else self._alloc_like(v, dict(h=(), rho=(), a=(3,), dudt=()))
+        sd, sf = Stats(), Stats()
+        self._check(self.lib.sph_step(self.h, n, _ptr(x), _ptr(h0), _ptr(v), _ptr(m), _ptr(u), _ptr(out["h"]),
+                                      _ptr(out["rho"]), _ptr(out["a"]), _ptr(out["dudt"]), ctypes.byref(sd),
+                                      ctypes.byref(sf)))
+        return (DensityResult(out["h"], out["rho"], None, None, None, None, sd.as_dict()),
+                ForceResult(out["a"], out["dudt"], None, None, sf.as_dict()))
 
     def update_cells(self, x, h0):
         """New positions and h of the same particles; keeps the cells when they moved little

@@ -346,3 +346,38 @@ def test_node_arrays_grow_inside_the_level_build():
     p.h0[:] = 0.0
     g, _ = _check(p, split_count=4, split_fraction=0.0)
     assert g["stats_density"]["n_cells"] > 6000 // 8 + 1024
+
+
+@pytest.mark.parametrize("where", ["pinned", "pageable", "device"])
+def test_whole_step_call_equals_the_three_calls(where):
+    """sph_step (build + density + force with the host copies overlapped) gives bit-identical
+    h, rho, a, du/dt and the same stats as sph_build_cells + sph_density + sph_force, for host
+    (page-locked or pageable) and device arrays, on repeated steps of one context."""
+    import torch
+
+    import paper_1404_2303_b200 as sph
+    p = workloads.c1()
+    n = p.n
+    dev = torch.device("cuda:0")
+    if where == "device":
+        mk = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+        out = lambda *s: torch.empty(*s, device=dev)
+    else:
+        mk = lambda a: (torch.from_numpy(np.ascontiguousarray(a)).pin_memory() if where == "pinned"
+                        else torch.from_numpy(np.ascontiguousarray(a).copy()))
+        out = lambda *s: torch.empty(*s).pin_memory() if where == "pinned" else torch.empty(*s)
+    x, v, m, u = mk(p.x), mk(p.v), mk(p.m), mk(p.u)
+    ctx = sph.Context(sph.default_config(p.box, n_ngb_tol=1e-4, **BENCH_CFG))
+    ctx.build_cells(x)
+    d0 = ctx.density(v, m, u)
+    f0 = ctx.force(v)
+    ref = {k: getattr(d0, k).cpu().clone() for k in ("h", "rho")}
+    ref.update({k: getattr(f0, k).cpu().clone() for k in ("a", "dudt")})
+    for _ in range(2):
+        o = dict(h=out(n), rho=out(n), a=out(n, 3), dudt=out(n))
+        d, f = ctx.step(x, v, m, u, out=o)
+        for k in ("h", "rho", "a", "dudt"):
+            assert torch.equal(o[k].cpu(), ref[k]), k
+        assert d.stats["n_directed"] == d0.stats["n_directed"]
+        assert f.stats["n_pairs"] == f0.stats["n_pairs"]
+    ctx.close()
