@@ -286,7 +286,7 @@ def issue_from_profiles(kernel: str, ms: float):
         return None
     ach = inst / (ms * 1e6)
     return {"warp_inst_per_launch": inst, "achieved_ginst_s": ach, "peak_ginst_s": ISSUE_PEAK_GINST,
-            "frac": ach / ISSUE_PEAK_GINST, "source": "profiles/issue.json (ncu executed instructions, v18)"}
+            "frac": ach / ISSUE_PEAK_GINST, "source": "profiles/issue.json (ncu executed instructions, round-2 final code)"}
 
 
 def run_sph(args, rank, world, local_rank):
