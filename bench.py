@@ -64,8 +64,9 @@ def parse():
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--cpu-frac", type=float, default=0.02, help="cpu_baseline: fraction of the particles timed as targets")
     ap.add_argument("--scale-config", default="C5", help="N > 1 workload: C5 (strong scaling) or C4xN (weak)")
-    ap.add_argument("--transport", default="torch", choices=["torch", "libsph"],
-                    help="N > 1 halo exchange: torch.distributed P2P or libsph's NCCL communicator")
+    ap.add_argument("--transport", default="torch", choices=["torch", "libsph", "peer"],
+                    help="N > 1 halo exchange: torch.distributed P2P, libsph's NCCL communicator, or peer "
+                         "stores (the pack kernels write into the neighbours' CUDA IPC buffers)")
     return ap.parse_args()
 
 
@@ -541,10 +542,15 @@ def run_slab(args, rank, world, local_rank):
                              halo_width=width)
     ctx = sph.Context(cfg, device=local_rank, stream=stream.cuda_stream)
     # halo transport: torch.distributed P2P (NCCL) or libsph's own NCCL communicator
-    tr = slab.LibTransport(ctx, rank, world) if args.transport == "libsph" else slab.DistTransport(rank, world)
+    if args.transport == "peer":
+        tr = slab.PeerTransport(ctx, rank, world, cap_rows=len(own))
+    else:
+        tr = slab.LibTransport(ctx, rank, world) if args.transport == "libsph" else slab.DistTransport(rank, world)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     def step(inputs):
+        if args.transport == "peer":
+            return slab.evaluate_rank_peer(ctx, *inputs, lo, hi, width, tr)
         return slab.evaluate_rank(ctx, *inputs, lo, hi, width, tr)
 
     for _ in range(args.warmup):

@@ -311,6 +311,28 @@ int sph_slab_leavers(sph_ctx* ctx, int64_t n, const float* x, double lo, double 
  * sends the missing band [width, h_max) of its faces and evaluates again (slab.py). */
 int sph_halo_required(sph_ctx* ctx, double* h_max);
 
+/* ---- CUDA IPC for the peer-store halo (NEXT-f3: the pack kernel of one rank writes its rows
+ * straight into the neighbour's receive buffer over NVLink, P:1107-1146's communication
+ * without a separate send; slab.py PeerTransport). Handles are 64 opaque bytes the caller
+ * hands to the other process with any host transport. Everything created or opened here is
+ * released by sph_destroy. */
+
+/* A device buffer of `bytes` other processes can open (cudaMalloc'd on its own); *dev_ptr
+ * is its address here, handle[64] its IPC handle. */
+int sph_ipc_alloc(sph_ctx* ctx, int64_t bytes, void** dev_ptr, uint8_t* handle);
+/* Map another process's sph_ipc_alloc buffer (peer access enabled lazily): *dev_ptr. Device
+ * kernels of this context (sph_halo_pack, sph_export_state) may then write into it. */
+int sph_ipc_open(sph_ctx* ctx, const uint8_t* handle, void** dev_ptr);
+/* An interprocess event (no timing): *id for record / wait, handle[64] for the other side. */
+int sph_ipc_event_create(sph_ctx* ctx, int32_t* id, uint8_t* handle);
+/* Open another process's event: *id. */
+int sph_ipc_event_open(sph_ctx* ctx, const uint8_t* handle, int32_t* id);
+/* Record event id on the context's stream / make the stream wait for its last record (the
+ * caller orders record before wait across processes, e.g. by a host message sent after the
+ * record). */
+int sph_ipc_event_record(sph_ctx* ctx, int32_t id);
+int sph_ipc_event_wait(sph_ctx* ctx, int32_t id);
+
 /* Replace cfg.halo_width (after the band of a wider halo was received). width >= 0. */
 int sph_set_halo_width(sph_ctx* ctx, double width);
 

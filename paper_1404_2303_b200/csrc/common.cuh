@@ -125,6 +125,10 @@ struct sph_ctx {
   const float* pre_in[3] = {nullptr, nullptr, nullptr};
   const float* pre_dev[3] = {nullptr, nullptr, nullptr};
   bool pre_pending = false, pre_ready = false, pre_side = false, defer_out = false;
+  // CUDA IPC (peer-store halo): buffers this context exposes, buffers of other processes it
+  // opened, and interprocess events (created here or opened from a handle)
+  std::vector<void*> ipc_own, ipc_open;
+  std::vector<cudaEvent_t> ipc_ev;
   void* comm = nullptr;   // ncclComm_t of the slab decomposition (sph_comm_init), or null
   int device = 0;
   cudaStream_t stream = nullptr;

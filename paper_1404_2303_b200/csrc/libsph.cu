@@ -876,6 +876,9 @@ int sph_destroy(sph_ctx* c) {
   cudaStreamSynchronize(c->stream);
   for (int i = 0; i < B_COUNT; ++i) dev_free(c, c->b[i].p);
   if (c->hpin) cudaFreeHost(c->hpin);
+  for (void* p : c->ipc_open) cudaIpcCloseMemHandle(p);
+  for (void* p : c->ipc_own) cudaFree(p);
+  for (cudaEvent_t e : c->ipc_ev) cudaEventDestroy(e);
   if (c->ev_ok) {
     for (int i = 0; i < 12; ++i) cudaEventDestroy(c->ev[i]);
     for (int i = 0; i < 4; ++i) cudaEventDestroy(c->ev_side[i]);
@@ -1523,6 +1526,79 @@ int sph_slab_leavers(sph_ctx* ctx, int64_t n, const float* x, double lo, double 
     return SPH_OK;
   }
   face_select(c, n, x, lo, hi, 0.0, idx_lo_out, idx_hi_out, counts_out);
+  API_END
+  return SPH_OK;
+}
+
+// ------------------------------------------------------------------ CUDA IPC (peer stores) -----
+int sph_ipc_alloc(sph_ctx* ctx, int64_t bytes, void** dev_ptr, uint8_t* handle) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(bytes > 0 && dev_ptr && handle, SPH_E_ARG, "bad argument");
+  void* p = nullptr;
+  CUDA_TRY(cudaMalloc(&p, (size_t)bytes));   // its own allocation: the handle names exactly it
+  c->ipc_own.push_back(p);
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, p));
+  static_assert(sizeof(h) == 64, "IPC handle size");
+  memcpy(handle, &h, sizeof(h));
+  *dev_ptr = p;
+  API_END
+  return SPH_OK;
+}
+
+int sph_ipc_open(sph_ctx* ctx, const uint8_t* handle, void** dev_ptr) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(handle && dev_ptr, SPH_E_ARG, "bad argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  void* p = nullptr;
+  CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  c->ipc_open.push_back(p);
+  *dev_ptr = p;
+  API_END
+  return SPH_OK;
+}
+
+int sph_ipc_event_create(sph_ctx* ctx, int32_t* id, uint8_t* handle) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(id && handle, SPH_E_ARG, "bad argument");
+  cudaEvent_t e;
+  CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventInterprocess));
+  c->ipc_ev.push_back(e);
+  cudaIpcEventHandle_t h;
+  CUDA_TRY(cudaIpcGetEventHandle(&h, e));
+  static_assert(sizeof(h) == 64, "IPC event handle size");
+  memcpy(handle, &h, sizeof(h));
+  *id = (int32_t)c->ipc_ev.size() - 1;
+  API_END
+  return SPH_OK;
+}
+
+int sph_ipc_event_open(sph_ctx* ctx, const uint8_t* handle, int32_t* id) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(id && handle, SPH_E_ARG, "bad argument");
+  cudaIpcEventHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  cudaEvent_t e;
+  CUDA_TRY(cudaIpcOpenEventHandle(&e, h));
+  c->ipc_ev.push_back(e);
+  *id = (int32_t)c->ipc_ev.size() - 1;
+  API_END
+  return SPH_OK;
+}
+
+int sph_ipc_event_record(sph_ctx* ctx, int32_t id) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(id >= 0 && id < (int32_t)c->ipc_ev.size(), SPH_E_ARG, "unknown event");
+  CUDA_TRY(cudaEventRecord(c->ipc_ev[id], c->stream));
+  API_END
+  return SPH_OK;
+}
+
+int sph_ipc_event_wait(sph_ctx* ctx, int32_t id) {
+  API_BEGIN(ctx)
+  SPH_REQUIRE(id >= 0 && id < (int32_t)c->ipc_ev.size(), SPH_E_ARG, "unknown event");
+  CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ipc_ev[id], 0));
   API_END
   return SPH_OK;
 }

@@ -200,15 +200,21 @@ class SlabRank:
         self.ctx, self.x, self.v, self.m, self.u, self.h0 = ctx, x, v, m, u, h0
         self.lo, self.hi, self.width, self.world = lo, hi, width, world
         self.n_own = int(x.shape[0])
+        ctx.set_halo_width(float(width))   # a band round of an earlier evaluation may have widened it
 
-    def select(self):
-        """Phase 1: (to lower neighbour, to upper neighbour) packed x, v, m, u, h0."""
+    def select_idx(self):
+        """Phase 1 indices: the owned particles within the halo width of each face."""
         import torch
         self.idx_lo, self.idx_hi = self.ctx.halo_select(self.x, self.lo, self.hi, self.width)
         if self.world == 2 and self.idx_lo.numel() and self.idx_hi.numel():
             # both faces border the same rank: send a particle near both faces only once
             keep = ~torch.isin(self.idx_hi, self.idx_lo)
             self.idx_hi = self.idx_hi[keep].contiguous()
+        return self.idx_lo, self.idx_hi
+
+    def select(self):
+        """Phase 1: (to lower neighbour, to upper neighbour) packed x, v, m, u, h0."""
+        self.select_idx()
         # CUDA: one libsph kernel per face (k_halo_pack); CPU tensors: the gloo tests of the host logic
         return self._pack(self.idx_lo), self._pack(self.idx_hi)
 
@@ -241,6 +247,11 @@ class SlabRank:
     def extend(self, width):
         """The band of the faces between the current halo width and `width`, packed like
         `select` (to lower, to upper); the band rows follow the first ones in the halo order."""
+        b_lo, b_hi = self.extend_idx(width)
+        return self._pack(b_lo), self._pack(b_hi)
+
+    def extend_idx(self, width):
+        """Indices of the band `extend` sends (the halo bookkeeping updated)."""
         import torch
         if not (width <= self.hi - self.lo):
             raise ValueError("an owned h exceeds the slab width (next-nearest slabs would be needed)")
@@ -254,7 +265,7 @@ class SlabRank:
         self.idx_hi = torch.cat([self.idx_hi, b_hi])
         self.width = float(width)
         self.ctx.set_halo_width(self.width)
-        return self._pack(b_lo), self._pack(b_hi)
+        return b_lo, b_hi
 
     def _pack(self, idx):
         if self.x.is_cuda:
@@ -300,6 +311,125 @@ def evaluate_rank(ctx, x, v, m, u, h0, lo, hi, width, transport):
         raise RuntimeError("halo band rounds did not converge")
     e_lo, e_hi = r.export()
     return r.force(*transport.exchange(e_lo, e_hi))
+
+
+class PeerTransport:
+    """The ring's halo rows by peer stores (NEXT-f3; the paper's per-cell messages without a
+    separate send): every rank exposes two receive buffers through CUDA IPC (rows
+    from its lower and from its upper neighbour), and each neighbour's libsph pack kernel
+    (sph_halo_pack / sph_export_state) writes its rows straight into them, over NVLink between
+    GPUs. torch.distributed carries the handles once and, per exchange, the row counts and a
+    notification; these host messages also order the interprocess events: a rank records
+    `consumed` for its receive buffers before it sends the counts of the next exchange, and
+    `written` for a destination before it sends the notification.
+
+    exchange_into(k_lo, k_hi, write_lo, write_hi, cols) -> (rows from lower, rows from upper):
+    write_lo(out) must fill out [k_lo, cols] (device) with the rows for the lower neighbour.
+    The returned views alias the receive buffers until `consumed()`."""
+
+    def __init__(self, ctx, rank: int, world: int, cap_rows: int, group=None):
+        import torch.distributed as dist
+        if world < 2:
+            raise ValueError("PeerTransport needs two or more ranks")
+        self.dist, self.ctx, self.rank, self.world, self.group = dist, ctx, rank, world, group
+        self.lower, self.upper = neighbours(rank, world)
+        self.cap = int(cap_rows)
+        nbytes = self.cap * PACK_COLS * 4
+        self.recv_lo, h_rlo = ctx.ipc_alloc(nbytes)     # rows from my lower neighbour
+        self.recv_hi, h_rhi = ctx.ipc_alloc(nbytes)     # rows from my upper neighbour
+        self.ev_w_lo, h_wlo = ctx.ipc_event_create()    # my rows written into my lower's buffer
+        self.ev_w_hi, h_whi = ctx.ipc_event_create()
+        self.ev_c_lo, h_clo = ctx.ipc_event_create()    # my recv_lo consumed
+        self.ev_c_hi, h_chi = ctx.ipc_event_create()
+        info = dict(recv_lo=h_rlo, recv_hi=h_rhi, w_lo=h_wlo, w_hi=h_whi, c_lo=h_clo, c_hi=h_chi)
+        every = [None] * world
+        dist.all_gather_object(every, info, group=group)
+        lo_i, up_i = every[self.lower], every[self.upper]
+        # my rows for the lower neighbour arrive in its "from upper" buffer, and vice versa
+        self.dst_lo = ctx.ipc_open(lo_i["recv_hi"])
+        self.dst_hi = ctx.ipc_open(up_i["recv_lo"])
+        self.ev_dst_lo_free = ctx.ipc_event_open(lo_i["c_hi"])
+        self.ev_dst_hi_free = ctx.ipc_event_open(up_i["c_lo"])
+        self.ev_src_lo_written = ctx.ipc_event_open(lo_i["w_hi"])   # my lower writes my recv_lo
+        self.ev_src_hi_written = ctx.ipc_event_open(up_i["w_lo"])
+
+    def _pair(self, send_hi, send_lo, recv_lo, recv_hi):
+        d = self.dist
+        ops = [d.P2POp(d.isend, send_hi, self.upper, self.group), d.P2POp(d.isend, send_lo, self.lower, self.group),
+               d.P2POp(d.irecv, recv_lo, self.lower, self.group), d.P2POp(d.irecv, recv_hi, self.upper, self.group)]
+        for r in d.batch_isend_irecv(ops):
+            r.wait()
+
+    def _host_tensor(self, vals):
+        import torch
+        dev = "cuda" if self.dist.get_backend(self.group) == "nccl" else "cpu"
+        return torch.tensor(vals, dtype=torch.int64, device=dev)
+
+    def exchange_into(self, k_lo: int, k_hi: int, write_lo, write_hi, cols: int):
+        from .sph import device_view
+        if max(k_lo, k_hi) > self.cap or cols > PACK_COLS:
+            raise ValueError("halo rows exceed the peer buffers")
+        # round 1: counts (each rank recorded `consumed` for its buffers before sending them)
+        s_lo, s_hi = self._host_tensor([k_lo]), self._host_tensor([k_hi])
+        r_lo, r_hi = self._host_tensor([0]), self._host_tensor([0])
+        self._pair(s_hi, s_lo, r_lo, r_hi)
+        m_lo, m_hi = int(r_lo.item()), int(r_hi.item())
+        # the destinations are free once their owners consumed the previous rows
+        self.ctx.ipc_event_wait(self.ev_dst_lo_free)
+        self.ctx.ipc_event_wait(self.ev_dst_hi_free)
+        if k_lo:
+            write_lo(device_view(self.dst_lo, (k_lo, cols)))
+        self.ctx.ipc_event_record(self.ev_w_lo)
+        if k_hi:
+            write_hi(device_view(self.dst_hi, (k_hi, cols)))
+        self.ctx.ipc_event_record(self.ev_w_hi)
+        # round 2: the notification (sent after the records), then wait for the writers
+        z = [self._host_tensor([1]) for _ in range(4)]
+        self._pair(z[0], z[1], z[2], z[3])
+        self.ctx.ipc_event_wait(self.ev_src_lo_written)
+        self.ctx.ipc_event_wait(self.ev_src_hi_written)
+        return device_view(self.recv_lo, (m_lo, cols)), device_view(self.recv_hi, (m_hi, cols))
+
+    def consumed(self):
+        """The receive buffers' rows are used (stream-ordered): the neighbours may overwrite them."""
+        self.ctx.ipc_event_record(self.ev_c_lo)
+        self.ctx.ipc_event_record(self.ev_c_hi)
+
+    def allreduce_max(self, value: float) -> float:
+        import torch
+        t = torch.tensor([value], dtype=torch.float64)
+        if self.dist.get_backend(self.group) == "nccl":
+            t = t.cuda()
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())
+
+
+def evaluate_rank_peer(ctx, x, v, m, u, h0, lo, hi, width, transport: PeerTransport):
+    """evaluate_rank with both halo exchanges (and any band re-send) as peer stores: the pack
+    kernels write into the neighbours' buffers; the received rows are copied out once (the
+    band rounds need them again) and the buffers released."""
+    import torch
+    r = SlabRank(ctx, x, v, m, u, h0, lo, hi, width, transport.world)
+    pk = lambda idx: (lambda out: ctx.halo_pack(x, v, m, u, h0, idx, out=out))
+    i_lo, i_hi = r.select_idx()
+    g_lo, g_hi = transport.exchange_into(int(i_lo.numel()), int(i_hi.numel()), pk(i_lo), pk(i_hi), PACK_COLS)
+    got_lo, got_hi = g_lo.clone(), g_hi.clone()
+    transport.consumed()
+    for _ in range(MAX_BAND_ROUNDS + 1):
+        need = transport.allreduce_max(r.density(got_lo, got_hi))
+        if not need > r.width:
+            break
+        b_lo, b_hi = r.extend_idx(_grow(need))
+        e_lo, e_hi = transport.exchange_into(int(b_lo.numel()), int(b_hi.numel()), pk(b_lo), pk(b_hi), PACK_COLS)
+        got_lo, got_hi = torch.cat([got_lo, e_lo]), torch.cat([got_hi, e_hi])
+        transport.consumed()
+    else:
+        raise RuntimeError("halo band rounds did not converge")
+    ex = lambda idx: (lambda out: ctx.export_state(idx, out=out))
+    s_lo, s_hi = transport.exchange_into(int(r.idx_lo.numel()), int(r.idx_hi.numel()), ex(r.idx_lo), ex(r.idx_hi), 5)
+    res = r.force(s_lo, s_hi)
+    transport.consumed()
+    return res
 
 
 def evaluate_ring_sequential(ranks):

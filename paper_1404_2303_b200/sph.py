@@ -78,7 +78,9 @@ EXPORTS = ("sph_config_default", "sph_create", "sph_destroy", "sph_set_allocator
            "sph_import_halo_state", "sph_x_histogram", "sph_guess_h", "sph_comm_unique_id", "sph_comm_init",
            "sph_halo_counts", "sph_halo_exchange", "sph_allreduce", "sph_kick", "sph_drift", "sph_timestep", "sph_set_active", "sph_update_cells", "sph_kick_each", "sph_neighbour_min",
            "sph_debug_export", "sph_pair_ablation", "sph_halo_pack", "sph_timebins", "sph_timebins_wake",
-           "sph_x_histogram_weighted", "sph_slab_leavers", "sph_halo_required", "sph_set_halo_width", "sph_step")
+           "sph_x_histogram_weighted", "sph_slab_leavers", "sph_halo_required", "sph_set_halo_width", "sph_step",
+           "sph_ipc_alloc", "sph_ipc_open", "sph_ipc_event_create", "sph_ipc_event_open", "sph_ipc_event_record",
+           "sph_ipc_event_wait")
 
 
 def load(path: str | None = None):
@@ -115,6 +117,12 @@ def load(path: str | None = None):
     lib.sph_slab_leavers.argtypes = [P, i64, P, ctypes.c_double, ctypes.c_double, P, P, P]
     lib.sph_halo_required.argtypes = [P, P]
     lib.sph_set_halo_width.argtypes = [P, ctypes.c_double]
+    lib.sph_ipc_alloc.argtypes = [P, i64, ctypes.POINTER(ctypes.c_void_p), P]
+    lib.sph_ipc_open.argtypes = [P, P, ctypes.POINTER(ctypes.c_void_p)]
+    lib.sph_ipc_event_create.argtypes = [P, ctypes.POINTER(ctypes.c_int32), P]
+    lib.sph_ipc_event_open.argtypes = [P, P, ctypes.POINTER(ctypes.c_int32)]
+    lib.sph_ipc_event_record.argtypes = [P, ctypes.c_int32]
+    lib.sph_ipc_event_wait.argtypes = [P, ctypes.c_int32]
     lib.sph_step.argtypes = [P, i64, P, P, P, P, P, P, P, P, P, ctypes.POINTER(Stats), ctypes.POINTER(Stats)]
     lib.sph_comm_unique_id.argtypes = [P]
     lib.sph_comm_init.argtypes = [P, P]
@@ -284,6 +292,36 @@ class Context:
                                               _ptr(ilo, np.int32), _ptr(ihi, np.int32), cnt.ctypes.data))
         return ilo[: int(cnt[0])], ihi[: int(cnt[1])]
 
+    # -- CUDA IPC (peer-store halo, include/sph.h sph_ipc_*) ---------------------------
+    def ipc_alloc(self, nbytes):
+        """(device address, 64-byte handle) of a new buffer other processes can open."""
+        p = ctypes.c_void_p()
+        h = ctypes.create_string_buffer(64)
+        self._check(self.lib.sph_ipc_alloc(self.h, int(nbytes), ctypes.byref(p), h))
+        return int(p.value), bytes(h.raw)
+
+    def ipc_open(self, handle: bytes):
+        p = ctypes.c_void_p()
+        self._check(self.lib.sph_ipc_open(self.h, ctypes.create_string_buffer(handle, 64), ctypes.byref(p)))
+        return int(p.value)
+
+    def ipc_event_create(self):
+        i = ctypes.c_int32()
+        h = ctypes.create_string_buffer(64)
+        self._check(self.lib.sph_ipc_event_create(self.h, ctypes.byref(i), h))
+        return int(i.value), bytes(h.raw)
+
+    def ipc_event_open(self, handle: bytes):
+        i = ctypes.c_int32()
+        self._check(self.lib.sph_ipc_event_open(self.h, ctypes.create_string_buffer(handle, 64), ctypes.byref(i)))
+        return int(i.value)
+
+    def ipc_event_record(self, eid: int):
+        self._check(self.lib.sph_ipc_event_record(self.h, int(eid)))
+
+    def ipc_event_wait(self, eid: int):
+        self._check(self.lib.sph_ipc_event_wait(self.h, int(eid)))
+
     def halo_required(self) -> float:
         """The largest owned h of the last density call (the halo width it needs)."""
         v = ctypes.c_double(0.0)
@@ -303,20 +341,21 @@ class Context:
                                                       int(nbins), _ptr(out, np.int64)))
         return out
 
-    def halo_pack(self, x, v, m, u, h0, idx):
-        """[k, 9] rows {x, v, m, u, h0} of the owned particles idx (device), one libsph kernel."""
+    def halo_pack(self, x, v, m, u, h0, idx, out=None):
+        """[k, 9] rows {x, v, m, u, h0} of the owned particles idx (device), one libsph kernel;
+        out: a preallocated [k, 9] device tensor (e.g. a peer's IPC buffer, `device_view`)."""
         import torch
         k = int(idx.shape[0])
-        out = torch.empty(k, 9, dtype=torch.float32, device=idx.device)
+        out = out if out is not None else torch.empty(k, 9, dtype=torch.float32, device=idx.device)
         if k:
             self._check(self.lib.sph_halo_pack(self.h, _ptr(x), _ptr(v), _ptr(m), _ptr(u), _ptr(h0), k,
                                                _ptr(idx, np.int32), _ptr(out)))
         return out
 
-    def export_state(self, idx):
+    def export_state(self, idx, out=None):
         import torch
         k = int(idx.shape[0])
-        out = torch.empty(k, 5, dtype=torch.float32, device=idx.device)
+        out = out if out is not None else torch.empty(k, 5, dtype=torch.float32, device=idx.device)
         if k:
             self._check(self.lib.sph_export_state(self.h, k, _ptr(idx, np.int32), _ptr(out)))
         return out
@@ -515,3 +554,18 @@ class Context:
                 import torch
                 out[k] = torch.zeros(shape, dtype=torch.int32 if is_int else torch.float32, device=like.device)
         return out
+
+
+class _DevArray:
+    """A raw device address as a CUDA array (__cuda_array_interface__ v3), for zero-copy
+    torch views of IPC buffers."""
+
+    def __init__(self, ptr: int, shape, typestr="<f4"):
+        self.__cuda_array_interface__ = {"data": (int(ptr), False), "shape": tuple(int(s) for s in shape),
+                                         "typestr": typestr, "strides": None, "version": 3}
+
+
+def device_view(ptr: int, shape, device=None):
+    """float32 torch tensor viewing `shape` elements at device address ptr (no copy)."""
+    import torch
+    return torch.as_tensor(_DevArray(ptr, shape), device=device or torch.device("cuda", torch.cuda.current_device()))
