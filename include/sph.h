@@ -231,8 +231,7 @@ int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const floa
  * the work: v, m, u are copied up on a side stream while the cells and neighbour lists are
  * built, and h, rho come down on the side stream while the force loop runs (page-locked host
  * arrays make these copies asynchronous). Same results, statuses and stats as the three calls;
- * every output is complete on return. st_density / st_force may be NULL. The first call on a
- * context (or one with a new n) stages v, m, u inside the density call instead. */
+ * every output is complete on return. st_density / st_force may be NULL. */
 int sph_step(sph_ctx* ctx, int64_t n, const float* x, const float* h0, const float* v, const float* m,
              const float* u, float* h_out, float* rho_out, float* a_out, float* dudt_out, sph_stats* st_density,
              sph_stats* st_force);

@@ -1450,7 +1450,6 @@ int sph_step(sph_ctx* ctx, int64_t n, const float* x, const float* h0, const flo
   API_BEGIN(ctx)
   SPH_REQUIRE(n > 0 && x && v && m && u && h_out && rho_out && a_out && dudt_out, SPH_E_ARG,
               "required pointer is NULL");
-  SPH_REQUIRE(c->n == 0 || n == c->n, SPH_E_ARG, "n changed between calls");
   // v, m, u are staged by the build right after it enqueued x (copies queued before x would
   // delay the build: one copy engine serves both streams in order)
   c->pre_in[0] = v;
