@@ -89,9 +89,30 @@ def main():
         near = dist < h
         return float(h[near].max()) * (1 + 1e-6) if near.any() else 0.0
 
-    def run_partition(name, edges, per_face=False):
+    T = 64   # face tiles per axis for the tile-width halo (tile edge >= the largest h near a face)
+
+    def tile_width(e):
+        """per face tile (y, z): the largest h of a particle within h of cut e in that tile,
+        dilated over the 3 x 3 neighbouring tiles (a pair crosses at most one tile boundary
+        when the tile edge is >= its reach)"""
+        xs = p.x[:, 0].astype(np.float64)
+        dist = np.abs(xs - e)
+        dist = np.minimum(dist, Lx - dist)
+        near = np.nonzero(dist < h)[0]
+        ty = np.minimum((p.x[near, 1] / p.box[1] * T).astype(np.int64), T - 1)
+        tz = np.minimum((p.x[near, 2] / p.box[2] * T).astype(np.int64), T - 1)
+        W = np.zeros((T, T))
+        np.maximum.at(W, (ty, tz), h[near])
+        D = W.copy()
+        for dy in (-1, 0, 1):
+            for dz in (-1, 0, 1):
+                D = np.maximum(D, np.roll(np.roll(W, dy, 0), dz, 1))
+        return D * (1 + 1e-6)
+
+    def run_partition(name, edges, per_face=False, tiles=False):
         width = need_width(edges)
         fw = [face_need(e) for e in edges[:-1]] if per_face else [width] * args.P
+        tw = [tile_width(e) for e in edges[:-1]] if tiles else None
         ranks = []
         for r in range(args.P):
             lo, hi = edges[r], edges[r + 1]
@@ -100,7 +121,14 @@ def main():
             own = np.nonzero((xs >= lo) & (xs < hi))[0]
             dlo = (lo - xs) % Lx                      # distance below the lower face (periodic)
             dhi = (xs - hi) % Lx                      # distance above the upper face
-            halo = np.nonzero(((dlo > 0) & (dlo <= w_lo)) | ((dhi >= 0) & (dhi < w_hi)))[0]
+            if tiles:
+                ty = np.minimum((p.x[:, 1] / p.box[1] * T).astype(np.int64), T - 1)
+                tz = np.minimum((p.x[:, 2] / p.box[2] * T).astype(np.int64), T - 1)
+                wl, wh = tw[r][ty, tz], tw[(r + 1) % args.P][ty, tz]
+                halo = np.nonzero(((dlo > 0) & (dlo <= wl)) | ((dhi >= 0) & (dhi < wh)))[0]
+                w_lo, w_hi = float(tw[r].max()), float(tw[(r + 1) % args.P].max())
+            else:
+                halo = np.nonzero(((dlo > 0) & (dlo <= w_lo)) | ((dhi >= 0) & (dhi < w_hi)))[0]
             halo = np.setdiff1d(halo, own)
             idx = np.concatenate([own, halo])
             # the libsph check takes one width: the wider face's (the narrower face's halo is
@@ -134,6 +162,7 @@ def main():
     edges_n = slab.slab_cuts(hist_n, 0.0, Lx, args.P)
     run_partition("count", edges_n)
     run_partition("count, per-face width", edges_n, per_face=True)
+    run_partition(f"count, {T}x{T} face-tile widths", edges_n, tiles=True)
     for fixed in args.fixed:
         w = (nn + nf + fixed).astype(np.float64)
         b = np.clip(np.floor(p.x[:, 0].astype(np.float64) / Lx * 8192).astype(np.int64), 0, 8191)
