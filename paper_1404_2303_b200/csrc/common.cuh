@@ -191,7 +191,8 @@ struct sph_ctx {
   DBuf b[96];
   cudaEvent_t ev[12];
   cudaStream_t stream2 = nullptr;   // side stream: host->device copies overlapped with the h iteration
-  cudaEvent_t ev_side[4];   // [0] side stream may start, [1] v, m, u copied, [2] h ready, [3] h copied back
+  cudaEvent_t ev_side[6];   // [0] side stream may start, [1] v, m, u copied, [2] h ready, [3] h copied back,
+                            // [4] v, m, u may be read, [5] v, m, u checked and in cell order
   bool ev_ok = false;
 };
 
@@ -211,7 +212,7 @@ enum BufId {
   // groups and interaction lists
   B_GROUPS, B_GOFF, B_GLEN, B_LIST, B_NBR2, B_NBCNT, B_NBOFF, B_NBOVF, B_OVFIDX, B_NBENT, B_GKEYS, B_GORDER, B_SHRUNK, B_OVFC, B_OVFCNT, B_HCTR, B_RGL, B_RGCNT, B_XREF, B_TGT, B_ACTIVE, B_TSTEP, B_WALKRAW, B_GFLAG, B_GSEL, B_HRCH,
   // misc scratch
-  B_ABLIST, B_WIN, B_CTRINIT, B_PGROUP, B_SYM_IA, B_SYM_IVS, B_SYM_ICNT, B_SYM_JA, B_SYM_JVS, B_SYM_JCNT,
+  B_ABLIST, B_WIN, B_CTRINIT, B_VERR, B_PGROUP, B_SYM_IA, B_SYM_IVS, B_SYM_ICNT, B_SYM_JA, B_SYM_JVS, B_SYM_JCNT,
   B_TMPI0, B_TMPI1, B_TMPL0, B_TMPL1, B_COUNTERS, B_OUT0, B_OUT1, B_OUT2, B_OUT3, B_OUT4, B_OUT5,
   B_FOUT0, B_FOUT1, B_FOUT2, B_FOUT3,
   B_COUNT

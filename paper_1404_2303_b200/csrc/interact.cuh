@@ -44,6 +44,12 @@ struct GhostOut {
   int64_t n_own;       // caller indices >= n_own are halo (source-only) particles
   float* h_o;          // caller-order state kept for the force loop: h
   float4* g_o;         //   {A, rho, c, f}
+  // the force loop's cell-order inputs of the targets written here (null: k_gather_force
+  // writes them): fx = {x, y, z, 1/h}, fs = {A (8/pi) h^-4, rho, c, f}, hr = h
+  const float4* xh;
+  float4* fx;
+  float4* fs;
+  float* hr;
 };
 
 struct DensOut {
@@ -60,9 +66,9 @@ struct DensOut {
 };
 
 // a9 for one target from its density sums (k_density's epilogue)
-__device__ __forceinline__ void ghost_one(const GhostOut& out, uint32_t o, float h, float uu, float smf, float smqfp,
-                                          float divs, float crx, float cry, float crz, int cnt, float gamma,
-                                          float beps) {
+__device__ __forceinline__ void ghost_one(const GhostOut& out, uint32_t o, int64_t s, float h, float uu, float smf,
+                                          float smqfp, float divs, float crx, float cry, float crz, int cnt,
+                                          float gamma, float beps) {
   const float hinv = 1.0f / h;
   const float rho = SPH_CNORM * hinv * hinv * hinv * smf;
   const float omega = -smqfp / (3.f * smf);
@@ -78,6 +84,13 @@ __device__ __forceinline__ void ghost_one(const GhostOut& out, uint32_t o, float
   const float fb = cn / (fabsf(div) + cn + beps * c * hinv);
   out.h_o[o] = h;
   out.g_o[o] = make_float4(A, rho, c, fb);
+  if (out.fx) {   // the same arithmetic as k_gather_force
+    const float4 p = out.xh[s];
+    const float h2i = hinv * hinv;
+    out.fx[s] = make_float4(p.x, p.y, p.z, hinv);
+    out.fs[s] = make_float4(A * SPH_CNORM * h2i * h2i, rho, c, fb);
+    out.hr[s] = h;
+  }
   if (out.h) out.h[o] = h;
   out.rho[o] = rho;
   if (out.omega) out.omega[o] = omega;
@@ -232,7 +245,7 @@ __global__ void __launch_bounds__(DENS_WARPS * 32, DENS_MINB) k_density(GroupLis
   long long nd = 0, nbad = 0;
   if (act) {
     if (!NONLY && out.ghost) {
-      ghost_one(out.g, perm[s], hi, out.u[s], smf, smqfp, divs, crx, cry, crz, cnt, out.gamma, out.beps);
+      ghost_one(out.g, perm[s], s, hi, out.u[s], smf, smqfp, divs, crx, cry, crz, cnt, out.gamma, out.beps);
       nd = cnt;
       // the h iteration's convergence, re-checked from this loop's sum at the final h (R4)
       nbad = fabs((32.0 / 3.0) * sf - (double)out.n_t) > (double)out.tol_check ? 1 : 0;

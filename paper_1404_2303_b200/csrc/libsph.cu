@@ -120,7 +120,8 @@ struct DbgTimer {
 struct PhaseTimer {
   sph_ctx* c;
   size_t k;
-  PhaseTimer(sph_ctx* c_, int phase) : c(c_) {
+  cudaStream_t st;
+  PhaseTimer(sph_ctx* c_, int phase, cudaStream_t s = nullptr) : c(c_), st(s ? s : c_->stream) {
     if (c->timed_used == c->timed.size()) {
       sph_ctx::Timed t;
       CUDA_TRY(cudaEventCreate(&t.a));
@@ -129,9 +130,9 @@ struct PhaseTimer {
     }
     k = c->timed_used++;
     c->timed[k].phase = phase;
-    CUDA_TRY(cudaEventRecord(c->timed[k].a, c->stream));
+    CUDA_TRY(cudaEventRecord(c->timed[k].a, st));
   }
-  ~PhaseTimer() { cudaEventRecord(c->timed[k].b, c->stream); }
+  ~PhaseTimer() { cudaEventRecord(c->timed[k].b, st); }
 };
 static void phase_resolve(sph_ctx* c) {
   for (size_t k = 0; k < c->timed_used; ++k) {
@@ -844,7 +845,7 @@ int sph_create(const sph_config* cfg, int dev, void* stream, sph_ctx** out) {
     }
     for (int i = 0; i < 12; ++i) CUDA_TRY(cudaEventCreate(&c->ev[i]));
     CUDA_TRY(cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
-    for (int i = 0; i < 4; ++i) CUDA_TRY(cudaEventCreateWithFlags(&c->ev_side[i], cudaEventDisableTiming));
+    for (int i = 0; i < 6; ++i) CUDA_TRY(cudaEventCreateWithFlags(&c->ev_side[i], cudaEventDisableTiming));
     float dirs[14][3];
     for (int d = 0; d < 13; ++d) {
       const int k = d + 14;
@@ -881,7 +882,7 @@ int sph_destroy(sph_ctx* c) {
   for (cudaEvent_t e : c->ipc_ev) cudaEventDestroy(e);
   if (c->ev_ok) {
     for (int i = 0; i < 12; ++i) cudaEventDestroy(c->ev[i]);
-    for (int i = 0; i < 4; ++i) cudaEventDestroy(c->ev_side[i]);
+    for (int i = 0; i < 6; ++i) cudaEventDestroy(c->ev_side[i]);
     cudaStreamDestroy(c->stream2);
   }
   for (auto& t : c->timed) {
@@ -981,6 +982,9 @@ int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const floa
   }
   c->pool = 0;
   c->list_rebuilds = 0;
+  // side-stream work of an earlier sph_density that returned early must not overlap the
+  // staging buffers this build writes
+  if (c->ev_ok) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_side[5], 0));
   CUDA_TRY(cudaEventRecord(c->ev[0], c->stream));
   phase_reset(c);
   CUDA_TRY(cudaMemsetAsync(B<unsigned long long>(c, B_NBENT, 1), 0, sizeof(unsigned long long), c->stream));
@@ -1124,6 +1128,23 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
     md = dv[1];
     ud = dv[2];
   }
+  // v, m, u checked and gathered into cell order on the side stream (behind their copies),
+  // concurrently with the h rounds and the union walk; joined before the density kernel
+  float4* vm = B<float4>(c, B_VM, n);
+  float* uc = B<float>(c, B_U, n);
+  unsigned long long* verr = B<unsigned long long>(c, B_VERR, C_NCOUNTERS);
+  float4* vmc = B<float4>(c, B_XC, n);   // caller-order {v, m} (the positions' staging is free again)
+  CUDA_TRY(cudaEventRecord(c->ev_side[4], c->stream));   // the caller's device arrays, perm
+  CUDA_TRY(cudaStreamWaitEvent(c->stream2, c->ev_side[4], 0));
+  CUDA_TRY(cudaMemsetAsync(verr, 0, C_NCOUNTERS * sizeof(unsigned long long), c->stream2));
+  {
+    PhaseTimer _p(c, 3, c->stream2);   // the rest of a3 (permute + pack)
+    k_validate_pack_vmu<<<grid1d(c, n, 256), 256, 0, c->stream2>>>(vd, md, ud, n, vmc, verr);
+    k_gather_vmu<<<grid1d(c, n, 256), 256, 0, c->stream2>>>(Bget<uint32_t>(c, B_PERM), n, vmc, ud, vm, uc);
+    CUDA_TRY(cudaGetLastError());
+    c->launches += 2;
+  }
+  CUDA_TRY(cudaEventRecord(c->ev_side[5], c->stream2));
   unsigned long long hc[C_NCOUNTERS];
 
   uint8_t* state = Bget<uint8_t>(c, B_STATE);
@@ -1209,18 +1230,11 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
     CUDA_TRY(cudaMemcpyAsync(h_out, hs, c->n_own * sizeof(float), cudaMemcpyDeviceToHost, c->stream2));
     CUDA_TRY(cudaEventRecord(c->ev_side[3], c->stream2));
   }
-  // join the side-stream copies of v, m, u; validate and gather them into cell order
-  if (side) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_side[1], 0));
+  // join the side stream's v, m, u (checked, in cell order); their error bits are read with
+  // the density kernel's counters below (one host round trip)
+  CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_side[5], 0));
+  (void)side;
   ctr_reset(c);
-  float4* vm = B<float4>(c, B_VM, n);
-  float* uc = B<float>(c, B_U, n);
-  {
-    PhaseTimer _p(c, 3);   // the rest of a3 (permute + pack): v, m, u checked, into cell order
-    float4* vmc = B<float4>(c, B_XC, n);   // caller-order {v, m} (the positions' staging is free again)
-    LAUNCH(k_validate_pack_vmu, grid1d(c, n, 256), 256, 0, vd, md, ud, n, vmc, ctr(c));
-    LAUNCH(k_gather_vmu, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, vmc, ud, vm, uc);
-  }
-  // (their error bits are read with the density kernel's counters below: one host round trip)
   // a9 ghost fused into the density kernel: the caller-order outputs and the force state
   std::vector<OutMap> maps;
   GhostOut go;
@@ -1235,6 +1249,12 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   go.n_own = no;
   go.h_o = B<float>(c, B_HFIN_O, n);
   go.g_o = B<float4>(c, B_GST_O, n);
+  // the targets' force inputs in cell order straight from the epilogue; sph_force gathers
+  // only when other particles (halo, inactive) need theirs
+  go.xh = Bget<float4>(c, B_XH);
+  go.fx = B<float4>(c, B_FX, n);
+  go.fs = B<float4>(c, B_FS, n);
+  go.hr = Bget<float>(c, B_HRCH);
   DensOut dout;
   memset(&dout, 0, sizeof(dout));
   dout.ghost = true;
@@ -1269,7 +1289,13 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
     if (h_early) CUDA_TRY(cudaStreamSynchronize(c->stream2));
   }
   bool noconv = unconv > 0;
-  ctr_read(c, hc);
+  CUDA_TRY(cudaMemcpyAsync(c->hpin, ctr(c), sizeof(unsigned long long) * C_NCOUNTERS, cudaMemcpyDeviceToHost,
+                           c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->hpin + C_NCOUNTERS, verr + C_ERR, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                           c->stream));
+  sync(c);
+  memcpy(hc, c->hpin, sizeof(hc));
+  hc[C_ERR] |= c->hpin[C_NCOUNTERS];
   if ((hc[C_ERR] & (ERRBIT_NONFINITE | ERRBIT_MASS | ERRBIT_U)) && c->defer_out)
     cudaStreamSynchronize(c->stream2);   // no copy may outlive the failed call
   SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_NONFINITE), SPH_E_DOMAIN, "non-finite velocity");
@@ -1352,8 +1378,10 @@ static void prepare_force(sph_ctx* c) {
   float4* fx = B<float4>(c, B_FX, n);
   float4* fs = B<float4>(c, B_FS, n);
   float* hr = Bget<float>(c, B_HRCH);
-  LAUNCH(k_gather_force, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, Bget<float4>(c, B_XH),
-         Bget<float>(c, B_HFIN_O), Bget<float4>(c, B_GST_O), fx, fs, hr);
+  // every particle a target: the density epilogue wrote them all
+  if (c->n != c->n_own || c->has_active)
+    LAUNCH(k_gather_force, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, Bget<float4>(c, B_XH),
+           Bget<float>(c, B_HFIN_O), Bget<float4>(c, B_GST_O), fx, fs, hr);
   if (!c->force_lists) build_union(c, hr);
   c->force_lists = true;
 }
