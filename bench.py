@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--calls", default="step", choices=["step", "three"],
+                    help="one step = sph_step (default) or sph_build_cells + sph_density + sph_force")
     ap.add_argument("--no-warm", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--cpu-frac", type=float, default=0.02, help="cpu_baseline: fraction of the particles timed as targets")
@@ -316,6 +318,9 @@ def run_sph(args, rank, world, local_rank):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     def step(xx, hh, vv, mm, uu, od, of):
+        if args.calls == "step":   # the whole-step call (sph_step): no host round trips between phases
+            d, f = ctx.step(xx, vv, mm, uu, hh, out=dict(h=od["h"], rho=od["rho"], a=of["a"], dudt=of["dudt"]))
+            return d.stats, f.stats
         ctx.build_cells(xx, hh)
         d = ctx.density(vv, mm, uu, out=od)
         f = ctx.force(vv, out=of)
@@ -475,7 +480,8 @@ def run_sph(args, rank, world, local_rank):
                    "N": N, "box": list(p.box), "l2": "flushed (256 MiB write) before every timed step",
                    "parallelism": "replicas" if world > 1 else "single GPU",
                    "split_count": CONFIG_TUNING["split_count"], "split_fraction": CONFIG_TUNING["split_fraction"],
-                   "n_ngb": 48, "n_ngb_tol": cfg.n_ngb_tol},
+                   "n_ngb": 48, "n_ngb_tol": cfg.n_ngb_tol,
+                   "step_call": "sph_step" if args.calls == "step" else "sph_build_cells + sph_density + sph_force"},
         "roofline": dominant,
         "roofline_others": secondary,
         "roofline_binning": roof_bin,
