@@ -253,7 +253,8 @@ __device__ __forceinline__ int block_sum_i(int v, int* red) {
 
 #define LEVEL_THREADS 256
 // guess_n > 0: a cold start; each leaf, once decided, writes the occupancy guess of h (as
-// k_guess_h, n_ngb = guess_n, ancestors up to guess_min particles) into xh_w[].w where 0.
+// k_guess_h, n_ngb = guess_n, ancestors up to |guess_min| particles) into xh_w[].w where 0
+// (guess_min < 0: into every particle's, no h0 was given).
 __global__ void __launch_bounds__(LEVEL_THREADS) k_build_levels(LevelBuild L, const float4* __restrict__ xh,
                                                                 const uint64_t* __restrict__ keys, LevelGeom g,
                                                                 int depth, int split_count, float split_frac,
@@ -292,15 +293,19 @@ __global__ void __launch_bounds__(LEVEL_THREADS) k_build_levels(LevelBuild L, co
             const float vol = g.E[ly][0] * g.E[ly][1] * g.E[ly][2];
             if (cy >= GUESS_MIN_COUNT) dens = fmaxf(dens, (float)cy / vol);
             const int py = __ldcg(N.parent + y);
-            if (cy >= guess_min || py < 0) {
+            if (cy >= abs(guess_min) || py < 0) {
               if (dens == 0.f) dens = (float)cy / vol;
               break;
             }
             y = py;
           }
           const float hg = fminf(cbrtf(3.f * guess_n / (4.f * 3.14159265f * dens)), hcap);
-          for (int s = first + lane; s < first + cnt; s += 32)
-            if (xh_w[s].w == 0.f) xh_w[s].w = hg;
+          if (guess_min < 0) {   // no h0 at all: every particle takes the guess (no read)
+            for (int s = first + lane; s < first + cnt; s += 32) xh_w[s].w = hg;
+          } else {
+            for (int s = first + lane; s < first + cnt; s += 32)
+              if (xh_w[s].w == 0.f) xh_w[s].w = hg;
+          }
         }
         continue;
       }

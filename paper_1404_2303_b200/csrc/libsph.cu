@@ -357,7 +357,7 @@ static void sort_particles(sph_ctx* c, float h0max, bool have_h) {
 // a4: the hierarchy from the sorted keys. Split rule: count > split_count and (rule on)
 // more than split_fraction of the particles have h < edge/2; with
 // use_fraction false the count alone decides (occupancy tree of the cold start).
-static void build_nodes(sph_ctx* c, bool use_fraction, bool guess = false) {
+static void build_nodes(sph_ctx* c, bool use_fraction, bool guess = false, bool guess_all = false) {
   DbgTimer _t(c, "nodes");
   const int64_t n = c->n;
   const uint64_t* keys = Bget<uint64_t>(c, B_KEYS0);
@@ -405,7 +405,7 @@ static void build_nodes(sph_ctx* c, bool use_fraction, bool guess = false) {
     CUDA_TRY(cudaMemsetAsync(lev, 0, (SPH_MAX_DEPTH + 8) * sizeof(int), c->stream));
     N = nodes(c);
     float guess_n = guess ? c->cfg.n_ngb : 0.f;
-    int guess_min = (int)c->cfg.n_ngb;
+    int guess_min = guess_all ? -(int)c->cfg.n_ngb : (int)c->cfg.n_ngb;
     float hcap = h_cap(c);
     float4* xh_w = Bget<float4>(c, B_XH);
     int n0_arg = n0;
@@ -1002,7 +1002,7 @@ int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const floa
   // a4: the hierarchy; the cold start guesses h from the occupancy of the count-rule tree
   const bool frac = c->cfg.split_fraction > 0.f;
   // (the leaves write the guess as the level build decides them: k_build_levels)
-  build_nodes(c, frac && !need_guess, need_guess);
+  build_nodes(c, frac && !need_guess, need_guess, need_guess && h0 == nullptr);
   float margin = c->cfg.h_margin;
   if (need_guess) {
     // the guess is off by up to ~2x either way (C4 p1/p99 0.68/1.88): record at the guess
