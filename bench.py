@@ -64,6 +64,8 @@ def parse():
                     help="one step = sph_step (default) or sph_build_cells + sph_density + sph_force")
     ap.add_argument("--no-warm", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--ref-budget-s", type=float, default=120.0,
+                    help="--impl reference: wall seconds for the warm-up + timed steps together")
     ap.add_argument("--cpu-frac", type=float, default=0.02, help="cpu_baseline: fraction of the particles timed as targets")
     ap.add_argument("--scale-config", default="C5", help="N > 1 workload: C5 (strong scaling) or C4xN (weak)")
     ap.add_argument("--transport", default="torch", choices=["torch", "libsph", "peer"],
@@ -112,27 +114,6 @@ class Clocks:
 
 
 # --------------------------------------------------------------------- oracle ---
-def oracle_sample(budget_s: float):
-    """Time the oracle (as it stands) on a bounded sample of the C4 workload: the same
-    clustered generator (64 clumps, seed 140423034) at a reduced N, full evaluation
-    (h root + density + force). N is chosen from a calibration run to fit budget_s."""
-    import numpy as np
-
-    import oracle
-    import workloads
-
-    def one(n):
-        p = workloads.c4(n=n)
-        t0 = time.perf_counter()
-        out = oracle.evaluate_all(p.x, p.v, p.m, p.u, p.box)
-        return time.perf_counter() - t0, int(out["n_pairs"])
-
-    t_cal, _ = one(8192)
-    n = int(8192 * max(1.0, budget_s / max(t_cal, 1e-3)))
-    n = int(2 ** math.floor(math.log2(max(8192, min(n, 1 << 20)))))
-    return n, one, np
-
-
 # ---- cpu_baseline: the oracle on a seeded 2% subset of the headline input itself ----------
 _G = {}   # inherited by the forked pool workers (x, v, m, box, tree, h and state of all particles)
 
@@ -166,6 +147,77 @@ def _w_force(idx):
     fo = oracle.force_at(g["x"], g["v"], g["m"], g["h"], g["rho"], g["A"], g["c"], g["f"], g["box"], targets=idx,
                          tree=g["tree"])
     return int(fo["n_nbr_force"].sum()), time.perf_counter() - t0
+
+
+def _w_closure(T):
+    """Pool worker of the reference arm: the oracle's full evaluation for targets T of the
+    workload itself, from nothing but positions, velocities, masses and energies. The targets'
+    force sums need h, rho, A, c, f of every force partner j (r < max(h_i, h_j)); a partner
+    by its own h has h_j > r, and h_j <= hb[j] (the bound below), so the closure C = T + every
+    j within h_i or within hb[j] of a target holds them all: the oracle solves h on C, the
+    density and state on the partners, the force on T. Returns (pair interactions: directed
+    density contributions of the partners + directed force pairs of T, seconds)."""
+    import numpy as np
+
+    import oracle
+    import oracle.neighbours as nb
+    from scipy.spatial import cKDTree
+    nb.WORKERS = 1
+    g = _G
+    x, box, n = g["x"], g["box"], g["x"].shape[0]
+    t0 = time.perf_counter()
+    hT = oracle.solve_h(x, box, targets=T, tree=g["tree"])
+    _, j1, _, _ = nb.ball_pairs(x, box, x[T], hT, tree=g["tree"])
+    j2, _, _, _ = nb.ball_pairs(x[T], box, x, g["hb"], tree=cKDTree(x[T], boxsize=box))
+    C = np.union1d(np.union1d(j1, j2), T)
+    h = np.zeros(n)
+    h[C] = oracle.solve_h(x, box, targets=C, tree=g["tree"])
+    _, fj, _, _ = oracle.sph.force_pairs(x, h, box, T, tree=g["tree"])
+    S = np.union1d(fj, T)   # within C: a partner outside it has h = 0 and r >= h_i
+    den = oracle.density_at(x, g["v"], g["m"], h, box, targets=S, tree=g["tree"])
+    st = oracle.particle_state(den["rho"], den["omega"], g["u"][S], h[S], den["div"], den["curl"])
+    rho, A, c, f = np.zeros(n), np.zeros(n), np.zeros(n), np.zeros(n)
+    rho[S], A[S], c[S], f[S] = den["rho"], np.nan_to_num(st["A"]), st["c"], st["f"]
+    fo = oracle.force_at(x, g["v"], g["m"], h, rho, A, c, f, box, targets=T, tree=g["tree"])
+    work = int(den["n_nbr"].sum()) + int(fo["n_nbr_force"].sum())
+    if g.get("keep"):   # tests: the targets' results
+        g["kept"] = dict(h=h[T], rho=rho[T], a=fo["a"], dudt=fo["dudt"])
+    return work, time.perf_counter() - t0
+
+
+def oracle_closure_setup(p):
+    """Untimed setup of the reference arm on the workload itself: the tree and, per particle, an
+    upper bound of its h. N(h) >= (32/3)(1 + 0.25 k) with k the other particles within h/2
+    (f(q) >= 0.25 for q <= 1/2), so N(h) = 48 allows at most 14 of them: h <= 2 d_15, with d_15
+    the distance to the 15th nearest other particle."""
+    import numpy as np
+    from scipy.spatial import cKDTree
+
+    import oracle.neighbours as nb
+    x = p.x.astype(np.float64)
+    box = np.asarray(p.box, np.float64)
+    tree = cKDTree(x, boxsize=box)
+    d, _ = tree.query(x, k=16, workers=-1)
+    hb = 2.0 * d[:, 15] * (1.0 + 1e-9)
+    _G.clear()
+    _G.update(x=x, v=p.v.astype(np.float64), m=p.m.astype(np.float64), u=p.u.astype(np.float64), box=box,
+              tree=tree, hb=hb)
+    return nb
+
+
+def oracle_closure_step(p, k, procs, seed):
+    """One reference step: k seeded targets of the workload, split over a process pool."""
+    import multiprocessing as mp
+
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    T = np.sort(rng.choice(p.n, k, replace=False))
+    chunks = [c for c in np.array_split(T, procs) if c.size]
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(len(chunks)) as pool:
+        res = pool.map(_w_closure, chunks)
+    return time.perf_counter() - t0, sum(r[0] for r in res)
 
 
 def oracle_subset_rate(p, gpu, frac=0.02, procs=None, seed=140423098):
@@ -240,27 +292,65 @@ def cores_used():
         return os.cpu_count()
 
 
+def arm_config(args, p, world, n_ngb_tol):
+    """The `config` object of the bench line: the same for this arm and the reference arm
+    (which evaluates a sample of the same workload)."""
+    import numpy as np
+    cold = not bool(np.any(p.h0 > 0))
+    return {"workload": f"{args.config}: {p.n} particles ({p.name} generator, seeds in workloads/), "
+                        f"cold h0" + (" (library guess)" if cold else ""),
+            "N": p.n, "box": list(p.box), "l2": "flushed (256 MiB write) before every timed step",
+            "parallelism": "replicas" if world > 1 else "single GPU",
+            "split_count": CONFIG_TUNING["split_count"], "split_fraction": CONFIG_TUNING["split_fraction"],
+            "n_ngb": 48, "n_ngb_tol": n_ngb_tol,
+            "step_call": "sph_step" if args.calls == "step" else "sph_build_cells + sph_density + sph_force"}
+
+
+def reference_config(args, p):
+    import numpy as np
+    return arm_config(args, p, 1, float(np.float32(1e-4)))   # sph_config_default's n_ngb_tol
+
+
 def run_reference(args, rank, world):
+    """The reference arm: the fp64 oracle as it stands on the host cores, on this arm's
+    workload itself (args.config, every particle a source); each step the full oracle work
+    for a seeded sample of targets (oracle_closure_step). The sample size is calibrated so
+    that a step takes about cpu_budget_s / (steps + warmup) of wall time."""
     if rank != 0:
         return
-    n, one, _ = oracle_sample(min(args.cpu_budget_s, 150.0 / max(1, args.steps + args.warmup)))
-    for _ in range(args.warmup):
-        one(n)
-    ts, fs = [], []
-    for _ in range(args.steps):
-        t, F = one(n)
+    import workloads
+    p = workloads.make(args.config)
+    oracle_closure_setup(p)
+    procs = cores_used()
+    budget = args.ref_budget_s / max(1, args.steps + args.warmup)
+    # t(k) = a + b k (the per-step work has a fixed part: each worker's queries over all
+    # particles for the partners reaching in by their own h); two calibration points
+    k0, k1 = 8 * procs, 64 * procs
+    t0_, _ = oracle_closure_step(p, k0, procs, seed=140423100)
+    t1_, _ = oracle_closure_step(p, k1, procs, seed=140423100)
+    b = max((t1_ - t0_) / (k1 - k0), 1e-9)
+    a = max(t0_ - b * k0, 0.0)
+    k = int(max(k1, (budget - a) / b))
+    k = min(k, p.n // 4)
+    for w in range(args.warmup):
+        oracle_closure_step(p, k, procs, seed=140423101 + w)
+    ts, ws = [], []
+    for s_ in range(args.steps):
+        t, wk = oracle_closure_step(p, k, procs, seed=140423200 + s_)
         ts.append(t)
-        fs.append(F)
+        ws.append(wk)
     T = sum(ts)
-    value = 2.0 * sum(fs) / T
-    sample = (f"C4 generator (64 Plummer clumps + 30% background, seed 140423034) at N={n}; "
-              f"full oracle evaluation per step: h root (Eq. 3) + density + force, fp64 numpy/scipy")
+    value = sum(ws) / T
+    sample = (f"{p.name} itself ({p.n} particles, every one a source): per step {k} seeded targets; the oracle "
+              f"solves h on each target's closure (its partners within max(h_i, h_j), h_j bounded by twice "
+              f"the 15th-neighbour distance), the density and state of the partners and the targets' force, "
+              f"fp64 numpy/scipy, {procs} processes x 1 thread; value = (directed density contributions "
+              f"+ directed force pairs computed) / wall")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": f"C4-recipe sample N={n} (oracle)"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores_used(), "kind": "oracle",
-                             "sample": sample},
+            "data": "synthetic", "config": reference_config(args, p),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -475,13 +565,7 @@ def run_sph(args, rank, world, local_rank):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {N} particles ({p.name} generator, seeds in workloads/), "
-                               f"cold h0" + (" (library guess)" if h0 is None else ""),
-                   "N": N, "box": list(p.box), "l2": "flushed (256 MiB write) before every timed step",
-                   "parallelism": "replicas" if world > 1 else "single GPU",
-                   "split_count": CONFIG_TUNING["split_count"], "split_fraction": CONFIG_TUNING["split_fraction"],
-                   "n_ngb": 48, "n_ngb_tol": cfg.n_ngb_tol,
-                   "step_call": "sph_step" if args.calls == "step" else "sph_build_cells + sph_density + sph_force"},
+        "config": arm_config(args, p, world, cfg.n_ngb_tol),
         "roofline": dominant,
         "roofline_others": secondary,
         "roofline_binning": roof_bin,

@@ -26,3 +26,30 @@ def test_issue_rate():
     assert bench.issue_from_profiles("k_force", 0.0) is None
     assert bench.issue_from_profiles("no_such_kernel", 1.0) is None
     assert bench.traffic_from_profiles("no_such_kernel") is None
+
+
+def test_reference_closure_reproduces_the_whole_evaluation():
+    """The reference arm's per-target closure (h on the targets and every possible force
+    partner, density and state of the partners, force on the targets) gives the same h, rho,
+    a and du/dt as the oracle's whole-box evaluation, on a clustered input where partners by
+    their own (larger) h occur."""
+    import numpy as np
+
+    import bench
+    import oracle
+    import workloads
+    p = workloads.tiny(4, n=3000, clump_frac=0.5, n_dup=0)
+    ref = oracle.evaluate_all(p.x, p.v, p.m, p.u, p.box)
+    bench.oracle_closure_setup(p)
+    assert np.all(bench._G["hb"] >= ref["h"])                 # the bound holds
+    T = np.sort(np.random.default_rng(3).choice(p.n, 60, replace=False))
+    bench._G["keep"] = True
+    work, _ = bench._w_closure(T)
+    k = bench._G.pop("kept")
+    bench._G.pop("keep")
+    assert work > 0
+    assert np.allclose(k["h"], ref["h"][T], rtol=1e-12)
+    assert np.allclose(k["rho"], ref["rho"][T], rtol=1e-12)
+    scale = np.abs(ref["a"]).max()
+    assert np.abs(k["a"] - ref["a"][T]).max() <= 1e-10 * scale
+    assert np.abs(k["dudt"] - ref["dudt"][T]).max() <= 1e-10 * np.abs(ref["dudt"]).max()
