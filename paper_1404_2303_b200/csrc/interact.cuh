@@ -179,7 +179,6 @@ __global__ void __launch_bounds__(DENS_WARPS * 32, DENS_MINB) k_density(GroupLis
       sxyz[wib][2][32 * k + lane] = a.z;
     }
     __syncwarp();
-    ncand += act ? min(32 * DENS_ST, (len - stg + nst - 1) / nst) : 0;
     unsigned hm[DENS_ST];
 #pragma unroll
     for (int k = 0; k < DENS_ST; ++k) {
@@ -193,6 +192,7 @@ __global__ void __launch_bounds__(DENS_WARPS * 32, DENS_MINB) k_density(GroupLis
         m |= ((unsigned)(r2.x < hi2) | ((unsigned)(r2.y < hi2) << 1)) << (2 * t);
       }
       hm[k] = m;
+      cnt += __popc(m);   // the directed neighbours (the target's own entry taken off below)
     }
     if (DIAG && act) {
       // same r^2 as the hit loop; the band |r^2 - h^2| <= 2 SPH_BAND h^2 is |r/h - 1| <= SPH_BAND
@@ -237,11 +237,14 @@ __global__ void __launch_bounds__(DENS_WARPS * 32, DENS_MINB) k_density(GroupLis
         crx = fmaf(gf, dvy * dz - dvz * dy, crx);
         cry = fmaf(gf, dvz * dx - dvx * dz, cry);
         crz = fmaf(gf, dvx * dy - dvy * dx, crz);
-        cnt += (__float_as_int(b.w) == s) ? 0 : 1;
       }
     }
     __syncwarp();
   }
+  // every staged entry was tested once (the stages partition the list); the target's own
+  // entry (r = 0, image code 0) is in its group's list exactly once
+  ncand = act ? len : 0;
+  if (act) cnt -= 1;
   long long nd = 0, nbad = 0;
   if (act) {
     if (!NONLY && out.ghost) {
@@ -392,7 +395,6 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FORCE_MINB) k_force(GroupLis
       SJ[32 * k + lane] = jj;
     }
     __syncwarp();
-    ncand += act ? min(32 * FORCE_ST, (len - stg + nst - 1) / nst) : 0;
     unsigned hm[FORCE_ST];
 #pragma unroll
     for (int k = 0; k < FORCE_ST; ++k) {
@@ -415,10 +417,13 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FORCE_MINB) k_force(GroupLis
       const int sl = sself[wib][lane];
 #if FORCE_ST == 1
       if (sl >= 0) hm[0] &= ~(1u << sl);
+      cnt += __popc(hm[0]);
 #else
 #pragma unroll
       for (int k = 0; k < FORCE_ST; ++k)
         if (sl >= 0 && (sl >> 5) == k) hm[k] &= ~(1u << (sl & 31));
+#pragma unroll
+      for (int k = 0; k < FORCE_ST; ++k) cnt += __popc(hm[k]);
 #endif
     }
     if (DIAG && act) {
@@ -471,10 +476,10 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FORCE_MINB) k_force(GroupLis
       az = fmaf(-mT, dz, az);
       du = fmaf(mj * vdx, AGi + 0.125f * V, du);
       vsig = fmaxf(vsig, cs);
-      cnt += 1;
     }
     __syncwarp();
   }
+  ncand = act ? len : 0;   // every entry staged and tested once
   if (act) {
     const uint32_t p = out.perm[s];
     out.a[3 * (int64_t)p] = ax;
