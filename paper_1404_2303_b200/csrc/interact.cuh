@@ -52,14 +52,9 @@ struct GhostOut {
   float* hr;
 };
 
+// the density loop's epilogue is the ghost (a9): it writes the
+// caller-order outputs and the force state, not the sums
 struct DensOut {
-  double* sf;     // sum f            (N_i = (32/3) sum f, Eq. 3)
-  float4* acc0;   // sum m f, sum m q f', sum q f', sum m (f'/r) dv.dx
-  float4* acc1;   // sum m (f'/r) dv x dx (xyz), neighbour count (int bits)
-  float* s2;      // sum q^2 f''      (second derivative of N for the Halley step)
-  // ghost fused into the epilogue (a9): the sums above are then not
-  // written; the caller-order outputs and the force state are
-  bool ghost;
   const float* u;
   float gamma, beps, n_t, tol_check;
   GhostOut g;
@@ -145,7 +140,7 @@ __global__ void __launch_bounds__(DENS_WARPS * 32, DENS_MINB) k_density(GroupLis
   const float hi2 = act ? hi * hi : -1.f;
   const float hinv = act ? 1.0f / hi : 0.f;
   double sf = 0.0;
-  float sqfp = 0.f, sq2fpp = 0.f, smf = 0.f, smqfp = 0.f, divs = 0.f, crx = 0.f, cry = 0.f, crz = 0.f;
+  float smf = 0.f, smqfp = 0.f, divs = 0.f, crx = 0.f, cry = 0.f, crz = 0.f;
   int cnt = 0;
   long long ncand = 0, nbord = 0, ncoin = 0;
   const int64_t off = G.off[gid];
@@ -221,11 +216,9 @@ __global__ void __launch_bounds__(DENS_WARPS * 32, DENS_MINB) k_density(GroupLis
       const float rinv = r2 > 0.f ? rsqrtf(r2) : 0.f;
       const float qq = r2 * rinv * hinv;
       float f, fp, fpp;
-      spline(qq, f, fp, fpp);
+      spline(qq, f, fp, fpp);   // (f'' is for the h iteration's sums only: unused here)
       sf += (double)f;
       const float qfp = qq * fp;
-      sqfp += qfp;
-      sq2fpp = fmaf(qq * qq, fpp, sq2fpp);
       if (!NONLY) {
         const float4 b = SV[t];
         const float mj = q.w;
@@ -247,17 +240,11 @@ __global__ void __launch_bounds__(DENS_WARPS * 32, DENS_MINB) k_density(GroupLis
   if (act) cnt -= 1;
   long long nd = 0, nbad = 0;
   if (act) {
-    if (!NONLY && out.ghost) {
-      ghost_one(out.g, perm[s], s, hi, out.u[s], smf, smqfp, divs, crx, cry, crz, cnt, out.gamma, out.beps);
-      nd = cnt;
-      // the h iteration's convergence, re-checked from this loop's sum at the final h (R4)
-      nbad = fabs((32.0 / 3.0) * sf - (double)out.n_t) > (double)out.tol_check ? 1 : 0;
-    } else {
-      out.sf[s] = sf;
-      out.s2[s] = sq2fpp;
-      out.acc0[s] = make_float4(smf, smqfp, sqfp, divs);
-      out.acc1[s] = make_float4(crx, cry, crz, __int_as_float(cnt));
-    }
+    // the ghost (a9) in the epilogue: the caller-order outputs and the force state
+    ghost_one(out.g, perm[s], s, hi, out.u[s], smf, smqfp, divs, crx, cry, crz, cnt, out.gamma, out.beps);
+    nd = cnt;
+    // the h iteration's convergence, re-checked from this loop's sum at the final h (R4)
+    nbad = fabs((32.0 / 3.0) * sf - (double)out.n_t) > (double)out.tol_check ? 1 : 0;
   }
 #pragma unroll
   for (int o2 = 16; o2 > 0; o2 >>= 1) {

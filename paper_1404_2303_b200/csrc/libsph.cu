@@ -1257,7 +1257,6 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
   go.hr = Bget<float>(c, B_HRCH);
   DensOut dout;
   memset(&dout, 0, sizeof(dout));
-  dout.ghost = true;
   dout.g = go;
   dout.u = uc;
   dout.gamma = c->cfg.gamma;
