@@ -199,7 +199,8 @@ __global__ void __launch_bounds__(DENS_WARPS * 32, DENS_MINB) k_density(GroupLis
         ncoin += (r2 == 0.f && __float_as_int(SV[t].w) != s) ? 1 : 0;
       }
     }
-    // interaction body for this lane's hits
+    // interaction body for this lane's hits (sum f per stage in fp32, then into the fp64 sum)
+    float sfs = 0.f;
     while (true) {
       int t = -1;
 #pragma unroll
@@ -213,11 +214,11 @@ __global__ void __launch_bounds__(DENS_WARPS * 32, DENS_MINB) k_density(GroupLis
       const float4 q = SP[t];
       const float dx = xi - q.x, dy = yi - q.y, dz = zi - q.z;
       const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-      const float rinv = r2 > 0.f ? rsqrtf(r2) : 0.f;
+      const float rinv = rsqrtf(fmaxf(r2, 1e-37f));   // r = 0 (self, duplicates): f' = 0 zeroes every r^-1 term
       const float qq = r2 * rinv * hinv;
       float f, fp, fpp;
       spline(qq, f, fp, fpp);   // (f'' is for the h iteration's sums only: unused here)
-      sf += (double)f;
+      sfs += f;
       const float qfp = qq * fp;
       if (!NONLY) {
         const float4 b = SV[t];
@@ -232,6 +233,7 @@ __global__ void __launch_bounds__(DENS_WARPS * 32, DENS_MINB) k_density(GroupLis
         crz = fmaf(gf, dvx * dy - dvy * dx, crz);
       }
     }
+    sf += (double)sfs;
     __syncwarp();
   }
   // every staged entry was tested once (the stages partition the list); the target's own
@@ -440,7 +442,7 @@ __global__ void __launch_bounds__(FORCE_WARPS * 32, FORCE_MINB) k_force(GroupLis
       const float hj2i = hjinv * hjinv;
       const bool in_i = r2 < hi2;
       const bool in_j = r2 * hj2i < 1.0f;
-      const float rinv = r2 > 0.f ? rsqrtf(r2) : 0.f;
+      const float rinv = rsqrtf(fmaxf(r2, 1e-37f));   // r = 0 (self, duplicates): f' = 0 zeroes every r^-1 term
       const float r = r2 * rinv;
       const float fpi = in_i ? spline_fp(r * hinv) : 0.f;
       const float fpj = in_j ? spline_fp(r * hjinv) : 0.f;
