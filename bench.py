@@ -64,7 +64,7 @@ def parse():
                     help="one step = sph_step (default) or sph_build_cells + sph_density + sph_force")
     ap.add_argument("--no-warm", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
-    ap.add_argument("--ref-budget-s", type=float, default=120.0,
+    ap.add_argument("--ref-budget-s", type=float, default=90.0,
                     help="--impl reference: wall seconds for the warm-up + timed steps together")
     ap.add_argument("--cpu-frac", type=float, default=0.02, help="cpu_baseline: fraction of the particles timed as targets")
     ap.add_argument("--scale-config", default="C5", help="N > 1 workload: C5 (strong scaling) or C4xN (weak)")
@@ -76,40 +76,76 @@ def parse():
 
 # --------------------------------------------------------------------- clocks ---
 class Clocks:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    """nvidia-smi samples (every 20 ms, with timestamps) of the SM clock and throttle reasons.
+    The sampler runs from construction (before the warm-up, so it is up when the timed region
+    starts); `region()` brackets the timed steps and only samples inside it (+-25 ms) count;
+    a region shorter than the sampling period reports the samples nearest to it."""
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.t0 = self.t1 = None
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.FIELDS}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", "20"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except FileNotFoundError:
             self.p = None
 
+    def wait_running(self, busy, limit_s: float = 5.0):
+        """Run `busy` (untimed GPU work) until the sampler has written a sample."""
+        t = time.time()
+        while self.p is not None and time.time() - t < limit_s:
+            self.f.flush()
+            if os.path.getsize(self.f.name) > 0:
+                return
+            busy()
+
+    def start(self):
+        import datetime
+        self.t0 = datetime.datetime.now()
+
+    def end(self):
+        import datetime
+        self.t1 = datetime.datetime.now()
+
     def stop(self):
+        import datetime
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi missing"]}
+        if self.t1 is None:
+            self.end()
+        time.sleep(0.05)   # the sample after the region
         self.p.terminate()
         self.p.wait()
         self.f.flush()
         rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
         os.unlink(self.f.name)
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        samples = []
         for r in rows:
             r = [x.strip() for x in r]
             try:
-                sm.append(float(r[0]))
-                smax.append(float(r[1]))
+                ts = datetime.datetime.strptime(r[0], "%Y/%m/%d %H:%M:%S.%f")
+                samples.append((ts, float(r[1]), float(r[2]), r[5:9]))
             except (ValueError, IndexError):
                 continue
+        tol = datetime.timedelta(milliseconds=25)
+        t0 = self.t0 or self.t1
+        inside = [x for x in samples if t0 - tol <= x[0] <= self.t1 + tol]
+        if not inside and samples:   # a region shorter than the sampling period
+            mid = t0 + (self.t1 - t0) / 2
+            inside = sorted(samples, key=lambda x: abs((x[0] - mid).total_seconds()))[:2]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for x in inside:
             for k, nm in enumerate(names):
-                if len(r) > 4 + k and r[4 + k].lower().startswith("active"):
+                if len(x[3]) > k and x[3][k].lower().startswith("active"):
                     reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+        sm = [x[1] for x in inside]
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(x[2] for x in inside) if inside else None,
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
@@ -155,8 +191,8 @@ def _w_closure(T):
     force sums need h, rho, A, c, f of every force partner j (r < max(h_i, h_j)); a partner
     by its own h has h_j > r, and h_j <= hb[j] (the bound below), so the closure C = T + every
     j within h_i or within hb[j] of a target holds them all: the oracle solves h on C, the
-    density and state on the partners, the force on T. Returns (pair interactions: directed
-    density contributions of the partners + directed force pairs of T, seconds)."""
+    density and state on the partners, the force on T. Returns (pair interactions: the
+    targets' directed force pairs = their share of 2F, the bench metric's count; seconds)."""
     import numpy as np
 
     import oracle
@@ -179,7 +215,7 @@ def _w_closure(T):
     rho, A, c, f = np.zeros(n), np.zeros(n), np.zeros(n), np.zeros(n)
     rho[S], A[S], c[S], f[S] = den["rho"], np.nan_to_num(st["A"]), st["c"], st["f"]
     fo = oracle.force_at(x, g["v"], g["m"], h, rho, A, c, f, box, targets=T, tree=g["tree"])
-    work = int(den["n_nbr"].sum()) + int(fo["n_nbr_force"].sum())
+    work = int(fo["n_nbr_force"].sum())   # the targets' share of 2F (the metric's count)
     if g.get("keep"):   # tests: the targets' results
         g["kept"] = dict(h=h[T], rho=rho[T], a=fo["a"], dudt=fo["dudt"])
     return work, time.perf_counter() - t0
@@ -206,13 +242,17 @@ def oracle_closure_setup(p):
 
 
 def oracle_closure_step(p, k, procs, seed):
-    """One reference step: k seeded targets of the workload, split over a process pool."""
+    """One reference step: k targets of the workload in `procs` compact blobs (the k/procs
+    particles nearest to a seeded random particle: blobs sample the particles, and a blob's
+    closure adds only a shell of partners), one blob per process."""
     import multiprocessing as mp
 
     import numpy as np
     rng = np.random.default_rng(seed)
-    T = np.sort(rng.choice(p.n, k, replace=False))
-    chunks = [c for c in np.array_split(T, procs) if c.size]
+    kb = max(1, k // procs)
+    centres = rng.choice(p.n, procs, replace=False)
+    _, idx = _G["tree"].query(_G["x"][centres], k=kb, workers=-1)
+    chunks = [np.sort(np.asarray(r).reshape(-1)) for r in np.atleast_2d(idx)]
     ctx = mp.get_context("fork")
     t0 = time.perf_counter()
     with ctx.Pool(len(chunks)) as pool:
@@ -323,15 +363,14 @@ def run_reference(args, rank, world):
     oracle_closure_setup(p)
     procs = cores_used()
     budget = args.ref_budget_s / max(1, args.steps + args.warmup)
-    # t(k) = a + b k (the per-step work has a fixed part: each worker's queries over all
-    # particles for the partners reaching in by their own h); two calibration points
-    k0, k1 = 8 * procs, 64 * procs
+    # t(k) = a + b k: each process's queries over all particles (partners reaching in by
+    # their own h) are a fixed cost per step; two calibration steps fit a and b
+    k0, k1 = 1024 * procs, 4096 * procs
     t0_, _ = oracle_closure_step(p, k0, procs, seed=140423100)
     t1_, _ = oracle_closure_step(p, k1, procs, seed=140423100)
     b = max((t1_ - t0_) / (k1 - k0), 1e-9)
     a = max(t0_ - b * k0, 0.0)
-    k = int(max(k1, (budget - a) / b))
-    k = min(k, p.n // 4)
+    k = int(min(max(k0, (budget - a) / b), p.n // 4))
     for w in range(args.warmup):
         oracle_closure_step(p, k, procs, seed=140423101 + w)
     ts, ws = [], []
@@ -341,11 +380,12 @@ def run_reference(args, rank, world):
         ws.append(wk)
     T = sum(ts)
     value = sum(ws) / T
-    sample = (f"{p.name} itself ({p.n} particles, every one a source): per step {k} seeded targets; the oracle "
-              f"solves h on each target's closure (its partners within max(h_i, h_j), h_j bounded by twice "
-              f"the 15th-neighbour distance), the density and state of the partners and the targets' force, "
-              f"fp64 numpy/scipy, {procs} processes x 1 thread; value = (directed density contributions "
-              f"+ directed force pairs computed) / wall")
+    sample = (f"{p.name} itself ({p.n} particles, every one a source): per step {k} targets in {procs} compact "
+              f"blobs (the particles nearest to seeded random particles); the oracle solves h on the blobs' "
+              f"closure (every possible force partner: within max(h_i, h_j), h_j bounded by twice the 15th-"
+              f"neighbour distance), the density and state of the partners and the targets' force, fp64 "
+              f"numpy/scipy, {procs} processes x 1 thread; value = the targets' directed force pairs (their "
+              f"share of 2F) / wall")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -431,8 +471,11 @@ def run_sph(args, rank, world, local_rank):
         if dist:
             td.barrier()
         torch.cuda.synchronize()
-        l0 = ctx.kernel_launches
         clk = Clocks(local_rank)
+        clk.wait_running(lambda: stepf(*inputs, outs_d, outs_f))   # untimed steps until sampling
+        torch.cuda.synchronize()
+        l0 = ctx.kernel_launches
+        clk.start()
         for _ in range(args.steps):
             flush.zero_()                       # evict the inputs from L2 between steps
             e0 = torch.cuda.Event(enable_timing=True)
@@ -443,6 +486,7 @@ def run_sph(args, rank, world, local_rank):
             e1.synchronize()
             total_ms += e0.elapsed_time(e1)
             stats.append((sd, sf))
+        clk.end()
         clocks = clk.stop()
         torch.cuda.synchronize()
         if dist:
@@ -652,7 +696,8 @@ def run_slab(args, rank, world, local_rank):
         td.barrier()
         torch.cuda.synchronize()
         l0 = ctx.kernel_launches
-        clk = Clocks(local_rank)
+        clk = Clocks(local_rank)   # (every rank runs the same steps: no per-rank warm-up here)
+        clk.start()
         for _ in range(args.steps):
             flush.zero_()
             e0 = torch.cuda.Event(enable_timing=True)
@@ -663,6 +708,7 @@ def run_slab(args, rank, world, local_rank):
             e1.record(stream)
             e1.synchronize()
             total += e0.elapsed_time(e1)
+        clk.end()
         clocks = clk.stop()
         torch.cuda.synchronize()
         td.barrier()
