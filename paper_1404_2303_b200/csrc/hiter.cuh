@@ -37,11 +37,13 @@ __device__ __forceinline__ float spline_fp(float q) {
   return q <= 0.5f ? a : b;
 }
 
-// The neighbour lists hold r (NB_STORE_R = 1: the square root is taken once, when the walk
-// records the entry, instead of once per entry in every iteration) or r^2 (NB_STORE_R = 0).
-// Both give the same fp32 r = r^2 * rsqrt(r^2), so the two layouts agree bit for bit.
+// The neighbour lists hold r^2 (NB_STORE_R = 0: the square root is taken per entry and
+// evaluation of the h sums, ~1.8 per entry) or r (NB_STORE_R = 1: taken when the walk tests
+// the source, i.e. for every staged candidate on every lane, ~15x as many). Both give the
+// same fp32 r = r^2 * rsqrt(r^2), so the two layouts agree bit for bit (C4: r^2 is 0.06 ms
+// faster with the round-2 walk, profiles/round2/walk_experiments.md).
 #ifndef NB_STORE_R
-#define NB_STORE_R 1
+#define NB_STORE_R 0
 #endif
 __device__ __forceinline__ float nb_dist_of_r2(float r2) { return r2 * rsqrtf(fmaxf(r2, 1e-37f)); }
 __device__ __forceinline__ float nb_stored(float r2) { return NB_STORE_R ? nb_dist_of_r2(r2) : r2; }
