@@ -112,7 +112,7 @@ typedef struct {
                             cells holding <= group_container particles. 0 = 512; -1 = pack sibling
                             leaves instead */
   float cold_margin;     /* h0 == 0 (library guess): rows are recorded for h_build = guess x this.
-                            0 = 1.0 */
+                            0 = 1.2 */
 } sph_config;
 
 typedef struct {         /* host struct, filled when non-NULL */

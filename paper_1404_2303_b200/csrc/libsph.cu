@@ -488,6 +488,7 @@ static WalkParams walk_params(sph_ctx* c, const float* reach) {
   P.g = level_geom(c);
   P.topmap = Bget<int>(c, B_TOPMAP);
   P.sorted = Bget<SortEntry>(c, B_SORTED);
+  P.any_sorted = c->n_sorted > 0;
   float Lmax = (float)std::max(c->cfg.box[0], std::max(c->cfg.box[1], c->cfg.box[2]));
   P.slack = 4e-7f * Lmax + c->skin;   // + the drift since the cells were sorted (sph_update_cells)
   P.ctr = ctr(c);
@@ -1005,8 +1006,8 @@ int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const floa
   build_nodes(c, frac && !need_guess, need_guess, need_guess && h0 == nullptr);
   float margin = c->cfg.h_margin;
   if (need_guess) {
-    // the guess is off by up to ~2x either way (C4 p1/p99 0.68/1.88): record at the guess
-    // itself; particles whose root lies beyond it are re-walked in the same warp (lists.cuh)
+    // the guess is off by up to ~2x either way (C4 p1/p99 0.68/1.88): record at 1.2x the
+    // guess; particles whose root lies beyond it are re-walked in the same warp (lists.cuh)
     margin = c->cold_margin;
     if (frac) build_nodes(c, true);     // the paper's split rule needs h
   }

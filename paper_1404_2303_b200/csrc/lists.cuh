@@ -113,6 +113,7 @@ struct WalkParams {
   LevelGeom g;
   const int* topmap;
   const SortEntry* sorted;
+  int any_sorted;           // some leaf has presorted lists (else no sortoff is read)
   float reach_max;          // UNION: max source reach (bound for the top-cell range)
   const unsigned long long* reach_max_bits;   // if set: reach_max as float bits on the device
   float slack;              // absolute slack of the box tests (fp32 rounding of corners)
@@ -359,7 +360,7 @@ template <int MODE>
 __device__ __forceinline__ void sweep_node(const WalkParams& P, WalkState& W, WalkSmem& S, int node, int code) {
   const int lane = W.lane;
   const int first = P.N.first[node], cnt = P.N.count[node];
-  const int64_t soff = P.N.sortoff[node];
+  const int64_t soff = P.any_sorted ? P.N.sortoff[node] : -1;
   const float* L = P.g.L;
   int k = 13;
   float3 cr = make_float3(0.f, 0.f, 0.f);
@@ -499,7 +500,11 @@ template <int MODE>
 #ifndef WALK_MINB
 #define WALK_MINB 0     // min resident blocks for __launch_bounds__ (0: none; register use is then the compiler's)
 #endif
-#if defined(WALK_MAXNREG)
+#ifndef WALK_MAXNREG
+#define WALK_MAXNREG 72   // pinned: left free, ptxas flips k_walk<NB> between 72 (small spills) and 96
+                          // registers on unrelated edits, and 96 costs 0.5 ms (21 instead of 28 warps/SM)
+#endif
+#if WALK_MAXNREG > 0
 #define WALK_BOUNDS __maxnreg__(WALK_MAXNREG)
 #elif WALK_MINB > 0
 #define WALK_BOUNDS __launch_bounds__(WALK_WARPS * 32, WALK_MINB)
@@ -660,7 +665,7 @@ __global__ void WALK_BOUNDS k_walk(WalkParams P) {
         reach = node_in_spheres<MODE>(P, W, S, nd, code, reach, hn, &fh);
         if (lane < k) {
           leaf = reach && !(rec.z >= 0 && rec.y > WALK_TAKE);
-          srt = leaf && P.N.sortoff[nd] >= 0;
+          srt = leaf && P.any_sorted && P.N.sortoff[nd] >= 0;
         }
         // reached internal nodes push their children
         const int nch = (reach && !leaf) ? __popc(rec.w & 0xff) : 0;
