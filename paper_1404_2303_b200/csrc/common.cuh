@@ -98,7 +98,9 @@ __device__ __forceinline__ float3 dir_unit(int d) { return make_float3(c_dirs[d]
 #define SPH_CNORM (8.0f / SPH_PI_F)   // 8/pi of W
 #define SPH_MAX_DEPTH 12              // Morton levels below the top grid
 #define SPH_COLD_MARGIN 1.2f   // h_build / guess at a cold start (C4: 1.0 7.85, 1.1 7.77, 1.2 7.69, 1.3 7.88 ms; C3 flat: tools/cold_margin_sweep.sh)
+#ifndef SPH_REGROW_MARGIN
 #define SPH_REGROW_MARGIN 1.1f        // h_build / h after a Newton step left the list (tuned: tools/sweep.sh)
+#endif
 #define SPH_BAND 1e-6f   // borderline band |r/h - 1| <= 1e-6 (north_star; R5)
 #define SPH_IDX_BITS 27               // list entry = (periodic image code << 27) | source index
 #define SPH_IDX_MASK ((1u << SPH_IDX_BITS) - 1u)
