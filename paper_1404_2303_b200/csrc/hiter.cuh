@@ -118,6 +118,45 @@ __device__ __forceinline__ void nsums_row(const float* r2l, int e1, float hinv, 
   }
 }
 
+// nsums for one particle split over a segment of HSOLVE_SEG lanes (sub-lane sl): float4
+// chunks sl, sl + SEG, ... of a 16-byte aligned contiguous row (the f of a chunk summed in
+// fp32, then into the fp64 total), else entries sl, sl + SEG, ...
+#ifndef HSOLVE_SEG
+#define HSOLVE_SEG 4
+#endif
+__device__ __forceinline__ void nsums_seg(const float* r2l, int64_t stride, int cnt, int sl, float hinv, double& S0,
+                                          float& S1, float& S2) {
+  if (stride == 1 && ((reinterpret_cast<uintptr_t>(r2l) & 15) == 0)) {
+    const float4* r4 = reinterpret_cast<const float4*>(r2l);
+    const int nq = cnt >> 2;
+    for (int q = sl; q < nq; q += HSOLVE_SEG) {
+      const float4 v = r4[q];
+      const float r2[4] = {v.x, v.y, v.z, v.w};
+      float fs = 0.f;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float qq = fminf(nb_r(r2[k]) * hinv, 1.f);
+        float f, fp, fpp;
+        spline(qq, f, fp, fpp);
+        fs += f;
+        S1 = fmaf(qq, fp, S1);
+        S2 = fmaf(qq * qq, fpp, S2);
+      }
+      S0 += (double)fs;
+    }
+    for (int e = 4 * nq + sl; e < cnt; e += HSOLVE_SEG) {   // the last cnt % 4 entries
+      const float qq = fminf(nb_r(r2l[e]) * hinv, 1.f);
+      float f, fp, fpp;
+      spline(qq, f, fp, fpp);
+      S0 += (double)f;
+      S1 = fmaf(qq, fp, S1);
+      S2 = fmaf(qq * qq, fpp, S2);
+    }
+  } else {
+    nsums(r2l, stride, sl, cnt, HSOLVE_SEG, hinv, S0, S1, S2);
+  }
+}
+
 // One Newton/Halley update from the sums at h. Returns the new state: HS_DONE (converged),
 // HS_ACTIVE (h updated, iterate), HS_REGROW (the new h lies beyond h_build).
 __device__ __forceinline__ uint8_t hstep(double S0, float S1, float S2, float& h, float& hbs, float& l, float& u,
@@ -204,7 +243,63 @@ __device__ __forceinline__ void warp_hsolve(bool act, const float* r2l, int64_t 
     H.h = fminf(H.h, H.hbs);
   }
   const bool shortl = act && H.st == HS_ACTIVE && cnt <= HSOLVE_LONG;
+#if HSOLVE_SEG > 1
+  // Segments of HSOLVE_SEG lanes evaluate the sums of one particle each (the lane's own
+  // particle loop left ~11 of 32 lanes busy: rows of different lengths, particles converging
+  // after different numbers of steps). Each round takes the first 32 / HSOLVE_SEG pending
+  // particles in lane order, one evaluation each; a particle stays pending while it iterates.
+  {
+    constexpr int NS = 32 / HSOLVE_SEG;
+    const int seg = lane / HSOLVE_SEG, sl = lane % HSOLVE_SEG;
+    unsigned pend = __ballot_sync(FULL_MASK, shortl && max_iter > 0);
+    while (pend) {
+      unsigned mm = pend;
+      for (int k = 0; k < seg && mm; ++k) mm &= mm - 1;   // drop the first seg pending lanes
+      const int owner = mm ? __ffs(mm) - 1 : -1;
+      const int src = owner < 0 ? 0 : owner;
+      const float* rp = reinterpret_cast<const float*>(__shfl_sync(FULL_MASK, (unsigned long long)r2l, src));
+      const int64_t rs = __shfl_sync(FULL_MASK, stride, src);
+      const int c = __shfl_sync(FULL_MASK, cnt, src);
+      float h = __shfl_sync(FULL_MASK, H.h, src), hb = __shfl_sync(FULL_MASK, H.hbs, src);
+      float l = __shfl_sync(FULL_MASK, H.l, src), u = __shfl_sync(FULL_MASK, H.u, src);
+      double S0 = 0.0;
+      float S1 = 0.f, S2 = 0.f;
+      if (owner >= 0) nsums_seg(rp, rs, c, sl, 1.0f / h, S0, S1, S2);
+#pragma unroll
+      for (int o = 1; o < HSOLVE_SEG; o <<= 1) {
+        S0 += __shfl_xor_sync(FULL_MASK, S0, o);
+        S1 += __shfl_xor_sync(FULL_MASK, S1, o);
+        S2 += __shfl_xor_sync(FULL_MASK, S2, o);
+      }
+      int st = HS_ACTIVE;
+      if (owner >= 0) st = hstep(S0, S1, S2, h, hb, l, u, n_t, tol, margin, hcap);
+      // back to the owners: a pending lane's segment is the number of pending lanes below it
+      const int myseg = __popc(pend & lanemask_lt());
+      const bool mine = ((pend >> lane) & 1u) && myseg < NS;
+      const int from = mine ? myseg * HSOLVE_SEG : 0;
+      h = __shfl_sync(FULL_MASK, h, from);
+      hb = __shfl_sync(FULL_MASK, hb, from);
+      l = __shfl_sync(FULL_MASK, l, from);
+      u = __shfl_sync(FULL_MASK, u, from);
+      st = __shfl_sync(FULL_MASK, st, from);
+      bool again = ((pend >> lane) & 1u) != 0;
+      if (mine) {
+        H.h = h;
+        H.hbs = hb;
+        H.l = l;
+        H.u = u;
+        H.st = (uint8_t)st;
+        H.ev += cnt;
+        H.it += st == HS_REGROW ? 2 : 1;
+        again = H.st == HS_ACTIVE && H.it < max_iter;
+      }
+      pend = __ballot_sync(FULL_MASK, again);
+    }
+  }
+  if (false) {
+#else
   if (shortl) {
+#endif
     for (; H.it < max_iter && H.st == HS_ACTIVE; ++H.it) {
       double S0 = 0.0;
       float S1 = 0.f, S2 = 0.f;
