@@ -178,7 +178,9 @@ __global__ void k_write_top(const uint64_t* __restrict__ keys, int64_t n, int sh
   }
 }
 
-__global__ void k_top_counts(int n0, int64_t n, NodeArrays N) {
+// n0 (the occupied top cells) read on the device: the grid is launched for an upper bound
+__global__ void k_top_counts(const int* __restrict__ n0p, int64_t n, NodeArrays N) {
+  const int n0 = *n0p;
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n0) N.count[i] = (i + 1 < n0 ? N.first[i + 1] : (int)n) - N.first[i];
 }
@@ -194,6 +196,9 @@ __global__ void k_top_counts(int n0, int64_t n, NodeArrays N) {
 // children in parent order, octant order. A level
 // that would exceed the node capacity stops the loop (status[1] = 1: the host grows the
 // arrays and runs it again).
+#ifndef SORT_BLOCK_MAX
+#define SORT_BLOCK_MAX 4096
+#endif
 struct LevelBuild {
   int* lev_off;      // [SPH_MAX_DEPTH + 4]: level offsets (zeroed by the host; [1] = n0 written here)
   int* status;       // [0] levels processed, [1] 1 = node capacity exceeded, 2 = barrier timeout
@@ -201,6 +206,9 @@ struct LevelBuild {
   int* part;         // [gridDim.x] block sums
   int* nch;          // [cap] children per node of the level being built (index node - a)
   int cap;           // node capacity
+  int* presort;      // set to 1 if a leaf qualifies for presorted lists (count > sort_min_len): the
+                     // host skips the presort pass (and its scan's round trip) when it stays 0
+  int sort_min_len;
 };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -259,7 +267,8 @@ __global__ void __launch_bounds__(LEVEL_THREADS) k_build_levels(LevelBuild L, co
                                                                 const uint64_t* __restrict__ keys, LevelGeom g,
                                                                 int depth, int split_count, float split_frac,
                                                                 NodeArrays N, float guess_n, int guess_min,
-                                                                float hcap, float4* xh_w, int n0) {
+                                                                float hcap, float4* xh_w, const int* n0p) {
+  const int n0 = __ldcg(n0p);   // the occupied top cells (a device scan total: no host round trip)
   __shared__ int red[LEVEL_THREADS / 32];
   __shared__ int wsc[LEVEL_THREADS / 32];
   const int lane = threadIdx.x & 31;
@@ -282,6 +291,7 @@ __global__ void __launch_bounds__(LEVEL_THREADS) k_build_levels(LevelBuild L, co
       }
       const int sp = (l < depth) && (cnt > split_count) && frac_ok;
       if (lane == 0) N.split[node] = sp;
+      if (lane == 0 && !sp && cnt > L.sort_min_len && cnt > 1 && cnt <= SORT_BLOCK_MAX) *L.presort = 1;
       if (!sp) {
         if (lane == 0) L.nch[node - a] = 0;
         if (guess_n > 0.f) {
@@ -489,7 +499,6 @@ struct SortEntry {  // 8 bytes: projection key and cell-order particle index
   int idx;
 };
 
-#define SORT_BLOCK_MAX 4096
 // number of sorted entries of each leaf: 13 * count if it is presorted
 __global__ void k_sort_sizes(int nnodes, NodeArrays N, int sort_min_len, int64_t* __restrict__ sz) {
   const int y = blockIdx.x * blockDim.x + threadIdx.x;

@@ -169,6 +169,9 @@ struct sph_ctx {
   int nb_k = 192;            // capacity of a particle's neighbour list (NB walk)
   int64_t nb_k_for = -1;     // particle count nb_k was sized for
   int ucap = 768;            // capacity of a group's interaction list slab (UNION walk)
+  bool in_step = false;      // sph_build_cells called by sph_step (no end-of-call sync)
+  bool pos_check = false;    // k_keys' position checks not read yet (read with the level build's status)
+  bool maybe_presort = true; // some leaf of the last level build qualifies for presorted lists
   int group_cmax = 512;      // targets: balanced chunks of the deepest cells holding <= 512 (0: sibling packing)
   int64_t ovf_used = 0;      // entries of the neighbour-list overflow pool
   int64_t n_ovfidx = 0;      // particles that have a list in the pool (k_hsolve_pool)

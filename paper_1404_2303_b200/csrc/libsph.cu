@@ -188,6 +188,17 @@ static T scan_excl(sph_ctx* c, const T* in, T* out, int64_t n) {
   return total;
 }
 
+// the same scan leaving its total on the device (no host round trip): returns its address
+template <class T>
+static const T* scan_excl_dev(sph_ctx* c, const T* in, T* out, int64_t n) {
+  int64_t nb = std::max<int64_t>((n + SCAN_TILE - 1) / SCAN_TILE, 1);
+  T* sums = reinterpret_cast<T*>(B<char>(c, B_SCAN_TMP, (nb + 2) * sizeof(T)));
+  LAUNCH(k_scan_reduce<T>, (int)nb, SCAN_THREADS, 0, in, n, sums);
+  LAUNCH(k_scan_blocksums<T>, 1, SCAN_THREADS, 0, sums, nb, sums + nb);
+  LAUNCH(k_scan_final<T>, (int)nb, SCAN_THREADS, 0, in, n, sums, out);
+  return sums + nb;
+}
+
 // =========================================================== kernel attributes ==
 // cudaFuncSetAttribute acts on the current device: remember (device, kernel) pairs, so a
 // second context on another GPU of the same process raises the limit there too.
@@ -347,11 +358,15 @@ static void sort_particles(sph_ctx* c, float h0max, bool have_h) {
   // cell-order positions, and the reference of a later pseudo-Verlet update, in one pass
   LAUNCH(k_pack, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, xc, xh, B<float4>(c, B_XREF, n));
   c->skin = 0.f;
-  // the position checks of k_keys (the sort itself is harmless on invalid input)
-  unsigned long long hc[C_NCOUNTERS];
-  ctr_read(c, hc);
-  SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_NONFINITE), SPH_E_DOMAIN, "non-finite position");
-  SPH_REQUIRE(!(hc[C_ERR] & ERRBIT_XRANGE), SPH_E_DOMAIN, "position outside [0, L)");
+  // the position checks of k_keys (the sort itself is harmless on invalid input, and so is the
+  // level build on its keys) are read with the level build's status: one round trip for both
+  c->pos_check = true;
+}
+
+static void pos_check(sph_ctx* c, unsigned long long err) {
+  c->pos_check = false;
+  SPH_REQUIRE(!(err & ERRBIT_NONFINITE), SPH_E_DOMAIN, "non-finite position");
+  SPH_REQUIRE(!(err & ERRBIT_XRANGE), SPH_E_DOMAIN, "position outside [0, L)");
 }
 
 // a4: the hierarchy from the sorted keys. Split rule: count > split_count and (rule on)
@@ -367,15 +382,23 @@ static void build_nodes(sph_ctx* c, bool use_fraction, bool guess = false, bool 
   const int depth = c->depth;
   const int sh = 3 * depth;
   LAUNCH(k_mark_top, grid1d(c, n, 256), 256, 0, keys, n, sh, flag);
-  const int n0 = scan_excl<int>(c, flag, idx, n);
-  ensure_nodes(c, std::max<int64_t>(2 * (int64_t)n0 + 1024, n / 8));
   const int64_t ntot = (int64_t)c->ntop[0] * c->ntop[1] * c->ntop[2];
+  // the occupied top cells n0 <= min(ntot, n) stay on the device (k_top_counts and
+  // k_build_levels read them) when that bound is small; else the count is read first
+  const int* n0d = scan_excl_dev<int>(c, flag, idx, n);
+  const int64_t n0b = std::min<int64_t>(ntot, n);
+  int n0h = -1;
+  if (n0b > n / 8) {
+    read_dev(c, &n0h, n0d, sizeof(int));
+    ensure_nodes(c, std::max<int64_t>(2 * (int64_t)n0h + 1024, n / 8));
+  } else {
+    ensure_nodes(c, std::max<int64_t>(2 * n0b + 1024, n / 8));
+  }
   int* topmap = B<int>(c, B_TOPMAP, ntot);
   CUDA_TRY(cudaMemsetAsync(topmap, 0xff, ntot * sizeof(int), c->stream));
   NodeArrays N = nodes(c);
   LAUNCH(k_write_top, grid1d(c, n, 256), 256, 0, keys, n, sh, flag, idx, c->ntop[0], c->ntop[1], N, topmap);
-  LAUNCH(k_top_counts, gridfull(n0, 256), 256, 0, n0, n, N);
-  c->lev_off.assign({0, n0});
+  LAUNCH(k_top_counts, gridfull(n0h >= 0 ? n0h : n0b, 256), 256, 0, n0d, n, N);
   // the levels in one cooperative launch (k_build_levels); grown and re-run if the nodes
   // outgrow the arrays (they keep their size across builds)
   const LevelGeom g = level_geom(c);
@@ -386,7 +409,7 @@ static void build_nodes(sph_ctx* c, bool use_fraction, bool guess = false, bool 
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_build_levels, LEVEL_THREADS, 0));
     grid = std::max(1, per_sm) * c->num_sms;
   }
-  int* lev = B<int>(c, B_N_LEV, SPH_MAX_DEPTH + 8);
+  int* lev = B<int>(c, B_N_LEV, SPH_MAX_DEPTH + 12);
   int* part = B<int>(c, B_N_CHBASE, grid);
   for (int attempt = 0;; ++attempt) {
     const int64_t cap = std::min({(int64_t)(c->b[B_N_FIRST].bytes / sizeof(int)),
@@ -402,26 +425,36 @@ static void build_nodes(sph_ctx* c, bool use_fraction, bool guess = false, bool 
     Lb.part = part;
     Lb.nch = B<int>(c, B_N_NCH, cap);
     Lb.cap = (int)std::min<int64_t>(cap, INT_MAX);
-    CUDA_TRY(cudaMemsetAsync(lev, 0, (SPH_MAX_DEPTH + 8) * sizeof(int), c->stream));
+    Lb.presort = lev + SPH_MAX_DEPTH + 8;
+    Lb.sort_min_len = c->cfg.sort_min_len;
+    CUDA_TRY(cudaMemsetAsync(lev, 0, (SPH_MAX_DEPTH + 12) * sizeof(int), c->stream));
     N = nodes(c);
     float guess_n = guess ? c->cfg.n_ngb : 0.f;
     int guess_min = guess_all ? -(int)c->cfg.n_ngb : (int)c->cfg.n_ngb;
     float hcap = h_cap(c);
     float4* xh_w = Bget<float4>(c, B_XH);
-    int n0_arg = n0;
+    const int* n0_arg = n0d;
     void* args[] = {&Lb,  (void*)&xh, (void*)&keys, (void*)&g,  (void*)&depth, &c->cfg.split_count, (void*)&frac,
-                    &N,   &guess_n,   &guess_min,   &hcap,      &xh_w,         &n0_arg};
+                    &N,   &guess_n,   &guess_min,   &hcap,      &xh_w,         (void*)&n0_arg};
     CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_build_levels, grid, LEVEL_THREADS, args, 0, c->stream));
     c->launches++;
-    int hl[SPH_MAX_DEPTH + 6];
-    read_dev(c, hl, lev, sizeof(hl));
+    // the level offsets and status, and the position checks of the sort, in one round trip
+    int hl[SPH_MAX_DEPTH + 10];
+    CUDA_TRY(cudaMemcpyAsync(c->hpin, lev, sizeof(hl), cudaMemcpyDeviceToHost, c->stream));
+    if (c->pos_check)
+      CUDA_TRY(cudaMemcpyAsync(c->hpin + 16, ctr(c) + C_ERR, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                               c->stream));
+    sync(c);
+    memcpy(hl, c->hpin, sizeof(hl));
+    if (c->pos_check) pos_check(c, c->hpin[16]);
+    c->maybe_presort = hl[SPH_MAX_DEPTH + 8] != 0;
     SPH_REQUIRE(hl[SPH_MAX_DEPTH + 5] != 2, SPH_E_CUDA, "k_build_levels: grid barrier timed out");
     if (hl[SPH_MAX_DEPTH + 5] == 1) {   // node capacity exceeded: grow and run again
       SPH_REQUIRE(attempt < 8, SPH_E_OOM, "node arrays keep overflowing");
       ensure_nodes(c, 2 * cap);
       continue;
     }
-    c->lev_off.assign({0, n0});
+    c->lev_off.assign({0, hl[1]});   // [1] = n0, written by k_build_levels
     for (int l = 0; l + 2 < SPH_MAX_DEPTH + 4 && hl[l + 2] > hl[l + 1]; ++l) c->lev_off.push_back(hl[l + 2]);
     break;
   }
@@ -437,6 +470,11 @@ static void build_nodes(sph_ctx* c, bool use_fraction, bool guess = false, bool 
 static void build_sorted(sph_ctx* c) {
   DbgTimer _t(c, "sorted lists");
   const int nn = c->n_nodes;
+  if (!c->maybe_presort) {   // no leaf qualifies (k_build_levels): no lists, no scan
+    c->n_sorted = 0;
+    CUDA_TRY(cudaMemsetAsync(Bget<int64_t>(c, B_N_SORTOFF), 0xff, nn * sizeof(int64_t), c->stream));
+    return;
+  }
   int64_t* sz = B<int64_t>(c, B_TMPL0, nn);
   int64_t* sc = B<int64_t>(c, B_TMPL1, nn);
   NodeArrays N = nodes(c);
@@ -1046,7 +1084,8 @@ int sph_build_cells_halo(sph_ctx* ctx, int64_t n_own, int64_t n_halo, const floa
   nb_walk(c, -1);
   c->state = 1;
   CUDA_TRY(cudaEventRecord(c->ev[1], c->stream));
-  sync(c);
+  // inside sph_step the density call's first counter read is the next round trip
+  if (!c->in_step) sync(c);
 #ifdef SPH_WALK_STATS
   {
     unsigned long long z[8][5];
@@ -1293,7 +1332,11 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
                            c->stream));
   CUDA_TRY(cudaMemcpyAsync(c->hpin + C_NCOUNTERS, verr + C_ERR, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                            c->stream));
+  // the recorded neighbour-list entries in the same round trip
+  CUDA_TRY(cudaMemcpyAsync(c->hpin + C_NCOUNTERS + 1, Bget<unsigned long long>(c, B_NBENT), sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, c->stream));
   sync(c);
+  c->nb_entries = (int64_t)c->hpin[C_NCOUNTERS + 1];
   memcpy(hc, c->hpin, sizeof(hc));
   hc[C_ERR] |= c->hpin[C_NCOUNTERS];
   if ((hc[C_ERR] & (ERRBIT_NONFINITE | ERRBIT_MASS | ERRBIT_U)) && c->defer_out)
@@ -1324,11 +1367,6 @@ int sph_density(sph_ctx* ctx, const float* v, const float* m, const float* u, fl
                     " within h of a slab face exceeds cfg.halo_width");
   }
   phase_resolve(c);
-  {
-    unsigned long long ne = 0;
-    read_dev(c, &ne, Bget<unsigned long long>(c, B_NBENT), sizeof(ne));
-    c->nb_entries = (int64_t)ne;
-  }
   if (st) {
     memset(st, 0, sizeof(*st));
     fill_struct_stats(c, st);
@@ -1486,7 +1524,9 @@ int sph_step(sph_ctx* ctx, int64_t n, const float* x, const float* h0, const flo
   c->pre_pending = true;
   c->pre_ready = false;
   API_END
+  ctx->in_step = true;
   int rc = sph_build_cells(ctx, n, x, h0);
+  ctx->in_step = false;
   ctx->pre_pending = false;
   if (rc != SPH_OK) {
     ctx->pre_ready = false;
