@@ -662,6 +662,7 @@ static void build_union(sph_ctx* c, const float* reach) {
     CUDA_TRY(cudaMemsetAsync(P.raw_out, 0, sizeof(unsigned long long), c->stream));
   }
   P.reach_max_bits = ctr(c) + C_HMAXBITS;
+  P.reach_xhw = c->n == c->n_own && reach == Bget<float>(c, B_HRCH);   // k_reach_owned copied xh.w for all
   P.nsel = ng;
   P.off = B<int64_t>(c, B_GOFF, ng);
   P.len = B<int>(c, B_GLEN, ng);

@@ -105,6 +105,7 @@ struct WalkParams {
   unsigned long long* raw_out;  // if set: sources streamed through the filters, summed (SPH_F_COUNT_CANDIDATES)
   const float4* xh;         // cell-order positions
   const float* reach;       // per particle: NB h_build; UNION the h used for the reach (0: none)
+  int reach_xhw;            // UNION: reach[j] == xh[j].w for every particle (no halo): read it from the position record
   const uint8_t* tsel;      // NB: targets are the particles with tsel == tsel_val (null: owned)
   uint8_t tsel_val;
   const uint32_t* perm;     // cell order -> caller index; targets are owned (perm < n_own)
@@ -380,8 +381,9 @@ __device__ __forceinline__ void sweep_node(const WalkParams& P, WalkState& W, Wa
       float3 p = make_float3(0.f, 0.f, 0.f);
       float hj = 0.f;
       if (v) {
-        p = rel_pos(P.xh[first + e], code, W.o, W.oL, L);
-        hj = P.reach[first + e];
+        const float4 q = P.xh[first + e];
+        p = rel_pos(q, code, W.o, W.oL, L);
+        hj = P.reach_xhw ? q.w : P.reach[first + e];
       }
       emit_chunk<MODE>(P, W, S, v, first + e, p, hj, code);
     }
@@ -410,8 +412,9 @@ __device__ __forceinline__ void sweep_node(const WalkParams& P, WalkState& W, Wa
     float3 p = make_float3(0.f, 0.f, 0.f);
     float hj = 0.f;
     if (v) {
-      p = rel_pos(P.xh[j], code, W.o, W.oL, L);
-      hj = P.reach[j];
+      const float4 q = P.xh[j];
+      p = rel_pos(q, code, W.o, W.oL, L);
+      hj = P.reach_xhw ? q.w : P.reach[j];
     }
     emit_chunk<MODE>(P, W, S, v, j, p, hj, code);
     if (__popc(inwin) < min(32, cnt - b0)) break;   // early exit
@@ -453,7 +456,7 @@ __device__ __forceinline__ void flush_ranges(const WalkParams& P, WalkState& W, 
       code = S.rq_code[r];
       const float4 q = P.xh[j], so = S.rq_so[r], oo = S.rq_oo[r];
       p = make_float3((q.x + so.x) - oo.x, (q.y + so.y) - oo.y, (q.z + so.z) - oo.z);
-      hj = P.reach[j];
+      hj = P.reach_xhw ? q.w : P.reach[j];
     }
     emit_chunk<MODE>(P, W, S, v, j, p, hj, code);
   }
