@@ -146,13 +146,10 @@ __global__ void __launch_bounds__(256) k_keys(const float* __restrict__ x, const
 // ---------------------------------------------------------------- a3 ---------
 // cell-order positions (and the pseudo-Verlet reference) from the packed caller-order records
 __global__ void k_pack(const uint32_t* __restrict__ perm, int64_t n, const float4* __restrict__ xc,
-                       float4* __restrict__ xh, float4* __restrict__ xref) {
+                       float4* __restrict__ xh) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n;
-       s += (int64_t)gridDim.x * blockDim.x) {
-    const float4 q = xc[perm[s]];
-    xh[s] = q;
-    xref[s] = q;
-  }
+       s += (int64_t)gridDim.x * blockDim.x)
+    xh[s] = xc[perm[s]];
 }
 
 // top-level nodes = runs of equal top-cell index in the sorted keys

@@ -169,6 +169,7 @@ struct sph_ctx {
   int nb_k = 192;            // capacity of a particle's neighbour list (NB walk)
   int64_t nb_k_for = -1;     // particle count nb_k was sized for
   int ucap = 768;            // capacity of a group's interaction list slab (UNION walk)
+  bool xref_valid = false;   // B_XREF holds the last build's cell-order positions (sph_update_cells)
   bool in_step = false;      // sph_build_cells called by sph_step (no end-of-call sync)
   bool pos_check = false;    // k_keys' position checks not read yet (read with the level build's status)
   bool maybe_presort = true; // some leaf of the last level build qualifies for presorted lists

@@ -355,8 +355,10 @@ static void sort_particles(sph_ctx* c, float h0max, bool have_h) {
   if (v0 == Bget<uint32_t>(c, B_VALS0)) std::swap(c->b[B_PERM], c->b[B_VALS0]);
   else std::swap(c->b[B_PERM], c->b[B_VALS1]);
   float4* xh = B<float4>(c, B_XH, n);
-  // cell-order positions, and the reference of a later pseudo-Verlet update, in one pass
-  LAUNCH(k_pack, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, xc, xh, B<float4>(c, B_XREF, n));
+  // cell-order positions (the pseudo-Verlet reference is copied from them by the first
+  // sph_update_cells after this build, not written by every build)
+  LAUNCH(k_pack, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, xc, xh);
+  c->xref_valid = false;
   c->skin = 0.f;
   // the position checks of k_keys (the sort itself is harmless on invalid input, and so is the
   // level build on its keys) are read with the level build's status: one round trip for both
@@ -1810,7 +1812,7 @@ int sph_update_cells(sph_ctx* ctx, const float* x, const float* h0) {
   SPH_REQUIRE(x && h0, SPH_E_ARG, "x or h0 NULL");
   SPH_REQUIRE(!c->has_active || c->n_active_for == c->n_own, SPH_E_ARG,
               "an active mask (sph_set_active) must cover the n_own particles of the last build");
-  const bool can = c->state >= 1 && c->n == c->n_own && c->n_sorted == 0 && c->b[B_XREF].p;
+  const bool can = c->state >= 1 && c->n == c->n_own && c->n_sorted == 0;
   if (!can) {
     c->cells_reused = false;
     return sph_build_cells_halo(ctx, c->n_own, 0, x, h0);
@@ -1824,6 +1826,11 @@ int sph_update_cells(sph_ctx* ctx, const float* x, const float* h0) {
   LAUNCH(k_hrange, grid1d(c, n, 256), 256, 0, c->hin, n, ctr(c));
   ctr_read(c, hc);
   const float hmin = as_float(hc[C_HMINBITS]);
+  if (!c->xref_valid) {   // the build's positions (xh holds them until the first update)
+    CUDA_TRY(cudaMemcpyAsync(B<float4>(c, B_XREF, n), Bget<float4>(c, B_XH), n * sizeof(float4),
+                             cudaMemcpyDeviceToDevice, c->stream));
+    c->xref_valid = true;
+  }
   ctr_reset(c);
   LAUNCH(k_update_pos, grid1d(c, n, 256), 256, 0, Bget<uint32_t>(c, B_PERM), n, c->xin, c->hin,
          Bget<float4>(c, B_XREF), (float)c->cfg.box[0], (float)c->cfg.box[1],
