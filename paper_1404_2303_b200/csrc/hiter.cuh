@@ -124,13 +124,30 @@ __device__ __forceinline__ void nsums_row(const float* r2l, int e1, float hinv, 
 #ifndef HSOLVE_SEG
 #define HSOLVE_SEG 4
 #endif
+#ifndef HSEG_PIPE
+#define HSEG_PIPE 1     // load the next float4 chunk before summing this one (C4 build -0.07 ms)
+#endif
 __device__ __forceinline__ void nsums_seg(const float* r2l, int64_t stride, int cnt, int sl, float hinv, double& S0,
                                           float& S1, float& S2) {
   if (stride == 1 && ((reinterpret_cast<uintptr_t>(r2l) & 15) == 0)) {
     const float4* r4 = reinterpret_cast<const float4*>(r2l);
     const int nq = cnt >> 2;
+#if HSEG_PIPE == 2
+    float4 nxt = sl < nq ? r4[sl] : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 nx2 = sl + HSOLVE_SEG < nq ? r4[sl + HSOLVE_SEG] : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int q = sl; q < nq; q += HSOLVE_SEG) {
+      const float4 v = nxt;
+      nxt = nx2;
+      if (q + 2 * HSOLVE_SEG < nq) nx2 = r4[q + 2 * HSOLVE_SEG];
+#elif HSEG_PIPE
+    float4 nxt = sl < nq ? r4[sl] : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int q = sl; q < nq; q += HSOLVE_SEG) {
+      const float4 v = nxt;
+      if (q + HSOLVE_SEG < nq) nxt = r4[q + HSOLVE_SEG];   // the next chunk's load in flight
+#else
     for (int q = sl; q < nq; q += HSOLVE_SEG) {
       const float4 v = r4[q];
+#endif
       const float r2[4] = {v.x, v.y, v.z, v.w};
       float fs = 0.f;
 #pragma unroll
