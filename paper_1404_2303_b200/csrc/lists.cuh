@@ -428,11 +428,12 @@ __device__ __forceinline__ void flush_ranges(const WalkParams& P, WalkState& W, 
   const int lane = W.lane;
   const int total = S.rq_pre[nq];
   int rs = 0;                                       // the range holding b0
-  for (int b0 = 0; b0 < total; b0 += 32) {
+  // lane gi = b0 + lane of a chunk: its range r and source j (range starts inside [b0, b0 + 32)
+  // as a bit mask: queued ranges are never empty, so starts are distinct; lane gi lies in range
+  // rs + #{starts <= gi})
+  auto locate = [&](int b0, int& r, int& j, bool& v) {
     const int gi = b0 + lane;
-    const bool v = gi < total;
-    // range starts inside [b0, b0 + 32) as a bit mask (queued ranges are never empty, so
-    // starts are distinct): lane gi lies in range rs + #{starts <= gi}
+    v = gi < total;
 #if RANGE_MASK
     unsigned bm = 0u;
     if (rs + 1 + lane < nq) {
@@ -440,19 +441,24 @@ __device__ __forceinline__ void flush_ranges(const WalkParams& P, WalkState& W, 
       if (B < b0 + 32) bm = 1u << (B - b0);
     }
     bm = __reduce_or_sync(FULL_MASK, bm);
-    const int r = rs + __popc(bm & (lanemask_lt() | (1u << lane)));
+    r = rs + __popc(bm & (lanemask_lt() | (1u << lane)));
     rs += __popc(bm);
 #else
-    int r = 0;                                    // rq_pre[r] <= gi < rq_pre[r+1]
+    r = 0;                                        // rq_pre[r] <= gi < rq_pre[r+1]
 #pragma unroll
     for (int step = 32; step > 0; step >>= 1)
       if (r + step < nq && S.rq_pre[r + step] <= gi) r += step;
 #endif
-    int j = 0, code = 0;
+    j = v ? S.rq_first[r] + (gi - S.rq_pre[r]) : 0;
+  };
+  for (int b0 = 0; b0 < total; b0 += 32) {
+    int r, j;
+    bool v;
+    locate(b0, r, j, v);
+    int code = 0;
     float3 p = make_float3(0.f, 0.f, 0.f);
     float hj = 0.f;
     if (v) {
-      j = S.rq_first[r] + (gi - S.rq_pre[r]);
       code = S.rq_code[r];
       const float4 q = P.xh[j], so = S.rq_so[r], oo = S.rq_oo[r];
       p = make_float3((q.x + so.x) - oo.x, (q.y + so.y) - oo.y, (q.z + so.z) - oo.z);
