@@ -1,3 +1,6 @@
+"""Host <-> device copy bandwidth from pinned memory (the e2e path's copies): 25 MB (x) and
+67 MB (x, v, m, u) each way, CUDA events around torch copies.
+  python tools/pcie_bw_probe.py"""
 import torch, time
 for mb in (25.2, 67):
     n = int(mb * 1e6 / 4)
