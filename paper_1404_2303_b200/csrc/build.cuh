@@ -206,6 +206,8 @@ struct LevelBuild {
   int* presort;      // set to 1 if a leaf qualifies for presorted lists (count > sort_min_len): the
                      // host skips the presort pass (and its scan's round trip) when it stays 0
   int sort_min_len;
+  int* ngroups;      // target groups of the tree (cmax > 0: chunks of <= SPH_GROUP of every container,
+  int cmax;          // as k_group_count counts them), summed here so the host needs no scan total
 };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -275,6 +277,7 @@ __global__ void __launch_bounds__(LEVEL_THREADS) k_build_levels(LevelBuild L, co
   const int gw = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int nwarps = (int)(gridDim.x * (blockDim.x >> 5));
   volatile int* lev = L.lev_off;
+  int wgroups = 0;   // lane 0: groups of the containers this warp decided (all levels)
   for (int l = 0;; ++l) {
     // level 0 (the top cells, 0..n0) from the argument: lev[] is written only under barriers
     const int a = l == 0 ? 0 : lev[l], b = l == 0 ? n0 : lev[l + 1];
@@ -300,6 +303,11 @@ __global__ void __launch_bounds__(LEVEL_THREADS) k_build_levels(LevelBuild L, co
       }
       const int sp = (l < depth) && (cnt > split_count) && frac_ok;
       if (lane == 0) N.split[node] = sp;
+      if (lane == 0 && L.cmax > 0) {   // is_container (below), with this level's split decision
+        const int par = __ldcg(N.parent + node);
+        const bool cont = cnt <= L.cmax ? (par < 0 || __ldcg(N.count + par) > L.cmax) : !sp;
+        if (cont) wgroups += (cnt + SPH_GROUP - 1) / SPH_GROUP;
+      }
       if (lane == 0 && !sp && cnt > L.sort_min_len && cnt > 1 && cnt <= SORT_BLOCK_MAX) *L.presort = 1;
       if (!sp) {
         if (lane == 0) L.nch[node - a] = 0;
@@ -345,6 +353,10 @@ __global__ void __launch_bounds__(LEVEL_THREADS) k_build_levels(LevelBuild L, co
       const unsigned bal = __ballot_sync(FULL_MASK, lane < 8 && nxt - start > 0);
       if (lane < 8) N.child[8 * (int64_t)node + lane] = start;
       if (lane == 0) L.nch[node - a] = __popc(bal);
+    }
+    if (lane == 0 && wgroups) {
+      atomicAdd(L.ngroups, wgroups);
+      wgroups = 0;
     }
 #if LEVEL_CHUNK_A
     __syncthreads();   // the block's nch entries are its own writes

@@ -172,6 +172,7 @@ struct sph_ctx {
   bool xref_valid = false;   // B_XREF holds the last build's cell-order positions (sph_update_cells)
   bool in_step = false;      // sph_build_cells called by sph_step (no end-of-call sync)
   bool pos_check = false;    // k_keys' position checks not read yet (read with the level build's status)
+  int n_groups_lev = -1;     // groups counted by the last level build (-1: not counted)
   bool maybe_presort = true; // some leaf of the last level build qualifies for presorted lists
   int group_cmax = 512;      // targets: balanced chunks of the deepest cells holding <= 512 (0: sibling packing)
   int64_t ovf_used = 0;      // entries of the neighbour-list overflow pool

@@ -429,6 +429,8 @@ static void build_nodes(sph_ctx* c, bool use_fraction, bool guess = false, bool 
     Lb.cap = (int)std::min<int64_t>(cap, INT_MAX);
     Lb.presort = lev + SPH_MAX_DEPTH + 8;
     Lb.sort_min_len = c->cfg.sort_min_len;
+    Lb.ngroups = lev + SPH_MAX_DEPTH + 9;
+    Lb.cmax = c->group_cmax;
     CUDA_TRY(cudaMemsetAsync(lev, 0, (SPH_MAX_DEPTH + 12) * sizeof(int), c->stream));
     N = nodes(c);
     float guess_n = guess ? c->cfg.n_ngb : 0.f;
@@ -450,6 +452,7 @@ static void build_nodes(sph_ctx* c, bool use_fraction, bool guess = false, bool 
     memcpy(hl, c->hpin, sizeof(hl));
     if (c->pos_check) pos_check(c, c->hpin[16]);
     c->maybe_presort = hl[SPH_MAX_DEPTH + 8] != 0;
+    c->n_groups_lev = c->group_cmax > 0 ? hl[SPH_MAX_DEPTH + 9] : -1;
     SPH_REQUIRE(hl[SPH_MAX_DEPTH + 5] != 2, SPH_E_CUDA, "k_build_levels: grid barrier timed out");
     if (hl[SPH_MAX_DEPTH + 5] == 1) {   // node capacity exceeded: grow and run again
       SPH_REQUIRE(attempt < 8, SPH_E_OOM, "node arrays keep overflowing");
@@ -500,7 +503,12 @@ static void build_groups(sph_ctx* c) {
   NodeArrays N = nodes(c);
   const int cmax = c->group_cmax;
   LAUNCH(k_group_count, gridfull(nn, 256), 256, 0, nn, N, cmax, nchunk);
-  c->n_groups = scan_excl<int>(c, nchunk, cscan, nn);
+  if (c->n_groups_lev >= 0) {   // counted by the level build: the offsets stay on the device
+    scan_excl_dev<int>(c, nchunk, cscan, nn);
+    c->n_groups = c->n_groups_lev;
+  } else {
+    c->n_groups = scan_excl<int>(c, nchunk, cscan, nn);
+  }
   int4* groups = B<int4>(c, B_GROUPS, c->n_groups);
   LAUNCH(k_group_write, gridfull(nn, 256), 256, 0, nn, N, cmax, cscan, groups);
 }
