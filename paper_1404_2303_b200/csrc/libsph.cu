@@ -1493,9 +1493,13 @@ int sph_force(sph_ctx* ctx, float* a_out, float* dudt_out, float* vsig_out, int3
     }
   }
   CUDA_TRY(cudaEventRecord(c->ev[11], c->stream));
+  // the counters come back with the outputs' copies (one round trip)
+  CUDA_TRY(cudaMemcpyAsync(c->hpin, ctr(c), sizeof(unsigned long long) * C_NCOUNTERS, cudaMemcpyDeviceToHost,
+                           c->stream));
   flush_out(c, maps, c->ev[5]);
+  if (maps.empty()) sync(c);
   unsigned long long hc[C_NCOUNTERS];
-  ctr_read(c, hc);
+  memcpy(hc, c->hpin, sizeof(hc));
   SPH_REQUIRE(!(hc[C_ERR] & (1ull << 20)), SPH_E_CUDA, "interaction list count/fill mismatch");
   DBG("force: groups %d cand %llu pairs %llu; host syncs so far %lld, launches %lld\n", c->n_groups, hc[C_CAND],
       hc[C_NFORCE] / 2, (long long)g_syncs, (long long)c->launches);
