@@ -313,10 +313,9 @@ __device__ __forceinline__ void warp_hsolve(bool act, const float* r2l, int64_t 
       pend = __ballot_sync(FULL_MASK, again);
     }
   }
-  if (false) {
 #else
+  // one lane per particle, on its own row
   if (shortl) {
-#endif
     for (; H.it < max_iter && H.st == HS_ACTIVE; ++H.it) {
       double S0 = 0.0;
       float S1 = 0.f, S2 = 0.f;
@@ -329,6 +328,7 @@ __device__ __forceinline__ void warp_hsolve(bool act, const float* r2l, int64_t 
       if (H.st == HS_REGROW) ++H.it;
     }
   }
+#endif
   unsigned lm = __ballot_sync(FULL_MASK, act && H.st == HS_ACTIVE && cnt > HSOLVE_LONG);
   while (lm) {
     const int t = __ffs(lm) - 1;
